@@ -1,0 +1,170 @@
+/*
+ * lsb.h — C ABI of the B200 splat hot path (libsplat_b200.so).
+ *
+ * Drop-in boundary for the reference package livsplat (arXiv 2501.08672
+ * desk-scale reimplementation).  The reference has no native boundary of its
+ * own: its hot path is the Python entry points render / backward / pose_rows
+ * (raster.py:212,309,450), photometric_loss / optimize_window (optimize.py:48,
+ * 122), visual_measurement's H/b (estimator.py:260-323) and the HashOctree
+ * batch operations (voxmap.py:99-251).  Each function below replaces the
+ * numba/numpy body of one of those entry points; the Python host layer
+ * (paper_2501_08672_b200/) keeps the reference's names and signatures and
+ * binds this header with ctypes.
+ *
+ * Conventions
+ *  - All array arguments are DEVICE pointers allocated by the caller (torch
+ *    tensors on the host side).  The library never allocates or frees caller
+ *    memory; scratch lives in a caller-provided workspace whose size comes
+ *    from lsb_workspace_bytes().
+ *  - Every call is asynchronous and stream-ordered on `stream` (a
+ *    cudaStream_t passed as void*).  Only the *_counts / *_read functions
+ *    synchronise, and they say so.
+ *  - Return value: LSB_OK or an error code; lsb_last_error() gives a
+ *    thread-local message.  The host layer maps codes to the reference's
+ *    exception types (errors.py): LSB_EMISSING_CACHE -> MissingCache,
+ *    LSB_EINVAL -> ValueError, LSB_ECAPACITY -> retry with a larger workspace.
+ *  - No global mutable state: concurrent calls on different streams with
+ *    different workspaces are safe (reference SPEC.md:322).
+ */
+#ifndef LSB_H
+#define LSB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LSB_ABI_VERSION 1
+
+enum lsb_status {
+    LSB_OK = 0,
+    LSB_EINVAL = 1,          /* bad argument                                  */
+    LSB_ECAPACITY = 2,       /* workspace capacity exceeded: grow and retry   */
+    LSB_ECUDA = 3,           /* CUDA runtime error                            */
+    LSB_EMISSING_CACHE = 4   /* backward on a render without its state        */
+};
+
+/* PinholeCamera (geometry.py:231-244). */
+typedef struct lsb_camera {
+    double fx, fy, cx, cy;
+    int32_t width, height;
+} lsb_camera;
+
+/* RasterSettings (raster.py:24-34). */
+typedef struct lsb_settings {
+    double near_plane;         /* near                                     */
+    double dilation;           /* px^2 added to both 2-D eigenvalues       */
+    double alpha_clamp;
+    double transmittance_min;
+    double footprint_sigma;
+    double alpha_cut;
+    double max_footprint_px;
+    double background[3];
+    int32_t sh_degree;
+    int32_t _pad;
+} lsb_settings;
+
+/* World->camera rigid transform T_cw (SE3, geometry.py:125-171): p_c = R p_w + t.
+ * R is row-major.  cam_center = -R^T t (raster.py:233) is passed explicitly so
+ * host and device use the bit-identical value. */
+typedef struct lsb_pose {
+    double R[9];
+    double t[3];
+    double cam_center[3];
+} lsb_pose;
+
+/* Window parameter arena, f32 structure-of-arrays (window.py:45-60):
+ * means (n,3), rots (n,9) row-major 3x3, scales (n,3), opacities (n),
+ * shs (n,K,3).  Device pointers. */
+typedef struct lsb_params {
+    const float* means;
+    const float* rots;
+    const float* scales;
+    const float* opacities;
+    const float* shs;
+    int64_t n;
+    int32_t sh_coeffs;   /* K = (degree+1)^2 stored per Gaussian */
+    int32_t _pad;
+} lsb_params;
+
+/* Gradient buffers, same shapes as lsb_params but rot is the (n,3) right
+ * tangent (ParamGradients, raster.py:85-98).  Backward ACCUMULATES (+=) into
+ * them, so multi-view gradients sum without extra passes. */
+typedef struct lsb_grads {
+    float* mean;
+    float* rot;
+    float* scale;
+    float* opacity;
+    float* sh;
+} lsb_grads;
+
+/* Sizes that fix the workspace layout of one render state. */
+typedef struct lsb_dims {
+    int64_t n;            /* Gaussians                                  */
+    int32_t width, height;
+    int32_t sh_coeffs;
+    int32_t tile;         /* must be 16                                 */
+    int64_t isect_cap;    /* capacity for (tile, splat) intersections   */
+} lsb_dims;
+
+/* ---- size queries / diagnostics ------------------------------------- */
+int lsb_abi_version(void);
+const char* lsb_last_error(void);
+int lsb_workspace_bytes(const lsb_dims* dims, size_t* bytes);
+
+/* ---- render: replaces raster.render (raster.py:212-264) ---------------
+ * Preprocess (projection, EWA covariance, footprint, SH colour; raster.py:
+ * 134-185, 232-238), tile binning + per-tile depth sort (replaces the global
+ * argsort + build_csr, raster.py:221, _kernels.py:21-59) and the front-to-back
+ * blend (_kernels.py:62-119).  Outputs: image (H,W,3) f32, t_final (H,W) f32,
+ * n_contrib (H,W) i32 and, if non-NULL, depth (H,W) f32 = sum_k w_k z_k.
+ * The workspace then holds the render state consumed by lsb_render_bwd and
+ * lsb_pose_rows.  If the intersection count exceeds dims->isect_cap the
+ * outputs are invalid and lsb_render_counts reports overflow. */
+int lsb_render_fwd(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T_cw,
+                   const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
+                   float* image, float* t_final, int32_t* n_contrib, float* depth,
+                   void* stream);
+
+/* Synchronises `stream`; counts[0]=visible splats M, [1]=intersections I,
+ * [2]=overflow flag (1 if I > isect_cap), [3]=isect_cap. */
+int lsb_render_counts(const void* ws, const lsb_dims* dims, int64_t counts[4], void* stream);
+
+/* Export the render state for parity checks (async):
+ *   what=0: visible Gaussian ids, ascending (= slot order)  -> int32[M]
+ *   what=1: bboxes [x0,x1,y0,y1] in slot order               -> int32[M*4]
+ *   what=2: per-tile ranges [start,end)                      -> int32[ntiles*2]
+ *   what=3: Gaussian id of every sorted tile entry           -> int32[I]
+ *   what=4: camera depth (f64 sort key) in slot order        -> double[M]
+ * M and I must come from lsb_render_counts. */
+int lsb_render_export(const void* ws, const lsb_dims* dims, int what, void* dst, void* stream);
+
+/* ---- backward: replaces raster.backward (raster.py:309-399) ----------
+ * grad_image (H,W,3) f32 = dL/dI, multiplied by grad_scale.  Param
+ * gradients are ACCUMULATED into `g`.  pose_out (device, 9 doubles) receives
+ * the camera-tangent pose pieces [rho_cam(3), tau_cam(3), d_cam_center(3)];
+ * the host applies -R d_cam_center and the IMU adjoint (raster.py:376-383). */
+int lsb_render_bwd(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T_cw,
+                   const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
+                   const float* image, const float* t_final, const int32_t* n_contrib,
+                   const float* grad_image, float grad_scale, const lsb_grads* g,
+                   double* pose_out, void* stream);
+
+/* ---- photometric loss: replaces optimize.photometric_loss (optimize.py:48-74)
+ * kind 0 = L1, 1 = L2 over (npx, 3) f32 images; mask (npx) u8 may be NULL.
+ * grad_out (npx,3) f32 = sign(diff) (L1) or 2 diff (L2), times grad_scale
+ * (the host passes 1/(3*mask_count) [/ views]); may be NULL.
+ * sums_out: device buffer of lsb_loss_scratch_doubles() doubles, zeroed once
+ * at allocation; on completion sums_out[0] = sum |diff| (L1) or sum diff^2
+ * (L2) and sums_out[1] = sum diff^2 over the mask.  Deterministic. */
+int lsb_loss_scratch_doubles(void);
+int lsb_photometric_loss(const float* rendered, const float* observed, const uint8_t* mask,
+                         int64_t npx, int64_t mask_count, int kind, float grad_scale,
+                         float* grad_out, double* sums_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSB_H */

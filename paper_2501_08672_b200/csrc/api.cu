@@ -1,0 +1,176 @@
+// extern "C" entry points of libsplat_b200.so (declared in include/lsb.h).
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "common.cuh"
+
+namespace lsb {
+cudaError_t launch_preprocess(const lsb_params&, const lsb_camera&, const lsb_pose&, const lsb_settings&,
+                              const Ws&, cudaStream_t);
+cudaError_t launch_blend_fwd(const Ws&, const lsb_settings&, int, int, float*, float*, int32_t*, float*,
+                             cudaStream_t);
+cudaError_t launch_blend_bwd(const Ws&, const lsb_settings&, int, int, const float*, const int32_t*,
+                             const float*, float, cudaStream_t);
+cudaError_t launch_chain(const Ws&, const lsb_params&, const lsb_grads&, const lsb_camera&, const lsb_pose&,
+                         const lsb_settings&, double*, cudaStream_t);
+cudaError_t launch_loss(const float*, const float*, const uint8_t*, int64_t, int, float, float*, double*,
+                        cudaStream_t);
+int loss_scratch_doubles();
+}  // namespace lsb
+
+using namespace lsb;
+
+static thread_local char g_err[512] = "";
+
+static int fail(int code, const char* msg) {
+    snprintf(g_err, sizeof(g_err), "%s", msg);
+    return code;
+}
+
+static int check_cuda(cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return LSB_OK;
+    snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+    return LSB_ECUDA;
+}
+
+static int dims_ok(const lsb_dims* d) {
+    if (!d) return fail(LSB_EINVAL, "dims is NULL");
+    if (d->n < 0 || d->width <= 0 || d->height <= 0) return fail(LSB_EINVAL, "bad dims");
+    if (d->width > 32767 || d->height > 32767) return fail(LSB_EINVAL, "image larger than 32767 px");
+    if (d->tile != TILE) return fail(LSB_EINVAL, "tile must be 16");
+    if (d->isect_cap < 1 || d->isect_cap > 0x7fffffffLL) return fail(LSB_EINVAL, "bad isect_cap");
+    if (d->n > 0x7fffffffLL) return fail(LSB_EINVAL, "too many Gaussians for int32 ids");
+    return LSB_OK;
+}
+
+static int get_ws(void* ws, size_t ws_bytes, const lsb_dims* d, Ws* w) {
+    int rc = dims_ok(d);
+    if (rc) return rc;
+    if (!ws) return fail(LSB_EMISSING_CACHE, "workspace is NULL (render state missing)");
+    const size_t need = carve(*d, nullptr, nullptr);
+    if (ws_bytes < need) return fail(LSB_EINVAL, "workspace too small");
+    carve(*d, (char*)ws, w);
+    return LSB_OK;
+}
+
+extern "C" {
+
+int lsb_abi_version(void) { return LSB_ABI_VERSION; }
+
+const char* lsb_last_error(void) { return g_err; }
+
+int lsb_workspace_bytes(const lsb_dims* d, size_t* bytes) {
+    int rc = dims_ok(d);
+    if (rc) return rc;
+    if (!bytes) return fail(LSB_EINVAL, "bytes is NULL");
+    *bytes = carve(*d, nullptr, nullptr);
+    return LSB_OK;
+}
+
+int lsb_loss_scratch_doubles(void) { return loss_scratch_doubles(); }
+
+int lsb_render_fwd(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T, const lsb_settings* s,
+                   void* ws, size_t ws_bytes, const lsb_dims* d, float* image, float* t_final,
+                   int32_t* n_contrib, float* depth, void* stream) {
+    if (!p || !cam || !T || !s) return fail(LSB_EINVAL, "NULL argument");
+    if (!image || !t_final || !n_contrib) return fail(LSB_EINVAL, "NULL output");
+    if (p->n != d->n || cam->width != d->width || cam->height != d->height)
+        return fail(LSB_EINVAL, "dims do not match params/camera");
+    if (p->n > 0 && (!p->means || !p->rots || !p->scales || !p->opacities || !p->shs))
+        return fail(LSB_EINVAL, "NULL parameter array");
+    if (p->sh_coeffs < 1 || p->sh_coeffs > 16) return fail(LSB_EINVAL, "sh_coeffs must be 1..16");
+    Ws w;
+    int rc = get_ws(ws, ws_bytes, d, &w);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    rc = check_cuda(launch_preprocess(*p, *cam, *T, *s, w, st), "preprocess");
+    if (rc) return rc;
+    return check_cuda(launch_blend_fwd(w, *s, d->width, d->height, image, t_final, n_contrib, depth, st),
+                      "blend_fwd");
+}
+
+int lsb_render_counts(const void* ws, const lsb_dims* d, int64_t counts[4], void* stream) {
+    Ws w;
+    int rc = get_ws((void*)ws, (size_t)-1, d, &w);
+    if (rc) return rc;
+    unsigned long long h[3];
+    cudaStream_t st = (cudaStream_t)stream;
+    rc = check_cuda(cudaMemcpyAsync(h, w.ctr, sizeof(h), cudaMemcpyDeviceToHost, st), "counts");
+    if (rc) return rc;
+    rc = check_cuda(cudaStreamSynchronize(st), "counts sync");
+    if (rc) return rc;
+    counts[0] = (int64_t)h[0];
+    counts[1] = (int64_t)h[1];
+    counts[2] = (int64_t)h[2];
+    counts[3] = d->isect_cap;
+    return LSB_OK;
+}
+
+namespace lsb {
+__global__ void k_export(Ws w, int what, void* dst) {
+    const int64_t M = (int64_t)w.ctr[0];
+    const int64_t I = (int64_t)w.ctr[1];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (what == 0) {
+        for (int64_t i = i0; i < M; i += stride) ((int32_t*)dst)[i] = w.rec[i].id;
+    } else if (what == 1) {
+        for (int64_t i = i0; i < M; i += stride) {
+            const Rec& r = w.rec[i];
+            int32_t* o = (int32_t*)dst + 4 * i;
+            o[0] = r.bbx & 0xffff; o[1] = r.bbx >> 16; o[2] = r.bby & 0xffff; o[3] = r.bby >> 16;
+        }
+    } else if (what == 2) {
+        for (int64_t t = i0; t < w.ntiles; t += stride) {
+            ((int32_t*)dst)[2 * t] = w.tile_start[t];
+            ((int32_t*)dst)[2 * t + 1] = w.tile_start[t + 1];
+        }
+    } else if (what == 3) {
+        for (int64_t j = i0; j < I && j < w.cap; j += stride) ((int32_t*)dst)[j] = w.rec[w.tile_slot[j]].id;
+    } else if (what == 4) {
+        for (int64_t i = i0; i < M; i += stride) ((double*)dst)[i] = __longlong_as_double((long long)w.vkey[i]);
+    }
+}
+}  // namespace lsb
+
+int lsb_render_export(const void* ws, const lsb_dims* d, int what, void* dst, void* stream) {
+    Ws w;
+    int rc = get_ws((void*)ws, (size_t)-1, d, &w);
+    if (rc) return rc;
+    if (!dst || what < 0 || what > 4) return fail(LSB_EINVAL, "bad export request");
+    k_export<<<148, 256, 0, (cudaStream_t)stream>>>(w, what, dst);
+    return check_cuda(cudaGetLastError(), "export");
+}
+
+int lsb_render_bwd(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T, const lsb_settings* s,
+                   void* ws, size_t ws_bytes, const lsb_dims* d, const float* image,
+                   const float* t_final, const int32_t* n_contrib, const float* grad_image,
+                   float grad_scale, const lsb_grads* g, double* pose_out, void* stream) {
+    (void)t_final;
+    if (!p || !cam || !T || !s || !g) return fail(LSB_EINVAL, "NULL argument");
+    if (!image || !n_contrib || !grad_image) return fail(LSB_EMISSING_CACHE, "render outputs missing");
+    if (p->n > 0 && (!g->mean || !g->rot || !g->scale || !g->opacity || !g->sh))
+        return fail(LSB_EINVAL, "NULL gradient array");
+    Ws w;
+    int rc = get_ws(ws, ws_bytes, d, &w);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    rc = check_cuda(launch_blend_bwd(w, *s, d->width, d->height, image, n_contrib, grad_image, grad_scale, st),
+                    "blend_bwd");
+    if (rc) return rc;
+    return check_cuda(launch_chain(w, *p, *g, *cam, *T, *s, pose_out, st), "chain");
+}
+
+int lsb_photometric_loss(const float* rendered, const float* observed, const uint8_t* mask, int64_t npx,
+                         int64_t mask_count, int kind, float grad_scale, float* grad_out,
+                         double* sums_out, void* stream) {
+    (void)mask_count;
+    if (!rendered || !observed || !sums_out) return fail(LSB_EINVAL, "NULL argument");
+    if (kind != 0 && kind != 1) return fail(LSB_EINVAL, "kind must be 0 (l1) or 1 (l2)");
+    return check_cuda(launch_loss(rendered, observed, mask, npx, kind, grad_scale, grad_out, sums_out,
+                                  (cudaStream_t)stream),
+                      "loss");
+}
+
+}  // extern "C"

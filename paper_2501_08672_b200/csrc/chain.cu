@@ -1,0 +1,280 @@
+// K5 backward chain: one thread per visible splat (fixed grid, grid-stride).
+//
+// Sums the splat's per-intersection partials in intersection order (fixed,
+// so the result is deterministic), then applies the reference's chain rule
+// in f64 (raster.py:267-399): 2-D covariance -> world covariance ->
+// (rotation right tangent, scale); 2-D mean -> camera mean -> world mean;
+// SH colour with the clamp gate and view-direction term; camera-tangent pose
+// pieces reduced per block and finally by the last block (ticket), again in a
+// fixed order.  Param gradients are accumulated (+=) into the N-shaped
+// buffers, so multiple views add up in stream order without atomics.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace lsb {
+
+struct ChainArgs {
+    lsb_params p;
+    lsb_grads g;
+    lsb_camera cam;
+    lsb_pose T;
+    int degree;
+    double* pose_out;
+};
+
+__constant__ double c_SH2[16] = {
+    0.28209479177387814, 0.4886025119029199, 1.0925484305920792, -1.0925484305920792,
+    0.31539156525252005, -1.0925484305920792, 0.5462742152960396, -0.5900435899266435,
+    2.890611442640554, -0.4570457994644658, 0.3731763325901154, -0.4570457994644658,
+    1.445305721320277, -0.5900435899266435, 0.0, 0.0};
+
+__device__ void sh_basis_d(int degree, double x, double y, double z, double* b) {
+    const double* C = c_SH2;
+    b[0] = C[0];
+    if (degree >= 1) { b[1] = -C[1] * y; b[2] = C[1] * z; b[3] = -C[1] * x; }
+    if (degree >= 2) {
+        const double xx = x * x, yy = y * y, zz = z * z;
+        b[4] = C[2] * x * y; b[5] = C[3] * y * z; b[6] = C[4] * (2.0 * zz - xx - yy);
+        b[7] = C[5] * x * z; b[8] = C[6] * (xx - yy);
+        if (degree >= 3) {
+            b[9] = C[7] * y * (3.0 * xx - yy); b[10] = C[8] * x * y * z;
+            b[11] = C[9] * y * (4.0 * zz - xx - yy);
+            b[12] = C[10] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+            b[13] = C[11] * x * (4.0 * zz - xx - yy); b[14] = C[12] * z * (xx - yy);
+            b[15] = C[13] * x * (xx - 3.0 * yy);
+        }
+    }
+}
+
+// d basis_k / d dir (sh.py:66-109), g[k][3].
+__device__ void sh_basis_grad_d(int degree, double x, double y, double z, double (*g)[3]) {
+    const double* C = c_SH2;
+    const int K = (degree + 1) * (degree + 1);
+    for (int k = 0; k < K; ++k) g[k][0] = g[k][1] = g[k][2] = 0.0;
+    if (degree >= 1) { g[1][1] = -C[1]; g[2][2] = C[1]; g[3][0] = -C[1]; }
+    if (degree >= 2) {
+        g[4][0] = C[2] * y; g[4][1] = C[2] * x;
+        g[5][1] = C[3] * z; g[5][2] = C[3] * y;
+        g[6][0] = C[4] * (-2.0 * x); g[6][1] = C[4] * (-2.0 * y); g[6][2] = C[4] * (4.0 * z);
+        g[7][0] = C[5] * z; g[7][2] = C[5] * x;
+        g[8][0] = C[6] * (2.0 * x); g[8][1] = C[6] * (-2.0 * y);
+    }
+    if (degree >= 3) {
+        const double xx = x * x, yy = y * y, zz = z * z;
+        g[9][0] = C[7] * 6.0 * x * y; g[9][1] = C[7] * (3.0 * xx - 3.0 * yy);
+        g[10][0] = C[8] * y * z; g[10][1] = C[8] * x * z; g[10][2] = C[8] * x * y;
+        g[11][0] = C[9] * (-2.0 * x * y); g[11][1] = C[9] * (4.0 * zz - xx - 3.0 * yy);
+        g[11][2] = C[9] * (8.0 * y * z);
+        g[12][0] = C[10] * (-6.0 * x * z); g[12][1] = C[10] * (-6.0 * y * z);
+        g[12][2] = C[10] * (6.0 * zz - 3.0 * xx - 3.0 * yy);
+        g[13][0] = C[11] * (4.0 * zz - 3.0 * xx - yy); g[13][1] = C[11] * (-2.0 * x * y);
+        g[13][2] = C[11] * (8.0 * x * z);
+        g[14][0] = C[12] * (2.0 * x * z); g[14][1] = C[12] * (-2.0 * y * z); g[14][2] = C[12] * (xx - yy);
+        g[15][0] = C[13] * (3.0 * xx - 3.0 * yy); g[15][1] = C[13] * (-6.0 * x * y);
+    }
+}
+
+__global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
+    __shared__ double s_red[CHAIN_THREADS / 32][POSE_VALS];
+    __shared__ bool s_last;
+    const int64_t M = (int64_t)w.ctr[0];
+    const double* R = a.T.R;
+    double pose[POSE_VALS];
+#pragma unroll
+    for (int c = 0; c < POSE_VALS; ++c) pose[c] = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; slot < M; slot += stride) {
+        const Rec& r = w.rec[slot];
+        if (r.ebase < 0) continue;
+        const int nt = ((((r.bbx >> 16) - 1) >> 4) - ((r.bbx & 0xffff) >> 4) + 1) *
+                       ((((r.bby >> 16) - 1) >> 4) - ((r.bby & 0xffff) >> 4) + 1);
+        double q[NUM_PART];
+#pragma unroll
+        for (int c = 0; c < NUM_PART; ++c) q[c] = 0.0;
+        for (int k = 0; k < nt; ++k) {
+#pragma unroll
+            for (int c = 0; c < NUM_PART; ++c) q[c] += (double)w.part[(int64_t)c * w.cap + r.ebase + k];
+        }
+        bool nz = false;
+#pragma unroll
+        for (int c = 0; c < NUM_PART; ++c) nz |= (q[c] != 0.0);
+        if (!nz) continue;
+        const int64_t i = r.id;
+        // ---- recompute the forward geometry in f64 ----
+        const double px = a.p.means[3 * i], py = a.p.means[3 * i + 1], pz = a.p.means[3 * i + 2];
+        const double x = R[0] * px + R[1] * py + R[2] * pz + a.T.t[0];
+        const double y = R[3] * px + R[4] * py + R[5] * pz + a.T.t[1];
+        const double z = R[6] * px + R[7] * py + R[8] * pz + a.T.t[2];
+        const double fx = a.cam.fx, fy = a.cam.fy;
+        const double J00 = fx / z, J02 = -fx * x / (z * z);
+        const double J11 = fy / z, J12 = -fy * y / (z * z);
+        double Rg[9], S[3], B[9], Wc[9];
+        for (int k = 0; k < 9; ++k) Rg[k] = a.p.rots[9 * i + k];
+        for (int k = 0; k < 3; ++k) S[k] = a.p.scales[3 * i + k];
+        for (int r3 = 0; r3 < 3; ++r3)
+            for (int c3 = 0; c3 < 3; ++c3) B[3 * r3 + c3] = Rg[3 * r3 + c3] * S[c3];
+        for (int r3 = 0; r3 < 3; ++r3)
+            for (int c3 = 0; c3 < 3; ++c3)
+                Wc[3 * r3 + c3] = B[3 * r3] * B[3 * c3] + B[3 * r3 + 1] * B[3 * c3 + 1] +
+                                  B[3 * r3 + 2] * B[3 * c3 + 2];
+        double Mm[6];   // M = J R (2x3)
+        for (int k = 0; k < 3; ++k) {
+            Mm[k] = J00 * R[k] + J02 * R[6 + k];
+            Mm[3 + k] = J11 * R[3 + k] + J12 * R[6 + k];
+        }
+        // ---- 2-D covariance chain (raster.py:286-298) ----
+        const double S00 = q[6], S01 = q[7], S11 = q[8];
+        double SM[6];   // S M (2x3)
+        for (int k = 0; k < 3; ++k) {
+            SM[k] = S00 * Mm[k] + S01 * Mm[3 + k];
+            SM[3 + k] = S01 * Mm[k] + S11 * Mm[3 + k];
+        }
+        double dCw[9];  // M^T S M
+        for (int r3 = 0; r3 < 3; ++r3)
+            for (int c3 = 0; c3 < 3; ++c3) dCw[3 * r3 + c3] = Mm[r3] * SM[c3] + Mm[3 + r3] * SM[3 + c3];
+        double dM[6];   // 2 S M W
+        for (int r2 = 0; r2 < 2; ++r2)
+            for (int c3 = 0; c3 < 3; ++c3)
+                dM[3 * r2 + c3] = 2.0 * (SM[3 * r2] * Wc[c3] + SM[3 * r2 + 1] * Wc[3 + c3] +
+                                         SM[3 * r2 + 2] * Wc[6 + c3]);
+        double dJ[6];   // dM R^T
+        for (int r2 = 0; r2 < 2; ++r2)
+            for (int c3 = 0; c3 < 3; ++c3)
+                dJ[3 * r2 + c3] = dM[3 * r2] * R[3 * c3] + dM[3 * r2 + 1] * R[3 * c3 + 1] +
+                                  dM[3 * r2 + 2] * R[3 * c3 + 2];
+        // d_W = J^T dM (3x3), J rows (J00,0,J02), (0,J11,J12)
+        double dW[9];
+        for (int c3 = 0; c3 < 3; ++c3) {
+            dW[c3] = J00 * dM[c3];
+            dW[3 + c3] = J11 * dM[3 + c3];
+            dW[6 + c3] = J02 * dM[c3] + J12 * dM[3 + c3];
+        }
+        // ---- mean chain ----
+        const double dm0 = q[4], dm1 = q[5];
+        double dmc[3] = {J00 * dm0, J11 * dm1, J02 * dm0 + J12 * dm1};
+        const double gxx = -fx / (z * z), gyy = -fy / (z * z);
+        dmc[0] += dJ[2] * gxx;
+        dmc[1] += dJ[5] * gyy;
+        dmc[2] += dJ[0] * gxx + dJ[4] * gyy + dJ[2] * (2.0 * fx * x / (z * z * z)) +
+                  dJ[5] * (2.0 * fy * y / (z * z * z));
+        double dmean[3];
+        for (int k = 0; k < 3; ++k) dmean[k] = dmc[0] * R[k] + dmc[1] * R[3 + k] + dmc[2] * R[6 + k];
+        // ---- covariance -> rotation tangent, scale ----
+        double dB[9];
+        for (int r3 = 0; r3 < 3; ++r3)
+            for (int c3 = 0; c3 < 3; ++c3)
+                dB[3 * r3 + c3] = 2.0 * (dCw[3 * r3] * B[c3] + dCw[3 * r3 + 1] * B[3 + c3] +
+                                         dCw[3 * r3 + 2] * B[6 + c3]);
+        double Y[9];   // Rg^T (dB * S)
+        for (int r3 = 0; r3 < 3; ++r3)
+            for (int c3 = 0; c3 < 3; ++c3)
+                Y[3 * r3 + c3] = (Rg[r3] * dB[c3] + Rg[3 + r3] * dB[3 + c3] + Rg[6 + r3] * dB[6 + c3]) * S[c3];
+        const double drot[3] = {Y[7] - Y[5], Y[2] - Y[6], Y[3] - Y[1]};
+        double dscale[3];
+        for (int c3 = 0; c3 < 3; ++c3)
+            dscale[c3] = Rg[c3] * dB[c3] + Rg[3 + c3] * dB[3 + c3] + Rg[6 + c3] * dB[6 + c3];
+        // ---- appearance ----
+        const uint32_t cm = w.colmask[slot];
+        const double dcol[3] = {(cm & 1u) ? q[0] : 0.0, (cm & 2u) ? q[1] : 0.0, (cm & 4u) ? q[2] : 0.0};
+        const double* cc3 = a.T.cam_center;
+        const double dvx = px - cc3[0], dvy = py - cc3[1], dvz = pz - cc3[2];
+        const double dn = sqrt(dvx * dvx + dvy * dvy + dvz * dvz);
+        double dx_ = 0.0, dy_ = 0.0, dz_ = 1.0;
+        if (dn > 0.0) {
+            const double inv = fmax(dn, 1e-30);
+            dx_ = dvx / inv; dy_ = dvy / inv; dz_ = dvz / inv;
+        }
+        double b[16];
+        sh_basis_d(a.degree, dx_, dy_, dz_, b);
+        const int K = a.p.sh_coeffs;
+        const int kk = (a.degree + 1) * (a.degree + 1);
+        float* gsh = a.g.sh + i * K * 3;
+        for (int k = 0; k < kk; ++k)
+            for (int c = 0; c < 3; ++c) gsh[3 * k + c] += (float)(b[k] * dcol[c]);
+        double dpt[3] = {0.0, 0.0, 0.0};
+        if (a.degree >= 1) {
+            double gb[16][3];
+            sh_basis_grad_d(a.degree, dx_, dy_, dz_, gb);
+            const float* shp = a.p.shs + i * K * 3;
+            double dd[3] = {0.0, 0.0, 0.0};
+            for (int k = 0; k < kk; ++k) {
+                const double t = dcol[0] * shp[3 * k] + dcol[1] * shp[3 * k + 1] + dcol[2] * shp[3 * k + 2];
+                dd[0] += t * gb[k][0]; dd[1] += t * gb[k][1]; dd[2] += t * gb[k][2];
+            }
+            const double dot = dx_ * dd[0] + dy_ * dd[1] + dz_ * dd[2];
+            const double rr = fmax(dn, 1e-30);
+            dpt[0] = (dd[0] - dx_ * dot) / rr;
+            dpt[1] = (dd[1] - dy_ * dot) / rr;
+            dpt[2] = (dd[2] - dz_ * dot) / rr;
+            dmean[0] += dpt[0]; dmean[1] += dpt[1]; dmean[2] += dpt[2];
+        }
+        // ---- write (accumulate) ----
+        for (int k = 0; k < 3; ++k) {
+            a.g.mean[3 * i + k] += (float)dmean[k];
+            a.g.rot[3 * i + k] += (float)drot[k];
+            a.g.scale[3 * i + k] += (float)dscale[k];
+        }
+        a.g.opacity[i] += (float)q[3];
+        // ---- pose pieces (camera tangent) ----
+        double Z[9];   // dW R^T
+        for (int r3 = 0; r3 < 3; ++r3)
+            for (int c3 = 0; c3 < 3; ++c3)
+                Z[3 * r3 + c3] = dW[3 * r3] * R[3 * c3] + dW[3 * r3 + 1] * R[3 * c3 + 1] +
+                                 dW[3 * r3 + 2] * R[3 * c3 + 2];
+        pose[0] += y * dmc[2] - z * dmc[1] + (Z[7] - Z[5]);
+        pose[1] += z * dmc[0] - x * dmc[2] + (Z[2] - Z[6]);
+        pose[2] += x * dmc[1] - y * dmc[0] + (Z[3] - Z[1]);
+        pose[3] += dmc[0];
+        pose[4] += dmc[1];
+        pose[5] += dmc[2];
+        pose[6] -= dpt[0];
+        pose[7] -= dpt[1];
+        pose[8] -= dpt[2];
+    }
+    // ---- deterministic pose reduction ----
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int c = 0; c < POSE_VALS; ++c) {
+        double v = pose[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) s_red[warp][c] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < POSE_VALS) {
+        double v = 0.0;
+        for (int k = 0; k < CHAIN_THREADS / 32; ++k) v += s_red[k][threadIdx.x];
+        w.pose_part[blockIdx.x * POSE_VALS + threadIdx.x] = v;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned long long t = atomicAdd(&w.ctr[4], 1ull);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        if (threadIdx.x < POSE_VALS) {
+            double v = 0.0;
+            for (int b2 = 0; b2 < (int)gridDim.x; ++b2)
+                v += ((volatile double*)w.pose_part)[b2 * POSE_VALS + threadIdx.x];
+            if (a.pose_out) a.pose_out[threadIdx.x] = v;
+        }
+        if (threadIdx.x == 0) w.ctr[4] = 0;
+    }
+}
+
+cudaError_t launch_chain(const Ws& w, const lsb_params& p, const lsb_grads& g, const lsb_camera& cam,
+                         const lsb_pose& T, const lsb_settings& s, double* pose_out,
+                         cudaStream_t st) {
+    ChainArgs a{p, g, cam, T, 0, pose_out};
+    int deg_store = 0;
+    while ((deg_store + 2) * (deg_store + 2) <= p.sh_coeffs) ++deg_store;
+    a.degree = s.sh_degree < deg_store ? s.sh_degree : deg_store;
+    k_chain<<<CHAIN_BLOCKS, CHAIN_THREADS, 0, st>>>(w, a);
+    return cudaGetLastError();
+}
+
+}  // namespace lsb

@@ -1,0 +1,110 @@
+// Shared device-side definitions for the B200 splat path.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lsb.h"
+
+namespace lsb {
+
+constexpr int TILE = 16;
+constexpr int NUM_PART = 9;          // d_color(3), d_opac, d_mean2d(2), d_cov2d(3)
+constexpr int POSE_VALS = 9;         // rho_cam(3), tau_cam(3), d_cam_center(3)
+constexpr int PRE_THREADS = 256;     // preprocess block size
+constexpr int PRE_ITEMS = 1;         // Gaussians per preprocess thread
+constexpr int CHAIN_BLOCKS = 296;    // fixed grid of the chain kernel (2 x 148 SMs)
+constexpr int CHAIN_THREADS = 256;
+constexpr double LOG2E = 1.4426950408889634;
+
+// One visible splat, 64 B, written once by preprocess and read by every tile
+// that the splat's bbox touches (4 x 16 B vector loads).
+struct __align__(16) Rec {
+    double mx, my;      // mu_i (f64: the blend subtracts the tile origin in f64)
+    float A, s, E, op;  // exponent: log2 g = A*u^2 + E*dy^2, u = dx + s*dy
+    float c0, c1, c2, z;  // clamped RGB and camera depth
+    int32_t bbx, bby;   // x0 | x1 << 16, y0 | y1 << 16 (half-open pixel bbox)
+    int32_t id, ebase;  // Gaussian id, first intersection index
+};
+static_assert(sizeof(Rec) == 64, "Rec must be 64 bytes");
+
+struct Ws {
+    unsigned long long* ctr;    // [0] M, [1] I, [2] overflow, [3] ticket
+    unsigned long long* scan;   // chained-scan state: 2 words per preprocess block
+    Rec* rec;                   // [n] (only the first M are live)
+    uint64_t* vkey;             // [n] depth bits of live splats
+    uint32_t* colmask;          // [n] interior bits (3) of live splats
+    int32_t* tile_count;        // [ntiles]
+    int32_t* tile_start;        // [ntiles + 1]
+    int32_t* tile_cursor;       // [ntiles]
+    int32_t* tile_last;         // [ntiles] one past the last list entry any pixel used
+    int32_t* emit_slot;         // [cap] visible slot of intersection e
+    int32_t* tile_e;            // [cap] intersection index, per-tile depth order
+    int32_t* tile_slot;         // [cap] visible slot, per-tile depth order
+    int32_t* sort_scratch;      // [cap * 8] fallback sort buffers (tiles > SORT_CAP)
+    float* part;                // [NUM_PART * cap] per-intersection gradient partials
+    double* pose_part;          // [CHAIN_BLOCKS * POSE_VALS]
+    int64_t n, cap;
+    int32_t ntx, nty, ntiles, nblocks_pre;
+};
+
+inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Carve the caller's workspace; returns the total size needed.
+inline size_t carve(const lsb_dims& d, char* base, Ws* w) {
+    Ws t{};
+    t.n = d.n;
+    t.cap = d.isect_cap;
+    t.ntx = (d.width + TILE - 1) / TILE;
+    t.nty = (d.height + TILE - 1) / TILE;
+    t.ntiles = t.ntx * t.nty;
+    const int64_t per_block = (int64_t)PRE_THREADS * PRE_ITEMS;
+    t.nblocks_pre = (int32_t)((d.n + per_block - 1) / per_block);
+    if (t.nblocks_pre < 1) t.nblocks_pre = 1;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off = align_up(off + bytes);
+        return base ? (void*)(base + o) : nullptr;
+    };
+    const size_t n = (size_t)(d.n > 0 ? d.n : 1);
+    const size_t cap = (size_t)(d.isect_cap > 0 ? d.isect_cap : 1);
+    // zeroed prefix: counters, scan flags, tile histogram, tile cursors
+    t.ctr = (unsigned long long*)take(8 * sizeof(unsigned long long));
+    t.scan = (unsigned long long*)take(2 * sizeof(unsigned long long) * (size_t)t.nblocks_pre);
+    t.tile_count = (int32_t*)take(sizeof(int32_t) * t.ntiles);
+    t.tile_cursor = (int32_t*)take(sizeof(int32_t) * t.ntiles);
+    // not zeroed
+    t.tile_start = (int32_t*)take(sizeof(int32_t) * (t.ntiles + 1));
+    t.tile_last = (int32_t*)take(sizeof(int32_t) * t.ntiles);
+    t.rec = (Rec*)take(sizeof(Rec) * n);
+    t.vkey = (uint64_t*)take(sizeof(uint64_t) * n);
+    t.colmask = (uint32_t*)take(sizeof(uint32_t) * n);
+    t.emit_slot = (int32_t*)take(sizeof(int32_t) * cap);
+    t.tile_e = (int32_t*)take(sizeof(int32_t) * cap);
+    t.tile_slot = (int32_t*)take(sizeof(int32_t) * cap);
+    t.sort_scratch = (int32_t*)take(sizeof(int32_t) * cap * 8);
+    t.part = (float*)take(sizeof(float) * NUM_PART * cap);
+    t.pose_part = (double*)take(sizeof(double) * CHAIN_BLOCKS * POSE_VALS);
+    if (w) *w = t;
+    return off;
+}
+
+// Bytes of the workspace prefix that must be zeroed before a render
+// (counters, chained-scan flags, tile histograms).
+inline size_t zero_prefix_bytes(const Ws& w) {
+    return (size_t)((char*)w.tile_start - (char*)w.ctr);
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+}  // namespace lsb

@@ -1,0 +1,480 @@
+// K1 preprocess + K2 tile binning (scan, scatter, per-tile depth sort).
+//
+// This translation unit is compiled with --fmad=false: every f64 operation of
+// the projection is rounded exactly where the reference (numpy) rounds it, and
+// the one place numpy fuses (the OpenBLAS k=3 dgemm behind `means @ R.T`,
+// raster.py:137) is written as explicit __fma_rn.  The discrete decisions —
+// near cull, footprint bbox, on-image test, depth order — therefore follow
+// the reference's own arithmetic.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace lsb {
+
+struct PreArgs {
+    lsb_params p;
+    lsb_camera cam;
+    lsb_pose T;
+    lsb_settings s;
+    int degree;
+};
+
+__constant__ double c_SH[16] = {
+    0.28209479177387814, 0.4886025119029199, 1.0925484305920792, -1.0925484305920792,
+    0.31539156525252005, -1.0925484305920792, 0.5462742152960396, -0.5900435899266435,
+    2.890611442640554, -0.4570457994644658, 0.3731763325901154, -0.4570457994644658,
+    1.445305721320277, -0.5900435899266435, 0.0, 0.0};
+
+// Real SH basis (sh.py:36-63), f64.
+__device__ __forceinline__ void sh_basis(int degree, double x, double y, double z, double* b) {
+    b[0] = c_SH[0];
+    if (degree >= 1) {
+        b[1] = -c_SH[1] * y;
+        b[2] = c_SH[1] * z;
+        b[3] = -c_SH[1] * x;
+    }
+    if (degree >= 2) {
+        const double xx = x * x, yy = y * y, zz = z * z;
+        b[4] = c_SH[2] * x * y;
+        b[5] = c_SH[3] * y * z;
+        b[6] = c_SH[4] * (2.0 * zz - xx - yy);
+        b[7] = c_SH[5] * x * z;
+        b[8] = c_SH[6] * (xx - yy);
+        if (degree >= 3) {
+            b[9] = c_SH[7] * y * (3.0 * xx - yy);
+            b[10] = c_SH[8] * x * y * z;
+            b[11] = c_SH[9] * y * (4.0 * zz - xx - yy);
+            b[12] = c_SH[10] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+            b[13] = c_SH[11] * x * (4.0 * zz - xx - yy);
+            b[14] = c_SH[12] * z * (xx - yy);
+            b[15] = c_SH[13] * x * (xx - 3.0 * yy);
+        }
+    }
+}
+
+// Projection + EWA covariance + footprint (raster.py:134-185) for Gaussian i.
+// Returns false if culled; fills the record, its tile count and depth key.
+__device__ bool splat_one(const PreArgs& a, int64_t i, Rec& r, int& ntiles, uint64_t& key,
+                          uint32_t& cmask) {
+    const float* mp = a.p.means + 3 * i;
+    const double px = mp[0], py = mp[1], pz = mp[2];
+    const double* R = a.T.R;
+    const double* t = a.T.t;
+    // mu_c = means @ R^T + t, in the dgemm FMA order
+    const double x = __fma_rn(R[2], pz, __fma_rn(R[1], py, R[0] * px)) + t[0];
+    const double y = __fma_rn(R[5], pz, __fma_rn(R[4], py, R[3] * px)) + t[1];
+    const double z = __fma_rn(R[8], pz, __fma_rn(R[7], py, R[6] * px)) + t[2];
+    if (!(z > a.s.near_plane)) return false;
+    const double fx = a.cam.fx, fy = a.cam.fy;
+    const double mux = fx * x / z + a.cam.cx;
+    const double muy = fy * y / z + a.cam.cy;
+    const double zz = z * z;
+    const double J00 = fx / z, J02 = -fx * x / zz;
+    const double J11 = fy / z, J12 = -fy * y / zz;
+    // world covariance B B^T, B = rot * scale (columns scaled)
+    const float* rp = a.p.rots + 9 * i;
+    const float* sp = a.p.scales + 3 * i;
+    const double s0 = sp[0], s1 = sp[1], s2 = sp[2];
+    double B[9];
+#pragma unroll
+    for (int r3 = 0; r3 < 3; ++r3) {
+        B[3 * r3 + 0] = (double)rp[3 * r3 + 0] * s0;
+        B[3 * r3 + 1] = (double)rp[3 * r3 + 1] * s1;
+        B[3 * r3 + 2] = (double)rp[3 * r3 + 2] * s2;
+    }
+    double W[9];
+#pragma unroll
+    for (int r3 = 0; r3 < 3; ++r3)
+#pragma unroll
+        for (int c3 = 0; c3 < 3; ++c3)
+            W[3 * r3 + c3] = __fma_rn(B[3 * r3 + 2], B[3 * c3 + 2],
+                                      __fma_rn(B[3 * r3 + 1], B[3 * c3 + 1], B[3 * r3] * B[3 * c3]));
+    // M = J R_cw (2x3)
+    double M0[3], M1[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        M0[k] = J00 * R[k] + J02 * R[6 + k];
+        M1[k] = J11 * R[3 + k] + J12 * R[6 + k];
+    }
+    // cov_i = M W M^T + dilation I
+    double T0[3], T1[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        T0[k] = M0[0] * W[k] + M0[1] * W[3 + k] + M0[2] * W[6 + k];
+        T1[k] = M1[0] * W[k] + M1[1] * W[3 + k] + M1[2] * W[6 + k];
+    }
+    const double ca = T0[0] * M0[0] + T0[1] * M0[1] + T0[2] * M0[2] + a.s.dilation;
+    const double cb = T0[0] * M1[0] + T0[1] * M1[1] + T0[2] * M1[2];
+    const double cc = T1[0] * M1[0] + T1[1] * M1[1] + T1[2] * M1[2] + a.s.dilation;
+    const double det = ca * cc - cb * cb;
+    const double mid = 0.5 * (ca + cc);
+    const double amc = ca - cc;
+    const double disc = sqrt(fmax(0.25 * (amc * amc) + cb * cb, 0.0));
+    const double op = a.p.opacities[i];
+    double nsig = a.s.footprint_sigma;
+    if (a.s.alpha_cut > 0.0) {
+        const double ratio = fmax(op / a.s.alpha_cut, 1.0);
+        nsig = fmin(nsig, sqrt(2.0 * log(ratio)));
+    }
+    const double radius = nsig * sqrt(fmax(mid + disc, 0.0));
+    const double W_ = a.cam.width, H_ = a.cam.height;
+    const double x0 = fmax(floor(mux - radius), 0.0);
+    const double x1 = fmin(floor(mux + radius) + 1.0, W_);
+    const double y0 = fmax(floor(muy - radius), 0.0);
+    const double y1 = fmin(floor(muy + radius) + 1.0, H_);
+    if (!(x0 < x1 && y0 < y1 && radius <= a.s.max_footprint_px)) return false;
+    const int ix0 = (int)x0, ix1 = (int)x1, iy0 = (int)y0, iy1 = (int)y1;
+    ntiles = (((ix1 - 1) >> 4) - (ix0 >> 4) + 1) * (((iy1 - 1) >> 4) - (iy0 >> 4) + 1);
+    // conic = cov_i^-1 = (cc, -cb, ca) / det; exponent in the shear form
+    //   q = a_k u^2 + dy^2 / cc,  u = dx - (cb/cc) dy   (no cancellation)
+    const double ak = cc / det;
+    r.mx = mux;
+    r.my = muy;
+    r.A = (float)(-0.5 * LOG2E * ak);
+    r.s = (float)(-cb / cc);
+    r.E = (float)(-0.5 * LOG2E / cc);
+    r.op = (float)op;
+    // SH colour (raster.py:232-238, sh.py:112-123)
+    const double* cc3 = a.T.cam_center;
+    const double dvx = px - cc3[0], dvy = py - cc3[1], dvz = pz - cc3[2];
+    const double dn = sqrt(dvx * dvx + dvy * dvy + dvz * dvz);
+    double dx_ = 0.0, dy_ = 0.0, dz_ = 1.0;
+    if (dn > 0.0) {
+        const double inv = fmax(dn, 1e-30);
+        dx_ = dvx / inv;
+        dy_ = dvy / inv;
+        dz_ = dvz / inv;
+    }
+    double b[16];
+    sh_basis(a.degree, dx_, dy_, dz_, b);
+    const int K = a.p.sh_coeffs;
+    const int kk = (a.degree + 1) * (a.degree + 1);
+    const float* shp = a.p.shs + (int64_t)i * K * 3;
+    float col[3];
+    cmask = 0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        double acc = b[0] * (double)shp[c];
+        for (int k = 1; k < kk; ++k) acc += b[k] * (double)shp[3 * k + c];
+        const double raw = 0.5 + acc;
+        col[c] = (float)fmin(fmax(raw, 0.0), 1.0);
+        if (raw > 0.0 && raw < 1.0) cmask |= 1u << c;
+    }
+    r.c0 = col[0];
+    r.c1 = col[1];
+    r.c2 = col[2];
+    r.z = (float)z;
+    r.bbx = ix0 | (ix1 << 16);
+    r.bby = iy0 | (iy1 << 16);
+    r.id = (int32_t)i;
+    key = (uint64_t)__double_as_longlong(z);
+    return true;
+}
+
+constexpr unsigned long long ST_AGG = 1ull << 62, ST_INC = 2ull << 62, VAL_MASK = (1ull << 62) - 1;
+
+// Decoupled look-back for one running total (chained scan, single pass).
+__device__ unsigned long long lookback(unsigned long long* flags, int blk,
+                                       unsigned long long agg) {
+    if (blk == 0) {
+        atomicExch(&flags[0], ST_INC | agg);
+        return 0;
+    }
+    atomicExch(&flags[blk], ST_AGG | agg);
+    unsigned long long excl = 0;
+    int j = blk - 1;
+    while (true) {
+        const unsigned long long v = *((volatile unsigned long long*)&flags[j]);
+        const unsigned long long st = v & ~VAL_MASK;
+        if (st == 0) continue;
+        excl += v & VAL_MASK;
+        if (st == ST_INC) break;
+        --j;
+    }
+    atomicExch(&flags[blk], ST_INC | (excl + agg));
+    return excl;
+}
+
+// K1: one thread per Gaussian.  Visible splats are compacted in ascending id
+// order (chained scan with decoupled look-back), so slot order == the
+// reference's np.nonzero order and (depth, slot) ties break exactly as its
+// stable argsort (raster.py:221).  Each visible splat also reserves a
+// contiguous run of intersection indices and bumps the per-tile histogram.
+__global__ void __launch_bounds__(PRE_THREADS)
+k_preprocess(PreArgs a, Ws w) {
+    __shared__ unsigned long long s_blk;
+    __shared__ int s_wv[PRE_THREADS / 32], s_wt[PRE_THREADS / 32];
+    __shared__ unsigned long long s_base_v, s_base_t;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_blk = atomicAdd(&w.ctr[3], 1ull);
+    __syncthreads();
+    const int blk = (int)s_blk;
+    const int64_t i = (int64_t)blk * PRE_THREADS + tid;
+    Rec r;
+    int nt = 0;
+    uint64_t key = 0;
+    uint32_t cm = 0;
+    const bool vis = (i < a.p.n) && splat_one(a, i, r, nt, key, cm);
+    int v = vis ? 1 : 0;
+    int tcount = vis ? nt : 0;
+    // block-wide exclusive scan of (v, tcount)
+    int iv = v, it = tcount;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int nv = __shfl_up_sync(0xffffffffu, iv, o);
+        const int ntt = __shfl_up_sync(0xffffffffu, it, o);
+        if (lane >= o) {
+            iv += nv;
+            it += ntt;
+        }
+    }
+    if (lane == 31) {
+        s_wv[warp] = iv;
+        s_wt[warp] = it;
+    }
+    __syncthreads();
+    int wv = 0, wt = 0, totv = 0, tott = 0;
+#pragma unroll
+    for (int k = 0; k < PRE_THREADS / 32; ++k) {
+        if (k < warp) {
+            wv += s_wv[k];
+            wt += s_wt[k];
+        }
+        totv += s_wv[k];
+        tott += s_wt[k];
+    }
+    if (tid == 0) {
+        s_base_v = lookback(w.scan, blk, (unsigned long long)totv);
+        s_base_t = lookback(w.scan + w.nblocks_pre, blk, (unsigned long long)tott);
+        if (blk == w.nblocks_pre - 1) {
+            w.ctr[0] = s_base_v + totv;
+            w.ctr[1] = s_base_t + tott;
+            if (s_base_t + tott > (unsigned long long)w.cap) w.ctr[2] = 1;
+        }
+    }
+    __syncthreads();
+    if (!vis) return;
+    const int64_t slot = (int64_t)(s_base_v + wv + iv - v);
+    const int64_t e0 = (int64_t)(s_base_t + wt + it - tcount);
+    const bool fits = e0 + nt <= w.cap;
+    r.ebase = fits ? (int32_t)e0 : -1;
+    w.rec[slot] = r;
+    w.vkey[slot] = key;
+    w.colmask[slot] = cm;
+    if (!fits) return;
+    const int tx0 = (r.bbx & 0xffff) >> 4, tx1 = ((r.bbx >> 16) - 1) >> 4;
+    const int ty0 = (r.bby & 0xffff) >> 4, ty1 = ((r.bby >> 16) - 1) >> 4;
+    for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&w.tile_count[ty * w.ntx + tx], 1);
+}
+
+// Exclusive scan of the tile histogram (single CTA, chunked).
+__global__ void __launch_bounds__(1024) k_scan_tiles(Ws w) {
+    __shared__ int s_w[32];
+    __shared__ int s_carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (int base = 0; base < w.ntiles; base += 1024) {
+        const int idx = base + tid;
+        const int v = idx < w.ntiles ? w.tile_count[idx] : 0;
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            int y = s_w[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int z = __shfl_up_sync(0xffffffffu, y, o);
+                if (lane >= o) y += z;
+            }
+            s_w[lane] = y;
+        }
+        __syncthreads();
+        const int incl = x + (warp > 0 ? s_w[warp - 1] : 0) + s_carry;
+        if (idx < w.ntiles) w.tile_start[idx] = incl - v;
+        __syncthreads();
+        if (tid == 1023) s_carry = incl;
+        __syncthreads();
+    }
+    if (tid == 0) w.tile_start[w.ntiles] = s_carry;
+}
+
+// Scatter every (tile, splat) intersection into its tile's bucket.  Order
+// inside a bucket is arbitrary here and fixed by k_tile_sort.
+__global__ void __launch_bounds__(256) k_scatter(Ws w) {
+    const int64_t M = (int64_t)w.ctr[0];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; slot < M; slot += stride) {
+        const Rec& r = w.rec[slot];
+        const int e0 = r.ebase;
+        if (e0 < 0) continue;
+        const int tx0 = (r.bbx & 0xffff) >> 4, tx1 = ((r.bbx >> 16) - 1) >> 4;
+        const int ty0 = (r.bby & 0xffff) >> 4, ty1 = ((r.bby >> 16) - 1) >> 4;
+        int e = e0;
+        for (int ty = ty0; ty <= ty1; ++ty) {
+            for (int tx = tx0; tx <= tx1; ++tx, ++e) {
+                const int t = ty * w.ntx + tx;
+                const int j = w.tile_start[t] + atomicAdd(&w.tile_cursor[t], 1);
+                w.tile_e[j] = e;
+                w.emit_slot[e] = (int32_t)slot;
+            }
+        }
+    }
+}
+
+constexpr int SORT_CAP = 4096;   // entries sorted entirely in shared memory
+
+__device__ __forceinline__ bool key_less(uint64_t ka, int sa, uint64_t kb, int sb) {
+    return ka < kb || (ka == kb && sa < sb);
+}
+
+// Bitonic sort of n <= SORT_CAP (depth, slot) keys held in shared memory.
+__device__ void smem_bitonic(uint64_t* k, int* s, int* e, int n) {
+    int P = 1;
+    while (P < n) P <<= 1;
+    for (int i = n + threadIdx.x; i < P; i += blockDim.x) {
+        k[i] = ~0ull;
+        s[i] = 0x7fffffff;
+        e[i] = -1;
+    }
+    __syncthreads();
+    for (int kk = 2; kk <= P; kk <<= 1) {
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const bool up = (i & kk) == 0;
+                    const bool lt = key_less(k[ixj], s[ixj], k[i], s[i]);
+                    if (lt == up) {
+                        const uint64_t tk = k[i]; k[i] = k[ixj]; k[ixj] = tk;
+                        const int ts = s[i]; s[i] = s[ixj]; s[ixj] = ts;
+                        const int te = e[i]; e[i] = e[ixj]; e[ixj] = te;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Per-tile depth sort: one CTA per tile.  Keys are (camera depth bits, slot);
+// slot order is id order, so the per-tile list is the reference's global
+// stable depth order restricted to the tile.  Tiles longer than SORT_CAP are
+// sorted as SORT_CAP chunks in shared memory followed by rank-merge passes
+// in global memory.
+__global__ void __launch_bounds__(256) k_tile_sort(Ws w) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* sk = (uint64_t*)smem;
+    int* ss = (int*)(sk + SORT_CAP);
+    int* se = ss + SORT_CAP;
+    const int t = blockIdx.x;
+    const int start = w.tile_start[t], end = w.tile_start[t + 1];
+    const int n = end - start;
+    if (n <= 0) return;
+    if (n <= SORT_CAP) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const int e = w.tile_e[start + i];
+            const int slot = w.emit_slot[e];
+            sk[i] = w.vkey[slot];
+            ss[i] = slot;
+            se[i] = e;
+        }
+        __syncthreads();
+        if (n > 1) smem_bitonic(sk, ss, se, n);
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            w.tile_e[start + i] = se[i];
+            w.tile_slot[start + i] = ss[i];
+        }
+        return;
+    }
+    // ---- long tile: chunk sort + global rank merges (ping-pong buffers) ----
+    // buffer layout per entry: key (2 ints), slot, e  -> 4 ints
+    int* bufA = w.sort_scratch;
+    int* bufB = w.sort_scratch + 4 * w.cap;
+    for (int c0 = 0; c0 < n; c0 += SORT_CAP) {
+        const int cn = min(SORT_CAP, n - c0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < cn; i += blockDim.x) {
+            const int e = w.tile_e[start + c0 + i];
+            const int slot = w.emit_slot[e];
+            sk[i] = w.vkey[slot];
+            ss[i] = slot;
+            se[i] = e;
+        }
+        __syncthreads();
+        smem_bitonic(sk, ss, se, cn);
+        for (int i = threadIdx.x; i < cn; i += blockDim.x) {
+            int* o = bufA + 4 * (int64_t)(start + c0 + i);
+            *(uint64_t*)o = sk[i];
+            o[2] = ss[i];
+            o[3] = se[i];
+        }
+    }
+    __syncthreads();
+    int* src = bufA;
+    int* dst = bufB;
+    for (int run = SORT_CAP; run < n; run <<= 1) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const int r0 = (i / (2 * run)) * (2 * run);
+            const bool inA = (i - r0) < run;
+            const int a0 = r0, a1 = min(r0 + run, n);
+            const int b0 = a1, b1 = min(r0 + 2 * run, n);
+            const int* me = src + 4 * (int64_t)(start + i);
+            const uint64_t mk = *(const uint64_t*)me;
+            const int ms = me[2];
+            // rank of me in the other run (keys are unique)
+            int lo = inA ? b0 : a0, hi = inA ? b1 : a1;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                const int* o = src + 4 * (int64_t)(start + mid);
+                if (key_less(*(const uint64_t*)o, o[2], mk, ms)) lo = mid + 1;
+                else hi = mid;
+            }
+            const int pos = r0 + (inA ? (i - a0) + (lo - b0) : (i - b0) + (lo - a0));
+            int* d = dst + 4 * (int64_t)(start + pos);
+            *(uint64_t*)d = mk;
+            d[2] = ms;
+            d[3] = me[3];
+        }
+        __syncthreads();
+        int* tmp = src; src = dst; dst = tmp;
+        __threadfence_block();
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int* o = src + 4 * (int64_t)(start + i);
+        w.tile_slot[start + i] = o[2];
+        w.tile_e[start + i] = o[3];
+    }
+}
+
+size_t tile_sort_smem() { return SORT_CAP * (sizeof(uint64_t) + 2 * sizeof(int)); }
+
+cudaError_t launch_preprocess(const lsb_params& p, const lsb_camera& cam, const lsb_pose& T,
+                              const lsb_settings& s, const Ws& w, cudaStream_t st) {
+    PreArgs a{p, cam, T, s, 0};
+    int deg_store = 0;
+    while ((deg_store + 2) * (deg_store + 2) <= p.sh_coeffs) ++deg_store;
+    a.degree = s.sh_degree < deg_store ? s.sh_degree : deg_store;
+    cudaError_t err = cudaMemsetAsync(w.ctr, 0, zero_prefix_bytes(w), st);
+    if (err != cudaSuccess) return err;
+    k_preprocess<<<w.nblocks_pre, PRE_THREADS, 0, st>>>(a, w);
+    k_scan_tiles<<<1, 1024, 0, st>>>(w);
+    k_scatter<<<4 * 148, 256, 0, st>>>(w);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tile_sort_smem());
+        attr_set = true;
+    }
+    k_tile_sort<<<w.ntiles, 256, tile_sort_smem(), st>>>(w);
+    return cudaGetLastError();
+}
+
+}  // namespace lsb

@@ -1,0 +1,311 @@
+"""render / backward — drop-in for livsplat.raster on the B200.
+
+Same entry points, argument meaning and error behaviour as the reference
+(raster.py:212 render, :309 backward); the numba/numpy body is replaced by
+libsplat_b200.so (include/lsb.h) working on HBM-resident torch tensors:
+
+    K1 preprocess  (projection, EWA covariance, footprint, SH colour)   f64
+    K2 binning     (tile histogram, scan, scatter, per-tile depth sort) int
+    K3 blend fwd   (one CTA per 16x16 tile, smem-staged records)        f32
+    K4 blend bwd   (forward-order recompute, warp reductions)           f32
+    K5 chain       (per-splat chain rule, pose reduction)               f64
+
+Outputs are device tensors (image (H,W,3) f32, final_transmittance (H,W),
+contrib_count (H,W) int32); `RenderOutput.numpy()` gives host copies.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import MissingCache
+from .geometry import SE3, as_se3, imu_camera_adjoint
+
+TILE = 16
+
+
+@dataclass
+class RasterSettings:
+    """raster.py:24-34 (identical fields and defaults)."""
+
+    near: float = 0.01
+    dilation: float = 0.3
+    alpha_clamp: float = 0.99
+    transmittance_min: float = 1e-4
+    footprint_sigma: float = 6.0
+    alpha_cut: float = 0.0
+    max_footprint_px: float = 512.0
+    background: tuple = (0.0, 0.0, 0.0)
+    sh_degree: int = 0
+
+
+def _dev(device=None):
+    return torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+
+
+def _f32(x, shape, device):
+    t = torch.as_tensor(x)
+    if t.dtype != torch.float32 or t.device != device:
+        t = t.to(device=device, dtype=torch.float32)
+    return t.reshape(shape).contiguous()
+
+
+class GaussianArrays:
+    """Structure-of-arrays Gaussian parameters in HBM, f32 (the window
+    arena's storage type, window.py:51-55; the reference upcasts the same
+    f32 values to f64 for its math, raster.py:47-52)."""
+
+    def __init__(self, means, rots, scales, opacities, shs, device=None):
+        dev = _dev(device)
+        n = int(np.shape(means)[0]) if not torch.is_tensor(means) else int(means.shape[0])
+        self.means = _f32(means, (n, 3), dev)
+        self.rots = _f32(rots, (n, 3, 3), dev)
+        self.scales = _f32(scales, (n, 3), dev)
+        self.opacities = _f32(opacities, (n,), dev)
+        k = (int(np.prod(np.shape(shs))) // (3 * n)) if n else 1
+        self.shs = _f32(shs, (n, max(k, 1), 3), dev)
+
+    def __len__(self):
+        return self.means.shape[0]
+
+    @property
+    def device(self):
+        return self.means.device
+
+    @staticmethod
+    def from_gaussians(gaussians, device=None) -> "GaussianArrays":
+        if not gaussians:
+            return GaussianArrays(np.zeros((0, 3)), np.zeros((0, 3, 3)), np.zeros((0, 3)), np.zeros(0),
+                                  np.zeros((0, 1, 3)), device)
+        k = max(g.sh.shape[0] for g in gaussians)
+        shs = np.zeros((len(gaussians), k, 3))
+        for i, g in enumerate(gaussians):
+            shs[i, : g.sh.shape[0]] = g.sh
+        return GaussianArrays(np.stack([g.mean_w for g in gaussians]), np.stack([g.rot for g in gaussians]),
+                              np.stack([g.scale for g in gaussians]),
+                              np.array([g.opacity for g in gaussians], dtype=float), shs, device)
+
+    def params(self) -> _lib.Params:
+        return _lib.Params(self.means.data_ptr(), self.rots.data_ptr(), self.scales.data_ptr(),
+                           self.opacities.data_ptr(), self.shs.data_ptr(), len(self),
+                           int(self.shs.shape[1]), 0)
+
+
+@dataclass
+class ParamGradients:
+    """Per-Gaussian gradients aligned with the input arrays (raster.py:85-98);
+    device tensors that are views of one flat f32 buffer (`flat`), so a
+    multi-GPU step all-reduces a single contiguous allocation."""
+
+    mean: torch.Tensor
+    rot: torch.Tensor
+    scale: torch.Tensor
+    opacity: torch.Tensor
+    sh: torch.Tensor
+    flat: Optional[torch.Tensor] = field(default=None, repr=False)
+
+    @staticmethod
+    def zeros(n: int, k: int, device) -> "ParamGradients":
+        flat = torch.zeros(n * (10 + 3 * k), dtype=torch.float32, device=device)
+        o = 0
+        views = []
+        for size, shape in ((3 * n, (n, 3)), (3 * n, (n, 3)), (3 * n, (n, 3)), (n, (n,)), (3 * k * n, (n, k, 3))):
+            views.append(flat[o:o + size].view(shape))
+            o += size
+        return ParamGradients(*views, flat=flat)
+
+    def struct(self) -> _lib.Grads:
+        return _lib.Grads(self.mean.data_ptr(), self.rot.data_ptr(), self.scale.data_ptr(),
+                          self.opacity.data_ptr(), self.sh.data_ptr())
+
+    def numpy(self) -> dict:
+        return {k: getattr(self, k).detach().cpu().numpy().astype(np.float64)
+                for k in ("mean", "rot", "scale", "opacity", "sh")}
+
+
+class PoseGradient:
+    """Loss gradient w.r.t. the rendering pose (raster.py:101-115).  The
+    device computes the camera-tangent pieces; the 6x6 extrinsic chain runs
+    on the host when first read (one 72-byte copy)."""
+
+    def __init__(self, dev_vals: torch.Tensor, R_cw: np.ndarray, T_ic):
+        self._dev = dev_vals
+        self._R_cw = R_cw
+        self._T_ic = T_ic
+        self._host = None
+
+    def _resolve(self):
+        if self._host is None:
+            v = self._dev.cpu().numpy()
+            rho_cam = v[0:3].copy()
+            tau_cam = v[3:6] - self._R_cw @ v[6:9]      # raster.py:380
+            A = imu_camera_adjoint(self._R_cw, self._T_ic)
+            imu = A.T @ np.concatenate([rho_cam, tau_cam])
+            self._host = (imu[:3], imu[3:], rho_cam, tau_cam)
+        return self._host
+
+    rho = property(lambda self: self._resolve()[0])
+    tau = property(lambda self: self._resolve()[1])
+    camera_rho = property(lambda self: self._resolve()[2])
+    camera_tau = property(lambda self: self._resolve()[3])
+
+    def as_vector(self) -> np.ndarray:
+        return np.concatenate([self.rho, self.tau])
+
+
+@dataclass
+class RenderOutput:
+    image: torch.Tensor                 # (H, W, 3) f32, device
+    final_transmittance: torch.Tensor   # (H, W) f32
+    contrib_count: torch.Tensor         # (H, W) int32, splats processed per pixel
+    cache: Optional["RenderState"] = field(default=None, repr=False)
+    depth: Optional[torch.Tensor] = None
+
+    def numpy(self) -> dict:
+        out = {"image": self.image.cpu().numpy().astype(np.float64),
+               "final_transmittance": self.final_transmittance.cpu().numpy().astype(np.float64),
+               "contrib_count": self.contrib_count.cpu().numpy().astype(np.int64)}
+        if self.depth is not None:
+            out["depth"] = self.depth.cpu().numpy().astype(np.float64)
+        return out
+
+
+# capacity hints per (n, W, H): the intersection count seen last time
+_CAP_HINT: dict = {}
+
+
+class RenderState:
+    """The render 'cache': the device workspace (records, tile lists,
+    partials) plus the structs the backward needs.  Opaque to callers, like
+    the reference's cache dict (raster.py:246-258)."""
+
+    def __init__(self, arrays: GaussianArrays, cam, R_cw, t_cw, settings: RasterSettings,
+                 isect_cap: int):
+        self.arrays = arrays
+        self.cam = cam
+        self.settings = settings
+        self.R_cw = np.asarray(R_cw, dtype=np.float64)
+        self.t_cw = np.asarray(t_cw, dtype=np.float64)
+        self.c_cam = _lib.make_camera(cam)
+        self.c_set = _lib.make_settings(settings)
+        self.c_pose = _lib.make_pose(self.R_cw, self.t_cw)
+        self.dims = _lib.Dims(len(arrays), int(cam.width), int(cam.height), int(arrays.shs.shape[1]), TILE,
+                              int(isect_cap))
+        nb = ctypes.c_size_t()
+        _lib.check(_lib.load().lsb_workspace_bytes(ctypes.byref(self.dims), ctypes.byref(nb)), "workspace")
+        self.ws = torch.empty(nb.value, dtype=torch.uint8, device=arrays.device)
+        self.counts = None
+
+    @property
+    def ws_bytes(self) -> int:
+        return self.ws.numel()
+
+    def read_counts(self, stream=None):
+        c = (ctypes.c_int64 * 4)()
+        _lib.check(_lib.load().lsb_render_counts(ctypes.c_void_p(self.ws.data_ptr()), ctypes.byref(self.dims),
+                                                 c, _lib.stream_ptr(stream)), "counts")
+        self.counts = tuple(int(v) for v in c)
+        return self.counts
+
+    def export(self, what: int, stream=None) -> np.ndarray:
+        """Parity hooks: 0 ids, 1 bboxes, 2 tile ranges, 3 tile entry ids, 4 depth."""
+        M, I = self.counts[0], self.counts[1]
+        ntiles = ((self.dims.width + TILE - 1) // TILE) * ((self.dims.height + TILE - 1) // TILE)
+        shape, dt = {0: ((M,), torch.int32), 1: ((M, 4), torch.int32), 2: ((ntiles, 2), torch.int32),
+                     3: ((I,), torch.int32), 4: ((M,), torch.float64)}[what]
+        dst = torch.empty(shape, dtype=dt, device=self.ws.device)
+        if dst.numel():
+            _lib.check(_lib.load().lsb_render_export(ctypes.c_void_p(self.ws.data_ptr()), ctypes.byref(self.dims),
+                                                     what, ctypes.c_void_p(dst.data_ptr()),
+                                                     _lib.stream_ptr(stream)), "export")
+        return dst.cpu().numpy()
+
+
+def _as_arrays(source) -> GaussianArrays:
+    if isinstance(source, GaussianArrays):
+        return source
+    if hasattr(source, "as_gaussian_arrays"):
+        a = source.as_gaussian_arrays()
+        return a if isinstance(a, GaussianArrays) else GaussianArrays(a.means, a.rots, a.scales, a.opacities,
+                                                                       a.shs)
+    if all(hasattr(source, k) for k in ("means", "rots", "scales", "opacities", "shs")):
+        return GaussianArrays(source.means, source.rots, source.scales, source.opacities, source.shs)
+    raise TypeError(f"cannot render from {type(source)!r}")
+
+
+def render_fwd(state: RenderState, image, t_final, n_contrib, depth=None, stream=None) -> None:
+    """Launch K1-K3 into `state` (async, no host sync)."""
+    p = state.arrays.params()
+    _lib.check(_lib.load().lsb_render_fwd(
+        ctypes.byref(p), ctypes.byref(state.c_cam), ctypes.byref(state.c_pose), ctypes.byref(state.c_set),
+        ctypes.c_void_p(state.ws.data_ptr()), state.ws_bytes, ctypes.byref(state.dims),
+        ctypes.c_void_p(image.data_ptr()), ctypes.c_void_p(t_final.data_ptr()),
+        ctypes.c_void_p(n_contrib.data_ptr()), ctypes.c_void_p(depth.data_ptr()) if depth is not None else None,
+        _lib.stream_ptr(stream)), "render")
+
+
+def render_bwd(state: RenderState, out: "RenderOutput", grad_image: torch.Tensor, grad_scale: float,
+               grads: ParamGradients, pose_dev: Optional[torch.Tensor], stream=None) -> None:
+    """Launch K4-K5 (async): ACCUMULATES into `grads`."""
+    p = state.arrays.params()
+    g = grads.struct()
+    _lib.check(_lib.load().lsb_render_bwd(
+        ctypes.byref(p), ctypes.byref(state.c_cam), ctypes.byref(state.c_pose), ctypes.byref(state.c_set),
+        ctypes.c_void_p(state.ws.data_ptr()), state.ws_bytes, ctypes.byref(state.dims),
+        ctypes.c_void_p(out.image.data_ptr()), ctypes.c_void_p(out.final_transmittance.data_ptr()),
+        ctypes.c_void_p(out.contrib_count.data_ptr()), ctypes.c_void_p(grad_image.data_ptr()),
+        float(grad_scale), ctypes.byref(g),
+        ctypes.c_void_p(pose_dev.data_ptr()) if pose_dev is not None else None,
+        _lib.stream_ptr(stream)), "backward")
+
+
+def render(source, T_wc, cam, settings: RasterSettings = RasterSettings(), retain_cache: bool = True,
+           with_depth: bool = False) -> RenderOutput:
+    """Splat, bin, depth-sort per tile and composite (raster.py:212-264).
+
+    Synchronises once to size the intersection buffers (the reference API is
+    synchronous too); the multi-view engine (engine.py) avoids that sync."""
+    _lib.require()
+    arrays = _as_arrays(source)
+    T_cw = as_se3(T_wc).inverse()
+    dev = arrays.device
+    h, w = int(cam.height), int(cam.width)
+    key = (len(arrays), w, h, float(settings.alpha_cut))
+    cap = max(_CAP_HINT.get(key, 0), 1 << 16, 8 * len(arrays))
+    image = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
+    t_final = torch.empty((h, w), dtype=torch.float32, device=dev)
+    n_contrib = torch.empty((h, w), dtype=torch.int32, device=dev)
+    depth = torch.empty((h, w), dtype=torch.float32, device=dev) if with_depth else None
+    while True:
+        state = RenderState(arrays, cam, T_cw.R, T_cw.t, settings, cap)
+        render_fwd(state, image, t_final, n_contrib, depth)
+        M, I, overflow, _ = state.read_counts()
+        if not overflow:
+            break
+        cap = int(I * 1.25) + 1024
+    _CAP_HINT[key] = int(I * 1.25) + 1024
+    return RenderOutput(image=image, final_transmittance=t_final, contrib_count=n_contrib,
+                        cache=state if retain_cache else None, depth=depth)
+
+
+def backward(out: RenderOutput, grad_image, T_ic=None):
+    """Analytic gradients for image gradient `grad_image` (raster.py:309-399).
+
+    Returns (ParamGradients on the device, PoseGradient)."""
+    state = out.cache
+    if state is None:
+        raise MissingCache("render() must be called with retain_cache=True")
+    T_ic = SE3.identity() if T_ic is None else T_ic
+    dev = state.ws.device
+    h, w = state.dims.height, state.dims.width
+    g_img = _f32(grad_image, (h, w, 3), dev)
+    grads = ParamGradients.zeros(len(state.arrays), int(state.arrays.shs.shape[1]), dev)
+    pose_dev = torch.zeros(9, dtype=torch.float64, device=dev)
+    render_bwd(state, out, g_img, 1.0, grads, pose_dev)
+    return grads, PoseGradient(pose_dev, state.R_cw, T_ic)
