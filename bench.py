@@ -1,0 +1,346 @@
+"""Benchmark: sliding-window splat fwd+bwd+Adam on B200 (BASELINE.json config 2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg2] [--alpha-cut 0.00392156862745098]
+
+One step = every keyframe view rendered (preprocess, tile binning, blend),
+scored (L1 photometric loss) and back-propagated into the window's
+gradient buffer, an NCCL all-reduce of that buffer when N > 1 (views sharded
+v -> rank v mod N), then one Adam step in storage coordinates on all window
+Gaussians.  Inputs: the reference's own synthetic room scene (sim.bake_scene
+restated in paper_2501_08672_b200/scene.py), orbit keyframes, observed images
+= clean renders, window = scene with SH colours perturbed U(-0.1, 0.1) (seed 0).
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the reference's CPU
+algorithm (the oracle port, oracle/) on this host's cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "splat fwd+bwd Mpix/s & Gaussians/s at 1/2/4/8 B200; % HBM roofline"
+CONFIGS = {
+    # name: (v_s, n_views, width, height)
+    "cfg1": (0.323, 1, 640, 512),
+    "cfg2": (0.0723, 10, 1280, 1024),
+    "cfg5": (0.0229, 64, 1920, 1080),
+}
+FALLBACK_HBM_GBS = 6650.0
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def build_workload(cfg_name, alpha_cut):
+    from paper_2501_08672_b200.scene import bake_room, camera_for, orbit_views
+    v_s, V, W, H = CONFIGS[cfg_name]
+    means, rots, scales, opac, shs = bake_room(v_s)
+    rng = np.random.default_rng(0)
+    shs_win = shs.copy()
+    shs_win[:, 0, :] += rng.uniform(-0.1, 0.1, size=shs_win[:, 0, :].shape)
+    return dict(gt=(means, rots, scales, opac, shs), win=(means, rots, scales, opac, shs_win),
+                cam=camera_for(W, H), views=orbit_views(V), V=V, W=W, H=H, N=len(means),
+                alpha_cut=alpha_cut)
+
+
+# ---------------------------------------------------------------- CPU legs ---
+def cpu_sample(wl, n_views_sample):
+    """Reference algorithm on this host (oracle port, C + numpy, all cores):
+    n_views_sample views of render + L1 loss + backward, then one Adam step
+    on all window Gaussians.  Returns (seconds per sampled view, seconds per
+    Adam step, host threads)."""
+    from types import SimpleNamespace
+    from oracle import raster as orc
+    from oracle.optim import Adam, DEFAULT_CFG, adam_param_step, photometric_loss
+
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)
+    keys = ("means", "rots", "scales", "opacities", "shs")
+    gt = {k: f32(v) for k, v in zip(keys, wl["gt"])}
+    P = {k: f32(v) for k, v in zip(keys, wl["win"])}
+    cam = wl["cam"]
+    st = SimpleNamespace(near=0.01, dilation=0.3, alpha_clamp=0.99, transmittance_min=1e-4, footprint_sigma=6.0,
+                         alpha_cut=wl["alpha_cut"], max_footprint_px=512.0, background=np.zeros(3), sh_degree=0)
+    t_view = []
+    for T in wl["views"][:n_views_sample]:
+        T_cw = T.inverse()
+        obs = orc.render(gt, T_cw.R, T_cw.t, cam, st)["image"]
+        t0 = time.perf_counter()
+        c = orc.render(P, T_cw.R, T_cw.t, cam, st)
+        _, _, g_img = photometric_loss(c["image"], obs)
+        orc.backward(c, g_img)
+        t_view.append(time.perf_counter() - t0)
+        del c
+    n = len(P["means"])
+    adam = Adam({"mean": (n, 3), "rot": (n, 3), "scale": (n, 3), "opacity": (n,), "sh": P["shs"].shape})
+    rng = np.random.default_rng(1)
+    grads = {"mean": rng.normal(size=(n, 3)), "rot": rng.normal(size=(n, 3)), "scale": rng.normal(size=(n, 3)),
+             "opacity": rng.normal(size=n), "sh": rng.normal(size=P["shs"].shape)}
+    t0 = time.perf_counter()
+    adam_param_step(P, grads, adam, DEFAULT_CFG, np.zeros(n, bool))
+    t_adam = time.perf_counter() - t0
+    return float(np.mean(t_view)), t_adam, os.cpu_count()
+
+
+def run_reference(args, wl, rank):
+    if rank != 0:
+        return
+    V, P_px = wl["V"], wl["W"] * wl["H"]
+    times = []
+    for i in range(args.warmup + args.steps):
+        tv, ta, cores = cpu_sample(wl, 1)
+        if i >= args.warmup:
+            times.append(V * tv + ta)      # one full step, extrapolated from one sampled view
+    t = float(np.mean(times))
+    value = V * P_px / t / 1e6
+    sample = (f"1 of {V} views per step (render + L1 loss + backward, {wl['W']}x{wl['H']}, {wl['N']} Gaussians, "
+              f"alpha_cut={wl['alpha_cut']:.6g}) + one Adam step; step time = {V} x view + Adam")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Mpix/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "gaussians_per_s": V * wl["N"] / t,
+        "config": {"workload": args.config, "gaussians": wl["N"], "views": V, "width": wl["W"],
+                   "height": wl["H"], "alpha_cut": wl["alpha_cut"], "parallelism": "cpu threads"},
+        "cpu_baseline": {"value": value, "unit": "Mpix/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ---------------------------------------------------------------- GPU leg ----
+def algorithmic_bytes(N, K, M, I, P):
+    """Per-launch algorithmic HBM bytes."""
+    prm = 4 * (16 + 3 * K)          # one Gaussian's parameters (f32)
+    grd = 4 * (10 + 3 * K)          # one Gaussian's gradient / moment row
+    return {
+        "bin": N * prm + M * (64 + 8 + 4) + I * (4 + 4 + 4 + 8 + 4 + 4),
+        "blend_fwd": I * (64 + 4) + P * (12 + 4 + 4),
+        "blend_bwd": I * (64 + 4 + 4 + 36) + P * (12 + 12 + 4),
+        "chain": M * (64 + 4 + prm + 2 * grd) + I * 36,
+        "adam": N * (2 * prm + grd + 4 * grd + 1),
+    }
+
+
+def run_ours(args, wl, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2501_08672_b200.optimize import OptimConfig, WindowEngine
+    from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    settings = RasterSettings(alpha_cut=wl["alpha_cut"])
+    V, W, H, N = wl["V"], wl["W"], wl["H"], wl["N"]
+    gt = GaussianArrays(*wl["gt"], device=dev)
+    win = GaussianArrays(*wl["win"], device=dev)
+    my_views = [v for v in range(V) if v % world == rank]
+    observed = [render(gt, wl["views"][v], wl["cam"], settings, retain_cache=False).image.clone()
+                for v in my_views]
+    del gt
+    stream = torch.cuda.Stream(dev)
+    eng = WindowEngine(win, wl["cam"], [wl["views"][v] for v in my_views], settings, OptimConfig(),
+                       n_views_total=V, stream=stream)
+    counts = []
+    for v in range(len(my_views)):      # per-view M, I for the byte model
+        T = eng.views[v]
+        eng.state.set_pose(T.R, T.t)
+        from paper_2501_08672_b200.raster import render_bin
+        render_bin(eng.state, stream)
+        counts.append(eng.state.read_counts(stream)[:2])
+    allreduce = (lambda t: dist.all_reduce(t)) if world > 1 else None
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            eng.step(observed, allreduce=allreduce)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    timers: dict = {}
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    smi_index = int(vis.split(",")[local_rank]) if vis and vis.split(",")[local_rank].isdigit() else local_rank
+    with ClockSampler(smi_index) as clk:
+        time.sleep(0.3)
+        with torch.cuda.stream(stream):
+            start.record(stream)
+            for _ in range(args.steps):
+                eng.step(observed, allreduce=allreduce, timers=timers)
+            eng.finish()
+            end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(end) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    assert eng.check_capacity(), "intersection capacity exceeded during the timed region"
+    losses = eng.losses()
+
+    # per-kernel device time inside the timed region (event pairs on `stream`)
+    ktime = {k: [ev[i].elapsed_time(ev[i + 1]) for i in range(0, len(ev), 2)] for k, ev in timers.items()}
+    M_avg = float(np.mean([c[0] for c in counts])) if counts else 0.0
+    I_avg = float(np.mean([c[1] for c in counts])) if counts else 0.0
+    K = int(win.shs.shape[1])
+    ab = algorithmic_bytes(N, K, M_avg, I_avg, W * H)
+    per_step_ms = {k: float(np.sum(v)) / args.steps for k, v in ktime.items()}
+    dom = max(("bin", "blend_fwd", "blend_bwd", "chain"), key=lambda k: per_step_ms.get(k, 0.0))
+    dom_ms = float(np.mean(ktime[dom]))
+    hbm, hbm_src = peaks()
+    achieved = ab[dom] / (dom_ms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(dom)
+    step_bytes = sum(ab[k] * (len(my_views) if k != "adam" else 1) for k in ab)
+
+    # end-to-end through the public API with host buffers: H2D of this rank's
+    # observed images from pinned memory + the step + D2H of the loss sums
+    host_obs = [o.cpu().pin_memory() for o in observed]
+    dev_obs = [torch.empty_like(o) for o in observed]
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e_start.record(stream)
+        for _ in range(args.steps):
+            for h, d in zip(host_obs, dev_obs):
+                d.copy_(h, non_blocking=True)
+            eng.step(dev_obs, allreduce=allreduce)
+            _ = eng.loss.sums().to("cpu", non_blocking=False)
+        e_end.record(stream)
+    torch.cuda.synchronize()
+    e_ms = e_start.elapsed_time(e_end) / args.steps
+    if world > 1:
+        t = torch.tensor([e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+    h2d = sum(o.numel() * 4 for o in observed)
+    d2h = int(eng.loss.sums().numel() * 8)
+
+    if rank == 0:
+        value = V * W * H / (ms * 1e-3) / 1e6
+        out = {
+            "metric": METRIC, "value": value, "unit": "Mpix/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "gaussians_per_s": V * N / (ms * 1e-3),
+            "visible_splats_per_s": float(sum(c[0] for c in counts)) * world / (ms * 1e-3),
+            "config": {"workload": args.config, "gaussians": N, "views": V, "width": W, "height": H,
+                       "alpha_cut": wl["alpha_cut"], "parallelism": f"view-sharded dp{world}",
+                       "l2": "working set > L2: observed views alone are V x 15.7 MB",
+                       "loss_last_step": float(np.mean(losses))},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "peak_source": hbm_src,
+                         "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": ab[dom], "avg_launch_ms": dom_ms,
+                         "note": "blend is FP32-issue bound (SURVEY.md §8(d)); see profiles/"},
+            "step_roofline": {"algorithmic_bytes_per_step_rank0": step_bytes,
+                              "frac": step_bytes / (ms * 1e-3) / 1e9 / hbm},
+            "kernel_ms_per_step": per_step_ms,
+            "counts_per_view": {"visible_M": M_avg, "intersections_I": I_avg},
+            "clocks": clk.summary(),
+            "e2e": {"value": V * W * H / (e_ms * 1e-3) / 1e6, "unit": "Mpix/s",
+                    "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world, "ms_per_step": e_ms},
+            "gpu_launches": args.steps * (len(my_views) * 8 + 1) + 1,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            tv, ta, cores = cpu_sample(wl, 2)
+            t_cpu = V * tv + ta
+            out["cpu_baseline"] = {
+                "value": V * W * H / t_cpu / 1e6, "unit": "Mpix/s", "cores": cores, "kind": "port",
+                "sample": f"2 of {V} views (render + L1 + backward) + 1 Adam step on the oracle port; "
+                          f"step = {V} x mean view time + Adam ({t_cpu:.2f} s)"}
+        print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--alpha-cut", type=float, default=1.0 / 255.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    wl = build_workload(args.config, args.alpha_cut)
+    if args.impl == "reference":
+        run_reference(args, wl, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, wl, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

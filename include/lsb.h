@@ -152,6 +152,37 @@ int lsb_render_bwd(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T
                    const float* grad_image, float grad_scale, const lsb_grads* g,
                    double* pose_out, void* stream);
 
+/* ---- split launches of the same passes (for per-kernel timing / overlap) --
+ * lsb_render_fwd == lsb_render_bin + lsb_render_blend;
+ * lsb_render_bwd == lsb_render_blend_bwd + lsb_render_chain.            */
+int lsb_render_bin(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T_cw,
+                   const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
+                   void* stream);
+int lsb_render_blend(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
+                     float* image, float* t_final, int32_t* n_contrib, float* depth, void* stream);
+int lsb_render_blend_bwd(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
+                         const float* image, const int32_t* n_contrib, const float* grad_image,
+                         float grad_scale, void* stream);
+int lsb_render_chain(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T_cw,
+                     const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
+                     const lsb_grads* g, double* pose_out, void* stream);
+
+/* ---- Adam in storage coordinates: replaces AdamState.update + the
+ * optimize_window parameter steps (optimize.py:103-119, 159-188).
+ * Updates the window arena IN PLACE through p (means, rots, scales,
+ * opacities, shs).  grads/m/v are flat f32 buffers laid out
+ * [mean 3n | rot 3n | scale 3n | opacity n | sh 3Kn] (the ParamGradients
+ * layout); touched (n bytes) records rotation rows that were stepped. */
+typedef struct lsb_adam_cfg {
+    double lr_mean, lr_rot, lr_scale, lr_opacity, lr_sh;
+    double beta1, beta2, eps, scene_scale, opacity_clip, scale_floor;
+    int64_t step;          /* 1-based shared step count (bias correction) */
+} lsb_adam_cfg;
+int lsb_adam_step(const lsb_params* p, const float* grads, float* m, float* v, uint8_t* touched,
+                  const lsb_adam_cfg* cfg, void* stream);
+/* Column Gram-Schmidt of touched rotation rows (optimize.py:91-100,193-194). */
+int lsb_orthonormalize(float* rots, const uint8_t* touched, int64_t n, void* stream);
+
 /* ---- photometric loss: replaces optimize.photometric_loss (optimize.py:48-74)
  * kind 0 = L1, 1 = L2 over (npx, 3) f32 images; mask (npx) u8 may be NULL.
  * grad_out (npx,3) f32 = sign(diff) (L1) or 2 diff (L2), times grad_scale

@@ -51,6 +51,12 @@ class Dims(_c.Structure):
                 ("sh_coeffs", _c.c_int32), ("tile", _c.c_int32), ("isect_cap", _c.c_int64)]
 
 
+class AdamCfg(_c.Structure):
+    _fields_ = [(k, _c.c_double) for k in ("lr_mean", "lr_rot", "lr_scale", "lr_opacity", "lr_sh", "beta1",
+                                           "beta2", "eps", "scene_scale", "opacity_clip", "scale_floor")] + [
+        ("step", _c.c_int64)]
+
+
 # (name, restype, argtypes) for every symbol include/lsb.h declares
 SIGNATURES = [
     ("lsb_abi_version", _c.c_int, []),
@@ -64,6 +70,17 @@ SIGNATURES = [
     ("lsb_render_bwd", _c.c_int, [_c.POINTER(Params), _c.POINTER(Camera), _c.POINTER(Pose),
                                   _c.POINTER(Settings), _P, _c.c_size_t, _c.POINTER(Dims),
                                   _P, _P, _P, _P, _c.c_float, _c.POINTER(Grads), _P, _P]),
+    ("lsb_render_bin", _c.c_int, [_c.POINTER(Params), _c.POINTER(Camera), _c.POINTER(Pose),
+                                  _c.POINTER(Settings), _P, _c.c_size_t, _c.POINTER(Dims), _P]),
+    ("lsb_render_blend", _c.c_int, [_c.POINTER(Settings), _P, _c.c_size_t, _c.POINTER(Dims), _P, _P, _P, _P,
+                                    _P]),
+    ("lsb_render_blend_bwd", _c.c_int, [_c.POINTER(Settings), _P, _c.c_size_t, _c.POINTER(Dims), _P, _P, _P,
+                                        _c.c_float, _P]),
+    ("lsb_render_chain", _c.c_int, [_c.POINTER(Params), _c.POINTER(Camera), _c.POINTER(Pose),
+                                    _c.POINTER(Settings), _P, _c.c_size_t, _c.POINTER(Dims),
+                                    _c.POINTER(Grads), _P, _P]),
+    ("lsb_adam_step", _c.c_int, [_c.POINTER(Params), _P, _P, _P, _P, _c.POINTER(AdamCfg), _P]),
+    ("lsb_orthonormalize", _c.c_int, [_P, _P, _c.c_int64, _P]),
     ("lsb_loss_scratch_doubles", _c.c_int, []),
     ("lsb_photometric_loss", _c.c_int, [_P, _P, _P, _c.c_int64, _c.c_int64, _c.c_int, _c.c_float,
                                         _P, _P, _P]),

@@ -17,6 +17,9 @@ cudaError_t launch_chain(const Ws&, const lsb_params&, const lsb_grads&, const l
 cudaError_t launch_loss(const float*, const float*, const uint8_t*, int64_t, int, float, float*, double*,
                         cudaStream_t);
 int loss_scratch_doubles();
+cudaError_t launch_adam(const lsb_params&, const float*, float*, float*, uint8_t*, const lsb_adam_cfg&,
+                        cudaStream_t);
+cudaError_t launch_orthonormalize(float*, const uint8_t*, int64_t, cudaStream_t);
 }  // namespace lsb
 
 using namespace lsb;
@@ -160,6 +163,78 @@ int lsb_render_bwd(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T
                     "blend_bwd");
     if (rc) return rc;
     return check_cuda(launch_chain(w, *p, *g, *cam, *T, *s, pose_out, st), "chain");
+}
+
+static int params_ok(const lsb_params* p, const lsb_dims* d) {
+    if (!p) return fail(LSB_EINVAL, "NULL params");
+    if (p->n != d->n) return fail(LSB_EINVAL, "dims do not match params");
+    if (p->n > 0 && (!p->means || !p->rots || !p->scales || !p->opacities || !p->shs))
+        return fail(LSB_EINVAL, "NULL parameter array");
+    if (p->sh_coeffs < 1 || p->sh_coeffs > 16) return fail(LSB_EINVAL, "sh_coeffs must be 1..16");
+    return LSB_OK;
+}
+
+int lsb_render_bin(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T, const lsb_settings* s,
+                   void* ws, size_t ws_bytes, const lsb_dims* d, void* stream) {
+    if (!cam || !T || !s) return fail(LSB_EINVAL, "NULL argument");
+    Ws w;
+    int rc = get_ws(ws, ws_bytes, d, &w);
+    if (rc) return rc;
+    rc = params_ok(p, d);
+    if (rc) return rc;
+    if (cam->width != d->width || cam->height != d->height) return fail(LSB_EINVAL, "camera/dims mismatch");
+    return check_cuda(launch_preprocess(*p, *cam, *T, *s, w, (cudaStream_t)stream), "bin");
+}
+
+int lsb_render_blend(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* d, float* image,
+                     float* t_final, int32_t* n_contrib, float* depth, void* stream) {
+    if (!s || !image || !t_final || !n_contrib) return fail(LSB_EINVAL, "NULL argument");
+    Ws w;
+    int rc = get_ws(ws, ws_bytes, d, &w);
+    if (rc) return rc;
+    return check_cuda(launch_blend_fwd(w, *s, d->width, d->height, image, t_final, n_contrib, depth,
+                                       (cudaStream_t)stream), "blend");
+}
+
+int lsb_render_blend_bwd(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* d,
+                         const float* image, const int32_t* n_contrib, const float* grad_image,
+                         float grad_scale, void* stream) {
+    if (!s) return fail(LSB_EINVAL, "NULL argument");
+    if (!image || !n_contrib || !grad_image) return fail(LSB_EMISSING_CACHE, "render outputs missing");
+    Ws w;
+    int rc = get_ws(ws, ws_bytes, d, &w);
+    if (rc) return rc;
+    return check_cuda(launch_blend_bwd(w, *s, d->width, d->height, image, n_contrib, grad_image, grad_scale,
+                                       (cudaStream_t)stream), "blend_bwd");
+}
+
+int lsb_render_chain(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T, const lsb_settings* s,
+                     void* ws, size_t ws_bytes, const lsb_dims* d, const lsb_grads* g, double* pose_out,
+                     void* stream) {
+    if (!cam || !T || !s || !g) return fail(LSB_EINVAL, "NULL argument");
+    Ws w;
+    int rc = get_ws(ws, ws_bytes, d, &w);
+    if (rc) return rc;
+    rc = params_ok(p, d);
+    if (rc) return rc;
+    if (p->n > 0 && (!g->mean || !g->rot || !g->scale || !g->opacity || !g->sh))
+        return fail(LSB_EINVAL, "NULL gradient array");
+    return check_cuda(launch_chain(w, *p, *g, *cam, *T, *s, pose_out, (cudaStream_t)stream), "chain");
+}
+
+int lsb_adam_step(const lsb_params* p, const float* grads, float* m, float* v, uint8_t* touched,
+                  const lsb_adam_cfg* cfg, void* stream) {
+    if (!p || !cfg) return fail(LSB_EINVAL, "NULL argument");
+    if (p->n > 0 && (!grads || !m || !v || !touched || !p->means || !p->rots || !p->scales || !p->opacities ||
+                     !p->shs))
+        return fail(LSB_EINVAL, "NULL array");
+    if (cfg->step < 1) return fail(LSB_EINVAL, "Adam step count must be >= 1");
+    return check_cuda(launch_adam(*p, grads, m, v, touched, *cfg, (cudaStream_t)stream), "adam");
+}
+
+int lsb_orthonormalize(float* rots, const uint8_t* touched, int64_t n, void* stream) {
+    if (n > 0 && (!rots || !touched)) return fail(LSB_EINVAL, "NULL array");
+    return check_cuda(launch_orthonormalize(rots, touched, n, (cudaStream_t)stream), "orthonormalize");
 }
 
 int lsb_photometric_loss(const float* rendered, const float* observed, const uint8_t* mask, int64_t npx,

@@ -1,0 +1,301 @@
+"""Photometric window optimisation on the B200 — drop-in for livsplat.optimize.
+
+photometric_loss (optimize.py:48-74), OptimConfig / LossReport, and
+optimize_window (optimize.py:122-202) keep the reference's names, arguments
+and error behaviour.  The multi-keyframe step the benchmark configs ask for
+ is `WindowEngine`: per step, every keyframe view is
+rendered, scored and back-propagated into one gradient buffer (the mean of
+the per-view reference gradients), optionally all-reduced across ranks
+(views sharded by rank), then one Adam step in storage coordinates runs.
+No host synchronisation inside a step.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import EmptyMask
+from .geometry import as_se3
+from .raster import (GaussianArrays, ParamGradients, RasterSettings, RenderState, _as_arrays, _f32,
+                     render_bin, render_blend, render_blend_bwd, render_chain)
+
+
+@dataclass
+class OptimConfig:
+    """optimize.py:22-36 (identical fields and defaults)."""
+
+    iters: int = 10
+    lr_mean: float = 1.6e-4
+    lr_sh: float = 2.5e-3
+    lr_opacity: float = 5e-2
+    lr_scale: float = 5e-3
+    lr_rot: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-15
+    scene_scale: float = 1.0
+    loss: str = "l1"
+    opacity_clip: float = 1e-4
+    scale_floor: float = 1e-6
+
+
+@dataclass
+class LossReport:
+    value: float
+    residual: Optional[torch.Tensor] = field(default=None, repr=False)
+    pixel_count: int = 0
+    mse: float = 0.0
+    t_ms: float = 0.0
+
+
+_KIND = {"l1": 0, "l2": 1}
+
+
+class LossBuffers:
+    """Device scratch for one loss evaluation (zeroed once, reused)."""
+
+    def __init__(self, device, views: int = 1):
+        n = _lib.load().lsb_loss_scratch_doubles()
+        self.n = n
+        self.buf = torch.zeros((views, n), dtype=torch.float64, device=device)
+
+    def ptr(self, v: int = 0):
+        return ctypes.c_void_p(self.buf[v].data_ptr())
+
+    def sums(self) -> torch.Tensor:
+        return self.buf[:, :2]
+
+
+def launch_loss(rendered: torch.Tensor, observed: torch.Tensor, mask: Optional[torch.Tensor], count: int,
+                kind: str, grad_scale: float, grad_out: Optional[torch.Tensor], scratch_ptr, stream=None):
+    npx = rendered.numel() // 3
+    _lib.check(_lib.load().lsb_photometric_loss(
+        ctypes.c_void_p(rendered.data_ptr()), ctypes.c_void_p(observed.data_ptr()),
+        ctypes.c_void_p(mask.data_ptr()) if mask is not None else None, npx, count, _KIND[kind],
+        float(grad_scale), ctypes.c_void_p(grad_out.data_ptr()) if grad_out is not None else None,
+        scratch_ptr, _lib.stream_ptr(stream)), "photometric_loss")
+
+
+def _mask_u8(mask, h, w, device):
+    if mask is None:
+        return None, h * w
+    m = torch.as_tensor(mask).to(device=device).reshape(h, w).to(torch.uint8).contiguous()
+    return m, int(m.sum().item())
+
+
+def photometric_loss(rendered, observed, mask=None, kind: str = "l1"):
+    """Masked mean per-channel photometric error and its image gradient
+    (optimize.py:48-74).  Returns (LossReport, grad (H,W,3) device f32)."""
+    _lib.require()
+    if kind not in _KIND:
+        raise ValueError(f"unknown loss kind {kind!r}")
+    dev = rendered.device if torch.is_tensor(rendered) and rendered.is_cuda else torch.device("cuda")
+    r = _f32(rendered, tuple(np.shape(rendered)), dev)
+    o = _f32(observed, tuple(np.shape(observed)), dev)
+    if r.shape != o.shape:
+        raise ValueError("image shapes differ")
+    h, w = r.shape[:2]
+    m, count = _mask_u8(mask, h, w, dev)
+    if count == 0:
+        raise EmptyMask("mask selects no pixels")
+    denom = 3.0 * count
+    grad = torch.empty_like(r)
+    lb = LossBuffers(dev)
+    launch_loss(r, o, m, count, kind, 1.0 / denom, grad, lb.ptr())
+    s = lb.sums()[0].cpu().numpy()
+    diff = (r - o).abs().mean(dim=2)
+    residual = diff if m is None else diff * m
+    return LossReport(value=float(s[0] / denom), residual=residual, pixel_count=count,
+                      mse=float(s[1] / denom)), grad
+
+
+def adam_cfg(cfg: OptimConfig, step: int) -> _lib.AdamCfg:
+    return _lib.AdamCfg(cfg.lr_mean, cfg.lr_rot, cfg.lr_scale, cfg.lr_opacity, cfg.lr_sh, cfg.beta1, cfg.beta2,
+                        cfg.eps, cfg.scene_scale, cfg.opacity_clip, cfg.scale_floor, int(step))
+
+
+class AdamState:
+    """Moments per parameter group (optimize.py:103-119), device-resident
+    and laid out like ParamGradients.flat so one kernel steps every group."""
+
+    def __init__(self, arrays: GaussianArrays, cfg: OptimConfig):
+        n, k = len(arrays), int(arrays.shs.shape[1])
+        self.cfg = cfg
+        self.step = 0
+        self.m = torch.zeros(n * (10 + 3 * k), dtype=torch.float32, device=arrays.device)
+        self.v = torch.zeros_like(self.m)
+        self.touched = torch.zeros(n, dtype=torch.uint8, device=arrays.device)
+
+    def apply(self, arrays: GaussianArrays, grads: ParamGradients, stream=None) -> None:
+        """One Adam step in storage coordinates, in place on the arena."""
+        self.step += 1
+        c = adam_cfg(self.cfg, self.step)
+        p = arrays.params()
+        _lib.check(_lib.load().lsb_adam_step(ctypes.byref(p), ctypes.c_void_p(grads.flat.data_ptr()),
+                                             ctypes.c_void_p(self.m.data_ptr()), ctypes.c_void_p(self.v.data_ptr()),
+                                             ctypes.c_void_p(self.touched.data_ptr()), ctypes.byref(c),
+                                             _lib.stream_ptr(stream)), "adam")
+
+    def orthonormalize(self, arrays: GaussianArrays, stream=None) -> None:
+        _lib.check(_lib.load().lsb_orthonormalize(ctypes.c_void_p(arrays.rots.data_ptr()),
+                                                  ctypes.c_void_p(self.touched.data_ptr()), len(arrays),
+                                                  _lib.stream_ptr(stream)), "orthonormalize")
+
+
+class WindowEngine:
+    """Multi-keyframe photometric optimisation of one window on one GPU.
+
+    `views` are the keyframe poses T_WC this rank renders; `n_views_total` is
+    the number of views in the whole (possibly sharded) step, so every rank
+    scales its gradient by 1/n_views_total and an all-reduce(sum) yields the
+    mean of the per-view gradients.  One render workspace is reused for all
+    views (views run back to back on one stream)."""
+
+    def __init__(self, arrays: GaussianArrays, cam, views: Sequence, settings: RasterSettings,
+                 cfg: OptimConfig = OptimConfig(), n_views_total: Optional[int] = None,
+                 isect_cap: Optional[int] = None, stream=None):
+        _lib.require()
+        self.arrays = arrays
+        self.cam = cam
+        self.settings = settings
+        self.cfg = cfg
+        self.stream = stream
+        self.views = [as_se3(T).inverse() for T in views]
+        self.n_total = n_views_total or len(self.views)
+        dev = arrays.device
+        h, w = int(cam.height), int(cam.width)
+        self.h, self.w = h, w
+        self.image = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
+        self.t_final = torch.empty((h, w), dtype=torch.float32, device=dev)
+        self.n_contrib = torch.empty((h, w), dtype=torch.int32, device=dev)
+        self.grad_image = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
+        self.loss = LossBuffers(dev, max(1, len(self.views)))
+        self.grads = ParamGradients.zeros(len(arrays), int(arrays.shs.shape[1]), dev)
+        self.adam = AdamState(arrays, cfg)
+        if isect_cap is None:
+            isect_cap = self.calibrate()
+        T0 = self.views[0] if self.views else _identity()
+        self.state = RenderState(arrays, cam, T0.R, T0.t, settings, isect_cap)
+
+    def calibrate(self, headroom: float = 1.3) -> int:
+        """Measure the largest per-view intersection count (one sync per view)."""
+        cap = max(1 << 16, 8 * len(self.arrays))
+        worst = 0
+        for T in self.views:
+            while True:
+                st = RenderState(self.arrays, self.cam, T.R, T.t, self.settings, cap)
+                render_bin(st, stream=self.stream)
+                M, I, over, _ = st.read_counts(self.stream)
+                if not over:
+                    break
+                cap = int(I * 1.25) + 1024
+            worst = max(worst, I)
+        self.max_isect = worst
+        return int(worst * headroom) + 1024
+
+    def check_capacity(self) -> bool:
+        """True if the last render in the workspace fit (syncs)."""
+        return not self.state.read_counts(self.stream)[2]
+
+    def step(self, observed: Sequence[torch.Tensor], allreduce=None, timers: Optional[dict] = None) -> None:
+        """One optimisation step over this rank's views (async)."""
+        st = self.state
+        gscale = 1.0 / (3.0 * self.h * self.w * self.n_total)
+        self.grads.flat.zero_()
+
+        def mark(name, start):
+            # timers[name] collects (start, end) event pairs on this stream
+            if timers is not None:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(self.stream)
+                timers.setdefault(name, []).append(ev)
+
+        for v, T in enumerate(self.views):
+            st.set_pose(T.R, T.t)
+            mark("bin", True); render_bin(st, self.stream); mark("bin", False)
+            mark("blend_fwd", True)
+            render_blend(st, self.image, self.t_final, self.n_contrib, stream=self.stream)
+            mark("blend_fwd", False)
+            launch_loss(self.image, observed[v], None, self.h * self.w, self.cfg.loss, gscale, self.grad_image,
+                        self.loss.ptr(v), self.stream)
+            mark("blend_bwd", True)
+            render_blend_bwd(st, self.image, self.n_contrib, self.grad_image, 1.0, self.stream)
+            mark("blend_bwd", False)
+            mark("chain", True); render_chain(st, self.grads, None, self.stream); mark("chain", False)
+        if allreduce is not None:
+            allreduce(self.grads.flat)
+        mark("adam", True); self.adam.apply(self.arrays, self.grads, self.stream); mark("adam", False)
+
+    def finish(self) -> None:
+        """End of the window optimisation: re-orthonormalise stepped rotations."""
+        self.adam.orthonormalize(self.arrays, self.stream)
+
+    def losses(self) -> np.ndarray:
+        """Per-view loss values of the last step (syncs; one small D2H)."""
+        s = self.loss.sums()[: len(self.views)].cpu().numpy()
+        return s[:, 0] / (3.0 * self.h * self.w)
+
+
+def _identity():
+    from .geometry import SE3
+    return SE3.identity()
+
+
+def optimize_window(window, observed, T_wc, cam, cfg: OptimConfig = OptimConfig(),
+                    settings: RasterSettings = RasterSettings(), iters: int = None, mask=None) -> list:
+    """Render, back-propagate and step the window parameters in place
+    (optimize.py:122-202).  `window` is anything with a device arena
+    (`as_gaussian_arrays()` returning GaussianArrays, or GaussianArrays
+    itself); its tensors are updated in place.  Returns one LossReport per
+    iteration."""
+    iters = cfg.iters if iters is None else iters
+    history: list = []
+    arrays = _as_arrays(window)
+    if iters == 0 or len(arrays) == 0:
+        return history
+    dev = arrays.device
+    h, w = int(cam.height), int(cam.width)
+    obs = _f32(observed, (h, w, 3), dev)
+    m, count = _mask_u8(mask, h, w, dev)
+    if count == 0:
+        raise EmptyMask("mask selects no pixels")
+    eng = WindowEngine(arrays, cam, [T_wc], settings, cfg)
+    for _ in range(iters):
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record()
+        if m is None:
+            eng.step([obs])
+            if not eng.check_capacity():
+                raise RuntimeError("intersection capacity exceeded mid-optimisation")
+        else:
+            _masked_step(eng, obs, m, count)
+        end.record()
+        s = eng.loss.sums()[0].cpu().numpy()
+        rep = LossReport(value=float(s[0] / (3.0 * count)), pixel_count=count, mse=float(s[1] / (3.0 * count)),
+                         t_ms=start.elapsed_time(end))
+        history.append(rep)
+    eng.finish()
+    if hasattr(window, "mark_device_dirty_live"):
+        window.mark_device_dirty_live()
+    torch.cuda.synchronize()
+    return history
+
+
+def _masked_step(eng: WindowEngine, obs, m, count):
+    st = eng.state
+    T = eng.views[0]
+    eng.grads.flat.zero_()
+    st.set_pose(T.R, T.t)
+    render_bin(st)
+    render_blend(st, eng.image, eng.t_final, eng.n_contrib)
+    launch_loss(eng.image, obs, m, count, eng.cfg.loss, 1.0 / (3.0 * count), eng.grad_image, eng.loss.ptr(0))
+    render_blend_bwd(st, eng.image, eng.n_contrib, eng.grad_image, 1.0)
+    render_chain(st, eng.grads, None)
+    eng.adam.apply(eng.arrays, eng.grads)

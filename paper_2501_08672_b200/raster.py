@@ -206,6 +206,14 @@ class RenderState:
     def ws_bytes(self) -> int:
         return self.ws.numel()
 
+    def set_pose(self, R_cw, t_cw) -> None:
+        self.R_cw = np.asarray(R_cw, dtype=np.float64)
+        self.t_cw = np.asarray(t_cw, dtype=np.float64)
+        self.c_pose = _lib.make_pose(self.R_cw, self.t_cw)
+
+    def _ws(self):
+        return ctypes.c_void_p(self.ws.data_ptr())
+
     def read_counts(self, stream=None):
         c = (ctypes.c_int64 * 4)()
         _lib.check(_lib.load().lsb_render_counts(ctypes.c_void_p(self.ws.data_ptr()), ctypes.byref(self.dims),
@@ -248,6 +256,43 @@ def render_fwd(state: RenderState, image, t_final, n_contrib, depth=None, stream
         ctypes.c_void_p(image.data_ptr()), ctypes.c_void_p(t_final.data_ptr()),
         ctypes.c_void_p(n_contrib.data_ptr()), ctypes.c_void_p(depth.data_ptr()) if depth is not None else None,
         _lib.stream_ptr(stream)), "render")
+
+
+def render_bin(state: RenderState, stream=None) -> None:
+    """K1 preprocess + K2 binning/sort (async)."""
+    p = state.arrays.params()
+    _lib.check(_lib.load().lsb_render_bin(ctypes.byref(p), ctypes.byref(state.c_cam), ctypes.byref(state.c_pose),
+                                          ctypes.byref(state.c_set), state._ws(), state.ws_bytes,
+                                          ctypes.byref(state.dims), _lib.stream_ptr(stream)), "bin")
+
+
+def render_blend(state: RenderState, image, t_final, n_contrib, depth=None, stream=None) -> None:
+    """K3 blend forward (async)."""
+    _lib.check(_lib.load().lsb_render_blend(
+        ctypes.byref(state.c_set), state._ws(), state.ws_bytes, ctypes.byref(state.dims),
+        ctypes.c_void_p(image.data_ptr()), ctypes.c_void_p(t_final.data_ptr()),
+        ctypes.c_void_p(n_contrib.data_ptr()), ctypes.c_void_p(depth.data_ptr()) if depth is not None else None,
+        _lib.stream_ptr(stream)), "blend")
+
+
+def render_blend_bwd(state: RenderState, image, n_contrib, grad_image, grad_scale: float = 1.0,
+                     stream=None) -> None:
+    """K4 blend backward into the per-intersection partials (async)."""
+    _lib.check(_lib.load().lsb_render_blend_bwd(
+        ctypes.byref(state.c_set), state._ws(), state.ws_bytes, ctypes.byref(state.dims),
+        ctypes.c_void_p(image.data_ptr()), ctypes.c_void_p(n_contrib.data_ptr()),
+        ctypes.c_void_p(grad_image.data_ptr()), float(grad_scale), _lib.stream_ptr(stream)), "blend_bwd")
+
+
+def render_chain(state: RenderState, grads: "ParamGradients", pose_dev=None, stream=None) -> None:
+    """K5 chain rule; ACCUMULATES into grads (async)."""
+    p = state.arrays.params()
+    g = grads.struct()
+    _lib.check(_lib.load().lsb_render_chain(
+        ctypes.byref(p), ctypes.byref(state.c_cam), ctypes.byref(state.c_pose), ctypes.byref(state.c_set),
+        state._ws(), state.ws_bytes, ctypes.byref(state.dims), ctypes.byref(g),
+        ctypes.c_void_p(pose_dev.data_ptr()) if pose_dev is not None else None, _lib.stream_ptr(stream)),
+        "chain")
 
 
 def render_bwd(state: RenderState, out: "RenderOutput", grad_image: torch.Tensor, grad_scale: float,

@@ -94,3 +94,31 @@ def test_tile_lists_reproduce_reference_csr(case):
         inside = lst[(bb[lst, 0] <= x) & (x < bb[lst, 1]) & (bb[lst, 2] <= y) & (y < bb[lst, 3])]
         ref = d["entry_splat"][d["offsets"][p]:d["offsets"][p + 1]]
         assert np.array_equal(inside, ref)
+
+
+def test_adam_update_matches_reference():
+    from oracle.optim import Adam
+    d = load("adam")
+    a = Adam({"x": (50, 3)})
+    for g, ref in zip(d["grads"], d["steps"]):
+        a.step += 1
+        assert np.array_equal(a.update("x", g, 1e-3), ref)
+
+
+def test_optimize_window_matches_reference():
+    from types import SimpleNamespace
+    from oracle.optim import optimize_views
+    d = load("optimize_plane")
+    n = len(d["in_means"])
+    P = {"means": d["in_means"].astype(float), "rots": d["in_rots"].astype(float).reshape(n, 3, 3),
+         "scales": d["in_scales"].astype(float), "opacities": d["in_opacities"].astype(float),
+         "shs": d["in_shs"].astype(float)}
+    fx, fy, cx, cy, w, h = d["cam"]
+    cam = SimpleNamespace(fx=fx, fy=fy, cx=cx, cy=cy, width=int(w), height=int(h))
+    st = SimpleNamespace(near=0.01, dilation=0.3, alpha_clamp=0.99, transmittance_min=1e-4, footprint_sigma=6.0,
+                         alpha_cut=0.0, max_footprint_px=512.0, background=np.zeros(3), sh_degree=0)
+    out, hist = optimize_views(P, [d["observed"]], [(np.eye(3), np.zeros(3))], cam, st, 10)
+    assert np.abs(np.array(hist)[:, 0] - d["loss"]).max() <= 1e-9
+    for k in ("means", "scales", "opacities", "shs"):
+        assert np.abs(out[k].astype(np.float32) - d["out_" + k]).max() <= 1e-6, k
+    assert np.abs(out["rots"].reshape(n, 9).astype(np.float32) - d["out_rots"]).max() <= 1e-6
