@@ -21,17 +21,16 @@ k_loss(const float* __restrict__ rend, const float* __restrict__ obs, const uint
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const bool m = mask ? (mask[i / 3] != 0) : true;
-        const float d = rend[i] - obs[i];
+        const double dd = (double)rend[i] - (double)obs[i];
         float gv = 0.f;
         if (m) {
-            const double dd = (double)d;
             acc1 += dd * dd;
             if (kind == 0) {
                 acc0 += fabs(dd);
-                gv = (d > 0.f) ? gscale : ((d < 0.f) ? -gscale : 0.f);
+                gv = (dd > 0.0) ? gscale : ((dd < 0.0) ? -gscale : 0.f);
             } else {
                 acc0 += dd * dd;
-                gv = 2.f * d * gscale;
+                gv = (float)(2.0 * dd * (double)gscale);
             }
         }
         if (grad) grad[i] = gv;
