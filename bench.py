@@ -176,7 +176,7 @@ def algorithmic_bytes(N, K, M, I, P):
     grd = 4 * (10 + 3 * K)          # one Gaussian's gradient / moment row
     return {
         "bin": N * prm + M * (64 + 8 + 4) + I * (4 + 4 + 4 + 8 + 4 + 4),
-        "blend_fwd": I * (64 + 4) + P * (12 + 4 + 4),
+        "blend_fwd": I * (64 + 4) + P * (12 + 4 + 4 + 12 + 12),   # + fused loss: read observed, write dL/dI
         "blend_bwd": I * (64 + 4 + 4 + 36) + P * (12 + 12 + 4),
         "chain": M * (64 + 4 + prm + 2 * grd) + I * 36,
         "adam": N * (2 * prm + grd + 4 * grd + 1),
@@ -302,7 +302,8 @@ def run_ours(args, wl, rank, world, local_rank):
             "clocks": clk.summary(),
             "e2e": {"value": V * W * H / (e_ms * 1e-3) / 1e6, "unit": "Mpix/s",
                     "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world, "ms_per_step": e_ms},
-            "gpu_launches": args.steps * (len(my_views) * 8 + 1) + 1,
+            "gpu_launches": args.steps * (len(my_views) * 8 + 1) + 1,   # per view: preprocess, scan, scatter,
+            # tile sort, big-tile sort, blend+loss, blend bwd, chain; + adam per step; + final orthonormalize
         }
         if world == 1 and not args.no_cpu_baseline:
             tv, ta, cores = cpu_sample(wl, 2)

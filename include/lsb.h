@@ -160,6 +160,14 @@ int lsb_render_bin(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T
                    void* stream);
 int lsb_render_blend(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
                      float* image, float* t_final, int32_t* n_contrib, float* depth, void* stream);
+/* Blend forward fused with the photometric loss (optimize.py:48-74, no mask):
+ * also writes grad_out (H,W,3) = dL/dI * grad_scale from observed (H,W,3) and
+ * loss_out[0..1] = [sum |diff| (L1) or diff^2 (L2), sum diff^2] over all
+ * pixels (deterministic: per-tile partials summed in tile order). */
+int lsb_render_blend_loss(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
+                          float* image, float* t_final, int32_t* n_contrib, float* depth,
+                          const float* observed, int kind, float grad_scale, float* grad_out,
+                          double* loss_out, void* stream);
 int lsb_render_blend_bwd(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
                          const float* image, const int32_t* n_contrib, const float* grad_image,
                          float grad_scale, void* stream);
@@ -182,6 +190,77 @@ int lsb_adam_step(const lsb_params* p, const float* grads, float* m, float* v, u
                   const lsb_adam_cfg* cfg, void* stream);
 /* Column Gram-Schmidt of touched rotation rows (optimize.py:91-100,193-194). */
 int lsb_orthonormalize(float* rots, const uint8_t* touched, int64_t n, void* stream);
+
+/* ---- pose rows + IESKF H/b: replaces raster.pose_rows (raster.py:402-508)
+ * and the H^T R^-1 H / H^T R^-1 z products of ieskf_update
+ * (estimator.py:278-280, 314-318) for the visual measurement.
+ * lsb_pose_prepare writes LSB_POSE_CHAIN_FLOATS floats per visible splat
+ * (L_mu, L_sig and the SH view-direction pieces) into `chain` (M rows, M
+ * from lsb_render_counts).  lsb_pose_rows: one warp per selected pixel id
+ * (flat row-major), rows_out (m,6) f64 = d gray(I_hat(u)) / d xi_IMU, using
+ * the 6x6 row-major adjoint A (geometry.imu_camera_adjoint) and R_cw. */
+#define LSB_POSE_CHAIN_FLOATS 48
+int lsb_pose_prepare(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T_cw,
+                     const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
+                     float* chain, void* stream);
+int lsb_pose_rows(const lsb_settings* s, int sh_degree_used, void* ws, size_t ws_bytes,
+                  const lsb_dims* dims, const float* image, const int32_t* n_contrib,
+                  const float* chain, const int32_t* pixel_ids, int64_t m, const double* A,
+                  const double* R_cw, double* rows_out, void* stream);
+/* out (42 doubles): [0..35] sum h h^T / sigma^2 (6x6), [36..41] sum h z / sigma^2,
+ * h = -row (the pose block of H).  Deterministic single-CTA reduction. */
+int lsb_hb_reduce(const double* rows, const double* z, int64_t m, double inv_sigma2, double* out,
+                  void* stream);
+/* Semi-dense candidate mask (estimator.py:241-252): Sobel/8 magnitude of the
+ * grey observed image (nearest border) > grad_thr and t_final < t_max. */
+int lsb_semidense_mask(const float* observed, const float* t_final, int32_t width, int32_t height,
+                       double grad_thr, double t_max, uint8_t* mask_out, void* stream);
+
+/* ---- voxel map: replaces HashOctree's batch operations (voxmap.py:99-251)
+ * Open-addressing table of octree LEAVES (the octree is implied by its leaf
+ * set; parents/roots by floor division).  All arrays are caller-allocated
+ * device memory of `cap` entries (cap a power of two); keys start as
+ * 0xFF..FF, count/sum/outer as 0, gslot as -1, claim as INT32_MAX.
+ * Keys are floor(p / edge) in f64 with true division (voxmap.py:45-65). */
+typedef struct lsb_voxmap {
+    uint64_t* keys;          /* packed (ix, iy, iz), 21 bits each            */
+    uint64_t* count;         /* points accumulated per leaf                 */
+    double* sum;             /* (cap, 3) sum p                              */
+    double* outer;           /* (cap, 6) sum p p^T: xx xy xz yy yz zz       */
+    int32_t* gslot;          /* Gaussian id held by the leaf, -1 if none     */
+    int32_t* claim;          /* try_insert scratch                          */
+    uint64_t* n_used;        /* occupied slots (device counter)             */
+    uint64_t* flags;         /* sticky error flag (table full / key range)  */
+    int64_t cap;
+    double root_len;
+    int32_t max_level;
+    int32_t _pad;
+} lsb_voxmap;
+/* keys_of_points: (n,3) f64 points -> (n,3) int64 floor(p / edge). */
+int lsb_voxmap_keys(const double* pts, int64_t n, double edge, int64_t* keys_out, void* stream);
+/* accumulate_points: create leaves and add (count, sum, outer); slots_out
+ * (n) int64 receives each point's leaf slot (may be NULL). */
+int lsb_voxmap_insert_points(const lsb_voxmap* m, const double* pts, int64_t n, int64_t* slots_out,
+                             void* stream);
+/* try_insert for a batch of Gaussian means with leaf_capacity 1: the lowest
+ * batch index landing in an empty leaf is stored (gslot = first_gid + i) and
+ * gets status 1 (Inserted), the others 0 (Full).  slots (n) int64 scratch. */
+int lsb_voxmap_try_insert(const lsb_voxmap* m, const double* means, int64_t n, int32_t first_gid,
+                          int64_t* slots, int32_t* status_out, void* stream);
+/* get_leaf for (n,3) int64 leaf keys -> slot or -1. */
+int lsb_voxmap_lookup(const lsb_voxmap* m, const int64_t* keys, int64_t n, int64_t* slots_out,
+                      void* stream);
+/* FoV leaves: leaves holding a Gaussian under the root voxels touched by
+ * pts (leaf_keys_under_roots(keys_of_points(pts, root_len, 0))).  rset is a
+ * caller scratch of rcap (power of two) u64; out (out_cap,3) int64 keys,
+ * n_out (device u64) the count (may exceed out_cap: then grow and retry). */
+int lsb_voxmap_fov(const lsb_voxmap* m, const double* pts, int64_t n, uint64_t* rset, int64_t rcap,
+                   int64_t* out, uint64_t* n_out, int64_t out_cap, void* stream);
+/* Occupied leaves -> (keys (k,3) int64, slots (k) int64), k in *n_out. */
+int lsb_voxmap_dump(const lsb_voxmap* m, int64_t* keys, int64_t* slots, uint64_t* n_out,
+                    int64_t out_cap, void* stream);
+/* Re-insert every leaf of `src` into the (larger, empty) table `dst`. */
+int lsb_voxmap_rehash(const lsb_voxmap* src, const lsb_voxmap* dst, void* stream);
 
 /* ---- photometric loss: replaces optimize.photometric_loss (optimize.py:48-74)
  * kind 0 = L1, 1 = L2 over (npx, 3) f32 images; mask (npx) u8 may be NULL.

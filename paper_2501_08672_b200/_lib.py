@@ -74,6 +74,8 @@ SIGNATURES = [
                                   _c.POINTER(Settings), _P, _c.c_size_t, _c.POINTER(Dims), _P]),
     ("lsb_render_blend", _c.c_int, [_c.POINTER(Settings), _P, _c.c_size_t, _c.POINTER(Dims), _P, _P, _P, _P,
                                     _P]),
+    ("lsb_render_blend_loss", _c.c_int, [_c.POINTER(Settings), _P, _c.c_size_t, _c.POINTER(Dims), _P, _P, _P,
+                                         _P, _P, _c.c_int, _c.c_float, _P, _P, _P]),
     ("lsb_render_blend_bwd", _c.c_int, [_c.POINTER(Settings), _P, _c.c_size_t, _c.POINTER(Dims), _P, _P, _P,
                                         _c.c_float, _P]),
     ("lsb_render_chain", _c.c_int, [_c.POINTER(Params), _c.POINTER(Camera), _c.POINTER(Pose),
@@ -81,6 +83,12 @@ SIGNATURES = [
                                     _c.POINTER(Grads), _P, _P]),
     ("lsb_adam_step", _c.c_int, [_c.POINTER(Params), _P, _P, _P, _P, _c.POINTER(AdamCfg), _P]),
     ("lsb_orthonormalize", _c.c_int, [_P, _P, _c.c_int64, _P]),
+    ("lsb_pose_prepare", _c.c_int, [_c.POINTER(Params), _c.POINTER(Camera), _c.POINTER(Pose),
+                                    _c.POINTER(Settings), _P, _c.c_size_t, _c.POINTER(Dims), _P, _P]),
+    ("lsb_pose_rows", _c.c_int, [_c.POINTER(Settings), _c.c_int, _P, _c.c_size_t, _c.POINTER(Dims), _P, _P, _P,
+                                 _P, _c.c_int64, _c.POINTER(_c.c_double), _c.POINTER(_c.c_double), _P, _P]),
+    ("lsb_hb_reduce", _c.c_int, [_P, _P, _c.c_int64, _c.c_double, _P, _P]),
+    ("lsb_semidense_mask", _c.c_int, [_P, _P, _c.c_int32, _c.c_int32, _c.c_double, _c.c_double, _P, _P]),
     ("lsb_loss_scratch_doubles", _c.c_int, []),
     ("lsb_photometric_loss", _c.c_int, [_P, _P, _P, _c.c_int64, _c.c_int64, _c.c_int, _c.c_float,
                                         _P, _P, _P]),

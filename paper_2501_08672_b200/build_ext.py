@@ -16,7 +16,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path
           "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 # per-file extra flags: the preprocess keeps f64 rounding where numpy rounds
 EXTRA = {"preprocess.cu": ["--fmad=false"]}
-SOURCES = ["preprocess.cu", "blend.cu", "chain.cu", "loss.cu", "adam.cu", "api.cu"]
+SOURCES = ["preprocess.cu", "blend.cu", "chain.cu", "loss.cu", "adam.cu", "pose.cu", "voxmap.cu", "api.cu"]
 
 
 def build(verbose: bool = False) -> str:

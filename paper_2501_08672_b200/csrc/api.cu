@@ -9,7 +9,7 @@ namespace lsb {
 cudaError_t launch_preprocess(const lsb_params&, const lsb_camera&, const lsb_pose&, const lsb_settings&,
                               const Ws&, cudaStream_t);
 cudaError_t launch_blend_fwd(const Ws&, const lsb_settings&, int, int, float*, float*, int32_t*, float*,
-                             cudaStream_t);
+                             const float*, int, float, float*, double*, cudaStream_t);
 cudaError_t launch_blend_bwd(const Ws&, const lsb_settings&, int, int, const float*, const int32_t*,
                              const float*, float, cudaStream_t);
 cudaError_t launch_chain(const Ws&, const lsb_params&, const lsb_grads&, const lsb_camera&, const lsb_pose&,
@@ -20,6 +20,22 @@ int loss_scratch_doubles();
 cudaError_t launch_adam(const lsb_params&, const float*, float*, float*, uint8_t*, const lsb_adam_cfg&,
                         cudaStream_t);
 cudaError_t launch_orthonormalize(float*, const uint8_t*, int64_t, cudaStream_t);
+cudaError_t launch_pose_prepare(const Ws&, const lsb_params&, const lsb_camera&, const lsb_pose&,
+                                const lsb_settings&, float*, cudaStream_t);
+cudaError_t launch_pose_rows(const Ws&, const lsb_settings&, int, int, int, const float*, const int32_t*,
+                             const float*, const int32_t*, int64_t, const double*, const double*, double*,
+                             cudaStream_t);
+cudaError_t launch_hb(const double*, const double*, int64_t, double, double*, cudaStream_t);
+cudaError_t launch_semidense(const float*, const float*, int, int, double, double, uint8_t*, cudaStream_t);
+cudaError_t launch_vox_keys(const double*, int64_t, double, int64_t*, cudaStream_t);
+cudaError_t launch_vox_insert(const lsb_voxmap&, const double*, int64_t, int64_t*, cudaStream_t);
+cudaError_t launch_vox_try_insert(const lsb_voxmap&, const double*, int64_t, int32_t, int64_t*, int32_t*,
+                                  cudaStream_t);
+cudaError_t launch_vox_lookup(const lsb_voxmap&, const int64_t*, int64_t, int64_t*, cudaStream_t);
+cudaError_t launch_vox_fov(const lsb_voxmap&, const double*, int64_t, unsigned long long*, int64_t, int64_t*,
+                           unsigned long long*, int64_t, cudaStream_t);
+cudaError_t launch_vox_dump(const lsb_voxmap&, int64_t*, int64_t*, unsigned long long*, int64_t, cudaStream_t);
+cudaError_t launch_vox_rehash(const lsb_voxmap&, const lsb_voxmap&, cudaStream_t);
 }  // namespace lsb
 
 using namespace lsb;
@@ -89,7 +105,8 @@ int lsb_render_fwd(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T
     cudaStream_t st = (cudaStream_t)stream;
     rc = check_cuda(launch_preprocess(*p, *cam, *T, *s, w, st), "preprocess");
     if (rc) return rc;
-    return check_cuda(launch_blend_fwd(w, *s, d->width, d->height, image, t_final, n_contrib, depth, st),
+    return check_cuda(launch_blend_fwd(w, *s, d->width, d->height, image, t_final, n_contrib, depth, nullptr, 0, 0.f, nullptr,
+                                       nullptr, st),
                       "blend_fwd");
 }
 
@@ -192,8 +209,22 @@ int lsb_render_blend(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb
     Ws w;
     int rc = get_ws(ws, ws_bytes, d, &w);
     if (rc) return rc;
-    return check_cuda(launch_blend_fwd(w, *s, d->width, d->height, image, t_final, n_contrib, depth,
-                                       (cudaStream_t)stream), "blend");
+    return check_cuda(launch_blend_fwd(w, *s, d->width, d->height, image, t_final, n_contrib, depth, nullptr, 0,
+                                       0.f, nullptr, nullptr, (cudaStream_t)stream), "blend");
+}
+
+int lsb_render_blend_loss(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* d, float* image,
+                          float* t_final, int32_t* n_contrib, float* depth, const float* observed, int kind,
+                          float grad_scale, float* grad_out, double* loss_out, void* stream) {
+    if (!s || !image || !t_final || !n_contrib || !observed || !grad_out || !loss_out)
+        return fail(LSB_EINVAL, "NULL argument");
+    if (kind != 0 && kind != 1) return fail(LSB_EINVAL, "kind must be 0 (l1) or 1 (l2)");
+    Ws w;
+    int rc = get_ws(ws, ws_bytes, d, &w);
+    if (rc) return rc;
+    return check_cuda(launch_blend_fwd(w, *s, d->width, d->height, image, t_final, n_contrib, depth, observed,
+                                       kind, grad_scale, grad_out, loss_out, (cudaStream_t)stream),
+                      "blend_loss");
 }
 
 int lsb_render_blend_bwd(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* d,
@@ -235,6 +266,105 @@ int lsb_adam_step(const lsb_params* p, const float* grads, float* m, float* v, u
 int lsb_orthonormalize(float* rots, const uint8_t* touched, int64_t n, void* stream) {
     if (n > 0 && (!rots || !touched)) return fail(LSB_EINVAL, "NULL array");
     return check_cuda(launch_orthonormalize(rots, touched, n, (cudaStream_t)stream), "orthonormalize");
+}
+
+int lsb_pose_prepare(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T, const lsb_settings* s,
+                     void* ws, size_t ws_bytes, const lsb_dims* d, float* chain, void* stream) {
+    if (!cam || !T || !s || !chain) return fail(LSB_EINVAL, "NULL argument");
+    Ws w;
+    int rc = get_ws(ws, ws_bytes, d, &w);
+    if (rc) return rc;
+    rc = params_ok(p, d);
+    if (rc) return rc;
+    return check_cuda(launch_pose_prepare(w, *p, *cam, *T, *s, chain, (cudaStream_t)stream), "pose_prepare");
+}
+
+int lsb_pose_rows(const lsb_settings* s, int sh_degree_used, void* ws, size_t ws_bytes, const lsb_dims* d,
+                  const float* image, const int32_t* n_contrib, const float* chain, const int32_t* ids, int64_t m,
+                  const double* A, const double* R_cw, double* rows, void* stream) {
+    if (!s || !A || !R_cw) return fail(LSB_EINVAL, "NULL argument");
+    if (m > 0 && (!image || !n_contrib || !chain || !ids || !rows)) return fail(LSB_EINVAL, "NULL array");
+    Ws w;
+    int rc = get_ws(ws, ws_bytes, d, &w);
+    if (rc) return rc;
+    return check_cuda(launch_pose_rows(w, *s, sh_degree_used, d->width, d->height, image, n_contrib, chain, ids, m,
+                                       A, R_cw, rows, (cudaStream_t)stream), "pose_rows");
+}
+
+int lsb_hb_reduce(const double* rows, const double* z, int64_t m, double inv_sigma2, double* out, void* stream) {
+    if (!out || (m > 0 && (!rows || !z))) return fail(LSB_EINVAL, "NULL argument");
+    return check_cuda(launch_hb(rows, z, m, inv_sigma2, out, (cudaStream_t)stream), "hb_reduce");
+}
+
+int lsb_semidense_mask(const float* obs, const float* tfin, int32_t W, int32_t H, double thr, double tmax,
+                       uint8_t* out, void* stream) {
+    if (!obs || !tfin || !out || W <= 0 || H <= 0) return fail(LSB_EINVAL, "bad argument");
+    return check_cuda(launch_semidense(obs, tfin, W, H, thr, tmax, out, (cudaStream_t)stream), "semidense");
+}
+
+static int vox_ok(const lsb_voxmap* m) {
+    if (!m || !m->keys || !m->count || !m->sum || !m->outer || !m->gslot || !m->claim || !m->n_used || !m->flags)
+        return fail(LSB_EINVAL, "voxmap: NULL array");
+    if (m->cap < 2 || (m->cap & (m->cap - 1))) return fail(LSB_EINVAL, "voxmap: cap must be a power of two");
+    if (!(m->root_len > 0.0)) return fail(LSB_EINVAL, "root_len must be positive");
+    if (m->max_level < 0 || m->max_level > 16) return fail(LSB_EINVAL, "max_level out of range");
+    return LSB_OK;
+}
+
+int lsb_voxmap_keys(const double* pts, int64_t n, double edge, int64_t* out, void* stream) {
+    if (n > 0 && (!pts || !out)) return fail(LSB_EINVAL, "NULL argument");
+    if (!(edge > 0.0)) return fail(LSB_EINVAL, "root voxel length must be positive");
+    return check_cuda(launch_vox_keys(pts, n, edge, out, (cudaStream_t)stream), "voxmap_keys");
+}
+
+int lsb_voxmap_insert_points(const lsb_voxmap* m, const double* pts, int64_t n, int64_t* slots, void* stream) {
+    int rc = vox_ok(m);
+    if (rc) return rc;
+    if (n > 0 && !pts) return fail(LSB_EINVAL, "NULL points");
+    return check_cuda(launch_vox_insert(*m, pts, n, slots, (cudaStream_t)stream), "voxmap_insert");
+}
+
+int lsb_voxmap_try_insert(const lsb_voxmap* m, const double* means, int64_t n, int32_t first_gid, int64_t* slots,
+                          int32_t* status, void* stream) {
+    int rc = vox_ok(m);
+    if (rc) return rc;
+    if (n > 0 && (!means || !slots || !status)) return fail(LSB_EINVAL, "NULL argument");
+    return check_cuda(launch_vox_try_insert(*m, means, n, first_gid, slots, status, (cudaStream_t)stream),
+                      "voxmap_try_insert");
+}
+
+int lsb_voxmap_lookup(const lsb_voxmap* m, const int64_t* keys, int64_t n, int64_t* out, void* stream) {
+    int rc = vox_ok(m);
+    if (rc) return rc;
+    if (n > 0 && (!keys || !out)) return fail(LSB_EINVAL, "NULL argument");
+    return check_cuda(launch_vox_lookup(*m, keys, n, out, (cudaStream_t)stream), "voxmap_lookup");
+}
+
+int lsb_voxmap_fov(const lsb_voxmap* m, const double* pts, int64_t n, uint64_t* rset, int64_t rcap, int64_t* out,
+                   uint64_t* n_out, int64_t out_cap, void* stream) {
+    int rc = vox_ok(m);
+    if (rc) return rc;
+    if (!rset || !n_out || (out_cap > 0 && !out) || (n > 0 && !pts)) return fail(LSB_EINVAL, "NULL argument");
+    if (rcap < 2 || (rcap & (rcap - 1))) return fail(LSB_EINVAL, "rcap must be a power of two");
+    return check_cuda(launch_vox_fov(*m, pts, n, (unsigned long long*)rset, rcap, out, (unsigned long long*)n_out,
+                                     out_cap, (cudaStream_t)stream), "voxmap_fov");
+}
+
+int lsb_voxmap_dump(const lsb_voxmap* m, int64_t* keys, int64_t* slots, uint64_t* n_out, int64_t out_cap,
+                    void* stream) {
+    int rc = vox_ok(m);
+    if (rc) return rc;
+    if (!n_out || (out_cap > 0 && (!keys || !slots))) return fail(LSB_EINVAL, "NULL argument");
+    return check_cuda(launch_vox_dump(*m, keys, slots, (unsigned long long*)n_out, out_cap, (cudaStream_t)stream),
+                      "voxmap_dump");
+}
+
+int lsb_voxmap_rehash(const lsb_voxmap* src, const lsb_voxmap* dst, void* stream) {
+    int rc = vox_ok(src);
+    if (rc) return rc;
+    rc = vox_ok(dst);
+    if (rc) return rc;
+    return check_cuda(launch_vox_rehash(*src, *dst, (cudaStream_t)stream), "voxmap_rehash");
 }
 
 int lsb_photometric_loss(const float* rendered, const float* observed, const uint8_t* mask, int64_t npx,

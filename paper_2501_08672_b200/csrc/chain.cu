@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
         for (int c = 0; c < NUM_PART; ++c) q[c] = 0.0;
         for (int k = 0; k < nt; ++k) {
 #pragma unroll
-            for (int c = 0; c < NUM_PART; ++c) q[c] += (double)w.part[(int64_t)c * w.cap + r.ebase + k];
+            for (int c = 0; c < NUM_PART; ++c) q[c] += (double)w.part[(int64_t)(r.ebase + k) * NUM_PART + c];
         }
         bool nz = false;
 #pragma unroll

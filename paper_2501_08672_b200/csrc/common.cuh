@@ -12,8 +12,8 @@ constexpr int NUM_PART = 9;          // d_color(3), d_opac, d_mean2d(2), d_cov2d
 constexpr int POSE_VALS = 9;         // rho_cam(3), tau_cam(3), d_cam_center(3)
 constexpr int PRE_THREADS = 256;     // preprocess block size
 constexpr int PRE_ITEMS = 1;         // Gaussians per preprocess thread
-constexpr int CHAIN_BLOCKS = 296;    // fixed grid of the chain kernel (2 x 148 SMs)
-constexpr int CHAIN_THREADS = 256;
+constexpr int CHAIN_BLOCKS = 592;    // fixed grid of the chain kernel (4 x 148 SMs)
+constexpr int CHAIN_THREADS = 64;
 constexpr double LOG2E = 1.4426950408889634;
 
 // One visible splat, 64 B, written once by preprocess and read by every tile
@@ -28,7 +28,7 @@ struct __align__(16) Rec {
 static_assert(sizeof(Rec) == 64, "Rec must be 64 bytes");
 
 struct Ws {
-    unsigned long long* ctr;    // [0] M, [1] I, [2] overflow, [3] ticket
+    unsigned long long* ctr;    // [0] M, [1] I, [2] overflow, [3] preprocess ticket, [4] chain ticket, [5] loss ticket, [6] big-tile count
     unsigned long long* scan;   // chained-scan state: 2 words per preprocess block
     Rec* rec;                   // [n] (only the first M are live)
     uint64_t* vkey;             // [n] depth bits of live splats
@@ -41,8 +41,11 @@ struct Ws {
     int32_t* tile_e;            // [cap] intersection index, per-tile depth order
     int32_t* tile_slot;         // [cap] visible slot, per-tile depth order
     int32_t* sort_scratch;      // [cap * 8] fallback sort buffers (tiles > SORT_CAP)
-    float* part;                // [NUM_PART * cap] per-intersection gradient partials
+    float* part;                // [cap * NUM_PART] per-intersection gradient partials (AoS)
     double* pose_part;          // [CHAIN_BLOCKS * POSE_VALS]
+    double* loss_part;          // [ntiles * 2] fused-loss tile partials
+    int32_t* vis_ebase;         // [n + 1] first intersection of each visible slot (exclusive scan)
+    int32_t* big_tiles;         // [ntiles] tiles queued for the shared-memory sort
     int64_t n, cap;
     int32_t ntx, nty, ntiles, nblocks_pre;
 };
@@ -85,6 +88,9 @@ inline size_t carve(const lsb_dims& d, char* base, Ws* w) {
     t.sort_scratch = (int32_t*)take(sizeof(int32_t) * cap * 8);
     t.part = (float*)take(sizeof(float) * NUM_PART * cap);
     t.pose_part = (double*)take(sizeof(double) * CHAIN_BLOCKS * POSE_VALS);
+    t.loss_part = (double*)take(sizeof(double) * 2 * t.ntiles);
+    t.vis_ebase = (int32_t*)take(sizeof(int32_t) * (n + 1));
+    t.big_tiles = (int32_t*)take(sizeof(int32_t) * t.ntiles);
     if (w) *w = t;
     return off;
 }

@@ -1,0 +1,374 @@
+// K6 photometric pose rows and the IESKF H/b reduction (raster.py:402-508,
+// estimator.py:241-323).
+//
+//   k_pose_prepare : per visible splat, the 6x2 / 6x3 maps from screen-space
+//                    gradients to the camera tangent (L_mu, L_sig,
+//                    raster.py:402-447) plus the SH view-direction pieces.
+//   k_pose_rows    : one warp per selected pixel.  The warp walks the pixel's
+//                    tile list 32 entries at a time; lanes test bbox
+//                    membership and evaluate alpha in parallel, a warp scan
+//                    gives each entry its transmittance T_k and prefix colour,
+//                    and each lane applies d(alpha) -> (d mu, d Sigma) -> L to
+//                    its entry.  The 6-vector is warp-reduced and mapped to
+//                    the IMU tangent with the adjoint A (raster.py:501-507).
+//   k_hb_reduce    : A6 = sum h h^T / sigma^2, b6 = sum h z / sigma^2 with
+//                    h = -row (estimator.py:278-280, 314-318), one CTA, fixed
+//                    order (deterministic).
+//   k_semidense    : Sobel/8 gradient magnitude of the observed grey image
+//                    (nearest border) > threshold and coverage T < max
+//                    (estimator.py:241-252).
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace lsb {
+
+constexpr int CHAIN_F = 48;   // floats per splat in the pose-chain buffer
+
+struct PosePrepArgs {
+    lsb_params p;
+    lsb_camera cam;
+    lsb_pose T;
+    int degree;
+    float* out;
+};
+
+__constant__ double c_SH3[16] = {
+    0.28209479177387814, 0.4886025119029199, 1.0925484305920792, -1.0925484305920792,
+    0.31539156525252005, -1.0925484305920792, 0.5462742152960396, -0.5900435899266435,
+    2.890611442640554, -0.4570457994644658, 0.3731763325901154, -0.4570457994644658,
+    1.445305721320277, -0.5900435899266435, 0.0, 0.0};
+
+__device__ void sh_grad3(int degree, double x, double y, double z, int k, double* g) {
+    const double* C = c_SH3;
+    g[0] = g[1] = g[2] = 0.0;
+    const double xx = x * x, yy = y * y, zz = z * z;
+    switch (k) {
+        case 1: g[1] = -C[1]; break;
+        case 2: g[2] = C[1]; break;
+        case 3: g[0] = -C[1]; break;
+        case 4: g[0] = C[2] * y; g[1] = C[2] * x; break;
+        case 5: g[1] = C[3] * z; g[2] = C[3] * y; break;
+        case 6: g[0] = C[4] * (-2.0 * x); g[1] = C[4] * (-2.0 * y); g[2] = C[4] * (4.0 * z); break;
+        case 7: g[0] = C[5] * z; g[2] = C[5] * x; break;
+        case 8: g[0] = C[6] * (2.0 * x); g[1] = C[6] * (-2.0 * y); break;
+        case 9: g[0] = C[7] * 6.0 * x * y; g[1] = C[7] * (3.0 * xx - 3.0 * yy); break;
+        case 10: g[0] = C[8] * y * z; g[1] = C[8] * x * z; g[2] = C[8] * x * y; break;
+        case 11: g[0] = C[9] * (-2.0 * x * y); g[1] = C[9] * (4.0 * zz - xx - 3.0 * yy); g[2] = C[9] * (8.0 * y * z); break;
+        case 12: g[0] = C[10] * (-6.0 * x * z); g[1] = C[10] * (-6.0 * y * z);
+                 g[2] = C[10] * (6.0 * zz - 3.0 * xx - 3.0 * yy); break;
+        case 13: g[0] = C[11] * (4.0 * zz - 3.0 * xx - yy); g[1] = C[11] * (-2.0 * x * y); g[2] = C[11] * (8.0 * x * z); break;
+        case 14: g[0] = C[12] * (2.0 * x * z); g[1] = C[12] * (-2.0 * y * z); g[2] = C[12] * (xx - yy); break;
+        case 15: g[0] = C[13] * (3.0 * xx - 3.0 * yy); g[1] = C[13] * (-6.0 * x * y); break;
+        default: break;
+    }
+}
+
+// Layout of one splat's chain record (floats):
+//   [0..11]  L_mu (6x2 row-major)   [12..29] L_sig (6x3 row-major)
+//   [30..38] Pm[c][d] = d colour_c / d dir_d   [39..41] dir   [42] 1/r
+//   [43] interior bits (as float)
+__global__ void __launch_bounds__(256) k_pose_prepare(Ws w, PosePrepArgs a) {
+    const int64_t M = (int64_t)w.ctr[0];
+    const double* R = a.T.R;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; slot < M; slot += stride) {
+        const int64_t i = w.rec[slot].id;
+        const double px = a.p.means[3 * i], py = a.p.means[3 * i + 1], pz = a.p.means[3 * i + 2];
+        const double x = R[0] * px + R[1] * py + R[2] * pz + a.T.t[0];
+        const double y = R[3] * px + R[4] * py + R[5] * pz + a.T.t[1];
+        const double z = R[6] * px + R[7] * py + R[8] * pz + a.T.t[2];
+        const double fx = a.cam.fx, fy = a.cam.fy;
+        const double J00 = fx / z, J02 = -fx * x / (z * z), J11 = fy / z, J12 = -fy * y / (z * z);
+        double B[9], Wc[9];
+        for (int r3 = 0; r3 < 3; ++r3)
+            for (int c3 = 0; c3 < 3; ++c3) B[3 * r3 + c3] = (double)a.p.rots[9 * i + 3 * r3 + c3] * a.p.scales[3 * i + c3];
+        for (int r3 = 0; r3 < 3; ++r3)
+            for (int c3 = 0; c3 < 3; ++c3)
+                Wc[3 * r3 + c3] = B[3 * r3] * B[3 * c3] + B[3 * r3 + 1] * B[3 * c3 + 1] + B[3 * r3 + 2] * B[3 * c3 + 2];
+        double Mm[6];
+        for (int k = 0; k < 3; ++k) {
+            Mm[k] = J00 * R[k] + J02 * R[6 + k];
+            Mm[3 + k] = J11 * R[3 + k] + J12 * R[6 + k];
+        }
+        double MC[6];   // M W
+        for (int r2 = 0; r2 < 2; ++r2)
+            for (int c3 = 0; c3 < 3; ++c3)
+                MC[3 * r2 + c3] = Mm[3 * r2] * Wc[c3] + Mm[3 * r2 + 1] * Wc[3 + c3] + Mm[3 * r2 + 2] * Wc[6 + c3];
+        float* o = a.out + slot * CHAIN_F;
+        // L_mu: column i = (mu_c x J_i, J_i), J_0 = (J00, 0, J02), J_1 = (0, J11, J12)
+        const double Jr[2][3] = {{J00, 0.0, J02}, {0.0, J11, J12}};
+        for (int c = 0; c < 2; ++c) {
+            const double* j = Jr[c];
+            o[0 * 2 + c] = (float)(y * j[2] - z * j[1]);
+            o[1 * 2 + c] = (float)(z * j[0] - x * j[2]);
+            o[2 * 2 + c] = (float)(x * j[1] - y * j[0]);
+            o[3 * 2 + c] = (float)j[0];
+            o[4 * 2 + c] = (float)j[1];
+            o[5 * 2 + c] = (float)j[2];
+        }
+        // L_sig: basis b in {E00, E01+E10, E11}; dM_b = 2 E_b M W
+        const double gxx = -fx / (z * z), gyy = -fy / (z * z);
+        for (int b = 0; b < 3; ++b) {
+            double dM[6];
+            for (int c3 = 0; c3 < 3; ++c3) {
+                const double r0 = MC[c3], r1 = MC[3 + c3];
+                dM[c3] = 2.0 * (b == 0 ? r0 : (b == 1 ? r1 : 0.0));
+                dM[3 + c3] = 2.0 * (b == 0 ? 0.0 : (b == 1 ? r0 : r1));
+            }
+            double dJ[6];
+            for (int r2 = 0; r2 < 2; ++r2)
+                for (int c3 = 0; c3 < 3; ++c3)
+                    dJ[3 * r2 + c3] = dM[3 * r2] * R[3 * c3] + dM[3 * r2 + 1] * R[3 * c3 + 1] + dM[3 * r2 + 2] * R[3 * c3 + 2];
+            double dW[9];
+            for (int c3 = 0; c3 < 3; ++c3) {
+                dW[c3] = J00 * dM[c3];
+                dW[3 + c3] = J11 * dM[3 + c3];
+                dW[6 + c3] = J02 * dM[c3] + J12 * dM[3 + c3];
+            }
+            const double dmu[3] = {dJ[2] * gxx, dJ[5] * gyy,
+                                   dJ[0] * gxx + dJ[4] * gyy + dJ[2] * (2.0 * fx * x / (z * z * z)) +
+                                       dJ[5] * (2.0 * fy * y / (z * z * z))};
+            double Z[9];
+            for (int r3 = 0; r3 < 3; ++r3)
+                for (int c3 = 0; c3 < 3; ++c3)
+                    Z[3 * r3 + c3] = dW[3 * r3] * R[3 * c3] + dW[3 * r3 + 1] * R[3 * c3 + 1] + dW[3 * r3 + 2] * R[3 * c3 + 2];
+            o[12 + 0 * 3 + b] = (float)(y * dmu[2] - z * dmu[1] + (Z[7] - Z[5]));
+            o[12 + 1 * 3 + b] = (float)(z * dmu[0] - x * dmu[2] + (Z[2] - Z[6]));
+            o[12 + 2 * 3 + b] = (float)(x * dmu[1] - y * dmu[0] + (Z[3] - Z[1]));
+            o[12 + 3 * 3 + b] = (float)dmu[0];
+            o[12 + 4 * 3 + b] = (float)dmu[1];
+            o[12 + 5 * 3 + b] = (float)dmu[2];
+        }
+        // SH view-direction pieces
+        const double* cc3 = a.T.cam_center;
+        const double dvx = px - cc3[0], dvy = py - cc3[1], dvz = pz - cc3[2];
+        const double dn = sqrt(dvx * dvx + dvy * dvy + dvz * dvz);
+        double d0 = 0.0, d1 = 0.0, d2 = 1.0;
+        if (dn > 0.0) {
+            const double inv = fmax(dn, 1e-30);
+            d0 = dvx / inv; d1 = dvy / inv; d2 = dvz / inv;
+        }
+        const int K = a.p.sh_coeffs, kk = (a.degree + 1) * (a.degree + 1);
+        double Pm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+        for (int k = 1; k < kk; ++k) {
+            double g[3];
+            sh_grad3(a.degree, d0, d1, d2, k, g);
+            for (int c = 0; c < 3; ++c) {
+                const double s = a.p.shs[(i * K + k) * 3 + c];
+                Pm[3 * c] += s * g[0]; Pm[3 * c + 1] += s * g[1]; Pm[3 * c + 2] += s * g[2];
+            }
+        }
+        for (int k = 0; k < 9; ++k) o[30 + k] = (float)Pm[k];
+        o[39] = (float)d0; o[40] = (float)d1; o[41] = (float)d2;
+        o[42] = (float)(1.0 / fmax(dn, 1e-30));
+        o[43] = (float)w.colmask[slot];
+        o[44] = o[45] = o[46] = o[47] = 0.f;
+    }
+}
+
+struct RowArgs {
+    int W, H;
+    float clamp, cut;
+    int degree;
+    double A[36];
+    double Rcw[9];
+};
+
+__device__ __forceinline__ float warp_scan_mul_excl(float v, int lane, float& total) {
+    float x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x *= y;
+    }
+    total = __shfl_sync(0xffffffffu, x, 31);
+    const float ex = __shfl_up_sync(0xffffffffu, x, 1);
+    return lane == 0 ? 1.f : ex;
+}
+
+__device__ __forceinline__ float warp_scan_add_incl(float v, int lane, float& total) {
+    float x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    total = __shfl_sync(0xffffffffu, x, 31);
+    return x;
+}
+
+__global__ void __launch_bounds__(128) k_pose_rows(Ws w, RowArgs a, const float* __restrict__ image,
+                                                   const int32_t* __restrict__ n_contrib,
+                                                   const float* __restrict__ chain, const int32_t* __restrict__ ids,
+                                                   int64_t m, double* __restrict__ rows) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (r >= m) return;
+    const int p = ids[r];
+    const int px = p % a.W, py = p / a.W;
+    const int tile = (py / TILE) * w.ntx + px / TILE;
+    const int ox = (px / TILE) * TILE, oy = (py / TILE) * TILE;
+    const float fx = (float)(px - ox), fy = (float)(py - oy);
+    const int start = w.tile_start[tile], end = w.tile_last[tile];
+    int rem = n_contrib[p];
+    const float ir = image[3 * p], ig = image[3 * p + 1], ib = image[3 * p + 2];
+    const float k2 = -2.0f / (float)LOG2E;
+    float Tc = 1.f, Pr = 0.f, Pg = 0.f, Pb = 0.f;
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    for (int base = start; base < end && rem > 0; base += 32) {
+        const int j = base + lane;
+        bool inside = false;
+        int slot = 0;
+        Rec rc;
+        if (j < end) {
+            slot = w.tile_slot[j];
+            rc = w.rec[slot];
+            const int x0 = rc.bbx & 0xffff, x1 = rc.bbx >> 16, y0 = rc.bby & 0xffff, y1 = rc.bby >> 16;
+            inside = px >= x0 && px < x1 && py >= y0 && py < y1;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, inside);
+        const int ord = __popc(bal & ((1u << lane) - 1u));
+        const bool active = inside && ord < rem;
+        rem -= min(__popc(bal), rem);
+        float G = 0.f, al = 0.f, u = 0.f, dy = 0.f;
+        bool contrib = false;
+        if (active) {
+            const float mxl = (float)(rc.mx - (double)ox), myl = (float)(rc.my - (double)oy);
+            dy = fy - myl;
+            u = fmaf(rc.s, dy, fx - mxl);
+            G = ex2_approx(fmaf(rc.A, u * u, rc.E * dy * dy));
+            al = fminf(rc.op * G, a.clamp);
+            contrib = (al >= a.cut) && al != 0.f;
+        }
+        float tot;
+        const float Tk = Tc * warp_scan_mul_excl(contrib ? 1.f - al : 1.f, lane, tot);
+        const float wt = contrib ? al * Tk : 0.f;
+        float sr, sg, sb;
+        const float pr = Pr + warp_scan_add_incl(wt * (active ? rc.c0 : 0.f), lane, sr);
+        const float pg = Pg + warp_scan_add_incl(wt * (active ? rc.c1 : 0.f), lane, sg);
+        const float pb = Pb + warp_scan_add_incl(wt * (active ? rc.c2 : 0.f), lane, sb);
+        Tc *= tot;
+        Pr += sr; Pg += sg; Pb += sb;
+        if (contrib) {
+            const float inv = 1.f / (1.f - al);
+            const float third = 1.f / 3.f;
+            const float da = third * (rc.c0 * Tk - (ir - pr) * inv) + third * (rc.c1 * Tk - (ig - pg) * inv) +
+                             third * (rc.c2 * Tk - (ib - pb) * inv);
+            float emu0 = 0.f, emu1 = 0.f, ec0 = 0.f, ec1 = 0.f, ec2 = 0.f;
+            if (al < a.clamp) {
+                const float gq = rc.op * da * G;
+                const float v0 = (rc.A * k2) * u;
+                const float v1 = fmaf(rc.s, v0, (rc.E * k2) * dy);
+                emu0 = gq * v0; emu1 = gq * v1;
+                ec0 = 0.5f * gq * v0 * v0; ec1 = 0.5f * gq * v0 * v1; ec2 = 0.5f * gq * v1 * v1;
+            }
+            const float* L = chain + (int64_t)slot * CHAIN_F;
+            double c6[6];
+#pragma unroll
+            for (int q = 0; q < 6; ++q)
+                c6[q] = (double)L[2 * q] * emu0 + (double)L[2 * q + 1] * emu1 + (double)L[12 + 3 * q] * ec0 +
+                        (double)L[12 + 3 * q + 1] * ec1 + (double)L[12 + 3 * q + 2] * ec2;
+            if (a.degree >= 1) {
+                const int im = (int)L[43];
+                const double dc[3] = {(im & 1) ? wt / 3.0 : 0.0, (im & 2) ? wt / 3.0 : 0.0, (im & 4) ? wt / 3.0 : 0.0};
+                double dd[3];
+                for (int q = 0; q < 3; ++q) dd[q] = dc[0] * L[30 + q] + dc[1] * L[33 + q] + dc[2] * L[36 + q];
+                const double dot = L[39] * dd[0] + L[40] * dd[1] + L[41] * dd[2];
+                double pt[3];
+                for (int q = 0; q < 3; ++q) pt[q] = (dd[q] - L[39 + q] * dot) * L[42];
+                for (int q = 0; q < 3; ++q)
+                    c6[3 + q] += a.Rcw[3 * q] * pt[0] + a.Rcw[3 * q + 1] * pt[1] + a.Rcw[3 * q + 2] * pt[2];
+            }
+#pragma unroll
+            for (int q = 0; q < 6; ++q) acc[q] += c6[q];
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+    }
+    if (lane < 6) {
+        double v = 0.0;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) v += acc[q] * a.A[6 * q + lane];
+        rows[6 * r + lane] = v;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_hb_reduce(const double* __restrict__ rows, const double* __restrict__ z,
+                                                   int64_t m, double inv_s2, double* __restrict__ out) {
+    // out[0..35] = sum h h^T inv_s2 (6x6), out[36..41] = sum h z inv_s2, h = -row
+    __shared__ double s[256];
+    for (int q = 0; q < 42; ++q) {
+        double v = 0.0;
+        for (int64_t r = threadIdx.x; r < m; r += blockDim.x) {
+            const double* row = rows + 6 * r;
+            v += (q < 36) ? row[q / 6] * row[q % 6] : -row[q - 36] * z[r];
+        }
+        s[threadIdx.x] = v;
+        __syncthreads();
+        for (int o = 128; o > 0; o >>= 1) {
+            if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) out[q] = s[0] * inv_s2;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(256) k_semidense(const float* __restrict__ obs, const float* __restrict__ tfin,
+                                                   int W, int H, double thr, double tmax, uint8_t* __restrict__ out) {
+    const int64_t n = (int64_t)W * H;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(p % W), y = (int)(p / W);
+        double g[3][3];
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int xx = min(max(x + dx, 0), W - 1), yy = min(max(y + dy, 0), H - 1);
+                const float* q = obs + 3 * ((int64_t)yy * W + xx);
+                g[dy + 1][dx + 1] = ((double)q[0] + (double)q[1] + (double)q[2]) / 3.0;
+            }
+        // ndimage.sobel(axis=1): d/dx [-1,0,1], smoothed [1,2,1] along y; axis=0 the transpose
+        const double gx = ((g[0][2] - g[0][0]) + 2.0 * (g[1][2] - g[1][0]) + (g[2][2] - g[2][0])) / 8.0;
+        const double gy = ((g[2][0] - g[0][0]) + 2.0 * (g[2][1] - g[0][1]) + (g[2][2] - g[0][2])) / 8.0;
+        out[p] = (hypot(gx, gy) > thr && (double)tfin[p] < tmax) ? 1 : 0;
+    }
+}
+
+cudaError_t launch_pose_prepare(const Ws& w, const lsb_params& p, const lsb_camera& cam, const lsb_pose& T,
+                                const lsb_settings& s, float* out, cudaStream_t st) {
+    PosePrepArgs a{p, cam, T, 0, out};
+    int deg_store = 0;
+    while ((deg_store + 2) * (deg_store + 2) <= p.sh_coeffs) ++deg_store;
+    a.degree = s.sh_degree < deg_store ? s.sh_degree : deg_store;
+    k_pose_prepare<<<2 * 148, 256, 0, st>>>(w, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pose_rows(const Ws& w, const lsb_settings& s, int degree, int W, int H, const float* image,
+                             const int32_t* n_contrib, const float* chain, const int32_t* ids, int64_t m,
+                             const double* A, const double* Rcw, double* rows, cudaStream_t st) {
+    RowArgs a;
+    a.W = W; a.H = H; a.clamp = (float)s.alpha_clamp; a.cut = (float)s.alpha_cut; a.degree = degree;
+    for (int k = 0; k < 36; ++k) a.A[k] = A[k];
+    for (int k = 0; k < 9; ++k) a.Rcw[k] = Rcw[k];
+    if (m == 0) return cudaSuccess;
+    const int64_t threads = m * 32;
+    k_pose_rows<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(w, a, image, n_contrib, chain, ids, m, rows);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hb(const double* rows, const double* z, int64_t m, double inv_s2, double* out, cudaStream_t st) {
+    k_hb_reduce<<<1, 256, 0, st>>>(rows, z, m, inv_s2, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_semidense(const float* obs, const float* tfin, int W, int H, double thr, double tmax,
+                             uint8_t* out, cudaStream_t st) {
+    k_semidense<<<4 * 148, 256, 0, st>>>(obs, tfin, W, H, thr, tmax, out);
+    return cudaGetLastError();
+}
+
+}  // namespace lsb

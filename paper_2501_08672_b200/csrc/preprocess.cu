@@ -156,7 +156,9 @@ __device__ bool splat_one(const PreArgs& a, int64_t i, Rec& r, int& ntiles, uint
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         double acc = b[0] * (double)shp[c];
-        for (int k = 1; k < kk; ++k) acc += b[k] * (double)shp[3 * k + c];
+#pragma unroll
+        for (int k = 1; k < 16; ++k)
+            if (k < kk) acc += b[k] * (double)shp[3 * k + c];
         const double raw = 0.5 + acc;
         col[c] = (float)fmin(fmax(raw, 0.0), 1.0);
         if (raw > 0.0 && raw < 1.0) cmask |= 1u << c;
@@ -250,6 +252,7 @@ k_preprocess(PreArgs a, Ws w) {
         if (blk == w.nblocks_pre - 1) {
             w.ctr[0] = s_base_v + totv;
             w.ctr[1] = s_base_t + tott;
+            w.vis_ebase[s_base_v + totv] = (int32_t)min(s_base_t + tott, 0x7fffffffull);
             if (s_base_t + tott > (unsigned long long)w.cap) w.ctr[2] = 1;
         }
     }
@@ -260,6 +263,7 @@ k_preprocess(PreArgs a, Ws w) {
     const bool fits = e0 + nt <= w.cap;
     r.ebase = fits ? (int32_t)e0 : -1;
     w.rec[slot] = r;
+    w.vis_ebase[slot] = (int32_t)min(e0, (int64_t)0x7fffffff);
     w.vkey[slot] = key;
     w.colmask[slot] = cm;
     if (!fits) return;
@@ -306,26 +310,32 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(Ws w) {
     if (tid == 0) w.tile_start[w.ntiles] = s_carry;
 }
 
-// Scatter every (tile, splat) intersection into its tile's bucket.  Order
-// inside a bucket is arbitrary here and fixed by k_tile_sort.
+// Scatter every (tile, splat) intersection into its tile's bucket, one thread
+// per intersection e: its splat is found by binary search in the exclusive
+// scan vis_ebase (monotone in slot order), its tile is the k-th tile of the
+// splat's bbox in row-major order.  Order inside a bucket is arbitrary here
+// and fixed by the per-tile sort.
 __global__ void __launch_bounds__(256) k_scatter(Ws w) {
     const int64_t M = (int64_t)w.ctr[0];
+    const int64_t I = min((int64_t)w.ctr[1], w.cap);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; slot < M; slot += stride) {
-        const Rec& r = w.rec[slot];
-        const int e0 = r.ebase;
-        if (e0 < 0) continue;
-        const int tx0 = (r.bbx & 0xffff) >> 4, tx1 = ((r.bbx >> 16) - 1) >> 4;
-        const int ty0 = (r.bby & 0xffff) >> 4, ty1 = ((r.bby >> 16) - 1) >> 4;
-        int e = e0;
-        for (int ty = ty0; ty <= ty1; ++ty) {
-            for (int tx = tx0; tx <= tx1; ++tx, ++e) {
-                const int t = ty * w.ntx + tx;
-                const int j = w.tile_start[t] + atomicAdd(&w.tile_cursor[t], 1);
-                w.tile_e[j] = e;
-                w.emit_slot[e] = (int32_t)slot;
-            }
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < I; e += stride) {
+        int64_t lo = 0, hi = M - 1;          // largest s with vis_ebase[s] <= e
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if ((int64_t)w.vis_ebase[mid] <= e) lo = mid;
+            else hi = mid - 1;
         }
+        const Rec& r = w.rec[lo];
+        if (r.ebase < 0) continue;           // this splat's run overflowed the capacity
+        const int k = (int)(e - r.ebase);
+        const int tx0 = (r.bbx & 0xffff) >> 4, tx1 = ((r.bbx >> 16) - 1) >> 4;
+        const int ty0 = (r.bby & 0xffff) >> 4;
+        const int nx = tx1 - tx0 + 1;
+        const int t = (ty0 + k / nx) * w.ntx + tx0 + k % nx;
+        const int j = w.tile_start[t] + atomicAdd(&w.tile_cursor[t], 1);
+        w.tile_e[j] = (int32_t)e;
+        w.emit_slot[e] = (int32_t)lo;
     }
 }
 
@@ -364,93 +374,190 @@ __device__ void smem_bitonic(uint64_t* k, int* s, int* e, int n) {
     }
 }
 
-// Per-tile depth sort: one CTA per tile.  Keys are (camera depth bits, slot);
-// slot order is id order, so the per-tile list is the reference's global
-// stable depth order restricted to the tile.  Tiles longer than SORT_CAP are
-// sorted as SORT_CAP chunks in shared memory followed by rank-merge passes
-// in global memory.
-__global__ void __launch_bounds__(256) k_tile_sort(Ws w) {
+// Bitonic sort of up to 32*R (depth, slot, e) triples held in registers by
+// one warp: element i lives in lane (i & 31), register (i >> 5).
+template <int R>
+__device__ void warp_bitonic(uint64_t* k, int* s, int* e, int lane) {
+    constexpr int P = 32 * R;
+#pragma unroll
+    for (int kk = 2; kk <= P; kk <<= 1) {
+#pragma unroll
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+                const int jr = j >> 5;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int rp = r ^ jr;
+                    if (rp > r) {
+                        const int i = r * 32 + lane;
+                        const bool up = (i & kk) == 0;
+                        const bool lt = key_less(k[rp], s[rp], k[r], s[r]);
+                        if (lt == up) {
+                            const uint64_t tk = k[r]; k[r] = k[rp]; k[rp] = tk;
+                            const int ts = s[r]; s[r] = s[rp]; s[rp] = ts;
+                            const int te = e[r]; e[r] = e[rp]; e[rp] = te;
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int i = r * 32 + lane;
+                    const uint64_t ok = __shfl_xor_sync(0xffffffffu, k[r], j);
+                    const int os = __shfl_xor_sync(0xffffffffu, s[r], j);
+                    const int oe = __shfl_xor_sync(0xffffffffu, e[r], j);
+                    const bool up = (i & kk) == 0;
+                    const bool lower = (lane & j) == 0;
+                    // lower element keeps the smaller key when ascending
+                    const bool other_less = key_less(ok, os, k[r], s[r]);
+                    const bool take = (lower == up) ? other_less : !other_less;
+                    if (take) { k[r] = ok; s[r] = os; e[r] = oe; }
+                }
+            }
+        }
+    }
+}
+
+template <int R>
+__device__ void warp_sort_tile(const Ws& w, int start, int n, int lane) {
+    uint64_t k[R];
+    int s[R], e[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = r * 32 + lane;
+        if (i < n) {
+            e[r] = w.tile_e[start + i];
+            s[r] = w.emit_slot[e[r]];
+            k[r] = w.vkey[s[r]];
+        } else {
+            k[r] = ~0ull;
+            s[r] = 0x7fffffff;
+            e[r] = -1;
+        }
+    }
+    warp_bitonic<R>(k, s, e, lane);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = r * 32 + lane;
+        if (i < n) {
+            w.tile_e[start + i] = e[r];
+            w.tile_slot[start + i] = s[r];
+        }
+    }
+}
+
+constexpr int WARP_SORT_CAP = 256;
+
+// Per-tile depth sort, one warp per tile (4 tiles per CTA).  Keys are
+// (camera depth bits, slot); slot order is id order, so the per-tile list is
+// the reference's global stable depth order restricted to the tile.  Tiles
+// longer than WARP_SORT_CAP are queued for k_tile_sort_big.
+__global__ void __launch_bounds__(128) k_tile_sort(Ws w) {
+    const int lane = threadIdx.x & 31;
+    const int t = blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (t >= w.ntiles) return;
+    const int start = w.tile_start[t], n = w.tile_start[t + 1] - start;
+    if (n <= 0) return;
+    if (n == 1) {
+        if (lane == 0) w.tile_slot[start] = w.emit_slot[w.tile_e[start]];
+    } else if (n <= 32) {
+        warp_sort_tile<1>(w, start, n, lane);
+    } else if (n <= 64) {
+        warp_sort_tile<2>(w, start, n, lane);
+    } else if (n <= 128) {
+        warp_sort_tile<4>(w, start, n, lane);
+    } else if (n <= WARP_SORT_CAP) {
+        warp_sort_tile<8>(w, start, n, lane);
+    } else if (lane == 0) {
+        const unsigned long long q = atomicAdd(&w.ctr[6], 1ull);
+        w.big_tiles[q] = t;
+    }
+}
+
+// Long tiles: one CTA per queued tile (grid-stride over the queue).  Up to
+// SORT_CAP entries are bitonic-sorted in shared memory; longer lists are
+// sorted as SORT_CAP chunks followed by rank-merge passes in global memory.
+__global__ void __launch_bounds__(256) k_tile_sort_big(Ws w) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* sk = (uint64_t*)smem;
     int* ss = (int*)(sk + SORT_CAP);
     int* se = ss + SORT_CAP;
-    const int t = blockIdx.x;
-    const int start = w.tile_start[t], end = w.tile_start[t + 1];
-    const int n = end - start;
-    if (n <= 0) return;
-    if (n <= SORT_CAP) {
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const int e = w.tile_e[start + i];
-            const int slot = w.emit_slot[e];
-            sk[i] = w.vkey[slot];
-            ss[i] = slot;
-            se[i] = e;
-        }
+    const int nbig = (int)w.ctr[6];
+    for (int q = blockIdx.x; q < nbig; q += gridDim.x) {
+        const int t = w.big_tiles[q];
+        const int start = w.tile_start[t], end = w.tile_start[t + 1];
+        const int n = end - start;
         __syncthreads();
-        if (n > 1) smem_bitonic(sk, ss, se, n);
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            w.tile_e[start + i] = se[i];
-            w.tile_slot[start + i] = ss[i];
-        }
-        return;
-    }
-    // ---- long tile: chunk sort + global rank merges (ping-pong buffers) ----
-    // buffer layout per entry: key (2 ints), slot, e  -> 4 ints
-    int* bufA = w.sort_scratch;
-    int* bufB = w.sort_scratch + 4 * w.cap;
-    for (int c0 = 0; c0 < n; c0 += SORT_CAP) {
-        const int cn = min(SORT_CAP, n - c0);
-        __syncthreads();
-        for (int i = threadIdx.x; i < cn; i += blockDim.x) {
-            const int e = w.tile_e[start + c0 + i];
-            const int slot = w.emit_slot[e];
-            sk[i] = w.vkey[slot];
-            ss[i] = slot;
-            se[i] = e;
-        }
-        __syncthreads();
-        smem_bitonic(sk, ss, se, cn);
-        for (int i = threadIdx.x; i < cn; i += blockDim.x) {
-            int* o = bufA + 4 * (int64_t)(start + c0 + i);
-            *(uint64_t*)o = sk[i];
-            o[2] = ss[i];
-            o[3] = se[i];
-        }
-    }
-    __syncthreads();
-    int* src = bufA;
-    int* dst = bufB;
-    for (int run = SORT_CAP; run < n; run <<= 1) {
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const int r0 = (i / (2 * run)) * (2 * run);
-            const bool inA = (i - r0) < run;
-            const int a0 = r0, a1 = min(r0 + run, n);
-            const int b0 = a1, b1 = min(r0 + 2 * run, n);
-            const int* me = src + 4 * (int64_t)(start + i);
-            const uint64_t mk = *(const uint64_t*)me;
-            const int ms = me[2];
-            // rank of me in the other run (keys are unique)
-            int lo = inA ? b0 : a0, hi = inA ? b1 : a1;
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                const int* o = src + 4 * (int64_t)(start + mid);
-                if (key_less(*(const uint64_t*)o, o[2], mk, ms)) lo = mid + 1;
-                else hi = mid;
+        if (n <= SORT_CAP) {
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                const int e = w.tile_e[start + i];
+                const int slot = w.emit_slot[e];
+                sk[i] = w.vkey[slot];
+                ss[i] = slot;
+                se[i] = e;
             }
-            const int pos = r0 + (inA ? (i - a0) + (lo - b0) : (i - b0) + (lo - a0));
-            int* d = dst + 4 * (int64_t)(start + pos);
-            *(uint64_t*)d = mk;
-            d[2] = ms;
-            d[3] = me[3];
+            __syncthreads();
+            smem_bitonic(sk, ss, se, n);
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                w.tile_e[start + i] = se[i];
+                w.tile_slot[start + i] = ss[i];
+            }
+            continue;
+        }
+        int* bufA = w.sort_scratch;
+        int* bufB = w.sort_scratch + 4 * w.cap;
+        for (int c0 = 0; c0 < n; c0 += SORT_CAP) {
+            const int cn = min(SORT_CAP, n - c0);
+            __syncthreads();
+            for (int i = threadIdx.x; i < cn; i += blockDim.x) {
+                const int e = w.tile_e[start + c0 + i];
+                const int slot = w.emit_slot[e];
+                sk[i] = w.vkey[slot];
+                ss[i] = slot;
+                se[i] = e;
+            }
+            __syncthreads();
+            smem_bitonic(sk, ss, se, cn);
+            for (int i = threadIdx.x; i < cn; i += blockDim.x) {
+                int* o = bufA + 4 * (int64_t)(start + c0 + i);
+                *(uint64_t*)o = sk[i];
+                o[2] = ss[i];
+                o[3] = se[i];
+            }
         }
         __syncthreads();
-        int* tmp = src; src = dst; dst = tmp;
-        __threadfence_block();
-    }
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int* o = src + 4 * (int64_t)(start + i);
-        w.tile_slot[start + i] = o[2];
-        w.tile_e[start + i] = o[3];
+        int* src = bufA;
+        int* dst = bufB;
+        for (int run = SORT_CAP; run < n; run <<= 1) {
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                const int r0 = (i / (2 * run)) * (2 * run);
+                const bool inA = (i - r0) < run;
+                const int a0 = r0, a1 = min(r0 + run, n);
+                const int b0 = a1, b1 = min(r0 + 2 * run, n);
+                const int* me = src + 4 * (int64_t)(start + i);
+                const uint64_t mk = *(const uint64_t*)me;
+                const int ms = me[2];
+                int lo = inA ? b0 : a0, hi = inA ? b1 : a1;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    const int* o = src + 4 * (int64_t)(start + mid);
+                    if (key_less(*(const uint64_t*)o, o[2], mk, ms)) lo = mid + 1;
+                    else hi = mid;
+                }
+                const int pos = r0 + (inA ? (i - a0) + (lo - b0) : (i - b0) + (lo - a0));
+                int* d = dst + 4 * (int64_t)(start + pos);
+                *(uint64_t*)d = mk;
+                d[2] = ms;
+                d[3] = me[3];
+            }
+            __syncthreads();
+            int* tmp = src; src = dst; dst = tmp;
+        }
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const int* o = src + 4 * (int64_t)(start + i);
+            w.tile_slot[start + i] = o[2];
+            w.tile_e[start + i] = o[3];
+        }
     }
 }
 
@@ -466,14 +573,10 @@ cudaError_t launch_preprocess(const lsb_params& p, const lsb_camera& cam, const 
     if (err != cudaSuccess) return err;
     k_preprocess<<<w.nblocks_pre, PRE_THREADS, 0, st>>>(a, w);
     k_scan_tiles<<<1, 1024, 0, st>>>(w);
-    k_scatter<<<4 * 148, 256, 0, st>>>(w);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)tile_sort_smem());
-        attr_set = true;
-    }
-    k_tile_sort<<<w.ntiles, 256, tile_sort_smem(), st>>>(w);
+    k_scatter<<<8 * 148, 256, 0, st>>>(w);
+    k_tile_sort<<<(w.ntiles + 3) / 4, 128, 0, st>>>(w);
+    cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_sort_smem());
+    k_tile_sort_big<<<148, 256, tile_sort_smem(), st>>>(w);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,323 @@
+// K8 voxel map: a GPU open-addressing hash of octree leaves
+// (voxmap.py:21-65, 99-251).
+//
+// The reference keeps a dict of root voxels, each an 8-ary octree down to
+// max_level, with leaf statistics in a flat dict.  An internal node exists
+// iff some leaf below it was created, so the whole octree is determined by
+// its set of leaf keys: the device table stores leaves only, keyed by the
+// packed leaf key (ix, iy, iz at max_level), and parents/roots are derived by
+// arithmetic shifts (floor division, voxmap.py:33-38).  The probe start is
+// the reference's prime-XOR hash (voxmap.py:27-28) passed through a 64-bit
+// finaliser; linear probing; insertion by atomicCAS on the key word.
+//
+// Keys are floor(p / edge) with TRUE division in f64 (voxmap.py:50,64), so
+// the integer keys are bit-exact with the reference.  Leaf statistics
+// (count, sum p, sum p p^T) accumulate with f64 atomics (order-dependent at
+// round-off level only).
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace lsb {
+
+constexpr unsigned long long EMPTY = ~0ull;
+constexpr int KB = 21;                       // bits per packed coordinate
+constexpr long long KOFF = 1ll << (KB - 1);  // signed offset
+constexpr unsigned long long KMASK = (1ull << KB) - 1;
+
+__device__ __forceinline__ unsigned long long pack_key(long long ix, long long iy, long long iz) {
+    return ((unsigned long long)(ix + KOFF) & KMASK) | (((unsigned long long)(iy + KOFF) & KMASK) << KB) |
+           (((unsigned long long)(iz + KOFF) & KMASK) << (2 * KB));
+}
+
+__device__ __forceinline__ void unpack_key(unsigned long long k, long long& ix, long long& iy, long long& iz) {
+    ix = (long long)(k & KMASK) - KOFF;
+    iy = (long long)((k >> KB) & KMASK) - KOFF;
+    iz = (long long)((k >> (2 * KB)) & KMASK) - KOFF;
+}
+
+__device__ __forceinline__ unsigned long long slot_of(long long ix, long long iy, long long iz, int level,
+                                                      unsigned long long mask) {
+    // VoxelKey.__hash__ (voxmap.py:27-28), then a murmur3 finaliser for the low bits
+    unsigned long long h = (unsigned long long)((ix * 73856093ll) ^ (iy * 19349669ll) ^ (iz * 83492791ll) ^ level);
+    h ^= h >> 33;
+    h *= 0xff51afd7ed558ccdull;
+    h ^= h >> 33;
+    h *= 0xc4ceb9fe1a85ec53ull;
+    h ^= h >> 33;
+    return h & mask;
+}
+
+__device__ __forceinline__ bool in_range(long long v) { return v >= -KOFF && v < KOFF; }
+
+// Find or create the slot of a leaf key; -1 if the table is full.
+__device__ long long find_or_insert(const lsb_voxmap& m, long long ix, long long iy, long long iz) {
+    const unsigned long long key = pack_key(ix, iy, iz);
+    const unsigned long long mask = (unsigned long long)m.cap - 1;
+    unsigned long long s = slot_of(ix, iy, iz, m.max_level, mask);
+    for (long long probe = 0; probe < m.cap; ++probe) {
+        const unsigned long long cur = (unsigned long long)m.keys[s];
+        if (cur == key) return (long long)s;
+        if (cur == EMPTY) {
+            const unsigned long long prev = atomicCAS((unsigned long long*)&m.keys[s], EMPTY, key);
+            if (prev == EMPTY) {
+                atomicAdd((unsigned long long*)m.n_used, 1ull);
+                return (long long)s;
+            }
+            if (prev == key) return (long long)s;
+        }
+        s = (s + 1) & mask;
+    }
+    return -1;
+}
+
+__device__ long long find(const lsb_voxmap& m, long long ix, long long iy, long long iz) {
+    const unsigned long long key = pack_key(ix, iy, iz);
+    const unsigned long long mask = (unsigned long long)m.cap - 1;
+    unsigned long long s = slot_of(ix, iy, iz, m.max_level, mask);
+    for (long long probe = 0; probe < m.cap; ++probe) {
+        const unsigned long long cur = (unsigned long long)m.keys[s];
+        if (cur == key) return (long long)s;
+        if (cur == EMPTY) return -1;
+        s = (s + 1) & mask;
+    }
+    return -1;
+}
+
+__device__ __forceinline__ void floor_key(const double* p, double edge, long long* k) {
+    k[0] = (long long)floor(p[0] / edge);
+    k[1] = (long long)floor(p[1] / edge);
+    k[2] = (long long)floor(p[2] / edge);
+}
+
+// keys_of_points (voxmap.py:59-65): floor(p / edge), true division.
+__global__ void k_keys(const double* __restrict__ pts, int64_t n, double edge, int64_t* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        long long k[3];
+        floor_key(pts + 3 * i, edge, k);
+        out[3 * i] = k[0];
+        out[3 * i + 1] = k[1];
+        out[3 * i + 2] = k[2];
+    }
+}
+
+// accumulate_points / group_by_leaf + ensure_leaf + add_leaf_stats
+// (voxmap.py:184-230): one thread per point.
+__global__ void k_insert_points(lsb_voxmap m, const double* __restrict__ pts, int64_t n, int64_t* __restrict__ slots) {
+    const double edge = m.root_len / (double)(1ll << m.max_level);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double* p = pts + 3 * i;
+        long long k[3];
+        floor_key(p, edge, k);
+        long long s = -1;
+        if (in_range(k[0]) && in_range(k[1]) && in_range(k[2])) s = find_or_insert(m, k[0], k[1], k[2]);
+        if (slots) slots[i] = s;
+        if (s < 0) {
+            atomicExch((unsigned long long*)m.flags, 1ull);   // table full or key out of range
+            continue;
+        }
+        atomicAdd((unsigned long long*)&m.count[s], 1ull);
+        const double x = p[0], y = p[1], z = p[2];
+        atomicAdd(&m.sum[3 * s], x);
+        atomicAdd(&m.sum[3 * s + 1], y);
+        atomicAdd(&m.sum[3 * s + 2], z);
+        double* o = m.outer + 6 * s;     // xx xy xz yy yz zz
+        atomicAdd(&o[0], x * x);
+        atomicAdd(&o[1], x * y);
+        atomicAdd(&o[2], x * z);
+        atomicAdd(&o[3], y * y);
+        atomicAdd(&o[4], y * z);
+        atomicAdd(&o[5], z * z);
+    }
+}
+
+// try_insert with leaf_capacity 1 (voxmap.py:171-182): the first Gaussian of
+// the batch (lowest index) landing in an empty leaf wins, as in the
+// reference's sequential loop.  Pass 1 claims with atomicMin, pass 2 writes.
+__global__ void k_claim(lsb_voxmap m, const double* __restrict__ means, int64_t n, int64_t* __restrict__ slots) {
+    const double edge = m.root_len / (double)(1ll << m.max_level);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        long long k[3];
+        floor_key(means + 3 * i, edge, k);
+        long long s = -1;
+        if (in_range(k[0]) && in_range(k[1]) && in_range(k[2])) s = find_or_insert(m, k[0], k[1], k[2]);
+        slots[i] = s;
+        if (s < 0) {
+            atomicExch((unsigned long long*)m.flags, 1ull);
+            continue;
+        }
+        if (m.gslot[s] < 0) atomicMin(&m.claim[s], (int)i);
+    }
+}
+
+__global__ void k_commit(lsb_voxmap m, const int64_t* __restrict__ slots, int64_t n, int32_t first_gid,
+                         int32_t* __restrict__ status) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const long long s = slots[i];
+        int st = 0;
+        if (s >= 0 && m.gslot[s] < 0 && m.claim[s] == (int)i) st = 1;
+        status[i] = st;
+    }
+}
+
+__global__ void k_commit2(lsb_voxmap m, const int64_t* __restrict__ slots, int64_t n, int32_t first_gid,
+                          const int32_t* __restrict__ status) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const long long s = slots[i];
+        if (status[i]) m.gslot[s] = first_gid + (int32_t)i;
+        if (s >= 0) m.claim[s] = 0x7fffffff;
+    }
+}
+
+// Batched get_leaf (voxmap.py:162-166): slot or -1 per leaf key.
+__global__ void k_lookup(lsb_voxmap m, const int64_t* __restrict__ keys, int64_t n, int64_t* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const long long ix = keys[3 * i], iy = keys[3 * i + 1], iz = keys[3 * i + 2];
+        out[i] = (in_range(ix) && in_range(iy) && in_range(iz)) ? find(m, ix, iy, iz) : -1;
+    }
+}
+
+// FoV: root keys of the scan points go into a small root set (same hashing),
+// then every occupied leaf holding a Gaussian whose root is in the set is
+// emitted (leaf_keys_under_roots, voxmap.py:232-251, over
+// keys_of_points(p, root_len, 0), pipeline.py:190-191).
+__global__ void k_fov_roots(const double* __restrict__ pts, int64_t n, double root_len, unsigned long long* rset,
+                            int64_t rcap) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        long long k[3];
+        floor_key(pts + 3 * i, root_len, k);
+        if (!(in_range(k[0]) && in_range(k[1]) && in_range(k[2]))) continue;
+        // root set: plain find-or-insert without the used counter
+        const unsigned long long key = pack_key(k[0], k[1], k[2]);
+        const unsigned long long mask = (unsigned long long)rcap - 1;
+        unsigned long long s = slot_of(k[0], k[1], k[2], 0, mask);
+        for (long long probe = 0; probe < rcap; ++probe) {
+            const unsigned long long cur = rset[s];
+            if (cur == key) break;
+            if (cur == EMPTY) {
+                const unsigned long long prev = atomicCAS(&rset[s], EMPTY, key);
+                if (prev == EMPTY || prev == key) break;
+            }
+            s = (s + 1) & mask;
+        }
+    }
+}
+
+__global__ void k_fov_leaves(lsb_voxmap m, const unsigned long long* __restrict__ rset, int64_t rcap,
+                             int64_t* __restrict__ out, unsigned long long* __restrict__ n_out, int64_t out_cap) {
+    const int L = m.max_level;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < m.cap; s += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long key = (unsigned long long)m.keys[s];
+        if (key == EMPTY || m.gslot[s] < 0) continue;
+        long long ix, iy, iz;
+        unpack_key(key, ix, iy, iz);
+        const long long rx = ix >> L, ry = iy >> L, rz = iz >> L;   // floor division by 2^L
+        const unsigned long long rkey = pack_key(rx, ry, rz);
+        const unsigned long long mask = (unsigned long long)rcap - 1;
+        unsigned long long q = slot_of(rx, ry, rz, 0, mask);
+        bool hit = false;
+        for (long long probe = 0; probe < rcap; ++probe) {
+            const unsigned long long cur = rset[q];
+            if (cur == rkey) { hit = true; break; }
+            if (cur == EMPTY) break;
+            q = (q + 1) & mask;
+        }
+        if (!hit) continue;
+        const unsigned long long o = atomicAdd(n_out, 1ull);
+        if ((int64_t)o < out_cap) {
+            out[3 * o] = ix;
+            out[3 * o + 1] = iy;
+            out[3 * o + 2] = iz;
+        }
+    }
+}
+
+// Dump occupied leaves (keys, counts, sums, outers, gslot) for export.
+__global__ void k_dump(lsb_voxmap m, int64_t* __restrict__ keys, int64_t* __restrict__ slots,
+                       unsigned long long* __restrict__ n_out, int64_t out_cap) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < m.cap; s += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long key = (unsigned long long)m.keys[s];
+        if (key == EMPTY) continue;
+        const unsigned long long o = atomicAdd(n_out, 1ull);
+        if ((int64_t)o >= out_cap) continue;
+        long long ix, iy, iz;
+        unpack_key(key, ix, iy, iz);
+        keys[3 * o] = ix;
+        keys[3 * o + 1] = iy;
+        keys[3 * o + 2] = iz;
+        slots[o] = s;
+    }
+}
+
+__global__ void k_rehash(lsb_voxmap src, lsb_voxmap dst) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < src.cap; s += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long key = (unsigned long long)src.keys[s];
+        if (key == EMPTY) continue;
+        long long ix, iy, iz;
+        unpack_key(key, ix, iy, iz);
+        const long long d = find_or_insert(dst, ix, iy, iz);
+        if (d < 0) {
+            atomicExch((unsigned long long*)dst.flags, 1ull);
+            continue;
+        }
+        dst.count[d] = src.count[s];
+        for (int k = 0; k < 3; ++k) dst.sum[3 * d + k] = src.sum[3 * s + k];
+        for (int k = 0; k < 6; ++k) dst.outer[6 * d + k] = src.outer[6 * s + k];
+        dst.gslot[d] = src.gslot[s];
+    }
+}
+
+static int grid_for(int64_t n) {
+    const int64_t b = (n + 255) / 256;
+    return (int)(b < 1 ? 1 : (b > 148 * 16 ? 148 * 16 : b));
+}
+
+cudaError_t launch_vox_keys(const double* pts, int64_t n, double edge, int64_t* out, cudaStream_t st) {
+    if (n > 0) k_keys<<<grid_for(n), 256, 0, st>>>(pts, n, edge, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vox_insert(const lsb_voxmap& m, const double* pts, int64_t n, int64_t* slots, cudaStream_t st) {
+    if (n > 0) k_insert_points<<<grid_for(n), 256, 0, st>>>(m, pts, n, slots);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vox_try_insert(const lsb_voxmap& m, const double* means, int64_t n, int32_t first_gid,
+                                  int64_t* slots, int32_t* status, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    k_claim<<<grid_for(n), 256, 0, st>>>(m, means, n, slots);
+    k_commit<<<grid_for(n), 256, 0, st>>>(m, slots, n, first_gid, status);
+    k_commit2<<<grid_for(n), 256, 0, st>>>(m, slots, n, first_gid, status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vox_lookup(const lsb_voxmap& m, const int64_t* keys, int64_t n, int64_t* out, cudaStream_t st) {
+    if (n > 0) k_lookup<<<grid_for(n), 256, 0, st>>>(m, keys, n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vox_fov(const lsb_voxmap& m, const double* pts, int64_t n, unsigned long long* rset, int64_t rcap,
+                           int64_t* out, unsigned long long* n_out, int64_t out_cap, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(rset, 0xff, sizeof(unsigned long long) * rcap, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(n_out, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    if (n > 0) k_fov_roots<<<grid_for(n), 256, 0, st>>>(pts, n, m.root_len, rset, rcap);
+    k_fov_leaves<<<grid_for(m.cap), 256, 0, st>>>(m, rset, rcap, out, n_out, out_cap);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vox_rehash(const lsb_voxmap& src, const lsb_voxmap& dst, cudaStream_t st) {
+    k_rehash<<<grid_for(src.cap), 256, 0, st>>>(src, dst);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vox_dump(const lsb_voxmap& m, int64_t* keys, int64_t* slots, unsigned long long* n_out,
+                            int64_t out_cap, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(n_out, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    k_dump<<<grid_for(m.cap), 256, 0, st>>>(m, keys, slots, n_out, out_cap);
+    return cudaGetLastError();
+}
+
+}  // namespace lsb

@@ -23,7 +23,7 @@ from . import _lib
 from .errors import EmptyMask
 from .geometry import as_se3
 from .raster import (GaussianArrays, ParamGradients, RasterSettings, RenderState, _as_arrays, _f32,
-                     render_bin, render_blend, render_blend_bwd, render_chain)
+                     render_bin, render_blend, render_blend_bwd, render_blend_loss, render_chain)
 
 
 @dataclass
@@ -220,10 +220,9 @@ class WindowEngine:
             st.set_pose(T.R, T.t)
             mark("bin", True); render_bin(st, self.stream); mark("bin", False)
             mark("blend_fwd", True)
-            render_blend(st, self.image, self.t_final, self.n_contrib, stream=self.stream)
+            render_blend_loss(st, self.image, self.t_final, self.n_contrib, observed[v], _KIND[self.cfg.loss],
+                              gscale, self.grad_image, self.loss.ptr(v), stream=self.stream)
             mark("blend_fwd", False)
-            launch_loss(self.image, observed[v], None, self.h * self.w, self.cfg.loss, gscale, self.grad_image,
-                        self.loss.ptr(v), self.stream)
             mark("blend_bwd", True)
             render_blend_bwd(st, self.image, self.n_contrib, self.grad_image, 1.0, self.stream)
             mark("blend_bwd", False)

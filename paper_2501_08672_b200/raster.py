@@ -275,6 +275,17 @@ def render_blend(state: RenderState, image, t_final, n_contrib, depth=None, stre
         _lib.stream_ptr(stream)), "blend")
 
 
+def render_blend_loss(state: RenderState, image, t_final, n_contrib, observed, kind: int, grad_scale: float,
+                      grad_out, loss_ptr, depth=None, stream=None) -> None:
+    """K3 blend forward fused with the photometric loss (async)."""
+    _lib.check(_lib.load().lsb_render_blend_loss(
+        ctypes.byref(state.c_set), state._ws(), state.ws_bytes, ctypes.byref(state.dims),
+        ctypes.c_void_p(image.data_ptr()), ctypes.c_void_p(t_final.data_ptr()),
+        ctypes.c_void_p(n_contrib.data_ptr()), ctypes.c_void_p(depth.data_ptr()) if depth is not None else None,
+        ctypes.c_void_p(observed.data_ptr()), int(kind), float(grad_scale), ctypes.c_void_p(grad_out.data_ptr()),
+        loss_ptr, _lib.stream_ptr(stream)), "blend_loss")
+
+
 def render_blend_bwd(state: RenderState, image, n_contrib, grad_image, grad_scale: float = 1.0,
                      stream=None) -> None:
     """K4 blend backward into the per-intersection partials (async)."""
@@ -354,3 +365,43 @@ def backward(out: RenderOutput, grad_image, T_ic=None):
     pose_dev = torch.zeros(9, dtype=torch.float64, device=dev)
     render_bwd(state, out, g_img, 1.0, grads, pose_dev)
     return grads, PoseGradient(pose_dev, state.R_cw, T_ic)
+
+
+def _degree_used(state: RenderState) -> int:
+    K = int(state.arrays.shs.shape[1])
+    stored = int(round(np.sqrt(K))) - 1
+    return min(int(state.settings.sh_degree), stored)
+
+
+def pose_rows(out: RenderOutput, pixel_ids, T_ic=None, as_numpy: bool = True):
+    """IMU-tangent rows d gray(I_hat(u)) / d xi for selected pixels
+    (raster.py:450-508).  pixel_ids are flat row-major indices; returns
+    (m, 6) f64 with columns (rho, tau) — numpy by default, else a device
+    tensor."""
+    state = out.cache
+    if state is None:
+        raise MissingCache("render() must be called with retain_cache=True")
+    T_ic = SE3.identity() if T_ic is None else T_ic
+    dev = state.ws.device
+    ids = torch.as_tensor(np.asarray(pixel_ids, dtype=np.int32) if not torch.is_tensor(pixel_ids) else pixel_ids)
+    ids = ids.to(device=dev, dtype=torch.int32).contiguous()
+    m = int(ids.numel())
+    rows = torch.zeros((m, 6), dtype=torch.float64, device=dev)
+    if m:
+        M = state.counts[0] if state.counts is not None else state.read_counts()[0]
+        chain = torch.empty((max(M, 1), 48), dtype=torch.float32, device=dev)
+        p = state.arrays.params()
+        lib = _lib.load()
+        _lib.check(lib.lsb_pose_prepare(ctypes.byref(p), ctypes.byref(state.c_cam), ctypes.byref(state.c_pose),
+                                        ctypes.byref(state.c_set), state._ws(), state.ws_bytes,
+                                        ctypes.byref(state.dims), ctypes.c_void_p(chain.data_ptr()),
+                                        _lib.stream_ptr()), "pose_prepare")
+        A = imu_camera_adjoint(state.R_cw, T_ic)
+        Ac = (ctypes.c_double * 36)(*A.ravel().tolist())
+        Rc = (ctypes.c_double * 9)(*state.R_cw.ravel().tolist())
+        _lib.check(lib.lsb_pose_rows(ctypes.byref(state.c_set), _degree_used(state), state._ws(), state.ws_bytes,
+                                     ctypes.byref(state.dims), ctypes.c_void_p(out.image.data_ptr()),
+                                     ctypes.c_void_p(out.contrib_count.data_ptr()), ctypes.c_void_p(chain.data_ptr()),
+                                     ctypes.c_void_p(ids.data_ptr()), m, Ac, Rc, ctypes.c_void_p(rows.data_ptr()),
+                                     _lib.stream_ptr()), "pose_rows")
+    return rows.cpu().numpy() if as_numpy else rows

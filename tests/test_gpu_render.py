@@ -139,3 +139,11 @@ def test_zero_image_gradient_gives_zero_gradients():
     grads, pose = backward(out, np.zeros((32, 32, 3)))
     assert bool((grads.flat == 0).all())
     assert np.all(pose.as_vector() == 0)
+
+
+def test_pose_rows_match_reference(case):
+    from paper_2501_08672_b200.geometry import SE3
+    from paper_2501_08672_b200.raster import pose_rows
+    d, out = case
+    rows = pose_rows(out, d["pix_ids"], T_ic=SE3(d["R_ic"], d["t_ic"]))
+    assert rel(rows, d["pose_rows"]) <= GRAD_TOL, rel(rows, d["pose_rows"])
