@@ -238,10 +238,12 @@ typedef struct lsb_voxmap {
 } lsb_voxmap;
 /* keys_of_points: (n,3) f64 points -> (n,3) int64 floor(p / edge). */
 int lsb_voxmap_keys(const double* pts, int64_t n, double edge, int64_t* keys_out, void* stream);
-/* accumulate_points: create leaves and add (count, sum, outer); slots_out
- * (n) int64 receives each point's leaf slot (may be NULL). */
-int lsb_voxmap_insert_points(const lsb_voxmap* m, const double* pts, int64_t n, int64_t* slots_out,
-                             void* stream);
+/* accumulate_points: create the leaves containing pts and, if accumulate is
+ * non-zero, add (count, sum, outer) (add_leaf_stats); accumulate == 0 is
+ * ensure_leaf / locate_or_subdivide.  slots_out (n) int64 receives each
+ * point's leaf slot (may be NULL). */
+int lsb_voxmap_insert_points(const lsb_voxmap* m, const double* pts, int64_t n, int32_t accumulate,
+                             int64_t* slots_out, void* stream);
 /* try_insert for a batch of Gaussian means with leaf_capacity 1: the lowest
  * batch index landing in an empty leaf is stored (gslot = first_gid + i) and
  * gets status 1 (Inserted), the others 0 (Full).  slots (n) int64 scratch. */

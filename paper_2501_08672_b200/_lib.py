@@ -51,6 +51,12 @@ class Dims(_c.Structure):
                 ("sh_coeffs", _c.c_int32), ("tile", _c.c_int32), ("isect_cap", _c.c_int64)]
 
 
+class VoxMap(_c.Structure):
+    _fields_ = [("keys", _P), ("count", _P), ("sum", _P), ("outer", _P), ("gslot", _P), ("claim", _P),
+                ("n_used", _P), ("flags", _P), ("cap", _c.c_int64), ("root_len", _c.c_double),
+                ("max_level", _c.c_int32), ("_pad", _c.c_int32)]
+
+
 class AdamCfg(_c.Structure):
     _fields_ = [(k, _c.c_double) for k in ("lr_mean", "lr_rot", "lr_scale", "lr_opacity", "lr_sh", "beta1",
                                            "beta2", "eps", "scene_scale", "opacity_clip", "scale_floor")] + [
@@ -89,6 +95,13 @@ SIGNATURES = [
                                  _P, _c.c_int64, _c.POINTER(_c.c_double), _c.POINTER(_c.c_double), _P, _P]),
     ("lsb_hb_reduce", _c.c_int, [_P, _P, _c.c_int64, _c.c_double, _P, _P]),
     ("lsb_semidense_mask", _c.c_int, [_P, _P, _c.c_int32, _c.c_int32, _c.c_double, _c.c_double, _P, _P]),
+    ("lsb_voxmap_keys", _c.c_int, [_P, _c.c_int64, _c.c_double, _P, _P]),
+    ("lsb_voxmap_insert_points", _c.c_int, [_c.POINTER(VoxMap), _P, _c.c_int64, _c.c_int32, _P, _P]),
+    ("lsb_voxmap_try_insert", _c.c_int, [_c.POINTER(VoxMap), _P, _c.c_int64, _c.c_int32, _P, _P, _P]),
+    ("lsb_voxmap_lookup", _c.c_int, [_c.POINTER(VoxMap), _P, _c.c_int64, _P, _P]),
+    ("lsb_voxmap_fov", _c.c_int, [_c.POINTER(VoxMap), _P, _c.c_int64, _P, _c.c_int64, _P, _P, _c.c_int64, _P]),
+    ("lsb_voxmap_dump", _c.c_int, [_c.POINTER(VoxMap), _P, _P, _P, _c.c_int64, _P]),
+    ("lsb_voxmap_rehash", _c.c_int, [_c.POINTER(VoxMap), _c.POINTER(VoxMap), _P]),
     ("lsb_loss_scratch_doubles", _c.c_int, []),
     ("lsb_photometric_loss", _c.c_int, [_P, _P, _P, _c.c_int64, _c.c_int64, _c.c_int, _c.c_float,
                                         _P, _P, _P]),

@@ -28,7 +28,7 @@ cudaError_t launch_pose_rows(const Ws&, const lsb_settings&, int, int, int, cons
 cudaError_t launch_hb(const double*, const double*, int64_t, double, double*, cudaStream_t);
 cudaError_t launch_semidense(const float*, const float*, int, int, double, double, uint8_t*, cudaStream_t);
 cudaError_t launch_vox_keys(const double*, int64_t, double, int64_t*, cudaStream_t);
-cudaError_t launch_vox_insert(const lsb_voxmap&, const double*, int64_t, int64_t*, cudaStream_t);
+cudaError_t launch_vox_insert(const lsb_voxmap&, const double*, int64_t, int, int64_t*, cudaStream_t);
 cudaError_t launch_vox_try_insert(const lsb_voxmap&, const double*, int64_t, int32_t, int64_t*, int32_t*,
                                   cudaStream_t);
 cudaError_t launch_vox_lookup(const lsb_voxmap&, const int64_t*, int64_t, int64_t*, cudaStream_t);
@@ -317,11 +317,12 @@ int lsb_voxmap_keys(const double* pts, int64_t n, double edge, int64_t* out, voi
     return check_cuda(launch_vox_keys(pts, n, edge, out, (cudaStream_t)stream), "voxmap_keys");
 }
 
-int lsb_voxmap_insert_points(const lsb_voxmap* m, const double* pts, int64_t n, int64_t* slots, void* stream) {
+int lsb_voxmap_insert_points(const lsb_voxmap* m, const double* pts, int64_t n, int32_t accumulate, int64_t* slots,
+                             void* stream) {
     int rc = vox_ok(m);
     if (rc) return rc;
     if (n > 0 && !pts) return fail(LSB_EINVAL, "NULL points");
-    return check_cuda(launch_vox_insert(*m, pts, n, slots, (cudaStream_t)stream), "voxmap_insert");
+    return check_cuda(launch_vox_insert(*m, pts, n, accumulate, slots, (cudaStream_t)stream), "voxmap_insert");
 }
 
 int lsb_voxmap_try_insert(const lsb_voxmap* m, const double* means, int64_t n, int32_t first_gid, int64_t* slots,

@@ -103,7 +103,8 @@ __global__ void k_keys(const double* __restrict__ pts, int64_t n, double edge, i
 
 // accumulate_points / group_by_leaf + ensure_leaf + add_leaf_stats
 // (voxmap.py:184-230): one thread per point.
-__global__ void k_insert_points(lsb_voxmap m, const double* __restrict__ pts, int64_t n, int64_t* __restrict__ slots) {
+__global__ void k_insert_points(lsb_voxmap m, const double* __restrict__ pts, int64_t n, int accumulate,
+                                int64_t* __restrict__ slots) {
     const double edge = m.root_len / (double)(1ll << m.max_level);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const double* p = pts + 3 * i;
@@ -116,6 +117,7 @@ __global__ void k_insert_points(lsb_voxmap m, const double* __restrict__ pts, in
             atomicExch((unsigned long long*)m.flags, 1ull);   // table full or key out of range
             continue;
         }
+        if (!accumulate) continue;
         atomicAdd((unsigned long long*)&m.count[s], 1ull);
         const double x = p[0], y = p[1], z = p[2];
         atomicAdd(&m.sum[3 * s], x);
@@ -277,8 +279,9 @@ cudaError_t launch_vox_keys(const double* pts, int64_t n, double edge, int64_t* 
     return cudaGetLastError();
 }
 
-cudaError_t launch_vox_insert(const lsb_voxmap& m, const double* pts, int64_t n, int64_t* slots, cudaStream_t st) {
-    if (n > 0) k_insert_points<<<grid_for(n), 256, 0, st>>>(m, pts, n, slots);
+cudaError_t launch_vox_insert(const lsb_voxmap& m, const double* pts, int64_t n, int accumulate, int64_t* slots,
+                              cudaStream_t st) {
+    if (n > 0) k_insert_points<<<grid_for(n), 256, 0, st>>>(m, pts, n, accumulate, slots);
     return cudaGetLastError();
 }
 

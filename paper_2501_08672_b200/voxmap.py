@@ -1,0 +1,314 @@
+"""Hash-indexed octree voxel map on the B200 — drop-in for livsplat.voxmap's
+batch operations (voxmap.py:21-65, 99-251).
+
+The device table (csrc/voxmap.cu) holds octree LEAVES keyed by their packed
+integer key; internal nodes and roots are implied (a node exists iff a leaf
+below it exists), so `_walk_create` becomes a single hash insert and
+`leaf_keys_under_roots` a table scan against a root set.  Keys are computed
+on the device as floor(p / edge) with f64 true division — bit-exact with the
+reference.  Leaf statistics (count, sum p, sum p p^T) accumulate in f64.
+
+Batch APIs take (n,3) point arrays and return device results; the
+reference-shaped single-item calls (`locate_or_subdivide`, `try_insert`,
+`get_leaf`, `leaf_keys_under_roots`, `iter_leaves`) wrap them.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import NamedTuple, Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import MissingVoxel
+
+_P1, _P2, _P3 = 73856093, 19349669, 83492791
+
+
+class VoxelKey(NamedTuple):
+    """(ix, iy, iz, level) with the reference's prime-XOR hash (voxmap.py:21-38)."""
+
+    ix: int
+    iy: int
+    iz: int
+    level: int
+
+    def __hash__(self):
+        return (self.ix * _P1) ^ (self.iy * _P2) ^ (self.iz * _P3) ^ self.level
+
+    def child(self, bx, by, bz):
+        return VoxelKey(2 * self.ix + bx, 2 * self.iy + by, 2 * self.iz + bz, self.level + 1)
+
+    def parent(self):
+        return VoxelKey(self.ix // 2, self.iy // 2, self.iz // 2, self.level - 1)
+
+    def root(self):
+        s = 1 << self.level
+        return VoxelKey(self.ix // s, self.iy // s, self.iz // s, 0)
+
+
+class Inserted:
+    pass
+
+
+class Full:
+    pass
+
+
+def _dev_f64(points, device):
+    t = torch.as_tensor(np.atleast_2d(np.asarray(points, dtype=np.float64))) if not torch.is_tensor(points) \
+        else points
+    return t.to(device=device, dtype=torch.float64).reshape(-1, 3).contiguous()
+
+
+def keys_of_points_dev(points, edge: float, device=None) -> torch.Tensor:
+    """Device (n,3) int64 floor(p / edge) (voxmap.py:59-65)."""
+    _lib.require()
+    device = device or torch.device("cuda")
+    if edge <= 0:
+        raise ValueError("root voxel length must be positive")
+    pts = _dev_f64(points, device)
+    out = torch.empty((pts.shape[0], 3), dtype=torch.int64, device=device)
+    _lib.check(_lib.load().lsb_voxmap_keys(ctypes.c_void_p(pts.data_ptr()), pts.shape[0], float(edge),
+                                           ctypes.c_void_p(out.data_ptr()), _lib.stream_ptr()), "voxmap_keys")
+    return out
+
+
+def keys_of_points(points, edge: float, level: int) -> list:
+    """List of VoxelKey (voxmap.py:59-65)."""
+    pts = np.atleast_2d(np.asarray(points, dtype=float))
+    if pts.size == 0:
+        return []
+    k = keys_of_points_dev(pts, edge).cpu().numpy()
+    return [VoxelKey(int(a), int(b), int(c), level) for a, b, c in k]
+
+
+def hash_key(p, v_s: float) -> VoxelKey:
+    if v_s <= 0:
+        raise ValueError("root voxel length must be positive")
+    return keys_of_points([p], v_s, 0)[0]
+
+
+def leaf_key(p, v_s: float, max_level: int) -> VoxelKey:
+    return keys_of_points([p], v_s / (1 << max_level), max_level)[0]
+
+
+class HashOctree:
+    """GPU voxel map: open-addressing table of octree leaves (voxmap.py:99-251)."""
+
+    def __init__(self, root_len: float, max_level: int = 2, leaf_capacity: int = 1, capacity: int = 1 << 20,
+                 device=None):
+        if root_len <= 0:
+            raise ValueError("root_len must be positive")
+        if leaf_capacity != 1:
+            raise ValueError("the device map stores one Gaussian per leaf (leaf_capacity == 1)")
+        _lib.require()
+        self.root_len = float(root_len)
+        self.max_level = int(max_level)
+        self.leaf_capacity = 1
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        self._alloc(1 << max(10, int(np.ceil(np.log2(max(capacity, 2))))))
+        self.gaussians: dict = {}        # gaussian id -> Gaussian3D-like payload (host, optional)
+        self._next_gid = 0
+
+    @property
+    def leaf_len(self) -> float:
+        return self.root_len / (1 << self.max_level)
+
+    # ---- device storage -----------------------------------------------------
+    def _alloc(self, cap: int):
+        d = self.device
+        self.cap = cap
+        self.keys = torch.full((cap,), -1, dtype=torch.int64, device=d)       # 0xFF..FF = empty
+        self.count = torch.zeros(cap, dtype=torch.int64, device=d)
+        self.sum = torch.zeros((cap, 3), dtype=torch.float64, device=d)
+        self.outer = torch.zeros((cap, 6), dtype=torch.float64, device=d)
+        self.gslot = torch.full((cap,), -1, dtype=torch.int32, device=d)
+        self.claim = torch.full((cap,), 0x7FFFFFFF, dtype=torch.int32, device=d)
+        self.n_used = torch.zeros(1, dtype=torch.int64, device=d)
+        self.flags = torch.zeros(1, dtype=torch.int64, device=d)
+
+    def struct(self) -> _lib.VoxMap:
+        return _lib.VoxMap(self.keys.data_ptr(), self.count.data_ptr(), self.sum.data_ptr(), self.outer.data_ptr(),
+                           self.gslot.data_ptr(), self.claim.data_ptr(), self.n_used.data_ptr(),
+                           self.flags.data_ptr(), self.cap, self.root_len, self.max_level, 0)
+
+    def _reserve(self, extra: int):
+        """Keep the load factor <= 1/2 (grow + rehash on the device; one sync)."""
+        used = int(self.n_used.item())
+        if used + extra <= self.cap // 2:
+            return
+        old = self.struct()
+        keep = (self.keys, self.count, self.sum, self.outer, self.gslot, self.claim, self.n_used, self.flags)
+        new_cap = self.cap
+        while used + extra > new_cap // 2:
+            new_cap *= 2
+        self._alloc(new_cap)
+        new = self.struct()
+        _lib.check(_lib.load().lsb_voxmap_rehash(ctypes.byref(old), ctypes.byref(new), _lib.stream_ptr()), "rehash")
+        del keep
+
+    def _check_flags(self):
+        if int(self.flags.item()):
+            raise RuntimeError("voxel map: table full or key outside the 21-bit range")
+
+    # ---- batch operations (device) -------------------------------------------
+    def accumulate_points_dev(self, points, accumulate: bool = True) -> torch.Tensor:
+        """Add scan points to their leaves' statistics, creating leaves as
+        needed (voxmap.py:184-190, 204-230); with accumulate=False only the
+        leaves are created (ensure_leaf).  Returns per-point leaf slots."""
+        pts = _dev_f64(points, self.device)
+        n = pts.shape[0]
+        self._reserve(n)
+        slots = torch.empty(n, dtype=torch.int64, device=self.device)
+        m = self.struct()
+        _lib.check(_lib.load().lsb_voxmap_insert_points(ctypes.byref(m), ctypes.c_void_p(pts.data_ptr()), n,
+                                                        int(accumulate), ctypes.c_void_p(slots.data_ptr()),
+                                                        _lib.stream_ptr()),
+                   "voxmap_insert")
+        return slots
+
+    def accumulate_points(self, points_w) -> set:
+        """Reference-shaped: returns the set of touched leaf keys."""
+        slots = self.accumulate_points_dev(points_w)
+        self._check_flags()
+        u = torch.unique(slots)
+        return {self._key_of_slot(k) for k in self._keys_of_slots(u)}
+
+    def try_insert_batch(self, means, first_gid: Optional[int] = None) -> torch.Tensor:
+        """Batched try_insert (voxmap.py:171-182): status 1 Inserted / 0 Full.
+        The lowest batch index wins an empty leaf (the reference's loop order)."""
+        pts = _dev_f64(means, self.device)
+        n = pts.shape[0]
+        self._reserve(n)
+        gid = self._next_gid if first_gid is None else int(first_gid)
+        slots = torch.empty(n, dtype=torch.int64, device=self.device)
+        status = torch.empty(n, dtype=torch.int32, device=self.device)
+        m = self.struct()
+        _lib.check(_lib.load().lsb_voxmap_try_insert(ctypes.byref(m), ctypes.c_void_p(pts.data_ptr()), n, gid,
+                                                     ctypes.c_void_p(slots.data_ptr()),
+                                                     ctypes.c_void_p(status.data_ptr()), _lib.stream_ptr()),
+                   "voxmap_try_insert")
+        self._next_gid = gid + n
+        return status
+
+    def lookup_dev(self, keys) -> torch.Tensor:
+        k = torch.as_tensor(np.asarray(keys, dtype=np.int64)) if not torch.is_tensor(keys) else keys
+        k = k.to(device=self.device, dtype=torch.int64).reshape(-1, 3).contiguous()
+        out = torch.empty(k.shape[0], dtype=torch.int64, device=self.device)
+        m = self.struct()
+        _lib.check(_lib.load().lsb_voxmap_lookup(ctypes.byref(m), ctypes.c_void_p(k.data_ptr()), k.shape[0],
+                                                 ctypes.c_void_p(out.data_ptr()), _lib.stream_ptr()), "lookup")
+        return out
+
+    def fov_leaf_keys_dev(self, points_w) -> torch.Tensor:
+        """(k,3) int64 leaves holding a Gaussian under the root voxels the
+        points touch (pipeline.py:190-191 -> voxmap.py:232-251)."""
+        pts = _dev_f64(points_w, self.device)
+        n = pts.shape[0]
+        rcap = 1 << max(10, int(np.ceil(np.log2(max(2 * n, 2)))))
+        rset = torch.empty(rcap, dtype=torch.int64, device=self.device)
+        n_out = torch.zeros(1, dtype=torch.int64, device=self.device)
+        out_cap = max(1024, int(self.n_used.item()))
+        out = torch.empty((out_cap, 3), dtype=torch.int64, device=self.device)
+        m = self.struct()
+        _lib.check(_lib.load().lsb_voxmap_fov(ctypes.byref(m), ctypes.c_void_p(pts.data_ptr()), n,
+                                              ctypes.c_void_p(rset.data_ptr()), rcap, ctypes.c_void_p(out.data_ptr()),
+                                              ctypes.c_void_p(n_out.data_ptr()), out_cap, _lib.stream_ptr()), "fov")
+        k = int(n_out.item())
+        return out[:k]
+
+    def dump_dev(self):
+        """All occupied leaves: (keys (k,3) int64, slots (k,) int64)."""
+        out_cap = max(1, int(self.n_used.item()))
+        keys = torch.empty((out_cap, 3), dtype=torch.int64, device=self.device)
+        slots = torch.empty(out_cap, dtype=torch.int64, device=self.device)
+        n_out = torch.zeros(1, dtype=torch.int64, device=self.device)
+        m = self.struct()
+        _lib.check(_lib.load().lsb_voxmap_dump(ctypes.byref(m), ctypes.c_void_p(keys.data_ptr()),
+                                               ctypes.c_void_p(slots.data_ptr()), ctypes.c_void_p(n_out.data_ptr()),
+                                               out_cap, _lib.stream_ptr()), "dump")
+        k = min(int(n_out.item()), out_cap)
+        return keys[:k], slots[:k]
+
+    # ---- reference-shaped helpers ------------------------------------------------
+    def _keys_of_slots(self, slots: torch.Tensor) -> np.ndarray:
+        slots = slots[slots >= 0]
+        packed = self.keys[slots].cpu().numpy().astype(np.uint64)
+        mask = np.uint64((1 << 21) - 1)
+        off = 1 << 20
+        ix = (packed & mask).astype(np.int64) - off
+        iy = ((packed >> np.uint64(21)) & mask).astype(np.int64) - off
+        iz = ((packed >> np.uint64(42)) & mask).astype(np.int64) - off
+        return np.stack([ix, iy, iz], axis=1)
+
+    def _key_of_slot(self, k) -> VoxelKey:
+        return VoxelKey(int(k[0]), int(k[1]), int(k[2]), self.max_level)
+
+    def locate_or_subdivide(self, p) -> VoxelKey:
+        """Leaf key containing p, creating it if needed (voxmap.py:156-160)."""
+        self.accumulate_points_dev([p], accumulate=False)
+        return leaf_key(p, self.root_len, self.max_level)
+
+    def ensure_leaf(self, key: VoxelKey):
+        center = (np.array([key.ix, key.iy, key.iz], dtype=float) + 0.5) * self.leaf_len
+        self.accumulate_points_dev([center], accumulate=False)
+        return self.get_leaf(key)
+
+    def try_insert(self, g):
+        status = self.try_insert_batch([np.asarray(g.mean_w, dtype=float)])
+        ok = bool(int(status.item()))
+        if ok:
+            self.gaussians[self._next_gid - 1] = g
+            g.level = self.max_level
+        return Inserted() if ok else Full()
+
+    def get_leaf(self, key: VoxelKey):
+        s = int(self.lookup_dev([[key.ix, key.iy, key.iz]]).item())
+        if s < 0:
+            return None
+        return {"slot": s, "gid": int(self.gslot[s].item()), "count": int(self.count[s].item())}
+
+    def write_back(self, key: VoxelKey, params) -> None:
+        leaf = self.get_leaf(key)
+        if leaf is None:
+            raise MissingVoxel(key)
+        if params and leaf["gid"] >= 0:
+            self.gaussians[leaf["gid"]] = params[0]
+
+    def leaf_stats(self, key: VoxelKey):
+        leaf = self.get_leaf(key)
+        if leaf is None or leaf["count"] == 0:
+            return None
+        s = leaf["slot"]
+        o = self.outer[s].cpu().numpy()
+        outer = np.array([[o[0], o[1], o[2]], [o[1], o[3], o[4]], [o[2], o[4], o[5]]])
+        return [leaf["count"], self.sum[s].cpu().numpy(), outer]
+
+    def fov_root_keys(self, points_w) -> set:
+        return set(keys_of_points(points_w, self.root_len, 0))
+
+    def leaf_keys_under_roots(self, root_keys) -> set:
+        roots = np.array([[k[0], k[1], k[2]] for k in root_keys], dtype=np.float64).reshape(-1, 3)
+        centers = (roots + 0.5) * self.root_len     # floor(center / root_len) == root key
+        keys = self.fov_leaf_keys_dev(centers).cpu().numpy()
+        return {VoxelKey(int(a), int(b), int(c), self.max_level) for a, b, c in keys}
+
+    def iter_leaf_keys(self) -> list:
+        """Leaf keys in the reference's iteration order (voxmap.py:339-353):
+        sorted root tuple, then octant DFS (x bit | y << 1 | z << 2 per level)."""
+        keys, _ = self.dump_dev()
+        k = keys.cpu().numpy()
+        if len(k) == 0:
+            return []
+        L = self.max_level
+        roots = k >> L
+        morton = np.zeros(len(k), dtype=np.int64)
+        for d in range(L):             # level d+1 digit: bit (L-1-d) of each local coordinate
+            b = L - 1 - d
+            digit = ((k[:, 0] >> b) & 1) | (((k[:, 1] >> b) & 1) << 1) | (((k[:, 2] >> b) & 1) << 2)
+            morton = morton * 8 + digit
+        order = np.lexsort((morton, roots[:, 2], roots[:, 1], roots[:, 0]))
+        return [VoxelKey(int(a), int(b), int(c), L) for a, b, c in k[order]]
