@@ -56,3 +56,14 @@ adam_param_step(P2, ref, adam, DEFAULT_CFG, np.zeros(n, bool))
 for k, ak in (("means", "means"), ("rots", "rots"), ("scales", "scales"), ("opacities", "opacities"), ("shs", "shs")):
     got = getattr(arrays, ak).cpu().numpy().reshape(P2[k].shape)
     print("after adam", k, np.abs(got - P2[k]).max(), "moved", np.abs(P2[k] - P[k]).max())
+
+# ---- full optimize_window, per iteration, against the oracle ------------------
+from paper_2501_08672_b200.optimize import optimize_window
+from oracle.optim import optimize_views
+arrays2 = GaussianArrays(P["means"], P["rots"], P["scales"], P["opacities"], P["shs"])
+hist = optimize_window(arrays2, d["observed"], SE3.identity(), cam, OptimConfig(), RasterSettings(), iters=3)
+print("gpu losses", [h.value for h in hist])
+print("ref losses", d["loss"][:3])
+for it in (1, 2, 3):
+    Po, ho = optimize_views(P, [d["observed"]], [(np.eye(3), np.zeros(3))], cam, st, it)
+    print("oracle iters", it, "losses", [x[0] for x in ho])
