@@ -170,16 +170,18 @@ def run_reference(args, wl, rank):
 
 
 # ---------------------------------------------------------------- GPU leg ----
-def algorithmic_bytes(N, K, M, I, P):
-    """Per-launch algorithmic HBM bytes."""
-    prm = 4 * (16 + 3 * K)          # one Gaussian's parameters (f32)
-    grd = 4 * (10 + 3 * K)          # one Gaussian's gradient / moment row
+def algorithmic_bytes(N, K, M, I, P, pbytes=8):
+    """Per-launch algorithmic HBM bytes.  pbytes: bytes per
+    parameter of the working copy (8: the f64 copy optimize_window steps)."""
+    prm = pbytes * (16 + 3 * K)     # one Gaussian's parameters
+    grd = 4 * (10 + 3 * K)          # one Gaussian's gradient row (f32)
+    mom = pbytes * (10 + 3 * K)     # one Gaussian's Adam moment row
     return {
         "bin": N * prm + M * (64 + 8 + 4) + I * (4 + 4 + 4 + 8 + 4 + 4),
         "blend_fwd": I * (64 + 4) + P * (12 + 4 + 4 + 12 + 12),   # + fused loss: read observed, write dL/dI
         "blend_bwd": I * (64 + 4 + 4 + 36) + P * (12 + 12 + 4),
         "chain": M * (64 + 4 + prm + 2 * grd) + I * 36,
-        "adam": N * (2 * prm + grd + 4 * grd + 1),
+        "adam": N * (2 * prm + grd + 4 * mom + 1),
     }
 
 
@@ -245,7 +247,7 @@ def run_ours(args, wl, rank, world, local_rank):
     M_avg = float(np.mean([c[0] for c in counts])) if counts else 0.0
     I_avg = float(np.mean([c[1] for c in counts])) if counts else 0.0
     K = int(win.shs.shape[1])
-    ab = algorithmic_bytes(N, K, M_avg, I_avg, W * H)
+    ab = algorithmic_bytes(N, K, M_avg, I_avg, W * H, pbytes=eng.arrays.means.element_size())
     per_step_ms = {k: float(np.sum(v)) / args.steps for k, v in ktime.items()}
     dom = max(("bin", "blend_fwd", "blend_bwd", "chain"), key=lambda k: per_step_ms.get(k, 0.0))
     dom_ms = float(np.mean(ktime[dom]))

@@ -75,18 +75,20 @@ typedef struct lsb_pose {
     double cam_center[3];
 } lsb_pose;
 
-/* Window parameter arena, f32 structure-of-arrays (window.py:45-60):
+/* Window parameter arena, structure-of-arrays (window.py:45-60):
  * means (n,3), rots (n,9) row-major 3x3, scales (n,3), opacities (n),
- * shs (n,K,3).  Device pointers. */
+ * shs (n,K,3).  Device pointers.  dtype 0: f32 (the window arena's storage
+ * type); dtype 1: f64 (the working copy optimize_window steps,
+ * optimize.py:142-149, written back to f32 at the end). */
 typedef struct lsb_params {
-    const float* means;
-    const float* rots;
-    const float* scales;
-    const float* opacities;
-    const float* shs;
+    const void* means;
+    const void* rots;
+    const void* scales;
+    const void* opacities;
+    const void* shs;
     int64_t n;
     int32_t sh_coeffs;   /* K = (degree+1)^2 stored per Gaussian */
-    int32_t _pad;
+    int32_t dtype;       /* 0 = f32, 1 = f64 */
 } lsb_params;
 
 /* Gradient buffers, same shapes as lsb_params but rot is the (n,3) right
@@ -177,19 +179,21 @@ int lsb_render_chain(const lsb_params* p, const lsb_camera* cam, const lsb_pose*
 
 /* ---- Adam in storage coordinates: replaces AdamState.update + the
  * optimize_window parameter steps (optimize.py:103-119, 159-188).
- * Updates the window arena IN PLACE through p (means, rots, scales,
- * opacities, shs).  grads/m/v are flat f32 buffers laid out
- * [mean 3n | rot 3n | scale 3n | opacity n | sh 3Kn] (the ParamGradients
- * layout); touched (n bytes) records rotation rows that were stepped. */
+ * Updates the parameters IN PLACE through p (means, rots, scales,
+ * opacities, shs; f32 or f64 per p->dtype).  grads is a flat f32 buffer
+ * laid out [mean 3n | rot 3n | scale 3n | opacity n | sh 3Kn] (the
+ * ParamGradients layout); m and v use the same layout in p->dtype;
+ * touched (n bytes) records rotation rows that were stepped. */
 typedef struct lsb_adam_cfg {
     double lr_mean, lr_rot, lr_scale, lr_opacity, lr_sh;
     double beta1, beta2, eps, scene_scale, opacity_clip, scale_floor;
     int64_t step;          /* 1-based shared step count (bias correction) */
 } lsb_adam_cfg;
-int lsb_adam_step(const lsb_params* p, const float* grads, float* m, float* v, uint8_t* touched,
+int lsb_adam_step(const lsb_params* p, const float* grads, void* m, void* v, uint8_t* touched,
                   const lsb_adam_cfg* cfg, void* stream);
-/* Column Gram-Schmidt of touched rotation rows (optimize.py:91-100,193-194). */
-int lsb_orthonormalize(float* rots, const uint8_t* touched, int64_t n, void* stream);
+/* Column Gram-Schmidt of touched rotation rows (optimize.py:91-100,193-194);
+ * rots (n,9) in dtype (0 f32, 1 f64). */
+int lsb_orthonormalize(void* rots, int32_t dtype, const uint8_t* touched, int64_t n, void* stream);
 
 /* ---- pose rows + IESKF H/b: replaces raster.pose_rows (raster.py:402-508)
  * and the H^T R^-1 H / H^T R^-1 z products of ieskf_update

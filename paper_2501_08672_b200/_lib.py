@@ -39,7 +39,7 @@ class Pose(_c.Structure):
 
 class Params(_c.Structure):
     _fields_ = [("means", _P), ("rots", _P), ("scales", _P), ("opacities", _P), ("shs", _P),
-                ("n", _c.c_int64), ("sh_coeffs", _c.c_int32), ("_pad", _c.c_int32)]
+                ("n", _c.c_int64), ("sh_coeffs", _c.c_int32), ("dtype", _c.c_int32)]
 
 
 class Grads(_c.Structure):
@@ -88,7 +88,7 @@ SIGNATURES = [
                                     _c.POINTER(Settings), _P, _c.c_size_t, _c.POINTER(Dims),
                                     _c.POINTER(Grads), _P, _P]),
     ("lsb_adam_step", _c.c_int, [_c.POINTER(Params), _P, _P, _P, _P, _c.POINTER(AdamCfg), _P]),
-    ("lsb_orthonormalize", _c.c_int, [_P, _P, _c.c_int64, _P]),
+    ("lsb_orthonormalize", _c.c_int, [_P, _c.c_int32, _P, _c.c_int64, _P]),
     ("lsb_pose_prepare", _c.c_int, [_c.POINTER(Params), _c.POINTER(Camera), _c.POINTER(Pose),
                                     _c.POINTER(Settings), _P, _c.c_size_t, _c.POINTER(Dims), _P, _P]),
     ("lsb_pose_rows", _c.c_int, [_c.POINTER(Settings), _c.c_int, _P, _c.c_size_t, _c.POINTER(Dims), _P, _P, _P,

@@ -1,99 +1,112 @@
 // K7 Adam in storage coordinates (optimize.py:103-119, 159-201), one thread
 // per Gaussian, and the Gram-Schmidt re-orthonormalisation of touched
 // rotations (optimize.py:91-100, 193-194).  HBM-bound: params are updated in
-// place in the f32 window arena, moments are f32, arithmetic is f64.
+// place in the parameter arena's own type (f64 working copy or f32 arena).
 #include <cuda_runtime.h>
 
 #include "common.cuh"
 
 namespace lsb {
 
+template <typename PT>
 struct AdamArgs {
-    float* means;
-    float* rots;
-    float* scales;
-    float* opac;
-    float* shs;
+    PT* means;
+    PT* rots;
+    PT* scales;
+    PT* opac;
+    PT* shs;
     int64_t n;
     int K;
     const float* g;     // flat gradient [mean 3n | rot 3n | scale 3n | opac n | sh 3Kn]
-    float* m;           // flat first moments, same layout
-    float* v;           // flat second moments
+    PT* m;              // flat first moments, same layout
+    PT* v;              // flat second moments
     uint8_t* touched;   // rotation rows stepped at least once
     lsb_adam_cfg c;
-    double bc1, bc2;    // 1 - beta^t
+    PT ibc1, ibc2;      // 1 / (1 - beta^t)
 };
 
-__device__ __forceinline__ double adam_upd(const AdamArgs& a, int64_t idx, double g, double lr) {
-    const double m = a.c.beta1 * (double)a.m[idx] + (1.0 - a.c.beta1) * g;
-    const double v = a.c.beta2 * (double)a.v[idx] + (1.0 - a.c.beta2) * g * g;
-    a.m[idx] = (float)m;
-    a.v[idx] = (float)v;
-    return -lr * (m / a.bc1) / (sqrt(v / a.bc2) + a.c.eps);
+// AdamState.update (optimize.py:113-119): returns the additive step.
+template <typename PT>
+__device__ __forceinline__ PT adam_upd(const AdamArgs<PT>& a, int64_t idx, PT g, PT lr) {
+    const PT m = (PT)a.c.beta1 * a.m[idx] + (PT)(1.0 - a.c.beta1) * g;
+    const PT v = (PT)a.c.beta2 * a.v[idx] + (PT)(1.0 - a.c.beta2) * g * g;
+    a.m[idx] = m;
+    a.v[idx] = v;
+    return -lr * (m * a.ibc1) / (sqrt(v * a.ibc2) + (PT)a.c.eps);
 }
 
-__global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
+// One thread per Gaussian.  PT = double steps the f64 working copy exactly
+// like the reference (optimize.py:142-188); PT = float steps the f32 arena.
+template <typename PT>
+__global__ void __launch_bounds__(256) k_adam(AdamArgs<PT> a) {
     const int64_t n = a.n;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t o_rot = 3 * n, o_scale = 6 * n, o_op = 9 * n, o_sh = 10 * n;
+    const PT lr_mean = (PT)(a.c.lr_mean * a.c.scene_scale), lr_rot = (PT)a.c.lr_rot;
+    const PT lr_scale = (PT)a.c.lr_scale, lr_op = (PT)a.c.lr_opacity, lr_sh = (PT)a.c.lr_sh;
+    const PT floor_s = (PT)a.c.scale_floor, oclip = (PT)a.c.opacity_clip;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        // means
-        for (int k = 0; k < 3; ++k) {
-            const double st = adam_upd(a, 3 * i + k, a.g[3 * i + k], a.c.lr_mean * a.c.scene_scale);
-            a.means[3 * i + k] = (float)((double)a.means[3 * i + k] + st);
-        }
-        // rotation: R <- R Exp(phi) on rows with phi != 0
-        double phi[3];
-        for (int k = 0; k < 3; ++k) phi[k] = adam_upd(a, o_rot + 3 * i + k, a.g[o_rot + 3 * i + k], a.c.lr_rot);
-        if (phi[0] != 0.0 || phi[1] != 0.0 || phi[2] != 0.0) {
-            const double th = sqrt(phi[0] * phi[0] + phi[1] * phi[1] + phi[2] * phi[2]);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) a.means[3 * i + k] += adam_upd(a, 3 * i + k, (PT)a.g[3 * i + k], lr_mean);
+        // rotation: R <- R Exp(phi) on rows with phi != 0 (optimize.py:172-176)
+        PT phi[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) phi[k] = adam_upd(a, o_rot + 3 * i + k, (PT)a.g[o_rot + 3 * i + k], lr_rot);
+        if (phi[0] != (PT)0 || phi[1] != (PT)0 || phi[2] != (PT)0) {
+            const double p0 = phi[0], p1 = phi[1], p2 = phi[2];
+            const double th = sqrt(p0 * p0 + p1 * p1 + p2 * p2);
             const bool small = th < 1e-8;
             const double ca = small ? 1.0 : sin(th) / th;
             const double cb = small ? 0.5 : (1.0 - cos(th)) / (th * th);
-            const double S[9] = {0.0, -phi[2], phi[1], phi[2], 0.0, -phi[0], -phi[1], phi[0], 0.0};
+            const double S[9] = {0.0, -p2, p1, p2, 0.0, -p0, -p1, p0, 0.0};
             double E[9];
+#pragma unroll
             for (int r = 0; r < 3; ++r)
+#pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     const double s2 = S[3 * r] * S[c] + S[3 * r + 1] * S[3 + c] + S[3 * r + 2] * S[6 + c];
                     E[3 * r + c] = (r == c ? 1.0 : 0.0) + ca * S[3 * r + c] + cb * s2;
                 }
-            float* R = a.rots + 9 * i;
+            PT* R = a.rots + 9 * i;
             double Rd[9];
+#pragma unroll
             for (int k = 0; k < 9; ++k) Rd[k] = R[k];
+#pragma unroll
             for (int r = 0; r < 3; ++r)
+#pragma unroll
                 for (int c = 0; c < 3; ++c)
-                    R[3 * r + c] = (float)(Rd[3 * r] * E[c] + Rd[3 * r + 1] * E[3 + c] + Rd[3 * r + 2] * E[6 + c]);
+                    R[3 * r + c] = (PT)(Rd[3 * r] * E[c] + Rd[3 * r + 1] * E[3 + c] + Rd[3 * r + 2] * E[6 + c]);
             a.touched[i] = 1;
         }
-        // scale in log space; gradient chained by the current scale
+        // scale in log space; gradient chained by the current scale (optimize.py:178-181)
+#pragma unroll
         for (int k = 0; k < 3; ++k) {
-            const double s = a.scales[3 * i + k];
-            const double st = adam_upd(a, o_scale + 3 * i + k, (double)a.g[o_scale + 3 * i + k] * s, a.c.lr_scale);
-            if (st != 0.0)
-                a.scales[3 * i + k] = (float)fmax(exp(log(fmax(s, a.c.scale_floor)) + st), a.c.scale_floor);
+            const PT s = a.scales[3 * i + k];
+            const PT st = adam_upd(a, o_scale + 3 * i + k, (PT)a.g[o_scale + 3 * i + k] * s, lr_scale);
+            if (st != (PT)0) a.scales[3 * i + k] = fmax(exp(log(fmax(s, floor_s)) + st), floor_s);
         }
-        // opacity in logit space
+        // opacity in logit space (optimize.py:183-186)
         {
-            const double op = a.opac[i];
-            const double oc = fmin(fmax(op, a.c.opacity_clip), 1.0 - a.c.opacity_clip);
-            const double st = adam_upd(a, o_op + i, (double)a.g[o_op + i] * oc * (1.0 - oc), a.c.lr_opacity);
-            if (st != 0.0) a.opac[i] = (float)(1.0 / (1.0 + exp(-(log(oc / (1.0 - oc)) + st))));
+            const PT op = a.opac[i];
+            const PT oc = fmin(fmax(op, oclip), (PT)1 - oclip);
+            const PT st = adam_upd(a, o_op + i, (PT)a.g[o_op + i] * oc * ((PT)1 - oc), lr_op);
+            if (st != (PT)0) a.opac[i] = (PT)1 / ((PT)1 + exp(-(log(oc / ((PT)1 - oc)) + st)));
         }
         // SH coefficients
         const int64_t nk = 3 * (int64_t)a.K;
         for (int64_t k = 0; k < nk; ++k) {
             const int64_t idx = nk * i + k;
-            const double st = adam_upd(a, o_sh + idx, a.g[o_sh + idx], a.c.lr_sh);
-            a.shs[idx] = (float)((double)a.shs[idx] + st);
+            a.shs[idx] += adam_upd(a, o_sh + idx, (PT)a.g[o_sh + idx], lr_sh);
         }
     }
 }
 
-__global__ void __launch_bounds__(256) k_orthonormalize(float* rots, const uint8_t* touched, int64_t n) {
+template <typename PT>
+__global__ void __launch_bounds__(256) k_orthonormalize(PT* rots, const uint8_t* touched, int64_t n) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         if (!touched[i]) continue;
-        float* R = rots + 9 * i;
+        PT* R = rots + 9 * i;
         double c0[3] = {R[0], R[3], R[6]}, c1[3] = {R[1], R[4], R[7]};
         const double n0 = sqrt(c0[0] * c0[0] + c0[1] * c0[1] + c0[2] * c0[2]);
         for (int k = 0; k < 3; ++k) c0[k] /= n0;
@@ -104,29 +117,41 @@ __global__ void __launch_bounds__(256) k_orthonormalize(float* rots, const uint8
         const double c2[3] = {c0[1] * c1[2] - c0[2] * c1[1], c0[2] * c1[0] - c0[0] * c1[2],
                               c0[0] * c1[1] - c0[1] * c1[0]};
         for (int r = 0; r < 3; ++r) {
-            R[3 * r] = (float)c0[r];
-            R[3 * r + 1] = (float)c1[r];
-            R[3 * r + 2] = (float)c2[r];
+            R[3 * r] = (PT)c0[r];
+            R[3 * r + 1] = (PT)c1[r];
+            R[3 * r + 2] = (PT)c2[r];
         }
     }
 }
 
-cudaError_t launch_adam(const lsb_params& p, const float* g, float* m, float* v, uint8_t* touched,
-                        const lsb_adam_cfg& c, cudaStream_t st) {
-    AdamArgs a{(float*)p.means, (float*)p.rots, (float*)p.scales, (float*)p.opacities, (float*)p.shs,
-               p.n, p.sh_coeffs, g, m, v, touched, c, 0.0, 0.0};
-    a.bc1 = 1.0 - pow(c.beta1, (double)c.step);
-    a.bc2 = 1.0 - pow(c.beta2, (double)c.step);
-    if (p.n == 0) return cudaSuccess;
-    const int blocks = (int)((p.n + 255) / 256 < 148 * 8 ? (p.n + 255) / 256 : 148 * 8);
-    k_adam<<<blocks, 256, 0, st>>>(a);
+static int grid_of(int64_t n) {
+    const int64_t b = (n + 255) / 256;
+    return (int)(b < 148 * 8 ? b : 148 * 8);
+}
+
+template <typename PT>
+static cudaError_t adam_t(const lsb_params& p, const float* g, void* m, void* v, uint8_t* touched,
+                          const lsb_adam_cfg& c, cudaStream_t st) {
+    AdamArgs<PT> a{(PT*)p.means, (PT*)p.rots, (PT*)p.scales, (PT*)p.opacities, (PT*)p.shs, p.n, p.sh_coeffs,
+                   g, (PT*)m, (PT*)v, touched, c, (PT)0, (PT)0};
+    a.ibc1 = (PT)(1.0 / (1.0 - pow(c.beta1, (double)c.step)));
+    a.ibc2 = (PT)(1.0 / (1.0 - pow(c.beta2, (double)c.step)));
+    k_adam<PT><<<grid_of(p.n), 256, 0, st>>>(a);
     return cudaGetLastError();
 }
 
-cudaError_t launch_orthonormalize(float* rots, const uint8_t* touched, int64_t n, cudaStream_t st) {
+cudaError_t launch_adam(const lsb_params& p, const float* g, void* m, void* v, uint8_t* touched,
+                        const lsb_adam_cfg& c, cudaStream_t st) {
+    if (p.n == 0) return cudaSuccess;
+    return p.dtype ? adam_t<double>(p, g, m, v, touched, c, st) : adam_t<float>(p, g, m, v, touched, c, st);
+}
+
+cudaError_t launch_orthonormalize(void* rots, int dtype, const uint8_t* touched, int64_t n, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    const int blocks = (int)((n + 255) / 256 < 148 * 8 ? (n + 255) / 256 : 148 * 8);
-    k_orthonormalize<<<blocks, 256, 0, st>>>(rots, touched, n);
+    if (dtype)
+        k_orthonormalize<double><<<grid_of(n), 256, 0, st>>>((double*)rots, touched, n);
+    else
+        k_orthonormalize<float><<<grid_of(n), 256, 0, st>>>((float*)rots, touched, n);
     return cudaGetLastError();
 }
 

@@ -17,9 +17,8 @@ cudaError_t launch_chain(const Ws&, const lsb_params&, const lsb_grads&, const l
 cudaError_t launch_loss(const float*, const float*, const uint8_t*, int64_t, int, float, float*, double*,
                         cudaStream_t);
 int loss_scratch_doubles();
-cudaError_t launch_adam(const lsb_params&, const float*, float*, float*, uint8_t*, const lsb_adam_cfg&,
-                        cudaStream_t);
-cudaError_t launch_orthonormalize(float*, const uint8_t*, int64_t, cudaStream_t);
+cudaError_t launch_adam(const lsb_params&, const float*, void*, void*, uint8_t*, const lsb_adam_cfg&, cudaStream_t);
+cudaError_t launch_orthonormalize(void*, int, const uint8_t*, int64_t, cudaStream_t);
 cudaError_t launch_pose_prepare(const Ws&, const lsb_params&, const lsb_camera&, const lsb_pose&,
                                 const lsb_settings&, float*, cudaStream_t);
 cudaError_t launch_pose_rows(const Ws&, const lsb_settings&, int, int, int, const float*, const int32_t*,
@@ -99,6 +98,7 @@ int lsb_render_fwd(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T
     if (p->n > 0 && (!p->means || !p->rots || !p->scales || !p->opacities || !p->shs))
         return fail(LSB_EINVAL, "NULL parameter array");
     if (p->sh_coeffs < 1 || p->sh_coeffs > 16) return fail(LSB_EINVAL, "sh_coeffs must be 1..16");
+    if (p->dtype != 0 && p->dtype != 1) return fail(LSB_EINVAL, "params dtype must be 0 (f32) or 1 (f64)");
     Ws w;
     int rc = get_ws(ws, ws_bytes, d, &w);
     if (rc) return rc;
@@ -188,6 +188,7 @@ static int params_ok(const lsb_params* p, const lsb_dims* d) {
     if (p->n > 0 && (!p->means || !p->rots || !p->scales || !p->opacities || !p->shs))
         return fail(LSB_EINVAL, "NULL parameter array");
     if (p->sh_coeffs < 1 || p->sh_coeffs > 16) return fail(LSB_EINVAL, "sh_coeffs must be 1..16");
+    if (p->dtype != 0 && p->dtype != 1) return fail(LSB_EINVAL, "params dtype must be 0 (f32) or 1 (f64)");
     return LSB_OK;
 }
 
@@ -253,7 +254,7 @@ int lsb_render_chain(const lsb_params* p, const lsb_camera* cam, const lsb_pose*
     return check_cuda(launch_chain(w, *p, *g, *cam, *T, *s, pose_out, (cudaStream_t)stream), "chain");
 }
 
-int lsb_adam_step(const lsb_params* p, const float* grads, float* m, float* v, uint8_t* touched,
+int lsb_adam_step(const lsb_params* p, const float* grads, void* m, void* v, uint8_t* touched,
                   const lsb_adam_cfg* cfg, void* stream) {
     if (!p || !cfg) return fail(LSB_EINVAL, "NULL argument");
     if (p->n > 0 && (!grads || !m || !v || !touched || !p->means || !p->rots || !p->scales || !p->opacities ||
@@ -263,9 +264,10 @@ int lsb_adam_step(const lsb_params* p, const float* grads, float* m, float* v, u
     return check_cuda(launch_adam(*p, grads, m, v, touched, *cfg, (cudaStream_t)stream), "adam");
 }
 
-int lsb_orthonormalize(float* rots, const uint8_t* touched, int64_t n, void* stream) {
+int lsb_orthonormalize(void* rots, int32_t dtype, const uint8_t* touched, int64_t n, void* stream) {
     if (n > 0 && (!rots || !touched)) return fail(LSB_EINVAL, "NULL array");
-    return check_cuda(launch_orthonormalize(rots, touched, n, (cudaStream_t)stream), "orthonormalize");
+    if (dtype != 0 && dtype != 1) return fail(LSB_EINVAL, "dtype must be 0 (f32) or 1 (f64)");
+    return check_cuda(launch_orthonormalize(rots, dtype, touched, n, (cudaStream_t)stream), "orthonormalize");
 }
 
 int lsb_pose_prepare(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T, const lsb_settings* s,

@@ -177,12 +177,10 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
     if (live_tile && lane == 0) {
         L.sums[2 * tile] = l0;
         L.sums[2 * tile + 1] = l1;
+        __threadfence();          // every writer publishes before the ticket
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_final = atomicAdd(L.ticket, 1ull) == gridDim.x - 1;
-    }
+    if (threadIdx.x == 0) s_final = atomicAdd(L.ticket, 1ull) == gridDim.x - 1;
     __syncthreads();
     if (!s_final) return;
     __threadfence();

@@ -75,6 +75,37 @@ __device__ void sh_basis_grad_d(int degree, double x, double y, double z, double
     }
 }
 
+// Per visible splat, the sum of its intersections' partials (one warp per
+// splat, lanes stride over the intersections, fixed-order butterfly).
+__global__ void __launch_bounds__(256) k_part_reduce(Ws w) {
+    const int64_t M = (int64_t)w.ctr[0];
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t slot = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; slot < M; slot += nw) {
+        const Rec& r = w.rec[slot];
+        if (r.ebase < 0) continue;
+        const int nt = ((((r.bbx >> 16) - 1) >> 4) - ((r.bbx & 0xffff) >> 4) + 1) *
+                       ((((r.bby >> 16) - 1) >> 4) - ((r.bby & 0xffff) >> 4) + 1);
+        double q[NUM_PART];
+#pragma unroll
+        for (int c = 0; c < NUM_PART; ++c) q[c] = 0.0;
+        for (int k = lane; k < nt; k += 32) {
+            const float* src = w.part + (int64_t)(r.ebase + k) * NUM_PART;
+#pragma unroll
+            for (int c = 0; c < NUM_PART; ++c) q[c] += (double)src[c];
+        }
+#pragma unroll
+        for (int c = 0; c < NUM_PART; ++c) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) q[c] += __shfl_xor_sync(0xffffffffu, q[c], o);
+        }
+        double v = q[0];
+#pragma unroll
+        for (int c = 1; c < NUM_PART; ++c) v = (lane == c) ? q[c] : v;
+        if (lane < NUM_PART) w.qsum[slot * NUM_PART + lane] = v;
+    }
+}
+
 __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
     __shared__ double s_red[CHAIN_THREADS / 32][POSE_VALS];
     __shared__ bool s_last;
@@ -87,22 +118,18 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
     for (int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; slot < M; slot += stride) {
         const Rec& r = w.rec[slot];
         if (r.ebase < 0) continue;
-        const int nt = ((((r.bbx >> 16) - 1) >> 4) - ((r.bbx & 0xffff) >> 4) + 1) *
-                       ((((r.bby >> 16) - 1) >> 4) - ((r.bby & 0xffff) >> 4) + 1);
         double q[NUM_PART];
 #pragma unroll
-        for (int c = 0; c < NUM_PART; ++c) q[c] = 0.0;
-        for (int k = 0; k < nt; ++k) {
-#pragma unroll
-            for (int c = 0; c < NUM_PART; ++c) q[c] += (double)w.part[(int64_t)(r.ebase + k) * NUM_PART + c];
-        }
+        for (int c = 0; c < NUM_PART; ++c) q[c] = w.qsum[slot * NUM_PART + c];
         bool nz = false;
 #pragma unroll
         for (int c = 0; c < NUM_PART; ++c) nz |= (q[c] != 0.0);
         if (!nz) continue;
         const int64_t i = r.id;
         // ---- recompute the forward geometry in f64 ----
-        const double px = a.p.means[3 * i], py = a.p.means[3 * i + 1], pz = a.p.means[3 * i + 2];
+        const int f64 = a.p.dtype;
+        const double px = pld(a.p.means, 3 * i, f64), py = pld(a.p.means, 3 * i + 1, f64),
+                     pz = pld(a.p.means, 3 * i + 2, f64);
         const double x = R[0] * px + R[1] * py + R[2] * pz + a.T.t[0];
         const double y = R[3] * px + R[4] * py + R[5] * pz + a.T.t[1];
         const double z = R[6] * px + R[7] * py + R[8] * pz + a.T.t[2];
@@ -110,8 +137,8 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
         const double J00 = fx / z, J02 = -fx * x / (z * z);
         const double J11 = fy / z, J12 = -fy * y / (z * z);
         double Rg[9], S[3], B[9], Wc[9];
-        for (int k = 0; k < 9; ++k) Rg[k] = a.p.rots[9 * i + k];
-        for (int k = 0; k < 3; ++k) S[k] = a.p.scales[3 * i + k];
+        for (int k = 0; k < 9; ++k) Rg[k] = pld(a.p.rots, 9 * i + k, f64);
+        for (int k = 0; k < 3; ++k) S[k] = pld(a.p.scales, 3 * i + k, f64);
         for (int r3 = 0; r3 < 3; ++r3)
             for (int c3 = 0; c3 < 3; ++c3) B[3 * r3 + c3] = Rg[3 * r3 + c3] * S[c3];
         for (int r3 = 0; r3 < 3; ++r3)
@@ -196,10 +223,11 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
         if (a.degree >= 1) {
             double gb[16][3];
             sh_basis_grad_d(a.degree, dx_, dy_, dz_, gb);
-            const float* shp = a.p.shs + i * K * 3;
+            const int64_t sho = i * K * 3;
             double dd[3] = {0.0, 0.0, 0.0};
             for (int k = 0; k < kk; ++k) {
-                const double t = dcol[0] * shp[3 * k] + dcol[1] * shp[3 * k + 1] + dcol[2] * shp[3 * k + 2];
+                const double t = dcol[0] * pld(a.p.shs, sho + 3 * k, f64) + dcol[1] * pld(a.p.shs, sho + 3 * k + 1, f64) +
+                                 dcol[2] * pld(a.p.shs, sho + 3 * k + 2, f64);
                 dd[0] += t * gb[k][0]; dd[1] += t * gb[k][1]; dd[2] += t * gb[k][2];
             }
             const double dot = dx_ * dd[0] + dy_ * dd[1] + dz_ * dd[2];
@@ -269,6 +297,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
 cudaError_t launch_chain(const Ws& w, const lsb_params& p, const lsb_grads& g, const lsb_camera& cam,
                          const lsb_pose& T, const lsb_settings& s, double* pose_out,
                          cudaStream_t st) {
+    k_part_reduce<<<4 * 148, 256, 0, st>>>(w);
     ChainArgs a{p, g, cam, T, 0, pose_out};
     int deg_store = 0;
     while ((deg_store + 2) * (deg_store + 2) <= p.sh_coeffs) ++deg_store;

@@ -46,6 +46,7 @@ struct Ws {
     double* loss_part;          // [ntiles * 2] fused-loss tile partials
     int32_t* vis_ebase;         // [n + 1] first intersection of each visible slot (exclusive scan)
     int32_t* big_tiles;         // [ntiles] tiles queued for the shared-memory sort
+    double* qsum;               // [n * NUM_PART] per-splat sums of the intersection partials
     int64_t n, cap;
     int32_t ntx, nty, ntiles, nblocks_pre;
 };
@@ -91,6 +92,7 @@ inline size_t carve(const lsb_dims& d, char* base, Ws* w) {
     t.loss_part = (double*)take(sizeof(double) * 2 * t.ntiles);
     t.vis_ebase = (int32_t*)take(sizeof(int32_t) * (n + 1));
     t.big_tiles = (int32_t*)take(sizeof(int32_t) * t.ntiles);
+    t.qsum = (double*)take(sizeof(double) * NUM_PART * n);
     if (w) *w = t;
     return off;
 }
@@ -99,6 +101,11 @@ inline size_t carve(const lsb_dims& d, char* base, Ws* w) {
 // (counters, chained-scan flags, tile histograms).
 inline size_t zero_prefix_bytes(const Ws& w) {
     return (size_t)((char*)w.tile_start - (char*)w.ctr);
+}
+
+// Parameter load from an f32 or f64 arena (lsb_params.dtype), widened to f64.
+__device__ __forceinline__ double pld(const void* p, int64_t i, int f64) {
+    return f64 ? __ldg((const double*)p + i) : (double)__ldg((const float*)p + i);
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {

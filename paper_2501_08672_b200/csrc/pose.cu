@@ -74,7 +74,9 @@ __global__ void __launch_bounds__(256) k_pose_prepare(Ws w, PosePrepArgs a) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; slot < M; slot += stride) {
         const int64_t i = w.rec[slot].id;
-        const double px = a.p.means[3 * i], py = a.p.means[3 * i + 1], pz = a.p.means[3 * i + 2];
+        const int f64 = a.p.dtype;
+        const double px = pld(a.p.means, 3 * i, f64), py = pld(a.p.means, 3 * i + 1, f64),
+                     pz = pld(a.p.means, 3 * i + 2, f64);
         const double x = R[0] * px + R[1] * py + R[2] * pz + a.T.t[0];
         const double y = R[3] * px + R[4] * py + R[5] * pz + a.T.t[1];
         const double z = R[6] * px + R[7] * py + R[8] * pz + a.T.t[2];
@@ -82,7 +84,8 @@ __global__ void __launch_bounds__(256) k_pose_prepare(Ws w, PosePrepArgs a) {
         const double J00 = fx / z, J02 = -fx * x / (z * z), J11 = fy / z, J12 = -fy * y / (z * z);
         double B[9], Wc[9];
         for (int r3 = 0; r3 < 3; ++r3)
-            for (int c3 = 0; c3 < 3; ++c3) B[3 * r3 + c3] = (double)a.p.rots[9 * i + 3 * r3 + c3] * a.p.scales[3 * i + c3];
+            for (int c3 = 0; c3 < 3; ++c3)
+                B[3 * r3 + c3] = pld(a.p.rots, 9 * i + 3 * r3 + c3, f64) * pld(a.p.scales, 3 * i + c3, f64);
         for (int r3 = 0; r3 < 3; ++r3)
             for (int c3 = 0; c3 < 3; ++c3)
                 Wc[3 * r3 + c3] = B[3 * r3] * B[3 * c3] + B[3 * r3 + 1] * B[3 * c3 + 1] + B[3 * r3 + 2] * B[3 * c3 + 2];
@@ -155,7 +158,7 @@ __global__ void __launch_bounds__(256) k_pose_prepare(Ws w, PosePrepArgs a) {
             double g[3];
             sh_grad3(a.degree, d0, d1, d2, k, g);
             for (int c = 0; c < 3; ++c) {
-                const double s = a.p.shs[(i * K + k) * 3 + c];
+                const double s = pld(a.p.shs, (i * K + k) * 3 + c, f64);
                 Pm[3 * c] += s * g[0]; Pm[3 * c + 1] += s * g[1]; Pm[3 * c + 2] += s * g[2];
             }
         }

@@ -57,8 +57,9 @@ __device__ __forceinline__ void sh_basis(int degree, double x, double y, double 
 // Returns false if culled; fills the record, its tile count and depth key.
 __device__ bool splat_one(const PreArgs& a, int64_t i, Rec& r, int& ntiles, uint64_t& key,
                           uint32_t& cmask) {
-    const float* mp = a.p.means + 3 * i;
-    const double px = mp[0], py = mp[1], pz = mp[2];
+    const int f64 = a.p.dtype;
+    const double px = pld(a.p.means, 3 * i, f64), py = pld(a.p.means, 3 * i + 1, f64),
+                 pz = pld(a.p.means, 3 * i + 2, f64);
     const double* R = a.T.R;
     const double* t = a.T.t;
     // mu_c = means @ R^T + t, in the dgemm FMA order
@@ -73,15 +74,14 @@ __device__ bool splat_one(const PreArgs& a, int64_t i, Rec& r, int& ntiles, uint
     const double J00 = fx / z, J02 = -fx * x / zz;
     const double J11 = fy / z, J12 = -fy * y / zz;
     // world covariance B B^T, B = rot * scale (columns scaled)
-    const float* rp = a.p.rots + 9 * i;
-    const float* sp = a.p.scales + 3 * i;
-    const double s0 = sp[0], s1 = sp[1], s2 = sp[2];
+    const double s0 = pld(a.p.scales, 3 * i, f64), s1 = pld(a.p.scales, 3 * i + 1, f64),
+                 s2 = pld(a.p.scales, 3 * i + 2, f64);
     double B[9];
 #pragma unroll
     for (int r3 = 0; r3 < 3; ++r3) {
-        B[3 * r3 + 0] = (double)rp[3 * r3 + 0] * s0;
-        B[3 * r3 + 1] = (double)rp[3 * r3 + 1] * s1;
-        B[3 * r3 + 2] = (double)rp[3 * r3 + 2] * s2;
+        B[3 * r3 + 0] = pld(a.p.rots, 9 * i + 3 * r3 + 0, f64) * s0;
+        B[3 * r3 + 1] = pld(a.p.rots, 9 * i + 3 * r3 + 1, f64) * s1;
+        B[3 * r3 + 2] = pld(a.p.rots, 9 * i + 3 * r3 + 2, f64) * s2;
     }
     double W[9];
 #pragma unroll
@@ -111,7 +111,7 @@ __device__ bool splat_one(const PreArgs& a, int64_t i, Rec& r, int& ntiles, uint
     const double mid = 0.5 * (ca + cc);
     const double amc = ca - cc;
     const double disc = sqrt(fmax(0.25 * (amc * amc) + cb * cb, 0.0));
-    const double op = a.p.opacities[i];
+    const double op = pld(a.p.opacities, i, f64);
     double nsig = a.s.footprint_sigma;
     if (a.s.alpha_cut > 0.0) {
         const double ratio = fmax(op / a.s.alpha_cut, 1.0);
@@ -150,15 +150,15 @@ __device__ bool splat_one(const PreArgs& a, int64_t i, Rec& r, int& ntiles, uint
     sh_basis(a.degree, dx_, dy_, dz_, b);
     const int K = a.p.sh_coeffs;
     const int kk = (a.degree + 1) * (a.degree + 1);
-    const float* shp = a.p.shs + (int64_t)i * K * 3;
+    const int64_t sho = (int64_t)i * K * 3;
     float col[3];
     cmask = 0;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        double acc = b[0] * (double)shp[c];
+        double acc = b[0] * pld(a.p.shs, sho + c, f64);
 #pragma unroll
         for (int k = 1; k < 16; ++k)
-            if (k < kk) acc += b[k] * (double)shp[3 * k + c];
+            if (k < kk) acc += b[k] * pld(a.p.shs, sho + 3 * k + c, f64);
         const double raw = 0.5 + acc;
         col[c] = (float)fmin(fmax(raw, 0.0), 1.0);
         if (raw > 0.0 && raw < 1.0) cmask |= 1u << c;

@@ -128,7 +128,7 @@ class AdamState:
         n, k = len(arrays), int(arrays.shs.shape[1])
         self.cfg = cfg
         self.step = 0
-        self.m = torch.zeros(n * (10 + 3 * k), dtype=torch.float32, device=arrays.device)
+        self.m = torch.zeros(n * (10 + 3 * k), dtype=arrays.dtype, device=arrays.device)
         self.v = torch.zeros_like(self.m)
         self.touched = torch.zeros(n, dtype=torch.uint8, device=arrays.device)
 
@@ -144,6 +144,7 @@ class AdamState:
 
     def orthonormalize(self, arrays: GaussianArrays, stream=None) -> None:
         _lib.check(_lib.load().lsb_orthonormalize(ctypes.c_void_p(arrays.rots.data_ptr()),
+                                                  1 if arrays.dtype == torch.float64 else 0,
                                                   ctypes.c_void_p(self.touched.data_ptr()), len(arrays),
                                                   _lib.stream_ptr(stream)), "orthonormalize")
 
@@ -155,12 +156,22 @@ class WindowEngine:
     the number of views in the whole (possibly sharded) step, so every rank
     scales its gradient by 1/n_views_total and an all-reduce(sum) yields the
     mean of the per-view gradients.  One render workspace is reused for all
-    views (views run back to back on one stream)."""
+    views (views run back to back on one stream).
+
+    Like the reference (optimize.py:142-149) the steps act on an f64 working
+    copy of the window (`master="f64"`); `finish()` re-orthonormalises the
+    stepped rotations and writes the result back into the f32 arena
+    (optimize.py:193-201).  `master="arena"` steps the arena in place."""
 
     def __init__(self, arrays: GaussianArrays, cam, views: Sequence, settings: RasterSettings,
                  cfg: OptimConfig = OptimConfig(), n_views_total: Optional[int] = None,
-                 isect_cap: Optional[int] = None, stream=None):
+                 isect_cap: Optional[int] = None, stream=None, master: str = "f64"):
         _lib.require()
+        self.arena = arrays
+        if master == "f64" and arrays.dtype != torch.float64:
+            arrays = arrays.clone(torch.float64)
+        elif master not in ("f64", "arena"):
+            raise ValueError("master must be 'f64' or 'arena'")
         self.arrays = arrays
         self.cam = cam
         self.settings = settings
@@ -232,13 +243,25 @@ class WindowEngine:
         mark("adam", True); self.adam.apply(self.arrays, self.grads, self.stream); mark("adam", False)
 
     def finish(self) -> None:
-        """End of the window optimisation: re-orthonormalise stepped rotations."""
+        """End of the window optimisation: re-orthonormalise stepped rotations
+        and write the working copy back into the arena."""
         self.adam.orthonormalize(self.arrays, self.stream)
+        if self.arrays is not self.arena:
+            with torch.cuda.stream(self.stream) if self.stream is not None else _nullctx():
+                self.arena.copy_from(self.arrays)
 
     def losses(self) -> np.ndarray:
         """Per-view loss values of the last step (syncs; one small D2H)."""
         s = self.loss.sums()[: len(self.views)].cpu().numpy()
         return s[:, 0] / (3.0 * self.h * self.w)
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
 
 
 def _identity():

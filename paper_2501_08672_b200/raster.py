@@ -49,27 +49,47 @@ def _dev(device=None):
     return torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
 
 
-def _f32(x, shape, device):
+def _as(x, shape, device, dtype=torch.float32):
     t = torch.as_tensor(x)
-    if t.dtype != torch.float32 or t.device != device:
-        t = t.to(device=device, dtype=torch.float32)
+    if t.dtype != dtype or t.device != device:
+        t = t.to(device=device, dtype=dtype)
     return t.reshape(shape).contiguous()
 
 
-class GaussianArrays:
-    """Structure-of-arrays Gaussian parameters in HBM, f32 (the window
-    arena's storage type, window.py:51-55; the reference upcasts the same
-    f32 values to f64 for its math, raster.py:47-52)."""
+def _f32(x, shape, device):
+    return _as(x, shape, device, torch.float32)
 
-    def __init__(self, means, rots, scales, opacities, shs, device=None):
+
+class GaussianArrays:
+    """Structure-of-arrays Gaussian parameters in HBM.  f32 by default (the
+    window arena's storage type, window.py:51-55; the reference upcasts the
+    same f32 values to f64 for its math, raster.py:47-52); f64 for the
+    working copy that optimize_window steps (optimize.py:142-149)."""
+
+    def __init__(self, means, rots, scales, opacities, shs, device=None, dtype=torch.float32):
         dev = _dev(device)
+        if dtype not in (torch.float32, torch.float64):
+            raise ValueError("GaussianArrays dtype must be float32 or float64")
         n = int(np.shape(means)[0]) if not torch.is_tensor(means) else int(means.shape[0])
-        self.means = _f32(means, (n, 3), dev)
-        self.rots = _f32(rots, (n, 3, 3), dev)
-        self.scales = _f32(scales, (n, 3), dev)
-        self.opacities = _f32(opacities, (n,), dev)
+        self.means = _as(means, (n, 3), dev, dtype)
+        self.rots = _as(rots, (n, 3, 3), dev, dtype)
+        self.scales = _as(scales, (n, 3), dev, dtype)
+        self.opacities = _as(opacities, (n,), dev, dtype)
         k = (int(np.prod(np.shape(shs))) // (3 * n)) if n else 1
-        self.shs = _f32(shs, (n, max(k, 1), 3), dev)
+        self.shs = _as(shs, (n, max(k, 1), 3), dev, dtype)
+
+    @property
+    def dtype(self):
+        return self.means.dtype
+
+    def clone(self, dtype=None) -> "GaussianArrays":
+        return GaussianArrays(self.means, self.rots, self.scales, self.opacities, self.shs, self.device,
+                              dtype or self.dtype)
+
+    def copy_from(self, other: "GaussianArrays") -> None:
+        """In-place copy (with cast) of another arena's values."""
+        for k in ("means", "rots", "scales", "opacities", "shs"):
+            getattr(self, k).copy_(getattr(other, k))
 
     def __len__(self):
         return self.means.shape[0]
@@ -94,7 +114,7 @@ class GaussianArrays:
     def params(self) -> _lib.Params:
         return _lib.Params(self.means.data_ptr(), self.rots.data_ptr(), self.scales.data_ptr(),
                            self.opacities.data_ptr(), self.shs.data_ptr(), len(self),
-                           int(self.shs.shape[1]), 0)
+                           int(self.shs.shape[1]), 1 if self.dtype == torch.float64 else 0)
 
 
 @dataclass
