@@ -60,7 +60,7 @@ __device__ __forceinline__ void stage(const Ws& w, int j, int ox, int oy, Staged
     st.c = make_float4(r.c2, r.z, __int_as_float(r.bbx), __int_as_float(r.bby));
 }
 
-template <bool DEPTH>
+template <bool DEPTH, bool CUT>
 __global__ void __launch_bounds__(32 * WPB)
 k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __restrict__ t_final,
             int32_t* __restrict__ n_contrib, float* __restrict__ depth) {
@@ -75,22 +75,29 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
     const int qx = (lane & 3) * RUN, r0 = lane >> 2;      // rows r0 and r0 + 8
     const int gx0 = ox + qx;
     Staged* sr = s_rec[wib];
+    const float fx0 = (float)qx;
+    const float fy[2] = {(float)r0, (float)(r0 + 8)};
+    // A pixel composites while T >= t_min (the reference breaks when
+    // T < t_min, _kernels.py:98); pixels outside the image start at T = -1.
     float T[2][RUN], cr[2][RUN], cg[2][RUN], cb[2][RUN], dz[2][RUN];
-    int cnt[2][RUN];
-    unsigned alive = 0;    // bit (h*RUN + j): pixel still compositing
+    float cnt[2][RUN];     // processed-entry counts (exact in f32 below 2^24)
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
         for (int j = 0; j < RUN; ++j) {
-            T[h][j] = 1.f;
+            T[h][j] = (live_tile && oy + r0 + 8 * h < a.H && gx0 + j < a.W) ? 1.f : -1.f;
             cr[h][j] = cg[h][j] = cb[h][j] = dz[h][j] = 0.f;
-            cnt[h][j] = 0;
-            if (live_tile && oy + r0 + 8 * h < a.H && gx0 + j < a.W) alive |= 1u << (h * RUN + j);
+            cnt[h][j] = 0.f;
         }
     int last = 0;
     const int start = live_tile ? w.tile_start[tile] : 0, end = live_tile ? w.tile_start[tile + 1] : 0;
     for (int base = start; base < end; base += 32) {
-        if (!__any_sync(0xffffffffu, alive != 0)) break;
+        bool alive = false;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int j = 0; j < RUN; ++j) alive |= T[h][j] >= a.tmin;
+        if (!__any_sync(0xffffffffu, alive)) break;
         if (base + lane < end) stage(w, base + lane, ox, oy, sr[lane]);
         __syncwarp();
         const int nb = min(32, end - base);
@@ -99,30 +106,36 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
             const int bby = __float_as_int(qc.w), bbx = __float_as_int(qc.z);
             const int y0 = (bby & 0xffff) - oy, y1 = (bby >> 16) - oy;
             const int lo = max((bbx & 0xffff) - gx0, 0), hi = min((bbx >> 16) - gx0, RUN);
+            if (lo >= hi) continue;
+            bool inx[RUN];                                       // bbox columns of this run
+#pragma unroll
+            for (int j = 0; j < RUN; ++j) inx[j] = j >= lo && j < hi;
             const float4 qa = sr[k].a, qb = sr[k].b;
+            const float lop = __log2f(qb.y);
             bool used = false;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int row = r0 + 8 * h;
-                if (row < y0 || row >= y1 || lo >= hi) continue;
-                const float dy = (float)row - qa.y;
-                const float sdm = fmaf(qa.w, dy, -qa.x);          // u = x_local + s dy - mx
-                const float edy = qb.x * dy * dy;
+                if (row < y0 || row >= y1) continue;
+                const float dy = fy[h] - qa.y;
+                const float u0 = fmaf(qa.w, dy, fx0 - qa.x);      // u = x_local + s dy - mx
+                // log2(alpha) = A u^2 + E dy^2 + log2(op): opacity folded into the exponent
+                const float edy = fmaf(qb.x * dy, dy, lop);
 #pragma unroll
                 for (int j = 0; j < RUN; ++j) {
-                    const bool in = j >= lo && j < hi && ((alive >> (h * RUN + j)) & 1u);
-                    const float u = (float)(qx + j) + sdm;
-                    float al = fminf(qb.y * ex2_approx(fmaf(qa.z, u * u, edy)), a.clamp);
-                    cnt[h][j] += in ? 1 : 0;
+                    const bool in = inx[j] && T[h][j] >= a.tmin;
+                    const float u = j == 0 ? u0 : u0 + (float)j;
+                    float al = fminf(ex2_approx(fmaf(qa.z, u * u, edy)), a.clamp);
+                    cnt[h][j] += in ? 1.f : 0.f;
                     used |= in;
-                    al = (in && al >= a.cut) ? al : 0.f;
+                    const bool take = CUT ? (in && al >= a.cut) : in;
+                    al = take ? al : 0.f;
                     const float wt = T[h][j] * al;
                     cr[h][j] = fmaf(wt, qb.z, cr[h][j]);
                     cg[h][j] = fmaf(wt, qb.w, cg[h][j]);
                     cb[h][j] = fmaf(wt, qc.x, cb[h][j]);
                     if (DEPTH) dz[h][j] = fmaf(wt, qc.y, dz[h][j]);
                     T[h][j] = fmaf(-al, T[h][j], T[h][j]);
-                    if (T[h][j] < a.tmin) alive &= ~(1u << (h * RUN + j));
                 }
             }
             if (used) last = base + k + 1;
@@ -147,7 +160,7 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
             image[3 * p + 1] = ig;
             image[3 * p + 2] = ib;
             t_final[p] = T[h][j];
-            n_contrib[p] = cnt[h][j];
+            n_contrib[p] = (int32_t)cnt[h][j];
             if (DEPTH) depth[p] = dz[h][j];
             if (L.observed) {
                 const float i3[3] = {ir, ig, ib};
@@ -251,6 +264,8 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const int32_t* _
     const float k2 = -2.0f / (float)LOG2E;     // undo the exp2 scaling: a_k = A k2, e = E k2
     Staged* sr = s_rec[wib];
     float2* ske = s_ke[wib];
+    const float fx0 = (float)qx;
+    const float fy[2] = {(float)r0, (float)(r0 + 8)};
     // per-pixel state: T, gD = g . (I - prefix colour), g = dL/dI, entries left
     float T[2][RUN], gD[2][RUN], Gr[2][RUN], Gg[2][RUN], Gb[2][RUN];
     int rem[2][RUN];
@@ -290,6 +305,9 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const int32_t* _
             const int bby = __float_as_int(qc.w), bbx = __float_as_int(qc.z);
             const int y0 = (bby & 0xffff) - oy, y1 = (bby >> 16) - oy;
             const int lo = max((bbx & 0xffff) - gx0, 0), hi = min((bbx >> 16) - gx0, RUN);
+            bool inx[RUN];
+#pragma unroll
+            for (int j = 0; j < RUN; ++j) inx[j] = j >= lo && j < hi;
             const float4 qa = sr[k].a, qb = sr[k].b;
             const float2 qd = ske[k];
             // accumulators: colour (3), sum gd, sum gd v0, sum gd v1, sum gd v0^2,
@@ -303,19 +321,23 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const int32_t* _
             for (int h = 0; h < 2; ++h) {
                 const int row = r0 + 8 * h;
                 if (row < y0 || row >= y1 || lo >= hi) continue;
-                const float dy = (float)row - qa.y;
-                const float sdm = fmaf(qa.w, dy, -qa.x);
+                const float dy = fy[h] - qa.y;
+                const float u0 = fmaf(qa.w, dy, fx0 - qa.x);
                 const float edy = qb.x * dy * dy;
                 const float ey = qd.y * dy;
+                // branch-free per pixel: entries outside the bbox, past the
+                // pixel's processed count, or below alpha_cut get alpha = 0,
+                // which leaves T, gD and every accumulator unchanged
 #pragma unroll
                 for (int j = 0; j < RUN; ++j) {
-                    if (j < lo || j >= hi || rem[h][j] <= 0) continue;
-                    --rem[h][j];
-                    any = true;
-                    const float u = (float)(qx + j) + sdm;
+                    const bool in = inx[j] && rem[h][j] > 0;
+                    rem[h][j] -= in ? 1 : 0;
+                    any |= in;
+                    const float u = j == 0 ? u0 : u0 + (float)j;
                     const float G = ex2_approx(fmaf(qa.z, u * u, edy));
-                    const float al = fminf(qb.y * G, a.clamp);
-                    if (!(al >= a.cut) || al == 0.f) continue;
+                    const float al0 = fminf(qb.y * G, a.clamp);
+                    const bool take = in && al0 >= a.cut;
+                    const float al = take ? al0 : 0.f;
                     const float t = T[h][j];
                     const float wt = t * al;
                     const float gc = fmaf(Gr[h][j], qb.z, fmaf(Gg[h][j], qb.w, Gb[h][j] * qc.x));
@@ -324,18 +346,17 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const int32_t* _
                     acc[0] = fmaf(wt, Gr[h][j], acc[0]);
                     acc[1] = fmaf(wt, Gg[h][j], acc[1]);
                     acc[2] = fmaf(wt, Gb[h][j], acc[2]);
-                    if (al < a.clamp) {
-                        const float gd = G * da;
-                        const float v0 = qd.x * u;                  // (conic d)_x = a_k u
-                        const float v1 = fmaf(qa.w, v0, ey);        // (conic d)_y = s v0 + e dy
-                        const float g0 = gd * v0, g1 = gd * v1;
-                        acc[3] += gd;
-                        acc[4] += g0;
-                        acc[5] += g1;
-                        acc[6] = fmaf(g0, v0, acc[6]);
-                        acc[7] = fmaf(g0, v1, acc[7]);
-                        acc[8] = fmaf(g1, v1, acc[8]);
-                    }
+                    // clamp gate (_kernels.py:201): saturated alpha passes no geometry gradient
+                    const float gd = (take && al < a.clamp) ? G * da : 0.f;
+                    const float v0 = qd.x * u;                  // (conic d)_x = a_k u
+                    const float v1 = fmaf(qa.w, v0, ey);        // (conic d)_y = s v0 + e dy
+                    const float g0 = gd * v0, g1 = gd * v1;
+                    acc[3] += gd;
+                    acc[4] += g0;
+                    acc[5] += g1;
+                    acc[6] = fmaf(g0, v0, acc[6]);
+                    acc[7] = fmaf(g0, v1, acc[7]);
+                    acc[8] = fmaf(g1, v1, acc[8]);
                     T[h][j] = fmaf(-al, t, t);
                 }
             }
@@ -368,10 +389,15 @@ cudaError_t launch_blend_fwd(const Ws& w, const lsb_settings& s, int W, int H, f
                 (float)s.background[0], (float)s.background[1], (float)s.background[2]};
     LossArgs L{observed, grad, w.loss_part, loss_out, w.ctr + 5, kind, gscale};
     const int grid = (w.ntiles + WPB - 1) / WPB;
-    if (depth)
-        k_blend_fwd<true><<<grid, 32 * WPB, 0, st>>>(w, a, L, image, t_final, n_contrib, depth);
+    const bool cut = s.alpha_cut > 0.0;
+    if (depth && cut)
+        k_blend_fwd<true, true><<<grid, 32 * WPB, 0, st>>>(w, a, L, image, t_final, n_contrib, depth);
+    else if (depth)
+        k_blend_fwd<true, false><<<grid, 32 * WPB, 0, st>>>(w, a, L, image, t_final, n_contrib, depth);
+    else if (cut)
+        k_blend_fwd<false, true><<<grid, 32 * WPB, 0, st>>>(w, a, L, image, t_final, n_contrib, depth);
     else
-        k_blend_fwd<false><<<grid, 32 * WPB, 0, st>>>(w, a, L, image, t_final, n_contrib, depth);
+        k_blend_fwd<false, false><<<grid, 32 * WPB, 0, st>>>(w, a, L, image, t_final, n_contrib, depth);
     return cudaGetLastError();
 }
 
