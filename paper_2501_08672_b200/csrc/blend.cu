@@ -65,163 +65,154 @@ __global__ void __launch_bounds__(32 * WPB)
 k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __restrict__ t_final,
             int32_t* __restrict__ n_contrib, float* __restrict__ depth) {
     __shared__ Staged s_rec[WPB][32];
-    __shared__ double s_loss[WPB][2];
-    __shared__ bool s_final;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int tile = blockIdx.x * WPB + wib;
-    const bool live_tile = tile < w.ntiles;
-    const int tl = live_tile ? tile : 0;
-    const int ox = (tl % w.ntx) * TILE, oy = (tl / w.ntx) * TILE;
     const int qx = (lane & 3) * RUN, r0 = lane >> 2;      // rows r0 and r0 + 8
-    const int gx0 = ox + qx;
     Staged* sr = s_rec[wib];
     const float fx0 = (float)qx;
     const float fy[2] = {(float)r0, (float)(r0 + 8)};
-    // A pixel composites while T >= t_min (the reference breaks when
-    // T < t_min, _kernels.py:98); pixels outside the image start at T = -1.
-    float T[2][RUN], cr[2][RUN], cg[2][RUN], cb[2][RUN], dz[2][RUN];
-    float cnt[2][RUN];     // processed-entry counts (exact in f32 below 2^24)
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int j = 0; j < RUN; ++j) {
-            T[h][j] = (live_tile && oy + r0 + 8 * h < a.H && gx0 + j < a.W) ? 1.f : -1.f;
-            cr[h][j] = cg[h][j] = cb[h][j] = dz[h][j] = 0.f;
-            cnt[h][j] = 0.f;
-        }
-    int last = 0;
-    const int start = live_tile ? w.tile_start[tile] : 0, end = live_tile ? w.tile_start[tile + 1] : 0;
-    for (int base = start; base < end; base += 32) {
-        bool alive = false;
+    // persistent tile-warp: pull tiles from the queue until it is empty
+    for (;;) {
+        int tile = 0;
+        if (lane == 0) tile = (int)atomicAdd(&w.ctr[7], 1ull);
+        tile = __shfl_sync(0xffffffffu, tile, 0);
+        if (tile >= w.ntiles) break;
+        const int ox = (tile % w.ntx) * TILE, oy = (tile / w.ntx) * TILE;
+        const int gx0 = ox + qx;
+        double l0 = 0.0, l1 = 0.0;
+        // A pixel composites while T >= t_min (the reference breaks when
+        // T < t_min, _kernels.py:98); pixels outside the image start at T = -1.
+        float T[2][RUN], cr[2][RUN], cg[2][RUN], cb[2][RUN], dz[2][RUN];
+        float cnt[2][RUN];     // processed-entry counts (exact in f32 below 2^24)
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int j = 0; j < RUN; ++j) alive |= T[h][j] >= a.tmin;
-        if (!__any_sync(0xffffffffu, alive)) break;
-        if (base + lane < end) stage(w, base + lane, ox, oy, sr[lane]);
-        __syncwarp();
-        const int nb = min(32, end - base);
-        for (int k = 0; k < nb; ++k) {
-            const float4 qc = sr[k].c;
-            const int bby = __float_as_int(qc.w), bbx = __float_as_int(qc.z);
-            const int y0 = (bby & 0xffff) - oy, y1 = (bby >> 16) - oy;
-            const int lo = max((bbx & 0xffff) - gx0, 0), hi = min((bbx >> 16) - gx0, RUN);
-            if (lo >= hi) continue;
-            bool inx[RUN];                                       // bbox columns of this run
-#pragma unroll
-            for (int j = 0; j < RUN; ++j) inx[j] = j >= lo && j < hi;
-            const float4 qa = sr[k].a, qb = sr[k].b;
-            const float lop = __log2f(qb.y);
-            bool used = false;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int row = r0 + 8 * h;
-                if (row < y0 || row >= y1) continue;
-                const float dy = fy[h] - qa.y;
-                const float u0 = fmaf(qa.w, dy, fx0 - qa.x);      // u = x_local + s dy - mx
-                // log2(alpha) = A u^2 + E dy^2 + log2(op): opacity folded into the exponent
-                const float edy = fmaf(qb.x * dy, dy, lop);
-#pragma unroll
-                for (int j = 0; j < RUN; ++j) {
-                    const bool in = inx[j] && T[h][j] >= a.tmin;
-                    const float u = j == 0 ? u0 : u0 + (float)j;
-                    float al = fminf(ex2_approx(fmaf(qa.z, u * u, edy)), a.clamp);
-                    cnt[h][j] += in ? 1.f : 0.f;
-                    used |= in;
-                    const bool take = CUT ? (in && al >= a.cut) : in;
-                    al = take ? al : 0.f;
-                    const float wt = T[h][j] * al;
-                    cr[h][j] = fmaf(wt, qb.z, cr[h][j]);
-                    cg[h][j] = fmaf(wt, qb.w, cg[h][j]);
-                    cb[h][j] = fmaf(wt, qc.x, cb[h][j]);
-                    if (DEPTH) dz[h][j] = fmaf(wt, qc.y, dz[h][j]);
-                    T[h][j] = fmaf(-al, T[h][j], T[h][j]);
-                }
+            for (int j = 0; j < RUN; ++j) {
+                T[h][j] = (oy + r0 + 8 * h < a.H && gx0 + j < a.W) ? 1.f : -1.f;
+                cr[h][j] = cg[h][j] = cb[h][j] = dz[h][j] = 0.f;
+                cnt[h][j] = 0.f;
             }
-            if (used) last = base + k + 1;
-        }
-        __syncwarp();
-    }
+        int last = 0;
+        const int start = w.tile_start[tile], end = w.tile_start[tile + 1];
+        for (int base = start; base < end; base += 32) {
+            bool alive = false;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
-    if (live_tile && lane == 0) w.tile_last[tile] = max(last, start);
-    double l0 = 0.0, l1 = 0.0;
+            for (int h = 0; h < 2; ++h)
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int gy = oy + r0 + 8 * h;
-        if (!live_tile || gy >= a.H) continue;
+                for (int j = 0; j < RUN; ++j) alive |= T[h][j] >= a.tmin;
+            if (!__any_sync(0xffffffffu, alive)) break;
+            if (base + lane < end) stage(w, base + lane, ox, oy, sr[lane]);
+            __syncwarp();
+            const int nb = min(32, end - base);
+            for (int k = 0; k < nb; ++k) {
+                const float4 qc = sr[k].c;
+                const int bby = __float_as_int(qc.w), bbx = __float_as_int(qc.z);
+                const int y0 = (bby & 0xffff) - oy, y1 = (bby >> 16) - oy;
+                const int lo = max((bbx & 0xffff) - gx0, 0), hi = min((bbx >> 16) - gx0, RUN);
+                if (lo >= hi) continue;
+                bool inx[RUN];                                       // bbox columns of this run
 #pragma unroll
-        for (int j = 0; j < RUN; ++j) {
-            if (gx0 + j >= a.W) continue;
-            const int64_t p = (int64_t)gy * a.W + gx0 + j;
-            const float ir = cr[h][j] + T[h][j] * a.bg0, ig = cg[h][j] + T[h][j] * a.bg1,
-                        ib = cb[h][j] + T[h][j] * a.bg2;
-            image[3 * p] = ir;
-            image[3 * p + 1] = ig;
-            image[3 * p + 2] = ib;
-            t_final[p] = T[h][j];
-            n_contrib[p] = (int32_t)cnt[h][j];
-            if (DEPTH) depth[p] = dz[h][j];
-            if (L.observed) {
-                const float i3[3] = {ir, ig, ib};
+                for (int j = 0; j < RUN; ++j) inx[j] = j >= lo && j < hi;
+                const float4 qa = sr[k].a, qb = sr[k].b;
+                const float lop = __log2f(qb.y);
+                bool used = false;
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const double d = (double)i3[c] - (double)L.observed[3 * p + c];
-                    l1 += d * d;
-                    float gv;
-                    if (L.kind == 0) {
-                        l0 += fabs(d);
-                        gv = d > 0.0 ? L.gscale : (d < 0.0 ? -L.gscale : 0.f);
-                    } else {
-                        l0 += d * d;
-                        gv = (float)(2.0 * d * (double)L.gscale);
+                for (int h = 0; h < 2; ++h) {
+                    const int row = r0 + 8 * h;
+                    if (row < y0 || row >= y1) continue;
+                    const float dy = fy[h] - qa.y;
+                    const float u0 = fmaf(qa.w, dy, fx0 - qa.x);      // u = x_local + s dy - mx
+                    // log2(alpha) = A u^2 + E dy^2 + log2(op): opacity folded into the exponent
+                    const float edy = fmaf(qb.x * dy, dy, lop);
+#pragma unroll
+                    for (int j = 0; j < RUN; ++j) {
+                        const bool in = inx[j] && T[h][j] >= a.tmin;
+                        const float u = j == 0 ? u0 : u0 + (float)j;
+                        float al = fminf(ex2_approx(fmaf(qa.z, u * u, edy)), a.clamp);
+                        cnt[h][j] += in ? 1.f : 0.f;
+                        used |= in;
+                        const bool take = CUT ? (in && al >= a.cut) : in;
+                        al = take ? al : 0.f;
+                        const float wt = T[h][j] * al;
+                        cr[h][j] = fmaf(wt, qb.z, cr[h][j]);
+                        cg[h][j] = fmaf(wt, qb.w, cg[h][j]);
+                        cb[h][j] = fmaf(wt, qc.x, cb[h][j]);
+                        if (DEPTH) dz[h][j] = fmaf(wt, qc.y, dz[h][j]);
+                        T[h][j] = fmaf(-al, T[h][j], T[h][j]);
                     }
-                    L.grad[3 * p + c] = gv;
+                }
+                if (used) last = base + k + 1;
+            }
+            __syncwarp();
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
+        if (lane == 0) w.tile_last[tile] = max(last, start);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int gy = oy + r0 + 8 * h;
+            if (gy >= a.H) continue;
+#pragma unroll
+            for (int j = 0; j < RUN; ++j) {
+                if (gx0 + j >= a.W) continue;
+                const int64_t p = (int64_t)gy * a.W + gx0 + j;
+                const float ir = cr[h][j] + T[h][j] * a.bg0, ig = cg[h][j] + T[h][j] * a.bg1,
+                            ib = cb[h][j] + T[h][j] * a.bg2;
+                image[3 * p] = ir;
+                image[3 * p + 1] = ig;
+                image[3 * p + 2] = ib;
+                t_final[p] = T[h][j];
+                n_contrib[p] = (int32_t)cnt[h][j];
+                if (DEPTH) depth[p] = dz[h][j];
+                if (L.observed) {
+                    const float i3[3] = {ir, ig, ib};
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const double d = (double)i3[c] - (double)L.observed[3 * p + c];
+                        l1 += d * d;
+                        float gv;
+                        if (L.kind == 0) {
+                            l0 += fabs(d);
+                            gv = d > 0.0 ? L.gscale : (d < 0.0 ? -L.gscale : 0.f);
+                        } else {
+                            l0 += d * d;
+                            gv = (float)(2.0 * d * (double)L.gscale);
+                        }
+                        L.grad[3 * p + c] = gv;
+                    }
                 }
             }
         }
-    }
-    if (!L.observed) return;
+        if (!L.observed) continue;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        l0 += __shfl_xor_sync(0xffffffffu, l0, o);
-        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
-    }
-    if (live_tile && lane == 0) {
-        L.sums[2 * tile] = l0;
-        L.sums[2 * tile + 1] = l1;
-        __threadfence();          // every writer publishes before the ticket
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) s_final = atomicAdd(L.ticket, 1ull) == gridDim.x - 1;
-    __syncthreads();
-    if (!s_final) return;
-    __threadfence();
-    // last CTA: deterministic sum of the tile partials
-    double v0 = 0.0, v1 = 0.0;
-    for (int t = threadIdx.x; t < w.ntiles; t += 32 * WPB) {
-        v0 += ((volatile double*)L.sums)[2 * t];
-        v1 += ((volatile double*)L.sums)[2 * t + 1];
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        v0 += __shfl_xor_sync(0xffffffffu, v0, o);
-        v1 += __shfl_xor_sync(0xffffffffu, v1, o);
-    }
-    if (lane == 0) {
-        s_loss[wib][0] = v0;
-        s_loss[wib][1] = v1;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t0 = 0.0, t1 = 0.0;
-        for (int k = 0; k < WPB; ++k) {
-            t0 += s_loss[k][0];
-            t1 += s_loss[k][1];
+        for (int o = 16; o > 0; o >>= 1) {
+            l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+            l1 += __shfl_xor_sync(0xffffffffu, l1, o);
         }
-        L.sums_out[0] = t0;
-        L.sums_out[1] = t1;
-        *L.ticket = 0;
+        unsigned long long done = 0;
+        if (lane == 0) {
+            L.sums[2 * tile] = l0;
+            L.sums[2 * tile + 1] = l1;
+            __threadfence();       // publish the tile partial before counting the tile done
+            done = atomicAdd(L.ticket, 1ull);
+        }
+        done = __shfl_sync(0xffffffffu, done, 0);
+        if (done != (unsigned long long)w.ntiles - 1) continue;
+        // the warp that finished the last tile: deterministic sum in tile order
+        __threadfence();
+        double v0 = 0.0, v1 = 0.0;
+        for (int t = lane; t < w.ntiles; t += 32) {
+            v0 += ((volatile double*)L.sums)[2 * t];
+            v1 += ((volatile double*)L.sums)[2 * t + 1];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+            v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+        }
+        if (lane == 0) {
+            L.sums_out[0] = v0;
+            L.sums_out[1] = v1;
+        }
     }
 }
 
@@ -256,130 +247,145 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const int32_t* _
     __shared__ Staged s_rec[WPB][32];
     __shared__ float2 s_ke[WPB][32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int tile = blockIdx.x * WPB + wib;
-    if (tile >= w.ntiles) return;
-    const int ox = (tile % w.ntx) * TILE, oy = (tile / w.ntx) * TILE;
     const int qx = (lane & 3) * RUN, r0 = lane >> 2;
-    const int gx0 = ox + qx;
     const float k2 = -2.0f / (float)LOG2E;     // undo the exp2 scaling: a_k = A k2, e = E k2
     Staged* sr = s_rec[wib];
     float2* ske = s_ke[wib];
     const float fx0 = (float)qx;
     const float fy[2] = {(float)r0, (float)(r0 + 8)};
-    // per-pixel state: T, gD = g . (I - prefix colour), g = dL/dI, entries left
-    float T[2][RUN], gD[2][RUN], Gr[2][RUN], Gg[2][RUN], Gb[2][RUN];
-    int rem[2][RUN];
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int j = 0; j < RUN; ++j) {
-            T[h][j] = 1.f;
-            gD[h][j] = Gr[h][j] = Gg[h][j] = Gb[h][j] = 0.f;
-            rem[h][j] = 0;
-            const int gy = oy + r0 + 8 * h;
-            if (gy < a.H && gx0 + j < a.W) {
-                const int64_t p = (int64_t)gy * a.W + gx0 + j;
-                rem[h][j] = n_contrib[p];
-                Gr[h][j] = gimg[3 * p] * gscale;
-                Gg[h][j] = gimg[3 * p + 1] * gscale;
-                Gb[h][j] = gimg[3 * p + 2] * gscale;
-                gD[h][j] = Gr[h][j] * image[3 * p] + Gg[h][j] * image[3 * p + 1] + Gb[h][j] * image[3 * p + 2];
-            }
-        }
-    const int start = w.tile_start[tile], end = w.tile_last[tile];
-    for (int base = start; base < end; base += 32) {
-        bool alive = false;
+    for (;;) {
+        int tile = 0;
+        if (lane == 0) tile = (int)atomicAdd(&w.ctr[8], 1ull);
+        tile = __shfl_sync(0xffffffffu, tile, 0);
+        if (tile >= w.ntiles) break;
+        const int ox = (tile % w.ntx) * TILE, oy = (tile / w.ntx) * TILE;
+        const int gx0 = ox + qx;
+        // per-pixel state: T, gD = g . (I - prefix colour), g = dL/dI, entries left
+        float T[2][RUN], gD[2][RUN], Gr[2][RUN], Gg[2][RUN], Gb[2][RUN];
+        int rem[2][RUN];
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int j = 0; j < RUN; ++j) alive |= rem[h][j] > 0;
-        if (!__any_sync(0xffffffffu, alive)) break;
-        if (base + lane < end) {
-            stage(w, base + lane, ox, oy, sr[lane]);
-            ske[lane] = make_float2(sr[lane].a.z * k2, sr[lane].b.x * k2);
-        }
-        __syncwarp();
-        const int nb = min(32, end - base);
-        for (int k = 0; k < nb; ++k) {
-            const float4 qc = sr[k].c;
-            const int bby = __float_as_int(qc.w), bbx = __float_as_int(qc.z);
-            const int y0 = (bby & 0xffff) - oy, y1 = (bby >> 16) - oy;
-            const int lo = max((bbx & 0xffff) - gx0, 0), hi = min((bbx >> 16) - gx0, RUN);
-            bool inx[RUN];
-#pragma unroll
-            for (int j = 0; j < RUN; ++j) inx[j] = j >= lo && j < hi;
-            const float4 qa = sr[k].a, qb = sr[k].b;
-            const float2 qd = ske[k];
-            // accumulators: colour (3), sum gd, sum gd v0, sum gd v1, sum gd v0^2,
-            // sum gd v0 v1, sum gd v1^2 with gd = G dalpha and v = conic d
-            // (op is factored out and applied once per record below)
-            float acc[9];
-#pragma unroll
-            for (int c = 0; c < 9; ++c) acc[c] = 0.f;
-            bool any = false;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int row = r0 + 8 * h;
-                if (row < y0 || row >= y1 || lo >= hi) continue;
-                const float dy = fy[h] - qa.y;
-                const float u0 = fmaf(qa.w, dy, fx0 - qa.x);
-                const float edy = qb.x * dy * dy;
-                const float ey = qd.y * dy;
-                // branch-free per pixel: entries outside the bbox, past the
-                // pixel's processed count, or below alpha_cut get alpha = 0,
-                // which leaves T, gD and every accumulator unchanged
-#pragma unroll
-                for (int j = 0; j < RUN; ++j) {
-                    const bool in = inx[j] && rem[h][j] > 0;
-                    rem[h][j] -= in ? 1 : 0;
-                    any |= in;
-                    const float u = j == 0 ? u0 : u0 + (float)j;
-                    const float G = ex2_approx(fmaf(qa.z, u * u, edy));
-                    const float al0 = fminf(qb.y * G, a.clamp);
-                    const bool take = in && al0 >= a.cut;
-                    const float al = take ? al0 : 0.f;
-                    const float t = T[h][j];
-                    const float wt = t * al;
-                    const float gc = fmaf(Gr[h][j], qb.z, fmaf(Gg[h][j], qb.w, Gb[h][j] * qc.x));
-                    gD[h][j] = fmaf(-wt, gc, gD[h][j]);               // g . suffix colour after k
-                    const float da = fmaf(t, gc, -gD[h][j] * rcp_approx(1.f - al));
-                    acc[0] = fmaf(wt, Gr[h][j], acc[0]);
-                    acc[1] = fmaf(wt, Gg[h][j], acc[1]);
-                    acc[2] = fmaf(wt, Gb[h][j], acc[2]);
-                    // clamp gate (_kernels.py:201): saturated alpha passes no geometry gradient
-                    const float gd = (take && al < a.clamp) ? G * da : 0.f;
-                    const float v0 = qd.x * u;                  // (conic d)_x = a_k u
-                    const float v1 = fmaf(qa.w, v0, ey);        // (conic d)_y = s v0 + e dy
-                    const float g0 = gd * v0, g1 = gd * v1;
-                    acc[3] += gd;
-                    acc[4] += g0;
-                    acc[5] += g1;
-                    acc[6] = fmaf(g0, v0, acc[6]);
-                    acc[7] = fmaf(g0, v1, acc[7]);
-                    acc[8] = fmaf(g1, v1, acc[8]);
-                    T[h][j] = fmaf(-al, t, t);
+            for (int j = 0; j < RUN; ++j) {
+                T[h][j] = 1.f;
+                gD[h][j] = Gr[h][j] = Gg[h][j] = Gb[h][j] = 0.f;
+                rem[h][j] = 0;
+                const int gy = oy + r0 + 8 * h;
+                if (gy < a.H && gx0 + j < a.W) {
+                    const int64_t p = (int64_t)gy * a.W + gx0 + j;
+                    rem[h][j] = n_contrib[p];
+                    Gr[h][j] = gimg[3 * p] * gscale;
+                    Gg[h][j] = gimg[3 * p + 1] * gscale;
+                    Gb[h][j] = gimg[3 * p + 2] * gscale;
+                    gD[h][j] = Gr[h][j] * image[3 * p] + Gg[h][j] * image[3 * p + 1] + Gb[h][j] * image[3 * p + 2];
                 }
             }
-            float val = 0.f;
-            if (__any_sync(0xffffffffu, any)) {
-                // index i of the 8-vector lands in lanes 4i..4i+3 (reduce8)
-                const float r8 = reduce8(acc, lane);
-                float r9 = acc[8];
+        const int start = w.tile_start[tile], end = w.tile_last[tile];
+        for (int base = start; base < end; base += 32) {
+            bool alive = false;
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) r9 += __shfl_xor_sync(0xffffffffu, r9, o);
-                val = __shfl_sync(0xffffffffu, r8, 4 * min(lane, 7));
-                if (lane == 8) val = r9;
-                const float op = qb.y;
-                val *= (lane < 4) ? 1.f : ((lane < 6) ? op : 0.5f * op);
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int j = 0; j < RUN; ++j) alive |= rem[h][j] > 0;
+            if (!__any_sync(0xffffffffu, alive)) break;
+            if (base + lane < end) {
+                stage(w, base + lane, ox, oy, sr[lane]);
+                ske[lane] = make_float2(sr[lane].a.z * k2, sr[lane].b.x * k2);
             }
-            if (lane < NUM_PART) w.part[(int64_t)w.tile_e[base + k] * NUM_PART + lane] = val;
+            __syncwarp();
+            const int nb = min(32, end - base);
+            for (int k = 0; k < nb; ++k) {
+                const float4 qc = sr[k].c;
+                const int bby = __float_as_int(qc.w), bbx = __float_as_int(qc.z);
+                const int y0 = (bby & 0xffff) - oy, y1 = (bby >> 16) - oy;
+                const int lo = max((bbx & 0xffff) - gx0, 0), hi = min((bbx >> 16) - gx0, RUN);
+                bool inx[RUN];
+#pragma unroll
+                for (int j = 0; j < RUN; ++j) inx[j] = j >= lo && j < hi;
+                const float4 qa = sr[k].a, qb = sr[k].b;
+                const float2 qd = ske[k];
+                // accumulators: colour (3), sum gd, sum gd v0, sum gd v1, sum gd v0^2,
+                // sum gd v0 v1, sum gd v1^2 with gd = G dalpha and v = conic d
+                // (op is factored out and applied once per record below)
+                float acc[9];
+#pragma unroll
+                for (int c = 0; c < 9; ++c) acc[c] = 0.f;
+                bool any = false;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int row = r0 + 8 * h;
+                    if (row < y0 || row >= y1 || lo >= hi) continue;
+                    const float dy = fy[h] - qa.y;
+                    const float u0 = fmaf(qa.w, dy, fx0 - qa.x);
+                    const float edy = qb.x * dy * dy;
+                    const float ey = qd.y * dy;
+                    // branch-free per pixel: entries outside the bbox, past the
+                    // pixel's processed count, or below alpha_cut get alpha = 0,
+                    // which leaves T, gD and every accumulator unchanged
+#pragma unroll
+                    for (int j = 0; j < RUN; ++j) {
+                        const bool in = inx[j] && rem[h][j] > 0;
+                        rem[h][j] -= in ? 1 : 0;
+                        any |= in;
+                        const float u = j == 0 ? u0 : u0 + (float)j;
+                        const float G = ex2_approx(fmaf(qa.z, u * u, edy));
+                        const float al0 = fminf(qb.y * G, a.clamp);
+                        const bool take = in && al0 >= a.cut;
+                        const float al = take ? al0 : 0.f;
+                        const float t = T[h][j];
+                        const float wt = t * al;
+                        const float gc = fmaf(Gr[h][j], qb.z, fmaf(Gg[h][j], qb.w, Gb[h][j] * qc.x));
+                        gD[h][j] = fmaf(-wt, gc, gD[h][j]);               // g . suffix colour after k
+                        const float da = fmaf(t, gc, -gD[h][j] * rcp_approx(1.f - al));
+                        acc[0] = fmaf(wt, Gr[h][j], acc[0]);
+                        acc[1] = fmaf(wt, Gg[h][j], acc[1]);
+                        acc[2] = fmaf(wt, Gb[h][j], acc[2]);
+                        // clamp gate (_kernels.py:201): saturated alpha passes no geometry gradient
+                        const float gd = (take && al < a.clamp) ? G * da : 0.f;
+                        const float v0 = qd.x * u;                  // (conic d)_x = a_k u
+                        const float v1 = fmaf(qa.w, v0, ey);        // (conic d)_y = s v0 + e dy
+                        const float g0 = gd * v0, g1 = gd * v1;
+                        acc[3] += gd;
+                        acc[4] += g0;
+                        acc[5] += g1;
+                        acc[6] = fmaf(g0, v0, acc[6]);
+                        acc[7] = fmaf(g0, v1, acc[7]);
+                        acc[8] = fmaf(g1, v1, acc[8]);
+                        T[h][j] = fmaf(-al, t, t);
+                    }
+                }
+                float val = 0.f;
+                if (__any_sync(0xffffffffu, any)) {
+                    // index i of the 8-vector lands in lanes 4i..4i+3 (reduce8)
+                    const float r8 = reduce8(acc, lane);
+                    float r9 = acc[8];
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) r9 += __shfl_xor_sync(0xffffffffu, r9, o);
+                    val = __shfl_sync(0xffffffffu, r8, 4 * min(lane, 7));
+                    if (lane == 8) val = r9;
+                    const float op = qb.y;
+                    val *= (lane < 4) ? 1.f : ((lane < 6) ? op : 0.5f * op);
+                }
+                if (lane < NUM_PART) w.part[(int64_t)w.tile_e[base + k] * NUM_PART + lane] = val;
+            }
+            __syncwarp();
         }
-        __syncwarp();
+        // intersections the walk never reached contribute nothing
+        const int fin = w.tile_start[tile + 1];
+        for (int j = max(end, start); j < fin; ++j)
+            if (lane < NUM_PART) w.part[(int64_t)w.tile_e[j] * NUM_PART + lane] = 0.f;
     }
-    // intersections the walk never reached contribute nothing
-    const int fin = w.tile_start[tile + 1];
-    for (int j = max(end, start); j < fin; ++j)
-        if (lane < NUM_PART) w.part[(int64_t)w.tile_e[j] * NUM_PART + lane] = 0.f;
+}
+
+// CTAs to launch for a persistent tile-warp kernel: every resident slot once.
+static int persistent_grid(const void* fn, int ntiles) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * WPB, 0);
+    const int need = (ntiles + WPB - 1) / WPB;
+    const int g = sms * (per_sm > 0 ? per_sm : 1);
+    return g < need ? g : need;
 }
 
 cudaError_t launch_blend_fwd(const Ws& w, const lsb_settings& s, int W, int H, float* image, float* t_final,
@@ -388,8 +394,13 @@ cudaError_t launch_blend_fwd(const Ws& w, const lsb_settings& s, int W, int H, f
     BlendArgs a{W, H, (float)s.alpha_clamp, (float)s.transmittance_min, (float)s.alpha_cut,
                 (float)s.background[0], (float)s.background[1], (float)s.background[2]};
     LossArgs L{observed, grad, w.loss_part, loss_out, w.ctr + 5, kind, gscale};
-    const int grid = (w.ntiles + WPB - 1) / WPB;
+    // reset the loss done-count and the forward tile queue ([5], [7])
+    cudaError_t e = cudaMemsetAsync(w.ctr + 5, 0, 3 * sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
     const bool cut = s.alpha_cut > 0.0;
+    const int grid = persistent_grid(depth ? (cut ? (const void*)k_blend_fwd<true, true> : (const void*)k_blend_fwd<true, false>)
+                                           : (cut ? (const void*)k_blend_fwd<false, true> : (const void*)k_blend_fwd<false, false>),
+                                     w.ntiles);
     if (depth && cut)
         k_blend_fwd<true, true><<<grid, 32 * WPB, 0, st>>>(w, a, L, image, t_final, n_contrib, depth);
     else if (depth)
@@ -405,7 +416,10 @@ cudaError_t launch_blend_bwd(const Ws& w, const lsb_settings& s, int W, int H, c
                              const int32_t* n_contrib, const float* gimg, float gscale, cudaStream_t st) {
     BlendArgs a{W, H, (float)s.alpha_clamp, (float)s.transmittance_min, (float)s.alpha_cut,
                 (float)s.background[0], (float)s.background[1], (float)s.background[2]};
-    k_blend_bwd<<<(w.ntiles + WPB - 1) / WPB, 32 * WPB, 0, st>>>(w, a, image, n_contrib, gimg, gscale);
+    cudaError_t e = cudaMemsetAsync(w.ctr + 8, 0, sizeof(unsigned long long), st);   // backward tile queue
+    if (e != cudaSuccess) return e;
+    k_blend_bwd<<<persistent_grid((const void*)k_blend_bwd, w.ntiles), 32 * WPB, 0, st>>>(w, a, image, n_contrib,
+                                                                                         gimg, gscale);
     return cudaGetLastError();
 }
 

@@ -28,7 +28,8 @@ struct __align__(16) Rec {
 static_assert(sizeof(Rec) == 64, "Rec must be 64 bytes");
 
 struct Ws {
-    unsigned long long* ctr;    // [0] M, [1] I, [2] overflow, [3] preprocess ticket, [4] chain ticket, [5] loss ticket, [6] big-tile count
+    unsigned long long* ctr;    // [0] M, [1] I, [2] overflow, [3] preprocess ticket, [4] chain ticket,
+                                // [5] fused-loss tiles done, [6] big-tile count, [7] fwd / [8] bwd tile queues
     unsigned long long* scan;   // chained-scan state: 2 words per preprocess block
     Rec* rec;                   // [n] (only the first M are live)
     uint64_t* vkey;             // [n] depth bits of live splats
@@ -73,7 +74,7 @@ inline size_t carve(const lsb_dims& d, char* base, Ws* w) {
     const size_t n = (size_t)(d.n > 0 ? d.n : 1);
     const size_t cap = (size_t)(d.isect_cap > 0 ? d.isect_cap : 1);
     // zeroed prefix: counters, scan flags, tile histogram, tile cursors
-    t.ctr = (unsigned long long*)take(8 * sizeof(unsigned long long));
+    t.ctr = (unsigned long long*)take(16 * sizeof(unsigned long long));
     t.scan = (unsigned long long*)take(2 * sizeof(unsigned long long) * (size_t)t.nblocks_pre);
     t.tile_count = (int32_t*)take(sizeof(int32_t) * t.ntiles);
     t.tile_cursor = (int32_t*)take(sizeof(int32_t) * t.ntiles);

@@ -176,25 +176,34 @@ __device__ bool splat_one(const PreArgs& a, int64_t i, Rec& r, int& ntiles, uint
 
 constexpr unsigned long long ST_AGG = 1ull << 62, ST_INC = 2ull << 62, VAL_MASK = (1ull << 62) - 1;
 
-// Decoupled look-back for one running total (chained scan, single pass).
-__device__ unsigned long long lookback(unsigned long long* flags, int blk,
-                                       unsigned long long agg) {
+// Decoupled look-back for one running total (chained scan, single pass),
+// one warp: the 32 nearest predecessors are inspected per round, so a block
+// needs ~1 round trip to L2 instead of one per predecessor.
+__device__ unsigned long long warp_lookback(unsigned long long* flags, int blk, unsigned long long agg,
+                                            int lane) {
     if (blk == 0) {
-        atomicExch(&flags[0], ST_INC | agg);
+        if (lane == 0) atomicExch(&flags[0], ST_INC | agg);
         return 0;
     }
-    atomicExch(&flags[blk], ST_AGG | agg);
+    if (lane == 0) atomicExch(&flags[blk], ST_AGG | agg);
     unsigned long long excl = 0;
     int j = blk - 1;
     while (true) {
-        const unsigned long long v = *((volatile unsigned long long*)&flags[j]);
-        const unsigned long long st = v & ~VAL_MASK;
-        if (st == 0) continue;
-        excl += v & VAL_MASK;
-        if (st == ST_INC) break;
-        --j;
+        const int idx = j - lane;
+        unsigned long long v;
+        do {
+            v = idx >= 0 ? *((volatile unsigned long long*)&flags[idx]) : ST_INC;
+        } while (!__all_sync(0xffffffffu, (v & ~VAL_MASK) != 0));
+        const unsigned inc = __ballot_sync(0xffffffffu, (v & ~VAL_MASK) == ST_INC);
+        const int first = inc ? __ffs(inc) - 1 : 31;      // nearest predecessor with an inclusive prefix
+        unsigned long long x = lane <= first ? (v & VAL_MASK) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        excl += x;
+        if (inc) break;
+        j -= 32;
     }
-    atomicExch(&flags[blk], ST_INC | (excl + agg));
+    if (lane == 0) atomicExch(&flags[blk], ST_INC | (excl + agg));
     return excl;
 }
 
@@ -246,9 +255,15 @@ k_preprocess(PreArgs a, Ws w) {
         totv += s_wv[k];
         tott += s_wt[k];
     }
+    if (warp == 0) {
+        const unsigned long long b = warp_lookback(w.scan, blk, (unsigned long long)totv, lane);
+        if (lane == 0) s_base_v = b;
+    } else if (warp == 1) {
+        const unsigned long long b = warp_lookback(w.scan + w.nblocks_pre, blk, (unsigned long long)tott, lane);
+        if (lane == 0) s_base_t = b;
+    }
+    __syncthreads();
     if (tid == 0) {
-        s_base_v = lookback(w.scan, blk, (unsigned long long)totv);
-        s_base_t = lookback(w.scan + w.nblocks_pre, blk, (unsigned long long)tott);
         if (blk == w.nblocks_pre - 1) {
             w.ctr[0] = s_base_v + totv;
             w.ctr[1] = s_base_t + tott;

@@ -167,3 +167,55 @@ def orbit_views(n_views: int):
 def camera_for(width: int, height: int):
     from .geometry import PinholeCamera
     return PinholeCamera(0.9375 * width, 0.9375 * width, width / 2, height / 2, width, height)
+
+
+# -- LiDAR scans of the room (benchmark input for the voxel map, config 3) ----
+
+T_LI = SE3(np.eye(3), [0.03, 0.0, 0.05])      # cli.py:128
+
+
+def room_triangles(rects=None) -> np.ndarray:
+    """(T, 3, 3) triangles, two per rectangle (sim.py:83-86)."""
+    rects = default_room() if rects is None else rects
+    tris = []
+    for r in rects:
+        o, u, v = r.origin, r.edge_u, r.edge_v
+        tris += [[o, o + u, o + u + v], [o, o + u + v, o + v]]
+    return np.asarray(tris, dtype=np.float64)
+
+
+def scan_directions(n_az=1000, n_el=100, az_span=2 * np.pi, el_span=np.deg2rad(80.0)) -> np.ndarray:
+    """ScanPattern.directions (sim.py:300-310): (n_az * n_el, 3) unit rays."""
+    az = np.linspace(-az_span / 2, az_span / 2, n_az)
+    el = np.linspace(-el_span / 2, el_span / 2, n_el)
+    aa, ee = np.meshgrid(az, el, indexing="ij")
+    return np.stack([np.cos(ee) * np.cos(aa), np.cos(ee) * np.sin(aa), np.sin(ee)], axis=-1).reshape(-1, 3)
+
+
+def lidar_scan(T_wl, tris, dirs_l, device="cpu", chunk=1 << 15):
+    """Nearest-hit ray casting (Moeller-Trumbore, sim.py:321-346) of the scan
+    pattern from T_wl; returns the world-frame hit points (f64 tensor)."""
+    import torch
+    R = torch.as_tensor(np.asarray(T_wl.R), dtype=torch.float64, device=device)
+    o = torch.as_tensor(np.asarray(T_wl.t), dtype=torch.float64, device=device)
+    tr = torch.as_tensor(tris, dtype=torch.float64, device=device)
+    d_all = torch.as_tensor(dirs_l, dtype=torch.float64, device=device) @ R.T
+    v0, e1, e2 = tr[:, 0], tr[:, 1] - tr[:, 0], tr[:, 2] - tr[:, 0]
+    tvec = o[None, :] - v0
+    qvec = torch.cross(tvec, e1, dim=1)
+    out = []
+    for s in range(0, d_all.shape[0], chunk):
+        d = d_all[s:s + chunk]
+        pvec = torch.cross(d[:, None, :].expand(-1, tr.shape[0], -1), e2[None].expand(d.shape[0], -1, -1), dim=2)
+        det = (e1[None] * pvec).sum(-1)
+        ok = det.abs() > 1e-12
+        inv = torch.where(ok, 1.0 / torch.where(ok, det, torch.ones_like(det)), torch.zeros_like(det))
+        u = (tvec[None] * pvec).sum(-1) * inv
+        v = (d[:, None, :] * qvec[None]).sum(-1) * inv
+        t = (e2 * qvec).sum(-1)[None] * inv
+        valid = ok & (u >= -1e-12) & (v >= -1e-12) & (u + v <= 1 + 1e-12) & (t > 1e-6)
+        t = torch.where(valid, t, torch.full_like(t, float("inf")))
+        best = t.min(dim=1).values
+        hit = torch.isfinite(best)
+        out.append(o[None, :] + d[hit] * best[hit, None])
+    return torch.cat(out, dim=0)

@@ -1,0 +1,108 @@
+"""Multi-process (world size 2, gloo, CPU) tests of the view-sharded window
+step's host logic: view partition, the gradient all-reduce over the flat
+ParamGradients buffer, and replica identity after the deterministic update.
+The per-view gradients come from the CPU oracle (test infrastructure)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from golden_io import load
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_shard_views_partition():
+    from paper_2501_08672_b200.dist import shard_views
+    for n in (1, 10, 64):
+        for world in (1, 2, 4, 8):
+            parts = [shard_views(n, world, r) for r in range(world)]
+            flat = sorted(v for p in parts for v in p)
+            assert flat == list(range(n))
+            assert max(map(len, parts)) - min(map(len, parts)) <= 1
+
+
+def _views_and_scene():
+    from types import SimpleNamespace
+    from paper_2501_08672_b200.scene import camera_for, orbit_views
+    s = load("scene_room_0323")
+    P = {k: s[k].astype(np.float64) for k in ("means", "rots", "scales", "opacities", "shs")}
+    cam = camera_for(96, 80)
+    st = SimpleNamespace(near=0.01, dilation=0.3, alpha_clamp=0.99, transmittance_min=1e-4, footprint_sigma=6.0,
+                         alpha_cut=1 / 255, max_footprint_px=512.0, background=np.zeros(3), sh_degree=0)
+    return P, cam, st, orbit_views(4)
+
+
+def _view_grad_flat(P, cam, st, T_wc, V):
+    """Oracle gradient of one view's L1 loss against a shifted-colour target,
+    scaled by 1/V and packed in the ParamGradients flat layout."""
+    from oracle import raster as orc
+    from oracle.optim import photometric_loss
+    from paper_2501_08672_b200.raster import ParamGradients
+    T_cw = T_wc.inverse()
+    c = orc.render(P, T_cw.R, T_cw.t, cam, st)
+    target = np.clip(c["image"] * 0.9 + 0.05, 0, 1)
+    _, _, g_img = photometric_loss(c["image"], target)
+    g = orc.backward(c, g_img)["grads"]
+    n, k = len(P["means"]), P["shs"].shape[1]
+    pg = ParamGradients.zeros(n, k, "cpu")
+    for name in ("mean", "rot", "scale", "opacity", "sh"):
+        getattr(pg, name).copy_(torch.from_numpy(g[name] / V).to(torch.float32))
+    return pg.flat
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2501_08672_b200.dist import make_allreduce, replicas_identical, shard_views
+        P, cam, st, views = _views_and_scene()
+        V = len(views)
+        flat = None
+        for v in shard_views(V, world, rank):
+            g = _view_grad_flat(P, cam, st, views[v], V)
+            flat = g if flat is None else flat + g
+        allreduce = make_allreduce()
+        assert allreduce is not None
+        allreduce(flat)
+        # the same deterministic update on every rank keeps replicas identical
+        params = torch.from_numpy(P["means"].astype(np.float32).ravel().copy())
+        n = len(P["means"])
+        params -= 1e-3 * torch.sign(flat[: 3 * n])
+        ok = replicas_identical(params)
+        q.put((rank, flat.numpy(), ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_view_sharded_allreduce_equals_single_process_mean():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    out.sort(key=lambda x: x[0])
+    assert np.array_equal(out[0][1], out[1][1]), "ranks disagree after the all-reduce"
+    assert out[0][2] and out[1][2], "replicas diverged"
+    # single-process reference: the mean of all per-view gradients
+    P, cam, st, views = _views_and_scene()
+    ref = sum(_view_grad_flat(P, cam, st, T, len(views)) for T in views).numpy()
+    assert np.abs(out[0][1] - ref).max() <= 1e-6 * max(np.abs(ref).max(), 1e-12)

@@ -122,3 +122,28 @@ def test_optimize_window_matches_reference():
     for k in ("means", "scales", "opacities", "shs"):
         assert np.abs(out[k].astype(np.float32) - d["out_" + k]).max() <= 1e-6, k
     assert np.abs(out["rots"].reshape(n, 9).astype(np.float32) - d["out_rots"]).max() <= 1e-6
+
+
+def test_voxmap_oracle_matches_reference():
+    from oracle.voxmap import Map, keys
+    d = load("voxmap")
+    rl, L = float(d["root_len"]), int(d["max_level"])
+    assert np.array_equal(keys(d["pts"], rl), d["root_keys"][:, :3])
+    assert np.array_equal(keys(d["pts"], rl / (1 << L)), d["leaf_keys"][:, :3])
+    m = Map(rl, L)
+    m.accumulate_points(d["pts"])
+    sk = [tuple(k[:3]) for k in d["stat_keys"]]
+    assert set(sk) == set(m.leaves)
+    for i, k in enumerate(sk):
+        leaf = m.leaves[k]
+        assert leaf[0] == d["stat_count"][i]
+        assert np.allclose(leaf[1], d["stat_sum"][i], rtol=1e-12, atol=1e-12)
+        assert np.allclose(leaf[2], d["stat_outer"][i], rtol=1e-12, atol=1e-12)
+    rng = np.random.default_rng(11)
+    rng.uniform(-3, 3, size=(4000, 3)); rng.normal(scale=0.05, size=(1000, 3))
+    for p in rng.uniform(-2, 2, size=(600, 3)):
+        m.try_insert(p)
+    it = m.iter_keys()
+    assert np.array_equal(np.array(it), d["iter_keys"][:, :3])
+    assert np.array_equal(np.array([m.leaves[k][3] for k in it]), d["iter_has_g"])
+    assert m.leaf_keys_under_roots(d["fov_roots"]) == {tuple(k[:3]) for k in d["fov_keys"]}
