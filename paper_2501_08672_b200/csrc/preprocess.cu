@@ -192,7 +192,7 @@ __device__ unsigned long long warp_lookback(unsigned long long* flags, int blk, 
         const int idx = j - lane;
         unsigned long long v;
         do {
-            v = idx >= 0 ? *((volatile unsigned long long*)&flags[idx]) : ST_INC;
+            v = idx >= 0 ? *((volatile unsigned long long*)&flags[idx]) : (2ull << 62);   // before block 0: inclusive 0
         } while (!__all_sync(0xffffffffu, (v & ~VAL_MASK) != 0));
         const unsigned inc = __ballot_sync(0xffffffffu, (v & ~VAL_MASK) == ST_INC);
         const int first = inc ? __ffs(inc) - 1 : 31;      // nearest predecessor with an inclusive prefix
