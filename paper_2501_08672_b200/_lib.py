@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "libsplat_b200.so")
+# LSB_SO selects a tuning variant built next to the default library
+SO_PATH = os.environ.get("LSB_SO") or os.path.join(HERE, "libsplat_b200.so")
 
 LSB_OK, LSB_EINVAL, LSB_ECAPACITY, LSB_ECUDA, LSB_EMISSING_CACHE = range(5)
 

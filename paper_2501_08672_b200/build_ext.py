@@ -19,15 +19,19 @@ EXTRA = {"preprocess.cu": ["--fmad=false"]}
 SOURCES = ["preprocess.cu", "blend.cu", "chain.cu", "loss.cu", "adam.cu", "pose.cu", "voxmap.cu", "api.cu"]
 
 
-def build(verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, defines=(), out: str = OUT, tag: str = "") -> str:
+    """Compile every source for sm_100a and link `out`.  `defines` (e.g.
+    ["FWD_MIN_BLOCKS=7"]) and `tag` build tuning variants side by side."""
+    bdir = BUILD + (("_" + tag) if tag else "")
+    os.makedirs(bdir, exist_ok=True)
     objs = []
+    dflags = [f"-D{d}" for d in defines]
     for src in SOURCES:
-        obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+        obj = os.path.join(bdir, src.replace(".cu", ".o"))
         srcp = os.path.join(CSRC, src)
         deps = [srcp, os.path.join(CSRC, "common.cuh"), os.path.join(ROOT, "include", "lsb.h")]
         if not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(d) for d in deps):
-            cmd = [NVCC, *ARCH, *COMMON, *EXTRA.get(src, []), "-c", srcp, "-o", obj]
+            cmd = [NVCC, *ARCH, *COMMON, *dflags, *EXTRA.get(src, []), "-c", srcp, "-o", obj]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode != 0:
                 sys.stderr.write(r.stdout + r.stderr)
@@ -35,12 +39,12 @@ def build(verbose: bool = False) -> str:
             if verbose:
                 sys.stderr.write(r.stderr)
         objs.append(obj)
-    cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc link failed")
-    return OUT
+    return out
 
 
 if __name__ == "__main__":

@@ -30,6 +30,12 @@ namespace lsb {
 
 constexpr int WPB = 4;       // tile-warps per CTA
 constexpr int RUN = 4;       // pixels per lane and row (horizontal run)
+#ifndef FWD_MIN_BLOCKS
+#define FWD_MIN_BLOCKS 8     // <= 64 registers: 32 resident warps per SM
+#endif
+#ifndef BWD_MIN_BLOCKS
+#define BWD_MIN_BLOCKS 5
+#endif
 
 struct BlendArgs {
     int W, H;
@@ -61,7 +67,7 @@ __device__ __forceinline__ void stage(const Ws& w, int j, int ox, int oy, Staged
 }
 
 template <bool DEPTH, bool CUT>
-__global__ void __launch_bounds__(32 * WPB)
+__global__ void __launch_bounds__(32 * WPB, FWD_MIN_BLOCKS)
 k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __restrict__ t_final,
             int32_t* __restrict__ n_contrib, float* __restrict__ depth) {
     __shared__ Staged s_rec[WPB][32];
@@ -241,7 +247,7 @@ __device__ __forceinline__ float reduce8(const float* v, int lane) {
     return c;
 }
 
-__global__ void __launch_bounds__(32 * WPB)
+__global__ void __launch_bounds__(32 * WPB, BWD_MIN_BLOCKS)
 k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const int32_t* __restrict__ n_contrib,
             const float* __restrict__ gimg, float gscale) {
     __shared__ Staged s_rec[WPB][32];
