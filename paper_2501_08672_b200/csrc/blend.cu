@@ -4,9 +4,11 @@
 // read feeds eight pixel updates and the per-row terms (dy, E dy^2,
 // s dy - mx) are computed once per row.
 //
-// The warp stages 32 records at a time into its own shared-memory slice (one
-// 64 B record per lane, 16 B vector loads) and walks them in depth order;
-// every lane reads the same record (broadcast, conflict-free).  Each pixel
+// The warp streams its tile's records through a double-buffered
+// shared-memory slice: while it blends batch b (32 records, depth order,
+// every lane reading the same record — broadcast, conflict-free), the copy
+// engine path (cp.async, 4 x 16 B per record, no registers) is already
+// fetching batch b+1, and the slot indices of batch b+2 are in flight.  Each pixel
 // applies the reference's per-pixel bbox membership test (exact CSR
 // semantics, _kernels.py:21-59) before it counts or blends an entry.
 //
@@ -31,10 +33,10 @@ namespace lsb {
 constexpr int WPB = 4;       // tile-warps per CTA
 constexpr int RUN = 4;       // pixels per lane and row (horizontal run)
 #ifndef FWD_MIN_BLOCKS
-#define FWD_MIN_BLOCKS 8     // <= 64 registers: 32 resident warps per SM
+#define FWD_MIN_BLOCKS 6
 #endif
 #ifndef BWD_MIN_BLOCKS
-#define BWD_MIN_BLOCKS 5
+#define BWD_MIN_BLOCKS 4
 #endif
 
 struct BlendArgs {
@@ -53,27 +55,56 @@ struct LossArgs {
     float gscale;
 };
 
-struct Staged {              // one record as the blend reads it (48 B)
-    float4 a;                // mx_local, my_local, A, s
-    float4 b;                // E, op, c0, c1
-    float4 c;                // c2, z, bbx bits, bby bits
-};
-
-__device__ __forceinline__ void stage(const Ws& w, int j, int ox, int oy, Staged& st) {
-    const Rec r = w.rec[w.tile_slot[j]];
-    st.a = make_float4((float)(r.mx - (double)ox), (float)(r.my - (double)oy), r.A, r.s);
-    st.b = make_float4(r.E, r.op, r.c0, r.c1);
-    st.c = make_float4(r.c2, r.z, __int_as_float(r.bbx), __int_as_float(r.bby));
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// Per-warp record pipeline over one tile list [start, end).
+struct RecPipe {
+    Rec* buf;           // [2][32] in shared memory
+    int start, end, slot_next;
+    __device__ __forceinline__ void fetch(const Ws& w, int batch, int slot, int lane) {
+        if (slot >= 0) {
+            const float4* src = (const float4*)(w.rec + slot);
+            float4* dst = (float4*)(buf + (batch & 1) * 32 + lane);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cp_async16(dst + q, src + q);
+        }
+        cp_commit();
+    }
+    __device__ __forceinline__ int slot_at(const Ws& w, int j) const { return j < end ? w.tile_slot[j] : -1; }
+    // prologue: batch 0 in flight, slots of batch 1 loaded
+    __device__ __forceinline__ void begin(const Ws& w, int lane) {
+        fetch(w, 0, slot_at(w, start + lane), lane);
+        slot_next = slot_at(w, start + 32 + lane);
+    }
+    // start fetching batch b+1, then wait for batch b; returns its records
+    __device__ __forceinline__ const Rec* next(const Ws& w, int b, int lane) {
+        fetch(w, b + 1, slot_next, lane);
+        slot_next = slot_at(w, start + 32 * (b + 2) + lane);
+        cp_wait<1>();
+        __syncwarp();
+        return buf + (b & 1) * 32;
+    }
+    __device__ __forceinline__ void drain() {
+        cp_wait<0>();
+        __syncwarp();
+    }
+};
 
 template <bool DEPTH, bool CUT>
 __global__ void __launch_bounds__(32 * WPB, FWD_MIN_BLOCKS)
 k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __restrict__ t_final,
             int32_t* __restrict__ n_contrib, float* __restrict__ depth) {
-    __shared__ Staged s_rec[WPB][32];
+    __shared__ Rec s_rec[WPB][2 * 32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int qx = (lane & 3) * RUN, r0 = lane >> 2;      // rows r0 and r0 + 8
-    Staged* sr = s_rec[wib];
+    RecPipe pipe;
+    pipe.buf = s_rec[wib];
     const float fx0 = (float)qx;
     const float fy[2] = {(float)r0, (float)(r0 + 8)};
     // persistent tile-warp: pull tiles from the queue until it is empty
@@ -99,27 +130,33 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
             }
         int last = 0;
         const int start = w.tile_start[tile], end = w.tile_start[tile + 1];
-        for (int base = start; base < end; base += 32) {
+        const float oxf = (float)ox, oyf = (float)oy;
+        pipe.start = start;
+        pipe.end = end;
+        pipe.begin(w, lane);
+        for (int b = 0, base = start; base < end; ++b, base += 32) {
             bool alive = false;
 #pragma unroll
             for (int h = 0; h < 2; ++h)
 #pragma unroll
                 for (int j = 0; j < RUN; ++j) alive |= T[h][j] >= a.tmin;
             if (!__any_sync(0xffffffffu, alive)) break;
-            if (base + lane < end) stage(w, base + lane, ox, oy, sr[lane]);
-            __syncwarp();
+            const Rec* sr = pipe.next(w, b, lane);
             const int nb = min(32, end - base);
             for (int k = 0; k < nb; ++k) {
-                const float4 qc = sr[k].c;
-                const int bby = __float_as_int(qc.w), bbx = __float_as_int(qc.z);
+                const int4 qi = *(const int4*)&sr[k].bbx;
+                const int bby = qi.y, bbx = qi.x;
                 const int y0 = (bby & 0xffff) - oy, y1 = (bby >> 16) - oy;
                 const int lo = max((bbx & 0xffff) - gx0, 0), hi = min((bbx >> 16) - gx0, RUN);
                 if (lo >= hi) continue;
                 bool inx[RUN];                                       // bbox columns of this run
 #pragma unroll
                 for (int j = 0; j < RUN; ++j) inx[j] = j >= lo && j < hi;
-                const float4 qa = sr[k].a, qb = sr[k].b;
-                const float lop = __log2f(qb.y);
+                const float4 q0 = *(const float4*)&sr[k].mxh;        // mxh myh mxl myl
+                const float4 qa = make_float4((q0.x - oxf) + q0.z, (q0.y - oyf) + q0.w, sr[k].A, sr[k].s);
+                const float4 qb = *(const float4*)&sr[k].A;          // A s E op
+                const float4 qc = *(const float4*)&sr[k].c0;         // c0 c1 c2 z
+                const float lop = __log2f(qb.w);
                 bool used = false;
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -128,7 +165,7 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
                     const float dy = fy[h] - qa.y;
                     const float u0 = fmaf(qa.w, dy, fx0 - qa.x);      // u = x_local + s dy - mx
                     // log2(alpha) = A u^2 + E dy^2 + log2(op): opacity folded into the exponent
-                    const float edy = fmaf(qb.x * dy, dy, lop);
+                    const float edy = fmaf(qb.z * dy, dy, lop);
 #pragma unroll
                     for (int j = 0; j < RUN; ++j) {
                         const bool in = inx[j] && T[h][j] >= a.tmin;
@@ -139,10 +176,10 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
                         const bool take = CUT ? (in && al >= a.cut) : in;
                         al = take ? al : 0.f;
                         const float wt = T[h][j] * al;
-                        cr[h][j] = fmaf(wt, qb.z, cr[h][j]);
-                        cg[h][j] = fmaf(wt, qb.w, cg[h][j]);
-                        cb[h][j] = fmaf(wt, qc.x, cb[h][j]);
-                        if (DEPTH) dz[h][j] = fmaf(wt, qc.y, dz[h][j]);
+                        cr[h][j] = fmaf(wt, qc.x, cr[h][j]);
+                        cg[h][j] = fmaf(wt, qc.y, cg[h][j]);
+                        cb[h][j] = fmaf(wt, qc.z, cb[h][j]);
+                        if (DEPTH) dz[h][j] = fmaf(wt, qc.w, dz[h][j]);
                         T[h][j] = fmaf(-al, T[h][j], T[h][j]);
                     }
                 }
@@ -150,6 +187,7 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
             }
             __syncwarp();
         }
+        pipe.drain();
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
         if (lane == 0) w.tile_last[tile] = max(last, start);
@@ -250,13 +288,12 @@ __device__ __forceinline__ float reduce8(const float* v, int lane) {
 __global__ void __launch_bounds__(32 * WPB, BWD_MIN_BLOCKS)
 k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const int32_t* __restrict__ n_contrib,
             const float* __restrict__ gimg, float gscale) {
-    __shared__ Staged s_rec[WPB][32];
-    __shared__ float2 s_ke[WPB][32];
+    __shared__ Rec s_rec[WPB][2 * 32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int qx = (lane & 3) * RUN, r0 = lane >> 2;
     const float k2 = -2.0f / (float)LOG2E;     // undo the exp2 scaling: a_k = A k2, e = E k2
-    Staged* sr = s_rec[wib];
-    float2* ske = s_ke[wib];
+    RecPipe pipe;
+    pipe.buf = s_rec[wib];
     const float fx0 = (float)qx;
     const float fy[2] = {(float)r0, (float)(r0 + 8)};
     for (;;) {
@@ -287,29 +324,35 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const int32_t* _
                 }
             }
         const int start = w.tile_start[tile], end = w.tile_last[tile];
-        for (int base = start; base < end; base += 32) {
+        const float oxf = (float)ox, oyf = (float)oy;
+        pipe.start = start;
+        pipe.end = end;
+        pipe.begin(w, lane);
+        for (int b = 0, base = start; base < end; ++b, base += 32) {
             bool alive = false;
 #pragma unroll
             for (int h = 0; h < 2; ++h)
 #pragma unroll
                 for (int j = 0; j < RUN; ++j) alive |= rem[h][j] > 0;
             if (!__any_sync(0xffffffffu, alive)) break;
-            if (base + lane < end) {
-                stage(w, base + lane, ox, oy, sr[lane]);
-                ske[lane] = make_float2(sr[lane].a.z * k2, sr[lane].b.x * k2);
-            }
-            __syncwarp();
+            const Rec* sr = pipe.next(w, b, lane);
             const int nb = min(32, end - base);
             for (int k = 0; k < nb; ++k) {
-                const float4 qc = sr[k].c;
-                const int bby = __float_as_int(qc.w), bbx = __float_as_int(qc.z);
+                const float4 q0 = *(const float4*)&sr[k].mxh;        // mxh myh mxl myl
+                const float4 q1 = *(const float4*)&sr[k].A;          // A s E op
+                const float4 q2 = *(const float4*)&sr[k].c0;         // c0 c1 c2 z
+                const int4 q3 = *(const int4*)&sr[k].bbx;            // bbx bby id ebase
+                // record in the (mx, my, A, s) (E, op, c0, c1) (c2, z) layout the math below uses
+                const float4 qa = make_float4((q0.x - oxf) + q0.z, (q0.y - oyf) + q0.w, q1.x, q1.y);
+                const float4 qb = make_float4(q1.z, q1.w, q2.x, q2.y);
+                const float4 qc = make_float4(q2.z, q2.w, 0.f, 0.f);
+                const float2 qd = make_float2(q1.x * k2, q1.z * k2);
+                const int bby = q3.y, bbx = q3.x;
                 const int y0 = (bby & 0xffff) - oy, y1 = (bby >> 16) - oy;
                 const int lo = max((bbx & 0xffff) - gx0, 0), hi = min((bbx >> 16) - gx0, RUN);
                 bool inx[RUN];
 #pragma unroll
                 for (int j = 0; j < RUN; ++j) inx[j] = j >= lo && j < hi;
-                const float4 qa = sr[k].a, qb = sr[k].b;
-                const float2 qd = ske[k];
                 // accumulators: colour (3), sum gd, sum gd v0, sum gd v1, sum gd v0^2,
                 // sum gd v0 v1, sum gd v1^2 with gd = G dalpha and v = conic d
                 // (op is factored out and applied once per record below)
@@ -376,6 +419,7 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const int32_t* _
             }
             __syncwarp();
         }
+        pipe.drain();
         // intersections the walk never reached contribute nothing
         const int fin = w.tile_start[tile + 1];
         for (int j = max(end, start); j < fin; ++j)

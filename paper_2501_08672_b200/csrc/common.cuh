@@ -17,13 +17,15 @@ constexpr int CHAIN_THREADS = 64;
 constexpr double LOG2E = 1.4426950408889634;
 
 // One visible splat, 64 B, written once by preprocess and read by every tile
-// that the splat's bbox touches (4 x 16 B vector loads).
+// that the splat's bbox touches; the blend copies it to shared memory as is
+// (cp.async, 4 x 16 B).  mu_i is kept as an f32 hi/lo pair so a tile can form
+// its local coordinate (hi - origin) + lo without f64 arithmetic.
 struct __align__(16) Rec {
-    double mx, my;      // mu_i (f64: the blend subtracts the tile origin in f64)
-    float A, s, E, op;  // exponent: log2 g = A*u^2 + E*dy^2, u = dx + s*dy
-    float c0, c1, c2, z;  // clamped RGB and camera depth
-    int32_t bbx, bby;   // x0 | x1 << 16, y0 | y1 << 16 (half-open pixel bbox)
-    int32_t id, ebase;  // Gaussian id, first intersection index
+    float mxh, myh, mxl, myl;   // mu_i = hi + lo (lo = f32(mu_i - hi))
+    float A, s, E, op;          // exponent: log2 g = A*u^2 + E*dy^2, u = dx + s*dy
+    float c0, c1, c2, z;        // clamped RGB and camera depth
+    int32_t bbx, bby;           // x0 | x1 << 16, y0 | y1 << 16 (half-open pixel bbox)
+    int32_t id, ebase;          // Gaussian id, first intersection index
 };
 static_assert(sizeof(Rec) == 64, "Rec must be 64 bytes");
 

@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(128) k_pose_rows(Ws w, RowArgs a, const float*
         float G = 0.f, al = 0.f, u = 0.f, dy = 0.f;
         bool contrib = false;
         if (active) {
-            const float mxl = (float)(rc.mx - (double)ox), myl = (float)(rc.my - (double)oy);
+            const float mxl = (rc.mxh - (float)ox) + rc.mxl, myl = (rc.myh - (float)oy) + rc.myl;
             dy = fy - myl;
             u = fmaf(rc.s, dy, fx - mxl);
             G = ex2_approx(fmaf(rc.A, u * u, rc.E * dy * dy));

@@ -129,8 +129,10 @@ __device__ bool splat_one(const PreArgs& a, int64_t i, Rec& r, int& ntiles, uint
     // conic = cov_i^-1 = (cc, -cb, ca) / det; exponent in the shear form
     //   q = a_k u^2 + dy^2 / cc,  u = dx - (cb/cc) dy   (no cancellation)
     const double ak = cc / det;
-    r.mx = mux;
-    r.my = muy;
+    r.mxh = (float)mux;
+    r.myh = (float)muy;
+    r.mxl = (float)(mux - (double)r.mxh);
+    r.myl = (float)(muy - (double)r.myh);
     r.A = (float)(-0.5 * LOG2E * ak);
     r.s = (float)(-cb / cc);
     r.E = (float)(-0.5 * LOG2E / cc);
