@@ -204,7 +204,7 @@ def run_ours(args, wl, rank, world, local_rank):
     del gt
     stream = torch.cuda.Stream(dev)
     eng = WindowEngine(win, wl["cam"], [wl["views"][v] for v in my_views], settings, OptimConfig(),
-                       n_views_total=V, stream=stream)
+                       n_views_total=V, stream=stream, lanes=args.lanes)
     counts = []
     for v in range(len(my_views)):      # per-view M, I for the byte model
         T = eng.views[v]
@@ -292,6 +292,7 @@ def run_ours(args, wl, rank, world, local_rank):
             "visible_splats_per_s": float(sum(c[0] for c in counts)) * world / (ms * 1e-3),
             "config": {"workload": args.config, "gaussians": N, "views": V, "width": W, "height": H,
                        "alpha_cut": wl["alpha_cut"], "parallelism": f"view-sharded dp{world}",
+                       "view_lanes": args.lanes,
                        "l2": "working set > L2: observed views alone are V x 15.7 MB",
                        "loss_last_step": float(np.mean(losses))},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "peak_source": hbm_src,
@@ -413,6 +414,7 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS) + ["cfg3"])
     ap.add_argument("--alpha-cut", type=float, default=1.0 / 255.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--lanes", type=int, default=2, help="concurrent view pipelines per GPU")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

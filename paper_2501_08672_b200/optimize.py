@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes
 from dataclasses import dataclass, field
+from types import SimpleNamespace
 from typing import Optional, Sequence
 
 import numpy as np
@@ -165,7 +166,7 @@ class WindowEngine:
 
     def __init__(self, arrays: GaussianArrays, cam, views: Sequence, settings: RasterSettings,
                  cfg: OptimConfig = OptimConfig(), n_views_total: Optional[int] = None,
-                 isect_cap: Optional[int] = None, stream=None, master: str = "f64"):
+                 isect_cap: Optional[int] = None, stream=None, master: str = "f64", lanes: int = 1):
         _lib.require()
         self.arena = arrays
         if master == "f64" and arrays.dtype != torch.float64:
@@ -182,17 +183,30 @@ class WindowEngine:
         dev = arrays.device
         h, w = int(cam.height), int(cam.width)
         self.h, self.w = h, w
-        self.image = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
-        self.t_final = torch.empty((h, w), dtype=torch.float32, device=dev)
-        self.n_contrib = torch.empty((h, w), dtype=torch.int32, device=dev)
-        self.grad_image = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
         self.loss = LossBuffers(dev, max(1, len(self.views)))
         self.grads = ParamGradients.zeros(len(arrays), int(arrays.shs.shape[1]), dev)
         self.adam = AdamState(arrays, cfg)
         if isect_cap is None:
             isect_cap = self.calibrate()
         T0 = self.views[0] if self.views else _identity()
-        self.state = RenderState(arrays, cam, T0.R, T0.t, settings, isect_cap)
+        # `lanes` view pipelines, each with its own stream, workspace and image
+        # buffers: view v runs on lane v % lanes, so one view's latency-bound
+        # kernels (binning, chain) overlap the next view's blend.  The chain
+        # kernels, which accumulate into the shared gradient buffer, stay
+        # serialised in view order through events.
+        self.n_lanes = max(1, min(lanes, len(self.views) or 1))
+        self.lanes = []
+        for _ in range(self.n_lanes):
+            self.lanes.append(SimpleNamespace(
+                stream=torch.cuda.Stream(dev) if self.n_lanes > 1 else stream,
+                state=RenderState(arrays, cam, T0.R, T0.t, settings, isect_cap),
+                image=torch.empty((h, w, 3), dtype=torch.float32, device=dev),
+                t_final=torch.empty((h, w), dtype=torch.float32, device=dev),
+                n_contrib=torch.empty((h, w), dtype=torch.int32, device=dev),
+                grad_image=torch.empty((h, w, 3), dtype=torch.float32, device=dev)))
+        self.state = self.lanes[0].state
+        self.image, self.t_final, self.n_contrib = self.lanes[0].image, self.lanes[0].t_final, self.lanes[0].n_contrib
+        self.grad_image = self.lanes[0].grad_image
 
     def calibrate(self, headroom: float = 1.3) -> int:
         """Measure the largest per-view intersection count (one sync per view)."""
@@ -211,36 +225,54 @@ class WindowEngine:
         return int(worst * headroom) + 1024
 
     def check_capacity(self) -> bool:
-        """True if the last render in the workspace fit (syncs)."""
-        return not self.state.read_counts(self.stream)[2]
+        """True if the last render in every lane's workspace fit (syncs)."""
+        return all(not ln.state.read_counts(ln.stream)[2] for ln in self.lanes)
 
     def step(self, observed: Sequence[torch.Tensor], allreduce=None, timers: Optional[dict] = None) -> None:
         """One optimisation step over this rank's views (async)."""
-        st = self.state
         gscale = 1.0 / (3.0 * self.h * self.w * self.n_total)
-        self.grads.flat.zero_()
+        main = self.stream if self.stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(main):
+            self.grads.flat.zero_()
+        ready = torch.cuda.Event()
+        ready.record(main)
 
-        def mark(name, start):
-            # timers[name] collects (start, end) event pairs on this stream
+        def mark(name, stream):
+            # timers[name] collects (start, end) event pairs on the launching stream
             if timers is not None:
                 ev = torch.cuda.Event(enable_timing=True)
-                ev.record(self.stream)
+                ev.record(stream)
                 timers.setdefault(name, []).append(ev)
 
+        prev_chain = None
         for v, T in enumerate(self.views):
+            ln = self.lanes[v % self.n_lanes]
+            st, sm = ln.state, (ln.stream if ln.stream is not None else main)
+            if sm is not main:
+                sm.wait_event(ready)
             st.set_pose(T.R, T.t)
-            mark("bin", True); render_bin(st, self.stream); mark("bin", False)
-            mark("blend_fwd", True)
-            render_blend_loss(st, self.image, self.t_final, self.n_contrib, observed[v], _KIND[self.cfg.loss],
-                              gscale, self.grad_image, self.loss.ptr(v), stream=self.stream)
-            mark("blend_fwd", False)
-            mark("blend_bwd", True)
-            render_blend_bwd(st, self.image, self.n_contrib, self.grad_image, 1.0, self.stream)
-            mark("blend_bwd", False)
-            mark("chain", True); render_chain(st, self.grads, None, self.stream); mark("chain", False)
-        if allreduce is not None:
-            allreduce(self.grads.flat)
-        mark("adam", True); self.adam.apply(self.arrays, self.grads, self.stream); mark("adam", False)
+            mark("bin", sm); render_bin(st, sm); mark("bin", sm)
+            mark("blend_fwd", sm)
+            render_blend_loss(st, ln.image, ln.t_final, ln.n_contrib, observed[v], _KIND[self.cfg.loss],
+                              gscale, ln.grad_image, self.loss.ptr(v), stream=sm)
+            mark("blend_fwd", sm)
+            mark("blend_bwd", sm)
+            render_blend_bwd(st, ln.image, ln.n_contrib, ln.grad_image, 1.0, sm)
+            mark("blend_bwd", sm)
+            if prev_chain is not None and sm is not main:
+                sm.wait_event(prev_chain)
+            mark("chain", sm); render_chain(st, self.grads, None, sm); mark("chain", sm)
+            prev_chain = torch.cuda.Event()
+            prev_chain.record(sm)
+        for ln in self.lanes:
+            if ln.stream is not None and ln.stream is not main:
+                done = torch.cuda.Event()
+                done.record(ln.stream)
+                main.wait_event(done)
+        with torch.cuda.stream(main):
+            if allreduce is not None:
+                allreduce(self.grads.flat)
+            mark("adam", main); self.adam.apply(self.arrays, self.grads, main); mark("adam", main)
 
     def finish(self) -> None:
         """End of the window optimisation: re-orthonormalise stepped rotations
