@@ -20,7 +20,8 @@ import torch
 
 from . import _lib
 from .errors import TooFewPixels
-from .geometry import SE3
+from .errors import SingularGain
+from .geometry import SE3, so3_exp, so3_left_jacobian, so3_log, so3_right_jacobian_inv
 from .raster import RasterSettings, _f32, pose_rows, render
 
 DIM = 15
@@ -40,7 +41,28 @@ class FilterConfig:
 
 @dataclass
 class NavState:
+    """Filter state (estimator.py:45-83): pose, velocity, biases; 15-dim
+    error state (d_rho, d_tau, d_v, d_bg, d_ba) with the boxplus retraction."""
+
     T_WI: SE3 = field(default_factory=SE3.identity)
+    velocity: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    bias_gyro: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    bias_accel: np.ndarray = field(default_factory=lambda: np.zeros(3))
+
+    def clone(self) -> "NavState":
+        return NavState(SE3(self.T_WI.R.copy(), self.T_WI.t.copy()), np.array(self.velocity, float).copy(),
+                        np.array(self.bias_gyro, float).copy(), np.array(self.bias_accel, float).copy())
+
+    def boxplus(self, xi, bias_limit: float = 0.5) -> "NavState":
+        xi = np.asarray(xi, dtype=float)
+        return NavState(SE3(self.T_WI.R @ so3_exp(xi[0:3]), self.T_WI.t + xi[3:6]), self.velocity + xi[6:9],
+                        np.clip(self.bias_gyro + xi[9:12], -bias_limit, bias_limit),
+                        np.clip(self.bias_accel + xi[12:15], -bias_limit, bias_limit))
+
+    def boxminus(self, other: "NavState") -> np.ndarray:
+        return np.concatenate([so3_log(other.T_WI.R.T @ self.T_WI.R), self.T_WI.t - other.T_WI.t,
+                               self.velocity - other.velocity, self.bias_gyro - other.bias_gyro,
+                               self.bias_accel - other.bias_accel])
 
 
 @dataclass
@@ -114,3 +136,43 @@ def visual_measurement(state, observed, window, cam, T_ic, cfg: FilterConfig,
     H[:, :6] = -rows_h
     return Measurement(z=res.cpu().numpy(), H=H, R_diag=np.full(n_ok, cfg.photo_sigma ** 2), rows_dev=rows,
                        z_dev=res)
+
+
+def ieskf_visual_update(state: NavState, cov: np.ndarray, observed, window, cam, T_ic, cfg: FilterConfig,
+                        settings: RasterSettings, max_iter: int = 5, step_tol: float = 1e-6,
+                        bias_limit: float = 0.5):
+    """Iterated EKF update with the photometric measurement (estimator.py:
+    292-331).  Each iteration re-renders the window at the running estimate
+    and reduces the pose block of H^T R^-1 H and H^T R^-1 z on the GPU
+    (Measurement.hb); only the 15x15 filter algebra runs on the host, using
+    K z = S^-1 b and K H = S^-1 A (H is zero outside its 6 pose columns)."""
+    x_bar, x_hat = state, state.clone()
+    K_H = P = None
+    for _ in range(max_iter):
+        meas = visual_measurement(x_hat, observed, window, cam, T_ic, cfg, settings)
+        A6, b6 = meas.hb()
+        delta = x_hat.boxminus(x_bar)
+        Hj_inv = np.eye(DIM)
+        Hj_inv[0:3, 0:3] = so3_left_jacobian(-delta[0:3])
+        P = Hj_inv @ cov @ Hj_inv.T
+        A = np.zeros((DIM, DIM))
+        A[:6, :6] = A6
+        b = np.zeros(DIM)
+        b[:6] = b6
+        try:
+            S = A + np.linalg.inv(P)
+            S_inv = np.linalg.inv(S)
+        except np.linalg.LinAlgError as exc:
+            raise SingularGain(str(exc)) from exc
+        K_H = S_inv @ A
+        Kz = S_inv @ b
+        if not np.all(np.isfinite(K_H)):
+            raise SingularGain("non-finite gain")
+        xi = -Kz - (np.eye(DIM) - K_H) @ (Hj_inv @ delta)
+        x_hat = x_hat.boxplus(xi, bias_limit=bias_limit)
+        if np.linalg.norm(xi) < step_tol:
+            break
+    if K_H is None:
+        return state.clone(), cov.copy()
+    cov_post = (np.eye(DIM) - K_H) @ P
+    return x_hat, 0.5 * (cov_post + cov_post.T)

@@ -102,3 +102,42 @@ class PinholeCamera:
             raise ValueError("focal lengths must be positive")
         if not (0 <= self.cx < self.width and 0 <= self.cy < self.height):
             raise ValueError("principal point outside image")
+
+
+def so3_log(R) -> np.ndarray:
+    """Inverse of so3_exp, theta in [0, pi] (geometry.py:56-79)."""
+    R = np.asarray(R, dtype=float)
+    cos_theta = np.clip(0.5 * (float(np.trace(R)) - 1.0), -1.0, 1.0)
+    theta = float(np.arccos(cos_theta))
+    w = np.array([R[2, 1] - R[1, 2], R[0, 2] - R[2, 0], R[1, 0] - R[0, 1]])
+    if theta < 1e-8:
+        return 0.5 * w
+    if np.pi - theta > 1e-6:
+        return (theta / (2.0 * np.sin(theta))) * w
+    B = 0.5 * (R + np.eye(3))
+    k = int(np.argmax(np.diag(B)))
+    axis = B[:, k] / np.sqrt(max(B[k, k], 1e-12))
+    axis = axis / np.linalg.norm(axis)
+    if np.dot(w, axis) < 0.0:
+        axis = -axis
+    return theta * axis
+
+
+def so3_left_jacobian(phi) -> np.ndarray:
+    phi = np.asarray(phi, dtype=float)
+    theta = float(np.linalg.norm(phi))
+    S = hat(phi)
+    if theta < 1e-6:
+        return np.eye(3) + 0.5 * S + (S @ S) / 6.0
+    return np.eye(3) + ((1.0 - np.cos(theta)) / theta**2) * S + ((theta - np.sin(theta)) / theta**3) * (S @ S)
+
+
+def so3_right_jacobian_inv(phi) -> np.ndarray:
+    """J_r^-1(phi) = J_l^-1(-phi) (geometry.py:96-107)."""
+    phi = -np.asarray(phi, dtype=float)
+    theta = float(np.linalg.norm(phi))
+    S = hat(phi)
+    if theta < 1e-6:
+        return np.eye(3) - 0.5 * S + (S @ S) / 12.0
+    b = (1.0 / theta**2) - 0.5 / (theta * np.tan(0.5 * theta))
+    return np.eye(3) - 0.5 * S + b * (S @ S)

@@ -55,3 +55,16 @@ def test_too_few_pixels_raises():
     with pytest.raises(TooFewPixels):
         visual_measurement(NavState(T_wi), np.zeros_like(d["observed"]), arrays, cam, T_ic,
                            FilterConfig(min_pixels=10 ** 6), RasterSettings(alpha_cut=1 / 255))
+
+
+def test_ieskf_visual_update_matches_reference():
+    """Three IESKF iterations with the photometric measurement: posterior pose
+    and covariance vs the reference's ieskf_update (estimator.py:292-331)."""
+    from paper_2501_08672_b200.estimator import FilterConfig, NavState, ieskf_visual_update
+    from paper_2501_08672_b200.raster import RasterSettings
+    d, arrays, cam, T_wi, T_ic = _setup()
+    post, cov = ieskf_visual_update(NavState(T_wi), d["cov0"], d["observed"], arrays, cam, T_ic, FilterConfig(),
+                                    RasterSettings(alpha_cut=1 / 255), max_iter=3)
+    assert np.abs(post.T_WI.t - d["post_t"]).max() <= 1e-6
+    assert np.abs(post.T_WI.R - d["post_R"]).max() <= 1e-6
+    assert np.abs(cov - d["post_cov"]).max() <= 1e-3 * np.abs(d["post_cov"]).max()

@@ -230,7 +230,12 @@ def main():
     meas = visual_measurement(prior, observed, _Src(), cam, T_IC, fcfg, RasterSettings(alpha_cut=1 / 255))
     out = render(arrays, prior.T_WI @ T_IC, cam, RasterSettings(alpha_cut=1 / 255))
     ids = select_semi_dense_pixels(observed, out.final_transmittance, fcfg)
+    from livsplat.estimator import ieskf_update, initial_covariance
+    cov0 = initial_covariance()
+    post, cov_post = ieskf_update(prior, cov0, lambda s: visual_measurement(
+        s, observed, _Src(), cam, T_IC, fcfg, RasterSettings(alpha_cut=1 / 255)), max_iter=3)
     np.savez_compressed(os.path.join(OUT, "visual_room.npz"), observed=observed,
+                        cov0=cov0, post_R=post.T_WI.R, post_t=post.T_WI.t, post_cov=cov_post,
                         R_wi=prior.T_WI.R, t_wi=prior.T_WI.t, sel_ids=ids, z=meas.z, H=meas.H,
                         R_diag=meas.R_diag, cam=np.array([cam.fx, cam.fy, cam.cx, cam.cy, W, H], dtype=float))
     print("golden fixtures written to", OUT)
