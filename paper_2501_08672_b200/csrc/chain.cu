@@ -29,12 +29,13 @@ __constant__ double c_SH2[16] = {
     2.890611442640554, -0.4570457994644658, 0.3731763325901154, -0.4570457994644658,
     1.445305721320277, -0.5900435899266435, 0.0, 0.0};
 
-__device__ void sh_basis_d(int degree, double x, double y, double z, double* b) {
+template <typename T>
+__device__ void sh_basis_d(int degree, T x, T y, T z, T* b) {
     const double* C = c_SH2;
     b[0] = C[0];
     if (degree >= 1) { b[1] = -C[1] * y; b[2] = C[1] * z; b[3] = -C[1] * x; }
     if (degree >= 2) {
-        const double xx = x * x, yy = y * y, zz = z * z;
+        const T xx = x * x, yy = y * y, zz = z * z;
         b[4] = C[2] * x * y; b[5] = C[3] * y * z; b[6] = C[4] * (2.0 * zz - xx - yy);
         b[7] = C[5] * x * z; b[8] = C[6] * (xx - yy);
         if (degree >= 3) {
@@ -48,7 +49,8 @@ __device__ void sh_basis_d(int degree, double x, double y, double z, double* b) 
 }
 
 // d basis_k / d dir (sh.py:66-109), g[k][3].
-__device__ void sh_basis_grad_d(int degree, double x, double y, double z, double (*g)[3]) {
+template <typename T>
+__device__ void sh_basis_grad_d(int degree, T x, T y, T z, T (*g)[3]) {
     const double* C = c_SH2;
     const int K = (degree + 1) * (degree + 1);
     for (int k = 0; k < K; ++k) g[k][0] = g[k][1] = g[k][2] = 0.0;
@@ -61,7 +63,7 @@ __device__ void sh_basis_grad_d(int degree, double x, double y, double z, double
         g[8][0] = C[6] * (2.0 * x); g[8][1] = C[6] * (-2.0 * y);
     }
     if (degree >= 3) {
-        const double xx = x * x, yy = y * y, zz = z * z;
+        const T xx = x * x, yy = y * y, zz = z * z;
         g[9][0] = C[7] * 6.0 * x * y; g[9][1] = C[7] * (3.0 * xx - 3.0 * yy);
         g[10][0] = C[8] * y * z; g[10][1] = C[8] * x * z; g[10][2] = C[8] * x * y;
         g[11][0] = C[9] * (-2.0 * x * y); g[11][1] = C[9] * (4.0 * zz - xx - 3.0 * yy);
@@ -106,11 +108,14 @@ __global__ void __launch_bounds__(256) k_part_reduce(Ws w) {
     }
 }
 
+using CT = float;   // chain-rule arithmetic (gradients need 1e-3 relative; f32 is ~1e-6)
+
 __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
     __shared__ double s_red[CHAIN_THREADS / 32][POSE_VALS];
     __shared__ bool s_last;
     const int64_t M = (int64_t)w.ctr[0];
-    const double* R = a.T.R;
+    CT R[9];
+    for (int k = 0; k < 9; ++k) R[k] = (CT)a.T.R[k];
     double pose[POSE_VALS];
 #pragma unroll
     for (int c = 0; c < POSE_VALS; ++c) pose[c] = 0.0;
@@ -130,13 +135,13 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
         const int f64 = a.p.dtype;
         const double px = pld(a.p.means, 3 * i, f64), py = pld(a.p.means, 3 * i + 1, f64),
                      pz = pld(a.p.means, 3 * i + 2, f64);
-        const double x = R[0] * px + R[1] * py + R[2] * pz + a.T.t[0];
-        const double y = R[3] * px + R[4] * py + R[5] * pz + a.T.t[1];
-        const double z = R[6] * px + R[7] * py + R[8] * pz + a.T.t[2];
-        const double fx = a.cam.fx, fy = a.cam.fy;
-        const double J00 = fx / z, J02 = -fx * x / (z * z);
-        const double J11 = fy / z, J12 = -fy * y / (z * z);
-        double Rg[9], S[3], B[9], Wc[9];
+        const CT x = (CT)(R[0] * px + R[1] * py + R[2] * pz + a.T.t[0]);
+        const CT y = (CT)(R[3] * px + R[4] * py + R[5] * pz + a.T.t[1]);
+        const CT z = (CT)(R[6] * px + R[7] * py + R[8] * pz + a.T.t[2]);
+        const CT fx = a.cam.fx, fy = a.cam.fy;
+        const CT J00 = fx / z, J02 = -fx * x / (z * z);
+        const CT J11 = fy / z, J12 = -fy * y / (z * z);
+        CT Rg[9], S[3], B[9], Wc[9];
         for (int k = 0; k < 9; ++k) Rg[k] = pld(a.p.rots, 9 * i + k, f64);
         for (int k = 0; k < 3; ++k) S[k] = pld(a.p.scales, 3 * i + k, f64);
         for (int r3 = 0; r3 < 3; ++r3)
@@ -145,93 +150,93 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
             for (int c3 = 0; c3 < 3; ++c3)
                 Wc[3 * r3 + c3] = B[3 * r3] * B[3 * c3] + B[3 * r3 + 1] * B[3 * c3 + 1] +
                                   B[3 * r3 + 2] * B[3 * c3 + 2];
-        double Mm[6];   // M = J R (2x3)
+        CT Mm[6];   // M = J R (2x3)
         for (int k = 0; k < 3; ++k) {
             Mm[k] = J00 * R[k] + J02 * R[6 + k];
             Mm[3 + k] = J11 * R[3 + k] + J12 * R[6 + k];
         }
         // ---- 2-D covariance chain (raster.py:286-298) ----
-        const double S00 = q[6], S01 = q[7], S11 = q[8];
-        double SM[6];   // S M (2x3)
+        const CT S00 = q[6], S01 = q[7], S11 = q[8];
+        CT SM[6];   // S M (2x3)
         for (int k = 0; k < 3; ++k) {
             SM[k] = S00 * Mm[k] + S01 * Mm[3 + k];
             SM[3 + k] = S01 * Mm[k] + S11 * Mm[3 + k];
         }
-        double dCw[9];  // M^T S M
+        CT dCw[9];  // M^T S M
         for (int r3 = 0; r3 < 3; ++r3)
             for (int c3 = 0; c3 < 3; ++c3) dCw[3 * r3 + c3] = Mm[r3] * SM[c3] + Mm[3 + r3] * SM[3 + c3];
-        double dM[6];   // 2 S M W
+        CT dM[6];   // 2 S M W
         for (int r2 = 0; r2 < 2; ++r2)
             for (int c3 = 0; c3 < 3; ++c3)
-                dM[3 * r2 + c3] = 2.0 * (SM[3 * r2] * Wc[c3] + SM[3 * r2 + 1] * Wc[3 + c3] +
+                dM[3 * r2 + c3] = 2.0f * (SM[3 * r2] * Wc[c3] + SM[3 * r2 + 1] * Wc[3 + c3] +
                                          SM[3 * r2 + 2] * Wc[6 + c3]);
-        double dJ[6];   // dM R^T
+        CT dJ[6];   // dM R^T
         for (int r2 = 0; r2 < 2; ++r2)
             for (int c3 = 0; c3 < 3; ++c3)
                 dJ[3 * r2 + c3] = dM[3 * r2] * R[3 * c3] + dM[3 * r2 + 1] * R[3 * c3 + 1] +
                                   dM[3 * r2 + 2] * R[3 * c3 + 2];
         // d_W = J^T dM (3x3), J rows (J00,0,J02), (0,J11,J12)
-        double dW[9];
+        CT dW[9];
         for (int c3 = 0; c3 < 3; ++c3) {
             dW[c3] = J00 * dM[c3];
             dW[3 + c3] = J11 * dM[3 + c3];
             dW[6 + c3] = J02 * dM[c3] + J12 * dM[3 + c3];
         }
         // ---- mean chain ----
-        const double dm0 = q[4], dm1 = q[5];
-        double dmc[3] = {J00 * dm0, J11 * dm1, J02 * dm0 + J12 * dm1};
-        const double gxx = -fx / (z * z), gyy = -fy / (z * z);
+        const CT dm0 = q[4], dm1 = q[5];
+        CT dmc[3] = {J00 * dm0, J11 * dm1, J02 * dm0 + J12 * dm1};
+        const CT gxx = -fx / (z * z), gyy = -fy / (z * z);
         dmc[0] += dJ[2] * gxx;
         dmc[1] += dJ[5] * gyy;
-        dmc[2] += dJ[0] * gxx + dJ[4] * gyy + dJ[2] * (2.0 * fx * x / (z * z * z)) +
-                  dJ[5] * (2.0 * fy * y / (z * z * z));
-        double dmean[3];
+        dmc[2] += dJ[0] * gxx + dJ[4] * gyy + dJ[2] * (2.0f * fx * x / (z * z * z)) +
+                  dJ[5] * (2.0f * fy * y / (z * z * z));
+        CT dmean[3];
         for (int k = 0; k < 3; ++k) dmean[k] = dmc[0] * R[k] + dmc[1] * R[3 + k] + dmc[2] * R[6 + k];
         // ---- covariance -> rotation tangent, scale ----
-        double dB[9];
+        CT dB[9];
         for (int r3 = 0; r3 < 3; ++r3)
             for (int c3 = 0; c3 < 3; ++c3)
-                dB[3 * r3 + c3] = 2.0 * (dCw[3 * r3] * B[c3] + dCw[3 * r3 + 1] * B[3 + c3] +
+                dB[3 * r3 + c3] = 2.0f * (dCw[3 * r3] * B[c3] + dCw[3 * r3 + 1] * B[3 + c3] +
                                          dCw[3 * r3 + 2] * B[6 + c3]);
-        double Y[9];   // Rg^T (dB * S)
+        CT Y[9];   // Rg^T (dB * S)
         for (int r3 = 0; r3 < 3; ++r3)
             for (int c3 = 0; c3 < 3; ++c3)
                 Y[3 * r3 + c3] = (Rg[r3] * dB[c3] + Rg[3 + r3] * dB[3 + c3] + Rg[6 + r3] * dB[6 + c3]) * S[c3];
-        const double drot[3] = {Y[7] - Y[5], Y[2] - Y[6], Y[3] - Y[1]};
-        double dscale[3];
+        const CT drot[3] = {Y[7] - Y[5], Y[2] - Y[6], Y[3] - Y[1]};
+        CT dscale[3];
         for (int c3 = 0; c3 < 3; ++c3)
             dscale[c3] = Rg[c3] * dB[c3] + Rg[3 + c3] * dB[3 + c3] + Rg[6 + c3] * dB[6 + c3];
         // ---- appearance ----
         const uint32_t cm = w.colmask[slot];
-        const double dcol[3] = {(cm & 1u) ? q[0] : 0.0, (cm & 2u) ? q[1] : 0.0, (cm & 4u) ? q[2] : 0.0};
+        const CT dcol[3] = {(cm & 1u) ? (CT)q[0] : 0.0f, (cm & 2u) ? (CT)q[1] : 0.0f, (cm & 4u) ? (CT)q[2] : 0.0f};
         const double* cc3 = a.T.cam_center;
-        const double dvx = px - cc3[0], dvy = py - cc3[1], dvz = pz - cc3[2];
-        const double dn = sqrt(dvx * dvx + dvy * dvy + dvz * dvz);
-        double dx_ = 0.0, dy_ = 0.0, dz_ = 1.0;
-        if (dn > 0.0) {
-            const double inv = fmax(dn, 1e-30);
+        const CT dvx = px - cc3[0], dvy = py - cc3[1], dvz = pz - cc3[2];
+        const CT dn = sqrt(dvx * dvx + dvy * dvy + dvz * dvz);
+        CT dx_ = 0.0f, dy_ = 0.0f, dz_ = 1.0f;
+        if (dn > 0.0f) {
+            const CT inv = fmax(dn, 1e-30f);
             dx_ = dvx / inv; dy_ = dvy / inv; dz_ = dvz / inv;
         }
-        double b[16];
+        CT b[16];
         sh_basis_d(a.degree, dx_, dy_, dz_, b);
         const int K = a.p.sh_coeffs;
         const int kk = (a.degree + 1) * (a.degree + 1);
         float* gsh = a.g.sh + i * K * 3;
         for (int k = 0; k < kk; ++k)
             for (int c = 0; c < 3; ++c) gsh[3 * k + c] += (float)(b[k] * dcol[c]);
-        double dpt[3] = {0.0, 0.0, 0.0};
+        CT dpt[3] = {0.0f, 0.0f, 0.0f};
         if (a.degree >= 1) {
-            double gb[16][3];
+            CT gb[16][3];
             sh_basis_grad_d(a.degree, dx_, dy_, dz_, gb);
             const int64_t sho = i * K * 3;
-            double dd[3] = {0.0, 0.0, 0.0};
+            CT dd[3] = {0.0f, 0.0f, 0.0f};
             for (int k = 0; k < kk; ++k) {
-                const double t = dcol[0] * pld(a.p.shs, sho + 3 * k, f64) + dcol[1] * pld(a.p.shs, sho + 3 * k + 1, f64) +
+                const CT t = dcol[0] * pld(a.p.shs, sho + 3 * k, f64) + dcol[1] * pld(a.p.shs, sho + 3 * k + 1, f64) +
                                  dcol[2] * pld(a.p.shs, sho + 3 * k + 2, f64);
                 dd[0] += t * gb[k][0]; dd[1] += t * gb[k][1]; dd[2] += t * gb[k][2];
             }
-            const double dot = dx_ * dd[0] + dy_ * dd[1] + dz_ * dd[2];
-            const double rr = fmax(dn, 1e-30);
+            const CT dot = dx_ * dd[0] + dy_ * dd[1] + dz_ * dd[2];
+            const CT rr = fmax(dn, 1e-30f);
             dpt[0] = (dd[0] - dx_ * dot) / rr;
             dpt[1] = (dd[1] - dy_ * dot) / rr;
             dpt[2] = (dd[2] - dz_ * dot) / rr;
@@ -245,7 +250,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
         }
         a.g.opacity[i] += (float)q[3];
         // ---- pose pieces (camera tangent) ----
-        double Z[9];   // dW R^T
+        CT Z[9];   // dW R^T
         for (int r3 = 0; r3 < 3; ++r3)
             for (int c3 = 0; c3 < 3; ++c3)
                 Z[3 * r3 + c3] = dW[3 * r3] * R[3 * c3] + dW[3 * r3 + 1] * R[3 * c3 + 1] +

@@ -203,7 +203,8 @@ class WindowEngine:
                 image=torch.empty((h, w, 3), dtype=torch.float32, device=dev),
                 t_final=torch.empty((h, w), dtype=torch.float32, device=dev),
                 n_contrib=torch.empty((h, w), dtype=torch.int32, device=dev),
-                grad_image=torch.empty((h, w, 3), dtype=torch.float32, device=dev)))
+                grad_image=torch.empty((h, w, 3), dtype=torch.float32, device=dev),
+                observed=None))
         self.state = self.lanes[0].state
         self.image, self.t_final, self.n_contrib = self.lanes[0].image, self.lanes[0].t_final, self.lanes[0].n_contrib
         self.grad_image = self.lanes[0].grad_image
@@ -229,7 +230,10 @@ class WindowEngine:
         return all(not ln.state.read_counts(ln.stream)[2] for ln in self.lanes)
 
     def step(self, observed: Sequence[torch.Tensor], allreduce=None, timers: Optional[dict] = None) -> None:
-        """One optimisation step over this rank's views (async)."""
+        """One optimisation step over this rank's views (async).  `observed`
+        are device images, or host (pinned) images: then each view's image is
+        copied on its lane's stream right before it is needed, so the H2D
+        transfer of one view overlaps the other lanes' kernels."""
         gscale = 1.0 / (3.0 * self.h * self.w * self.n_total)
         main = self.stream if self.stream is not None else torch.cuda.current_stream()
         with torch.cuda.stream(main):
@@ -251,9 +255,16 @@ class WindowEngine:
             if sm is not main:
                 sm.wait_event(ready)
             st.set_pose(T.R, T.t)
+            obs = observed[v]
+            if not obs.is_cuda:
+                if ln.observed is None:
+                    ln.observed = torch.empty((self.h, self.w, 3), dtype=torch.float32, device=self.grads.flat.device)
+                with torch.cuda.stream(sm):
+                    ln.observed.copy_(obs, non_blocking=True)
+                obs = ln.observed
             mark("bin", sm); render_bin(st, sm); mark("bin", sm)
             mark("blend_fwd", sm)
-            render_blend_loss(st, ln.image, ln.t_final, ln.n_contrib, observed[v], _KIND[self.cfg.loss],
+            render_blend_loss(st, ln.image, ln.t_final, ln.n_contrib, obs, _KIND[self.cfg.loss],
                               gscale, ln.grad_image, self.loss.ptr(v), stream=sm)
             mark("blend_fwd", sm)
             mark("blend_bwd", sm)
