@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(256) k_part_reduce(Ws w) {
     }
 }
 
-using CT = float;   // chain-rule arithmetic (gradients need 1e-3 relative; f32 is ~1e-6)
+using CT = double;  // chain-rule arithmetic: f64 keeps Adam's sign-sensitive first steps on the reference trajectory
 
 __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
     __shared__ double s_red[CHAIN_THREADS / 32][POSE_VALS];

@@ -29,4 +29,4 @@ def case_inputs(d):
 
 
 RENDER_CASES = [f"rand{s}_cut{c}" for s in range(4) for c in (0, 1)] + [
-    "room_v0_cut1", "room_v1_cut0", "room_v2_cut1"]
+    "odd_cut0", "odd_cut1", "room_v0_cut1", "room_v1_cut0", "room_v2_cut1"]

@@ -1,0 +1,84 @@
+"""Parity at BASELINE.json's full size (config 2: 203,877 Gaussians,
+1280x1024) against the CPU oracle, plus size-independent properties.
+
+The oracle needs a few seconds per view at this size on the box's cores."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GRAD_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def cfg2():
+    from types import SimpleNamespace
+    from oracle import raster as orc
+    from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
+    from paper_2501_08672_b200.scene import bake_room, camera_for, orbit_views
+    m, r, s, o, sh = bake_room(0.0723)
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)
+    P = {"means": f32(m), "rots": f32(r), "scales": f32(s), "opacities": f32(o), "shs": f32(sh)}
+    cam = camera_for(1280, 1024)
+    T_wc = orbit_views(10)[3]
+    T_cw = T_wc.inverse()
+    st = SimpleNamespace(near=0.01, dilation=0.3, alpha_clamp=0.99, transmittance_min=1e-4, footprint_sigma=6.0,
+                         alpha_cut=1 / 255, max_footprint_px=512.0, background=np.zeros(3), sh_degree=0)
+    ref = orc.render(P, T_cw.R, T_cw.t, cam, st)
+    arrays = GaussianArrays(P["means"], P["rots"], P["scales"], P["opacities"], P["shs"])
+    out = render(arrays, T_wc, cam, RasterSettings(alpha_cut=1 / 255))
+    return P, cam, T_wc, st, ref, arrays, out
+
+
+def test_fullsize_preprocess_and_binning_bit_exact(cfg2):
+    from oracle import raster as orc
+    P, cam, T_wc, st, ref, arrays, out = cfg2
+    s = out.cache
+    M, I, overflow, _ = s.counts
+    assert not overflow and M == len(ref["ids"])
+    order = np.argsort(ref["ids"])
+    assert np.array_equal(s.export(0), ref["ids"][order])
+    assert np.array_equal(s.export(1), ref["bboxes"][order])
+    assert np.array_equal(s.export(4), ref["mu_c"][order, 2])
+    ranges, entries, gid = orc.tile_lists(ref)
+    assert np.array_equal(s.export(2), ranges)
+    assert np.array_equal(s.export(3), gid)
+
+
+def test_fullsize_forward(cfg2):
+    P, cam, T_wc, st, ref, arrays, out = cfg2
+    o = out.numpy()
+    assert np.abs(o["image"] - ref["image"]).max() <= 1e-4
+    assert np.abs(o["final_transmittance"] - ref["t_final"].reshape(cam.height, cam.width)).max() <= 1e-4
+    flips = int((o["contrib_count"] != ref["n_proc"].reshape(cam.height, cam.width)).sum())
+    assert flips == 0, flips
+
+
+def test_fullsize_backward(cfg2):
+    from oracle import raster as orc
+    from paper_2501_08672_b200.raster import backward
+    P, cam, T_wc, st, ref, arrays, out = cfg2
+    rng = np.random.default_rng(3)
+    g_img = rng.choice([-1.0, 0.0, 1.0], size=(cam.height, cam.width, 3)) / (3.0 * cam.width * cam.height)
+    gr = orc.backward(ref, g_img)["grads"]
+    grads, _ = backward(out, g_img)
+    g = grads.numpy()
+    for k in ("mean", "rot", "scale", "opacity", "sh"):
+        rel = np.abs(g[k] - gr[k]).max() / max(np.abs(gr[k]).max(), 1e-30)
+        assert rel <= GRAD_TOL, (k, rel)
+
+
+def test_fullsize_conservation_and_determinism(cfg2):
+    """White splats over a black background: image + T == 1 per pixel
+    (test_raster.py:150-159 at full size); two renders are bit-identical."""
+    from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
+    from paper_2501_08672_b200.scene import SH_C0
+    P, cam, T_wc, st, ref, arrays, out = cfg2
+    white = np.zeros_like(P["shs"])
+    white[:, 0, :] = (1.0 - 0.5) / SH_C0
+    wa = GaussianArrays(P["means"], P["rots"], P["scales"], P["opacities"], white)
+    o1 = render(wa, T_wc, cam, RasterSettings(alpha_cut=0.0), retain_cache=False)
+    o2 = render(wa, T_wc, cam, RasterSettings(alpha_cut=0.0), retain_cache=False)
+    img, t = o1.image.cpu().numpy(), o1.final_transmittance.cpu().numpy()
+    assert np.abs(img[..., 0] + t - 1.0).max() <= 1e-5
+    assert bool((o1.image == o2.image).all()) and bool((o1.contrib_count == o2.contrib_count).all())

@@ -122,6 +122,15 @@ def main():
             st = RasterSettings(background=(0.15, 0.25, 0.35), alpha_cut=cut, sh_degree=deg)
             dump_render_case(f"rand{seed}_cut{int(cut > 0)}", arrays, T_wi @ T_ic, CAM32, st, T_ic,
                              np.random.default_rng(seed))
+    # 1b. odd image size (partial edge tiles), more Gaussians, non-identity pose
+    cam_odd = PinholeCamera(fx=50.0, fy=48.0, cx=22.5, cy=14.0, width=45, height=29)
+    for cut in (0.0, 1.0 / 255.0):
+        rng = np.random.default_rng(77)
+        arrays = random_scene(rng, 120, spread=1.5)
+        T_ic = SE3(so3_exp(rng.normal(size=3) * 0.3), rng.normal(size=3) * 0.2)
+        T_wi = SE3(so3_exp(rng.normal(size=3) * 0.05), rng.normal(size=3) * 0.05)
+        st = RasterSettings(background=(0.05, 0.1, 0.2), alpha_cut=cut)
+        dump_render_case(f"odd_cut{int(cut > 0)}", arrays, T_wi @ T_ic, cam_odd, st, T_ic, np.random.default_rng(5))
     # 2. the synthetic room (config-1 scene), reduced resolution, orbit views
     arrays = room_scene(0.323)
     np.savez_compressed(os.path.join(OUT, "scene_room_0323.npz"), means=arrays.means,
