@@ -65,9 +65,14 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi's start-up takes driver locks that stall kernel
+            # launches: wait for its first sample before the timed region
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.02)
         except OSError:
             self.proc = None
         return self
@@ -220,16 +225,39 @@ def run_ours(args, wl, rank, world, local_rank):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    timers: dict = {}
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
     smi_index = int(vis.split(",")[local_rank]) if vis and vis.split(",")[local_rank].isdigit() else local_rank
+
+    # pass 1 (eager launches, CUDA events around every kernel on its lane's
+    # stream): per-kernel device time for the roofline
+    timers: dict = {}
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        k0.record(stream)
+        for _ in range(args.steps):
+            eng.step(observed, allreduce=allreduce, timers=timers)
+        k1.record(stream)
+    torch.cuda.synchronize()
+    eager_ms = k0.elapsed_time(k1) / args.steps
+
+    # pass 2 (the headline): the same step captured once as a CUDA graph
+    use_graph = args.graph and world == 1
+    if use_graph:
+        eng.capture(observed)
+        with torch.cuda.stream(stream):
+            eng.replay()
+        torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
     with ClockSampler(smi_index) as clk:
-        time.sleep(0.3)
         with torch.cuda.stream(stream):
             start.record(stream)
             for _ in range(args.steps):
-                eng.step(observed, allreduce=allreduce, timers=timers)
+                if use_graph:
+                    eng.replay()
+                else:
+                    eng.step(observed, allreduce=allreduce)
             eng.finish()
             end.record(stream)
         torch.cuda.synchronize()
@@ -261,14 +289,22 @@ def run_ours(args, wl, rank, world, local_rank):
     step_bytes = sum(ab[k] * (len(my_views) if k != "adam" else 1) for k in ab)
 
     # end-to-end through the public API with host buffers: every step copies
-    # this rank's observed images from pinned host memory (on the view lanes,
-    # overlapping the other lanes' kernels) and reads the loss sums back
+    # this rank's observed images from pinned host memory (copy stream, in
+    # view order, overlapping the lanes' kernels) and reads the loss sums back
     host_obs = [o.cpu().pin_memory() for o in observed]
+    with torch.cuda.stream(stream):
+        eng.step(host_obs, allreduce=allreduce)            # e2e warm-up (staging buffers)
+    torch.cuda.synchronize()
+    if use_graph:
+        eng.capture(host_obs)
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         e_start.record(stream)
         for _ in range(args.steps):
-            eng.step(host_obs, allreduce=allreduce)
+            if use_graph:
+                eng.replay()
+            else:
+                eng.step(host_obs, allreduce=allreduce)
             _ = eng.loss.sums().to("cpu", non_blocking=False)
         e_end.record(stream)
     torch.cuda.synchronize()
@@ -290,7 +326,8 @@ def run_ours(args, wl, rank, world, local_rank):
             "visible_splats_per_s": float(sum(c[0] for c in counts)) * world / (ms * 1e-3),
             "config": {"workload": args.config, "gaussians": N, "views": V, "width": W, "height": H,
                        "alpha_cut": wl["alpha_cut"], "parallelism": f"view-sharded dp{world}",
-                       "view_lanes": args.lanes,
+                       "view_lanes": args.lanes, "cuda_graph": use_graph, "eager_ms_per_step": eager_ms,
+                       "kernel_timing": "eager pass of the same steps, events on each lane's stream",
                        "l2": "working set > L2: observed views alone are V x 15.7 MB",
                        "loss_last_step": float(np.mean(losses))},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "peak_source": hbm_src,
@@ -304,8 +341,9 @@ def run_ours(args, wl, rank, world, local_rank):
             "clocks": clk.summary(),
             "e2e": {"value": V * W * H / (e_ms * 1e-3) / 1e6, "unit": "Mpix/s",
                     "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world, "ms_per_step": e_ms},
-            "gpu_launches": args.steps * (len(my_views) * 8 + 1) + 1,   # per view: preprocess, scan, scatter,
-            # tile sort, big-tile sort, blend+loss, blend bwd, chain; + adam per step; + final orthonormalize
+            "gpu_launches": args.steps * (len(my_views) * 8 + 2) + 1,   # per view: preprocess, scan, scatter,
+            # tile sort, big-tile sort, blend+loss, blend bwd, chain; + adam and step counter per step;
+            # + final orthonormalize
         }
         if world == 1 and not args.no_cpu_baseline:
             tv, ta, cores = cpu_sample(wl, 2)
@@ -340,15 +378,16 @@ def run_voxel(args, rank, world, local_rank):
     lib = _lib.load()
     stream = torch.cuda.current_stream()
 
+    rcap = 1 << 18
+    rset = torch.empty(rcap, dtype=torch.int64, device=dev)
+    n_out = torch.zeros(1, dtype=torch.int64, device=dev)
+    slots = torch.empty(max(n_pts), dtype=torch.int64, device=dev)
+    cslots = torch.empty(max(c.shape[0] for c in cands), dtype=torch.int64, device=dev)
+    status = torch.empty_like(cslots, dtype=torch.int32)
+    out = torch.empty((1 << 23, 3), dtype=torch.int64, device=dev)
+
     def run(m, frames):
         st = m.struct()
-        rcap = 1 << 18
-        rset = torch.empty(rcap, dtype=torch.int64, device=dev)
-        n_out = torch.zeros(1, dtype=torch.int64, device=dev)
-        out = torch.empty((m.cap, 3), dtype=torch.int64, device=dev)
-        slots = torch.empty(max(n_pts), dtype=torch.int64, device=dev)
-        cslots = torch.empty(max(c.shape[0] for c in cands), dtype=torch.int64, device=dev)
-        status = torch.empty_like(cslots, dtype=torch.int32)
         gid = 0
         for f in frames:
             p, c = scans[f], cands[f]
@@ -465,6 +504,7 @@ def main():
     ap.add_argument("--alpha-cut", type=float, default=1.0 / 255.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--lanes", type=int, default=3, help="concurrent view pipelines per GPU")
+    ap.add_argument("--no-graph", dest="graph", action="store_false", help="eager launches instead of a CUDA graph")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -191,6 +191,17 @@ typedef struct lsb_adam_cfg {
 } lsb_adam_cfg;
 int lsb_adam_step(const lsb_params* p, const float* grads, void* m, void* v, uint8_t* touched,
                   const lsb_adam_cfg* cfg, void* stream);
+/* The same step with the step count on the device, so a captured CUDA graph
+ * can replay it: reads t = *step_dev + 1 (cfg->step is ignored), takes the
+ * bias corrections from ibc_table[2(t-1)], ibc_table[2(t-1)+1] = 1/(1-beta1^t),
+ * 1/(1-beta2^t) (host-computed like lsb_adam_step's; t beyond table_len uses
+ * the last row), then increments *step_dev. */
+int lsb_adam_step_dev(const lsb_params* p, const float* grads, void* m, void* v, uint8_t* touched,
+                      const lsb_adam_cfg* cfg, const double* ibc_table, int64_t table_len, int64_t* step_dev,
+                      void* stream);
+/* Stage host bytes (pinned) into device memory on `stream` (observed
+ * keyframe images each step; capturable into a CUDA graph). */
+int lsb_copy_h2d(void* dst, const void* src, size_t bytes, void* stream);
 /* Column Gram-Schmidt of touched rotation rows (optimize.py:91-100,193-194);
  * rots (n,9) in dtype (0 f32, 1 f64). */
 int lsb_orthonormalize(void* rots, int32_t dtype, const uint8_t* touched, int64_t n, void* stream);

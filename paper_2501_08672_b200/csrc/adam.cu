@@ -23,16 +23,19 @@ struct AdamArgs {
     uint8_t* touched;   // rotation rows stepped at least once
     lsb_adam_cfg c;
     PT ibc1, ibc2;      // 1 / (1 - beta^t)
+    const double* ibc_tab;   // device-step mode: per-step (ibc1, ibc2) rows
+    int64_t ibc_len;
+    const int64_t* step_dev; // steps taken so far
 };
 
 // AdamState.update (optimize.py:113-119): returns the additive step.
 template <typename PT>
-__device__ __forceinline__ PT adam_upd(const AdamArgs<PT>& a, int64_t idx, PT g, PT lr) {
+__device__ __forceinline__ PT adam_upd(const AdamArgs<PT>& a, PT ibc1, PT ibc2, int64_t idx, PT g, PT lr) {
     const PT m = (PT)a.c.beta1 * a.m[idx] + (PT)(1.0 - a.c.beta1) * g;
     const PT v = (PT)a.c.beta2 * a.v[idx] + (PT)(1.0 - a.c.beta2) * g * g;
     a.m[idx] = m;
     a.v[idx] = v;
-    return -lr * (m * a.ibc1) / (sqrt(v * a.ibc2) + (PT)a.c.eps);
+    return -lr * (m * ibc1) / (sqrt(v * ibc2) + (PT)a.c.eps);
 }
 
 // One thread per Gaussian.  PT = double steps the f64 working copy exactly
@@ -45,13 +48,20 @@ __global__ void __launch_bounds__(256) k_adam(AdamArgs<PT> a) {
     const PT lr_mean = (PT)(a.c.lr_mean * a.c.scene_scale), lr_rot = (PT)a.c.lr_rot;
     const PT lr_scale = (PT)a.c.lr_scale, lr_op = (PT)a.c.lr_opacity, lr_sh = (PT)a.c.lr_sh;
     const PT floor_s = (PT)a.c.scale_floor, oclip = (PT)a.c.opacity_clip;
+    PT ibc1 = a.ibc1, ibc2 = a.ibc2;
+    if (a.ibc_tab) {
+        int64_t t = *a.step_dev;
+        t = t < a.ibc_len ? t : a.ibc_len - 1;
+        ibc1 = (PT)a.ibc_tab[2 * t];
+        ibc2 = (PT)a.ibc_tab[2 * t + 1];
+    }
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
 #pragma unroll
-        for (int k = 0; k < 3; ++k) a.means[3 * i + k] += adam_upd(a, 3 * i + k, (PT)a.g[3 * i + k], lr_mean);
+        for (int k = 0; k < 3; ++k) a.means[3 * i + k] += adam_upd(a, ibc1, ibc2, 3 * i + k, (PT)a.g[3 * i + k], lr_mean);
         // rotation: R <- R Exp(phi) on rows with phi != 0 (optimize.py:172-176)
         PT phi[3];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) phi[k] = adam_upd(a, o_rot + 3 * i + k, (PT)a.g[o_rot + 3 * i + k], lr_rot);
+        for (int k = 0; k < 3; ++k) phi[k] = adam_upd(a, ibc1, ibc2, o_rot + 3 * i + k, (PT)a.g[o_rot + 3 * i + k], lr_rot);
         if (phi[0] != (PT)0 || phi[1] != (PT)0 || phi[2] != (PT)0) {
             const double p0 = phi[0], p1 = phi[1], p2 = phi[2];
             const double th = sqrt(p0 * p0 + p1 * p1 + p2 * p2);
@@ -82,21 +92,21 @@ __global__ void __launch_bounds__(256) k_adam(AdamArgs<PT> a) {
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             const PT s = a.scales[3 * i + k];
-            const PT st = adam_upd(a, o_scale + 3 * i + k, (PT)a.g[o_scale + 3 * i + k] * s, lr_scale);
+            const PT st = adam_upd(a, ibc1, ibc2, o_scale + 3 * i + k, (PT)a.g[o_scale + 3 * i + k] * s, lr_scale);
             if (st != (PT)0) a.scales[3 * i + k] = fmax(exp(log(fmax(s, floor_s)) + st), floor_s);
         }
         // opacity in logit space (optimize.py:183-186)
         {
             const PT op = a.opac[i];
             const PT oc = fmin(fmax(op, oclip), (PT)1 - oclip);
-            const PT st = adam_upd(a, o_op + i, (PT)a.g[o_op + i] * oc * ((PT)1 - oc), lr_op);
+            const PT st = adam_upd(a, ibc1, ibc2, o_op + i, (PT)a.g[o_op + i] * oc * ((PT)1 - oc), lr_op);
             if (st != (PT)0) a.opac[i] = (PT)1 / ((PT)1 + exp(-(log(oc / ((PT)1 - oc)) + st)));
         }
         // SH coefficients
         const int64_t nk = 3 * (int64_t)a.K;
         for (int64_t k = 0; k < nk; ++k) {
             const int64_t idx = nk * i + k;
-            a.shs[idx] += adam_upd(a, o_sh + idx, (PT)a.g[o_sh + idx], lr_sh);
+            a.shs[idx] += adam_upd(a, ibc1, ibc2, o_sh + idx, (PT)a.g[o_sh + idx], lr_sh);
         }
     }
 }
@@ -129,21 +139,29 @@ static int grid_of(int64_t n) {
     return (int)(b < 148 * 8 ? b : 148 * 8);
 }
 
+__global__ void k_step_bump(int64_t* step_dev) { *step_dev += 1; }
+
 template <typename PT>
 static cudaError_t adam_t(const lsb_params& p, const float* g, void* m, void* v, uint8_t* touched,
-                          const lsb_adam_cfg& c, cudaStream_t st) {
+                          const lsb_adam_cfg& c, const double* tab, int64_t tab_len, int64_t* step_dev,
+                          cudaStream_t st) {
     AdamArgs<PT> a{(PT*)p.means, (PT*)p.rots, (PT*)p.scales, (PT*)p.opacities, (PT*)p.shs, p.n, p.sh_coeffs,
-                   g, (PT*)m, (PT*)v, touched, c, (PT)0, (PT)0};
-    a.ibc1 = (PT)(1.0 / (1.0 - pow(c.beta1, (double)c.step)));
-    a.ibc2 = (PT)(1.0 / (1.0 - pow(c.beta2, (double)c.step)));
-    k_adam<PT><<<grid_of(p.n), 256, 0, st>>>(a);
+                   g, (PT*)m, (PT*)v, touched, c, (PT)0, (PT)0, tab, tab_len, step_dev};
+    if (!tab) {
+        a.ibc1 = (PT)(1.0 / (1.0 - pow(c.beta1, (double)c.step)));
+        a.ibc2 = (PT)(1.0 / (1.0 - pow(c.beta2, (double)c.step)));
+    }
+    if (p.n > 0) k_adam<PT><<<grid_of(p.n), 256, 0, st>>>(a);
+    if (step_dev) k_step_bump<<<1, 1, 0, st>>>(step_dev);
     return cudaGetLastError();
 }
 
 cudaError_t launch_adam(const lsb_params& p, const float* g, void* m, void* v, uint8_t* touched,
-                        const lsb_adam_cfg& c, cudaStream_t st) {
-    if (p.n == 0) return cudaSuccess;
-    return p.dtype ? adam_t<double>(p, g, m, v, touched, c, st) : adam_t<float>(p, g, m, v, touched, c, st);
+                        const lsb_adam_cfg& c, const double* tab, int64_t tab_len, int64_t* step_dev,
+                        cudaStream_t st) {
+    if (p.n == 0 && !step_dev) return cudaSuccess;
+    return p.dtype ? adam_t<double>(p, g, m, v, touched, c, tab, tab_len, step_dev, st)
+                   : adam_t<float>(p, g, m, v, touched, c, tab, tab_len, step_dev, st);
 }
 
 cudaError_t launch_orthonormalize(void* rots, int dtype, const uint8_t* touched, int64_t n, cudaStream_t st) {

@@ -17,7 +17,8 @@ cudaError_t launch_chain(const Ws&, const lsb_params&, const lsb_grads&, const l
 cudaError_t launch_loss(const float*, const float*, const uint8_t*, int64_t, int, float, float*, double*,
                         cudaStream_t);
 int loss_scratch_doubles();
-cudaError_t launch_adam(const lsb_params&, const float*, void*, void*, uint8_t*, const lsb_adam_cfg&, cudaStream_t);
+cudaError_t launch_adam(const lsb_params&, const float*, void*, void*, uint8_t*, const lsb_adam_cfg&, const double*,
+                        int64_t, int64_t*, cudaStream_t);
 cudaError_t launch_orthonormalize(void*, int, const uint8_t*, int64_t, cudaStream_t);
 cudaError_t launch_pose_prepare(const Ws&, const lsb_params&, const lsb_camera&, const lsb_pose&,
                                 const lsb_settings&, float*, cudaStream_t);
@@ -261,7 +262,26 @@ int lsb_adam_step(const lsb_params* p, const float* grads, void* m, void* v, uin
                      !p->shs))
         return fail(LSB_EINVAL, "NULL array");
     if (cfg->step < 1) return fail(LSB_EINVAL, "Adam step count must be >= 1");
-    return check_cuda(launch_adam(*p, grads, m, v, touched, *cfg, (cudaStream_t)stream), "adam");
+    return check_cuda(launch_adam(*p, grads, m, v, touched, *cfg, nullptr, 0, nullptr, (cudaStream_t)stream),
+                      "adam");
+}
+
+int lsb_adam_step_dev(const lsb_params* p, const float* grads, void* m, void* v, uint8_t* touched,
+                      const lsb_adam_cfg* cfg, const double* ibc_table, int64_t table_len, int64_t* step_dev,
+                      void* stream) {
+    if (!p || !cfg || !ibc_table || !step_dev) return fail(LSB_EINVAL, "NULL argument");
+    if (table_len < 1) return fail(LSB_EINVAL, "empty bias-correction table");
+    if (p->n > 0 && (!grads || !m || !v || !touched || !p->means || !p->rots || !p->scales || !p->opacities ||
+                     !p->shs))
+        return fail(LSB_EINVAL, "NULL array");
+    return check_cuda(launch_adam(*p, grads, m, v, touched, *cfg, ibc_table, table_len, step_dev,
+                                  (cudaStream_t)stream), "adam_dev");
+}
+
+int lsb_copy_h2d(void* dst, const void* src, size_t bytes, void* stream) {
+    if (bytes == 0) return LSB_OK;
+    if (!dst || !src) return fail(LSB_EINVAL, "NULL argument");
+    return check_cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream), "copy_h2d");
 }
 
 int lsb_orthonormalize(void* rots, int32_t dtype, const uint8_t* touched, int64_t n, void* stream) {

@@ -208,24 +208,34 @@ __global__ void k_fov_roots(const double* __restrict__ pts, int64_t n, double ro
 __global__ void k_fov_leaves(lsb_voxmap m, const unsigned long long* __restrict__ rset, int64_t rcap,
                              int64_t* __restrict__ out, unsigned long long* __restrict__ n_out, int64_t out_cap) {
     const int L = m.max_level;
+    const unsigned lane = threadIdx.x & 31;
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < m.cap; s += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long key = (unsigned long long)m.keys[s];
-        if (key == EMPTY || m.gslot[s] < 0) continue;
-        long long ix, iy, iz;
-        unpack_key(key, ix, iy, iz);
-        const long long rx = ix >> L, ry = iy >> L, rz = iz >> L;   // floor division by 2^L
-        const unsigned long long rkey = pack_key(rx, ry, rz);
-        const unsigned long long mask = (unsigned long long)rcap - 1;
-        unsigned long long q = slot_of(rx, ry, rz, 0, mask);
         bool hit = false;
-        for (long long probe = 0; probe < rcap; ++probe) {
-            const unsigned long long cur = rset[q];
-            if (cur == rkey) { hit = true; break; }
-            if (cur == EMPTY) break;
-            q = (q + 1) & mask;
+        long long ix = 0, iy = 0, iz = 0;
+        if (key != EMPTY && m.gslot[s] >= 0) {
+            unpack_key(key, ix, iy, iz);
+            const long long rx = ix >> L, ry = iy >> L, rz = iz >> L;   // floor division by 2^L
+            const unsigned long long rkey = pack_key(rx, ry, rz);
+            const unsigned long long mask = (unsigned long long)rcap - 1;
+            unsigned long long q = slot_of(rx, ry, rz, 0, mask);
+            for (long long probe = 0; probe < rcap; ++probe) {
+                const unsigned long long cur = rset[q];
+                if (cur == rkey) { hit = true; break; }
+                if (cur == EMPTY) break;
+                q = (q + 1) & mask;
+            }
         }
+        // warp-aggregated output slot: one atomic per warp instead of per leaf
+        const unsigned act = __activemask();
+        const unsigned hits = __ballot_sync(act, hit);
+        if (!hits) continue;
+        const int leader = __ffs(hits) - 1;
+        unsigned long long base = 0;
+        if ((int)lane == leader) base = atomicAdd(n_out, (unsigned long long)__popc(hits));
+        base = __shfl_sync(act, base, leader);
         if (!hit) continue;
-        const unsigned long long o = atomicAdd(n_out, 1ull);
+        const unsigned long long o = base + __popc(hits & ((1u << lane) - 1u));
         if ((int64_t)o < out_cap) {
             out[3 * o] = ix;
             out[3 * o + 1] = iy;

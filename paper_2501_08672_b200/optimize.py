@@ -7,7 +7,8 @@ and error behaviour.  The multi-keyframe step the benchmark configs ask for
 rendered, scored and back-propagated into one gradient buffer (the mean of
 the per-view reference gradients), optionally all-reduced across ranks
 (views sharded by rank), then one Adam step in storage coordinates runs.
-No host synchronisation inside a step.
+No host synchronisation inside a step, so a step can be captured once as a
+CUDA graph (`WindowEngine.capture`) and replayed with one launch.
 """
 
 from __future__ import annotations
@@ -121,9 +122,21 @@ def adam_cfg(cfg: OptimConfig, step: int) -> _lib.AdamCfg:
                         cfg.eps, cfg.scene_scale, cfg.opacity_clip, cfg.scale_floor, int(step))
 
 
+IBC_ROWS = 1 << 16     # beyond 2^16 steps both bias corrections are exactly 1.0 in f64
+
+
+def bias_correction_table(beta1: float, beta2: float, rows: int = IBC_ROWS) -> np.ndarray:
+    """(rows, 2) of 1/(1-beta1^t), 1/(1-beta2^t) for t = 1..rows, with the
+    C library pow the reference's `beta ** t` uses (optimize.py:116-117)."""
+    import math
+    return np.array([(1.0 / (1.0 - math.pow(beta1, t)), 1.0 / (1.0 - math.pow(beta2, t)))
+                     for t in range(1, rows + 1)], dtype=np.float64)
+
+
 class AdamState:
     """Moments per parameter group (optimize.py:103-119), device-resident
-    and laid out like ParamGradients.flat so one kernel steps every group."""
+    and laid out like ParamGradients.flat so one kernel steps every group.
+    `apply_dev` keeps the step count on the device (graph-replayable)."""
 
     def __init__(self, arrays: GaussianArrays, cfg: OptimConfig):
         n, k = len(arrays), int(arrays.shs.shape[1])
@@ -132,6 +145,22 @@ class AdamState:
         self.m = torch.zeros(n * (10 + 3 * k), dtype=arrays.dtype, device=arrays.device)
         self.v = torch.zeros_like(self.m)
         self.touched = torch.zeros(n, dtype=torch.uint8, device=arrays.device)
+        self.step_dev = None
+        self.ibc = None
+
+    def apply_dev(self, arrays: GaussianArrays, grads: ParamGradients, stream=None) -> None:
+        """Like apply(), with the step count read and advanced on the device."""
+        if self.step_dev is None:
+            self.ibc = torch.from_numpy(bias_correction_table(self.cfg.beta1, self.cfg.beta2)).to(self.m.device)
+            self.step_dev = torch.full((1,), self.step, dtype=torch.int64, device=self.m.device)
+        self.step += 1
+        c = adam_cfg(self.cfg, self.step)
+        p = arrays.params()
+        _lib.check(_lib.load().lsb_adam_step_dev(
+            ctypes.byref(p), ctypes.c_void_p(grads.flat.data_ptr()), ctypes.c_void_p(self.m.data_ptr()),
+            ctypes.c_void_p(self.v.data_ptr()), ctypes.c_void_p(self.touched.data_ptr()), ctypes.byref(c),
+            ctypes.c_void_p(self.ibc.data_ptr()), int(self.ibc.shape[0]), ctypes.c_void_p(self.step_dev.data_ptr()),
+            _lib.stream_ptr(stream)), "adam_dev")
 
     def apply(self, arrays: GaussianArrays, grads: ParamGradients, stream=None) -> None:
         """One Adam step in storage coordinates, in place on the arena."""
@@ -205,6 +234,13 @@ class WindowEngine:
                 n_contrib=torch.empty((h, w), dtype=torch.int32, device=dev),
                 grad_image=torch.empty((h, w, 3), dtype=torch.float32, device=dev),
                 observed=None))
+        # host-input staging: one device buffer per view, filled on a copy
+        # stream in view order so the H2D transfers run back to back while
+        # the lanes bin (and blend) the views already resident
+        self.copy_stream = None
+        self.obs_dev: list = []
+        self._consumed: list = [None] * len(self.views)
+        self.graph = None
         self.state = self.lanes[0].state
         self.image, self.t_final, self.n_contrib = self.lanes[0].image, self.lanes[0].t_final, self.lanes[0].n_contrib
         self.grad_image = self.lanes[0].grad_image
@@ -229,17 +265,46 @@ class WindowEngine:
         """True if the last render in every lane's workspace fit (syncs)."""
         return all(not ln.state.read_counts(ln.stream)[2] for ln in self.lanes)
 
+    def _stage(self, observed, ready, capturing):
+        """Queue the H2D copies of host `observed` images; returns one event per view."""
+        dev = self.grads.flat.device
+        if self.copy_stream is None:
+            self.copy_stream = torch.cuda.Stream(dev)
+            self.obs_dev = [torch.empty((self.h, self.w, 3), dtype=torch.float32, device=dev) for _ in self.views]
+        cs = self.copy_stream
+        cs.wait_event(ready)
+        lib = _lib.load()
+        events = []
+        for v, obs in enumerate(observed):
+            if obs.dtype != torch.float32 or tuple(obs.shape) != (self.h, self.w, 3) or not obs.is_contiguous():
+                raise ValueError("observed images must be contiguous float32 (H, W, 3)")
+            if capturing and not obs.is_pinned():
+                raise ValueError("graph capture needs pinned host images")
+            if self._consumed[v] is not None and not capturing:
+                cs.wait_event(self._consumed[v])      # previous step's blend of this view is done
+            _lib.check(lib.lsb_copy_h2d(ctypes.c_void_p(self.obs_dev[v].data_ptr()), ctypes.c_void_p(obs.data_ptr()),
+                                        obs.numel() * 4, _lib.stream_ptr(cs)), "copy_h2d")
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            events.append(ev)
+        return events
+
     def step(self, observed: Sequence[torch.Tensor], allreduce=None, timers: Optional[dict] = None) -> None:
         """One optimisation step over this rank's views (async).  `observed`
-        are device images, or host (pinned) images: then each view's image is
-        copied on its lane's stream right before it is needed, so the H2D
-        transfer of one view overlaps the other lanes' kernels."""
+        are device images, or host images (pinned for overlap): then all
+        views are copied on a dedicated copy stream in view order and each
+        view's blend waits for its own copy only."""
         gscale = 1.0 / (3.0 * self.h * self.w * self.n_total)
         main = self.stream if self.stream is not None else torch.cuda.current_stream()
+        capturing = torch.cuda.is_current_stream_capturing()
+        if capturing:
+            timers = None
         with torch.cuda.stream(main):
             self.grads.flat.zero_()
         ready = torch.cuda.Event()
         ready.record(main)
+        host = len(observed) > 0 and not observed[0].is_cuda
+        copied = self._stage(observed, ready, capturing) if host else None
 
         def mark(name, stream):
             # timers[name] collects (start, end) event pairs on the launching stream
@@ -255,18 +320,19 @@ class WindowEngine:
             if sm is not main:
                 sm.wait_event(ready)
             st.set_pose(T.R, T.t)
-            obs = observed[v]
-            if not obs.is_cuda:
-                if ln.observed is None:
-                    ln.observed = torch.empty((self.h, self.w, 3), dtype=torch.float32, device=self.grads.flat.device)
-                with torch.cuda.stream(sm):
-                    ln.observed.copy_(obs, non_blocking=True)
-                obs = ln.observed
             mark("bin", sm); render_bin(st, sm); mark("bin", sm)
+            obs = observed[v]
+            if host:
+                sm.wait_event(copied[v])
+                obs = self.obs_dev[v]
             mark("blend_fwd", sm)
             render_blend_loss(st, ln.image, ln.t_final, ln.n_contrib, obs, _KIND[self.cfg.loss],
                               gscale, ln.grad_image, self.loss.ptr(v), stream=sm)
             mark("blend_fwd", sm)
+            if host and not capturing:
+                ev = torch.cuda.Event()
+                ev.record(sm)
+                self._consumed[v] = ev
             mark("blend_bwd", sm)
             render_blend_bwd(st, ln.image, ln.n_contrib, ln.grad_image, 1.0, sm)
             mark("blend_bwd", sm)
@@ -280,10 +346,35 @@ class WindowEngine:
                 done = torch.cuda.Event()
                 done.record(ln.stream)
                 main.wait_event(done)
+        if host:
+            done = torch.cuda.Event()
+            done.record(self.copy_stream)
+            main.wait_event(done)
         with torch.cuda.stream(main):
             if allreduce is not None:
                 allreduce(self.grads.flat)
-            mark("adam", main); self.adam.apply(self.arrays, self.grads, main); mark("adam", main)
+            mark("adam", main); self.adam.apply_dev(self.arrays, self.grads, main); mark("adam", main)
+
+    def capture(self, observed: Sequence[torch.Tensor], allreduce=None) -> None:
+        """Capture one step() as a CUDA graph; replay() then runs a whole step
+        (H2D staging, every view on every lane, Adam) with one launch.  The
+        `observed` tensors are re-read from the same addresses at each replay
+        (refresh pinned host buffers in place).  Run one eager step first."""
+        saved = self.adam.step
+        self.graph = torch.cuda.CUDAGraph()
+        kw = {"stream": self.stream} if self.stream is not None else {}
+        with torch.cuda.graph(self.graph, **kw):
+            self.step(observed, allreduce)
+        self.adam.step = saved
+        self._graph_obs = list(observed)
+
+    def replay(self) -> None:
+        if self.graph is None:
+            raise RuntimeError("capture() first")
+        main = self.stream if self.stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(main):
+            self.graph.replay()
+        self.adam.step += 1
 
     def finish(self) -> None:
         """End of the window optimisation: re-orthonormalise stepped rotations
