@@ -12,18 +12,30 @@
 // applies the reference's per-pixel bbox membership test (exact CSR
 // semantics, _kernels.py:21-59) before it counts or blends an entry.
 //
-// Forward (_kernels.py:62-119): branch-free per pixel — alpha is evaluated
-// for the whole 4-pixel run and masked, so no divergence inside the record
-// loop.  Optionally fuses the photometric loss (optimize.py:48-74): the
+// Issue budget.  The inner loops are bound by instruction issue, and the ALU
+// pipe (compares, selects, min/max — half rate on this SM) was the hot one,
+// so per (pixel, splat) pair the code keeps ALU work to the two predicates
+// the semantics need (alive-and-in-bbox, alpha >= cut) and puts everything
+// else on the FMA pipe: the alpha clamp is a saturate (alpha = clamp * sat(
+// op g / clamp), 1/clamp folded into the exponent and clamp into the
+// colours), and the gated updates are predicated instead of selected.
+//
+// Forward (_kernels.py:62-119): alpha is evaluated for the whole 4-pixel run
+// and the updates are predicated, so there is no divergence inside the
+// record loop.  Optionally fuses the photometric loss (optimize.py:48-74): the
 // epilogue reads the observed pixels, writes dL/dI and reduces the loss per
 // tile; the last CTA (ticket) adds the tile sums in tile order.
 //
 // Backward (_kernels.py:122-216): per pixel the forward is recomputed front
-// to back, carrying T and gD = g . (I - sum_{j<=k} w_j c_j) — the dot product
-// of dL/dI with the reference's suffix colour, updated as a scalar.  The 9
-// screen partials of a (tile, splat) pair are reduced across the warp with a
-// transpose-reduce and written once per intersection: no global atomics,
-// deterministic.
+// to back with the SAME instruction sequence (shared helpers below), so T is
+// bit-identical to the forward's and a pixel stops exactly where it stopped
+// there (T < t_min) without a per-pixel entry count.  It carries T and
+// gD = g . (I - sum_{j<=k} w_j c_j) — the dot product of dL/dI with the
+// reference's suffix colour, updated as a scalar.  Per row the geometric
+// terms are accumulated as raw moments of (u, dy) (sum gd, gd u, gd u^2) and
+// mapped to the conic-space sums once per record; the 9 screen partials of
+// a (tile, splat) pair are reduced across the warp with a transpose-reduce
+// and written once per intersection: no global atomics, deterministic.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -43,7 +55,124 @@ struct BlendArgs {
     int W, H;
     float clamp, tmin, cut;
     float bg0, bg1, bg2;
+    float cutp;       // cut / clamp: the test on the saturated alpha
+    float lgk;        // -log2(clamp), added to the exponent
+    float ik;         // 1 / clamp
 };
+
+// Per-record frame of one lane: the splat mean relative to the lane's first
+// pixel (gx0, gy0) and the opacity folded into the exponent.
+struct Frame {
+    float mxr, myr, lop;
+};
+
+__device__ __forceinline__ float lg2_approx(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ Frame frame_of(float4 q0, float op, float gx0f, float gy0f, float lgk) {
+    Frame f;
+    f.mxr = __fadd_rn(__fsub_rn(q0.x, gx0f), q0.z);
+    f.myr = __fadd_rn(__fsub_rn(q0.y, gy0f), q0.w);
+    f.lop = __fadd_rn(lg2_approx(op), lgk);
+    return f;
+}
+
+// Row terms: u0 = x_local + s dy - mx at the run's first pixel, and the
+// row part of the exponent E dy^2 + log2(op / clamp).
+__device__ __forceinline__ void row_terms(const Frame& f, float s, float E, float rowoff, float& dy, float& u0,
+                                          float& edy) {
+    dy = __fsub_rn(rowoff, f.myr);
+    u0 = __fmaf_rn(s, dy, -f.mxr);
+    edy = __fmaf_rn(__fmul_rn(E, dy), dy, f.lop);
+}
+
+// Saturated alpha of pixel j of the run: a = min(1, op g / clamp).
+__device__ __forceinline__ float alpha_sat(float A, float u0, float edy, int j, float& u) {
+    u = j == 0 ? u0 : __fadd_rn(u0, (float)j);
+    return __saturatef(ex2_approx(__fmaf_rn(A, __fmul_rn(u, u), edy)));
+}
+
+// Per-column liveness threshold of a record: T must reach t_min for pixels
+// inside the bbox columns [cx0, cx1) of the run, +inf outside, so one
+// compare gives "alive and in bbox".
+__device__ __forceinline__ float col_thr(int j, int cx0, int cx1, float tmin) {
+    return (j >= cx0 && j < cx1) ? tmin : __int_as_float(0x7f800000);
+}
+
+// Forward pixel update, predicated (no branches, no selects):
+//   in   = T >= thr            (alive and inside the bbox)   -> count
+//   take = in && a >= cut'                                    -> composite
+//   w = T a;  C += w c';  T += w (-clamp)
+__device__ __forceinline__ void fwd_pixel(float al, float thr, float cutp, float nkap, float c0, float c1, float c2,
+                                          float& T, float& cnt, float& cr, float& cg, float& cb) {
+    asm("{\n\t.reg .pred pi, pt;\n\t.reg .f32 w;\n\t"
+        "setp.ge.f32 pi, %0, %5;\n\t"
+        "@pi add.f32 %1, %1, 0f3F800000;\n\t"
+        "setp.ge.and.f32 pt, %6, %7, pi;\n\t"
+        "mul.rn.f32 w, %0, %6;\n\t"
+        "@pt fma.rn.f32 %2, w, %8, %2;\n\t"
+        "@pt fma.rn.f32 %3, w, %9, %3;\n\t"
+        "@pt fma.rn.f32 %4, w, %10, %4;\n\t"
+        "@pt fma.rn.f32 %0, w, %11, %0;\n\t}"
+        : "+f"(T), "+f"(cnt), "+f"(cr), "+f"(cg), "+f"(cb)
+        : "f"(thr), "f"(al), "f"(cutp), "f"(c0), "f"(c1), "f"(c2), "f"(nkap));
+}
+
+__device__ __forceinline__ void fwd_pixel_depth(float al, float thr, float cutp, float nkap, float c0, float c1,
+                                                float c2, float zk, float& T, float& cnt, float& cr, float& cg,
+                                                float& cb, float& dz) {
+    asm("{\n\t.reg .pred pi, pt;\n\t.reg .f32 w;\n\t"
+        "setp.ge.f32 pi, %0, %6;\n\t"
+        "@pi add.f32 %1, %1, 0f3F800000;\n\t"
+        "setp.ge.and.f32 pt, %7, %8, pi;\n\t"
+        "mul.rn.f32 w, %0, %7;\n\t"
+        "@pt fma.rn.f32 %2, w, %9, %2;\n\t"
+        "@pt fma.rn.f32 %3, w, %10, %3;\n\t"
+        "@pt fma.rn.f32 %4, w, %11, %4;\n\t"
+        "@pt fma.rn.f32 %5, w, %12, %5;\n\t"
+        "@pt fma.rn.f32 %0, w, %13, %0;\n\t}"
+        : "+f"(T), "+f"(cnt), "+f"(cr), "+f"(cg), "+f"(cb), "+f"(dz)
+        : "f"(thr), "f"(al), "f"(cutp), "f"(c0), "f"(c1), "f"(c2), "f"(zk), "f"(nkap));
+}
+
+// Backward pixel update (same T recurrence as fwd_pixel), predicated:
+//   take: w = T a; gc' = g.c'; gD -= w gc'; dap = T gc' - gD / (1/clamp - a);
+//         colour sums += w g; T += w (-clamp)
+//   gate = take && a < 1 (unclamped): gd = a dap; S0 += gd; S1 += gd u; S2 += gd u^2
+__device__ __forceinline__ void bwd_pixel(float al, float u, float thr, float cutp, float nkap, float ik, float c0,
+                                          float c1, float c2, float Gr, float Gg, float Gb, float& T, float& gD,
+                                          float& s0, float& s1, float& s2, float& S0, float& S1, float& S2) {
+    asm("{\n\t.reg .pred pi, pt, pg;\n\t.reg .f32 w, gc, r, tg, da, gd, gu;\n\t"
+        "setp.ge.f32 pi, %0, %8;\n\t"
+        "setp.ge.and.f32 pt, %9, %10, pi;\n\t"
+        "setp.lt.and.f32 pg, %9, 0f3F800000, pt;\n\t"
+        "mul.rn.f32 w, %0, %9;\n\t"
+        "mul.rn.f32 gc, %20, %15;\n\t"
+        "fma.rn.f32 gc, %19, %14, gc;\n\t"
+        "fma.rn.f32 gc, %18, %13, gc;\n\t"
+        "neg.f32 r, w;\n\t"
+        "@pt fma.rn.f32 %1, r, gc, %1;\n\t"
+        "sub.f32 r, %12, %9;\n\t"
+        "rcp.approx.ftz.f32 r, r;\n\t"
+        "mul.rn.f32 tg, %0, gc;\n\t"
+        "neg.f32 da, %1;\n\t"
+        "fma.rn.f32 da, da, r, tg;\n\t"
+        "@pt fma.rn.f32 %2, w, %18, %2;\n\t"
+        "@pt fma.rn.f32 %3, w, %19, %3;\n\t"
+        "@pt fma.rn.f32 %4, w, %20, %4;\n\t"
+        "mul.rn.f32 gd, %9, da;\n\t"
+        "mul.rn.f32 gu, gd, %16;\n\t"
+        "@pg add.f32 %5, %5, gd;\n\t"
+        "@pg add.f32 %6, %6, gu;\n\t"
+        "@pg fma.rn.f32 %7, gu, %16, %7;\n\t"
+        "@pt fma.rn.f32 %0, w, %11, %0;\n\t}"
+        : "+f"(T), "+f"(gD), "+f"(s0), "+f"(s1), "+f"(s2), "+f"(S0), "+f"(S1), "+f"(S2)
+        : "f"(thr), "f"(al), "f"(cutp), "f"(nkap), "f"(ik), "f"(c0), "f"(c1), "f"(c2), "f"(u), "f"(0.f),
+          "f"(Gr), "f"(Gg), "f"(Gb));
+}
 
 struct LossArgs {
     const float* observed;   // (H,W,3) or NULL: no fused loss
@@ -105,8 +234,7 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
     const int qx = (lane & 3) * RUN, r0 = lane >> 2;      // rows r0 and r0 + 8
     RecPipe pipe;
     pipe.buf = s_rec[wib];
-    const float fx0 = (float)qx;
-    const float fy[2] = {(float)r0, (float)(r0 + 8)};
+    const float kap = a.clamp;
     // persistent tile-warp: pull tiles from the queue until it is empty
     for (;;) {
         int tile = 0;
@@ -114,7 +242,8 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
         tile = __shfl_sync(0xffffffffu, tile, 0);
         if (tile >= w.ntiles) break;
         const int ox = (tile % w.ntx) * TILE, oy = (tile / w.ntx) * TILE;
-        const int gx0 = ox + qx;
+        const int gx0 = ox + qx, gy0 = oy + r0;
+        const float gx0f = (float)gx0, gy0f = (float)gy0;
         double l0 = 0.0, l1 = 0.0;
         // A pixel composites while T >= t_min (the reference breaks when
         // T < t_min, _kernels.py:98); pixels outside the image start at T = -1.
@@ -124,13 +253,12 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
         for (int h = 0; h < 2; ++h)
 #pragma unroll
             for (int j = 0; j < RUN; ++j) {
-                T[h][j] = (oy + r0 + 8 * h < a.H && gx0 + j < a.W) ? 1.f : -1.f;
+                T[h][j] = (gy0 + 8 * h < a.H && gx0 + j < a.W) ? 1.f : -1.f;
                 cr[h][j] = cg[h][j] = cb[h][j] = dz[h][j] = 0.f;
                 cnt[h][j] = 0.f;
             }
         int last = 0;
         const int start = w.tile_start[tile], end = w.tile_start[tile + 1];
-        const float oxf = (float)ox, oyf = (float)oy;
         pipe.start = start;
         pipe.end = end;
         pipe.begin(w, lane);
@@ -145,45 +273,38 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
             const int nb = min(32, end - base);
             for (int k = 0; k < nb; ++k) {
                 const int4 qi = *(const int4*)&sr[k].bbx;
-                const int bby = qi.y, bbx = qi.x;
-                const int y0 = (bby & 0xffff) - oy, y1 = (bby >> 16) - oy;
-                const int lo = max((bbx & 0xffff) - gx0, 0), hi = min((bbx >> 16) - gx0, RUN);
-                if (lo >= hi) continue;
-                bool inx[RUN];                                       // bbox columns of this run
+                // bbox relative to the lane's run: columns [cx0, cx1), rows [ry0, ry1)
+                const int cx0 = (qi.x & 0xffff) - gx0, cx1 = (qi.x >> 16) - gx0;
+                const int ry0 = (qi.y & 0xffff) - gy0, ry1 = (qi.y >> 16) - gy0;
+                const bool row0 = ry0 <= 0 && ry1 > 0, row1 = ry0 <= 8 && ry1 > 8;
+                if (cx0 >= RUN || cx1 <= 0 || !(row0 || row1)) continue;
+                if (alive) last = base + k + 1;
+                float thr[RUN];                                      // bbox columns of this run
 #pragma unroll
-                for (int j = 0; j < RUN; ++j) inx[j] = j >= lo && j < hi;
+                for (int j = 0; j < RUN; ++j) thr[j] = col_thr(j, cx0, cx1, a.tmin);
                 const float4 q0 = *(const float4*)&sr[k].mxh;        // mxh myh mxl myl
-                const float4 qa = make_float4((q0.x - oxf) + q0.z, (q0.y - oyf) + q0.w, sr[k].A, sr[k].s);
                 const float4 qb = *(const float4*)&sr[k].A;          // A s E op
                 const float4 qc = *(const float4*)&sr[k].c0;         // c0 c1 c2 z
-                const float lop = __log2f(qb.w);
-                bool used = false;
+                const Frame f = frame_of(q0, qb.w, gx0f, gy0f, a.lgk);
+                const float c0 = __fmul_rn(kap, qc.x), c1 = __fmul_rn(kap, qc.y), c2 = __fmul_rn(kap, qc.z);
+                const float zk = DEPTH ? __fmul_rn(kap, qc.w) : 0.f;
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const int row = r0 + 8 * h;
-                    if (row < y0 || row >= y1) continue;
-                    const float dy = fy[h] - qa.y;
-                    const float u0 = fmaf(qa.w, dy, fx0 - qa.x);      // u = x_local + s dy - mx
-                    // log2(alpha) = A u^2 + E dy^2 + log2(op): opacity folded into the exponent
-                    const float edy = fmaf(qb.z * dy, dy, lop);
+                    if (!(h ? row1 : row0)) continue;
+                    float dy, u0, edy;
+                    row_terms(f, qb.y, qb.z, 8.f * h, dy, u0, edy);
 #pragma unroll
                     for (int j = 0; j < RUN; ++j) {
-                        const bool in = inx[j] && T[h][j] >= a.tmin;
-                        const float u = j == 0 ? u0 : u0 + (float)j;
-                        float al = fminf(ex2_approx(fmaf(qa.z, u * u, edy)), a.clamp);
-                        cnt[h][j] += in ? 1.f : 0.f;
-                        used |= in;
-                        const bool take = CUT ? (in && al >= a.cut) : in;
-                        al = take ? al : 0.f;
-                        const float wt = T[h][j] * al;
-                        cr[h][j] = fmaf(wt, qc.x, cr[h][j]);
-                        cg[h][j] = fmaf(wt, qc.y, cg[h][j]);
-                        cb[h][j] = fmaf(wt, qc.z, cb[h][j]);
-                        if (DEPTH) dz[h][j] = fmaf(wt, qc.w, dz[h][j]);
-                        T[h][j] = fmaf(-al, T[h][j], T[h][j]);
+                        float u;
+                        const float al = alpha_sat(qb.x, u0, edy, j, u);
+                        if (DEPTH)
+                            fwd_pixel_depth(al, thr[j], CUT ? a.cutp : 0.f, -kap, c0, c1, c2, zk, T[h][j], cnt[h][j],
+                                            cr[h][j], cg[h][j], cb[h][j], dz[h][j]);
+                        else
+                            fwd_pixel(al, thr[j], CUT ? a.cutp : 0.f, -kap, c0, c1, c2, T[h][j], cnt[h][j], cr[h][j],
+                                      cg[h][j], cb[h][j]);
                     }
                 }
-                if (used) last = base + k + 1;
             }
             __syncwarp();
         }
@@ -193,7 +314,7 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
         if (lane == 0) w.tile_last[tile] = max(last, start);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const int gy = oy + r0 + 8 * h;
+            const int gy = gy0 + 8 * h;
             if (gy >= a.H) continue;
 #pragma unroll
             for (int j = 0; j < RUN; ++j) {
@@ -286,37 +407,34 @@ __device__ __forceinline__ float reduce8(const float* v, int lane) {
 }
 
 __global__ void __launch_bounds__(32 * WPB, BWD_MIN_BLOCKS)
-k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const int32_t* __restrict__ n_contrib,
-            const float* __restrict__ gimg, float gscale) {
+k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __restrict__ gimg, float gscale) {
     __shared__ Rec s_rec[WPB][2 * 32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int qx = (lane & 3) * RUN, r0 = lane >> 2;
     const float k2 = -2.0f / (float)LOG2E;     // undo the exp2 scaling: a_k = A k2, e = E k2
+    const float kap = a.clamp;
     RecPipe pipe;
     pipe.buf = s_rec[wib];
-    const float fx0 = (float)qx;
-    const float fy[2] = {(float)r0, (float)(r0 + 8)};
     for (;;) {
         int tile = 0;
         if (lane == 0) tile = (int)atomicAdd(&w.ctr[8], 1ull);
         tile = __shfl_sync(0xffffffffu, tile, 0);
         if (tile >= w.ntiles) break;
         const int ox = (tile % w.ntx) * TILE, oy = (tile / w.ntx) * TILE;
-        const int gx0 = ox + qx;
-        // per-pixel state: T, gD = g . (I - prefix colour), g = dL/dI, entries left
+        const int gx0 = ox + qx, gy0 = oy + r0;
+        const float gx0f = (float)gx0, gy0f = (float)gy0;
+        // per-pixel state: T (as in the forward), gD = g . (I - prefix colour), g = dL/dI
         float T[2][RUN], gD[2][RUN], Gr[2][RUN], Gg[2][RUN], Gb[2][RUN];
-        int rem[2][RUN];
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
             for (int j = 0; j < RUN; ++j) {
-                T[h][j] = 1.f;
+                T[h][j] = -1.f;
                 gD[h][j] = Gr[h][j] = Gg[h][j] = Gb[h][j] = 0.f;
-                rem[h][j] = 0;
-                const int gy = oy + r0 + 8 * h;
+                const int gy = gy0 + 8 * h;
                 if (gy < a.H && gx0 + j < a.W) {
                     const int64_t p = (int64_t)gy * a.W + gx0 + j;
-                    rem[h][j] = n_contrib[p];
+                    T[h][j] = 1.f;
                     Gr[h][j] = gimg[3 * p] * gscale;
                     Gg[h][j] = gimg[3 * p + 1] * gscale;
                     Gb[h][j] = gimg[3 * p + 2] * gscale;
@@ -324,7 +442,6 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const int32_t* _
                 }
             }
         const int start = w.tile_start[tile], end = w.tile_last[tile];
-        const float oxf = (float)ox, oyf = (float)oy;
         pipe.start = start;
         pipe.end = end;
         pipe.begin(w, lane);
@@ -333,7 +450,7 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const int32_t* _
 #pragma unroll
             for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int j = 0; j < RUN; ++j) alive |= rem[h][j] > 0;
+                for (int j = 0; j < RUN; ++j) alive |= T[h][j] >= a.tmin;
             if (!__any_sync(0xffffffffu, alive)) break;
             const Rec* sr = pipe.next(w, b, lane);
             const int nb = min(32, end - base);
@@ -342,78 +459,62 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const int32_t* _
                 const float4 q1 = *(const float4*)&sr[k].A;          // A s E op
                 const float4 q2 = *(const float4*)&sr[k].c0;         // c0 c1 c2 z
                 const int4 q3 = *(const int4*)&sr[k].bbx;            // bbx bby id ebase
-                // record in the (mx, my, A, s) (E, op, c0, c1) (c2, z) layout the math below uses
-                const float4 qa = make_float4((q0.x - oxf) + q0.z, (q0.y - oyf) + q0.w, q1.x, q1.y);
-                const float4 qb = make_float4(q1.z, q1.w, q2.x, q2.y);
-                const float4 qc = make_float4(q2.z, q2.w, 0.f, 0.f);
-                const float2 qd = make_float2(q1.x * k2, q1.z * k2);
-                const int bby = q3.y, bbx = q3.x;
-                const int y0 = (bby & 0xffff) - oy, y1 = (bby >> 16) - oy;
-                const int lo = max((bbx & 0xffff) - gx0, 0), hi = min((bbx >> 16) - gx0, RUN);
-                bool inx[RUN];
+                const int cx0 = (q3.x & 0xffff) - gx0, cx1 = (q3.x >> 16) - gx0;
+                const int ry0 = (q3.y & 0xffff) - gy0, ry1 = (q3.y >> 16) - gy0;
+                const bool row0 = ry0 <= 0 && ry1 > 0, row1 = ry0 <= 8 && ry1 > 8;
+                const bool over = alive && cx0 < RUN && cx1 > 0 && (row0 || row1);
+                // accumulators: colour (3, x clamp) and the moments sum gd, gd u,
+                // gd dy, gd u^2, gd u dy, gd dy^2 with gd = alpha dL/dalpha
+                float c[3] = {0.f, 0.f, 0.f}, M[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                if (over) {
+                    float thr[RUN];
 #pragma unroll
-                for (int j = 0; j < RUN; ++j) inx[j] = j >= lo && j < hi;
-                // accumulators: colour (3), sum gd, sum gd v0, sum gd v1, sum gd v0^2,
-                // sum gd v0 v1, sum gd v1^2 with gd = G dalpha and v = conic d
-                // (op is factored out and applied once per record below)
-                float acc[9];
+                    for (int j = 0; j < RUN; ++j) thr[j] = col_thr(j, cx0, cx1, a.tmin);
+                    const Frame f = frame_of(q0, q1.w, gx0f, gy0f, a.lgk);
+                    const float c0 = __fmul_rn(kap, q2.x), c1 = __fmul_rn(kap, q2.y), c2 = __fmul_rn(kap, q2.z);
 #pragma unroll
-                for (int c = 0; c < 9; ++c) acc[c] = 0.f;
-                bool any = false;
+                    for (int h = 0; h < 2; ++h) {
+                        if (!(h ? row1 : row0)) continue;
+                        float dy, u0, edy;
+                        row_terms(f, q1.y, q1.z, 8.f * h, dy, u0, edy);
+                        float S0 = 0.f, S1 = 0.f, S2 = 0.f;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int row = r0 + 8 * h;
-                    if (row < y0 || row >= y1 || lo >= hi) continue;
-                    const float dy = fy[h] - qa.y;
-                    const float u0 = fmaf(qa.w, dy, fx0 - qa.x);
-                    const float edy = qb.x * dy * dy;
-                    const float ey = qd.y * dy;
-                    // branch-free per pixel: entries outside the bbox, past the
-                    // pixel's processed count, or below alpha_cut get alpha = 0,
-                    // which leaves T, gD and every accumulator unchanged
-#pragma unroll
-                    for (int j = 0; j < RUN; ++j) {
-                        const bool in = inx[j] && rem[h][j] > 0;
-                        rem[h][j] -= in ? 1 : 0;
-                        any |= in;
-                        const float u = j == 0 ? u0 : u0 + (float)j;
-                        const float G = ex2_approx(fmaf(qa.z, u * u, edy));
-                        const float al0 = fminf(qb.y * G, a.clamp);
-                        const bool take = in && al0 >= a.cut;
-                        const float al = take ? al0 : 0.f;
-                        const float t = T[h][j];
-                        const float wt = t * al;
-                        const float gc = fmaf(Gr[h][j], qb.z, fmaf(Gg[h][j], qb.w, Gb[h][j] * qc.x));
-                        gD[h][j] = fmaf(-wt, gc, gD[h][j]);               // g . suffix colour after k
-                        const float da = fmaf(t, gc, -gD[h][j] * rcp_approx(1.f - al));
-                        acc[0] = fmaf(wt, Gr[h][j], acc[0]);
-                        acc[1] = fmaf(wt, Gg[h][j], acc[1]);
-                        acc[2] = fmaf(wt, Gb[h][j], acc[2]);
-                        // clamp gate (_kernels.py:201): saturated alpha passes no geometry gradient
-                        const float gd = (take && al < a.clamp) ? G * da : 0.f;
-                        const float v0 = qd.x * u;                  // (conic d)_x = a_k u
-                        const float v1 = fmaf(qa.w, v0, ey);        // (conic d)_y = s v0 + e dy
-                        const float g0 = gd * v0, g1 = gd * v1;
-                        acc[3] += gd;
-                        acc[4] += g0;
-                        acc[5] += g1;
-                        acc[6] = fmaf(g0, v0, acc[6]);
-                        acc[7] = fmaf(g0, v1, acc[7]);
-                        acc[8] = fmaf(g1, v1, acc[8]);
-                        T[h][j] = fmaf(-al, t, t);
+                        for (int j = 0; j < RUN; ++j) {
+                            float u;
+                            const float al = alpha_sat(q1.x, u0, edy, j, u);
+                            bwd_pixel(al, u, thr[j], a.cutp, -kap, a.ik, c0, c1, c2, Gr[h][j], Gg[h][j], Gb[h][j],
+                                      T[h][j], gD[h][j], c[0], c[1], c[2], S0, S1, S2);
+                        }
+                        M[0] += S0;
+                        M[1] += S1;
+                        M[2] = fmaf(S0, dy, M[2]);
+                        M[3] += S2;
+                        M[4] = fmaf(S1, dy, M[4]);
+                        M[5] = fmaf(S0 * dy, dy, M[5]);
                     }
                 }
                 float val = 0.f;
-                if (__any_sync(0xffffffffu, any)) {
+                if (__any_sync(0xffffffffu, over)) {
+                    // moments -> conic-space sums with v0 = a_k u, v1 = s v0 + e dy
+                    const float ak = q1.x * k2, ek = q1.z * k2, sa = q1.y * ak;
+                    float v[9];
+                    v[0] = c[0];
+                    v[1] = c[1];
+                    v[2] = c[2];
+                    v[3] = M[0];
+                    v[4] = ak * M[1];
+                    v[5] = fmaf(sa, M[1], ek * M[2]);
+                    v[6] = ak * ak * M[3];
+                    v[7] = ak * fmaf(sa, M[3], ek * M[4]);
+                    v[8] = fmaf(sa * sa, M[3], fmaf(2.f * sa * ek, M[4], ek * ek * M[5]));
                     // index i of the 8-vector lands in lanes 4i..4i+3 (reduce8)
-                    const float r8 = reduce8(acc, lane);
-                    float r9 = acc[8];
+                    const float r8 = reduce8(v, lane);
+                    float r9 = v[8];
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) r9 += __shfl_xor_sync(0xffffffffu, r9, o);
                     val = __shfl_sync(0xffffffffu, r8, 4 * min(lane, 7));
                     if (lane == 8) val = r9;
-                    const float op = qb.y;
-                    val *= (lane < 4) ? 1.f : ((lane < 6) ? op : 0.5f * op);
+                    val *= (lane < 3) ? kap : ((lane == 3) ? 1.f / q1.w : ((lane < 6) ? 1.f : 0.5f));
                 }
                 if (lane < NUM_PART) w.part[(int64_t)w.tile_e[base + k] * NUM_PART + lane] = val;
             }
@@ -425,6 +526,15 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const int32_t* _
         for (int j = max(end, start); j < fin; ++j)
             if (lane < NUM_PART) w.part[(int64_t)w.tile_e[j] * NUM_PART + lane] = 0.f;
     }
+}
+
+static BlendArgs blend_args(const lsb_settings& s, int W, int H) {
+    BlendArgs a{W, H, (float)s.alpha_clamp, (float)s.transmittance_min, (float)s.alpha_cut,
+                (float)s.background[0], (float)s.background[1], (float)s.background[2], 0.f, 0.f, 0.f};
+    a.cutp = (float)(s.alpha_cut / s.alpha_clamp);
+    a.lgk = (float)(-log2(s.alpha_clamp));
+    a.ik = (float)(1.0 / s.alpha_clamp);
+    return a;
 }
 
 // CTAs to launch for a persistent tile-warp kernel: every resident slot once.
@@ -441,8 +551,7 @@ static int persistent_grid(const void* fn, int ntiles) {
 cudaError_t launch_blend_fwd(const Ws& w, const lsb_settings& s, int W, int H, float* image, float* t_final,
                              int32_t* n_contrib, float* depth, const float* observed, int kind, float gscale,
                              float* grad, double* loss_out, cudaStream_t st) {
-    BlendArgs a{W, H, (float)s.alpha_clamp, (float)s.transmittance_min, (float)s.alpha_cut,
-                (float)s.background[0], (float)s.background[1], (float)s.background[2]};
+    const BlendArgs a = blend_args(s, W, H);
     LossArgs L{observed, grad, w.loss_part, loss_out, w.ctr + 5, kind, gscale};
     // reset the loss done-count and the forward tile queue ([5], [7])
     cudaError_t e = cudaMemsetAsync(w.ctr + 5, 0, 3 * sizeof(unsigned long long), st);
@@ -464,12 +573,12 @@ cudaError_t launch_blend_fwd(const Ws& w, const lsb_settings& s, int W, int H, f
 
 cudaError_t launch_blend_bwd(const Ws& w, const lsb_settings& s, int W, int H, const float* image,
                              const int32_t* n_contrib, const float* gimg, float gscale, cudaStream_t st) {
-    BlendArgs a{W, H, (float)s.alpha_clamp, (float)s.transmittance_min, (float)s.alpha_cut,
-                (float)s.background[0], (float)s.background[1], (float)s.background[2]};
+    (void)n_contrib;    // liveness is recomputed bit-identically from T
+    const BlendArgs a = blend_args(s, W, H);
     cudaError_t e = cudaMemsetAsync(w.ctr + 8, 0, sizeof(unsigned long long), st);   // backward tile queue
     if (e != cudaSuccess) return e;
-    k_blend_bwd<<<persistent_grid((const void*)k_blend_bwd, w.ntiles), 32 * WPB, 0, st>>>(w, a, image, n_contrib,
-                                                                                         gimg, gscale);
+    k_blend_bwd<<<persistent_grid((const void*)k_blend_bwd, w.ntiles), 32 * WPB, 0, st>>>(w, a, image, gimg,
+                                                                                         gscale);
     return cudaGetLastError();
 }
 
