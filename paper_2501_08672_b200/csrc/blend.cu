@@ -238,9 +238,12 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
     // persistent tile-warp: pull tiles from the queue until it is empty
     for (;;) {
         int tile = 0;
-        if (lane == 0) tile = (int)atomicAdd(&w.ctr[7], 1ull);
+        if (lane == 0) {
+            const int q = (int)atomicAdd(&w.ctr[7], 1ull);
+            tile = q < w.ntiles ? w.tile_order[q] : -1;
+        }
         tile = __shfl_sync(0xffffffffu, tile, 0);
-        if (tile >= w.ntiles) break;
+        if (tile < 0) break;
         const int ox = (tile % w.ntx) * TILE, oy = (tile / w.ntx) * TILE;
         const int gx0 = ox + qx, gy0 = oy + r0;
         const float gx0f = (float)gx0, gy0f = (float)gy0;
@@ -357,8 +360,8 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
         if (lane == 0) {
             L.sums[2 * tile] = l0;
             L.sums[2 * tile + 1] = l1;
-            __threadfence();       // publish the tile partial before counting the tile done
-            done = atomicAdd(L.ticket, 1ull);
+            // release: the tile partial is visible before the tile counts as done
+            asm volatile("atom.release.gpu.global.add.u64 %0, [%1], 1;" : "=l"(done) : "l"(L.ticket) : "memory");
         }
         done = __shfl_sync(0xffffffffu, done, 0);
         if (done != (unsigned long long)w.ntiles - 1) continue;
@@ -417,9 +420,12 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __r
     pipe.buf = s_rec[wib];
     for (;;) {
         int tile = 0;
-        if (lane == 0) tile = (int)atomicAdd(&w.ctr[8], 1ull);
+        if (lane == 0) {
+            const int q = (int)atomicAdd(&w.ctr[8], 1ull);
+            tile = q < w.ntiles ? w.tile_order[q] : -1;
+        }
         tile = __shfl_sync(0xffffffffu, tile, 0);
-        if (tile >= w.ntiles) break;
+        if (tile < 0) break;
         const int ox = (tile % w.ntx) * TILE, oy = (tile / w.ntx) * TILE;
         const int gx0 = ox + qx, gy0 = oy + r0;
         const float gx0f = (float)gx0, gy0f = (float)gy0;

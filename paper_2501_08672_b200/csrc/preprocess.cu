@@ -325,6 +325,34 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(Ws w) {
         __syncthreads();
     }
     if (tid == 0) w.tile_start[w.ntiles] = s_carry;
+    // Processing order of the persistent blend kernels: a counting sort of
+    // the tiles by descending list length (4-entry buckets), so the longest
+    // tiles start first and the tail of the tile queue is short work.
+    __shared__ int s_hist[256];
+    if (tid < 256) s_hist[tid] = 0;
+    __syncthreads();
+    auto key = [](int c) { return 255 - min(c >> 2, 255); };
+    for (int t = tid; t < w.ntiles; t += 1024) atomicAdd(&s_hist[key(w.tile_count[t])], 1);
+    __syncthreads();
+    if (warp == 0) {
+        int loc[8], sum = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            loc[i] = sum;
+            sum += s_hist[8 * lane + i];
+        }
+        int x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        const int excl = x - sum;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s_hist[8 * lane + i] = excl + loc[i];
+    }
+    __syncthreads();
+    for (int t = tid; t < w.ntiles; t += 1024) w.tile_order[atomicAdd(&s_hist[key(w.tile_count[t])], 1)] = t;
 }
 
 // Scatter every (tile, splat) intersection into its tile's bucket, one thread
