@@ -458,6 +458,8 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __r
 #pragma unroll
                 for (int j = 0; j < RUN; ++j) alive |= T[h][j] >= a.tmin;
             if (!__any_sync(0xffffffffu, alive)) break;
+            // intersection ids of this batch, one per lane (written per record below)
+            const int ecur = base + lane < end ? w.tile_e[base + lane] : 0;
             const Rec* sr = pipe.next(w, b, lane);
             const int nb = min(32, end - base);
             for (int k = 0; k < nb; ++k) {
@@ -472,25 +474,32 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __r
                 // accumulators: colour (3, x clamp) and the moments sum gd, gd u,
                 // gd dy, gd u^2, gd u dy, gd dy^2 with gd = alpha dL/dalpha
                 float c[3] = {0.f, 0.f, 0.f}, M[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                if (over) {
+                const bool wover = __any_sync(0xffffffffu, over);
+                if (wover) {
+                    // warp-uniform from here: lanes without work get +inf thresholds
                     float thr[RUN];
 #pragma unroll
-                    for (int j = 0; j < RUN; ++j) thr[j] = col_thr(j, cx0, cx1, a.tmin);
+                    for (int j = 0; j < RUN; ++j) thr[j] = over ? col_thr(j, cx0, cx1, a.tmin) : __int_as_float(0x7f800000);
                     const Frame f = frame_of(q0, q1.w, gx0f, gy0f, a.lgk);
                     const float c0 = __fmul_rn(kap, q2.x), c1 = __fmul_rn(kap, q2.y), c2 = __fmul_rn(kap, q2.z);
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        if (!(h ? row1 : row0)) continue;
+                        const bool rin = over && (h ? row1 : row0);
                         float dy, u0, edy;
                         row_terms(f, q1.y, q1.z, 8.f * h, dy, u0, edy);
+                        float al[RUN], uu[RUN];
+#pragma unroll
+                        for (int j = 0; j < RUN; ++j) al[j] = alpha_sat(q1.x, u0, edy, j, uu[j]);
+                        // skip the half-tile when no pixel of it can reach alpha_cut
+                        // (a superset of the exact per-pixel test applied below)
+                        const float amax = fmaxf(fmaxf(al[0], al[1]), fmaxf(al[2], al[3]));
+                        if (!__any_sync(0xffffffffu, rin && amax >= a.cutp)) continue;
+                        if (!rin) continue;
                         float S0 = 0.f, S1 = 0.f, S2 = 0.f;
 #pragma unroll
-                        for (int j = 0; j < RUN; ++j) {
-                            float u;
-                            const float al = alpha_sat(q1.x, u0, edy, j, u);
-                            bwd_pixel(al, u, thr[j], a.cutp, -kap, a.ik, c0, c1, c2, Gr[h][j], Gg[h][j], Gb[h][j],
-                                      T[h][j], gD[h][j], c[0], c[1], c[2], S0, S1, S2);
-                        }
+                        for (int j = 0; j < RUN; ++j)
+                            bwd_pixel(al[j], uu[j], thr[j], a.cutp, -kap, a.ik, c0, c1, c2, Gr[h][j], Gg[h][j],
+                                      Gb[h][j], T[h][j], gD[h][j], c[0], c[1], c[2], S0, S1, S2);
                         M[0] += S0;
                         M[1] += S1;
                         M[2] = fmaf(S0, dy, M[2]);
@@ -500,7 +509,7 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __r
                     }
                 }
                 float val = 0.f;
-                if (__any_sync(0xffffffffu, over)) {
+                if (wover) {
                     // moments -> conic-space sums with v0 = a_k u, v1 = s v0 + e dy
                     const float ak = q1.x * k2, ek = q1.z * k2, sa = q1.y * ak;
                     float v[9];
@@ -520,17 +529,18 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __r
                     for (int o = 16; o > 0; o >>= 1) r9 += __shfl_xor_sync(0xffffffffu, r9, o);
                     val = __shfl_sync(0xffffffffu, r8, 4 * min(lane, 7));
                     if (lane == 8) val = r9;
-                    val *= (lane < 3) ? kap : ((lane == 3) ? 1.f / q1.w : ((lane < 6) ? 1.f : 0.5f));
+                    val *= (lane < 3) ? kap : ((lane == 3) ? rcp_approx(q1.w) : ((lane < 6) ? 1.f : 0.5f));
                 }
-                if (lane < NUM_PART) w.part[(int64_t)w.tile_e[base + k] * NUM_PART + lane] = val;
+                const int e = __shfl_sync(0xffffffffu, ecur, k);
+                if (lane < NUM_PART) w.part[(int64_t)e * NUM_PART + lane] = val;
             }
             __syncwarp();
         }
         pipe.drain();
         // intersections the walk never reached contribute nothing
-        const int fin = w.tile_start[tile + 1];
-        for (int j = max(end, start); j < fin; ++j)
-            if (lane < NUM_PART) w.part[(int64_t)w.tile_e[j] * NUM_PART + lane] = 0.f;
+        const int fin = w.tile_start[tile + 1], from = max(end, start);
+        for (int q = lane; q < (fin - from) * NUM_PART; q += 32)
+            w.part[(int64_t)w.tile_e[from + q / NUM_PART] * NUM_PART + q % NUM_PART] = 0.f;
     }
 }
 
