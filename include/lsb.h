@@ -63,7 +63,13 @@ typedef struct lsb_settings {
     double max_footprint_px;
     double background[3];
     int32_t sh_degree;
-    int32_t _pad;
+    /* Tile-list mode.  0: every splat whose footprint bbox touches the tile
+     * (the reference's per-pixel CSR lists, _kernels.py:21-59; n_contrib is
+     * the reference's processed-entry count).  1 (only with alpha_cut > 0):
+     * only splats whose alpha >= alpha_cut ellipse can reach a pixel of the
+     * tile — the entries the blend could composite; image, T, depth and
+     * gradients are bit-identical to mode 0, n_contrib counts list entries. */
+    int32_t bin_mode;
 } lsb_settings;
 
 /* World->camera rigid transform T_cw (SE3, geometry.py:125-171): p_c = R p_w + t.

@@ -440,3 +440,62 @@ def tile_lists(cache, tile: int = 16):
     starts = np.searchsorted(tiles_sorted, np.arange(tx_n * ty_n), side="left")
     ends = np.searchsorted(tiles_sorted, np.arange(tx_n * ty_n), side="right")
     return np.column_stack([starts, ends]), entries, cache["ids"][entries]
+
+
+def contributing_tile_rows(cache, tile: int = 16):
+    """CPU restatement of the bin_mode-1 tile sets (csrc/preprocess.cu
+    cull_row_cols; no reference counterpart).  A pair (pixel, splat) is
+    composited by _kernels.py:104 only if q = d^T cov_i^-1 d <= 2 ln(op/cut);
+    per tile row the tiles whose rows can reach that ellipse (threshold with
+    the kernel's margin x1.001 + 0.01) form one column interval, clipped to the
+    bbox.  Returns a list per sorted splat of (ty, tx0, tx1) rows."""
+    st = cache["st"]
+    assert st.alpha_cut > 0.0
+    mu, cov, bb, op = cache["mu_i"], cache["cov_i"], cache["bboxes"], cache["opac"]
+    out = []
+    for s in range(len(bb)):
+        x0, x1, y0, y1 = (int(v) for v in bb[s])
+        mux, muy = float(mu[s, 0]), float(mu[s, 1])
+        ca, cb, cc = float(cov[s, 0, 0]), float(cov[s, 0, 1]), float(cov[s, 1, 1])
+        thr = 2.0 * np.log(max(float(op[s]) / st.alpha_cut, 1.0)) * 1.001 + 0.01
+        rows = []
+        for ty in range(y0 // tile, (y1 - 1) // tile + 1):
+            ya, yb = max(ty * tile, y0), min(ty * tile + tile - 1, y1 - 1)
+            hy = np.sqrt(thr * cc)
+            da, db = max(ya - muy, -hy), min(yb - muy, hy)
+            if not da <= db:
+                continue
+            det = ca * cc - cb * cb
+            k, w2 = cb / cc, det / cc
+            dyr = cb * np.sqrt(thr / ca)
+            dr, dl = min(max(dyr, da), db), min(max(-dyr, da), db)
+            xr = k * dr + np.sqrt(max(w2 * (thr - dr * dr / cc), 0.0))
+            xl = k * dl - np.sqrt(max(w2 * (thr - dl * dl / cc), 0.0))
+            c0, c1 = max(x0, int(np.ceil(mux + xl))), min(x1 - 1, int(np.floor(mux + xr)))
+            if c0 <= c1:
+                rows.append((ty, c0 // tile, c1 // tile))
+        out.append(rows)
+    return out
+
+
+def contributing_tile_lists(cache, tile: int = 16):
+    """tile_lists() for bin_mode 1: the same (ranges, entries, ids) triple
+    over the contributing tile sets of contributing_tile_rows()."""
+    cam = cache["cam"]
+    tx_n = (cam.width + tile - 1) // tile
+    ty_n = (cam.height + tile - 1) // tile
+    rows = contributing_tile_rows(cache, tile)
+    tiles, rank = [], []
+    for s, rs in enumerate(rows):
+        for ty, a, b in rs:
+            t = ty * tx_n + np.arange(a, b + 1)
+            tiles.append(t)
+            rank.append(np.full(len(t), s, np.int64))
+    tiles = np.concatenate(tiles) if tiles else np.zeros(0, np.int64)
+    rank = np.concatenate(rank) if rank else np.zeros(0, np.int64)
+    order = np.argsort(tiles, kind="stable")
+    tiles_sorted = tiles[order]
+    entries = rank[order]
+    starts = np.searchsorted(tiles_sorted, np.arange(tx_n * ty_n), side="left")
+    ends = np.searchsorted(tiles_sorted, np.arange(tx_n * ty_n), side="right")
+    return np.column_stack([starts, ends]), entries, cache["ids"][entries]

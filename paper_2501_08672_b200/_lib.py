@@ -31,7 +31,7 @@ class Settings(_c.Structure):
     _fields_ = [("near_plane", _c.c_double), ("dilation", _c.c_double), ("alpha_clamp", _c.c_double),
                 ("transmittance_min", _c.c_double), ("footprint_sigma", _c.c_double),
                 ("alpha_cut", _c.c_double), ("max_footprint_px", _c.c_double),
-                ("background", _c.c_double * 3), ("sh_degree", _c.c_int32), ("_pad", _c.c_int32)]
+                ("background", _c.c_double * 3), ("sh_degree", _c.c_int32), ("bin_mode", _c.c_int32)]
 
 
 class Pose(_c.Structure):
@@ -175,11 +175,13 @@ def make_camera(cam) -> Camera:
                   int(cam.height))
 
 
-def make_settings(s) -> Settings:
+def make_settings(s, bin_mode: int = 0) -> Settings:
+    """RasterSettings -> lsb_settings.  bin_mode 1 (contributing tile lists)
+    only takes effect with alpha_cut > 0 (include/lsb.h)."""
     bg = np.asarray(s.background, dtype=np.float64).reshape(3)
     return Settings(float(s.near), float(s.dilation), float(s.alpha_clamp), float(s.transmittance_min),
                     float(s.footprint_sigma), float(s.alpha_cut), float(s.max_footprint_px),
-                    (ctypes.c_double * 3)(*bg.tolist()), int(s.sh_degree), 0)
+                    (ctypes.c_double * 3)(*bg.tolist()), int(s.sh_degree), int(bin_mode))
 
 
 def make_pose(R_cw: np.ndarray, t_cw: np.ndarray) -> Pose:

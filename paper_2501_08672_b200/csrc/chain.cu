@@ -86,8 +86,7 @@ __global__ void __launch_bounds__(256) k_part_reduce(Ws w) {
     for (int64_t slot = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; slot < M; slot += nw) {
         const Rec& r = w.rec[slot];
         if (r.ebase < 0) continue;
-        const int nt = ((((r.bbx >> 16) - 1) >> 4) - ((r.bbx & 0xffff) >> 4) + 1) *
-                       ((((r.bby >> 16) - 1) >> 4) - ((r.bby & 0xffff) >> 4) + 1);
+        const int nt = w.vis_ebase[slot + 1] - r.ebase;      // this splat's intersections
         double q[NUM_PART];
 #pragma unroll
         for (int c = 0; c < NUM_PART; ++c) q[c] = 0.0;

@@ -29,6 +29,14 @@ struct __align__(16) Rec {
 };
 static_assert(sizeof(Rec) == 64, "Rec must be 64 bytes");
 
+// Footprint of a splat's alpha >= alpha_cut region for the contributing-list
+// binning mode (lsb_settings.bin_mode = 1): the ellipse
+// d^T cov_i^-1 d <= thr around mu_i, f64 (written by the preprocess, re-read
+// by the scatter so both enumerate the same tiles).
+struct CullGeo {
+    double mux, muy, ca, cb, cc, thr;
+};
+
 struct Ws {
     unsigned long long* ctr;    // [0] M, [1] I, [2] overflow, [3] preprocess ticket, [4] chain ticket,
                                 // [5] fused-loss tiles done, [6] big-tile count, [7] fwd / [8] bwd tile queues
@@ -51,6 +59,7 @@ struct Ws {
     int32_t* big_tiles;         // [ntiles] tiles queued for the shared-memory sort
     int32_t* tile_order;        // [ntiles] blend processing order: heaviest tiles first
     double* qsum;               // [n * NUM_PART] per-splat sums of the intersection partials
+    CullGeo* cgeo;              // [n] alpha_cut ellipses (bin_mode 1 only)
     int64_t n, cap;
     int32_t ntx, nty, ntiles, nblocks_pre;
 };
@@ -98,6 +107,7 @@ inline size_t carve(const lsb_dims& d, char* base, Ws* w) {
     t.big_tiles = (int32_t*)take(sizeof(int32_t) * t.ntiles);
     t.tile_order = (int32_t*)take(sizeof(int32_t) * t.ntiles);
     t.qsum = (double*)take(sizeof(double) * NUM_PART * n);
+    t.cgeo = (CullGeo*)take(sizeof(CullGeo) * n);
     if (w) *w = t;
     return off;
 }

@@ -18,7 +18,61 @@ struct PreArgs {
     lsb_pose T;
     lsb_settings s;
     int degree;
+    int cull;          // bin_mode 1 with alpha_cut > 0: contributing tile lists
 };
+
+// ---- contributing-list binning (bin_mode 1) ---------------------------------
+// The blend composites a (pixel, splat) pair only if op g >= alpha_cut, i.e.
+// q = d^T cov_i^-1 d <= 2 ln(op / cut) (_kernels.py:104 with the alpha clamp
+// folded out).  A tile whose pixels all lie outside that ellipse contributes
+// nothing, so mode 1 drops it from the splat's tile set.  The threshold gets a
+// margin (0.1% + 0.01) far above the f32 rounding of the blend's own test, so
+// no pair the blend would composite is ever dropped: image, T, depth and
+// gradients stay bit-identical to the full lists (the dropped entries add
+// exact zeros).
+
+__device__ __forceinline__ double cull_thr(double op, double cut) {
+    return 2.0 * log(fmax(op / cut, 1.0)) * 1.001 + 0.01;
+}
+
+// Pixel columns [c0, c1] of the ellipse over the pixel rows [ya, yb], clipped
+// to the bbox columns [x0, x1).  Rows are relaxed to the continuous band
+// (a superset); over a band the right edge k dy + w(dy) is concave in dy, so
+// its maximum is at the ellipse's rightmost point dy = cb sqrt(thr / ca)
+// clamped to the band (mirror for the left edge).
+__device__ __forceinline__ bool cull_row_cols(const CullGeo& g, int ya, int yb, int x0, int x1, int& c0, int& c1) {
+    const double hy = sqrt(g.thr * g.cc);
+    const double da = fmax((double)ya - g.muy, -hy), db = fmin((double)yb - g.muy, hy);
+    if (!(da <= db)) return false;
+    const double det = g.ca * g.cc - g.cb * g.cb;
+    const double k = g.cb / g.cc, w2 = det / g.cc;
+    const double dyr = g.cb * sqrt(g.thr / g.ca);
+    const double dr = fmin(fmax(dyr, da), db), dl = fmin(fmax(-dyr, da), db);
+    const double xr = k * dr + sqrt(fmax(w2 * (g.thr - dr * dr / g.cc), 0.0));
+    const double xl = k * dl - sqrt(fmax(w2 * (g.thr - dl * dl / g.cc), 0.0));
+    c0 = max(x0, (int)ceil(g.mux + xl));
+    c1 = min(x1 - 1, (int)floor(g.mux + xr));
+    return c0 <= c1;
+}
+
+// Tile range [tx0, tx1] of tile row ty (false if the ellipse misses the row).
+__device__ __forceinline__ bool cull_tile_row(const CullGeo& g, int ty, int x0, int x1, int y0, int y1, int& tx0,
+                                              int& tx1) {
+    int c0, c1;
+    if (!cull_row_cols(g, max(ty * TILE, y0), min(ty * TILE + TILE - 1, y1 - 1), x0, x1, c0, c1)) return false;
+    tx0 = c0 >> 4;
+    tx1 = c1 >> 4;
+    return true;
+}
+
+__device__ int cull_tile_count(const CullGeo& g, int x0, int x1, int y0, int y1) {
+    int n = 0;
+    for (int ty = y0 >> 4; ty <= (y1 - 1) >> 4; ++ty) {
+        int a, b;
+        if (cull_tile_row(g, ty, x0, x1, y0, y1, a, b)) n += b - a + 1;
+    }
+    return n;
+}
 
 __constant__ double c_SH[16] = {
     0.28209479177387814, 0.4886025119029199, 1.0925484305920792, -1.0925484305920792,
@@ -56,7 +110,7 @@ __device__ __forceinline__ void sh_basis(int degree, double x, double y, double 
 // Projection + EWA covariance + footprint (raster.py:134-185) for Gaussian i.
 // Returns false if culled; fills the record, its tile count and depth key.
 __device__ bool splat_one(const PreArgs& a, int64_t i, Rec& r, int& ntiles, uint64_t& key,
-                          uint32_t& cmask) {
+                          uint32_t& cmask, CullGeo& geo) {
     const int f64 = a.p.dtype;
     const double px = pld(a.p.means, 3 * i, f64), py = pld(a.p.means, 3 * i + 1, f64),
                  pz = pld(a.p.means, 3 * i + 2, f64);
@@ -125,7 +179,12 @@ __device__ bool splat_one(const PreArgs& a, int64_t i, Rec& r, int& ntiles, uint
     const double y1 = fmin(floor(muy + radius) + 1.0, H_);
     if (!(x0 < x1 && y0 < y1 && radius <= a.s.max_footprint_px)) return false;
     const int ix0 = (int)x0, ix1 = (int)x1, iy0 = (int)y0, iy1 = (int)y1;
-    ntiles = (((ix1 - 1) >> 4) - (ix0 >> 4) + 1) * (((iy1 - 1) >> 4) - (iy0 >> 4) + 1);
+    if (a.cull) {
+        geo = CullGeo{mux, muy, ca, cb, cc, cull_thr(op, a.s.alpha_cut)};
+        ntiles = cull_tile_count(geo, ix0, ix1, iy0, iy1);
+    } else {
+        ntiles = (((ix1 - 1) >> 4) - (ix0 >> 4) + 1) * (((iy1 - 1) >> 4) - (iy0 >> 4) + 1);
+    }
     // conic = cov_i^-1 = (cc, -cb, ca) / det; exponent in the shear form
     //   q = a_k u^2 + dy^2 / cc,  u = dx - (cb/cc) dy   (no cancellation)
     const double ak = cc / det;
@@ -228,7 +287,8 @@ k_preprocess(PreArgs a, Ws w) {
     int nt = 0;
     uint64_t key = 0;
     uint32_t cm = 0;
-    const bool vis = (i < a.p.n) && splat_one(a, i, r, nt, key, cm);
+    CullGeo geo;
+    const bool vis = (i < a.p.n) && splat_one(a, i, r, nt, key, cm, geo);
     int v = vis ? 1 : 0;
     int tcount = vis ? nt : 0;
     // block-wide exclusive scan of (v, tcount)
@@ -284,10 +344,18 @@ k_preprocess(PreArgs a, Ws w) {
     w.vkey[slot] = key;
     w.colmask[slot] = cm;
     if (!fits) return;
-    const int tx0 = (r.bbx & 0xffff) >> 4, tx1 = ((r.bbx >> 16) - 1) >> 4;
-    const int ty0 = (r.bby & 0xffff) >> 4, ty1 = ((r.bby >> 16) - 1) >> 4;
-    for (int ty = ty0; ty <= ty1; ++ty)
-        for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&w.tile_count[ty * w.ntx + tx], 1);
+    const int x0 = r.bbx & 0xffff, x1 = r.bbx >> 16, y0 = r.bby & 0xffff, y1 = r.bby >> 16;
+    if (a.cull) {
+        w.cgeo[slot] = geo;
+        for (int ty = y0 >> 4; ty <= (y1 - 1) >> 4; ++ty) {
+            int tx0, tx1;
+            if (!cull_tile_row(geo, ty, x0, x1, y0, y1, tx0, tx1)) continue;
+            for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&w.tile_count[ty * w.ntx + tx], 1);
+        }
+        return;
+    }
+    for (int ty = y0 >> 4; ty <= (y1 - 1) >> 4; ++ty)
+        for (int tx = x0 >> 4; tx <= (x1 - 1) >> 4; ++tx) atomicAdd(&w.tile_count[ty * w.ntx + tx], 1);
 }
 
 // Exclusive scan of the tile histogram (single CTA, chunked).
@@ -358,9 +426,9 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(Ws w) {
 // Scatter every (tile, splat) intersection into its tile's bucket, one thread
 // per intersection e: its splat is found by binary search in the exclusive
 // scan vis_ebase (monotone in slot order), its tile is the k-th tile of the
-// splat's bbox in row-major order.  Order inside a bucket is arbitrary here
-// and fixed by the per-tile sort.
-__global__ void __launch_bounds__(256) k_scatter(Ws w) {
+// splat's bbox in row-major order (mode 1: of its contributing tiles, row by
+// row).  Order inside a bucket is arbitrary here and fixed by the per-tile sort.
+__global__ void __launch_bounds__(256) k_scatter(Ws w, int cull) {
     const int64_t M = (int64_t)w.ctr[0];
     const int64_t I = min((int64_t)w.ctr[1], w.cap);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -373,11 +441,28 @@ __global__ void __launch_bounds__(256) k_scatter(Ws w) {
         }
         const Rec& r = w.rec[lo];
         if (r.ebase < 0) continue;           // this splat's run overflowed the capacity
-        const int k = (int)(e - r.ebase);
-        const int tx0 = (r.bbx & 0xffff) >> 4, tx1 = ((r.bbx >> 16) - 1) >> 4;
-        const int ty0 = (r.bby & 0xffff) >> 4;
-        const int nx = tx1 - tx0 + 1;
-        const int t = (ty0 + k / nx) * w.ntx + tx0 + k % nx;
+        int k = (int)(e - r.ebase);
+        int t;
+        if (cull) {
+            const int x0 = r.bbx & 0xffff, x1 = r.bbx >> 16, y0 = r.bby & 0xffff, y1 = r.bby >> 16;
+            const CullGeo g = w.cgeo[lo];
+            t = -1;
+            for (int ty = y0 >> 4; ty <= (y1 - 1) >> 4; ++ty) {
+                int tx0, tx1;
+                if (!cull_tile_row(g, ty, x0, x1, y0, y1, tx0, tx1)) continue;
+                if (k <= tx1 - tx0) {
+                    t = ty * w.ntx + tx0 + k;
+                    break;
+                }
+                k -= tx1 - tx0 + 1;
+            }
+            if (t < 0) continue;             // unreachable: the count came from the same walk
+        } else {
+            const int tx0 = (r.bbx & 0xffff) >> 4, tx1 = ((r.bbx >> 16) - 1) >> 4;
+            const int ty0 = (r.bby & 0xffff) >> 4;
+            const int nx = tx1 - tx0 + 1;
+            t = (ty0 + k / nx) * w.ntx + tx0 + k % nx;
+        }
         const int j = w.tile_start[t] + atomicAdd(&w.tile_cursor[t], 1);
         w.tile_e[j] = (int32_t)e;
         w.emit_slot[e] = (int32_t)lo;
@@ -610,7 +695,7 @@ size_t tile_sort_smem() { return SORT_CAP * (sizeof(uint64_t) + 2 * sizeof(int))
 
 cudaError_t launch_preprocess(const lsb_params& p, const lsb_camera& cam, const lsb_pose& T,
                               const lsb_settings& s, const Ws& w, cudaStream_t st) {
-    PreArgs a{p, cam, T, s, 0};
+    PreArgs a{p, cam, T, s, 0, (s.bin_mode == 1 && s.alpha_cut > 0.0) ? 1 : 0};
     int deg_store = 0;
     while ((deg_store + 2) * (deg_store + 2) <= p.sh_coeffs) ++deg_store;
     a.degree = s.sh_degree < deg_store ? s.sh_degree : deg_store;
@@ -618,7 +703,7 @@ cudaError_t launch_preprocess(const lsb_params& p, const lsb_camera& cam, const 
     if (err != cudaSuccess) return err;
     k_preprocess<<<w.nblocks_pre, PRE_THREADS, 0, st>>>(a, w);
     k_scan_tiles<<<1, 1024, 0, st>>>(w);
-    k_scatter<<<8 * 148, 256, 0, st>>>(w);
+    k_scatter<<<8 * 148, 256, 0, st>>>(w, a.cull);
     k_tile_sort<<<(w.ntiles + 3) / 4, 128, 0, st>>>(w);
     cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_sort_smem());
     k_tile_sort_big<<<148, 256, tile_sort_smem(), st>>>(w);

@@ -191,12 +191,19 @@ class WindowEngine:
     Like the reference (optimize.py:142-149) the steps act on an f64 working
     copy of the window (`master="f64"`); `finish()` re-orthonormalises the
     stepped rotations and writes the result back into the f32 arena
-    (optimize.py:193-201).  `master="arena"` steps the arena in place."""
+    (optimize.py:193-201).  `master="arena"` steps the arena in place.
+
+    `bin_mode` 1 (the default when alpha_cut > 0) bins each splat only into
+    the tiles its alpha >= alpha_cut ellipse reaches (include/lsb.h): the
+    step's image, loss and gradients are bit-identical to the full
+    reference-bbox lists (0), with fewer tile entries to blend."""
 
     def __init__(self, arrays: GaussianArrays, cam, views: Sequence, settings: RasterSettings,
                  cfg: OptimConfig = OptimConfig(), n_views_total: Optional[int] = None,
-                 isect_cap: Optional[int] = None, stream=None, master: str = "f64", lanes: int = 1):
+                 isect_cap: Optional[int] = None, stream=None, master: str = "f64", lanes: int = 1,
+                 bin_mode: Optional[int] = None):
         _lib.require()
+        self.bin_mode = (1 if settings.alpha_cut > 0.0 else 0) if bin_mode is None else int(bin_mode)
         self.arena = arrays
         if master == "f64" and arrays.dtype != torch.float64:
             arrays = arrays.clone(torch.float64)
@@ -228,7 +235,7 @@ class WindowEngine:
         for _ in range(self.n_lanes):
             self.lanes.append(SimpleNamespace(
                 stream=torch.cuda.Stream(dev) if self.n_lanes > 1 else stream,
-                state=RenderState(arrays, cam, T0.R, T0.t, settings, isect_cap),
+                state=RenderState(arrays, cam, T0.R, T0.t, settings, isect_cap, self.bin_mode),
                 image=torch.empty((h, w, 3), dtype=torch.float32, device=dev),
                 t_final=torch.empty((h, w), dtype=torch.float32, device=dev),
                 n_contrib=torch.empty((h, w), dtype=torch.int32, device=dev),
@@ -251,7 +258,7 @@ class WindowEngine:
         worst = 0
         for T in self.views:
             while True:
-                st = RenderState(self.arrays, self.cam, T.R, T.t, self.settings, cap)
+                st = RenderState(self.arrays, self.cam, T.R, T.t, self.settings, cap, self.bin_mode)
                 render_bin(st, stream=self.stream)
                 M, I, over, _ = st.read_counts(self.stream)
                 if not over:

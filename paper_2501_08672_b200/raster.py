@@ -206,14 +206,15 @@ class RenderState:
     the reference's cache dict (raster.py:246-258)."""
 
     def __init__(self, arrays: GaussianArrays, cam, R_cw, t_cw, settings: RasterSettings,
-                 isect_cap: int):
+                 isect_cap: int, bin_mode: int = 0):
         self.arrays = arrays
         self.cam = cam
         self.settings = settings
+        self.bin_mode = bin_mode
         self.R_cw = np.asarray(R_cw, dtype=np.float64)
         self.t_cw = np.asarray(t_cw, dtype=np.float64)
         self.c_cam = _lib.make_camera(cam)
-        self.c_set = _lib.make_settings(settings)
+        self.c_set = _lib.make_settings(settings, bin_mode)
         self.c_pose = _lib.make_pose(self.R_cw, self.t_cw)
         self.dims = _lib.Dims(len(arrays), int(cam.width), int(cam.height), int(arrays.shs.shape[1]), TILE,
                               int(isect_cap))
@@ -342,24 +343,27 @@ def render_bwd(state: RenderState, out: "RenderOutput", grad_image: torch.Tensor
 
 
 def render(source, T_wc, cam, settings: RasterSettings = RasterSettings(), retain_cache: bool = True,
-           with_depth: bool = False) -> RenderOutput:
+           with_depth: bool = False, bin_mode: int = 0) -> RenderOutput:
     """Splat, bin, depth-sort per tile and composite (raster.py:212-264).
 
     Synchronises once to size the intersection buffers (the reference API is
-    synchronous too); the multi-view engine (engine.py) avoids that sync."""
+    synchronous too); the multi-view engine (optimize.WindowEngine) avoids
+    that sync.  bin_mode 1 (alpha_cut > 0) bins into contributing tiles only
+    (include/lsb.h): same image / T / depth / gradients, but contrib_count
+    then counts contributing-list entries instead of the reference's."""
     _lib.require()
     arrays = _as_arrays(source)
     T_cw = as_se3(T_wc).inverse()
     dev = arrays.device
     h, w = int(cam.height), int(cam.width)
-    key = (len(arrays), w, h, float(settings.alpha_cut))
+    key = (len(arrays), w, h, float(settings.alpha_cut), int(bin_mode))
     cap = max(_CAP_HINT.get(key, 0), 1 << 16, 8 * len(arrays))
     image = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
     t_final = torch.empty((h, w), dtype=torch.float32, device=dev)
     n_contrib = torch.empty((h, w), dtype=torch.int32, device=dev)
     depth = torch.empty((h, w), dtype=torch.float32, device=dev) if with_depth else None
     while True:
-        state = RenderState(arrays, cam, T_cw.R, T_cw.t, settings, cap)
+        state = RenderState(arrays, cam, T_cw.R, T_cw.t, settings, cap, bin_mode)
         render_fwd(state, image, t_final, n_contrib, depth)
         M, I, overflow, _ = state.read_counts()
         if not overflow:
