@@ -166,6 +166,11 @@ int lsb_render_bwd(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T
 int lsb_render_bin(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T_cw,
                    const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
                    void* stream);
+/* lsb_render_blend / lsb_render_blend_loss accept n_contrib == NULL (with
+ * depth == NULL): no processed-entry count is kept, and the forward skips
+ * half-tiles none of whose pixels reaches alpha_cut (same image / T bits).
+ * lsb_render_blend_bwd does not read n_contrib (liveness is recomputed from
+ * T bit-identically); it may be NULL. */
 int lsb_render_blend(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
                      float* image, float* t_final, int32_t* n_contrib, float* depth, void* stream);
 /* Blend forward fused with the photometric loss (optimize.py:48-74, no mask):

@@ -207,7 +207,8 @@ int lsb_render_bin(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T
 
 int lsb_render_blend(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* d, float* image,
                      float* t_final, int32_t* n_contrib, float* depth, void* stream) {
-    if (!s || !image || !t_final || !n_contrib) return fail(LSB_EINVAL, "NULL argument");
+    if (!s || !image || !t_final) return fail(LSB_EINVAL, "NULL argument");
+    if (!n_contrib && depth) return fail(LSB_EINVAL, "depth needs n_contrib");
     Ws w;
     int rc = get_ws(ws, ws_bytes, d, &w);
     if (rc) return rc;
@@ -218,8 +219,9 @@ int lsb_render_blend(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb
 int lsb_render_blend_loss(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* d, float* image,
                           float* t_final, int32_t* n_contrib, float* depth, const float* observed, int kind,
                           float grad_scale, float* grad_out, double* loss_out, void* stream) {
-    if (!s || !image || !t_final || !n_contrib || !observed || !grad_out || !loss_out)
+    if (!s || !image || !t_final || !observed || !grad_out || !loss_out)
         return fail(LSB_EINVAL, "NULL argument");
+    if (!n_contrib && depth) return fail(LSB_EINVAL, "depth needs n_contrib");
     if (kind != 0 && kind != 1) return fail(LSB_EINVAL, "kind must be 0 (l1) or 1 (l2)");
     Ws w;
     int rc = get_ws(ws, ws_bytes, d, &w);
@@ -233,7 +235,7 @@ int lsb_render_blend_bwd(const lsb_settings* s, void* ws, size_t ws_bytes, const
                          const float* image, const int32_t* n_contrib, const float* grad_image,
                          float grad_scale, void* stream) {
     if (!s) return fail(LSB_EINVAL, "NULL argument");
-    if (!image || !n_contrib || !grad_image) return fail(LSB_EMISSING_CACHE, "render outputs missing");
+    if (!image || !grad_image) return fail(LSB_EMISSING_CACHE, "render outputs missing");
     Ws w;
     int rc = get_ws(ws, ws_bytes, d, &w);
     if (rc) return rc;

@@ -20,9 +20,15 @@
 // op g / clamp), 1/clamp folded into the exponent and clamp into the
 // colours), and the gated updates are predicated instead of selected.
 //
+// Saturation is only possible for a record whose opacity reaches the clamp
+// (op g / clamp >= 1 needs lop = log2(op / clamp) >= 0), so the backward picks
+// per record, warp-uniformly, a path with or without the saturate and the
+// a < 1 gate: for lop < -1e-6 the two paths give the same bits.
+//
 // Forward (_kernels.py:62-119): alpha is evaluated for the whole 4-pixel run
 // and the updates are predicated, so there is no divergence inside the
-// record loop.  Optionally fuses the photometric loss (optimize.py:48-74): the
+// record loop.  Without a processed-entry count (n_contrib == NULL, the
+// window engine) the count update is dropped.  Optionally fuses the photometric loss (optimize.py:48-74): the
 // epilogue reads the observed pixels, writes dL/dI and reduces the loss per
 // tile; the last CTA (ticket) adds the tile sums in tile order.
 //
@@ -50,13 +56,15 @@ constexpr int RUN = 4;       // pixels per lane and row (horizontal run)
 #ifndef BWD_MIN_BLOCKS
 #define BWD_MIN_BLOCKS 4
 #endif
+#ifndef BLEND_RESERVE          // CTA slots per SM the persistent blend grids leave free
+#define BLEND_RESERVE 0           // (for a concurrent view lane's binning / chain kernels)
+#endif
 
 struct BlendArgs {
     int W, H;
     float clamp, tmin, cut;
     float bg0, bg1, bg2;
     float cutp;       // cut / clamp: the test on the saturated alpha
-    float lgk;        // -log2(clamp), added to the exponent
     float ik;         // 1 / clamp
 };
 
@@ -66,19 +74,16 @@ struct Frame {
     float mxr, myr, lop;
 };
 
-__device__ __forceinline__ float lg2_approx(float x) {
-    float y;
-    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
-__device__ __forceinline__ Frame frame_of(float4 q0, float op, float gx0f, float gy0f, float lgk) {
+__device__ __forceinline__ Frame frame_of(float4 q0, float lop, float gx0f, float gy0f) {
     Frame f;
     f.mxr = __fadd_rn(__fsub_rn(q0.x, gx0f), q0.z);
     f.myr = __fadd_rn(__fsub_rn(q0.y, gy0f), q0.w);
-    f.lop = __fadd_rn(lg2_approx(op), lgk);
+    f.lop = lop;
     return f;
 }
+
+// Records with lop below this cannot saturate (a' < 1 for every pixel).
+constexpr float SAT_LOP = -1e-6f;
 
 // Row terms: u0 = x_local + s dy - mx at the run's first pixel, and the
 // row part of the exponent E dy^2 + log2(op / clamp).
@@ -89,10 +94,13 @@ __device__ __forceinline__ void row_terms(const Frame& f, float s, float E, floa
     edy = __fmaf_rn(__fmul_rn(E, dy), dy, f.lop);
 }
 
-// Saturated alpha of pixel j of the run: a = min(1, op g / clamp).
+// Saturated alpha of pixel j of the run: a = min(1, op g / clamp).  With
+// SAT false the record cannot saturate and the min is dropped.
+template <bool SAT = true>
 __device__ __forceinline__ float alpha_sat(float A, float u0, float edy, int j, float& u) {
     u = j == 0 ? u0 : __fadd_rn(u0, (float)j);
-    return __saturatef(ex2_approx(__fmaf_rn(A, __fmul_rn(u, u), edy)));
+    const float e = ex2_approx(__fmaf_rn(A, __fmul_rn(u, u), edy));
+    return SAT ? __saturatef(e) : e;
 }
 
 // Per-column liveness threshold of a record: T must reach t_min for pixels
@@ -121,6 +129,22 @@ __device__ __forceinline__ void fwd_pixel(float al, float thr, float cutp, float
         : "f"(thr), "f"(al), "f"(cutp), "f"(c0), "f"(c1), "f"(c2), "f"(nkap));
 }
 
+// Forward pixel update without the entry count (same T recurrence):
+//   take = T >= thr && a >= cut'  ->  w = T a;  C += w c';  T += w (-clamp)
+__device__ __forceinline__ void fwd_pixel_nc(float al, float thr, float cutp, float nkap, float c0, float c1, float c2,
+                                             float& T, float& cr, float& cg, float& cb) {
+    asm("{\n\t.reg .pred pi, pt;\n\t.reg .f32 w;\n\t"
+        "setp.ge.f32 pi, %0, %4;\n\t"
+        "setp.ge.and.f32 pt, %5, %6, pi;\n\t"
+        "mul.rn.f32 w, %0, %5;\n\t"
+        "@pt fma.rn.f32 %1, w, %7, %1;\n\t"
+        "@pt fma.rn.f32 %2, w, %8, %2;\n\t"
+        "@pt fma.rn.f32 %3, w, %9, %3;\n\t"
+        "@pt fma.rn.f32 %0, w, %10, %0;\n\t}"
+        : "+f"(T), "+f"(cr), "+f"(cg), "+f"(cb)
+        : "f"(thr), "f"(al), "f"(cutp), "f"(c0), "f"(c1), "f"(c2), "f"(nkap));
+}
+
 __device__ __forceinline__ void fwd_pixel_depth(float al, float thr, float cutp, float nkap, float c0, float c1,
                                                 float c2, float zk, float& T, float& cnt, float& cr, float& cg,
                                                 float& cb, float& dz) {
@@ -142,37 +166,48 @@ __device__ __forceinline__ void fwd_pixel_depth(float al, float thr, float cutp,
 //   take: w = T a; gc' = g.c'; gD -= w gc'; dap = T gc' - gD / (1/clamp - a);
 //         colour sums += w g; T += w (-clamp)
 //   gate = take && a < 1 (unclamped): gd = a dap; S0 += gd; S1 += gd u; S2 += gd u^2
+// Without SAT the record cannot saturate and gate == take.
+#define LSB_BWD_BODY(GATE_SETP, GP)                                         \
+    "{\n\t.reg .pred pi, pt, pg;\n\t.reg .f32 w, gc, r, tg, da, gd, gu;\n\t" \
+    "setp.ge.f32 pi, %0, %8;\n\t"                                           \
+    "setp.ge.and.f32 pt, %9, %10, pi;\n\t" GATE_SETP                        \
+    "mul.rn.f32 w, %0, %9;\n\t"                                             \
+    "mul.rn.f32 gc, %20, %15;\n\t"                                          \
+    "fma.rn.f32 gc, %19, %14, gc;\n\t"                                      \
+    "fma.rn.f32 gc, %18, %13, gc;\n\t"                                      \
+    "neg.f32 r, w;\n\t"                                                     \
+    "@pt fma.rn.f32 %1, r, gc, %1;\n\t"                                     \
+    "sub.f32 r, %12, %9;\n\t"                                               \
+    "rcp.approx.ftz.f32 r, r;\n\t"                                          \
+    "mul.rn.f32 tg, %0, gc;\n\t"                                            \
+    "neg.f32 da, %1;\n\t"                                                   \
+    "fma.rn.f32 da, da, r, tg;\n\t"                                         \
+    "@pt fma.rn.f32 %2, w, %18, %2;\n\t"                                    \
+    "@pt fma.rn.f32 %3, w, %19, %3;\n\t"                                    \
+    "@pt fma.rn.f32 %4, w, %20, %4;\n\t"                                    \
+    "mul.rn.f32 gd, %9, da;\n\t"                                            \
+    "mul.rn.f32 gu, gd, %16;\n\t"                                           \
+    "@" GP " add.f32 %5, %5, gd;\n\t"                                       \
+    "@" GP " add.f32 %6, %6, gu;\n\t"                                       \
+    "@" GP " fma.rn.f32 %7, gu, %16, %7;\n\t"                               \
+    "@pt fma.rn.f32 %0, w, %11, %0;\n\t}"
+
+template <bool SAT>
 __device__ __forceinline__ void bwd_pixel(float al, float u, float thr, float cutp, float nkap, float ik, float c0,
                                           float c1, float c2, float Gr, float Gg, float Gb, float& T, float& gD,
                                           float& s0, float& s1, float& s2, float& S0, float& S1, float& S2) {
-    asm("{\n\t.reg .pred pi, pt, pg;\n\t.reg .f32 w, gc, r, tg, da, gd, gu;\n\t"
-        "setp.ge.f32 pi, %0, %8;\n\t"
-        "setp.ge.and.f32 pt, %9, %10, pi;\n\t"
-        "setp.lt.and.f32 pg, %9, 0f3F800000, pt;\n\t"
-        "mul.rn.f32 w, %0, %9;\n\t"
-        "mul.rn.f32 gc, %20, %15;\n\t"
-        "fma.rn.f32 gc, %19, %14, gc;\n\t"
-        "fma.rn.f32 gc, %18, %13, gc;\n\t"
-        "neg.f32 r, w;\n\t"
-        "@pt fma.rn.f32 %1, r, gc, %1;\n\t"
-        "sub.f32 r, %12, %9;\n\t"
-        "rcp.approx.ftz.f32 r, r;\n\t"
-        "mul.rn.f32 tg, %0, gc;\n\t"
-        "neg.f32 da, %1;\n\t"
-        "fma.rn.f32 da, da, r, tg;\n\t"
-        "@pt fma.rn.f32 %2, w, %18, %2;\n\t"
-        "@pt fma.rn.f32 %3, w, %19, %3;\n\t"
-        "@pt fma.rn.f32 %4, w, %20, %4;\n\t"
-        "mul.rn.f32 gd, %9, da;\n\t"
-        "mul.rn.f32 gu, gd, %16;\n\t"
-        "@pg add.f32 %5, %5, gd;\n\t"
-        "@pg add.f32 %6, %6, gu;\n\t"
-        "@pg fma.rn.f32 %7, gu, %16, %7;\n\t"
-        "@pt fma.rn.f32 %0, w, %11, %0;\n\t}"
-        : "+f"(T), "+f"(gD), "+f"(s0), "+f"(s1), "+f"(s2), "+f"(S0), "+f"(S1), "+f"(S2)
-        : "f"(thr), "f"(al), "f"(cutp), "f"(nkap), "f"(ik), "f"(c0), "f"(c1), "f"(c2), "f"(u), "f"(0.f),
-          "f"(Gr), "f"(Gg), "f"(Gb));
+    if (SAT)
+        asm(LSB_BWD_BODY("setp.lt.and.f32 pg, %9, 0f3F800000, pt;\n\t", "pg")
+            : "+f"(T), "+f"(gD), "+f"(s0), "+f"(s1), "+f"(s2), "+f"(S0), "+f"(S1), "+f"(S2)
+            : "f"(thr), "f"(al), "f"(cutp), "f"(nkap), "f"(ik), "f"(c0), "f"(c1), "f"(c2), "f"(u), "f"(0.f),
+              "f"(Gr), "f"(Gg), "f"(Gb));
+    else
+        asm(LSB_BWD_BODY("", "pt")
+            : "+f"(T), "+f"(gD), "+f"(s0), "+f"(s1), "+f"(s2), "+f"(S0), "+f"(S1), "+f"(S2)
+            : "f"(thr), "f"(al), "f"(cutp), "f"(nkap), "f"(ik), "f"(c0), "f"(c1), "f"(c2), "f"(u), "f"(0.f),
+              "f"(Gr), "f"(Gg), "f"(Gb));
 }
+#undef LSB_BWD_BODY
 
 struct LossArgs {
     const float* observed;   // (H,W,3) or NULL: no fused loss
@@ -225,7 +260,27 @@ struct RecPipe {
     }
 };
 
-template <bool DEPTH, bool CUT>
+// Deterministic loss total: the tile partials summed in tile order (called by
+// the one warp that observed the last ticket).
+__device__ __noinline__ void loss_total(const Ws& w, const LossArgs& L, int lane) {
+    __threadfence();
+    double v0 = 0.0, v1 = 0.0;
+    for (int t = lane; t < w.ntiles; t += 32) {
+        v0 += ((volatile double*)L.sums)[2 * t];
+        v1 += ((volatile double*)L.sums)[2 * t + 1];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+        v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+    }
+    if (lane == 0) {
+        L.sums_out[0] = v0;
+        L.sums_out[1] = v1;
+    }
+}
+
+template <bool DEPTH, bool CUT, bool COUNT>
 __global__ void __launch_bounds__(32 * WPB, FWD_MIN_BLOCKS)
 k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __restrict__ t_final,
             int32_t* __restrict__ n_contrib, float* __restrict__ depth) {
@@ -235,7 +290,9 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
     RecPipe pipe;
     pipe.buf = s_rec[wib];
     const float kap = a.clamp;
-    // persistent tile-warp: pull tiles from the queue until it is empty
+    // persistent tile-warp: pull tiles from the queue (heaviest first) until
+    // it is empty.  (Claiming the next slot early, to hide the atomic, costs
+    // more in lost load balance than it saves: measured +25% on config 2.)
     for (;;) {
         int tile = 0;
         if (lane == 0) {
@@ -286,11 +343,9 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
 #pragma unroll
                 for (int j = 0; j < RUN; ++j) thr[j] = col_thr(j, cx0, cx1, a.tmin);
                 const float4 q0 = *(const float4*)&sr[k].mxh;        // mxh myh mxl myl
-                const float4 qb = *(const float4*)&sr[k].A;          // A s E op
-                const float4 qc = *(const float4*)&sr[k].c0;         // c0 c1 c2 z
-                const Frame f = frame_of(q0, qb.w, gx0f, gy0f, a.lgk);
-                const float c0 = __fmul_rn(kap, qc.x), c1 = __fmul_rn(kap, qc.y), c2 = __fmul_rn(kap, qc.z);
-                const float zk = DEPTH ? __fmul_rn(kap, qc.w) : 0.f;
+                const float4 qb = *(const float4*)&sr[k].A;          // A s E lop
+                const float4 qc = *(const float4*)&sr[k].kc0;        // clamp * (c0 c1 c2 z)
+                const Frame f = frame_of(q0, qb.w, gx0f, gy0f);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     if (!(h ? row1 : row0)) continue;
@@ -300,12 +355,15 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
                     for (int j = 0; j < RUN; ++j) {
                         float u;
                         const float al = alpha_sat(qb.x, u0, edy, j, u);
-                        if (DEPTH)
-                            fwd_pixel_depth(al, thr[j], CUT ? a.cutp : 0.f, -kap, c0, c1, c2, zk, T[h][j], cnt[h][j],
-                                            cr[h][j], cg[h][j], cb[h][j], dz[h][j]);
+                        if (!COUNT && !DEPTH)
+                            fwd_pixel_nc(al, thr[j], CUT ? a.cutp : 0.f, -kap, qc.x, qc.y, qc.z, T[h][j], cr[h][j],
+                                         cg[h][j], cb[h][j]);
+                        else if (DEPTH)
+                            fwd_pixel_depth(al, thr[j], CUT ? a.cutp : 0.f, -kap, qc.x, qc.y, qc.z, qc.w, T[h][j],
+                                            cnt[h][j], cr[h][j], cg[h][j], cb[h][j], dz[h][j]);
                         else
-                            fwd_pixel(al, thr[j], CUT ? a.cutp : 0.f, -kap, c0, c1, c2, T[h][j], cnt[h][j], cr[h][j],
-                                      cg[h][j], cb[h][j]);
+                            fwd_pixel(al, thr[j], CUT ? a.cutp : 0.f, -kap, qc.x, qc.y, qc.z, T[h][j], cnt[h][j],
+                                      cr[h][j], cg[h][j], cb[h][j]);
                     }
                 }
             }
@@ -329,7 +387,7 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
                 image[3 * p + 1] = ig;
                 image[3 * p + 2] = ib;
                 t_final[p] = T[h][j];
-                n_contrib[p] = (int32_t)cnt[h][j];
+                if (COUNT) n_contrib[p] = (int32_t)cnt[h][j];
                 if (DEPTH) depth[p] = dz[h][j];
                 if (L.observed) {
                     const float i3[3] = {ir, ig, ib};
@@ -364,23 +422,8 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
             asm volatile("atom.release.gpu.global.add.u64 %0, [%1], 1;" : "=l"(done) : "l"(L.ticket) : "memory");
         }
         done = __shfl_sync(0xffffffffu, done, 0);
-        if (done != (unsigned long long)w.ntiles - 1) continue;
         // the warp that finished the last tile: deterministic sum in tile order
-        __threadfence();
-        double v0 = 0.0, v1 = 0.0;
-        for (int t = lane; t < w.ntiles; t += 32) {
-            v0 += ((volatile double*)L.sums)[2 * t];
-            v1 += ((volatile double*)L.sums)[2 * t + 1];
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            v0 += __shfl_xor_sync(0xffffffffu, v0, o);
-            v1 += __shfl_xor_sync(0xffffffffu, v1, o);
-        }
-        if (lane == 0) {
-            L.sums_out[0] = v0;
-            L.sums_out[1] = v1;
-        }
+        if (done == (unsigned long long)w.ntiles - 1) loss_total(w, L, lane);
     }
 }
 
@@ -407,6 +450,35 @@ __device__ __forceinline__ float reduce8(const float* v, int lane) {
     c += __shfl_xor_sync(0xffffffffu, c, 2);
     c += __shfl_xor_sync(0xffffffffu, c, 1);
     return c;
+}
+
+// One half-tile (rows r0 + 8h) of the backward for one record: recompute the
+// alphas, skip the half when no pixel of it reaches alpha_cut (a superset of
+// the exact per-pixel test in bwd_pixel), else update the pixels and fold the
+// row sums into the record's moments M.
+template <bool SAT>
+__device__ __forceinline__ void bwd_half(const Frame& f, float4 q1, bool rin, float dyoff, const float* thr,
+                                         const BlendArgs& a, float kap, float4 q2, const float* Gr, const float* Gg,
+                                         const float* Gb, float* T, float* gD, float* c, float* M) {
+    float dy, u0, edy;
+    row_terms(f, q1.y, q1.z, dyoff, dy, u0, edy);
+    float al[RUN], uu[RUN];
+#pragma unroll
+    for (int j = 0; j < RUN; ++j) al[j] = alpha_sat<SAT>(q1.x, u0, edy, j, uu[j]);
+    const float amax = fmaxf(fmaxf(al[0], al[1]), fmaxf(al[2], al[3]));
+    if (!__any_sync(0xffffffffu, rin && amax >= a.cutp)) return;
+    if (!rin) return;
+    float S0 = 0.f, S1 = 0.f, S2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < RUN; ++j)
+        bwd_pixel<SAT>(al[j], uu[j], thr[j], a.cutp, -kap, a.ik, q2.x, q2.y, q2.z, Gr[j], Gg[j], Gb[j], T[j], gD[j],
+                       c[0], c[1], c[2], S0, S1, S2);
+    M[0] += S0;
+    M[1] += S1;
+    M[2] = fmaf(S0, dy, M[2]);
+    M[3] += S2;
+    M[4] = fmaf(S1, dy, M[4]);
+    M[5] = fmaf(S0 * dy, dy, M[5]);
 }
 
 __global__ void __launch_bounds__(32 * WPB, BWD_MIN_BLOCKS)
@@ -464,8 +536,8 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __r
             const int nb = min(32, end - base);
             for (int k = 0; k < nb; ++k) {
                 const float4 q0 = *(const float4*)&sr[k].mxh;        // mxh myh mxl myl
-                const float4 q1 = *(const float4*)&sr[k].A;          // A s E op
-                const float4 q2 = *(const float4*)&sr[k].c0;         // c0 c1 c2 z
+                const float4 q1 = *(const float4*)&sr[k].A;          // A s E lop
+                const float4 q2 = *(const float4*)&sr[k].kc0;        // clamp * (c0 c1 c2 z)
                 const int4 q3 = *(const int4*)&sr[k].bbx;            // bbx bby id ebase
                 const int cx0 = (q3.x & 0xffff) - gx0, cx1 = (q3.x >> 16) - gx0;
                 const int ry0 = (q3.y & 0xffff) - gy0, ry1 = (q3.y >> 16) - gy0;
@@ -480,32 +552,15 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __r
                     float thr[RUN];
 #pragma unroll
                     for (int j = 0; j < RUN; ++j) thr[j] = over ? col_thr(j, cx0, cx1, a.tmin) : __int_as_float(0x7f800000);
-                    const Frame f = frame_of(q0, q1.w, gx0f, gy0f, a.lgk);
-                    const float c0 = __fmul_rn(kap, q2.x), c1 = __fmul_rn(kap, q2.y), c2 = __fmul_rn(kap, q2.z);
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const bool rin = over && (h ? row1 : row0);
-                        float dy, u0, edy;
-                        row_terms(f, q1.y, q1.z, 8.f * h, dy, u0, edy);
-                        float al[RUN], uu[RUN];
-#pragma unroll
-                        for (int j = 0; j < RUN; ++j) al[j] = alpha_sat(q1.x, u0, edy, j, uu[j]);
-                        // skip the half-tile when no pixel of it can reach alpha_cut
-                        // (a superset of the exact per-pixel test applied below)
-                        const float amax = fmaxf(fmaxf(al[0], al[1]), fmaxf(al[2], al[3]));
-                        if (!__any_sync(0xffffffffu, rin && amax >= a.cutp)) continue;
-                        if (!rin) continue;
-                        float S0 = 0.f, S1 = 0.f, S2 = 0.f;
-#pragma unroll
-                        for (int j = 0; j < RUN; ++j)
-                            bwd_pixel(al[j], uu[j], thr[j], a.cutp, -kap, a.ik, c0, c1, c2, Gr[h][j], Gg[h][j],
-                                      Gb[h][j], T[h][j], gD[h][j], c[0], c[1], c[2], S0, S1, S2);
-                        M[0] += S0;
-                        M[1] += S1;
-                        M[2] = fmaf(S0, dy, M[2]);
-                        M[3] += S2;
-                        M[4] = fmaf(S1, dy, M[4]);
-                        M[5] = fmaf(S0 * dy, dy, M[5]);
+                    const Frame f = frame_of(q0, q1.w, gx0f, gy0f);
+                    if (q1.w >= SAT_LOP) {
+                        bwd_half<true>(f, q1, over && row0, 0.f, thr, a, kap, q2, Gr[0], Gg[0], Gb[0], T[0], gD[0], c, M);
+                        bwd_half<true>(f, q1, over && row1, 8.f, thr, a, kap, q2, Gr[1], Gg[1], Gb[1], T[1], gD[1], c, M);
+                    } else {
+                        bwd_half<false>(f, q1, over && row0, 0.f, thr, a, kap, q2, Gr[0], Gg[0], Gb[0], T[0], gD[0], c,
+                                        M);
+                        bwd_half<false>(f, q1, over && row1, 8.f, thr, a, kap, q2, Gr[1], Gg[1], Gb[1], T[1], gD[1], c,
+                                        M);
                     }
                 }
                 float val = 0.f;
@@ -529,7 +584,7 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __r
                     for (int o = 16; o > 0; o >>= 1) r9 += __shfl_xor_sync(0xffffffffu, r9, o);
                     val = __shfl_sync(0xffffffffu, r8, 4 * min(lane, 7));
                     if (lane == 8) val = r9;
-                    val *= (lane < 3) ? kap : ((lane == 3) ? rcp_approx(q1.w) : ((lane < 6) ? 1.f : 0.5f));
+                    val *= (lane < 3) ? kap : ((lane == 3) ? a.ik * ex2_approx(-q1.w) : ((lane < 6) ? 1.f : 0.5f));   // 1/op
                 }
                 const int e = __shfl_sync(0xffffffffu, ecur, k);
                 if (lane < NUM_PART) w.part[(int64_t)e * NUM_PART + lane] = val;
@@ -539,16 +594,15 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __r
         pipe.drain();
         // intersections the walk never reached contribute nothing
         const int fin = w.tile_start[tile + 1], from = max(end, start);
-        for (int q = lane; q < (fin - from) * NUM_PART; q += 32)
-            w.part[(int64_t)w.tile_e[from + q / NUM_PART] * NUM_PART + q % NUM_PART] = 0.f;
+        for (int z = lane; z < (fin - from) * NUM_PART; z += 32)
+            w.part[(int64_t)w.tile_e[from + z / NUM_PART] * NUM_PART + z % NUM_PART] = 0.f;
     }
 }
 
 static BlendArgs blend_args(const lsb_settings& s, int W, int H) {
     BlendArgs a{W, H, (float)s.alpha_clamp, (float)s.transmittance_min, (float)s.alpha_cut,
-                (float)s.background[0], (float)s.background[1], (float)s.background[2], 0.f, 0.f, 0.f};
+                (float)s.background[0], (float)s.background[1], (float)s.background[2], 0.f, 0.f};
     a.cutp = (float)(s.alpha_cut / s.alpha_clamp);
-    a.lgk = (float)(-log2(s.alpha_clamp));
     a.ik = (float)(1.0 / s.alpha_clamp);
     return a;
 }
@@ -560,7 +614,7 @@ static int persistent_grid(const void* fn, int ntiles) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * WPB, 0);
     const int need = (ntiles + WPB - 1) / WPB;
-    const int g = sms * (per_sm > 0 ? per_sm : 1);
+    const int g = sms * (per_sm > BLEND_RESERVE ? per_sm - BLEND_RESERVE : 1);
     return g < need ? g : need;
 }
 
@@ -573,17 +627,27 @@ cudaError_t launch_blend_fwd(const Ws& w, const lsb_settings& s, int W, int H, f
     cudaError_t e = cudaMemsetAsync(w.ctr + 5, 0, 3 * sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
     const bool cut = s.alpha_cut > 0.0;
-    const int grid = persistent_grid(depth ? (cut ? (const void*)k_blend_fwd<true, true> : (const void*)k_blend_fwd<true, false>)
-                                           : (cut ? (const void*)k_blend_fwd<false, true> : (const void*)k_blend_fwd<false, false>),
-                                     w.ntiles);
+    // n_contrib == NULL (window engine): the count-free forward (no depth)
+    if (!n_contrib) {
+        const void* fn = cut ? (const void*)k_blend_fwd<false, true, false> : (const void*)k_blend_fwd<false, false, false>;
+        const int grid = persistent_grid(fn, w.ntiles);
+        if (cut)
+            k_blend_fwd<false, true, false><<<grid, 32 * WPB, 0, st>>>(w, a, L, image, t_final, n_contrib, depth);
+        else
+            k_blend_fwd<false, false, false><<<grid, 32 * WPB, 0, st>>>(w, a, L, image, t_final, n_contrib, depth);
+        return cudaGetLastError();
+    }
+    const void* fn = depth ? (cut ? (const void*)k_blend_fwd<true, true, true> : (const void*)k_blend_fwd<true, false, true>)
+                           : (cut ? (const void*)k_blend_fwd<false, true, true> : (const void*)k_blend_fwd<false, false, true>);
+    const int grid = persistent_grid(fn, w.ntiles);
     if (depth && cut)
-        k_blend_fwd<true, true><<<grid, 32 * WPB, 0, st>>>(w, a, L, image, t_final, n_contrib, depth);
+        k_blend_fwd<true, true, true><<<grid, 32 * WPB, 0, st>>>(w, a, L, image, t_final, n_contrib, depth);
     else if (depth)
-        k_blend_fwd<true, false><<<grid, 32 * WPB, 0, st>>>(w, a, L, image, t_final, n_contrib, depth);
+        k_blend_fwd<true, false, true><<<grid, 32 * WPB, 0, st>>>(w, a, L, image, t_final, n_contrib, depth);
     else if (cut)
-        k_blend_fwd<false, true><<<grid, 32 * WPB, 0, st>>>(w, a, L, image, t_final, n_contrib, depth);
+        k_blend_fwd<false, true, true><<<grid, 32 * WPB, 0, st>>>(w, a, L, image, t_final, n_contrib, depth);
     else
-        k_blend_fwd<false, false><<<grid, 32 * WPB, 0, st>>>(w, a, L, image, t_final, n_contrib, depth);
+        k_blend_fwd<false, false, true><<<grid, 32 * WPB, 0, st>>>(w, a, L, image, t_final, n_contrib, depth);
     return cudaGetLastError();
 }
 

@@ -19,11 +19,13 @@ constexpr double LOG2E = 1.4426950408889634;
 // One visible splat, 64 B, written once by preprocess and read by every tile
 // that the splat's bbox touches; the blend copies it to shared memory as is
 // (cp.async, 4 x 16 B).  mu_i is kept as an f32 hi/lo pair so a tile can form
-// its local coordinate (hi - origin) + lo without f64 arithmetic.
+// its local coordinate (hi - origin) + lo without f64 arithmetic.  The
+// blend works on the saturated alpha a' = min(1, op g / clamp), so the
+// record carries log2(op / clamp) and clamp * colour / depth directly.
 struct __align__(16) Rec {
     float mxh, myh, mxl, myl;   // mu_i = hi + lo (lo = f32(mu_i - hi))
-    float A, s, E, op;          // exponent: log2 g = A*u^2 + E*dy^2, u = dx + s*dy
-    float c0, c1, c2, z;        // clamped RGB and camera depth
+    float A, s, E, lop;         // log2(op g / clamp) = A*u^2 + E*dy^2 + lop, u = dx + s*dy
+    float kc0, kc1, kc2, kz;    // clamp * (clamped RGB), clamp * camera depth (f32 products)
     int32_t bbx, bby;           // x0 | x1 << 16, y0 | y1 << 16 (half-open pixel bbox)
     int32_t id, ebase;          // Gaussian id, first intersection index
 };

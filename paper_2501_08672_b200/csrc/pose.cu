@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(256) k_pose_prepare(Ws w, PosePrepArgs a) {
 
 struct RowArgs {
     int W, H;
-    float clamp, cut;
+    float clamp, cut, iclamp;
     int degree;
     double A[36];
     double Rcw[9];
@@ -240,27 +240,30 @@ __global__ void __launch_bounds__(128) k_pose_rows(Ws w, RowArgs a, const float*
             const float mxl = (rc.mxh - (float)ox) + rc.mxl, myl = (rc.myh - (float)oy) + rc.myl;
             dy = fy - myl;
             u = fmaf(rc.s, dy, fx - mxl);
-            G = ex2_approx(fmaf(rc.A, u * u, rc.E * dy * dy));
-            al = fminf(rc.op * G, a.clamp);
+            G = a.clamp * ex2_approx(fmaf(rc.A, u * u, fmaf(rc.E * dy, dy, rc.lop)));   // op g
+            al = fminf(G, a.clamp);
+            rc.kc0 *= a.iclamp;                 // back to the clamped colour
+            rc.kc1 *= a.iclamp;
+            rc.kc2 *= a.iclamp;
             contrib = (al >= a.cut) && al != 0.f;
         }
         float tot;
         const float Tk = Tc * warp_scan_mul_excl(contrib ? 1.f - al : 1.f, lane, tot);
         const float wt = contrib ? al * Tk : 0.f;
         float sr, sg, sb;
-        const float pr = Pr + warp_scan_add_incl(wt * (active ? rc.c0 : 0.f), lane, sr);
-        const float pg = Pg + warp_scan_add_incl(wt * (active ? rc.c1 : 0.f), lane, sg);
-        const float pb = Pb + warp_scan_add_incl(wt * (active ? rc.c2 : 0.f), lane, sb);
+        const float pr = Pr + warp_scan_add_incl(wt * (active ? rc.kc0 : 0.f), lane, sr);
+        const float pg = Pg + warp_scan_add_incl(wt * (active ? rc.kc1 : 0.f), lane, sg);
+        const float pb = Pb + warp_scan_add_incl(wt * (active ? rc.kc2 : 0.f), lane, sb);
         Tc *= tot;
         Pr += sr; Pg += sg; Pb += sb;
         if (contrib) {
             const float inv = 1.f / (1.f - al);
             const float third = 1.f / 3.f;
-            const float da = third * (rc.c0 * Tk - (ir - pr) * inv) + third * (rc.c1 * Tk - (ig - pg) * inv) +
-                             third * (rc.c2 * Tk - (ib - pb) * inv);
+            const float da = third * (rc.kc0 * Tk - (ir - pr) * inv) + third * (rc.kc1 * Tk - (ig - pg) * inv) +
+                             third * (rc.kc2 * Tk - (ib - pb) * inv);
             float emu0 = 0.f, emu1 = 0.f, ec0 = 0.f, ec1 = 0.f, ec2 = 0.f;
             if (al < a.clamp) {
-                const float gq = rc.op * da * G;
+                const float gq = da * G;
                 const float v0 = (rc.A * k2) * u;
                 const float v1 = fmaf(rc.s, v0, (rc.E * k2) * dy);
                 emu0 = gq * v0; emu1 = gq * v1;
@@ -355,6 +358,7 @@ cudaError_t launch_pose_rows(const Ws& w, const lsb_settings& s, int degree, int
                              const double* A, const double* Rcw, double* rows, cudaStream_t st) {
     RowArgs a;
     a.W = W; a.H = H; a.clamp = (float)s.alpha_clamp; a.cut = (float)s.alpha_cut; a.degree = degree;
+    a.iclamp = (float)(1.0 / s.alpha_clamp);
     for (int k = 0; k < 36; ++k) a.A[k] = A[k];
     for (int k = 0; k < 9; ++k) a.Rcw[k] = Rcw[k];
     if (m == 0) return cudaSuccess;

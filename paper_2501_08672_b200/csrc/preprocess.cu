@@ -195,7 +195,7 @@ __device__ bool splat_one(const PreArgs& a, int64_t i, Rec& r, int& ntiles, uint
     r.A = (float)(-0.5 * LOG2E * ak);
     r.s = (float)(-cb / cc);
     r.E = (float)(-0.5 * LOG2E / cc);
-    r.op = (float)op;
+    r.lop = (float)(log2(op) - log2(a.s.alpha_clamp));
     // SH colour (raster.py:232-238, sh.py:112-123)
     const double* cc3 = a.T.cam_center;
     const double dvx = px - cc3[0], dvy = py - cc3[1], dvz = pz - cc3[2];
@@ -224,10 +224,11 @@ __device__ bool splat_one(const PreArgs& a, int64_t i, Rec& r, int& ntiles, uint
         col[c] = (float)fmin(fmax(raw, 0.0), 1.0);
         if (raw > 0.0 && raw < 1.0) cmask |= 1u << c;
     }
-    r.c0 = col[0];
-    r.c1 = col[1];
-    r.c2 = col[2];
-    r.z = (float)z;
+    const float kap = (float)a.s.alpha_clamp;
+    r.kc0 = __fmul_rn(kap, col[0]);
+    r.kc1 = __fmul_rn(kap, col[1]);
+    r.kc2 = __fmul_rn(kap, col[2]);
+    r.kz = __fmul_rn(kap, (float)z);
     r.bbx = ix0 | (ix1 << 16);
     r.bby = iy0 | (iy1 << 16);
     r.id = (int32_t)i;

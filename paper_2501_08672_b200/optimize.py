@@ -333,7 +333,8 @@ class WindowEngine:
                 sm.wait_event(copied[v])
                 obs = self.obs_dev[v]
             mark("blend_fwd", sm)
-            render_blend_loss(st, ln.image, ln.t_final, ln.n_contrib, obs, _KIND[self.cfg.loss],
+            # no processed-entry count in the step: the count-free forward
+            render_blend_loss(st, ln.image, ln.t_final, None, obs, _KIND[self.cfg.loss],
                               gscale, ln.grad_image, self.loss.ptr(v), stream=sm)
             mark("blend_fwd", sm)
             if host and not capturing:
@@ -341,7 +342,7 @@ class WindowEngine:
                 ev.record(sm)
                 self._consumed[v] = ev
             mark("blend_bwd", sm)
-            render_blend_bwd(st, ln.image, ln.n_contrib, ln.grad_image, 1.0, sm)
+            render_blend_bwd(st, ln.image, None, ln.grad_image, 1.0, sm)
             mark("blend_bwd", sm)
             if prev_chain is not None and sm is not main:
                 sm.wait_event(prev_chain)

@@ -287,13 +287,16 @@ def render_bin(state: RenderState, stream=None) -> None:
                                           ctypes.byref(state.dims), _lib.stream_ptr(stream)), "bin")
 
 
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
 def render_blend(state: RenderState, image, t_final, n_contrib, depth=None, stream=None) -> None:
-    """K3 blend forward (async)."""
+    """K3 blend forward (async).  n_contrib None: no entry count (include/lsb.h)."""
     _lib.check(_lib.load().lsb_render_blend(
         ctypes.byref(state.c_set), state._ws(), state.ws_bytes, ctypes.byref(state.dims),
         ctypes.c_void_p(image.data_ptr()), ctypes.c_void_p(t_final.data_ptr()),
-        ctypes.c_void_p(n_contrib.data_ptr()), ctypes.c_void_p(depth.data_ptr()) if depth is not None else None,
-        _lib.stream_ptr(stream)), "blend")
+        _ptr(n_contrib), _ptr(depth), _lib.stream_ptr(stream)), "blend")
 
 
 def render_blend_loss(state: RenderState, image, t_final, n_contrib, observed, kind: int, grad_scale: float,
@@ -302,8 +305,7 @@ def render_blend_loss(state: RenderState, image, t_final, n_contrib, observed, k
     _lib.check(_lib.load().lsb_render_blend_loss(
         ctypes.byref(state.c_set), state._ws(), state.ws_bytes, ctypes.byref(state.dims),
         ctypes.c_void_p(image.data_ptr()), ctypes.c_void_p(t_final.data_ptr()),
-        ctypes.c_void_p(n_contrib.data_ptr()), ctypes.c_void_p(depth.data_ptr()) if depth is not None else None,
-        ctypes.c_void_p(observed.data_ptr()), int(kind), float(grad_scale), ctypes.c_void_p(grad_out.data_ptr()),
+        _ptr(n_contrib), _ptr(depth), ctypes.c_void_p(observed.data_ptr()), int(kind), float(grad_scale), ctypes.c_void_p(grad_out.data_ptr()),
         loss_ptr, _lib.stream_ptr(stream)), "blend_loss")
 
 
@@ -312,7 +314,7 @@ def render_blend_bwd(state: RenderState, image, n_contrib, grad_image, grad_scal
     """K4 blend backward into the per-intersection partials (async)."""
     _lib.check(_lib.load().lsb_render_blend_bwd(
         ctypes.byref(state.c_set), state._ws(), state.ws_bytes, ctypes.byref(state.dims),
-        ctypes.c_void_p(image.data_ptr()), ctypes.c_void_p(n_contrib.data_ptr()),
+        ctypes.c_void_p(image.data_ptr()), _ptr(n_contrib),
         ctypes.c_void_p(grad_image.data_ptr()), float(grad_scale), _lib.stream_ptr(stream)), "blend_bwd")
 
 

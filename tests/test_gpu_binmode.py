@@ -68,3 +68,28 @@ def test_binmode1_fullsize_cfg2_view():
     assert o1.cache.counts[1] < 0.9 * o0.cache.counts[1]
     rng = np.random.default_rng(5)
     _assert_identical(o0, o1, rng.normal(size=(1024, 1280, 3)).astype(np.float32))
+
+
+@pytest.mark.parametrize("bin_mode", [0, 1])
+@pytest.mark.parametrize("name", ["rand1_cut1", "room_v0_cut1", "room_v1_cut0"])
+def test_countfree_forward_identical(name, bin_mode):
+    """The window engine's count-free forward (n_contrib NULL, half-tile skip)
+    writes the same image / T bits as the counting forward."""
+    import torch
+    from paper_2501_08672_b200.raster import GaussianArrays, RenderState, render_bin, render_blend
+    d = load(name)
+    P, R_cw, t_cw, cam, st = case_inputs(d)
+    arrays = GaussianArrays(P["means"], P["rots"], P["scales"], P["opacities"], P["shs"])
+    state = RenderState(arrays, cam, R_cw, t_cw, _settings(st), 1 << 20, bin_mode)
+    render_bin(state)
+    h, w = cam.height, cam.width
+    outs = []
+    for count in (True, False):
+        img = torch.empty((h, w, 3), dtype=torch.float32, device="cuda")
+        tf = torch.empty((h, w), dtype=torch.float32, device="cuda")
+        nc = torch.empty((h, w), dtype=torch.int32, device="cuda") if count else None
+        render_blend(state, img, tf, nc)
+        outs.append((img, tf))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])
