@@ -107,6 +107,10 @@ __global__ void __launch_bounds__(256) k_part_reduce(Ws w) {
     }
 }
 
+#ifndef CHAIN_FUSED_REDUCE      // sum a splat's partials inside k_chain (1) or in k_part_reduce (0)
+#define CHAIN_FUSED_REDUCE 1
+#endif
+
 using CT = double;  // chain-rule arithmetic: f64 keeps Adam's sign-sensitive first steps on the reference trajectory
 
 __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
@@ -123,8 +127,26 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
         const Rec& r = w.rec[slot];
         if (r.ebase < 0) continue;
         double q[NUM_PART];
+#if CHAIN_FUSED_REDUCE
+        // the splat's intersection partials (contiguous, e in [ebase, ebase + nt)),
+        // summed in e order
+#pragma unroll
+        for (int c = 0; c < NUM_PART; ++c) q[c] = 0.0;
+        {
+            const float* src = w.part + (int64_t)r.ebase * NUM_PART;
+            const int nt = w.vis_ebase[slot + 1] - r.ebase;
+            for (int k = 0; k < nt; ++k, src += NUM_PART) {
+                float v[NUM_PART];
+#pragma unroll
+                for (int c = 0; c < NUM_PART; ++c) v[c] = __ldcs(src + c);
+#pragma unroll
+                for (int c = 0; c < NUM_PART; ++c) q[c] += (double)v[c];
+            }
+        }
+#else
 #pragma unroll
         for (int c = 0; c < NUM_PART; ++c) q[c] = w.qsum[slot * NUM_PART + c];
+#endif
         bool nz = false;
 #pragma unroll
         for (int c = 0; c < NUM_PART; ++c) nz |= (q[c] != 0.0);
@@ -301,7 +323,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
 cudaError_t launch_chain(const Ws& w, const lsb_params& p, const lsb_grads& g, const lsb_camera& cam,
                          const lsb_pose& T, const lsb_settings& s, double* pose_out,
                          cudaStream_t st) {
-    k_part_reduce<<<4 * 148, 256, 0, st>>>(w);
+    if (!CHAIN_FUSED_REDUCE) k_part_reduce<<<4 * 148, 256, 0, st>>>(w);
     ChainArgs a{p, g, cam, T, 0, pose_out};
     int deg_store = 0;
     while ((deg_store + 2) * (deg_store + 2) <= p.sh_coeffs) ++deg_store;

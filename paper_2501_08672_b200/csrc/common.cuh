@@ -10,7 +10,10 @@ namespace lsb {
 constexpr int TILE = 16;
 constexpr int NUM_PART = 9;          // d_color(3), d_opac, d_mean2d(2), d_cov2d(3)
 constexpr int POSE_VALS = 9;         // rho_cam(3), tau_cam(3), d_cam_center(3)
-constexpr int PRE_THREADS = 256;     // preprocess block size
+#ifndef LSB_PRE_THREADS
+#define LSB_PRE_THREADS 256
+#endif
+constexpr int PRE_THREADS = LSB_PRE_THREADS;     // preprocess block size
 constexpr int PRE_ITEMS = 1;         // Gaussians per preprocess thread
 constexpr int CHAIN_BLOCKS = 592;    // fixed grid of the chain kernel (4 x 148 SMs)
 constexpr int CHAIN_THREADS = 64;
@@ -51,6 +54,7 @@ struct Ws {
     int32_t* tile_cursor;       // [ntiles]
     int32_t* tile_last;         // [ntiles] one past the last list entry any pixel used
     int32_t* emit_slot;         // [cap] visible slot of intersection e
+    int32_t* emit_tile;         // [cap] tile of intersection e
     int32_t* tile_e;            // [cap] intersection index, per-tile depth order
     int32_t* tile_slot;         // [cap] visible slot, per-tile depth order
     int32_t* sort_scratch;      // [cap * 8] fallback sort buffers (tiles > SORT_CAP)
@@ -99,6 +103,7 @@ inline size_t carve(const lsb_dims& d, char* base, Ws* w) {
     t.vkey = (uint64_t*)take(sizeof(uint64_t) * n);
     t.colmask = (uint32_t*)take(sizeof(uint32_t) * n);
     t.emit_slot = (int32_t*)take(sizeof(int32_t) * cap);
+    t.emit_tile = (int32_t*)take(sizeof(int32_t) * cap);
     t.tile_e = (int32_t*)take(sizeof(int32_t) * cap);
     t.tile_slot = (int32_t*)take(sizeof(int32_t) * cap);
     t.sort_scratch = (int32_t*)take(sizeof(int32_t) * cap * 8);

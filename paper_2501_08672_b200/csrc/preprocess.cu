@@ -124,6 +124,15 @@ __device__ bool splat_one(const PreArgs& a, int64_t i, Rec& r, int& ntiles, uint
     const double fx = a.cam.fx, fy = a.cam.fy;
     const double mux = fx * x / z + a.cam.cx;
     const double muy = fy * y / z + a.cam.cy;
+    // Exact early cull, before the covariance: a splat is kept only with
+    // radius <= max_footprint_px =: R, and then x1 <= floor(mux + R) + 1 < 0
+    // when mux + R < -1 (x0 >= floor(mux - R) >= W when mux - R >= W; same in
+    // y), so its bbox would be empty (raster.py:168-172).
+    {
+        const double R = a.s.max_footprint_px;
+        if (mux + R < -1.0 || mux - R >= (double)a.cam.width || muy + R < -1.0 || muy - R >= (double)a.cam.height)
+            return false;
+    }
     const double zz = z * z;
     const double J00 = fx / z, J02 = -fx * x / zz;
     const double J11 = fy / z, J12 = -fy * y / zz;
@@ -136,6 +145,21 @@ __device__ bool splat_one(const PreArgs& a, int64_t i, Rec& r, int& ntiles, uint
         B[3 * r3 + 0] = pld(a.p.rots, 9 * i + 3 * r3 + 0, f64) * s0;
         B[3 * r3 + 1] = pld(a.p.rots, 9 * i + 3 * r3 + 1, f64) * s1;
         B[3 * r3 + 2] = pld(a.p.rots, 9 * i + 3 * r3 + 2, f64) * s2;
+    }
+    // Exact cull with a radius bound, still before the covariance:
+    // lambda_max(cov_i) <= |J|_F^2 |B|_F^2 + dilation (spectral <= Frobenius,
+    // R_cw orthonormal), and nsig <= footprint_sigma, so the bbox is empty when
+    // the centre is farther than that radius (x 1.001 + 1 px against
+    // rounding) outside the image.
+    {
+        double bf = 0.0;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) bf += B[k] * B[k];
+        const double iz = 1.0 / z, xz = x * iz, yz = y * iz;
+        const double jf = (fx * iz) * (fx * iz) * (1.0 + xz * xz) + (fy * iz) * (fy * iz) * (1.0 + yz * yz);
+        const double rb = a.s.footprint_sigma * sqrt(jf * bf + a.s.dilation) * 1.001 + 1.0;
+        if (mux + rb < -1.0 || mux - rb >= (double)a.cam.width || muy + rb < -1.0 || muy - rb >= (double)a.cam.height)
+            return false;
     }
     double W[9];
 #pragma unroll
@@ -274,7 +298,10 @@ __device__ unsigned long long warp_lookback(unsigned long long* flags, int blk, 
 // reference's np.nonzero order and (depth, slot) ties break exactly as its
 // stable argsort (raster.py:221).  Each visible splat also reserves a
 // contiguous run of intersection indices and bumps the per-tile histogram.
-__global__ void __launch_bounds__(PRE_THREADS)
+#ifndef PRE_MIN_BLOCKS
+#define PRE_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(PRE_THREADS, PRE_MIN_BLOCKS)
 k_preprocess(PreArgs a, Ws w) {
     __shared__ unsigned long long s_blk;
     __shared__ int s_wv[PRE_THREADS / 32], s_wt[PRE_THREADS / 32];
@@ -346,54 +373,70 @@ k_preprocess(PreArgs a, Ws w) {
     w.colmask[slot] = cm;
     if (!fits) return;
     const int x0 = r.bbx & 0xffff, x1 = r.bbx >> 16, y0 = r.bby & 0xffff, y1 = r.bby >> 16;
+    // tile histogram, and each intersection's (slot, tile) for the scatter,
+    // e running row-major over the splat's tiles from e0
+    int e = (int)e0;
     if (a.cull) {
         w.cgeo[slot] = geo;
         for (int ty = y0 >> 4; ty <= (y1 - 1) >> 4; ++ty) {
             int tx0, tx1;
             if (!cull_tile_row(geo, ty, x0, x1, y0, y1, tx0, tx1)) continue;
-            for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&w.tile_count[ty * w.ntx + tx], 1);
+            for (int tx = tx0; tx <= tx1; ++tx, ++e) {
+                atomicAdd(&w.tile_count[ty * w.ntx + tx], 1);
+                w.emit_tile[e] = ty * w.ntx + tx;
+                w.emit_slot[e] = (int32_t)slot;
+            }
         }
         return;
     }
     for (int ty = y0 >> 4; ty <= (y1 - 1) >> 4; ++ty)
-        for (int tx = x0 >> 4; tx <= (x1 - 1) >> 4; ++tx) atomicAdd(&w.tile_count[ty * w.ntx + tx], 1);
+        for (int tx = x0 >> 4; tx <= (x1 - 1) >> 4; ++tx, ++e) {
+            atomicAdd(&w.tile_count[ty * w.ntx + tx], 1);
+            w.emit_tile[e] = ty * w.ntx + tx;
+            w.emit_slot[e] = (int32_t)slot;
+        }
 }
 
-// Exclusive scan of the tile histogram (single CTA, chunked).
+// Exclusive scan of the tile histogram (single CTA, one pass: each thread
+// owns a run of SCAN_PER consecutive tiles).
+constexpr int SCAN_PER = 16;      // tiles per thread: 16 K tiles (4K x 4K px) per CTA
 __global__ void __launch_bounds__(1024) k_scan_tiles(Ws w) {
     __shared__ int s_w[32];
-    __shared__ int s_carry;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_carry = 0;
+    const int per = (w.ntiles + 1023) / 1024;     // <= SCAN_PER (checked at launch)
+    const int b0 = tid * per;
+    int v[SCAN_PER];
+    int sum = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_PER; ++i) {
+        v[i] = (i < per && b0 + i < w.ntiles) ? w.tile_count[b0 + i] : 0;
+        sum += v[i];
+    }
+    int x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
     __syncthreads();
-    for (int base = 0; base < w.ntiles; base += 1024) {
-        const int idx = base + tid;
-        const int v = idx < w.ntiles ? w.tile_count[idx] : 0;
-        int x = v;
+    if (warp == 0) {
+        int y = s_w[lane];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
+            const int z = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += z;
         }
-        if (lane == 31) s_w[warp] = x;
-        __syncthreads();
-        if (warp == 0) {
-            int y = s_w[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int z = __shfl_up_sync(0xffffffffu, y, o);
-                if (lane >= o) y += z;
-            }
-            s_w[lane] = y;
-        }
-        __syncthreads();
-        const int incl = x + (warp > 0 ? s_w[warp - 1] : 0) + s_carry;
-        if (idx < w.ntiles) w.tile_start[idx] = incl - v;
-        __syncthreads();
-        if (tid == 1023) s_carry = incl;
-        __syncthreads();
+        s_w[lane] = y;
     }
-    if (tid == 0) w.tile_start[w.ntiles] = s_carry;
+    __syncthreads();
+    int run = x - sum + (warp > 0 ? s_w[warp - 1] : 0);
+#pragma unroll
+    for (int i = 0; i < SCAN_PER; ++i) {
+        if (i < per && b0 + i < w.ntiles) w.tile_start[b0 + i] = run;
+        run += v[i];
+    }
+    if (tid == 1023) w.tile_start[w.ntiles] = run;
     // Processing order of the persistent blend kernels: a counting sort of
     // the tiles by descending list length (4-entry buckets), so the longest
     // tiles start first and the tail of the tile queue is short work.
@@ -401,7 +444,16 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(Ws w) {
     if (tid < 256) s_hist[tid] = 0;
     __syncthreads();
     auto key = [](int c) { return 255 - min(c >> 2, 255); };
-    for (int t = tid; t < w.ntiles; t += 1024) atomicAdd(&s_hist[key(w.tile_count[t])], 1);
+    // (warp-aggregated: most tiles share a few buckets, and same-address
+    // shared atomics serialise)
+#pragma unroll
+    for (int i = 0; i < SCAN_PER; ++i) {
+        if (i >= per) break;
+        const bool ok = b0 + i < w.ntiles;
+        const int k = ok ? key(v[i]) : -1;
+        const unsigned grp = __match_any_sync(0xffffffffu, k);
+        if (ok && lane == __ffs(grp) - 1) atomicAdd(&s_hist[k], __popc(grp));
+    }
     __syncthreads();
     if (warp == 0) {
         int loc[8], sum = 0;
@@ -421,52 +473,30 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(Ws w) {
         for (int i = 0; i < 8; ++i) s_hist[8 * lane + i] = excl + loc[i];
     }
     __syncthreads();
-    for (int t = tid; t < w.ntiles; t += 1024) w.tile_order[atomicAdd(&s_hist[key(w.tile_count[t])], 1)] = t;
+#pragma unroll
+    for (int i = 0; i < SCAN_PER; ++i) {
+        if (i >= per) break;
+        const bool ok = b0 + i < w.ntiles;
+        const int k = ok ? key(v[i]) : -1;
+        const unsigned grp = __match_any_sync(0xffffffffu, k);
+        const int leader = __ffs(grp) - 1;
+        int base = 0;
+        if (ok && lane == leader) base = atomicAdd(&s_hist[k], __popc(grp));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (ok) w.tile_order[base + __popc(grp & ((1u << lane) - 1u))] = b0 + i;
+    }
 }
 
-// Scatter every (tile, splat) intersection into its tile's bucket, one thread
-// per intersection e: its splat is found by binary search in the exclusive
-// scan vis_ebase (monotone in slot order), its tile is the k-th tile of the
-// splat's bbox in row-major order (mode 1: of its contributing tiles, row by
-// row).  Order inside a bucket is arbitrary here and fixed by the per-tile sort.
-__global__ void __launch_bounds__(256) k_scatter(Ws w, int cull) {
-    const int64_t M = (int64_t)w.ctr[0];
+// Scatter with the (slot, tile) pairs the preprocess emitted: one thread per
+// intersection claims a position in its tile's bucket.
+__global__ void __launch_bounds__(256) k_scatter_emitted(Ws w) {
     const int64_t I = min((int64_t)w.ctr[1], w.cap);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < I; e += stride) {
-        int64_t lo = 0, hi = M - 1;          // largest s with vis_ebase[s] <= e
-        while (lo < hi) {
-            const int64_t mid = (lo + hi + 1) >> 1;
-            if ((int64_t)w.vis_ebase[mid] <= e) lo = mid;
-            else hi = mid - 1;
-        }
-        const Rec& r = w.rec[lo];
-        if (r.ebase < 0) continue;           // this splat's run overflowed the capacity
-        int k = (int)(e - r.ebase);
-        int t;
-        if (cull) {
-            const int x0 = r.bbx & 0xffff, x1 = r.bbx >> 16, y0 = r.bby & 0xffff, y1 = r.bby >> 16;
-            const CullGeo g = w.cgeo[lo];
-            t = -1;
-            for (int ty = y0 >> 4; ty <= (y1 - 1) >> 4; ++ty) {
-                int tx0, tx1;
-                if (!cull_tile_row(g, ty, x0, x1, y0, y1, tx0, tx1)) continue;
-                if (k <= tx1 - tx0) {
-                    t = ty * w.ntx + tx0 + k;
-                    break;
-                }
-                k -= tx1 - tx0 + 1;
-            }
-            if (t < 0) continue;             // unreachable: the count came from the same walk
-        } else {
-            const int tx0 = (r.bbx & 0xffff) >> 4, tx1 = ((r.bbx >> 16) - 1) >> 4;
-            const int ty0 = (r.bby & 0xffff) >> 4;
-            const int nx = tx1 - tx0 + 1;
-            t = (ty0 + k / nx) * w.ntx + tx0 + k % nx;
-        }
+        const int t = w.emit_tile[e];
         const int j = w.tile_start[t] + atomicAdd(&w.tile_cursor[t], 1);
         w.tile_e[j] = (int32_t)e;
-        w.emit_slot[e] = (int32_t)lo;
+        w.tile_slot[j] = w.emit_slot[e];
     }
 }
 
@@ -558,7 +588,7 @@ __device__ void warp_sort_tile(const Ws& w, int start, int n, int lane) {
         const int i = r * 32 + lane;
         if (i < n) {
             e[r] = w.tile_e[start + i];
-            s[r] = w.emit_slot[e[r]];
+            s[r] = w.tile_slot[start + i];
             k[r] = w.vkey[s[r]];
         } else {
             k[r] = ~0ull;
@@ -590,7 +620,7 @@ __global__ void __launch_bounds__(128) k_tile_sort(Ws w) {
     const int start = w.tile_start[t], n = w.tile_start[t + 1] - start;
     if (n <= 0) return;
     if (n == 1) {
-        if (lane == 0) w.tile_slot[start] = w.emit_slot[w.tile_e[start]];
+        // a single entry is already in place (the scatter wrote its slot)
     } else if (n <= 32) {
         warp_sort_tile<1>(w, start, n, lane);
     } else if (n <= 64) {
@@ -622,7 +652,7 @@ __global__ void __launch_bounds__(256) k_tile_sort_big(Ws w) {
         if (n <= SORT_CAP) {
             for (int i = threadIdx.x; i < n; i += blockDim.x) {
                 const int e = w.tile_e[start + i];
-                const int slot = w.emit_slot[e];
+                const int slot = w.tile_slot[start + i];
                 sk[i] = w.vkey[slot];
                 ss[i] = slot;
                 se[i] = e;
@@ -642,7 +672,7 @@ __global__ void __launch_bounds__(256) k_tile_sort_big(Ws w) {
             __syncthreads();
             for (int i = threadIdx.x; i < cn; i += blockDim.x) {
                 const int e = w.tile_e[start + c0 + i];
-                const int slot = w.emit_slot[e];
+                const int slot = w.tile_slot[start + c0 + i];
                 sk[i] = w.vkey[slot];
                 ss[i] = slot;
                 se[i] = e;
@@ -703,8 +733,9 @@ cudaError_t launch_preprocess(const lsb_params& p, const lsb_camera& cam, const 
     cudaError_t err = cudaMemsetAsync(w.ctr, 0, zero_prefix_bytes(w), st);
     if (err != cudaSuccess) return err;
     k_preprocess<<<w.nblocks_pre, PRE_THREADS, 0, st>>>(a, w);
+    if (w.ntiles > 1024 * SCAN_PER) return cudaErrorInvalidValue;     // > 16 K tiles: image too large
     k_scan_tiles<<<1, 1024, 0, st>>>(w);
-    k_scatter<<<8 * 148, 256, 0, st>>>(w, a.cull);
+    k_scatter_emitted<<<8 * 148, 256, 0, st>>>(w);
     k_tile_sort<<<(w.ntiles + 3) / 4, 128, 0, st>>>(w);
     cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_sort_smem());
     k_tile_sort_big<<<148, 256, tile_sort_smem(), st>>>(w);

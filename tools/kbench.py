@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--bin-mode", type=int, default=1)
     ap.add_argument("--vs", type=float, default=0.0723)
     ap.add_argument("--count", action="store_true", help="pass an n_contrib buffer (counting forward)")
+    ap.add_argument("--size", default="1280x1024", help="WxH")
+    ap.add_argument("--views", type=int, default=10, help="orbit views (the view index is into these)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -32,13 +34,14 @@ def main():
     from paper_2501_08672_b200.scene import bake_room, camera_for, orbit_views
     torch.cuda.set_device(0)
     P = bake_room(args.vs)
-    cam = camera_for(1280, 1024)
+    W, H = (int(v) for v in args.size.split("x"))
+    cam = camera_for(W, H)
     st = RasterSettings(alpha_cut=1.0 / 255.0)
     arrays = GaussianArrays(*P, device="cuda")
-    T = orbit_views(10)[args.view]
+    T = orbit_views(args.views)[args.view]
     obs = render(arrays, T, cam, st, retain_cache=False).image.clone()
     Tc = T.inverse()
-    state = RenderState(arrays, cam, Tc.R, Tc.t, st, 1 << 22, args.bin_mode)
+    state = RenderState(arrays, cam, Tc.R, Tc.t, st, 1 << 23, args.bin_mode)
     h, w = cam.height, cam.width
     img = torch.empty((h, w, 3), device="cuda")
     tf = torch.empty((h, w), device="cuda")
