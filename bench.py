@@ -292,6 +292,14 @@ def run_ours(args, wl, rank, world, local_rank):
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(dom)
     step_bytes = sum(ab[k] * (len(my_views) if k != "adam" else 1) for k in ab)
+    # issue-slot roofline of the same kernel: the blend is bound by instruction
+    # issue, not HBM.  Warp instructions per launch come from
+    # the committed ncu capture (profiles/issue.json); peak = 148 SMs x 4
+    # schedulers x 1 warp-instruction/clock at the SM clock sampled under load.
+    issue = None
+    ip = os.path.join(ROOT, "profiles", "issue.json")
+    if os.path.exists(ip):
+        issue = json.load(open(ip)).get(dom)
 
     # end-to-end through the public API with host buffers: every step copies
     # this rank's observed images from pinned host memory (copy stream, in
@@ -321,6 +329,7 @@ def run_ours(args, wl, rank, world, local_rank):
     h2d = sum(o.numel() * 4 for o in observed)
     d2h = int(eng.loss.sums().numel() * 8)
 
+    clk_sum = clk.summary()
     if rank == 0:
         value = V * W * H / (ms * 1e-3) / 1e6
         out = {
@@ -339,11 +348,17 @@ def run_ours(args, wl, rank, world, local_rank):
                          "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                          "algorithmic_bytes_per_launch": ab[dom], "avg_launch_ms": dom_ms,
                          "note": "blend is FP32-issue bound (SURVEY.md §8(d)); see profiles/"},
+            "issue_roofline": None if not issue else {
+                "kernel": dom, "unit": "warp-inst/s", "warp_inst_per_launch": issue["warp_inst_per_launch"],
+                "achieved": issue["warp_inst_per_launch"] / (dom_ms * 1e-3),
+                "peak": 148 * 4 * (clk_sum["sm_mhz"] or 1965.0) * 1e6,
+                "frac": issue["warp_inst_per_launch"] / (dom_ms * 1e-3) / (148 * 4 * (clk_sum["sm_mhz"] or 1965.0) * 1e6),
+                "source": f"ncu capture {issue.get('capture')} (one config-2 view), live launch time"},
             "step_roofline": {"algorithmic_bytes_per_step_rank0": step_bytes,
                               "frac": step_bytes / (ms * 1e-3) / 1e9 / hbm},
             "kernel_ms_per_step": per_step_ms,
             "counts_per_view": {"visible_M": M_avg, "intersections_I": I_avg},
-            "clocks": clk.summary(),
+            "clocks": clk_sum,
             "e2e": {"value": V * W * H / (e_ms * 1e-3) / 1e6, "unit": "Mpix/s",
                     "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world, "ms_per_step": e_ms},
             "gpu_launches": args.steps * (len(my_views) * 8 + 2) + 1,   # per view: preprocess, scan, scatter,
@@ -508,7 +523,7 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS) + ["cfg3", "cfg4"])
     ap.add_argument("--alpha-cut", type=float, default=1.0 / 255.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--lanes", type=int, default=3, help="concurrent view pipelines per GPU")
+    ap.add_argument("--lanes", type=int, default=5, help="concurrent view pipelines per GPU")
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="eager launches instead of a CUDA graph")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

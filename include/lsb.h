@@ -184,6 +184,16 @@ int lsb_render_blend_loss(const lsb_settings* s, void* ws, size_t ws_bytes, cons
 int lsb_render_blend_bwd(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
                          const float* image, const int32_t* n_contrib, const float* grad_image,
                          float grad_scale, void* stream);
+/* Blend backward with the photometric loss fused in (optimize.py:48-74, no
+ * mask): dL/dI = sign(I - observed) (L1) or 2 (I - observed) (L2), times
+ * grad_scale, is formed per pixel from image (the forward's output) and
+ * observed (H,W,3), back-propagated like lsb_render_blend_bwd, and
+ * loss_out[0..1] = [sum |diff| (L1) or diff^2 (L2), sum diff^2] (tile
+ * partials summed in tile order; deterministic).  The window engine's step:
+ * lsb_render_bin, lsb_render_blend (n_contrib NULL), this, lsb_render_chain. */
+int lsb_render_blend_bwd_loss(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
+                              const float* image, const float* observed, int kind, float grad_scale,
+                              double* loss_out, void* stream);
 int lsb_render_chain(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T_cw,
                      const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
                      const lsb_grads* g, double* pose_out, void* stream);

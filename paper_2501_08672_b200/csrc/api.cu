@@ -10,6 +10,8 @@ cudaError_t launch_preprocess(const lsb_params&, const lsb_camera&, const lsb_po
                               const Ws&, cudaStream_t);
 cudaError_t launch_blend_fwd(const Ws&, const lsb_settings&, int, int, float*, float*, int32_t*, float*,
                              const float*, int, float, float*, double*, cudaStream_t);
+cudaError_t launch_blend_bwd_loss(const Ws&, const lsb_settings&, int, int, const float*, const float*, int, float,
+                                  double*, cudaStream_t);
 cudaError_t launch_blend_bwd(const Ws&, const lsb_settings&, int, int, const float*, const int32_t*,
                              const float*, float, cudaStream_t);
 cudaError_t launch_chain(const Ws&, const lsb_params&, const lsb_grads&, const lsb_camera&, const lsb_pose&,
@@ -241,6 +243,20 @@ int lsb_render_blend_bwd(const lsb_settings* s, void* ws, size_t ws_bytes, const
     if (rc) return rc;
     return check_cuda(launch_blend_bwd(w, *s, d->width, d->height, image, n_contrib, grad_image, grad_scale,
                                        (cudaStream_t)stream), "blend_bwd");
+}
+
+int lsb_render_blend_bwd_loss(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* d,
+                              const float* image, const float* observed, int kind, float grad_scale,
+                              double* loss_out, void* stream) {
+    if (!s || !observed || !loss_out) return fail(LSB_EINVAL, "NULL argument");
+    if (!image) return fail(LSB_EMISSING_CACHE, "render outputs missing");
+    if (kind != 0 && kind != 1) return fail(LSB_EINVAL, "kind must be 0 (l1) or 1 (l2)");
+    Ws w;
+    int rc = get_ws(ws, ws_bytes, d, &w);
+    if (rc) return rc;
+    return check_cuda(launch_blend_bwd_loss(w, *s, d->width, d->height, image, observed, kind, grad_scale, loss_out,
+                                            (cudaStream_t)stream),
+                      "blend_bwd_loss");
 }
 
 int lsb_render_chain(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T, const lsb_settings* s,

@@ -56,6 +56,9 @@ constexpr int RUN = 4;       // pixels per lane and row (horizontal run)
 #ifndef BWD_MIN_BLOCKS
 #define BWD_MIN_BLOCKS 4
 #endif
+#ifndef BWD_LOSS_VARIANT
+#define BWD_LOSS_VARIANT 0
+#endif
 #ifndef BLEND_RESERVE          // CTA slots per SM the persistent blend grids leave free
 #define BLEND_RESERVE 0           // (for a concurrent view lane's binning / chain kernels)
 #endif
@@ -265,9 +268,23 @@ struct RecPipe {
 __device__ __noinline__ void loss_total(const Ws& w, const LossArgs& L, int lane) {
     __threadfence();
     double v0 = 0.0, v1 = 0.0;
-    for (int t = lane; t < w.ntiles; t += 32) {
-        v0 += ((volatile double*)L.sums)[2 * t];
-        v1 += ((volatile double*)L.sums)[2 * t + 1];
+    // lane l adds tiles l, l + 32, ... in order; the loads of 8 tiles are in
+    // flight together (L2-coherent ld.cg), the additions keep their order
+    constexpr int B = 8;
+    for (int t0 = lane; t0 < w.ntiles; t0 += 32 * B) {
+        double2 x[B];
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+            const int t = t0 + 32 * k;
+            x[k] = t < w.ntiles ? __ldcg((const double2*)L.sums + t) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+            if (t0 + 32 * k < w.ntiles) {
+                v0 += x[k].x;
+                v1 += x[k].y;
+            }
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -481,8 +498,10 @@ __device__ __forceinline__ void bwd_half(const Frame& f, float4 q1, bool rin, fl
     M[5] = fmaf(S0 * dy, dy, M[5]);
 }
 
+template <bool LOSS>
 __global__ void __launch_bounds__(32 * WPB, BWD_MIN_BLOCKS)
-k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __restrict__ gimg, float gscale) {
+k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __restrict__ gimg, float gscale,
+            LossArgs L) {
     __shared__ Rec s_rec[WPB][2 * 32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int qx = (lane & 3) * RUN, r0 = lane >> 2;
@@ -503,6 +522,7 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __r
         const float gx0f = (float)gx0, gy0f = (float)gy0;
         // per-pixel state: T (as in the forward), gD = g . (I - prefix colour), g = dL/dI
         float T[2][RUN], gD[2][RUN], Gr[2][RUN], Gg[2][RUN], Gb[2][RUN];
+        double l0 = 0.0, l1 = 0.0;
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -513,12 +533,56 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __r
                 if (gy < a.H && gx0 + j < a.W) {
                     const int64_t p = (int64_t)gy * a.W + gx0 + j;
                     T[h][j] = 1.f;
-                    Gr[h][j] = gimg[3 * p] * gscale;
-                    Gg[h][j] = gimg[3 * p + 1] * gscale;
-                    Gb[h][j] = gimg[3 * p + 2] * gscale;
-                    gD[h][j] = Gr[h][j] * image[3 * p] + Gg[h][j] * image[3 * p + 1] + Gb[h][j] * image[3 * p + 2];
+                    const float i0 = image[3 * p], i1 = image[3 * p + 1], i2 = image[3 * p + 2];
+                    float g3[3];
+                    if (LOSS) {
+                        // photometric loss fused here (optimize.py:48-74, no mask):
+                        // dL/dI from (rendered, observed), same arithmetic as the
+                        // fused forward / lsb_photometric_loss
+                        const float i3[3] = {i0, i1, i2};
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+#if BWD_LOSS_VARIANT == 0
+                            const double d = (double)i3[c] - (double)L.observed[3 * p + c];
+                            l1 += d * d;
+                            if (L.kind == 0) {
+                                l0 += fabs(d);
+                                g3[c] = d > 0.0 ? L.gscale : (d < 0.0 ? -L.gscale : 0.f);
+                            } else {
+                                l0 += d * d;
+                                g3[c] = (float)(2.0 * d * (double)L.gscale);
+                            }
+#elif BWD_LOSS_VARIANT == 1
+                            const float d = i3[c] - L.observed[3 * p + c];
+                            l1 += (double)(d * d);
+                            l0 += (double)fabsf(d);
+                            g3[c] = d > 0.f ? L.gscale : (d < 0.f ? -L.gscale : 0.f);
+#else
+                            const float d = i3[c] - L.observed[3 * p + c];
+                            g3[c] = d > 0.f ? L.gscale : (d < 0.f ? -L.gscale : 0.f);
+#endif
+                        }
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) g3[c] = gimg[3 * p + c];
+                    }
+                    Gr[h][j] = g3[0] * gscale;
+                    Gg[h][j] = g3[1] * gscale;
+                    Gb[h][j] = g3[2] * gscale;
+                    gD[h][j] = Gr[h][j] * i0 + Gg[h][j] * i1 + Gb[h][j] * i2;
                 }
             }
+        if (LOSS) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+                l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+            }
+            if (lane == 0) {
+                L.sums[2 * tile] = l0;
+                L.sums[2 * tile + 1] = l1;
+            }
+        }
         const int start = w.tile_start[tile], end = w.tile_last[tile];
         pipe.start = start;
         pipe.end = end;
@@ -651,14 +715,31 @@ cudaError_t launch_blend_fwd(const Ws& w, const lsb_settings& s, int W, int H, f
     return cudaGetLastError();
 }
 
+// One warp: the loss total from the tile partials, in tile order.
+__global__ void k_loss_total(Ws w, LossArgs L) { loss_total(w, L, threadIdx.x); }
+
 cudaError_t launch_blend_bwd(const Ws& w, const lsb_settings& s, int W, int H, const float* image,
                              const int32_t* n_contrib, const float* gimg, float gscale, cudaStream_t st) {
     (void)n_contrib;    // liveness is recomputed bit-identically from T
     const BlendArgs a = blend_args(s, W, H);
     cudaError_t e = cudaMemsetAsync(w.ctr + 8, 0, sizeof(unsigned long long), st);   // backward tile queue
     if (e != cudaSuccess) return e;
-    k_blend_bwd<<<persistent_grid((const void*)k_blend_bwd, w.ntiles), 32 * WPB, 0, st>>>(w, a, image, gimg,
-                                                                                         gscale);
+    const LossArgs L{nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0.f};
+    k_blend_bwd<false><<<persistent_grid((const void*)k_blend_bwd<false>, w.ntiles), 32 * WPB, 0, st>>>(
+        w, a, image, gimg, gscale, L);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_blend_bwd_loss(const Ws& w, const lsb_settings& s, int W, int H, const float* image,
+                                  const float* observed, int kind, float grad_scale, double* loss_out,
+                                  cudaStream_t st) {
+    const BlendArgs a = blend_args(s, W, H);
+    cudaError_t e = cudaMemsetAsync(w.ctr + 8, 0, sizeof(unsigned long long), st);   // backward tile queue
+    if (e != cudaSuccess) return e;
+    const LossArgs L{observed, nullptr, w.loss_part, loss_out, nullptr, kind, grad_scale};
+    k_blend_bwd<true><<<persistent_grid((const void*)k_blend_bwd<true>, w.ntiles), 32 * WPB, 0, st>>>(
+        w, a, image, nullptr, 1.0f, L);
+    k_loss_total<<<1, 32, 0, st>>>(w, L);
     return cudaGetLastError();
 }
 

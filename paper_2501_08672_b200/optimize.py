@@ -25,7 +25,8 @@ from . import _lib
 from .errors import EmptyMask
 from .geometry import as_se3
 from .raster import (GaussianArrays, ParamGradients, RasterSettings, RenderState, _as_arrays, _f32,
-                     render_bin, render_blend, render_blend_bwd, render_blend_loss, render_chain)
+                     render_bin, render_blend, render_blend_bwd, render_blend_bwd_loss, render_blend_loss,
+                     render_chain)
 
 
 @dataclass
@@ -204,6 +205,7 @@ class WindowEngine:
                  bin_mode: Optional[int] = None):
         _lib.require()
         self.bin_mode = (1 if settings.alpha_cut > 0.0 else 0) if bin_mode is None else int(bin_mode)
+        self.loss_in_backward = True        # photometric loss fused into the backward (else the forward)
         self.arena = arrays
         if master == "f64" and arrays.dtype != torch.float64:
             arrays = arrays.clone(torch.float64)
@@ -333,17 +335,26 @@ class WindowEngine:
                 sm.wait_event(copied[v])
                 obs = self.obs_dev[v]
             mark("blend_fwd", sm)
-            # no processed-entry count in the step: the count-free forward
-            render_blend_loss(st, ln.image, ln.t_final, None, obs, _KIND[self.cfg.loss],
-                              gscale, ln.grad_image, self.loss.ptr(v), stream=sm)
-            mark("blend_fwd", sm)
+            if self.loss_in_backward:
+                # count-free forward; the photometric loss and dL/dI are formed
+                # inside the backward, which reads the observed image
+                render_blend(st, ln.image, ln.t_final, None, stream=sm)
+                mark("blend_fwd", sm)
+                mark("blend_bwd", sm)
+                render_blend_bwd_loss(st, ln.image, obs, _KIND[self.cfg.loss], gscale, self.loss.ptr(v), stream=sm)
+                mark("blend_bwd", sm)
+            else:
+                # count-free forward with the loss fused into its epilogue
+                render_blend_loss(st, ln.image, ln.t_final, None, obs, _KIND[self.cfg.loss],
+                                  gscale, ln.grad_image, self.loss.ptr(v), stream=sm)
+                mark("blend_fwd", sm)
+                mark("blend_bwd", sm)
+                render_blend_bwd(st, ln.image, None, ln.grad_image, 1.0, sm)
+                mark("blend_bwd", sm)
             if host and not capturing:
                 ev = torch.cuda.Event()
                 ev.record(sm)
                 self._consumed[v] = ev
-            mark("blend_bwd", sm)
-            render_blend_bwd(st, ln.image, None, ln.grad_image, 1.0, sm)
-            mark("blend_bwd", sm)
             if prev_chain is not None and sm is not main:
                 sm.wait_event(prev_chain)
             mark("chain", sm); render_chain(st, self.grads, None, sm); mark("chain", sm)

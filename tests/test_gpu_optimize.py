@@ -83,7 +83,7 @@ def test_optimize_zero_iters_is_identity():
     assert bool((arrays.shs == before).all())
 
 
-def _room_engine(lanes, steps=2, mode="eager"):
+def _room_engine(lanes, steps=2, mode="eager", loss_in_backward=True):
     import torch
     from paper_2501_08672_b200.optimize import OptimConfig, WindowEngine
     from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
@@ -99,6 +99,7 @@ def _room_engine(lanes, steps=2, mode="eager"):
     win = GaussianArrays(s["means"], s["rots"], s["scales"], s["opacities"], shs)
     stream = torch.cuda.Stream()
     eng = WindowEngine(win, cam, views, st, OptimConfig(), lanes=lanes, stream=stream)
+    eng.loss_in_backward = loss_in_backward
     if mode == "host":      # pinned host images staged on the copy stream
         obs = [o.cpu().pin_memory() for o in obs]
     with torch.cuda.stream(stream):
@@ -120,6 +121,18 @@ def test_engine_view_lanes_bit_identical():
     bit-identical to the single-stream engine."""
     w1, l1, g1 = _room_engine(1)
     w2, l2, g2 = _room_engine(2)
+    assert bool((g1 == g2).all())
+    assert np.array_equal(l1, l2)
+    for k in ("means", "rots", "scales", "opacities", "shs"):
+        assert bool((getattr(w1, k) == getattr(w2, k)).all()), k
+
+
+def test_engine_loss_in_backward_bit_identical():
+    """The photometric loss fused into the backward (lsb_render_blend_bwd_loss)
+    gives the same losses, gradients and parameters as the loss fused into
+    the forward's epilogue (lsb_render_blend_loss + lsb_render_blend_bwd)."""
+    w1, l1, g1 = _room_engine(2, loss_in_backward=True)
+    w2, l2, g2 = _room_engine(2, loss_in_backward=False)
     assert bool((g1 == g2).all())
     assert np.array_equal(l1, l2)
     for k in ("means", "rots", "scales", "opacities", "shs"):

@@ -82,6 +82,8 @@ def main(tag):
              "|---|---|---|---|---|---|---|---|---|---|"]
     traffic_path = os.path.join(PROF, "traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+    issue_path = os.path.join(PROF, "issue.json")
+    issue = json.load(open(issue_path)) if os.path.exists(issue_path) else {}
     for rep in sorted(glob.glob(os.path.join(OUT, f"prof_{tag}_*.ncu-rep"))):
         for d in raw(rep):
             name = d["kernel"].replace("void ", "").split("(")[0].split("::")[-1].split("<")[0]
@@ -92,8 +94,10 @@ def main(tag):
                          f"{d.get('sm_active_cyc', 0) / max(d.get('elapsed_cyc', 1), 1):.2f} |")
             if name in KEY and name != "k_tile_sort":
                 traffic[KEY[name]] = tb
+                issue[KEY[name]] = {"warp_inst_per_launch": d.get("warp_inst", 0), "capture": tag}
     open(os.path.join(PROF, f"{tag}_kernels.md"), "w").write("\n".join(lines) + "\n")
     json.dump(traffic, open(traffic_path, "w"), indent=1)
+    json.dump(issue, open(issue_path, "w"), indent=1)
     lc = os.path.join(OUT, f"launches_{tag}.csv")
     if os.path.exists(lc):
         shutil.copy(lc, os.path.join(PROF, f"{tag}_launches.csv"))
