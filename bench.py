@@ -245,13 +245,30 @@ def run_ours(args, wl, rank, world, local_rank):
     eager_ms = k0.elapsed_time(k1) / args.steps
     del keng
 
-    # pass 2 (the headline): the same step captured once as a CUDA graph
-    use_graph = args.graph and world == 1
-    if use_graph:
-        eng.capture(observed)
-        with torch.cuda.stream(stream):
-            eng.replay()
-        torch.cuda.synchronize()
+    # pass 2 (the headline): the same step captured once as a CUDA graph (the
+    # NCCL all-reduce included when N > 1; if any rank fails to capture, all
+    # ranks fall back to eager launches)
+    def try_capture(obs):
+        ok = 1
+        try:
+            eng.capture(obs, allreduce)
+            with torch.cuda.stream(stream):
+                eng.replay()
+            torch.cuda.synchronize()
+        except Exception as exc:          # noqa: BLE001 - fall back to eager
+            ok = 0
+            eng.graph = None
+            print(f"[bench] rank {rank}: CUDA-graph capture failed ({exc}); eager launches", file=sys.stderr)
+        if world > 1:
+            t = torch.tensor([ok], device=dev, dtype=torch.int32)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            ok = int(t.item())
+            if not ok:
+                eng.graph = None
+        return bool(ok)
+
+    use_graph = bool(args.graph) and try_capture(observed)
+    graph_headline = use_graph
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -309,7 +326,7 @@ def run_ours(args, wl, rank, world, local_rank):
         eng.step(host_obs, allreduce=allreduce)            # e2e warm-up (staging buffers)
     torch.cuda.synchronize()
     if use_graph:
-        eng.capture(host_obs)
+        use_graph = try_capture(host_obs)
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         e_start.record(stream)
@@ -340,7 +357,8 @@ def run_ours(args, wl, rank, world, local_rank):
             "visible_splats_per_s": float(sum(c[0] for c in counts)) * world / (ms * 1e-3),
             "config": {"workload": args.config, "gaussians": N, "views": V, "width": W, "height": H,
                        "alpha_cut": wl["alpha_cut"], "parallelism": f"view-sharded dp{world}",
-                       "view_lanes": args.lanes, "cuda_graph": use_graph, "serial_ms_per_step": eager_ms,
+                       "view_lanes": args.lanes, "cuda_graph": graph_headline, "cuda_graph_e2e": use_graph,
+                       "serial_ms_per_step": eager_ms,
                        "kernel_timing": "separate one-lane eager pass of the same steps, events around each kernel",
                        "l2": "working set > L2: observed views alone are V x 15.7 MB",
                        "loss_last_step": float(np.mean(losses))},
@@ -361,9 +379,9 @@ def run_ours(args, wl, rank, world, local_rank):
             "clocks": clk_sum,
             "e2e": {"value": V * W * H / (e_ms * 1e-3) / 1e6, "unit": "Mpix/s",
                     "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world, "ms_per_step": e_ms},
-            "gpu_launches": args.steps * (len(my_views) * 8 + 2) + 1,   # per view: preprocess, scan, scatter,
-            # tile sort, big-tile sort, blend+loss, blend bwd, chain; + adam and step counter per step;
-            # + final orthonormalize
+            "gpu_launches": args.steps * (len(my_views) * 9 + 2) + 1,   # per view: preprocess, scan, scatter,
+            # tile sort, big-tile sort, blend fwd, blend bwd (+loss), loss total, chain; + adam and step counter
+            # per step; + final orthonormalize
         }
         if world == 1 and not args.no_cpu_baseline:
             tv, ta, cores = cpu_sample(wl, 2)
