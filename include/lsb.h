@@ -300,6 +300,38 @@ int lsb_voxmap_dump(const lsb_voxmap* m, int64_t* keys, int64_t* slots, uint64_t
 /* Re-insert every leaf of `src` into the (larger, empty) table `dst`. */
 int lsb_voxmap_rehash(const lsb_voxmap* src, const lsb_voxmap* dst, void* stream);
 
+/* ---- sliding window: replaces GaussianWindow.maintain (window.py:136-276)
+ * The live window is the f32 SoA arena `arena` (capacity rows, n live); the
+ * global map's Gaussians are rows of `store` (mean 3 | rot 9 | scale 3 |
+ * opacity 1 | sh 3K floats, the reference's arena row, window.py:58-60)
+ * indexed by the leaf's gid (lsb_voxmap.gslot).  Keys are "order keys"
+ * ((ix+2^20) << 42 | (iy+2^20) << 21 | (iz+2^20)): integer order is sorted
+ * VoxelKey order.  wkeys (capacity) holds the key of every slot, -1 if free.
+ *   mark:    rebuild the window hash (hkeys/hslots, hcap a power of two >=
+ *            2n) and probe the m FoV keys: keep[slot] = 1 for live ∩ FoV,
+ *            is_add[i] = 1 for FoV keys not live (diff, window.py:136-143).
+ *   plan:    one CTA: dels = deleted slots ascending, movers = the live slots
+ *            at or above the new live count, from the rear; counts = [k, h]
+ *            (deleted, moves).  Synchronise to read counts.
+ *   compact: write the k deleted rows back to the map store (their leaves'
+ *            gids; flag bit 2 on a missing leaf), then move movers[r] ->
+ *            dels[r] for r < h and free the top k slots (window.py:145-181).
+ *   leaf_gids / dist: per (sorted) add key, the map gid (-1: no Gaussian) and
+ *            the f64 distance of the voxel centre to `origin` (numpy's
+ *            norm, for the capacity ranking, window.py:262-270).
+ *   append:  the adds holding a Gaussian, in key order, to slots first_slot,
+ *            first_slot + 1, ... (*n_added on the device; window.py:183-209). */
+int lsb_window_mark(const int64_t* wkeys, int64_t n, uint64_t* hkeys, int32_t* hslots, int64_t hcap,
+                    const int64_t* fov, int64_t m, uint8_t* keep, uint8_t* is_add, void* stream);
+int lsb_window_plan(const uint8_t* keep, int64_t n, int32_t* dels, int32_t* movers, int64_t* counts, void* stream);
+int lsb_window_compact(const lsb_voxmap* m, const lsb_params* arena, int64_t* wkeys, const int32_t* dels, int64_t k,
+                       const int32_t* movers, int64_t h, int64_t n, float* store, void* stream);
+int lsb_window_leaf_gids(const lsb_voxmap* m, const int64_t* okeys, int64_t cnt, int32_t* gids, void* stream);
+int lsb_window_dist(const int64_t* okeys, int64_t cnt, double edge, const double* origin, double* out,
+                    void* stream);
+int lsb_window_append(const lsb_params* arena, int64_t* wkeys, const int64_t* okeys, const int32_t* gids, int64_t cnt,
+                      const float* store, int64_t first_slot, int64_t* n_added, void* stream);
+
 /* ---- photometric loss: replaces optimize.photometric_loss (optimize.py:48-74)
  * kind 0 = L1, 1 = L2 over (npx, 3) f32 images; mask (npx) u8 may be NULL.
  * grad_out (npx,3) f32 = sign(diff) (L1) or 2 diff (L2), times grad_scale

@@ -108,6 +108,13 @@ SIGNATURES = [
     ("lsb_voxmap_fov", _c.c_int, [_c.POINTER(VoxMap), _P, _c.c_int64, _P, _c.c_int64, _P, _P, _c.c_int64, _P]),
     ("lsb_voxmap_dump", _c.c_int, [_c.POINTER(VoxMap), _P, _P, _P, _c.c_int64, _P]),
     ("lsb_voxmap_rehash", _c.c_int, [_c.POINTER(VoxMap), _c.POINTER(VoxMap), _P]),
+    ("lsb_window_mark", _c.c_int, [_P, _c.c_int64, _P, _P, _c.c_int64, _P, _c.c_int64, _P, _P, _P]),
+    ("lsb_window_plan", _c.c_int, [_P, _c.c_int64, _P, _P, _P, _P]),
+    ("lsb_window_compact", _c.c_int, [_c.POINTER(VoxMap), _c.POINTER(Params), _P, _P, _c.c_int64, _P, _c.c_int64,
+                                      _c.c_int64, _P, _P]),
+    ("lsb_window_leaf_gids", _c.c_int, [_c.POINTER(VoxMap), _P, _c.c_int64, _P, _P]),
+    ("lsb_window_dist", _c.c_int, [_P, _c.c_int64, _c.c_double, _c.POINTER(_c.c_double), _P, _P]),
+    ("lsb_window_append", _c.c_int, [_c.POINTER(Params), _P, _P, _P, _c.c_int64, _P, _c.c_int64, _P, _P]),
     ("lsb_loss_scratch_doubles", _c.c_int, []),
     ("lsb_photometric_loss", _c.c_int, [_P, _P, _P, _c.c_int64, _c.c_int64, _c.c_int, _c.c_float,
                                         _P, _P, _P]),

@@ -16,7 +16,8 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path
           "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 # per-file extra flags: the preprocess keeps f64 rounding where numpy rounds
 EXTRA = {"preprocess.cu": ["--fmad=false"]}
-SOURCES = ["preprocess.cu", "blend.cu", "chain.cu", "loss.cu", "adam.cu", "pose.cu", "voxmap.cu", "api.cu"]
+SOURCES = ["preprocess.cu", "blend.cu", "chain.cu", "loss.cu", "adam.cu", "pose.cu", "voxmap.cu", "window.cu",
+           "api.cu"]
 
 
 def build(verbose: bool = False, defines=(), out: str = OUT, tag: str = "") -> str:
@@ -29,7 +30,8 @@ def build(verbose: bool = False, defines=(), out: str = OUT, tag: str = "") -> s
     for src in SOURCES:
         obj = os.path.join(bdir, src.replace(".cu", ".o"))
         srcp = os.path.join(CSRC, src)
-        deps = [srcp, os.path.join(CSRC, "common.cuh"), os.path.join(ROOT, "include", "lsb.h")]
+        deps = [srcp, os.path.join(ROOT, "include", "lsb.h")] + [os.path.join(CSRC, h) for h in os.listdir(CSRC)
+                                                                  if h.endswith(".cuh")]
         if not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(d) for d in deps):
             cmd = [NVCC, *ARCH, *COMMON, *dflags, *EXTRA.get(src, []), "-c", srcp, "-o", obj]
             r = subprocess.run(cmd, capture_output=True, text=True)

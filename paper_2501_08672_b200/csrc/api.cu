@@ -38,6 +38,15 @@ cudaError_t launch_vox_fov(const lsb_voxmap&, const double*, int64_t, unsigned l
                            unsigned long long*, int64_t, cudaStream_t);
 cudaError_t launch_vox_dump(const lsb_voxmap&, int64_t*, int64_t*, unsigned long long*, int64_t, cudaStream_t);
 cudaError_t launch_vox_rehash(const lsb_voxmap&, const lsb_voxmap&, cudaStream_t);
+cudaError_t launch_win_mark(const int64_t*, int64_t, uint64_t*, int32_t*, int64_t, const int64_t*, int64_t, uint8_t*,
+                            uint8_t*, cudaStream_t);
+cudaError_t launch_win_plan(const uint8_t*, int64_t, int32_t*, int32_t*, int64_t*, cudaStream_t);
+cudaError_t launch_win_compact(const lsb_voxmap&, const lsb_params&, int64_t*, const int32_t*, int64_t,
+                               const int32_t*, int64_t, int64_t, float*, cudaStream_t);
+cudaError_t launch_win_leaf_gids(const lsb_voxmap&, const int64_t*, int64_t, int32_t*, cudaStream_t);
+cudaError_t launch_win_dist(const int64_t*, int64_t, double, const double*, double*, cudaStream_t);
+cudaError_t launch_win_append(const lsb_params&, int64_t*, const int64_t*, const int32_t*, int64_t, const float*,
+                              int64_t, int64_t*, cudaStream_t);
 }  // namespace lsb
 
 using namespace lsb;
@@ -417,6 +426,64 @@ int lsb_photometric_loss(const float* rendered, const float* observed, const uin
     return check_cuda(launch_loss(rendered, observed, mask, npx, kind, grad_scale, grad_out, sums_out,
                                   (cudaStream_t)stream),
                       "loss");
+}
+
+static int arena_ok(const lsb_params* a) {
+    if (!a || !a->means || !a->rots || !a->scales || !a->opacities || !a->shs) return fail(LSB_EINVAL, "NULL arena");
+    if (a->dtype != 0) return fail(LSB_EINVAL, "the window arena is f32");
+    if (a->sh_coeffs < 1 || a->sh_coeffs > 16) return fail(LSB_EINVAL, "sh_coeffs must be in [1, 16]");
+    return LSB_OK;
+}
+
+int lsb_window_mark(const int64_t* wkeys, int64_t n, uint64_t* hkeys, int32_t* hslots, int64_t hcap,
+                    const int64_t* fov, int64_t m, uint8_t* keep, uint8_t* is_add, void* stream) {
+    if (n < 0 || m < 0) return fail(LSB_EINVAL, "negative count");
+    if (hcap <= 0 || (hcap & (hcap - 1)) || hcap < 2 * n) return fail(LSB_EINVAL, "window hash capacity");
+    if (!hkeys || !hslots || (n && (!wkeys || !keep)) || (m && (!fov || !is_add)))
+        return fail(LSB_EINVAL, "NULL array");
+    return check_cuda(launch_win_mark(wkeys, n, hkeys, hslots, hcap, fov, m, keep, is_add, (cudaStream_t)stream),
+                      "window_mark");
+}
+
+int lsb_window_plan(const uint8_t* keep, int64_t n, int32_t* dels, int32_t* movers, int64_t* counts, void* stream) {
+    if (n < 0 || !counts || (n && (!keep || !dels || !movers))) return fail(LSB_EINVAL, "NULL array");
+    return check_cuda(launch_win_plan(keep, n, dels, movers, counts, (cudaStream_t)stream), "window_plan");
+}
+
+int lsb_window_compact(const lsb_voxmap* m, const lsb_params* arena, int64_t* wkeys, const int32_t* dels, int64_t k,
+                       const int32_t* movers, int64_t h, int64_t n, float* store, void* stream) {
+    int rc = vox_ok(m);
+    if (rc) return rc;
+    rc = arena_ok(arena);
+    if (rc) return rc;
+    if (k < 0 || h < 0 || h > k || k > n) return fail(LSB_EINVAL, "bad counts");
+    if (k && (!dels || !store || !wkeys)) return fail(LSB_EINVAL, "NULL array");
+    if (h && !movers) return fail(LSB_EINVAL, "NULL array");
+    return check_cuda(launch_win_compact(*m, *arena, wkeys, dels, k, movers, h, n, store, (cudaStream_t)stream),
+                      "window_compact");
+}
+
+int lsb_window_leaf_gids(const lsb_voxmap* m, const int64_t* okeys, int64_t cnt, int32_t* gids, void* stream) {
+    int rc = vox_ok(m);
+    if (rc) return rc;
+    if (cnt < 0 || (cnt && (!okeys || !gids))) return fail(LSB_EINVAL, "NULL array");
+    return check_cuda(launch_win_leaf_gids(*m, okeys, cnt, gids, (cudaStream_t)stream), "window_leaf_gids");
+}
+
+int lsb_window_dist(const int64_t* okeys, int64_t cnt, double edge, const double* origin, double* out,
+                    void* stream) {
+    if (!origin || cnt < 0 || (cnt && (!okeys || !out))) return fail(LSB_EINVAL, "NULL array");
+    return check_cuda(launch_win_dist(okeys, cnt, edge, origin, out, (cudaStream_t)stream), "window_dist");
+}
+
+int lsb_window_append(const lsb_params* arena, int64_t* wkeys, const int64_t* okeys, const int32_t* gids, int64_t cnt,
+                      const float* store, int64_t first_slot, int64_t* n_added, void* stream) {
+    int rc = arena_ok(arena);
+    if (rc) return rc;
+    if (!n_added || cnt < 0 || (cnt && (!okeys || !gids || !store || !wkeys))) return fail(LSB_EINVAL, "NULL array");
+    return check_cuda(launch_win_append(*arena, wkeys, okeys, gids, cnt, store, first_slot, n_added,
+                                        (cudaStream_t)stream),
+                      "window_append");
 }
 
 }  // extern "C"

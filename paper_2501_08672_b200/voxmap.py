@@ -49,6 +49,17 @@ class VoxelKey(NamedTuple):
         return VoxelKey(self.ix // s, self.iy // s, self.iz // s, 0)
 
 
+def gaussian_row(g, width: Optional[int] = None) -> np.ndarray:
+    """A Gaussian3D-like object as one f32 arena row (window.py:58-71):
+    mean 3 | rot 9 | scale 3 | opacity 1 | sh 3K (K from `width` if given)."""
+    sh = np.asarray(g.sh, dtype=np.float64).reshape(-1, 3)
+    K = sh.shape[0] if width is None else (width - 16) // 3
+    shk = np.zeros((K, 3))
+    shk[: min(K, sh.shape[0])] = sh[:K]
+    return np.concatenate([np.asarray(g.mean_w, float).ravel(), np.asarray(g.rot, float).ravel(),
+                           np.asarray(g.scale, float).ravel(), [float(g.opacity)], shk.ravel()]).astype(np.float32)
+
+
 class Inserted:
     pass
 
@@ -233,6 +244,50 @@ class HashOctree:
         k = min(int(n_out.item()), out_cap)
         return keys[:k], slots[:k]
 
+    # ---- device Gaussian store (the map side of the sliding window) ------------
+    def _store_reserve(self, rows: int, width: int) -> None:
+        st = getattr(self, "store", None)
+        if st is not None and st.shape[1] != width:
+            raise ValueError(f"map rows have {st.shape[1]} floats, got {width}")
+        if st is None or st.shape[0] < rows:
+            cap = 1 << max(10, int(np.ceil(np.log2(max(rows, 2)))))
+            new = torch.zeros((cap, width), dtype=torch.float32, device=self.device)
+            if st is not None:
+                new[: st.shape[0]] = st
+            self.store = new
+
+    def set_gaussians_dev(self, keys, rows) -> torch.Tensor:
+        """Give each leaf key one Gaussian: rows (k, 16+3K) f32 in the
+        reference's arena row layout (mean 3 | rot 9 | scale 3 | opacity 1 |
+        sh 3K, window.py:58-60).  Leaves are created as needed (ensure_leaf);
+        a leaf that already holds a Gaussian has it replaced (write_back,
+        voxmap.py:190-194).  Returns the gids (k,) int32."""
+        k = torch.as_tensor(np.asarray(keys, dtype=np.int64)) if not torch.is_tensor(keys) else keys
+        k = k.to(device=self.device, dtype=torch.int64).reshape(-1, 3)
+        rows = torch.as_tensor(rows, dtype=torch.float32).to(self.device).reshape(k.shape[0], -1)
+        centers = (k.to(torch.float64) + 0.5) * self.leaf_len        # floor(centre / leaf_len) == key
+        tslots = self.accumulate_points_dev(centers, accumulate=False)
+        self._check_flags()
+        g = self.gslot[tslots]
+        new = g < 0
+        n_new = int(new.sum().item())
+        if n_new:
+            g[new] = torch.arange(self._next_gid, self._next_gid + n_new, dtype=torch.int32, device=self.device)
+            self._next_gid += n_new
+            self.gslot[tslots] = g
+        self._store_reserve(self._next_gid, rows.shape[1])
+        self.store[g.long()] = rows
+        return g
+
+    def gaussian_rows_dev(self, keys) -> torch.Tensor:
+        """Store rows of the leaves' Gaussians (NaN rows where none)."""
+        t = self.lookup_dev(keys)
+        g = torch.where(t >= 0, self.gslot[t.clamp(min=0)], torch.full_like(t, -1, dtype=torch.int32))
+        out = torch.full((t.shape[0], self.store.shape[1]), float("nan"), dtype=torch.float32, device=self.device)
+        ok = g >= 0
+        out[ok] = self.store[g[ok].long()]
+        return out
+
     # ---- reference-shaped helpers ------------------------------------------------
     def _keys_of_slots(self, slots: torch.Tensor) -> np.ndarray:
         slots = slots[slots >= 0]
@@ -261,8 +316,12 @@ class HashOctree:
         status = self.try_insert_batch([np.asarray(g.mean_w, dtype=float)])
         ok = bool(int(status.item()))
         if ok:
-            self.gaussians[self._next_gid - 1] = g
+            gid = self._next_gid - 1
+            self.gaussians[gid] = g
             g.level = self.max_level
+            row = gaussian_row(g)
+            self._store_reserve(gid + 1, row.shape[0])
+            self.store[gid] = torch.as_tensor(row, device=self.device)
         return Inserted() if ok else Full()
 
     def get_leaf(self, key: VoxelKey):
@@ -277,6 +336,8 @@ class HashOctree:
             raise MissingVoxel(key)
         if params and leaf["gid"] >= 0:
             self.gaussians[leaf["gid"]] = params[0]
+        if params and getattr(self, "store", None) is not None:
+            self.set_gaussians_dev([[key.ix, key.iy, key.iz]], gaussian_row(params[0], self.store.shape[1])[None])
 
     def leaf_stats(self, key: VoxelKey):
         leaf = self.get_leaf(key)
