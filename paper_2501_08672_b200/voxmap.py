@@ -319,9 +319,10 @@ class HashOctree:
             gid = self._next_gid - 1
             self.gaussians[gid] = g
             g.level = self.max_level
-            row = gaussian_row(g)
-            self._store_reserve(gid + 1, row.shape[0])
-            self.store[gid] = torch.as_tensor(row, device=self.device)
+            if all(hasattr(g, a) for a in ("rot", "scale", "opacity", "sh")):    # full payload: device row
+                row = gaussian_row(g, None if getattr(self, "store", None) is None else self.store.shape[1])
+                self._store_reserve(gid + 1, row.shape[0])
+                self.store[gid] = torch.as_tensor(row, device=self.device)
         return Inserted() if ok else Full()
 
     def get_leaf(self, key: VoxelKey):
