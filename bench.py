@@ -480,6 +480,90 @@ def run_voxel(args, rank, world, local_rank):
         }), flush=True)
 
 
+# ------------------------------------------------------------- window -------
+WINDOW_CFG = dict(frames=40, root_len=0.1, max_level=2, capacity=200_000)
+
+
+def run_window(args, rank, world, local_rank):
+    """Sliding-window maintenance (window.py:236-276):
+    per frame, the FoV leaves of an orbit LiDAR scan are diffed against the
+    live window, departing rows are written back to the map store, the
+    window is compacted and the arriving leaves' Gaussians appended (capacity
+    drops ranked by distance to the sensor).  The map (one Gaussian per leaf
+    of all scans) and each frame's FoV key set are built before the timed
+    region; the timed region is the maintain calls (host wall clock around
+    each, synchronised: maintain reads its counts back).  Replicas only."""
+    import torch
+    from paper_2501_08672_b200.scene import T_LI, lidar_scan, orbit_imu_pose, room_triangles, scan_directions
+    from paper_2501_08672_b200.voxmap import HashOctree
+    from paper_2501_08672_b200.window import GaussianWindow
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    F, K = WINDOW_CFG["frames"], 1
+    tris, dirs = room_triangles(), scan_directions()
+    poses = [orbit_imu_pose(a) @ T_LI for a in np.linspace(0.0, 1.5 * np.pi, F)]
+    scans = [lidar_scan(T, tris, dirs, device=dev).contiguous() for T in poses]
+    vmap = HashOctree(WINDOW_CFG["root_len"], WINDOW_CFG["max_level"], capacity=1 << 22, device=dev)
+    for p in scans:
+        vmap.accumulate_points_dev(p)
+    keys, _ = vmap.dump_dev()
+    leaf = vmap.leaf_len
+    rows = torch.zeros((keys.shape[0], 16 + 3 * K), dtype=torch.float32, device=dev)
+    rows[:, 0:3] = ((keys.to(torch.float64) + 0.5) * leaf).to(torch.float32)
+    rows[:, 3] = rows[:, 7] = rows[:, 11] = 1.0
+    rows[:, 12:15] = leaf / 2
+    rows[:, 15] = 0.5
+    rows[:, 16:] = torch.rand((keys.shape[0], 3 * K), generator=torch.Generator(device=dev).manual_seed(0),
+                              device=dev) - 0.5
+    vmap.set_gaussians_dev(keys, rows)
+    fovs = [vmap.fov_leaf_keys_dev(p).clone() for p in scans]
+    sensors = [np.asarray(T.t, dtype=np.float64) for T in poses]
+
+    def walk(win, frames):
+        times, reps = [], []
+        for f in frames:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            reps.append(win.maintain(vmap, fovs[f], sensor_pos=sensors[f]))
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+        return times, reps
+
+    walk(GaussianWindow(WINDOW_CFG["capacity"], K, device=dev), range(min(args.warmup, F)))
+    with ClockSampler(local_rank) as clk:
+        times, reps = walk(GaussianWindow(WINDOW_CFG["capacity"], K, device=dev), range(F))
+    ms = float(np.median(times)) * 1e3
+    fov_avg = float(np.mean([f.shape[0] for f in fovs]))
+    # CPU baseline: the oracle restatement (dict map) on the first frames
+    from oracle.window import Window
+    store = {tuple(int(v) for v in k): r for k, r in zip(keys.cpu().numpy(), rows.cpu().numpy())}
+    ow = Window(WINDOW_CFG["capacity"], 16 + 3 * K)
+    nb = 3
+    t_cpu = []
+    for f in range(nb):
+        fov = {tuple(int(v) for v in k) for k in fovs[f].cpu().numpy()}
+        t0 = time.perf_counter()
+        ow.maintain(store, fov, leaf, None, sensors[f])
+        t_cpu.append(time.perf_counter() - t0)
+    if rank == 0:
+        print(json.dumps({
+            "metric": "sliding-window maintain ms/frame (SURVEY.md §8(f) rank 1)", "value": ms, "unit": "ms/frame",
+            "n_gpus": 1, "steps": F, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "replicas", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "window", "frames": F, "root_len": WINDOW_CFG["root_len"],
+                       "max_level": WINDOW_CFG["max_level"], "capacity": WINDOW_CFG["capacity"],
+                       "map_gaussians": int(keys.shape[0]), "fov_keys_avg": fov_avg,
+                       "added_avg": float(np.mean([r.added for r in reps[1:]])),
+                       "removed_avg": float(np.mean([r.removed for r in reps[1:]])),
+                       "moved_avg": float(np.mean([r.moved for r in reps[1:]])),
+                       "dropped_avg": float(np.mean([r.dropped for r in reps[1:]])),
+                       "timing": "host wall clock per maintain (synchronised), median over frames"},
+            "clocks": clk.summary(),
+            "cpu_baseline": {"value": float(np.median(t_cpu)) * 1e3, "unit": "ms/frame", "cores": 1, "kind": "port",
+                             "sample": f"first {nb} frames on the oracle restatement (dict map)"},
+        }), flush=True)
+
+
 # ------------------------------------------------------------- config 4 -----
 def run_ieskf(args, rank, world, local_rank):
     """IESKF photometric update (config 4): 5 iterations, each re-rendering
@@ -538,7 +622,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS) + ["cfg3", "cfg4"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS) + ["cfg3", "cfg4", "window"])
     ap.add_argument("--alpha-cut", type=float, default=1.0 / 255.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--lanes", type=int, default=5, help="concurrent view pipelines per GPU")
@@ -552,6 +636,9 @@ def main():
         return
     if args.config == "cfg4":
         run_ieskf(args, rank, world, local_rank)
+        return
+    if args.config == "window":
+        run_window(args, rank, world, local_rank)
         return
     wl = build_workload(args.config, args.alpha_cut)
     if args.impl == "reference":
