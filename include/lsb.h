@@ -244,8 +244,10 @@ int lsb_pose_rows(const lsb_settings* s, int sh_degree_used, void* ws, size_t ws
                   const float* chain, const int32_t* pixel_ids, int64_t m, const double* A,
                   const double* R_cw, double* rows_out, void* stream);
 /* out (42 doubles): [0..35] sum h h^T / sigma^2 (6x6), [36..41] sum h z / sigma^2,
- * h = -row (the pose block of H).  Deterministic single-CTA reduction. */
-int lsb_hb_reduce(const double* rows, const double* z, int64_t m, double inv_sigma2, double* out,
+ * h = -row (the pose block of H).  Deterministic: fixed-grid CTA partials in
+ * `scratch` (lsb_hb_scratch_doubles() doubles), then a fixed-order sum. */
+int lsb_hb_scratch_doubles(void);
+int lsb_hb_reduce(const double* rows, const double* z, int64_t m, double inv_sigma2, double* out, double* scratch,
                   void* stream);
 /* Semi-dense candidate mask (estimator.py:241-252): Sobel/8 magnitude of the
  * grey observed image (nearest border) > grad_thr and t_final < t_max. */
@@ -299,6 +301,22 @@ int lsb_voxmap_dump(const lsb_voxmap* m, int64_t* keys, int64_t* slots, uint64_t
                     int64_t out_cap, void* stream);
 /* Re-insert every leaf of `src` into the (larger, empty) table `dst`. */
 int lsb_voxmap_rehash(const lsb_voxmap* src, const lsb_voxmap* dst, void* stream);
+
+/* Plane fits: replaces HashOctree.fit_planes / estimate_normal / plane_at
+ * (voxmap.py:255-335).  Per leaf key (k,3): the leaf's and its 6 face
+ * neighbours' statistics, the smallest-scatter eigenvector (f64 Jacobi)
+ * facing `origin` and the leaf's own centroid; valid[i] = 0 (NaN rows) for
+ * an empty leaf, fewer than 3 points or scatter rank < 2. */
+int lsb_voxmap_fit_planes(const lsb_voxmap* m, const int64_t* keys, int64_t k, const double* origin, double* normals,
+                          double* anchors, uint8_t* valid, void* stream);
+/* LiDAR point-to-plane rows: replaces the per-point part of
+ * lidar_measurement (estimator.py:190-238).  pts_l (n,3) f64 in the LiDAR
+ * frame; T_IL and T_WI as row-major R and t.  Per point: rows (n,6) =
+ * -H[:, :6] (the lsb_hb_reduce convention), z = n . (p_w - anchor),
+ * keep = a plane was found for the point's leaf and |z| <= gate. */
+int lsb_lidar_rows(const lsb_voxmap* m, const double* pts_l, int64_t n, const double* R_il, const double* t_il,
+                   const double* R_wi, const double* t_wi, double gate, double* rows, double* z, uint8_t* keep,
+                   void* stream);
 
 /* ---- sliding window: replaces GaussianWindow.maintain (window.py:136-276)
  * The live window is the f32 SoA arena `arena` (capacity rows, n live); the

@@ -99,7 +99,8 @@ SIGNATURES = [
                                     _c.POINTER(Settings), _P, _c.c_size_t, _c.POINTER(Dims), _P, _P]),
     ("lsb_pose_rows", _c.c_int, [_c.POINTER(Settings), _c.c_int, _P, _c.c_size_t, _c.POINTER(Dims), _P, _P, _P,
                                  _P, _c.c_int64, _c.POINTER(_c.c_double), _c.POINTER(_c.c_double), _P, _P]),
-    ("lsb_hb_reduce", _c.c_int, [_P, _P, _c.c_int64, _c.c_double, _P, _P]),
+    ("lsb_hb_scratch_doubles", _c.c_int, []),
+    ("lsb_hb_reduce", _c.c_int, [_P, _P, _c.c_int64, _c.c_double, _P, _P, _P]),
     ("lsb_semidense_mask", _c.c_int, [_P, _P, _c.c_int32, _c.c_int32, _c.c_double, _c.c_double, _P, _P]),
     ("lsb_voxmap_keys", _c.c_int, [_P, _c.c_int64, _c.c_double, _P, _P]),
     ("lsb_voxmap_insert_points", _c.c_int, [_c.POINTER(VoxMap), _P, _c.c_int64, _c.c_int32, _P, _P]),
@@ -108,6 +109,11 @@ SIGNATURES = [
     ("lsb_voxmap_fov", _c.c_int, [_c.POINTER(VoxMap), _P, _c.c_int64, _P, _c.c_int64, _P, _P, _c.c_int64, _P]),
     ("lsb_voxmap_dump", _c.c_int, [_c.POINTER(VoxMap), _P, _P, _P, _c.c_int64, _P]),
     ("lsb_voxmap_rehash", _c.c_int, [_c.POINTER(VoxMap), _c.POINTER(VoxMap), _P]),
+    ("lsb_voxmap_fit_planes", _c.c_int, [_c.POINTER(VoxMap), _P, _c.c_int64, _c.POINTER(_c.c_double), _P, _P, _P,
+                                         _P]),
+    ("lsb_lidar_rows", _c.c_int, [_c.POINTER(VoxMap), _P, _c.c_int64, _c.POINTER(_c.c_double),
+                                  _c.POINTER(_c.c_double), _c.POINTER(_c.c_double), _c.POINTER(_c.c_double),
+                                  _c.c_double, _P, _P, _P, _P]),
     ("lsb_window_mark", _c.c_int, [_P, _c.c_int64, _P, _P, _c.c_int64, _P, _c.c_int64, _P, _P, _P]),
     ("lsb_window_plan", _c.c_int, [_P, _c.c_int64, _P, _P, _P, _P]),
     ("lsb_window_compact", _c.c_int, [_c.POINTER(VoxMap), _c.POINTER(Params), _P, _P, _c.c_int64, _P, _c.c_int64,

@@ -27,7 +27,8 @@ cudaError_t launch_pose_prepare(const Ws&, const lsb_params&, const lsb_camera&,
 cudaError_t launch_pose_rows(const Ws&, const lsb_settings&, int, int, int, const float*, const int32_t*,
                              const float*, const int32_t*, int64_t, const double*, const double*, double*,
                              cudaStream_t);
-cudaError_t launch_hb(const double*, const double*, int64_t, double, double*, cudaStream_t);
+cudaError_t launch_hb(const double*, const double*, int64_t, double, double*, double*, cudaStream_t);
+int hb_scratch_doubles();
 cudaError_t launch_semidense(const float*, const float*, int, int, double, double, uint8_t*, cudaStream_t);
 cudaError_t launch_vox_keys(const double*, int64_t, double, int64_t*, cudaStream_t);
 cudaError_t launch_vox_insert(const lsb_voxmap&, const double*, int64_t, int, int64_t*, cudaStream_t);
@@ -38,6 +39,10 @@ cudaError_t launch_vox_fov(const lsb_voxmap&, const double*, int64_t, unsigned l
                            unsigned long long*, int64_t, cudaStream_t);
 cudaError_t launch_vox_dump(const lsb_voxmap&, int64_t*, int64_t*, unsigned long long*, int64_t, cudaStream_t);
 cudaError_t launch_vox_rehash(const lsb_voxmap&, const lsb_voxmap&, cudaStream_t);
+cudaError_t launch_fit_planes(const lsb_voxmap&, const int64_t*, int64_t, const double*, double*, double*, uint8_t*,
+                              cudaStream_t);
+cudaError_t launch_lidar_rows(const lsb_voxmap&, const double*, int64_t, const double*, const double*, const double*,
+                              const double*, double, double, double*, double*, uint8_t*, cudaStream_t);
 cudaError_t launch_win_mark(const int64_t*, int64_t, uint64_t*, int32_t*, int64_t, const int64_t*, int64_t, uint8_t*,
                             uint8_t*, cudaStream_t);
 cudaError_t launch_win_plan(const uint8_t*, int64_t, int32_t*, int32_t*, int64_t*, cudaStream_t);
@@ -340,9 +345,12 @@ int lsb_pose_rows(const lsb_settings* s, int sh_degree_used, void* ws, size_t ws
                                        A, R_cw, rows, (cudaStream_t)stream), "pose_rows");
 }
 
-int lsb_hb_reduce(const double* rows, const double* z, int64_t m, double inv_sigma2, double* out, void* stream) {
-    if (!out || (m > 0 && (!rows || !z))) return fail(LSB_EINVAL, "NULL argument");
-    return check_cuda(launch_hb(rows, z, m, inv_sigma2, out, (cudaStream_t)stream), "hb_reduce");
+int lsb_hb_scratch_doubles(void) { return hb_scratch_doubles(); }
+
+int lsb_hb_reduce(const double* rows, const double* z, int64_t m, double inv_sigma2, double* out, double* scratch,
+                  void* stream) {
+    if (!out || !scratch || (m > 0 && (!rows || !z))) return fail(LSB_EINVAL, "NULL argument");
+    return check_cuda(launch_hb(rows, z, m, inv_sigma2, out, scratch, (cudaStream_t)stream), "hb_reduce");
 }
 
 int lsb_semidense_mask(const float* obs, const float* tfin, int32_t W, int32_t H, double thr, double tmax,
@@ -484,6 +492,28 @@ int lsb_window_append(const lsb_params* arena, int64_t* wkeys, const int64_t* ok
     return check_cuda(launch_win_append(*arena, wkeys, okeys, gids, cnt, store, first_slot, n_added,
                                         (cudaStream_t)stream),
                       "window_append");
+}
+
+int lsb_voxmap_fit_planes(const lsb_voxmap* m, const int64_t* keys, int64_t k, const double* origin, double* normals,
+                          double* anchors, uint8_t* valid, void* stream) {
+    int rc = vox_ok(m);
+    if (rc) return rc;
+    if (!origin || k < 0 || (k && (!keys || !normals || !anchors || !valid))) return fail(LSB_EINVAL, "NULL array");
+    return check_cuda(launch_fit_planes(*m, keys, k, origin, normals, anchors, valid, (cudaStream_t)stream),
+                      "fit_planes");
+}
+
+int lsb_lidar_rows(const lsb_voxmap* m, const double* pts_l, int64_t n, const double* R_il, const double* t_il,
+                   const double* R_wi, const double* t_wi, double gate, double* rows, double* z, uint8_t* keep,
+                   void* stream) {
+    int rc = vox_ok(m);
+    if (rc) return rc;
+    if (!R_il || !t_il || !R_wi || !t_wi || n < 0 || (n && (!pts_l || !rows || !z || !keep)))
+        return fail(LSB_EINVAL, "NULL array");
+    const double leaf_len = m->root_len / (double)(1ll << m->max_level);
+    return check_cuda(launch_lidar_rows(*m, pts_l, n, R_il, t_il, R_wi, t_wi, leaf_len, gate, rows, z, keep,
+                                        (cudaStream_t)stream),
+                      "lidar_rows");
 }
 
 }  // extern "C"

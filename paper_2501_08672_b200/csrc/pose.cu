@@ -11,9 +11,10 @@
 //                    and each lane applies d(alpha) -> (d mu, d Sigma) -> L to
 //                    its entry.  The 6-vector is warp-reduced and mapped to
 //                    the IMU tangent with the adjoint A (raster.py:501-507).
-//   k_hb_reduce    : A6 = sum h h^T / sigma^2, b6 = sum h z / sigma^2 with
-//                    h = -row (estimator.py:278-280, 314-318), one CTA, fixed
-//                    order (deterministic).
+//   k_hb_partial / k_hb_final : A6 = sum h h^T / sigma^2, b6 = sum h z /
+//                    sigma^2 with h = -row (estimator.py:278-280, 314-318),
+//                    fixed-grid CTA partials then a fixed-order sum
+//                    (deterministic).
 //   k_semidense    : Sobel/8 gradient magnitude of the observed grey image
 //                    (nearest border) > threshold and coverage T < max
 //                    (estimator.py:241-252).
@@ -303,25 +304,64 @@ __global__ void __launch_bounds__(128) k_pose_rows(Ws w, RowArgs a, const float*
     }
 }
 
-__global__ void __launch_bounds__(256) k_hb_reduce(const double* __restrict__ rows, const double* __restrict__ z,
-                                                   int64_t m, double inv_s2, double* __restrict__ out) {
-    // out[0..35] = sum h h^T inv_s2 (6x6), out[36..41] = sum h z inv_s2, h = -row
-    __shared__ double s[256];
-    for (int q = 0; q < 42; ++q) {
-        double v = 0.0;
-        for (int64_t r = threadIdx.x; r < m; r += blockDim.x) {
-            const double* row = rows + 6 * r;
-            v += (q < 36) ? row[q / 6] * row[q % 6] : -row[q - 36] * z[r];
-        }
-        s[threadIdx.x] = v;
-        __syncthreads();
-        for (int o = 128; o > 0; o >>= 1) {
-            if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) out[q] = s[0] * inv_s2;
-        __syncthreads();
+// Pass 1: HB_BLOCKS fixed CTAs, each thread accumulates the 21 unique h h^T
+// entries and the 6 h z entries of its rows (fixed grid-stride partition),
+// a fixed tree reduces them per CTA.  Pass 2: one CTA adds the CTA partials
+// in CTA order.  Deterministic; every row is read once.
+constexpr int HB_BLOCKS = 296, HB_VALS = 27;
+__global__ void __launch_bounds__(256) k_hb_partial(const double* __restrict__ rows, const double* __restrict__ z,
+                                                    int64_t m, double* __restrict__ part) {
+    __shared__ double s[HB_VALS][256 / 32];
+    double v[HB_VALS];
+#pragma unroll
+    for (int q = 0; q < HB_VALS; ++q) v[q] = 0.0;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+        double h[6];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) h[c] = -rows[6 * r + c];
+        const double zr = z[r];
+        int q = 0;
+#pragma unroll
+        for (int i = 0; i < 6; ++i)
+#pragma unroll
+            for (int j = i; j < 6; ++j) v[q++] += h[i] * h[j];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) v[21 + i] += h[i] * zr;
     }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < HB_VALS; ++q) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+        if (lane == 0) s[q][warp] = v[q];
+    }
+    __syncthreads();
+    if (threadIdx.x < HB_VALS) {
+        double t = 0.0;
+        for (int w = 0; w < 256 / 32; ++w) t += s[threadIdx.x][w];
+        part[(int64_t)blockIdx.x * HB_VALS + threadIdx.x] = t;
+    }
+}
+
+__global__ void k_hb_final(const double* __restrict__ part, int nblocks, double inv_s2, double* __restrict__ out) {
+    // out[0..35] = sum h h^T inv_s2 (6x6), out[36..41] = sum h z inv_s2
+    if (threadIdx.x >= HB_VALS) return;
+    double t = 0.0;
+    for (int b = 0; b < nblocks; ++b) t += part[(int64_t)b * HB_VALS + threadIdx.x];
+    t *= inv_s2;
+    const int q = threadIdx.x;
+    if (q >= 21) {
+        out[36 + q - 21] = t;
+        return;
+    }
+    int i = 0, k = q;
+    while (k >= 6 - i) {
+        k -= 6 - i;
+        ++i;
+    }
+    const int j = i + k;
+    out[6 * i + j] = t;
+    out[6 * j + i] = t;
 }
 
 __global__ void __launch_bounds__(256) k_semidense(const float* __restrict__ obs, const float* __restrict__ tfin,
@@ -367,10 +407,14 @@ cudaError_t launch_pose_rows(const Ws& w, const lsb_settings& s, int degree, int
     return cudaGetLastError();
 }
 
-cudaError_t launch_hb(const double* rows, const double* z, int64_t m, double inv_s2, double* out, cudaStream_t st) {
-    k_hb_reduce<<<1, 256, 0, st>>>(rows, z, m, inv_s2, out);
+cudaError_t launch_hb(const double* rows, const double* z, int64_t m, double inv_s2, double* out, double* part,
+                      cudaStream_t st) {
+    k_hb_partial<<<HB_BLOCKS, 256, 0, st>>>(rows, z, m, part);
+    k_hb_final<<<1, 32, 0, st>>>(part, HB_BLOCKS, inv_s2, out);
     return cudaGetLastError();
 }
+
+int hb_scratch_doubles() { return HB_BLOCKS * HB_VALS; }
 
 cudaError_t launch_semidense(const float* obs, const float* tfin, int W, int H, double thr, double tmax,
                              uint8_t* out, cudaStream_t st) {

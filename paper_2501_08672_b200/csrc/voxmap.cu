@@ -270,4 +270,188 @@ cudaError_t launch_vox_dump(const lsb_voxmap& m, int64_t* keys, int64_t* slots, 
     return cudaGetLastError();
 }
 
+// ---- plane fits and the LiDAR point-to-plane measurement (§8(f) rank 2) ----
+// fit_planes / estimate_normal (voxmap.py:255-335): the leaf's and its 6 face
+// neighbours' statistics summed in the reference's order, scatter = outer/n -
+// mean mean^T, the smallest-eigenvalue eigenvector (f64 cyclic Jacobi: the
+// symmetric 3x3 problem numpy hands to LAPACK's dsyevd), flipped to face the
+// sensor; rejected with fewer than 3 points or rank < 2
+// (w1 <= 1e-12 + 1e-6 max(w2, 0)).  The anchor is the leaf's own centroid.
+
+__device__ void eig3_jacobi(double A[3][3], double w[3], double V[3][3]) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) V[i][j] = i == j ? 1.0 : 0.0;
+    for (int sweep = 0; sweep < 32; ++sweep) {
+        const double off = A[0][1] * A[0][1] + A[0][2] * A[0][2] + A[1][2] * A[1][2];
+        const double dia = A[0][0] * A[0][0] + A[1][1] * A[1][1] + A[2][2] * A[2][2];
+        if (off <= 1e-34 * dia || off == 0.0) break;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            const int p = r == 2 ? 1 : 0, q = r == 0 ? 1 : 2;
+            const double apq = A[p][q];
+            if (apq == 0.0) continue;
+            const double theta = (A[q][q] - A[p][p]) / (2.0 * apq);
+            const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+            const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {           // A <- J^T A J
+                const double akp = A[k][p], akq = A[k][q];
+                A[k][p] = c * akp - s * akq;
+                A[k][q] = s * akp + c * akq;
+            }
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const double apk = A[p][k], aqk = A[q][k];
+                A[p][k] = c * apk - s * aqk;
+                A[q][k] = s * apk + c * aqk;
+            }
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {           // V <- V J
+                const double vkp = V[k][p], vkq = V[k][q];
+                V[k][p] = c * vkp - s * vkq;
+                V[k][q] = s * vkp + c * vkq;
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) w[i] = A[i][i];
+}
+
+__device__ bool plane_fit(const lsb_voxmap& m, long long ix, long long iy, long long iz, const double* origin,
+                          double* normal, double* anchor) {
+    const long long self = find(m, ix, iy, iz);
+    if (self < 0 || m.count[self] == 0) return false;
+    const long long nb[7][3] = {{0, 0, 0}, {1, 0, 0}, {-1, 0, 0}, {0, 1, 0}, {0, -1, 0}, {0, 0, 1}, {0, 0, -1}};
+    unsigned long long n_tot = 0;
+    double s[3] = {0.0, 0.0, 0.0}, so[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int k = 0; k < 7; ++k) {
+        const long long t = find(m, ix + nb[k][0], iy + nb[k][1], iz + nb[k][2]);
+        if (t < 0 || m.count[t] == 0) continue;          // leaf_stats holds leaves that saw points
+        n_tot += m.count[t];
+        for (int c = 0; c < 3; ++c) s[c] = s[c] + m.sum[3 * t + c];
+        for (int c = 0; c < 6; ++c) so[c] = so[c] + m.outer[6 * t + c];
+    }
+    if (n_tot < 3) return false;
+    const double n = (double)n_tot;
+    const double mean[3] = {s[0] / n, s[1] / n, s[2] / n};
+    double A[3][3];
+    const int ij[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+    for (int c = 0; c < 6; ++c) {
+        const int i = ij[c][0], j = ij[c][1];
+        A[i][j] = A[j][i] = so[c] / n - mean[i] * mean[j];
+    }
+    double w[3], V[3][3];
+    eig3_jacobi(A, w, V);
+    int o[3] = {0, 1, 2};                     // ascending eigenvalues (eigh's order)
+    if (w[o[1]] < w[o[0]]) { const int x = o[0]; o[0] = o[1]; o[1] = x; }
+    if (w[o[2]] < w[o[1]]) { const int x = o[1]; o[1] = o[2]; o[2] = x; }
+    if (w[o[1]] < w[o[0]]) { const int x = o[0]; o[0] = o[1]; o[1] = x; }
+    const int i0 = o[0], i1 = o[1], i2 = o[2];
+    if (!(w[i1] > 1e-12 + 1e-6 * fmax(w[i2], 0.0))) return false;
+    double nv[3] = {V[0][i0], V[1][i0], V[2][i0]};
+    const double dot = nv[0] * (origin[0] - mean[0]) + nv[1] * (origin[1] - mean[1]) + nv[2] * (origin[2] - mean[2]);
+    if (dot < 0.0)
+        for (int c = 0; c < 3; ++c) nv[c] = -nv[c];
+    const double cnt = (double)m.count[self];
+    for (int c = 0; c < 3; ++c) {
+        normal[c] = nv[c];
+        anchor[c] = m.sum[3 * self + c] / cnt;
+    }
+    return true;
+}
+
+__global__ void k_fit_planes(lsb_voxmap m, const int64_t* __restrict__ keys, int64_t k, double ox, double oy,
+                             double oz, double* normals, double* anchors, uint8_t* valid) {
+    const double origin[3] = {ox, oy, oz};
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        double nv[3], an[3];
+        const long long ix = keys[3 * i], iy = keys[3 * i + 1], iz = keys[3 * i + 2];
+        const bool ok = in_range(ix) && in_range(iy) && in_range(iz) && plane_fit(m, ix, iy, iz, origin, nv, an);
+        valid[i] = ok ? 1 : 0;
+        for (int c = 0; c < 3; ++c) {
+            normals[3 * i + c] = ok ? nv[c] : __longlong_as_double(0x7ff8000000000000ll);
+            anchors[3 * i + c] = ok ? an[c] : __longlong_as_double(0x7ff8000000000000ll);
+        }
+    }
+}
+
+struct LidarArgs {
+    double R_il[9], t_il[3], R_wi[9], t_wi[3], origin[3];
+    double leaf_len, gate;
+};
+
+// x @ R^T + t as numpy/OpenBLAS evaluates it (k = 3 FMA chain, then + t).
+__device__ __forceinline__ void apply_rt(const double* R, const double* t, const double* x, double* y) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+        y[r] = __dadd_rn(__fma_rn(R[3 * r + 2], x[2], __fma_rn(R[3 * r + 1], x[1], __dmul_rn(R[3 * r], x[0]))), t[r]);
+}
+
+// lidar_measurement (estimator.py:190-238), one thread per scan point:
+// rows = -H[:, :6] (the convention of Measurement.rows_dev / lsb_hb_reduce),
+// z = n . (p_w - anchor), keep = plane found && |z| <= gate.
+__global__ void k_lidar_rows(lsb_voxmap m, const double* __restrict__ pts, int64_t n, LidarArgs a, double* rows,
+                             double* z, uint8_t* keep) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double pi[3], pw[3];
+        apply_rt(a.R_il, a.t_il, pts + 3 * i, pi);
+        apply_rt(a.R_wi, a.t_wi, pi, pw);
+        const long long ix = (long long)floor(__ddiv_rn(pw[0], a.leaf_len));
+        const long long iy = (long long)floor(__ddiv_rn(pw[1], a.leaf_len));
+        const long long iz = (long long)floor(__ddiv_rn(pw[2], a.leaf_len));
+        double nv[3], an[3];
+        bool ok = in_range(ix) && in_range(iy) && in_range(iz) && plane_fit(m, ix, iy, iz, a.origin, nv, an);
+        double r = 0.0;
+        if (ok) {
+            r = nv[0] * (pw[0] - an[0]) + nv[1] * (pw[1] - an[1]) + nv[2] * (pw[2] - an[2]);
+            ok = fabs(r) <= a.gate;
+        }
+        keep[i] = ok ? 1 : 0;
+        z[i] = r;
+        double h[6] = {0, 0, 0, 0, 0, 0};
+        if (ok) {
+            double nR[3];      // n^T R_wi
+            for (int c = 0; c < 3; ++c) nR[c] = nv[0] * a.R_wi[c] + nv[1] * a.R_wi[3 + c] + nv[2] * a.R_wi[6 + c];
+            h[0] = -(nR[1] * pi[2] - nR[2] * pi[1]);
+            h[1] = -(nR[2] * pi[0] - nR[0] * pi[2]);
+            h[2] = -(nR[0] * pi[1] - nR[1] * pi[0]);
+            h[3] = nv[0];
+            h[4] = nv[1];
+            h[5] = nv[2];
+        }
+        for (int c = 0; c < 6; ++c) rows[6 * i + c] = -h[c];
+    }
+}
+
+cudaError_t launch_fit_planes(const lsb_voxmap& m, const int64_t* keys, int64_t k, const double* origin,
+                              double* normals, double* anchors, uint8_t* valid, cudaStream_t st) {
+    if (k) k_fit_planes<<<grid_for(k), 256, 0, st>>>(m, keys, k, origin[0], origin[1], origin[2], normals, anchors, valid);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lidar_rows(const lsb_voxmap& m, const double* pts, int64_t n, const double* R_il,
+                              const double* t_il, const double* R_wi, const double* t_wi, double leaf_len,
+                              double gate, double* rows, double* z, uint8_t* keep, cudaStream_t st) {
+    LidarArgs a;
+    for (int c = 0; c < 9; ++c) {
+        a.R_il[c] = R_il[c];
+        a.R_wi[c] = R_wi[c];
+    }
+    for (int c = 0; c < 3; ++c) {
+        a.t_il[c] = t_il[c];
+        a.t_wi[c] = t_wi[c];
+    }
+    // T_WL = T_WI T_IL: its translation R_wi t_il + t_wi (SE3 compose, numpy
+    // matmul order) is the sensor origin of the normal flip
+    for (int r = 0; r < 3; ++r)
+        a.origin[r] = (R_wi[3 * r] * t_il[0] + R_wi[3 * r + 1] * t_il[1] + R_wi[3 * r + 2] * t_il[2]) + t_wi[r];
+    a.leaf_len = leaf_len;
+    a.gate = gate;
+    if (n) k_lidar_rows<<<grid_for(n), 256, 0, st>>>(m, pts, n, a, rows, z, keep);
+    return cudaGetLastError();
+}
+
 }  // namespace lsb
+

@@ -19,8 +19,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import TooFewPixels
-from .errors import SingularGain
+from .errors import NoAssociations, SingularGain, TooFewPixels
 from .geometry import SE3, so3_exp, so3_left_jacobian, so3_log, so3_right_jacobian_inv
 from .raster import RasterSettings, _f32, pose_rows, render
 
@@ -29,8 +28,10 @@ DIM = 15
 
 @dataclass
 class FilterConfig:
-    """The visual fields of estimator.FilterConfig (estimator.py:95-115)."""
+    """The measurement fields of estimator.FilterConfig (estimator.py:95-115)."""
 
+    lidar_sigma: float = 0.02
+    lidar_gate: float = 1.0
     photo_sigma: float = 0.1
     pixel_budget: int = 1024
     grad_threshold: float = 0.05
@@ -65,26 +66,54 @@ class NavState:
                                self.bias_accel - other.bias_accel])
 
 
-@dataclass
 class Measurement:
     """Stacked residuals with pose Jacobian rows padded to the full state
-    (estimator.py:84-92); numpy on the host, as the filter consumes it."""
+    (estimator.py:84-92).  The device measurements keep rows_dev (= -H[:, :6])
+    and z_dev on the GPU; the numpy z / H / R_diag the reference exposes are
+    materialised on first access, so an IESKF step that only needs hb() never
+    copies the rows to the host."""
 
-    z: np.ndarray
-    H: np.ndarray
-    R_diag: np.ndarray
-    rows_dev: torch.Tensor = field(default=None, repr=False)
-    z_dev: torch.Tensor = field(default=None, repr=False)
+    def __init__(self, z=None, H=None, R_diag=None, rows_dev: torch.Tensor = None, z_dev: torch.Tensor = None,
+                 sigma2: float = None):
+        self._z = None if z is None else np.asarray(z, dtype=float).reshape(-1)
+        self._H = None if H is None else np.asarray(H, dtype=float).reshape(-1, DIM)
+        self._R = None if R_diag is None else np.asarray(R_diag, dtype=float).reshape(-1)
+        self.rows_dev, self.z_dev, self.sigma2 = rows_dev, z_dev, sigma2
+
+    def __len__(self) -> int:
+        return int(self.z_dev.numel()) if self.z_dev is not None else len(self._z)
+
+    @property
+    def z(self) -> np.ndarray:
+        if self._z is None:
+            self._z = self.z_dev.cpu().numpy()
+        return self._z
+
+    @property
+    def H(self) -> np.ndarray:
+        if self._H is None:
+            H = np.zeros((len(self), DIM))
+            H[:, :6] = -self.rows_dev.cpu().numpy()
+            self._H = H
+        return self._H
+
+    @property
+    def R_diag(self) -> np.ndarray:
+        if self._R is None:
+            self._R = np.full(len(self), float(self.sigma2))
+        return self._R
 
     def hb(self) -> tuple[np.ndarray, np.ndarray]:
         """(6x6 sum h h^T / sigma^2, 6 sum h z / sigma^2) for the pose block,
         reduced on the device (estimator.py:314-318 with H = -rows)."""
         m = int(self.z_dev.numel())
+        inv = 1.0 / (self.sigma2 if self.sigma2 is not None else float(self.R_diag[0])) if m else 1.0
+        lib = _lib.load()
         out = torch.empty(42, dtype=torch.float64, device=self.z_dev.device)
-        _lib.check(_lib.load().lsb_hb_reduce(ctypes.c_void_p(self.rows_dev.data_ptr()),
-                                             ctypes.c_void_p(self.z_dev.data_ptr()), m,
-                                             float(1.0 / self.R_diag[0]) if m else 1.0,
-                                             ctypes.c_void_p(out.data_ptr()), _lib.stream_ptr()), "hb_reduce")
+        scratch = torch.empty(lib.lsb_hb_scratch_doubles(), dtype=torch.float64, device=self.z_dev.device)
+        _lib.check(lib.lsb_hb_reduce(ctypes.c_void_p(self.rows_dev.data_ptr()), ctypes.c_void_p(self.z_dev.data_ptr()),
+                                     m, float(inv), ctypes.c_void_p(out.data_ptr()),
+                                     ctypes.c_void_p(scratch.data_ptr()), _lib.stream_ptr()), "hb_reduce")
         o = out.cpu().numpy()
         return o[:36].reshape(6, 6), o[36:]
 
@@ -131,11 +160,38 @@ def visual_measurement(state, observed, window, cam, T_ic, cfg: FilterConfig,
     idt = idt[ok]
     res = res[ok].contiguous()
     rows = pose_rows(out, idt, T_ic=T_ic, as_numpy=False)
-    rows_h = rows.cpu().numpy()
-    H = np.zeros((n_ok, DIM))
-    H[:, :6] = -rows_h
-    return Measurement(z=res.cpu().numpy(), H=H, R_diag=np.full(n_ok, cfg.photo_sigma ** 2), rows_dev=rows,
-                       z_dev=res)
+    return Measurement(rows_dev=rows, z_dev=res, sigma2=cfg.photo_sigma ** 2)
+
+
+def lidar_measurement(state: NavState, points_l, vmap, T_il, cfg: FilterConfig,
+                      plane_cache: dict = None) -> Measurement:
+    """Point-to-plane residuals against the map's local planes
+    (estimator.py:190-238).  Every scan point is transformed, keyed, fitted
+    (its leaf and 6 face neighbours, csrc/voxmap.cu) and gated on the device;
+    rows keep the scan order.  plane_cache is accepted for the reference's
+    signature; the device refits per call (the map does not change between
+    the iterations of one update, so the fits are identical)."""
+    _lib.require()
+    dev = vmap.device
+    pts = torch.as_tensor(np.atleast_2d(np.asarray(points_l, dtype=np.float64))) if not torch.is_tensor(points_l) \
+        else points_l
+    pts = pts.to(device=dev, dtype=torch.float64).reshape(-1, 3).contiguous()
+    n = pts.shape[0]
+    rows = torch.empty((max(n, 1), 6), dtype=torch.float64, device=dev)
+    z = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    keep = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+    c = lambda a, k: (ctypes.c_double * k)(*np.asarray(a, dtype=np.float64).ravel().tolist())
+    m = vmap.struct()
+    _lib.check(_lib.load().lsb_lidar_rows(ctypes.byref(m), ctypes.c_void_p(pts.data_ptr()), n, c(T_il.R, 9),
+                                          c(T_il.t, 3), c(state.T_WI.R, 9), c(state.T_WI.t, 3),
+                                          float(cfg.lidar_gate), ctypes.c_void_p(rows.data_ptr()),
+                                          ctypes.c_void_p(z.data_ptr()), ctypes.c_void_p(keep.data_ptr()),
+                                          _lib.stream_ptr()), "lidar_rows")
+    k = keep[:n].bool()
+    m_ok = int(k.sum().item())
+    if m_ok == 0:
+        raise NoAssociations("no scan point matched a plane (or all residuals gated out)")
+    return Measurement(rows_dev=rows[:n][k].contiguous(), z_dev=z[:n][k].contiguous(), sigma2=cfg.lidar_sigma ** 2)
 
 
 def ieskf_visual_update(state: NavState, cov: np.ndarray, observed, window, cam, T_ic, cfg: FilterConfig,

@@ -244,6 +244,48 @@ class HashOctree:
         k = min(int(n_out.item()), out_cap)
         return keys[:k], slots[:k]
 
+    # ---- plane fits (voxmap.py:255-335) ------------------------------------------
+    def fit_planes_dev(self, keys, sensor_origin):
+        """Batched plane fits of leaf keys (k,3): (normals (k,3), centroids
+        (k,3), valid (k,) bool) on the device; NaN rows where no plane."""
+        k = torch.as_tensor(np.asarray(keys, dtype=np.int64)) if not torch.is_tensor(keys) else keys
+        k = k.to(device=self.device, dtype=torch.int64).reshape(-1, 3).contiguous()
+        n = k.shape[0]
+        normals = torch.empty((n, 3), dtype=torch.float64, device=self.device)
+        anchors = torch.empty((n, 3), dtype=torch.float64, device=self.device)
+        valid = torch.empty(n, dtype=torch.uint8, device=self.device)
+        o = (ctypes.c_double * 3)(*np.asarray(sensor_origin, dtype=np.float64).reshape(3).tolist())
+        m = self.struct()
+        _lib.check(_lib.load().lsb_voxmap_fit_planes(ctypes.byref(m), ctypes.c_void_p(k.data_ptr()), n, o,
+                                                     ctypes.c_void_p(normals.data_ptr()),
+                                                     ctypes.c_void_p(anchors.data_ptr()),
+                                                     ctypes.c_void_p(valid.data_ptr()), _lib.stream_ptr()),
+                   "fit_planes")
+        return normals, anchors, valid.bool()
+
+    def fit_planes(self, keys: list, sensor_origin) -> dict:
+        """{key: (normal, centroid) or None}, like voxmap.py:297-335."""
+        keys = list(keys)
+        if not keys:
+            return {}
+        nrm, anc, ok = (t.cpu().numpy() for t in self.fit_planes_dev([[k[0], k[1], k[2]] for k in keys],
+                                                                      sensor_origin))
+        return {k: ((nrm[i], anc[i]) if ok[i] else None) for i, k in enumerate(keys)}
+
+    def plane_at(self, key: VoxelKey, sensor_origin):
+        """(normal, centroid) or None (voxmap.py:286-295)."""
+        return self.fit_planes([key], sensor_origin)[key]
+
+    def estimate_normal(self, key: VoxelKey, sensor_origin) -> np.ndarray:
+        """Plane normal facing the sensor (voxmap.py:267-284); raises
+        Degenerate when there is no plane.  (Evaluated like plane_at, so an
+        empty leaf with populated neighbours is Degenerate here.)"""
+        from .errors import Degenerate
+        p = self.plane_at(key, sensor_origin)
+        if p is None:
+            raise Degenerate("no plane: fewer than 3 points, scatter rank < 2 or an empty leaf")
+        return p[0]
+
     # ---- device Gaussian store (the map side of the sliding window) ------------
     def _store_reserve(self, rows: int, width: int) -> None:
         st = getattr(self, "store", None)
