@@ -56,6 +56,9 @@ constexpr int RUN = 4;       // pixels per lane and row (horizontal run)
 #ifndef BWD_MIN_BLOCKS
 #define BWD_MIN_BLOCKS 4
 #endif
+#ifndef STATIC_FIRST_TILE
+#define STATIC_FIRST_TILE 1
+#endif
 #ifndef BWD_LOSS_VARIANT
 #define BWD_LOSS_VARIANT 0
 #endif
@@ -310,10 +313,21 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
     // persistent tile-warp: pull tiles from the queue (heaviest first) until
     // it is empty.  (Claiming the next slot early, to hide the atomic, costs
     // more in lost load balance than it saves: measured +25% on config 2.)
+#if STATIC_FIRST_TILE
+    // first tile: the warp's own slot of the (heaviest-first) order, no
+    // atomic; later tiles from the queue, which starts after the first wave
+    int q0 = blockIdx.x * WPB + wib;
+    const int nwarps = gridDim.x * WPB;
+#endif
     for (;;) {
         int tile = 0;
         if (lane == 0) {
+#if STATIC_FIRST_TILE
+            const int q = q0 >= 0 ? q0 : (int)atomicAdd(&w.ctr[7], 1ull) + nwarps;
+            q0 = -1;
+#else
             const int q = (int)atomicAdd(&w.ctr[7], 1ull);
+#endif
             tile = q < w.ntiles ? w.tile_order[q] : -1;
         }
         tile = __shfl_sync(0xffffffffu, tile, 0);
@@ -509,10 +523,21 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __r
     const float kap = a.clamp;
     RecPipe pipe;
     pipe.buf = s_rec[wib];
+#if STATIC_FIRST_TILE
+    // first tile: the warp's own slot of the (heaviest-first) order, no
+    // atomic; later tiles from the queue, which starts after the first wave
+    int q0 = blockIdx.x * WPB + wib;
+    const int nwarps = gridDim.x * WPB;
+#endif
     for (;;) {
         int tile = 0;
         if (lane == 0) {
+#if STATIC_FIRST_TILE
+            const int q = q0 >= 0 ? q0 : (int)atomicAdd(&w.ctr[8], 1ull) + nwarps;
+            q0 = -1;
+#else
             const int q = (int)atomicAdd(&w.ctr[8], 1ull);
+#endif
             tile = q < w.ntiles ? w.tile_order[q] : -1;
         }
         tile = __shfl_sync(0xffffffffu, tile, 0);
