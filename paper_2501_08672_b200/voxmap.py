@@ -49,6 +49,18 @@ class VoxelKey(NamedTuple):
         return VoxelKey(self.ix // s, self.iy // s, self.iz // s, 0)
 
 
+def _iter_order(k: np.ndarray, L: int) -> np.ndarray:
+    """Permutation of leaf keys (k,3) into iter_leaves order (voxmap.py:
+    339-353): sorted root tuple, then octant DFS (x | y << 1 | z << 2 per level)."""
+    roots = k >> L
+    morton = np.zeros(len(k), dtype=np.int64)
+    for d in range(L):             # level d+1 digit: bit (L-1-d) of each local coordinate
+        b = L - 1 - d
+        digit = ((k[:, 0] >> b) & 1) | (((k[:, 1] >> b) & 1) << 1) | (((k[:, 2] >> b) & 1) << 2)
+        morton = morton * 8 + digit
+    return np.lexsort((morton, roots[:, 2], roots[:, 1], roots[:, 0]))
+
+
 def gaussian_row(g, width: Optional[int] = None) -> np.ndarray:
     """A Gaussian3D-like object as one f32 arena row (window.py:58-71):
     mean 3 | rot 9 | scale 3 | opacity 1 | sh 3K (K from `width` if given)."""
@@ -330,6 +342,84 @@ class HashOctree:
         out[ok] = self.store[g[ok].long()]
         return out
 
+    # ---- persistence (voxmap.py:358-415) ---------------------------------------
+    _MAGIC = b"LSMAP001"
+
+    def _records(self):
+        """(keys (r,3) int64, rows (r, 16+3K) f32) of the leaves holding a
+        Gaussian, in the reference's iteration order (voxmap.py:339-353);
+        one device gather, one copy to the host."""
+        keys, slots = self.dump_dev()
+        g = self.gslot[slots] if slots.numel() else torch.empty(0, dtype=torch.int32, device=self.device)
+        has = g >= 0
+        keys, g = keys[has], g[has]
+        st = getattr(self, "store", None)
+        if keys.shape[0] == 0 or st is None:
+            return np.zeros((0, 3), np.int64), np.zeros((0, 19), np.float32)
+        rows = st[g.long()].cpu().numpy()
+        k = keys.cpu().numpy()
+        order = _iter_order(k, self.max_level)
+        return k[order], rows[order]
+
+    def gaussian_count(self) -> int:
+        return int(self._records()[0].shape[0])
+
+    def save(self, path) -> None:
+        """Binary snapshot, byte-identical to the reference's (voxmap.py:
+        362-375): magic, <IdII Q header, per record <qqqI key + level and the
+        f32 row (mean 3 | rot 9 | scale 3 | opacity 1 | sh 3K)."""
+        import struct
+        keys, rows = self._records()
+        sh_k = (rows.shape[1] - 16) // 3 if len(keys) else 1
+        rec = np.zeros(len(keys), dtype=np.dtype([("k", "<i8", (3,)), ("lv", "<u4"), ("f", "<f4", (16 + 3 * sh_k,))],
+                                                  align=False))
+        rec["k"] = keys
+        rec["lv"] = self.max_level
+        if len(keys):
+            rec["f"] = rows
+        with open(path, "wb") as f:
+            f.write(self._MAGIC)
+            f.write(struct.pack("<IdII Q", 1, self.root_len, self.max_level, sh_k, len(keys)))
+            f.write(rec.tobytes())
+
+    @classmethod
+    def load(cls, path, device=None) -> "HashOctree":
+        """Inverse of save (voxmap.py:377-399); the Gaussians go to the
+        device store of a new map."""
+        import struct
+        with open(path, "rb") as f:
+            if f.read(8) != cls._MAGIC:
+                raise ValueError("not a map snapshot")
+            hdr = struct.calcsize("<IdII Q")
+            version, root_len, max_level, sh_k, n = struct.unpack("<IdII Q", f.read(hdr))
+            if version != 1:
+                raise ValueError(f"unsupported snapshot version {version}")
+            rec = np.frombuffer(f.read(), dtype=np.dtype([("k", "<i8", (3,)), ("lv", "<u4"),
+                                                          ("f", "<f4", (16 + 3 * sh_k,))]), count=n)
+        m = cls(root_len, max_level, capacity=max(1 << 10, 2 * n), device=device)
+        if n:
+            if np.any(rec["lv"] != max_level):
+                raise ValueError("the device map holds leaf-level Gaussians only")
+            m.set_gaussians_dev(rec["k"].astype(np.int64), rec["f"].astype(np.float32))
+        return m
+
+    def export_ply(self, path) -> None:
+        """ASCII PLY of the means and view-independent colours, text-identical
+        to the reference's (voxmap.py:401-415)."""
+        _, rows = self._records()
+        c0 = 0.28209479177387814                      # sh.SH_C0
+        rgb = np.clip(0.5 + c0 * rows[:, 16:19].astype(np.float64), 0.0, 1.0)
+        q = np.round(rgb * 255).astype(int)
+        mean = rows[:, 0:3].astype(np.float64)
+        with open(path, "w") as f:
+            f.write("ply\nformat ascii 1.0\n")
+            f.write(f"element vertex {len(rows)}\n")
+            f.write("property float x\nproperty float y\nproperty float z\n")
+            f.write("property uchar red\nproperty uchar green\nproperty uchar blue\n")
+            f.write("end_header\n")
+            f.writelines(f"{a:.6f} {b:.6f} {c:.6f} {r} {g} {bl}\n"
+                         for (a, b, c), (r, g, bl) in zip(mean.tolist(), q.tolist()))
+
     # ---- reference-shaped helpers ------------------------------------------------
     def _keys_of_slots(self, slots: torch.Tensor) -> np.ndarray:
         slots = slots[slots >= 0]
@@ -408,11 +498,4 @@ class HashOctree:
         if len(k) == 0:
             return []
         L = self.max_level
-        roots = k >> L
-        morton = np.zeros(len(k), dtype=np.int64)
-        for d in range(L):             # level d+1 digit: bit (L-1-d) of each local coordinate
-            b = L - 1 - d
-            digit = ((k[:, 0] >> b) & 1) | (((k[:, 1] >> b) & 1) << 1) | (((k[:, 2] >> b) & 1) << 2)
-            morton = morton * 8 + digit
-        order = np.lexsort((morton, roots[:, 2], roots[:, 1], roots[:, 0]))
-        return [VoxelKey(int(a), int(b), int(c), L) for a, b, c in k[order]]
+        return [VoxelKey(int(a), int(b), int(c), L) for a, b, c in k[_iter_order(k, L)]]
