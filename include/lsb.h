@@ -318,6 +318,25 @@ int lsb_lidar_rows(const lsb_voxmap* m, const double* pts_l, int64_t n, const do
                    const double* R_wi, const double* t_wi, double gate, double* rows, double* z, uint8_t* keep,
                    void* stream);
 
+/* Batched Gaussian initialisation: replaces the per-leaf loop of
+ * pipeline._insert_new_gaussians + initialize.init_gaussian
+ * (pipeline.py:99-137, initialize.py:22-124).  keys (k,3) the scan's leaf
+ * groups in sorted order, centroids (k,3) f64 their scan centroids, image
+ * (H,W,3) f32, T_CW row-major, cam4 = fx fy cx cy, origin = the sensor
+ * position.  rows (k, 16+3K) f32 (the arena row layout) and status[i] = 1
+ * where a Gaussian was made (leaf empty, observable, in the image
+ * interior); the caller stores those rows in the map. */
+int lsb_init_gaussians(const lsb_voxmap* m, const int64_t* keys, const double* centroids, int64_t k,
+                       const float* image, int32_t width, int32_t height, const double* R_cw, const double* t_cw,
+                       const double* cam4, const double* origin, double near, double kappa, double delta,
+                       double opacity, int32_t sh_coeffs, float* rows, uint8_t* status, void* stream);
+
+/* Group means (group_by_leaf + points.mean(axis=0), voxmap.py:213-230,
+ * pipeline.py:113): group g is points perm[starts[g] .. starts[g]+counts[g])
+ * in that order; out (k,3) f64 = their sum, row by row, / count. */
+int lsb_segment_mean(const double* pts, const int64_t* perm, const int64_t* starts, const int64_t* counts, int64_t k,
+                     double* out, void* stream);
+
 /* ---- sliding window: replaces GaussianWindow.maintain (window.py:136-276)
  * The live window is the f32 SoA arena `arena` (capacity rows, n live); the
  * global map's Gaussians are rows of `store` (mean 3 | rot 9 | scale 3 |

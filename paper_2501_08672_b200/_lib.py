@@ -114,6 +114,11 @@ SIGNATURES = [
     ("lsb_lidar_rows", _c.c_int, [_c.POINTER(VoxMap), _P, _c.c_int64, _c.POINTER(_c.c_double),
                                   _c.POINTER(_c.c_double), _c.POINTER(_c.c_double), _c.POINTER(_c.c_double),
                                   _c.c_double, _P, _P, _P, _P]),
+    ("lsb_init_gaussians", _c.c_int, [_c.POINTER(VoxMap), _P, _P, _c.c_int64, _P, _c.c_int32, _c.c_int32,
+                                      _c.POINTER(_c.c_double), _c.POINTER(_c.c_double), _c.POINTER(_c.c_double),
+                                      _c.POINTER(_c.c_double), _c.c_double, _c.c_double, _c.c_double, _c.c_double,
+                                      _c.c_int32, _P, _P, _P]),
+    ("lsb_segment_mean", _c.c_int, [_P, _P, _P, _P, _c.c_int64, _P, _P]),
     ("lsb_window_mark", _c.c_int, [_P, _c.c_int64, _P, _P, _c.c_int64, _P, _c.c_int64, _P, _P, _P]),
     ("lsb_window_plan", _c.c_int, [_P, _c.c_int64, _P, _P, _P, _P]),
     ("lsb_window_compact", _c.c_int, [_c.POINTER(VoxMap), _c.POINTER(Params), _P, _P, _c.c_int64, _P, _c.c_int64,

@@ -43,6 +43,11 @@ cudaError_t launch_fit_planes(const lsb_voxmap&, const int64_t*, int64_t, const 
                               cudaStream_t);
 cudaError_t launch_lidar_rows(const lsb_voxmap&, const double*, int64_t, const double*, const double*, const double*,
                               const double*, double, double, double*, double*, uint8_t*, cudaStream_t);
+cudaError_t launch_init_gaussians(const lsb_voxmap&, const int64_t*, const double*, int64_t, const float*, int, int,
+                                  const double*, const double*, const double*, const double*, double, double, double,
+                                  double, int, float*, uint8_t*, cudaStream_t);
+cudaError_t launch_segment_mean(const double*, const int64_t*, const int64_t*, const int64_t*, int64_t, double*,
+                                cudaStream_t);
 cudaError_t launch_win_mark(const int64_t*, int64_t, uint64_t*, int32_t*, int64_t, const int64_t*, int64_t, uint8_t*,
                             uint8_t*, cudaStream_t);
 cudaError_t launch_win_plan(const uint8_t*, int64_t, int32_t*, int32_t*, int64_t*, cudaStream_t);
@@ -514,6 +519,26 @@ int lsb_lidar_rows(const lsb_voxmap* m, const double* pts_l, int64_t n, const do
     return check_cuda(launch_lidar_rows(*m, pts_l, n, R_il, t_il, R_wi, t_wi, leaf_len, gate, rows, z, keep,
                                         (cudaStream_t)stream),
                       "lidar_rows");
+}
+
+int lsb_init_gaussians(const lsb_voxmap* m, const int64_t* keys, const double* centroids, int64_t k,
+                       const float* image, int32_t width, int32_t height, const double* R_cw, const double* t_cw,
+                       const double* cam4, const double* origin, double near, double kappa, double delta,
+                       double opacity, int32_t sh_coeffs, float* rows, uint8_t* status, void* stream) {
+    int rc = vox_ok(m);
+    if (rc) return rc;
+    if (!R_cw || !t_cw || !cam4 || !origin || k < 0 || (k && (!keys || !centroids || !image || !rows || !status)))
+        return fail(LSB_EINVAL, "NULL array");
+    if (width < 4 || height < 4 || sh_coeffs < 1 || sh_coeffs > 16) return fail(LSB_EINVAL, "bad image / sh size");
+    return check_cuda(launch_init_gaussians(*m, keys, centroids, k, image, width, height, R_cw, t_cw, cam4, origin, near,
+                                            kappa, delta, opacity, sh_coeffs, rows, status, (cudaStream_t)stream),
+                      "init_gaussians");
+}
+
+int lsb_segment_mean(const double* pts, const int64_t* perm, const int64_t* starts, const int64_t* counts, int64_t k,
+                     double* out, void* stream) {
+    if (k < 0 || (k && (!pts || !perm || !starts || !counts || !out))) return fail(LSB_EINVAL, "NULL array");
+    return check_cuda(launch_segment_mean(pts, perm, starts, counts, k, out, (cudaStream_t)stream), "segment_mean");
 }
 
 }  // extern "C"

@@ -453,5 +453,144 @@ cudaError_t launch_lidar_rows(const lsb_voxmap& m, const double* pts, int64_t n,
     return cudaGetLastError();
 }
 
+// ---- batched Gaussian initialisation (§8(f) rank 3) ------------------------
+// pipeline.py:99-137 + initialize.py:22-124, one thread per new leaf group
+// (sorted keys, the scan's centroid of the leaf): skip leaves that already
+// hold a Gaussian; observability pre-check (z > near, 1 <= u <= W-2,
+// 1 <= v <= H-2); plane normal (plane_fit), else the unit view direction;
+// bilinear colour (area weights, pixel centres at integers) -> the degree-0
+// SH coefficient (c - 0.5) / SH_C0; slab frame (n, u, n x u) with
+// u = e_x x n / |e_x x n| (e_y if |e_x x n| < 1e-6); scale (delta, s, s),
+// s = kappa * root_len / 2^max_level.  status[i] = 1 if a row was made.
+
+struct InitArgs {
+    double R_cw[9], t_cw[3], origin[3];
+    double fx, fy, cx, cy;
+    int W, H, K;
+    double near, kappa, delta, opacity, root_len;
+};
+
+__device__ __forceinline__ double norm3(double x, double y, double z) {
+    return sqrt(__fma_rn(z, z, __fma_rn(y, y, x * x)));      // numpy's length-3 norm
+}
+
+__global__ void k_init_gaussians(lsb_voxmap m, const int64_t* __restrict__ keys, const double* __restrict__ cent,
+                                 int64_t k, const float* __restrict__ image, InitArgs a, float* rows,
+                                 uint8_t* status) {
+    const int R = 16 + 3 * a.K;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        status[i] = 0;
+        const long long ix = keys[3 * i], iy = keys[3 * i + 1], iz = keys[3 * i + 2];
+        if (!in_range(ix) || !in_range(iy) || !in_range(iz)) continue;
+        const long long t = find(m, ix, iy, iz);
+        if (t < 0 || m.gslot[t] >= 0) continue;                    // missing leaf or already full
+        const double c[3] = {cent[3 * i], cent[3 * i + 1], cent[3 * i + 2]};
+        double pc[3];
+        for (int r = 0; r < 3; ++r)
+            pc[r] = __dadd_rn(__fma_rn(a.R_cw[3 * r + 2], c[2], __fma_rn(a.R_cw[3 * r + 1], c[1], __dmul_rn(a.R_cw[3 * r], c[0]))),
+                              a.t_cw[r]);
+        if (!(pc[2] > a.near)) continue;
+        const double u = __dadd_rn(__ddiv_rn(__dmul_rn(a.fx, pc[0]), pc[2]), a.cx);
+        const double v = __dadd_rn(__ddiv_rn(__dmul_rn(a.fy, pc[1]), pc[2]), a.cy);
+        if (!(1.0 <= u && u <= (double)(a.W - 2) && 1.0 <= v && v <= (double)(a.H - 2))) continue;
+        double n[3], anc[3];
+        if (!plane_fit(m, ix, iy, iz, a.origin, n, anc)) {
+            const double vx = a.origin[0] - c[0], vy = a.origin[1] - c[1], vz = a.origin[2] - c[2];
+            const double nv = norm3(vx, vy, vz);
+            if (nv == 0.0) continue;
+            n[0] = vx / nv;
+            n[1] = vy / nv;
+            n[2] = vz / nv;
+        }
+        // bilinear colour (initialize.py:64-93)
+        const int x0 = (int)floor(u), y0 = (int)floor(v);
+        const double fxw = u - x0, fyw = v - y0;
+        const double wgt[4] = {(1.0 - fxw) * (1.0 - fyw), fxw * (1.0 - fyw), (1.0 - fxw) * fyw, fxw * fyw};
+        const int px[4] = {x0, x0 + 1, x0, x0 + 1}, py[4] = {y0, y0, y0 + 1, y0 + 1};
+        double col[3] = {0.0, 0.0, 0.0};
+        for (int q = 0; q < 4; ++q)
+            for (int ch = 0; ch < 3; ++ch)
+                col[ch] = __dadd_rn(col[ch], __dmul_rn(wgt[q], (double)image[3 * ((int64_t)py[q] * a.W + px[q]) + ch]));
+        // slab frame (initialize.py:30-61)
+        double ux = 0.0 * n[2] - 0.0 * n[1], uy = 0.0 * n[0] - 1.0 * n[2], uz = 1.0 * n[1] - 0.0 * n[0];
+        double nu = norm3(ux, uy, uz);
+        if (nu < 1e-6) {
+            ux = 1.0 * n[2] - 0.0 * n[1];
+            uy = 0.0 * n[0] - 0.0 * n[2];
+            uz = 0.0 * n[1] - 1.0 * n[0];
+            nu = norm3(ux, uy, uz);
+            if (nu < 1e-6) continue;                                // Degenerate
+        }
+        ux /= nu;
+        uy /= nu;
+        uz /= nu;
+        const double wx = n[1] * uz - n[2] * uy, wy = n[2] * ux - n[0] * uz, wz = n[0] * uy - n[1] * ux;   // n x u
+        float* o = rows + i * R;
+        for (int ch = 0; ch < 3; ++ch) o[ch] = (float)c[ch];
+        const double rot[9] = {n[0], ux, wx, n[1], uy, wy, n[2], uz, wz};
+        for (int q = 0; q < 9; ++q) o[3 + q] = (float)rot[q];
+        const double s = a.kappa * (a.root_len / (double)(1ll << m.max_level));
+        o[12] = (float)a.delta;
+        o[13] = (float)s;
+        o[14] = (float)s;
+        o[15] = (float)a.opacity;
+        for (int q = 0; q < 3 * a.K; ++q) o[16 + q] = 0.f;
+        for (int ch = 0; ch < 3; ++ch) o[16 + ch] = (float)((col[ch] - 0.5) / 0.28209479177387814);
+        status[i] = 1;
+    }
+}
+
+cudaError_t launch_init_gaussians(const lsb_voxmap& m, const int64_t* keys, const double* cent, int64_t k,
+                                  const float* image, int W, int H, const double* R_cw, const double* t_cw,
+                                  const double* cam4, const double* origin, double near, double kappa, double delta,
+                                  double opacity, int K, float* rows, uint8_t* status, cudaStream_t st) {
+    InitArgs a;
+    for (int q = 0; q < 9; ++q) a.R_cw[q] = R_cw[q];
+    for (int q = 0; q < 3; ++q) {
+        a.t_cw[q] = t_cw[q];
+        a.origin[q] = origin[q];
+    }
+    a.fx = cam4[0];
+    a.fy = cam4[1];
+    a.cx = cam4[2];
+    a.cy = cam4[3];
+    a.W = W;
+    a.H = H;
+    a.K = K;
+    a.near = near;
+    a.kappa = kappa;
+    a.delta = delta;
+    a.opacity = opacity;
+    a.root_len = m.root_len;
+    if (k) k_init_gaussians<<<grid_for(k), 128, 0, st>>>(m, keys, cent, k, image, a, rows, status);
+    return cudaGetLastError();
+}
+
+// Per group g (points perm[start_g .. start_g + count_g) in scan order): the
+// mean as numpy's axis-0 mean evaluates it (row-by-row sums, then / count).
+__global__ void k_segment_mean(const double* __restrict__ pts, const int64_t* __restrict__ perm,
+                               const int64_t* __restrict__ starts, const int64_t* __restrict__ counts, int64_t k,
+                               double* out) {
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < k; g += (int64_t)gridDim.x * blockDim.x) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+        const int64_t b = starts[g], n = counts[g];
+        for (int64_t j = 0; j < n; ++j) {
+            const int64_t p = perm[b + j];
+            s0 = __dadd_rn(s0, pts[3 * p]);
+            s1 = __dadd_rn(s1, pts[3 * p + 1]);
+            s2 = __dadd_rn(s2, pts[3 * p + 2]);
+        }
+        out[3 * g] = s0 / (double)n;
+        out[3 * g + 1] = s1 / (double)n;
+        out[3 * g + 2] = s2 / (double)n;
+    }
+}
+
+cudaError_t launch_segment_mean(const double* pts, const int64_t* perm, const int64_t* starts, const int64_t* counts,
+                                int64_t k, double* out, cudaStream_t st) {
+    if (k) k_segment_mean<<<grid_for(k), 128, 0, st>>>(pts, perm, starts, counts, k, out);
+    return cudaGetLastError();
+}
+
 }  // namespace lsb
 
