@@ -218,6 +218,23 @@ def run_ours(args, wl, rank, world, local_rank):
         render_bin(eng.state, stream)
         counts.append(eng.state.read_counts(stream)[:2])
     allreduce = (lambda t: dist.all_reduce(t)) if world > 1 else None
+    exchange = "nccl"
+    if world > 1 and args.exchange == "p2p":
+        # fused gradient exchange + Adam over NVLink peer memory (dist.PeerExchange);
+        # every rank falls back to NCCL if any rank cannot set it up
+        ok = 1
+        try:
+            from paper_2501_08672_b200.dist import PeerExchange
+            eng.exchange = PeerExchange(eng)
+        except Exception as exc:          # noqa: BLE001
+            ok = 0
+            print(f"[bench] rank {rank}: peer exchange unavailable ({exc}); NCCL all-reduce", file=sys.stderr)
+        t = torch.tensor([ok], device=dev, dtype=torch.int32)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if int(t.item()):
+            exchange = "p2p"
+        else:
+            eng.exchange = None
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
@@ -357,7 +374,8 @@ def run_ours(args, wl, rank, world, local_rank):
             "visible_splats_per_s": float(sum(c[0] for c in counts)) * world / (ms * 1e-3),
             "config": {"workload": args.config, "gaussians": N, "views": V, "width": W, "height": H,
                        "alpha_cut": wl["alpha_cut"], "parallelism": f"view-sharded dp{world}",
-                       "view_lanes": args.lanes, "cuda_graph": graph_headline, "cuda_graph_e2e": use_graph,
+                       "view_lanes": args.lanes, "exchange": exchange if world > 1 else None,
+                       "cuda_graph": graph_headline, "cuda_graph_e2e": use_graph,
                        "serial_ms_per_step": eager_ms,
                        "kernel_timing": "separate one-lane eager pass of the same steps, events around each kernel",
                        "l2": "working set > L2: observed views alone are V x 15.7 MB",
@@ -690,6 +708,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--lanes", type=int, default=5, help="concurrent view pipelines per GPU")
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="eager launches instead of a CUDA graph")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="N>1 gradient exchange: NCCL all-reduce + Adam, or the fused peer-memory step")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -220,6 +220,18 @@ int lsb_adam_step(const lsb_params* p, const float* grads, void* m, void* v, uin
 int lsb_adam_step_dev(const lsb_params* p, const float* grads, void* m, void* v, uint8_t* touched,
                       const lsb_adam_cfg* cfg, const double* ibc_table, int64_t table_len, int64_t* step_dev,
                       void* stream);
+/* Fused multi-GPU optimiser step over NVLink peer memory (replaces the
+ * NCCL all-reduce + Adam pair of the view-sharded step).  replicas[q] /
+ * grads[q] / touched[q] are rank q's parameter arena, flat f32 gradient
+ * buffer and touched flags as seen from this process (peer pointers, e.g.
+ * from torch symmetric memory); n_ranks <= 8.  For the Gaussians [lo, hi)
+ * this rank owns: gradients summed over ranks in rank order, Adam with this
+ * rank's moments m / v, new parameters (and touched flags) stored into
+ * EVERY replica.  The caller brackets the call with a cross-rank barrier.
+ * ibc_table / step_dev as in lsb_adam_step_dev (both or neither). */
+int lsb_adam_peer_step(const lsb_params* replicas, int32_t n_ranks, int32_t rank, const float* const* grads,
+                       int64_t lo, int64_t hi, void* m, void* v, uint8_t* const* touched, const lsb_adam_cfg* cfg,
+                       const double* ibc_table, int64_t table_len, int64_t* step_dev, void* stream);
 /* Stage host bytes (pinned) into device memory on `stream` (observed
  * keyframe images each step; capturable into a CUDA graph). */
 int lsb_copy_h2d(void* dst, const void* src, size_t bytes, void* stream);

@@ -15,7 +15,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
           "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 # per-file extra flags: the preprocess keeps f64 rounding where numpy rounds
-EXTRA = {"preprocess.cu": ["--fmad=false"]}
+EXTRA = {"preprocess.cu": ["--fmad=false"], "adam.cu": ["--fmad=false"]}
 SOURCES = ["preprocess.cu", "blend.cu", "chain.cu", "loss.cu", "adam.cu", "pose.cu", "voxmap.cu", "window.cu",
            "api.cu"]
 

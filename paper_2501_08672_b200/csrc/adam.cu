@@ -2,6 +2,8 @@
 // per Gaussian, and the Gram-Schmidt re-orthonormalisation of touched
 // rotations (optimize.py:91-100, 193-194).  HBM-bound: params are updated in
 // place in the parameter arena's own type (f64 working copy or f32 arena).
+// Compiled with --fmad=false: every operation rounds where numpy's does, and
+// the single-GPU and fused peer kernels give the same bits.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -38,77 +40,159 @@ __device__ __forceinline__ PT adam_upd(const AdamArgs<PT>& a, PT ibc1, PT ibc2, 
     return -lr * (m * ibc1) / (sqrt(v * ibc2) + (PT)a.c.eps);
 }
 
-// One thread per Gaussian.  PT = double steps the f64 working copy exactly
-// like the reference (optimize.py:142-188); PT = float steps the f32 arena.
+// Gradient sources: this rank's buffer, or the sum over every rank's buffer
+// (peer pointers, added in rank order) for the fused peer step.
+struct GradLocal {
+    const float* g;
+    __device__ __forceinline__ float operator()(int64_t idx) const { return g[idx]; }
+};
+constexpr int MAX_PEERS = 8;
+struct GradPeers {
+    const float* g[MAX_PEERS];
+    int G;
+    __device__ __forceinline__ float operator()(int64_t idx) const {
+        float s = g[0][idx];
+        for (int q = 1; q < G; ++q) s += g[q][idx];
+        return s;
+    }
+};
+
+// Parameter targets: read from this rank's arrays; write to them, or to
+// every replica (peer pointers) so all ranks hold the same bits.
 template <typename PT>
-__global__ void __launch_bounds__(256) k_adam(AdamArgs<PT> a) {
+struct ParamLocal {
+    PT *means, *rots, *scales, *opac, *shs;
+    uint8_t* touched;
+    __device__ __forceinline__ PT get(const PT* base, int64_t idx) const { return base[idx]; }
+    __device__ __forceinline__ void put(int f, int64_t idx, PT v) const { field(f)[idx] = v; }
+    __device__ __forceinline__ void touch(int64_t i) const { touched[i] = 1; }
+    __device__ __forceinline__ PT* field(int f) const {
+        return f == 0 ? means : (f == 1 ? rots : (f == 2 ? scales : (f == 3 ? opac : shs)));
+    }
+};
+template <typename PT>
+struct ParamPeers {
+    PT *means, *rots, *scales, *opac, *shs;             // this rank's replica (read)
+    PT* dst[MAX_PEERS][5];                               // every replica's arrays (write)
+    uint8_t* touched[MAX_PEERS];
+    int G;
+    __device__ __forceinline__ PT* field(int f) const {
+        return f == 0 ? means : (f == 1 ? rots : (f == 2 ? scales : (f == 3 ? opac : shs)));
+    }
+    __device__ __forceinline__ void put(int f, int64_t idx, PT v) const {
+        for (int q = 0; q < G; ++q) dst[q][f][idx] = v;
+    }
+    __device__ __forceinline__ void touch(int64_t i) const {
+        for (int q = 0; q < G; ++q) touched[q][i] = 1;
+    }
+};
+
+// One Gaussian of the storage-coordinate step (optimize.py:159-188).
+template <typename PT, typename GS, typename PS>
+__device__ __forceinline__ void adam_gaussian(const AdamArgs<PT>& a, const GS& gs, const PS& ps, int64_t i, PT ibc1,
+                                              PT ibc2) {
     const int64_t n = a.n;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t o_rot = 3 * n, o_scale = 6 * n, o_op = 9 * n, o_sh = 10 * n;
     const PT lr_mean = (PT)(a.c.lr_mean * a.c.scene_scale), lr_rot = (PT)a.c.lr_rot;
     const PT lr_scale = (PT)a.c.lr_scale, lr_op = (PT)a.c.lr_opacity, lr_sh = (PT)a.c.lr_sh;
     const PT floor_s = (PT)a.c.scale_floor, oclip = (PT)a.c.opacity_clip;
-    PT ibc1 = a.ibc1, ibc2 = a.ibc2;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const PT cur = ps.field(0)[3 * i + k];
+        ps.put(0, 3 * i + k, cur + adam_upd(a, ibc1, ibc2, 3 * i + k, (PT)gs(3 * i + k), lr_mean));
+    }
+    // rotation: R <- R Exp(phi) on rows with phi != 0 (optimize.py:172-176)
+    PT phi[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) phi[k] = adam_upd(a, ibc1, ibc2, o_rot + 3 * i + k, (PT)gs(o_rot + 3 * i + k), lr_rot);
+    if (phi[0] != (PT)0 || phi[1] != (PT)0 || phi[2] != (PT)0) {
+        const double p0 = phi[0], p1 = phi[1], p2 = phi[2];
+        const double th = sqrt(p0 * p0 + p1 * p1 + p2 * p2);
+        const bool small = th < 1e-8;
+        const double ca = small ? 1.0 : sin(th) / th;
+        const double cb = small ? 0.5 : (1.0 - cos(th)) / (th * th);
+        const double S[9] = {0.0, -p2, p1, p2, 0.0, -p0, -p1, p0, 0.0};
+        double E[9];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const double s2 = S[3 * r] * S[c] + S[3 * r + 1] * S[3 + c] + S[3 * r + 2] * S[6 + c];
+                E[3 * r + c] = (r == c ? 1.0 : 0.0) + ca * S[3 * r + c] + cb * s2;
+            }
+        const PT* R = ps.field(1) + 9 * i;
+        double Rd[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) Rd[k] = R[k];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                ps.put(1, 9 * i + 3 * r + c, (PT)(Rd[3 * r] * E[c] + Rd[3 * r + 1] * E[3 + c] + Rd[3 * r + 2] * E[6 + c]));
+        ps.touch(i);
+    }
+    // scale in log space; gradient chained by the current scale (optimize.py:178-181)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const PT s = ps.field(2)[3 * i + k];
+        const PT st = adam_upd(a, ibc1, ibc2, o_scale + 3 * i + k, (PT)gs(o_scale + 3 * i + k) * s, lr_scale);
+        if (st != (PT)0) ps.put(2, 3 * i + k, fmax(exp(log(fmax(s, floor_s)) + st), floor_s));
+    }
+    // opacity in logit space (optimize.py:183-186)
+    {
+        const PT op = ps.field(3)[i];
+        const PT oc = fmin(fmax(op, oclip), (PT)1 - oclip);
+        const PT st = adam_upd(a, ibc1, ibc2, o_op + i, (PT)gs(o_op + i) * oc * ((PT)1 - oc), lr_op);
+        if (st != (PT)0) ps.put(3, i, (PT)1 / ((PT)1 + exp(-(log(oc / ((PT)1 - oc)) + st))));
+    }
+    // SH coefficients
+    const int64_t nk = 3 * (int64_t)a.K;
+    for (int64_t k = 0; k < nk; ++k) {
+        const int64_t idx = nk * i + k;
+        const PT cur = ps.field(4)[idx];
+        ps.put(4, idx, cur + adam_upd(a, ibc1, ibc2, o_sh + idx, (PT)gs(o_sh + idx), lr_sh));
+    }
+}
+
+template <typename PT>
+__device__ __forceinline__ void bias_corr(const AdamArgs<PT>& a, PT& ibc1, PT& ibc2) {
+    ibc1 = a.ibc1;
+    ibc2 = a.ibc2;
     if (a.ibc_tab) {
         int64_t t = *a.step_dev;
         t = t < a.ibc_len ? t : a.ibc_len - 1;
         ibc1 = (PT)a.ibc_tab[2 * t];
         ibc2 = (PT)a.ibc_tab[2 * t + 1];
     }
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) a.means[3 * i + k] += adam_upd(a, ibc1, ibc2, 3 * i + k, (PT)a.g[3 * i + k], lr_mean);
-        // rotation: R <- R Exp(phi) on rows with phi != 0 (optimize.py:172-176)
-        PT phi[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) phi[k] = adam_upd(a, ibc1, ibc2, o_rot + 3 * i + k, (PT)a.g[o_rot + 3 * i + k], lr_rot);
-        if (phi[0] != (PT)0 || phi[1] != (PT)0 || phi[2] != (PT)0) {
-            const double p0 = phi[0], p1 = phi[1], p2 = phi[2];
-            const double th = sqrt(p0 * p0 + p1 * p1 + p2 * p2);
-            const bool small = th < 1e-8;
-            const double ca = small ? 1.0 : sin(th) / th;
-            const double cb = small ? 0.5 : (1.0 - cos(th)) / (th * th);
-            const double S[9] = {0.0, -p2, p1, p2, 0.0, -p0, -p1, p0, 0.0};
-            double E[9];
-#pragma unroll
-            for (int r = 0; r < 3; ++r)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const double s2 = S[3 * r] * S[c] + S[3 * r + 1] * S[3 + c] + S[3 * r + 2] * S[6 + c];
-                    E[3 * r + c] = (r == c ? 1.0 : 0.0) + ca * S[3 * r + c] + cb * s2;
-                }
-            PT* R = a.rots + 9 * i;
-            double Rd[9];
-#pragma unroll
-            for (int k = 0; k < 9; ++k) Rd[k] = R[k];
-#pragma unroll
-            for (int r = 0; r < 3; ++r)
-#pragma unroll
-                for (int c = 0; c < 3; ++c)
-                    R[3 * r + c] = (PT)(Rd[3 * r] * E[c] + Rd[3 * r + 1] * E[3 + c] + Rd[3 * r + 2] * E[6 + c]);
-            a.touched[i] = 1;
-        }
-        // scale in log space; gradient chained by the current scale (optimize.py:178-181)
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const PT s = a.scales[3 * i + k];
-            const PT st = adam_upd(a, ibc1, ibc2, o_scale + 3 * i + k, (PT)a.g[o_scale + 3 * i + k] * s, lr_scale);
-            if (st != (PT)0) a.scales[3 * i + k] = fmax(exp(log(fmax(s, floor_s)) + st), floor_s);
-        }
-        // opacity in logit space (optimize.py:183-186)
-        {
-            const PT op = a.opac[i];
-            const PT oc = fmin(fmax(op, oclip), (PT)1 - oclip);
-            const PT st = adam_upd(a, ibc1, ibc2, o_op + i, (PT)a.g[o_op + i] * oc * ((PT)1 - oc), lr_op);
-            if (st != (PT)0) a.opac[i] = (PT)1 / ((PT)1 + exp(-(log(oc / ((PT)1 - oc)) + st)));
-        }
-        // SH coefficients
-        const int64_t nk = 3 * (int64_t)a.K;
-        for (int64_t k = 0; k < nk; ++k) {
-            const int64_t idx = nk * i + k;
-            a.shs[idx] += adam_upd(a, ibc1, ibc2, o_sh + idx, (PT)a.g[o_sh + idx], lr_sh);
-        }
-    }
+}
+
+// One thread per Gaussian.  PT = double steps the f64 working copy exactly
+// like the reference (optimize.py:142-188); PT = float steps the f32 arena.
+template <typename PT>
+__global__ void __launch_bounds__(256) k_adam(AdamArgs<PT> a) {
+    PT ibc1, ibc2;
+    bias_corr(a, ibc1, ibc2);
+    const GradLocal gs{a.g};
+    const ParamLocal<PT> ps{a.means, a.rots, a.scales, a.opac, a.shs, a.touched};
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x)
+        adam_gaussian(a, gs, ps, i, ibc1, ibc2);
+}
+
+// Fused multi-GPU step over NVLink peer memory (one kernel per rank): for the
+// Gaussians [lo, hi) this rank owns, sum the G ranks' gradient buffers (peer
+// loads, rank order — the all-reduce), apply Adam with this rank's moments,
+// and store the new parameters into every rank's replica (peer stores — the
+// all-gather).  Every replica receives the same bits.  The caller brackets
+// it with a cross-rank barrier (gradients complete before; stores landed
+// after).
+template <typename PT>
+__global__ void __launch_bounds__(256) k_adam_peer(AdamArgs<PT> a, GradPeers gs, ParamPeers<PT> ps, int64_t lo,
+                                                   int64_t hi) {
+    PT ibc1, ibc2;
+    bias_corr(a, ibc1, ibc2);
+    for (int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x)
+        adam_gaussian(a, gs, ps, i, ibc1, ibc2);
+    __threadfence_system();
 }
 
 template <typename PT>
@@ -162,6 +246,48 @@ cudaError_t launch_adam(const lsb_params& p, const float* g, void* m, void* v, u
     if (p.n == 0 && !step_dev) return cudaSuccess;
     return p.dtype ? adam_t<double>(p, g, m, v, touched, c, tab, tab_len, step_dev, st)
                    : adam_t<float>(p, g, m, v, touched, c, tab, tab_len, step_dev, st);
+}
+
+template <typename PT>
+static cudaError_t adam_peer_t(const lsb_params* reps, int G, int rank, const float* const* grads, int64_t lo,
+                               int64_t hi, void* m, void* v, uint8_t* const* touched, const lsb_adam_cfg& c,
+                               const double* tab, int64_t tab_len, int64_t* step_dev, cudaStream_t st) {
+    const lsb_params& p = reps[rank];
+    AdamArgs<PT> a{(PT*)p.means, (PT*)p.rots, (PT*)p.scales, (PT*)p.opacities, (PT*)p.shs, p.n, p.sh_coeffs,
+                   nullptr, (PT*)m, (PT*)v, touched[rank], c, (PT)0, (PT)0, tab, tab_len, step_dev};
+    if (!tab) {
+        a.ibc1 = (PT)(1.0 / (1.0 - pow(c.beta1, (double)c.step)));
+        a.ibc2 = (PT)(1.0 / (1.0 - pow(c.beta2, (double)c.step)));
+    }
+    GradPeers gs{};
+    ParamPeers<PT> ps{};
+    gs.G = ps.G = G;
+    ps.means = (PT*)p.means;
+    ps.rots = (PT*)p.rots;
+    ps.scales = (PT*)p.scales;
+    ps.opac = (PT*)p.opacities;
+    ps.shs = (PT*)p.shs;
+    for (int q = 0; q < G; ++q) {
+        gs.g[q] = grads[q];
+        ps.dst[q][0] = (PT*)reps[q].means;
+        ps.dst[q][1] = (PT*)reps[q].rots;
+        ps.dst[q][2] = (PT*)reps[q].scales;
+        ps.dst[q][3] = (PT*)reps[q].opacities;
+        ps.dst[q][4] = (PT*)reps[q].shs;
+        ps.touched[q] = touched[q];
+    }
+    if (hi > lo) k_adam_peer<PT><<<grid_of(hi - lo), 256, 0, st>>>(a, gs, ps, lo, hi);
+    if (step_dev) k_step_bump<<<1, 1, 0, st>>>(step_dev);
+    return cudaGetLastError();
+}
+
+int adam_max_peers() { return MAX_PEERS; }
+
+cudaError_t launch_adam_peer(const lsb_params* reps, int G, int rank, const float* const* grads, int64_t lo,
+                             int64_t hi, void* m, void* v, uint8_t* const* touched, const lsb_adam_cfg& c,
+                             const double* tab, int64_t tab_len, int64_t* step_dev, cudaStream_t st) {
+    return reps[rank].dtype ? adam_peer_t<double>(reps, G, rank, grads, lo, hi, m, v, touched, c, tab, tab_len, step_dev, st)
+                            : adam_peer_t<float>(reps, G, rank, grads, lo, hi, m, v, touched, c, tab, tab_len, step_dev, st);
 }
 
 cudaError_t launch_orthonormalize(void* rots, int dtype, const uint8_t* touched, int64_t n, cudaStream_t st) {

@@ -22,6 +22,9 @@ int loss_scratch_doubles();
 cudaError_t launch_adam(const lsb_params&, const float*, void*, void*, uint8_t*, const lsb_adam_cfg&, const double*,
                         int64_t, int64_t*, cudaStream_t);
 cudaError_t launch_orthonormalize(void*, int, const uint8_t*, int64_t, cudaStream_t);
+cudaError_t launch_adam_peer(const lsb_params*, int, int, const float* const*, int64_t, int64_t, void*, void*,
+                             uint8_t* const*, const lsb_adam_cfg&, const double*, int64_t, int64_t*, cudaStream_t);
+int adam_max_peers();
 cudaError_t launch_pose_prepare(const Ws&, const lsb_params&, const lsb_camera&, const lsb_pose&,
                                 const lsb_settings&, float*, cudaStream_t);
 cudaError_t launch_pose_rows(const Ws&, const lsb_settings&, int, int, int, const float*, const int32_t*,
@@ -539,6 +542,25 @@ int lsb_segment_mean(const double* pts, const int64_t* perm, const int64_t* star
                      double* out, void* stream) {
     if (k < 0 || (k && (!pts || !perm || !starts || !counts || !out))) return fail(LSB_EINVAL, "NULL array");
     return check_cuda(launch_segment_mean(pts, perm, starts, counts, k, out, (cudaStream_t)stream), "segment_mean");
+}
+
+int lsb_adam_peer_step(const lsb_params* replicas, int32_t n_ranks, int32_t rank, const float* const* grads,
+                       int64_t lo, int64_t hi, void* m, void* v, uint8_t* const* touched, const lsb_adam_cfg* cfg,
+                       const double* ibc_table, int64_t table_len, int64_t* step_dev, void* stream) {
+    if (!replicas || !grads || !touched || !cfg || !m || !v) return fail(LSB_EINVAL, "NULL argument");
+    if (n_ranks < 1 || n_ranks > adam_max_peers() || rank < 0 || rank >= n_ranks)
+        return fail(LSB_EINVAL, "rank / n_ranks out of range (at most 8 ranks)");
+    const lsb_params& p = replicas[rank];
+    if (lo < 0 || hi < lo || hi > p.n) return fail(LSB_EINVAL, "bad shard");
+    for (int q = 0; q < n_ranks; ++q) {
+        if (!grads[q] || !touched[q] || replicas[q].n != p.n || replicas[q].dtype != p.dtype ||
+            replicas[q].sh_coeffs != p.sh_coeffs)
+            return fail(LSB_EINVAL, "replicas / gradient buffers disagree");
+    }
+    if ((ibc_table != nullptr) != (step_dev != nullptr)) return fail(LSB_EINVAL, "ibc_table and step_dev go together");
+    return check_cuda(launch_adam_peer(replicas, n_ranks, rank, grads, lo, hi, m, v, touched, *cfg, ibc_table,
+                                       table_len, step_dev, (cudaStream_t)stream),
+                      "adam_peer");
 }
 
 }  // extern "C"

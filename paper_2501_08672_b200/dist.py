@@ -73,3 +73,112 @@ class ViewShardedWindow:
 
     def finish(self) -> None:
         self.engine.finish()
+
+
+# ---- fused optimiser step over NVLink peer memory ---------------------------------
+
+def shard_range(n: int, world: int, rank: int) -> tuple:
+    """Gaussians [lo, hi) whose optimiser step `rank` owns (contiguous shards)."""
+    per = (n + world - 1) // world
+    lo = min(n, rank * per)
+    return lo, min(n, lo + per)
+
+
+def adam_peer_step(replicas: Sequence, grads: Sequence[torch.Tensor], touched: Sequence[torch.Tensor], rank: int,
+                   lo: int, hi: int, adam, stream=None) -> None:
+    """lsb_adam_peer_step: sum the ranks' gradient buffers (rank order) for
+    the Gaussians [lo, hi), step them with `adam`'s moments (device step
+    counter, like AdamState.apply_dev) and store the new parameters into
+    every replica.  replicas / grads / touched are per-rank views (peer
+    memory in a multi-process run; plain device tensors to simulate ranks on
+    one GPU)."""
+    import ctypes
+
+    from . import _lib
+    from .optimize import adam_cfg, bias_correction_table
+
+    G = len(replicas)
+    if adam.step_dev is None:
+        adam.ibc = torch.from_numpy(bias_correction_table(adam.cfg.beta1, adam.cfg.beta2)).to(adam.m.device)
+        adam.step_dev = torch.full((1,), adam.step, dtype=torch.int64, device=adam.m.device)
+    adam.step += 1
+    c = adam_cfg(adam.cfg, adam.step)
+    P = (_lib.Params * G)(*[r.params() for r in replicas])
+    gp = (ctypes.c_void_p * G)(*[g.data_ptr() for g in grads])
+    tp = (ctypes.c_void_p * G)(*[t.data_ptr() for t in touched])
+    _lib.check(_lib.load().lsb_adam_peer_step(
+        P, G, int(rank), gp, int(lo), int(hi), ctypes.c_void_p(adam.m.data_ptr()), ctypes.c_void_p(adam.v.data_ptr()),
+        tp, ctypes.byref(c), ctypes.c_void_p(adam.ibc.data_ptr()), int(adam.ibc.shape[0]),
+        ctypes.c_void_p(adam.step_dev.data_ptr()), _lib.stream_ptr(stream)), "adam_peer")
+    del np
+
+
+class PeerExchange:
+    """The view-sharded step's gradient exchange + optimiser as ONE kernel
+    over NVLink peer memory (instead of an NCCL all-reduce followed by Adam on
+    every rank): the window parameters, the flat gradient buffer and the
+    touched flags live in torch symmetric memory, so every rank can load its
+    peers' gradients and store into their parameter replicas.  Per step:
+    device barrier (all ranks' gradients complete) -> lsb_adam_peer_step on
+    this rank's shard of Gaussians (reduce-scatter + Adam + all-gather fused)
+    -> device barrier (all stores landed).  Replicas stay bit-identical.
+    Traffic per rank: (G-1)/G of the gradient rows in, (G-1)/G of the
+    parameter rows out; Adam runs on n/G Gaussians instead of n."""
+
+    def __init__(self, engine, group=None):
+        import torch.distributed._symmetric_memory as symm
+
+        from .raster import ParamGradients
+
+        self.group = group if group is not None else dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        if self.world > 8:
+            raise ValueError("the peer step addresses at most 8 ranks")
+        self.engine = engine
+        self._handles = []
+        if hasattr(symm, "enable_symm_mem_for_group"):
+            try:
+                symm.enable_symm_mem_for_group(self.group.group_name)
+            except Exception:       # noqa: BLE001 - already enabled / not needed on this version
+                pass
+
+        def sym(t):
+            s = symm.empty(t.shape, dtype=t.dtype, device=t.device)
+            s.copy_(t)
+            h = symm.rendezvous(s, self.group)
+            self._handles.append(h)
+            peers = [h.get_buffer(q, tuple(t.shape), t.dtype) for q in range(self.world)]
+            return s, h, peers
+
+        arr = engine.arrays
+        peer_fields = {}
+        for f in ("means", "rots", "scales", "opacities", "shs"):
+            s, _, peers = sym(getattr(arr, f))
+            setattr(arr, f, s)
+            peer_fields[f] = peers
+        flat, self._gh, gpeers = sym(engine.grads.flat)
+        engine.grads = ParamGradients.from_flat(flat, len(arr), int(arr.shs.shape[1]))
+        tflags, _, tpeers = sym(engine.adam.touched)
+        engine.adam.touched = tflags
+        from types import SimpleNamespace
+        self.replicas = [SimpleNamespace(params=(lambda q=q: _peer_params(arr, peer_fields, q))) for q in
+                         range(self.world)]
+        self.grads = gpeers
+        self.touched = tpeers
+        self.lo, self.hi = shard_range(len(arr), self.world, self.rank)
+
+    def step(self, stream=None) -> None:
+        s = stream if stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            self._gh.barrier(channel=0)
+            adam_peer_step(self.replicas, self.grads, self.touched, self.rank, self.lo, self.hi, self.engine.adam, s)
+            self._gh.barrier(channel=1)
+
+
+def _peer_params(arr, peer_fields, q):
+    from . import _lib
+    f = peer_fields
+    return _lib.Params(f["means"][q].data_ptr(), f["rots"][q].data_ptr(), f["scales"][q].data_ptr(),
+                       f["opacities"][q].data_ptr(), f["shs"][q].data_ptr(), len(arr), int(arr.shs.shape[1]),
+                       1 if arr.dtype == torch.float64 else 0)

@@ -206,6 +206,7 @@ class WindowEngine:
         _lib.require()
         self.bin_mode = (1 if settings.alpha_cut > 0.0 else 0) if bin_mode is None else int(bin_mode)
         self.loss_in_backward = True        # photometric loss fused into the backward (else the forward)
+        self.exchange = None                # dist.PeerExchange: multi-GPU step over NVLink peer memory
         self.arena = arrays
         if master == "f64" and arrays.dtype != torch.float64:
             arrays = arrays.clone(torch.float64)
@@ -370,9 +371,14 @@ class WindowEngine:
             done.record(self.copy_stream)
             main.wait_event(done)
         with torch.cuda.stream(main):
-            if allreduce is not None:
-                allreduce(self.grads.flat)
-            mark("adam", main); self.adam.apply_dev(self.arrays, self.grads, main); mark("adam", main)
+            mark("adam", main)
+            if self.exchange is not None:       # fused peer-memory exchange + Adam (dist.PeerExchange)
+                self.exchange.step(main)
+            else:
+                if allreduce is not None:
+                    allreduce(self.grads.flat)
+                self.adam.apply_dev(self.arrays, self.grads, main)
+            mark("adam", main)
 
     def capture(self, observed: Sequence[torch.Tensor], allreduce=None) -> None:
         """Capture one step() as a CUDA graph; replay() then runs a whole step

@@ -83,8 +83,10 @@ class GaussianArrays:
         return self.means.dtype
 
     def clone(self, dtype=None) -> "GaussianArrays":
-        return GaussianArrays(self.means, self.rots, self.scales, self.opacities, self.shs, self.device,
-                              dtype or self.dtype)
+        """A copy (new storage), optionally cast."""
+        dt = dtype or self.dtype
+        return GaussianArrays(*(t.to(dt).clone() for t in (self.means, self.rots, self.scales, self.opacities,
+                                                           self.shs)), device=self.device, dtype=dt)
 
     def copy_from(self, other: "GaussianArrays") -> None:
         """In-place copy (with cast) of another arena's values."""
@@ -132,7 +134,11 @@ class ParamGradients:
 
     @staticmethod
     def zeros(n: int, k: int, device) -> "ParamGradients":
-        flat = torch.zeros(n * (10 + 3 * k), dtype=torch.float32, device=device)
+        return ParamGradients.from_flat(torch.zeros(n * (10 + 3 * k), dtype=torch.float32, device=device), n, k)
+
+    @staticmethod
+    def from_flat(flat: torch.Tensor, n: int, k: int) -> "ParamGradients":
+        """Group views of an existing flat buffer (n * (10 + 3k) f32)."""
         o = 0
         views = []
         for size, shape in ((3 * n, (n, 3)), (3 * n, (n, 3)), (3 * n, (n, 3)), (n, (n,)), (3 * k * n, (n, k, 3))):
