@@ -110,7 +110,6 @@ def adam_peer_step(replicas: Sequence, grads: Sequence[torch.Tensor], touched: S
         P, G, int(rank), gp, int(lo), int(hi), ctypes.c_void_p(adam.m.data_ptr()), ctypes.c_void_p(adam.v.data_ptr()),
         tp, ctypes.byref(c), ctypes.c_void_p(adam.ibc.data_ptr()), int(adam.ibc.shape[0]),
         ctypes.c_void_p(adam.step_dev.data_ptr()), _lib.stream_ptr(stream)), "adam_peer")
-    del np
 
 
 class PeerExchange:

@@ -58,3 +58,85 @@ def test_adam_peer_step_simulated_ranks(G):
     for name, a, b in (("m", m, st_ref.m), ("v", v, st_ref.v)):
         bad = (a != b).nonzero().flatten()
         assert bad.numel() == 0, (name, bad[:5].tolist(), a[bad[:5]].tolist(), b[bad[:5]].tolist(), n, k)
+
+
+def test_peer_exchange_single_rank(tmp_path):
+    """dist.PeerExchange end to end on a one-rank NCCL group: symmetric-memory
+    arena, peer pointers, device barriers and the fused kernel inside the
+    engine step give the same bits as the plain engine step."""
+    import torch.distributed as dist
+    from paper_2501_08672_b200.dist import PeerExchange
+    from paper_2501_08672_b200.optimize import OptimConfig, WindowEngine
+    from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
+    from paper_2501_08672_b200.scene import camera_for, orbit_views
+    s = load("scene_room_0323")
+    cam = camera_for(160, 128)
+    views = orbit_views(3)
+    st = RasterSettings(alpha_cut=1 / 255)
+    gt = GaussianArrays(s["means"], s["rots"], s["scales"], s["opacities"], s["shs"])
+    obs = [render(gt, T, cam, st, retain_cache=False).image.clone() for T in views]
+    shs = s["shs"].copy()
+    shs[:, 0, :] += 0.05
+    results = []
+    dist.init_process_group("nccl", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        for peer in (False, True):
+            win = GaussianArrays(s["means"], s["rots"], s["scales"], s["opacities"], shs)
+            eng = WindowEngine(win, cam, views, st, OptimConfig(), lanes=2)
+            if peer:
+                eng.exchange = PeerExchange(eng)
+            for _ in range(3):
+                eng.step(obs)
+            eng.finish()
+            torch.cuda.synchronize()
+            results.append((win, eng.losses()))
+    finally:
+        dist.destroy_process_group()
+    (w0, l0), (w1, l1) = results
+    assert np.array_equal(l0, l1)
+    for f in ("means", "rots", "scales", "opacities", "shs"):
+        assert torch.equal(getattr(w0, f), getattr(w1, f)), f
+
+
+def test_peer_exchange_in_cuda_graph(tmp_path):
+    """The fused peer step (barriers + kernel) replays inside the step's CUDA
+    graph with the same bits as eager steps."""
+    import torch.distributed as dist
+    from paper_2501_08672_b200.dist import PeerExchange
+    from paper_2501_08672_b200.optimize import OptimConfig, WindowEngine
+    from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
+    from paper_2501_08672_b200.scene import camera_for, orbit_views
+    s = load("scene_room_0323")
+    cam = camera_for(160, 128)
+    views = orbit_views(3)
+    st = RasterSettings(alpha_cut=1 / 255)
+    gt = GaussianArrays(s["means"], s["rots"], s["scales"], s["opacities"], s["shs"])
+    obs = [render(gt, T, cam, st, retain_cache=False).image.clone() for T in views]
+    shs = s["shs"].copy()
+    shs[:, 0, :] += 0.05
+    out = []
+    dist.init_process_group("nccl", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        for graph in (False, True):
+            win = GaussianArrays(s["means"], s["rots"], s["scales"], s["opacities"], shs)
+            stream = torch.cuda.Stream()
+            eng = WindowEngine(win, cam, views, st, OptimConfig(), lanes=2, stream=stream)
+            eng.exchange = PeerExchange(eng)
+            with torch.cuda.stream(stream):
+                eng.step(obs)
+                if graph:
+                    eng.capture(obs)
+                    for _ in range(2):
+                        eng.replay()
+                else:
+                    for _ in range(2):
+                        eng.step(obs)
+                eng.finish()
+            torch.cuda.synchronize()
+            out.append(win)
+    finally:
+        dist.destroy_process_group()
+    for f in ("means", "rots", "scales", "opacities", "shs"):
+        assert torch.equal(getattr(out[0], f), getattr(out[1], f)), f
