@@ -30,7 +30,7 @@
 // record loop.  Without a processed-entry count (n_contrib == NULL, the
 // window engine) the count update is dropped.  Optionally fuses the photometric loss (optimize.py:48-74): the
 // epilogue reads the observed pixels, writes dL/dI and reduces the loss per
-// tile; the last CTA (ticket) adds the tile sums in tile order.
+// tile; k_loss_total then adds the tile sums in a fixed order.
 //
 // Backward (_kernels.py:122-216): per pixel the forward is recomputed front
 // to back with the SAME instruction sequence (shared helpers below), so T is
@@ -220,7 +220,7 @@ struct LossArgs {
     float* grad;             // (H,W,3) dL/dI out
     double* sums;            // [ntiles*2] tile partials
     double* sums_out;        // [2] totals
-    unsigned long long* ticket;
+    unsigned long long* ticket;    // (unused: the totals come from k_loss_total)
     int kind;                // 0 L1, 1 L2
     float gscale;
 };
@@ -266,28 +266,21 @@ struct RecPipe {
     }
 };
 
-// Deterministic loss total: the tile partials summed in tile order (called by
-// the one warp that observed the last ticket).
-__device__ __noinline__ void loss_total(const Ws& w, const LossArgs& L, int lane) {
-    __threadfence();
+// Deterministic loss total over the tile partials: one CTA of LT_THREADS;
+// thread t adds a contiguous run of tiles in order, then a fixed tree (warp
+// butterflies, then the warp sums in order).  Launched after the kernel that
+// wrote the partials, so every partial is visible.
+constexpr int LT_THREADS = 1024;
+__global__ void __launch_bounds__(LT_THREADS) k_loss_total(int ntiles, const double* __restrict__ sums,
+                                                         double* __restrict__ out) {
+    __shared__ double s0[LT_THREADS / 32], s1[LT_THREADS / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = (ntiles + LT_THREADS - 1) / LT_THREADS;
     double v0 = 0.0, v1 = 0.0;
-    // lane l adds tiles l, l + 32, ... in order; the loads of 8 tiles are in
-    // flight together (L2-coherent ld.cg), the additions keep their order
-    constexpr int B = 8;
-    for (int t0 = lane; t0 < w.ntiles; t0 += 32 * B) {
-        double2 x[B];
-#pragma unroll
-        for (int k = 0; k < B; ++k) {
-            const int t = t0 + 32 * k;
-            x[k] = t < w.ntiles ? __ldcg((const double2*)L.sums + t) : make_double2(0.0, 0.0);
-        }
-#pragma unroll
-        for (int k = 0; k < B; ++k) {
-            if (t0 + 32 * k < w.ntiles) {
-                v0 += x[k].x;
-                v1 += x[k].y;
-            }
-        }
+    for (int j = 0, t = tid * per; j < per && t < ntiles; ++j, ++t) {
+        const double2 x = ((const double2*)sums)[t];
+        v0 += x.x;
+        v1 += x.y;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -295,8 +288,18 @@ __device__ __noinline__ void loss_total(const Ws& w, const LossArgs& L, int lane
         v1 += __shfl_xor_sync(0xffffffffu, v1, o);
     }
     if (lane == 0) {
-        L.sums_out[0] = v0;
-        L.sums_out[1] = v1;
+        s0[warp] = v0;
+        s1[warp] = v1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double a0 = 0.0, a1 = 0.0;
+        for (int w = 0; w < LT_THREADS / 32; ++w) {
+            a0 += s0[w];
+            a1 += s1[w];
+        }
+        out[0] = a0;
+        out[1] = a1;
     }
 }
 
@@ -445,16 +448,10 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
             l0 += __shfl_xor_sync(0xffffffffu, l0, o);
             l1 += __shfl_xor_sync(0xffffffffu, l1, o);
         }
-        unsigned long long done = 0;
         if (lane == 0) {
             L.sums[2 * tile] = l0;
             L.sums[2 * tile + 1] = l1;
-            // release: the tile partial is visible before the tile counts as done
-            asm volatile("atom.release.gpu.global.add.u64 %0, [%1], 1;" : "=l"(done) : "l"(L.ticket) : "memory");
         }
-        done = __shfl_sync(0xffffffffu, done, 0);
-        // the warp that finished the last tile: deterministic sum in tile order
-        if (done == (unsigned long long)w.ntiles - 1) loss_total(w, L, lane);
     }
 }
 
@@ -707,13 +704,13 @@ static int persistent_grid(const void* fn, int ntiles) {
     return g < need ? g : need;
 }
 
-cudaError_t launch_blend_fwd(const Ws& w, const lsb_settings& s, int W, int H, float* image, float* t_final,
-                             int32_t* n_contrib, float* depth, const float* observed, int kind, float gscale,
-                             float* grad, double* loss_out, cudaStream_t st) {
+static cudaError_t blend_fwd_kernel(const Ws& w, const lsb_settings& s, int W, int H, float* image, float* t_final,
+                                    int32_t* n_contrib, float* depth, const float* observed, int kind, float gscale,
+                                    float* grad, double* loss_out, cudaStream_t st) {
     const BlendArgs a = blend_args(s, W, H);
-    LossArgs L{observed, grad, w.loss_part, loss_out, w.ctr + 5, kind, gscale};
-    // reset the loss done-count and the forward tile queue ([5], [7])
-    cudaError_t e = cudaMemsetAsync(w.ctr + 5, 0, 3 * sizeof(unsigned long long), st);
+    LossArgs L{observed, grad, w.loss_part, loss_out, nullptr, kind, gscale};
+    // reset the forward tile queue ([7])
+    cudaError_t e = cudaMemsetAsync(w.ctr + 7, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
     const bool cut = s.alpha_cut > 0.0;
     // n_contrib == NULL (window engine): the count-free forward (no depth)
@@ -740,8 +737,15 @@ cudaError_t launch_blend_fwd(const Ws& w, const lsb_settings& s, int W, int H, f
     return cudaGetLastError();
 }
 
-// One warp: the loss total from the tile partials, in tile order.
-__global__ void k_loss_total(Ws w, LossArgs L) { loss_total(w, L, threadIdx.x); }
+cudaError_t launch_blend_fwd(const Ws& w, const lsb_settings& s, int W, int H, float* image, float* t_final,
+                             int32_t* n_contrib, float* depth, const float* observed, int kind, float gscale,
+                             float* grad, double* loss_out, cudaStream_t st) {
+    cudaError_t e = blend_fwd_kernel(w, s, W, H, image, t_final, n_contrib, depth, observed, kind, gscale, grad,
+                                     loss_out, st);
+    if (e != cudaSuccess || !observed) return e;
+    k_loss_total<<<1, LT_THREADS, 0, st>>>(w.ntiles, w.loss_part, loss_out);     // fused loss: the total
+    return cudaGetLastError();
+}
 
 cudaError_t launch_blend_bwd(const Ws& w, const lsb_settings& s, int W, int H, const float* image,
                              const int32_t* n_contrib, const float* gimg, float gscale, cudaStream_t st) {
@@ -764,7 +768,7 @@ cudaError_t launch_blend_bwd_loss(const Ws& w, const lsb_settings& s, int W, int
     const LossArgs L{observed, nullptr, w.loss_part, loss_out, nullptr, kind, grad_scale};
     k_blend_bwd<true><<<persistent_grid((const void*)k_blend_bwd<true>, w.ntiles), 32 * WPB, 0, st>>>(
         w, a, image, nullptr, 1.0f, L);
-    k_loss_total<<<1, 32, 0, st>>>(w, L);
+    k_loss_total<<<1, LT_THREADS, 0, st>>>(w.ntiles, w.loss_part, loss_out);
     return cudaGetLastError();
 }
 
