@@ -339,6 +339,7 @@ def run_ours(args, wl, rank, world, local_rank):
     # this rank's observed images from pinned host memory (copy stream, in
     # view order, overlapping the lanes' kernels) and reads the loss sums back
     host_obs = [o.cpu().pin_memory() for o in observed]
+    eng.copy_streams = max(1, args.copy_streams)
     with torch.cuda.stream(stream):
         eng.step(host_obs, allreduce=allreduce)            # e2e warm-up (staging buffers)
     torch.cuda.synchronize()
@@ -708,6 +709,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--lanes", type=int, default=5, help="concurrent view pipelines per GPU")
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="eager launches instead of a CUDA graph")
+    ap.add_argument("--copy-streams", type=int, default=1, help="H2D staging streams for the e2e pass")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
                     help="N>1 gradient exchange: NCCL all-reduce + Adam, or the fused peer-memory step")
     args = ap.parse_args()

@@ -207,6 +207,7 @@ class WindowEngine:
         self.bin_mode = (1 if settings.alpha_cut > 0.0 else 0) if bin_mode is None else int(bin_mode)
         self.loss_in_backward = True        # photometric loss fused into the backward (else the forward)
         self.exchange = None                # dist.PeerExchange: multi-GPU step over NVLink peer memory
+        self.copy_streams = 1               # H2D staging streams (views round-robin)
         self.arena = arrays
         if master == "f64" and arrays.dtype != torch.float64:
             arrays = arrays.clone(torch.float64)
@@ -280,12 +281,14 @@ class WindowEngine:
         dev = self.grads.flat.device
         if self.copy_stream is None:
             self.copy_stream = torch.cuda.Stream(dev)
+            self._copy_streams = [self.copy_stream] + [torch.cuda.Stream(dev) for _ in range(self.copy_streams - 1)]
             self.obs_dev = [torch.empty((self.h, self.w, 3), dtype=torch.float32, device=dev) for _ in self.views]
-        cs = self.copy_stream
-        cs.wait_event(ready)
+        for cs in self._copy_streams:
+            cs.wait_event(ready)
         lib = _lib.load()
         events = []
         for v, obs in enumerate(observed):
+            cs = self._copy_streams[v % len(self._copy_streams)]
             if obs.dtype != torch.float32 or tuple(obs.shape) != (self.h, self.w, 3) or not obs.is_contiguous():
                 raise ValueError("observed images must be contiguous float32 (H, W, 3)")
             if capturing and not obs.is_pinned():
@@ -367,9 +370,10 @@ class WindowEngine:
                 done.record(ln.stream)
                 main.wait_event(done)
         if host:
-            done = torch.cuda.Event()
-            done.record(self.copy_stream)
-            main.wait_event(done)
+            for cs in self._copy_streams:
+                done = torch.cuda.Event()
+                done.record(cs)
+                main.wait_event(done)
         with torch.cuda.stream(main):
             mark("adam", main)
             if self.exchange is not None:       # fused peer-memory exchange + Adam (dist.PeerExchange)
