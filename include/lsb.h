@@ -191,6 +191,12 @@ int lsb_render_blend_bwd(const lsb_settings* s, void* ws, size_t ws_bytes, const
  * loss_out[0..1] = [sum |diff| (L1) or diff^2 (L2), sum diff^2] (tile
  * partials summed in tile order; deterministic).  The window engine's step:
  * lsb_render_bin, lsb_render_blend (n_contrib NULL), this, lsb_render_chain. */
+/* Forward + photometric loss + backward in one kernel (the window engine's
+ * step after lsb_render_bin): the same results as lsb_render_blend (no
+ * count) followed by lsb_render_blend_bwd_loss, without writing the image,
+ * T or dL/dI; loss_out as there. */
+int lsb_render_blend_fused_loss(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
+                                const float* observed, int kind, float grad_scale, double* loss_out, void* stream);
 int lsb_render_blend_bwd_loss(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
                               const float* image, const float* observed, int kind, float grad_scale,
                               double* loss_out, void* stream);

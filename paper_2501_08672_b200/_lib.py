@@ -85,6 +85,8 @@ SIGNATURES = [
                                          _P, _P, _c.c_int, _c.c_float, _P, _P, _P]),
     ("lsb_render_blend_bwd", _c.c_int, [_c.POINTER(Settings), _P, _c.c_size_t, _c.POINTER(Dims), _P, _P, _P,
                                         _c.c_float, _P]),
+    ("lsb_render_blend_fused_loss", _c.c_int, [_c.POINTER(Settings), _P, _c.c_size_t, _c.POINTER(Dims), _P,
+                                               _c.c_int, _c.c_float, _P, _P]),
     ("lsb_render_blend_bwd_loss", _c.c_int, [_c.POINTER(Settings), _P, _c.c_size_t, _c.POINTER(Dims), _P, _P,
                                              _c.c_int, _c.c_float, _P, _P]),
     ("lsb_render_chain", _c.c_int, [_c.POINTER(Params), _c.POINTER(Camera), _c.POINTER(Pose),

@@ -10,6 +10,7 @@ cudaError_t launch_preprocess(const lsb_params&, const lsb_camera&, const lsb_po
                               const Ws&, cudaStream_t);
 cudaError_t launch_blend_fwd(const Ws&, const lsb_settings&, int, int, float*, float*, int32_t*, float*,
                              const float*, int, float, float*, double*, cudaStream_t);
+cudaError_t launch_blend_fused(const Ws&, const lsb_settings&, int, int, const float*, int, float, double*, cudaStream_t);
 cudaError_t launch_blend_bwd_loss(const Ws&, const lsb_settings&, int, int, const float*, const float*, int, float,
                                   double*, cudaStream_t);
 cudaError_t launch_blend_bwd(const Ws&, const lsb_settings&, int, int, const float*, const int32_t*,
@@ -265,6 +266,18 @@ int lsb_render_blend_bwd(const lsb_settings* s, void* ws, size_t ws_bytes, const
     if (rc) return rc;
     return check_cuda(launch_blend_bwd(w, *s, d->width, d->height, image, n_contrib, grad_image, grad_scale,
                                        (cudaStream_t)stream), "blend_bwd");
+}
+
+int lsb_render_blend_fused_loss(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* d,
+                                const float* observed, int kind, float grad_scale, double* loss_out, void* stream) {
+    if (!s || !observed || !loss_out) return fail(LSB_EINVAL, "NULL argument");
+    if (kind != 0 && kind != 1) return fail(LSB_EINVAL, "kind must be 0 (l1) or 1 (l2)");
+    Ws w;
+    int rc = get_ws(ws, ws_bytes, d, &w);
+    if (rc) return rc;
+    return check_cuda(launch_blend_fused(w, *s, d->width, d->height, observed, kind, grad_scale, loss_out,
+                                         (cudaStream_t)stream),
+                      "blend_fused_loss");
 }
 
 int lsb_render_blend_bwd_loss(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* d,

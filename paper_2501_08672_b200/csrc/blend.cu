@@ -509,6 +509,94 @@ __device__ __forceinline__ void bwd_half(const Frame& f, float4 q1, bool rin, fl
     M[5] = fmaf(S0 * dy, dy, M[5]);
 }
 
+// The backward's record walk over one tile's list [start, end): the forward
+// recomputed per pixel (same instruction sequence as the forward, so T is
+// bit-identical), per-record screen partials reduced across the warp and
+// written per intersection; entries the walk never reaches get zeros.
+__device__ __forceinline__ void bwd_walk(const Ws& w, const BlendArgs& a, RecPipe& pipe, int tile, int start,
+                                         int end, int gx0, int gy0, float (&T)[2][RUN], float (&gD)[2][RUN],
+                                         float (&Gr)[2][RUN], float (&Gg)[2][RUN], float (&Gb)[2][RUN], int lane) {
+    const float k2 = -2.0f / (float)LOG2E;     // undo the exp2 scaling: a_k = A k2, e = E k2
+    const float kap = a.clamp;
+    const float gx0f = (float)gx0, gy0f = (float)gy0;
+    pipe.start = start;
+    pipe.end = end;
+    pipe.begin(w, lane);
+    for (int b = 0, base = start; base < end; ++b, base += 32) {
+        bool alive = false;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int j = 0; j < RUN; ++j) alive |= T[h][j] >= a.tmin;
+        if (!__any_sync(0xffffffffu, alive)) break;
+        // intersection ids of this batch, one per lane (written per record below)
+        const int ecur = base + lane < end ? w.tile_e[base + lane] : 0;
+        const Rec* sr = pipe.next(w, b, lane);
+        const int nb = min(32, end - base);
+        for (int k = 0; k < nb; ++k) {
+            const float4 q0 = *(const float4*)&sr[k].mxh;        // mxh myh mxl myl
+            const float4 q1 = *(const float4*)&sr[k].A;          // A s E lop
+            const float4 q2 = *(const float4*)&sr[k].kc0;        // clamp * (c0 c1 c2 z)
+            const int4 q3 = *(const int4*)&sr[k].bbx;            // bbx bby id ebase
+            const int cx0 = (q3.x & 0xffff) - gx0, cx1 = (q3.x >> 16) - gx0;
+            const int ry0 = (q3.y & 0xffff) - gy0, ry1 = (q3.y >> 16) - gy0;
+            const bool row0 = ry0 <= 0 && ry1 > 0, row1 = ry0 <= 8 && ry1 > 8;
+            const bool over = alive && cx0 < RUN && cx1 > 0 && (row0 || row1);
+            // accumulators: colour (3, x clamp) and the moments sum gd, gd u,
+            // gd dy, gd u^2, gd u dy, gd dy^2 with gd = alpha dL/dalpha
+            float c[3] = {0.f, 0.f, 0.f}, M[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            const bool wover = __any_sync(0xffffffffu, over);
+            if (wover) {
+                // warp-uniform from here: lanes without work get +inf thresholds
+                float thr[RUN];
+#pragma unroll
+                for (int j = 0; j < RUN; ++j) thr[j] = over ? col_thr(j, cx0, cx1, a.tmin) : __int_as_float(0x7f800000);
+                const Frame f = frame_of(q0, q1.w, gx0f, gy0f);
+                if (q1.w >= SAT_LOP) {
+                    bwd_half<true>(f, q1, over && row0, 0.f, thr, a, kap, q2, Gr[0], Gg[0], Gb[0], T[0], gD[0], c, M);
+                    bwd_half<true>(f, q1, over && row1, 8.f, thr, a, kap, q2, Gr[1], Gg[1], Gb[1], T[1], gD[1], c, M);
+                } else {
+                    bwd_half<false>(f, q1, over && row0, 0.f, thr, a, kap, q2, Gr[0], Gg[0], Gb[0], T[0], gD[0], c,
+                                    M);
+                    bwd_half<false>(f, q1, over && row1, 8.f, thr, a, kap, q2, Gr[1], Gg[1], Gb[1], T[1], gD[1], c,
+                                    M);
+                }
+            }
+            float val = 0.f;
+            if (wover) {
+                // moments -> conic-space sums with v0 = a_k u, v1 = s v0 + e dy
+                const float ak = q1.x * k2, ek = q1.z * k2, sa = q1.y * ak;
+                float v[9];
+                v[0] = c[0];
+                v[1] = c[1];
+                v[2] = c[2];
+                v[3] = M[0];
+                v[4] = ak * M[1];
+                v[5] = fmaf(sa, M[1], ek * M[2]);
+                v[6] = ak * ak * M[3];
+                v[7] = ak * fmaf(sa, M[3], ek * M[4]);
+                v[8] = fmaf(sa * sa, M[3], fmaf(2.f * sa * ek, M[4], ek * ek * M[5]));
+                // index i of the 8-vector lands in lanes 4i..4i+3 (reduce8)
+                const float r8 = reduce8(v, lane);
+                float r9 = v[8];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) r9 += __shfl_xor_sync(0xffffffffu, r9, o);
+                val = __shfl_sync(0xffffffffu, r8, 4 * min(lane, 7));
+                if (lane == 8) val = r9;
+                val *= (lane < 3) ? kap : ((lane == 3) ? a.ik * ex2_approx(-q1.w) : ((lane < 6) ? 1.f : 0.5f));   // 1/op
+            }
+            const int e = __shfl_sync(0xffffffffu, ecur, k);
+            if (lane < NUM_PART) w.part[(int64_t)e * NUM_PART + lane] = val;
+        }
+        __syncwarp();
+    }
+    pipe.drain();
+    // intersections the walk never reached contribute nothing
+    const int fin = w.tile_start[tile + 1], from = max(end, start);
+    for (int z = lane; z < (fin - from) * NUM_PART; z += 32)
+        w.part[(int64_t)w.tile_e[from + z / NUM_PART] * NUM_PART + z % NUM_PART] = 0.f;
+}
+
 template <bool LOSS>
 __global__ void __launch_bounds__(32 * WPB, BWD_MIN_BLOCKS)
 k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __restrict__ gimg, float gscale,
@@ -516,8 +604,6 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __r
     __shared__ Rec s_rec[WPB][2 * 32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int qx = (lane & 3) * RUN, r0 = lane >> 2;
-    const float k2 = -2.0f / (float)LOG2E;     // undo the exp2 scaling: a_k = A k2, e = E k2
-    const float kap = a.clamp;
     RecPipe pipe;
     pipe.buf = s_rec[wib];
 #if STATIC_FIRST_TILE
@@ -541,7 +627,6 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __r
         if (tile < 0) break;
         const int ox = (tile % w.ntx) * TILE, oy = (tile / w.ntx) * TILE;
         const int gx0 = ox + qx, gy0 = oy + r0;
-        const float gx0f = (float)gx0, gy0f = (float)gy0;
         // per-pixel state: T (as in the forward), gD = g . (I - prefix colour), g = dL/dI
         float T[2][RUN], gD[2][RUN], Gr[2][RUN], Gg[2][RUN], Gb[2][RUN];
         double l0 = 0.0, l1 = 0.0;
@@ -605,83 +690,7 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __r
                 L.sums[2 * tile + 1] = l1;
             }
         }
-        const int start = w.tile_start[tile], end = w.tile_last[tile];
-        pipe.start = start;
-        pipe.end = end;
-        pipe.begin(w, lane);
-        for (int b = 0, base = start; base < end; ++b, base += 32) {
-            bool alive = false;
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-                for (int j = 0; j < RUN; ++j) alive |= T[h][j] >= a.tmin;
-            if (!__any_sync(0xffffffffu, alive)) break;
-            // intersection ids of this batch, one per lane (written per record below)
-            const int ecur = base + lane < end ? w.tile_e[base + lane] : 0;
-            const Rec* sr = pipe.next(w, b, lane);
-            const int nb = min(32, end - base);
-            for (int k = 0; k < nb; ++k) {
-                const float4 q0 = *(const float4*)&sr[k].mxh;        // mxh myh mxl myl
-                const float4 q1 = *(const float4*)&sr[k].A;          // A s E lop
-                const float4 q2 = *(const float4*)&sr[k].kc0;        // clamp * (c0 c1 c2 z)
-                const int4 q3 = *(const int4*)&sr[k].bbx;            // bbx bby id ebase
-                const int cx0 = (q3.x & 0xffff) - gx0, cx1 = (q3.x >> 16) - gx0;
-                const int ry0 = (q3.y & 0xffff) - gy0, ry1 = (q3.y >> 16) - gy0;
-                const bool row0 = ry0 <= 0 && ry1 > 0, row1 = ry0 <= 8 && ry1 > 8;
-                const bool over = alive && cx0 < RUN && cx1 > 0 && (row0 || row1);
-                // accumulators: colour (3, x clamp) and the moments sum gd, gd u,
-                // gd dy, gd u^2, gd u dy, gd dy^2 with gd = alpha dL/dalpha
-                float c[3] = {0.f, 0.f, 0.f}, M[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                const bool wover = __any_sync(0xffffffffu, over);
-                if (wover) {
-                    // warp-uniform from here: lanes without work get +inf thresholds
-                    float thr[RUN];
-#pragma unroll
-                    for (int j = 0; j < RUN; ++j) thr[j] = over ? col_thr(j, cx0, cx1, a.tmin) : __int_as_float(0x7f800000);
-                    const Frame f = frame_of(q0, q1.w, gx0f, gy0f);
-                    if (q1.w >= SAT_LOP) {
-                        bwd_half<true>(f, q1, over && row0, 0.f, thr, a, kap, q2, Gr[0], Gg[0], Gb[0], T[0], gD[0], c, M);
-                        bwd_half<true>(f, q1, over && row1, 8.f, thr, a, kap, q2, Gr[1], Gg[1], Gb[1], T[1], gD[1], c, M);
-                    } else {
-                        bwd_half<false>(f, q1, over && row0, 0.f, thr, a, kap, q2, Gr[0], Gg[0], Gb[0], T[0], gD[0], c,
-                                        M);
-                        bwd_half<false>(f, q1, over && row1, 8.f, thr, a, kap, q2, Gr[1], Gg[1], Gb[1], T[1], gD[1], c,
-                                        M);
-                    }
-                }
-                float val = 0.f;
-                if (wover) {
-                    // moments -> conic-space sums with v0 = a_k u, v1 = s v0 + e dy
-                    const float ak = q1.x * k2, ek = q1.z * k2, sa = q1.y * ak;
-                    float v[9];
-                    v[0] = c[0];
-                    v[1] = c[1];
-                    v[2] = c[2];
-                    v[3] = M[0];
-                    v[4] = ak * M[1];
-                    v[5] = fmaf(sa, M[1], ek * M[2]);
-                    v[6] = ak * ak * M[3];
-                    v[7] = ak * fmaf(sa, M[3], ek * M[4]);
-                    v[8] = fmaf(sa * sa, M[3], fmaf(2.f * sa * ek, M[4], ek * ek * M[5]));
-                    // index i of the 8-vector lands in lanes 4i..4i+3 (reduce8)
-                    const float r8 = reduce8(v, lane);
-                    float r9 = v[8];
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) r9 += __shfl_xor_sync(0xffffffffu, r9, o);
-                    val = __shfl_sync(0xffffffffu, r8, 4 * min(lane, 7));
-                    if (lane == 8) val = r9;
-                    val *= (lane < 3) ? kap : ((lane == 3) ? a.ik * ex2_approx(-q1.w) : ((lane < 6) ? 1.f : 0.5f));   // 1/op
-                }
-                const int e = __shfl_sync(0xffffffffu, ecur, k);
-                if (lane < NUM_PART) w.part[(int64_t)e * NUM_PART + lane] = val;
-            }
-            __syncwarp();
-        }
-        pipe.drain();
-        // intersections the walk never reached contribute nothing
-        const int fin = w.tile_start[tile + 1], from = max(end, start);
-        for (int z = lane; z < (fin - from) * NUM_PART; z += 32)
-            w.part[(int64_t)w.tile_e[from + z / NUM_PART] * NUM_PART + z % NUM_PART] = 0.f;
+        bwd_walk(w, a, pipe, tile, w.tile_start[tile], w.tile_last[tile], gx0, gy0, T, gD, Gr, Gg, Gb, lane);
     }
 }
 
@@ -702,6 +711,156 @@ static int persistent_grid(const void* fn, int ntiles) {
     const int need = (ntiles + WPB - 1) / WPB;
     const int g = sms * (per_sm > BLEND_RESERVE ? per_sm - BLEND_RESERVE : 1);
     return g < need ? g : need;
+}
+
+// Forward + photometric loss + backward of one tile in ONE kernel (the window
+// engine's step).  Per tile-warp: the count-free forward walk (the same
+// instructions as k_blend_fwd<false, CUT, false>), then per pixel the image,
+// the loss partials and dL/dI in registers (the same arithmetic as the loss
+// fused into k_blend_bwd<true>), then the backward walk over the entries the
+// forward reached.  No image, T or gradient image goes through memory, and
+// the tile start (queue, ranges, record pipeline) is paid once.
+template <bool CUT>
+__global__ void __launch_bounds__(32 * WPB, BWD_MIN_BLOCKS)
+k_blend_fused(Ws w, BlendArgs a, LossArgs L) {
+    __shared__ Rec s_rec[WPB][2 * 32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int qx = (lane & 3) * RUN, r0 = lane >> 2;
+    RecPipe pipe;
+    pipe.buf = s_rec[wib];
+    const float kap = a.clamp;
+    int q0 = blockIdx.x * WPB + wib;
+    const int nwarps = gridDim.x * WPB;
+    for (;;) {
+        int tile = 0;
+        if (lane == 0) {
+            const int q = q0 >= 0 ? q0 : (int)atomicAdd(&w.ctr[8], 1ull) + nwarps;
+            q0 = -1;
+            tile = q < w.ntiles ? w.tile_order[q] : -1;
+        }
+        tile = __shfl_sync(0xffffffffu, tile, 0);
+        if (tile < 0) break;
+        const int ox = (tile % w.ntx) * TILE, oy = (tile / w.ntx) * TILE;
+        const int gx0 = ox + qx, gy0 = oy + r0;
+        const float gx0f = (float)gx0, gy0f = (float)gy0;
+        // ---- forward ----
+        float T[2][RUN], cr[2][RUN], cg[2][RUN], cb[2][RUN];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int j = 0; j < RUN; ++j) {
+                T[h][j] = (gy0 + 8 * h < a.H && gx0 + j < a.W) ? 1.f : -1.f;
+                cr[h][j] = cg[h][j] = cb[h][j] = 0.f;
+            }
+        int last = 0;
+        const int start = w.tile_start[tile], end = w.tile_start[tile + 1];
+        pipe.start = start;
+        pipe.end = end;
+        pipe.begin(w, lane);
+        for (int b = 0, base = start; base < end; ++b, base += 32) {
+            bool alive = false;
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int j = 0; j < RUN; ++j) alive |= T[h][j] >= a.tmin;
+            if (!__any_sync(0xffffffffu, alive)) break;
+            const Rec* sr = pipe.next(w, b, lane);
+            const int nb = min(32, end - base);
+            for (int k = 0; k < nb; ++k) {
+                const int4 qi = *(const int4*)&sr[k].bbx;
+                const int cx0 = (qi.x & 0xffff) - gx0, cx1 = (qi.x >> 16) - gx0;
+                const int ry0 = (qi.y & 0xffff) - gy0, ry1 = (qi.y >> 16) - gy0;
+                const bool row0 = ry0 <= 0 && ry1 > 0, row1 = ry0 <= 8 && ry1 > 8;
+                if (cx0 >= RUN || cx1 <= 0 || !(row0 || row1)) continue;
+                if (alive) last = base + k + 1;
+                float thr[RUN];
+#pragma unroll
+                for (int j = 0; j < RUN; ++j) thr[j] = col_thr(j, cx0, cx1, a.tmin);
+                const float4 q0v = *(const float4*)&sr[k].mxh;
+                const float4 qb = *(const float4*)&sr[k].A;
+                const float4 qc = *(const float4*)&sr[k].kc0;
+                const Frame f = frame_of(q0v, qb.w, gx0f, gy0f);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (!(h ? row1 : row0)) continue;
+                    float dy, u0, edy;
+                    row_terms(f, qb.y, qb.z, 8.f * h, dy, u0, edy);
+#pragma unroll
+                    for (int j = 0; j < RUN; ++j) {
+                        float u;
+                        const float al = alpha_sat(qb.x, u0, edy, j, u);
+                        fwd_pixel_nc(al, thr[j], CUT ? a.cutp : 0.f, -kap, qc.x, qc.y, qc.z, T[h][j], cr[h][j],
+                                     cg[h][j], cb[h][j]);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        pipe.drain();
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
+        last = max(last, start);
+        // ---- image, loss, dL/dI ----
+        float gD[2][RUN], Gr[2][RUN], Gg[2][RUN], Gb[2][RUN];
+        double l0 = 0.0, l1 = 0.0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int j = 0; j < RUN; ++j) {
+                gD[h][j] = Gr[h][j] = Gg[h][j] = Gb[h][j] = 0.f;
+                const int gy = gy0 + 8 * h;
+                const bool in = gy < a.H && gx0 + j < a.W;
+                if (in) {
+                    const int64_t p = (int64_t)gy * a.W + gx0 + j;
+                    const float i3[3] = {cr[h][j] + T[h][j] * a.bg0, cg[h][j] + T[h][j] * a.bg1,
+                                         cb[h][j] + T[h][j] * a.bg2};
+                    float g3[3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const double d = (double)i3[c] - (double)L.observed[3 * p + c];
+                        l1 += d * d;
+                        if (L.kind == 0) {
+                            l0 += fabs(d);
+                            g3[c] = d > 0.0 ? L.gscale : (d < 0.0 ? -L.gscale : 0.f);
+                        } else {
+                            l0 += d * d;
+                            g3[c] = (float)(2.0 * d * (double)L.gscale);
+                        }
+                    }
+                    Gr[h][j] = g3[0];
+                    Gg[h][j] = g3[1];
+                    Gb[h][j] = g3[2];
+                    gD[h][j] = Gr[h][j] * i3[0] + Gg[h][j] * i3[1] + Gb[h][j] * i3[2];
+                }
+                T[h][j] = in ? 1.f : -1.f;           // the backward recomputes T from the front
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+            l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+        }
+        if (lane == 0) {
+            L.sums[2 * tile] = l0;
+            L.sums[2 * tile + 1] = l1;
+        }
+        // ---- backward ----
+        bwd_walk(w, a, pipe, tile, start, last, gx0, gy0, T, gD, Gr, Gg, Gb, lane);
+    }
+}
+
+cudaError_t launch_blend_fused(const Ws& w, const lsb_settings& s, int W, int H, const float* observed, int kind,
+                               float grad_scale, double* loss_out, cudaStream_t st) {
+    const BlendArgs a = blend_args(s, W, H);
+    cudaError_t e = cudaMemsetAsync(w.ctr + 8, 0, sizeof(unsigned long long), st);   // tile queue
+    if (e != cudaSuccess) return e;
+    const LossArgs L{observed, nullptr, w.loss_part, loss_out, nullptr, kind, grad_scale};
+    if (s.alpha_cut > 0.0)
+        k_blend_fused<true><<<persistent_grid((const void*)k_blend_fused<true>, w.ntiles), 32 * WPB, 0, st>>>(w, a, L);
+    else
+        k_blend_fused<false><<<persistent_grid((const void*)k_blend_fused<false>, w.ntiles), 32 * WPB, 0, st>>>(w, a,
+                                                                                                             L);
+    k_loss_total<<<1, LT_THREADS, 0, st>>>(w.ntiles, w.loss_part, loss_out);
+    return cudaGetLastError();
 }
 
 static cudaError_t blend_fwd_kernel(const Ws& w, const lsb_settings& s, int W, int H, float* image, float* t_final,

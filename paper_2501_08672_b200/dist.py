@@ -136,11 +136,6 @@ class PeerExchange:
             raise ValueError("the peer step addresses at most 8 ranks")
         self.engine = engine
         self._handles = []
-        if hasattr(symm, "enable_symm_mem_for_group"):
-            try:
-                symm.enable_symm_mem_for_group(self.group.group_name)
-            except Exception:       # noqa: BLE001 - already enabled / not needed on this version
-                pass
 
         def sym(t):
             s = symm.empty(t.shape, dtype=t.dtype, device=t.device)

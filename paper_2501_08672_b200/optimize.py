@@ -25,8 +25,8 @@ from . import _lib
 from .errors import EmptyMask
 from .geometry import as_se3
 from .raster import (GaussianArrays, ParamGradients, RasterSettings, RenderState, _as_arrays, _f32,
-                     render_bin, render_blend, render_blend_bwd, render_blend_bwd_loss, render_blend_loss,
-                     render_chain)
+                     render_bin, render_blend, render_blend_bwd, render_blend_bwd_loss, render_blend_fused_loss,
+                     render_blend_loss, render_chain)
 
 
 @dataclass
@@ -205,7 +205,8 @@ class WindowEngine:
                  bin_mode: Optional[int] = None):
         _lib.require()
         self.bin_mode = (1 if settings.alpha_cut > 0.0 else 0) if bin_mode is None else int(bin_mode)
-        self.loss_in_backward = True        # photometric loss fused into the backward (else the forward)
+        self.fused_blend = True             # forward + loss + backward in one kernel per view
+        self.loss_in_backward = True        # (unfused) photometric loss fused into the backward (else the forward)
         self.exchange = None                # dist.PeerExchange: multi-GPU step over NVLink peer memory
         self.copy_streams = 1               # H2D staging streams (views round-robin)
         self.arena = arrays
@@ -339,7 +340,13 @@ class WindowEngine:
                 sm.wait_event(copied[v])
                 obs = self.obs_dev[v]
             mark("blend_fwd", sm)
-            if self.loss_in_backward:
+            if self.fused_blend:
+                # forward + loss + backward in one kernel
+                render_blend_fused_loss(st, obs, _KIND[self.cfg.loss], gscale, self.loss.ptr(v), stream=sm)
+                mark("blend_fwd", sm)
+                mark("blend_bwd", sm)
+                mark("blend_bwd", sm)
+            elif self.loss_in_backward:
                 # count-free forward; the photometric loss and dL/dI are formed
                 # inside the backward, which reads the observed image
                 render_blend(st, ln.image, ln.t_final, None, stream=sm)

@@ -324,6 +324,15 @@ def render_blend_bwd(state: RenderState, image, n_contrib, grad_image, grad_scal
         ctypes.c_void_p(grad_image.data_ptr()), float(grad_scale), _lib.stream_ptr(stream)), "blend_bwd")
 
 
+def render_blend_fused_loss(state: RenderState, observed, kind: int, grad_scale: float, loss_ptr,
+                            stream=None) -> None:
+    """K3 + loss + K4 in one kernel (the window engine's step; async)."""
+    _lib.check(_lib.load().lsb_render_blend_fused_loss(
+        ctypes.byref(state.c_set), state._ws(), state.ws_bytes, ctypes.byref(state.dims),
+        ctypes.c_void_p(observed.data_ptr()), int(kind), float(grad_scale), loss_ptr, _lib.stream_ptr(stream)),
+        "blend_fused_loss")
+
+
 def render_blend_bwd_loss(state: RenderState, image, observed, kind: int, grad_scale: float, loss_ptr,
                           stream=None) -> None:
     """K4 blend backward with the photometric loss fused in: dL/dI formed per

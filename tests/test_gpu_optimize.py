@@ -83,7 +83,7 @@ def test_optimize_zero_iters_is_identity():
     assert bool((arrays.shs == before).all())
 
 
-def _room_engine(lanes, steps=2, mode="eager", loss_in_backward=True):
+def _room_engine(lanes, steps=2, mode="eager", loss_in_backward=True, fused=True):
     import torch
     from paper_2501_08672_b200.optimize import OptimConfig, WindowEngine
     from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
@@ -100,6 +100,7 @@ def _room_engine(lanes, steps=2, mode="eager", loss_in_backward=True):
     stream = torch.cuda.Stream()
     eng = WindowEngine(win, cam, views, st, OptimConfig(), lanes=lanes, stream=stream)
     eng.loss_in_backward = loss_in_backward
+    eng.fused_blend = fused
     if mode == "host":      # pinned host images staged on the copy stream
         obs = [o.cpu().pin_memory() for o in obs]
     with torch.cuda.stream(stream):
@@ -131,8 +132,19 @@ def test_engine_loss_in_backward_bit_identical():
     """The photometric loss fused into the backward (lsb_render_blend_bwd_loss)
     gives the same losses, gradients and parameters as the loss fused into
     the forward's epilogue (lsb_render_blend_loss + lsb_render_blend_bwd)."""
-    w1, l1, g1 = _room_engine(2, loss_in_backward=True)
-    w2, l2, g2 = _room_engine(2, loss_in_backward=False)
+    w1, l1, g1 = _room_engine(2, loss_in_backward=True, fused=False)
+    w2, l2, g2 = _room_engine(2, loss_in_backward=False, fused=False)
+    assert bool((g1 == g2).all())
+    assert np.array_equal(l1, l2)
+    for k in ("means", "rots", "scales", "opacities", "shs"):
+        assert bool((getattr(w1, k) == getattr(w2, k)).all()), k
+
+
+def test_engine_fused_blend_bit_identical():
+    """Forward + loss + backward in one kernel (lsb_render_blend_fused_loss)
+    gives the same losses, gradients and parameters as the separate kernels."""
+    w1, l1, g1 = _room_engine(2, fused=True)
+    w2, l2, g2 = _room_engine(2, fused=False)
     assert bool((g1 == g2).all())
     assert np.array_equal(l1, l2)
     for k in ("means", "rots", "scales", "opacities", "shs"):

@@ -31,6 +31,7 @@ def main():
     from paper_2501_08672_b200.optimize import LossBuffers, ParamGradients
     from paper_2501_08672_b200.raster import (GaussianArrays, RasterSettings, RenderState, render, render_bin,
                                               render_blend, render_blend_bwd, render_blend_bwd_loss,
+                                              render_blend_fused_loss,
                                               render_blend_loss, render_chain)
     from paper_2501_08672_b200.scene import bake_room, camera_for, orbit_views
     torch.cuda.set_device(0)
@@ -58,6 +59,7 @@ def main():
         "blend_bwd": lambda: render_blend_bwd(state, img, nc, gimg, 1.0, s),
         "blend_nc": lambda: render_blend(state, img, tf, nc, stream=s),
         "blend_bwd_loss": lambda: render_blend_bwd_loss(state, img, obs, 0, 1.0 / (3 * h * w), loss.ptr(0), s),
+        "blend_fused": lambda: render_blend_fused_loss(state, obs, 0, 1.0 / (3 * h * w), loss.ptr(0), s),
         "chain": lambda: render_chain(state, grads, None, s),
     }
     for f in passes.values():
