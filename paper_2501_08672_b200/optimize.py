@@ -339,16 +339,15 @@ class WindowEngine:
             if host:
                 sm.wait_event(copied[v])
                 obs = self.obs_dev[v]
-            mark("blend_fwd", sm)
             if self.fused_blend:
                 # forward + loss + backward in one kernel
+                mark("blend", sm)
                 render_blend_fused_loss(st, obs, _KIND[self.cfg.loss], gscale, self.loss.ptr(v), stream=sm)
-                mark("blend_fwd", sm)
-                mark("blend_bwd", sm)
-                mark("blend_bwd", sm)
+                mark("blend", sm)
             elif self.loss_in_backward:
                 # count-free forward; the photometric loss and dL/dI are formed
                 # inside the backward, which reads the observed image
+                mark("blend_fwd", sm)
                 render_blend(st, ln.image, ln.t_final, None, stream=sm)
                 mark("blend_fwd", sm)
                 mark("blend_bwd", sm)
@@ -356,6 +355,7 @@ class WindowEngine:
                 mark("blend_bwd", sm)
             else:
                 # count-free forward with the loss fused into its epilogue
+                mark("blend_fwd", sm)
                 render_blend_loss(st, ln.image, ln.t_final, None, obs, _KIND[self.cfg.loss],
                                   gscale, ln.grad_image, self.loss.ptr(v), stream=sm)
                 mark("blend_fwd", sm)
