@@ -56,15 +56,6 @@ constexpr int RUN = 4;       // pixels per lane and row (horizontal run)
 #ifndef BWD_MIN_BLOCKS
 #define BWD_MIN_BLOCKS 4
 #endif
-#ifndef STATIC_FIRST_TILE
-#define STATIC_FIRST_TILE 1
-#endif
-#ifndef BWD_LOSS_VARIANT
-#define BWD_LOSS_VARIANT 0
-#endif
-#ifndef BLEND_RESERVE          // CTA slots per SM the persistent blend grids leave free
-#define BLEND_RESERVE 0           // (for a concurrent view lane's binning / chain kernels)
-#endif
 
 struct BlendArgs {
     int W, H;
@@ -313,24 +304,17 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
     RecPipe pipe;
     pipe.buf = s_rec[wib];
     const float kap = a.clamp;
-    // persistent tile-warp: pull tiles from the queue (heaviest first) until
-    // it is empty.  (Claiming the next slot early, to hide the atomic, costs
-    // more in lost load balance than it saves: measured +25% on config 2.)
-#if STATIC_FIRST_TILE
-    // first tile: the warp's own slot of the (heaviest-first) order, no
-    // atomic; later tiles from the queue, which starts after the first wave
+    // persistent tile-warp: the first tile is the warp's own slot of the
+    // heaviest-first order (no atomic), later ones come from the queue,
+    // which starts after the first wave.  (Claiming the next slot early, to
+    // hide the atomic, costs more in load balance than it saves: +25%.)
     int q0 = blockIdx.x * WPB + wib;
     const int nwarps = gridDim.x * WPB;
-#endif
     for (;;) {
         int tile = 0;
         if (lane == 0) {
-#if STATIC_FIRST_TILE
             const int q = q0 >= 0 ? q0 : (int)atomicAdd(&w.ctr[7], 1ull) + nwarps;
             q0 = -1;
-#else
-            const int q = (int)atomicAdd(&w.ctr[7], 1ull);
-#endif
             tile = q < w.ntiles ? w.tile_order[q] : -1;
         }
         tile = __shfl_sync(0xffffffffu, tile, 0);
@@ -606,21 +590,15 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __r
     const int qx = (lane & 3) * RUN, r0 = lane >> 2;
     RecPipe pipe;
     pipe.buf = s_rec[wib];
-#if STATIC_FIRST_TILE
     // first tile: the warp's own slot of the (heaviest-first) order, no
     // atomic; later tiles from the queue, which starts after the first wave
     int q0 = blockIdx.x * WPB + wib;
     const int nwarps = gridDim.x * WPB;
-#endif
     for (;;) {
         int tile = 0;
         if (lane == 0) {
-#if STATIC_FIRST_TILE
             const int q = q0 >= 0 ? q0 : (int)atomicAdd(&w.ctr[8], 1ull) + nwarps;
             q0 = -1;
-#else
-            const int q = (int)atomicAdd(&w.ctr[8], 1ull);
-#endif
             tile = q < w.ntiles ? w.tile_order[q] : -1;
         }
         tile = __shfl_sync(0xffffffffu, tile, 0);
@@ -649,7 +627,6 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __r
                         const float i3[3] = {i0, i1, i2};
 #pragma unroll
                         for (int c = 0; c < 3; ++c) {
-#if BWD_LOSS_VARIANT == 0
                             const double d = (double)i3[c] - (double)L.observed[3 * p + c];
                             l1 += d * d;
                             if (L.kind == 0) {
@@ -659,15 +636,6 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __r
                                 l0 += d * d;
                                 g3[c] = (float)(2.0 * d * (double)L.gscale);
                             }
-#elif BWD_LOSS_VARIANT == 1
-                            const float d = i3[c] - L.observed[3 * p + c];
-                            l1 += (double)(d * d);
-                            l0 += (double)fabsf(d);
-                            g3[c] = d > 0.f ? L.gscale : (d < 0.f ? -L.gscale : 0.f);
-#else
-                            const float d = i3[c] - L.observed[3 * p + c];
-                            g3[c] = d > 0.f ? L.gscale : (d < 0.f ? -L.gscale : 0.f);
-#endif
                         }
                     } else {
 #pragma unroll
@@ -709,7 +677,7 @@ static int persistent_grid(const void* fn, int ntiles) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * WPB, 0);
     const int need = (ntiles + WPB - 1) / WPB;
-    const int g = sms * (per_sm > BLEND_RESERVE ? per_sm - BLEND_RESERVE : 1);
+    const int g = sms * (per_sm > 0 ? per_sm : 1);
     return g < need ? g : need;
 }
 

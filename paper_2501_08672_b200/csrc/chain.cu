@@ -77,40 +77,6 @@ __device__ void sh_basis_grad_d(int degree, T x, T y, T z, T (*g)[3]) {
     }
 }
 
-// Per visible splat, the sum of its intersections' partials (one warp per
-// splat, lanes stride over the intersections, fixed-order butterfly).
-__global__ void __launch_bounds__(256) k_part_reduce(Ws w) {
-    const int64_t M = (int64_t)w.ctr[0];
-    const int lane = threadIdx.x & 31;
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t slot = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; slot < M; slot += nw) {
-        const Rec& r = w.rec[slot];
-        if (r.ebase < 0) continue;
-        const int nt = w.vis_ebase[slot + 1] - r.ebase;      // this splat's intersections
-        double q[NUM_PART];
-#pragma unroll
-        for (int c = 0; c < NUM_PART; ++c) q[c] = 0.0;
-        for (int k = lane; k < nt; k += 32) {
-            const float* src = w.part + (int64_t)(r.ebase + k) * NUM_PART;
-#pragma unroll
-            for (int c = 0; c < NUM_PART; ++c) q[c] += (double)src[c];
-        }
-#pragma unroll
-        for (int c = 0; c < NUM_PART; ++c) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) q[c] += __shfl_xor_sync(0xffffffffu, q[c], o);
-        }
-        double v = q[0];
-#pragma unroll
-        for (int c = 1; c < NUM_PART; ++c) v = (lane == c) ? q[c] : v;
-        if (lane < NUM_PART) w.qsum[slot * NUM_PART + lane] = v;
-    }
-}
-
-#ifndef CHAIN_FUSED_REDUCE      // sum a splat's partials inside k_chain (1) or in k_part_reduce (0)
-#define CHAIN_FUSED_REDUCE 1
-#endif
-
 using CT = double;  // chain-rule arithmetic: f64 keeps Adam's sign-sensitive first steps on the reference trajectory
 
 __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
@@ -127,7 +93,6 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
         const Rec& r = w.rec[slot];
         if (r.ebase < 0) continue;
         double q[NUM_PART];
-#if CHAIN_FUSED_REDUCE
         // the splat's intersection partials (contiguous, e in [ebase, ebase + nt)),
         // summed in e order
 #pragma unroll
@@ -143,10 +108,6 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
                 for (int c = 0; c < NUM_PART; ++c) q[c] += (double)v[c];
             }
         }
-#else
-#pragma unroll
-        for (int c = 0; c < NUM_PART; ++c) q[c] = w.qsum[slot * NUM_PART + c];
-#endif
         bool nz = false;
 #pragma unroll
         for (int c = 0; c < NUM_PART; ++c) nz |= (q[c] != 0.0);
@@ -323,7 +284,6 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
 cudaError_t launch_chain(const Ws& w, const lsb_params& p, const lsb_grads& g, const lsb_camera& cam,
                          const lsb_pose& T, const lsb_settings& s, double* pose_out,
                          cudaStream_t st) {
-    if (!CHAIN_FUSED_REDUCE) k_part_reduce<<<4 * 148, 256, 0, st>>>(w);
     ChainArgs a{p, g, cam, T, 0, pose_out};
     int deg_store = 0;
     while ((deg_store + 2) * (deg_store + 2) <= p.sh_coeffs) ++deg_store;

@@ -64,7 +64,6 @@ struct Ws {
     int32_t* vis_ebase;         // [n + 1] first intersection of each visible slot (exclusive scan)
     int32_t* big_tiles;         // [ntiles] tiles queued for the shared-memory sort
     int32_t* tile_order;        // [ntiles] blend processing order: heaviest tiles first
-    double* qsum;               // [n * NUM_PART] per-splat sums of the intersection partials
     CullGeo* cgeo;              // [n] alpha_cut ellipses (bin_mode 1 only)
     int64_t n, cap;
     int32_t ntx, nty, ntiles, nblocks_pre;
@@ -113,7 +112,6 @@ inline size_t carve(const lsb_dims& d, char* base, Ws* w) {
     t.vis_ebase = (int32_t*)take(sizeof(int32_t) * (n + 1));
     t.big_tiles = (int32_t*)take(sizeof(int32_t) * t.ntiles);
     t.tile_order = (int32_t*)take(sizeof(int32_t) * t.ntiles);
-    t.qsum = (double*)take(sizeof(double) * NUM_PART * n);
     t.cgeo = (CullGeo*)take(sizeof(CullGeo) * n);
     if (w) *w = t;
     return off;
