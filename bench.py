@@ -401,9 +401,9 @@ def run_ours(args, wl, rank, world, local_rank):
             "clocks": clk_sum,
             "e2e": {"value": V * W * H / (e_ms * 1e-3) / 1e6, "unit": "Mpix/s",
                     "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world, "ms_per_step": e_ms},
-            "gpu_launches": args.steps * (len(my_views) * 8 + 2) + 1,   # per view: preprocess, scan, scatter,
-            # tile sort, big-tile sort, fused blend (fwd + loss + bwd), loss total, chain; + adam and step
-            # counter per step; + final orthonormalize
+            "gpu_launches": args.steps * (len(my_views) * 10 + 2) + 1,   # per view: preprocess count / scan /
+            # emit, tile scan, scatter, tile sort, big-tile sort, fused blend (fwd + loss + bwd), loss total,
+            # chain; + adam and step counter per step; + final orthonormalize
         }
         if world == 1 and not args.no_cpu_baseline:
             tv, ta, cores = cpu_sample(wl, 2)

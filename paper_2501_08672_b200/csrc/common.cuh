@@ -45,7 +45,6 @@ struct CullGeo {
 struct Ws {
     unsigned long long* ctr;    // [0] M, [1] I, [2] overflow, [3] preprocess ticket, [4] chain ticket,
                                 // [5] fused-loss tiles done, [6] big-tile count, [7] fwd / [8] bwd tile queues
-    unsigned long long* scan;   // chained-scan state: 2 words per preprocess block
     Rec* rec;                   // [n] (only the first M are live)
     uint64_t* vkey;             // [n] depth bits of live splats
     uint32_t* colmask;          // [n] interior bits (3) of live splats
@@ -65,6 +64,9 @@ struct Ws {
     int32_t* big_tiles;         // [ntiles] tiles queued for the shared-memory sort
     int32_t* tile_order;        // [ntiles] blend processing order: heaviest tiles first
     CullGeo* cgeo;              // [n] alpha_cut ellipses (bin_mode 1 only)
+    uint32_t* warp_mask;        // [ceil(n/32)] visible lanes per preprocess warp
+    int32_t* warp_cnt;          // [2 ceil(n/32)] visible count, tile count per warp
+    int32_t* warp_off;          // [2 ceil(n/32)] their exclusive scans
     int64_t n, cap;
     int32_t ntx, nty, ntiles, nblocks_pre;
 };
@@ -90,9 +92,8 @@ inline size_t carve(const lsb_dims& d, char* base, Ws* w) {
     };
     const size_t n = (size_t)(d.n > 0 ? d.n : 1);
     const size_t cap = (size_t)(d.isect_cap > 0 ? d.isect_cap : 1);
-    // zeroed prefix: counters, scan flags, tile histogram, tile cursors
+    // zeroed prefix: counters, tile histogram, tile cursors
     t.ctr = (unsigned long long*)take(16 * sizeof(unsigned long long));
-    t.scan = (unsigned long long*)take(2 * sizeof(unsigned long long) * (size_t)t.nblocks_pre);
     t.tile_count = (int32_t*)take(sizeof(int32_t) * t.ntiles);
     t.tile_cursor = (int32_t*)take(sizeof(int32_t) * t.ntiles);
     // not zeroed
@@ -113,12 +114,16 @@ inline size_t carve(const lsb_dims& d, char* base, Ws* w) {
     t.big_tiles = (int32_t*)take(sizeof(int32_t) * t.ntiles);
     t.tile_order = (int32_t*)take(sizeof(int32_t) * t.ntiles);
     t.cgeo = (CullGeo*)take(sizeof(CullGeo) * n);
+    const size_t nw = (n + 31) / 32;
+    t.warp_mask = (uint32_t*)take(sizeof(uint32_t) * nw);
+    t.warp_cnt = (int32_t*)take(sizeof(int32_t) * 2 * nw);
+    t.warp_off = (int32_t*)take(sizeof(int32_t) * 2 * nw);
     if (w) *w = t;
     return off;
 }
 
 // Bytes of the workspace prefix that must be zeroed before a render
-// (counters, chained-scan flags, tile histograms).
+// (counters, tile histograms).
 inline size_t zero_prefix_bytes(const Ws& w) {
     return (size_t)((char*)w.tile_start - (char*)w.ctr);
 }

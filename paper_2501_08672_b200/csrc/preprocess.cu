@@ -109,6 +109,7 @@ __device__ __forceinline__ void sh_basis(int degree, double x, double y, double 
 
 // Projection + EWA covariance + footprint (raster.py:134-185) for Gaussian i.
 // Returns false if culled; fills the record, its tile count and depth key.
+template <bool FULL = true>
 __device__ bool splat_one(const PreArgs& a, int64_t i, Rec& r, int& ntiles, uint64_t& key,
                           uint32_t& cmask, CullGeo& geo) {
     const int f64 = a.p.dtype;
@@ -209,6 +210,7 @@ __device__ bool splat_one(const PreArgs& a, int64_t i, Rec& r, int& ntiles, uint
     } else {
         ntiles = (((ix1 - 1) >> 4) - (ix0 >> 4) + 1) * (((iy1 - 1) >> 4) - (iy0 >> 4) + 1);
     }
+    if (!FULL) return true;       // counting pass: visibility and tile count only
     // conic = cov_i^-1 = (cc, -cb, ca) / det; exponent in the shear form
     //   q = a_k u^2 + dy^2 / cc,  u = dx - (cb/cc) dy   (no cancellation)
     const double ak = cc / det;
@@ -260,111 +262,13 @@ __device__ bool splat_one(const PreArgs& a, int64_t i, Rec& r, int& ntiles, uint
     return true;
 }
 
-constexpr unsigned long long ST_AGG = 1ull << 62, ST_INC = 2ull << 62, VAL_MASK = (1ull << 62) - 1;
-
-// Decoupled look-back for one running total (chained scan, single pass),
-// one warp: the 32 nearest predecessors are inspected per round, so a block
-// needs ~1 round trip to L2 instead of one per predecessor.
-__device__ unsigned long long warp_lookback(unsigned long long* flags, int blk, unsigned long long agg,
-                                            int lane) {
-    if (blk == 0) {
-        if (lane == 0) atomicExch(&flags[0], ST_INC | agg);
-        return 0;
-    }
-    if (lane == 0) atomicExch(&flags[blk], ST_AGG | agg);
-    unsigned long long excl = 0;
-    int j = blk - 1;
-    while (true) {
-        const int idx = j - lane;
-        unsigned long long v;
-        do {
-            v = idx >= 0 ? *((volatile unsigned long long*)&flags[idx]) : (2ull << 62);   // before block 0: inclusive 0
-        } while (!__all_sync(0xffffffffu, (v & ~VAL_MASK) != 0));
-        const unsigned inc = __ballot_sync(0xffffffffu, (v & ~VAL_MASK) == ST_INC);
-        const int first = inc ? __ffs(inc) - 1 : 31;      // nearest predecessor with an inclusive prefix
-        unsigned long long x = lane <= first ? (v & VAL_MASK) : 0ull;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        excl += x;
-        if (inc) break;
-        j -= 32;
-    }
-    if (lane == 0) atomicExch(&flags[blk], ST_INC | (excl + agg));
-    return excl;
-}
-
-// K1: one thread per Gaussian.  Visible splats are compacted in ascending id
-// order (chained scan with decoupled look-back), so slot order == the
-// reference's np.nonzero order and (depth, slot) ties break exactly as its
-// stable argsort (raster.py:221).  Each visible splat also reserves a
-// contiguous run of intersection indices and bumps the per-tile histogram.
 #ifndef PRE_MIN_BLOCKS
 #define PRE_MIN_BLOCKS 1
 #endif
-__global__ void __launch_bounds__(PRE_THREADS, PRE_MIN_BLOCKS)
-k_preprocess(PreArgs a, Ws w) {
-    __shared__ unsigned long long s_blk;
-    __shared__ int s_wv[PRE_THREADS / 32], s_wt[PRE_THREADS / 32];
-    __shared__ unsigned long long s_base_v, s_base_t;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_blk = atomicAdd(&w.ctr[3], 1ull);
-    __syncthreads();
-    const int blk = (int)s_blk;
-    const int64_t i = (int64_t)blk * PRE_THREADS + tid;
-    Rec r;
-    int nt = 0;
-    uint64_t key = 0;
-    uint32_t cm = 0;
-    CullGeo geo;
-    const bool vis = (i < a.p.n) && splat_one(a, i, r, nt, key, cm, geo);
-    int v = vis ? 1 : 0;
-    int tcount = vis ? nt : 0;
-    // block-wide exclusive scan of (v, tcount)
-    int iv = v, it = tcount;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int nv = __shfl_up_sync(0xffffffffu, iv, o);
-        const int ntt = __shfl_up_sync(0xffffffffu, it, o);
-        if (lane >= o) {
-            iv += nv;
-            it += ntt;
-        }
-    }
-    if (lane == 31) {
-        s_wv[warp] = iv;
-        s_wt[warp] = it;
-    }
-    __syncthreads();
-    int wv = 0, wt = 0, totv = 0, tott = 0;
-#pragma unroll
-    for (int k = 0; k < PRE_THREADS / 32; ++k) {
-        if (k < warp) {
-            wv += s_wv[k];
-            wt += s_wt[k];
-        }
-        totv += s_wv[k];
-        tott += s_wt[k];
-    }
-    if (warp == 0) {
-        const unsigned long long b = warp_lookback(w.scan, blk, (unsigned long long)totv, lane);
-        if (lane == 0) s_base_v = b;
-    } else if (warp == 1) {
-        const unsigned long long b = warp_lookback(w.scan + w.nblocks_pre, blk, (unsigned long long)tott, lane);
-        if (lane == 0) s_base_t = b;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        if (blk == w.nblocks_pre - 1) {
-            w.ctr[0] = s_base_v + totv;
-            w.ctr[1] = s_base_t + tott;
-            w.vis_ebase[s_base_v + totv] = (int32_t)min(s_base_t + tott, 0x7fffffffull);
-            if (s_base_t + tott > (unsigned long long)w.cap) w.ctr[2] = 1;
-        }
-    }
-    __syncthreads();
-    if (!vis) return;
-    const int64_t slot = (int64_t)(s_base_v + wv + iv - v);
-    const int64_t e0 = (int64_t)(s_base_t + wt + it - tcount);
+// Write a visible splat's record, key and intersections (slot, first
+// intersection e0), and bump the tile histogram.
+__device__ __forceinline__ void emit_splat(const PreArgs& a, const Ws& w, Rec& r, int64_t slot, int64_t e0, int nt,
+                                           uint64_t key, uint32_t cm, const CullGeo& geo) {
     const bool fits = e0 + nt <= w.cap;
     r.ebase = fits ? (int32_t)e0 : -1;
     w.rec[slot] = r;
@@ -724,6 +628,118 @@ __global__ void __launch_bounds__(256) k_tile_sort_big(Ws w) {
 
 size_t tile_sort_smem() { return SORT_CAP * (sizeof(uint64_t) + 2 * sizeof(int)); }
 
+// ---- barrier-free preprocess: count, scan, emit ------------------------------
+// A single-pass preprocess with a chained scan (decoupled look-back) spent
+// ~60% of its stall samples in block barriers and look-back spins, and its
+// spinning CTAs co-ran badly with other views' blends.  Instead: (1) every warp independently computes its 32 Gaussians'
+// visibility and tile counts (no barrier, no record) and writes a ballot
+// mask and two counts; (2) one CTA scans the per-warp counts; (3) warps that
+// hold a visible Gaussian recompute it fully (the same code, so the same
+// bits) and write the records, keys and intersections at their offsets.
+// Slot order is still id order.
+
+__global__ void __launch_bounds__(PRE_THREADS) k_pre_count(PreArgs a, Ws w) {
+    const int64_t i = (int64_t)blockIdx.x * PRE_THREADS + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    Rec r;
+    int nt = 0;
+    uint64_t key = 0;
+    uint32_t cm = 0;
+    CullGeo geo;
+    const bool vis = (i < a.p.n) && splat_one<false>(a, i, r, nt, key, cm, geo);
+    const unsigned mask = __ballot_sync(0xffffffffu, vis);
+    int t = vis ? nt : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) {
+        const int64_t wid = i >> 5;
+        w.warp_mask[wid] = mask;
+        w.warp_cnt[2 * wid] = __popc(mask);
+        w.warp_cnt[2 * wid + 1] = t;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_pre_scan(Ws w, int64_t nw) {
+    __shared__ long long s_v[32], s_t[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t per = (nw + 1023) / 1024, b0 = tid * per;
+    long long sv = 0, st = 0;
+    for (int64_t k = 0; k < per; ++k)
+        if (b0 + k < nw) {
+            sv += w.warp_cnt[2 * (b0 + k)];
+            st += w.warp_cnt[2 * (b0 + k) + 1];
+        }
+    long long xv = sv, xt = st;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long yv = __shfl_up_sync(0xffffffffu, xv, o), yt = __shfl_up_sync(0xffffffffu, xt, o);
+        if (lane >= o) {
+            xv += yv;
+            xt += yt;
+        }
+    }
+    if (lane == 31) {
+        s_v[warp] = xv;
+        s_t[warp] = xt;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        long long yv = s_v[lane], yt = s_t[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long zv = __shfl_up_sync(0xffffffffu, yv, o), zt = __shfl_up_sync(0xffffffffu, yt, o);
+            if (lane >= o) {
+                yv += zv;
+                yt += zt;
+            }
+        }
+        s_v[lane] = yv;
+        s_t[lane] = yt;
+    }
+    __syncthreads();
+    long long rv = xv - sv + (warp > 0 ? s_v[warp - 1] : 0), rt = xt - st + (warp > 0 ? s_t[warp - 1] : 0);
+    for (int64_t k = 0; k < per; ++k)
+        if (b0 + k < nw) {
+            w.warp_off[2 * (b0 + k)] = (int32_t)rv;
+            w.warp_off[2 * (b0 + k) + 1] = (int32_t)min(rt, 0x7fffffffll);
+            rv += w.warp_cnt[2 * (b0 + k)];
+            rt += w.warp_cnt[2 * (b0 + k) + 1];
+        }
+    if (tid == 1023) {
+        w.ctr[0] = (unsigned long long)rv;
+        w.ctr[1] = (unsigned long long)rt;
+        w.vis_ebase[rv] = (int32_t)min(rt, 0x7fffffffll);
+        if (rt > w.cap) w.ctr[2] = 1;
+    }
+}
+
+__global__ void __launch_bounds__(PRE_THREADS, PRE_MIN_BLOCKS) k_pre_emit(PreArgs a, Ws w) {
+    const int64_t i = (int64_t)blockIdx.x * PRE_THREADS + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = i >> 5;
+    if (wid * 32 >= a.p.n) return;
+    const unsigned mask = w.warp_mask[wid];
+    if (mask == 0) return;                                   // warp-uniform
+    const bool mine = (mask >> lane) & 1u;
+    Rec r;
+    int nt = 0;
+    uint64_t key = 0;
+    uint32_t cm = 0;
+    CullGeo geo;
+    if (mine) splat_one<true>(a, i, r, nt, key, cm, geo);   // visible: the counting pass said so
+    int ex = mine ? nt : 0;                                  // exclusive scan of nt over the warp
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, ex, o);
+        if (lane >= o) ex += y;
+    }
+    ex -= mine ? nt : 0;
+    if (!mine) return;
+    const int64_t slot = (int64_t)w.warp_off[2 * wid] + __popc(mask & ((1u << lane) - 1u));
+    const int64_t e0 = (int64_t)w.warp_off[2 * wid + 1] + ex;
+    emit_splat(a, w, r, slot, e0, nt, key, cm, geo);
+}
+
 cudaError_t launch_preprocess(const lsb_params& p, const lsb_camera& cam, const lsb_pose& T,
                               const lsb_settings& s, const Ws& w, cudaStream_t st) {
     PreArgs a{p, cam, T, s, 0, (s.bin_mode == 1 && s.alpha_cut > 0.0) ? 1 : 0};
@@ -732,7 +748,13 @@ cudaError_t launch_preprocess(const lsb_params& p, const lsb_camera& cam, const 
     a.degree = s.sh_degree < deg_store ? s.sh_degree : deg_store;
     cudaError_t err = cudaMemsetAsync(w.ctr, 0, zero_prefix_bytes(w), st);
     if (err != cudaSuccess) return err;
-    k_preprocess<<<w.nblocks_pre, PRE_THREADS, 0, st>>>(a, w);
+    {
+        const int64_t nw = (p.n + 31) / 32;
+        const unsigned nb = (unsigned)((p.n + PRE_THREADS - 1) / PRE_THREADS);
+        if (p.n > 0) k_pre_count<<<nb, PRE_THREADS, 0, st>>>(a, w);
+        k_pre_scan<<<1, 1024, 0, st>>>(w, nw);
+        if (p.n > 0) k_pre_emit<<<nb, PRE_THREADS, 0, st>>>(a, w);
+    }
     if (w.ntiles > 1024 * SCAN_PER) return cudaErrorInvalidValue;     // > 16 K tiles: image too large
     k_scan_tiles<<<1, 1024, 0, st>>>(w);
     k_scatter_emitted<<<8 * 148, 256, 0, st>>>(w);

@@ -36,7 +36,7 @@ METRICS = [
     ("gpc__cycles_elapsed.max", "elapsed_cyc"),
 ]
 
-KEY = {"k_blend_fused": "blend", "k_blend_bwd": "blend_bwd", "k_blend_fwd": "blend_fwd", "k_preprocess": "bin",
+KEY = {"k_blend_fused": "blend", "k_blend_bwd": "blend_bwd", "k_blend_fwd": "blend_fwd", "k_preprocess": "bin", "k_pre_count": "bin",
        "k_chain": "chain",
        "k_adam": "adam", "k_tile_sort": "bin"}
 
