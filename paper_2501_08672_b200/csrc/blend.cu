@@ -671,13 +671,15 @@ static BlendArgs blend_args(const lsb_settings& s, int W, int H) {
 }
 
 // CTAs to launch for a persistent tile-warp kernel: every resident slot once.
-static int persistent_grid(const void* fn, int ntiles) {
+// `reserve` CTA slots per SM are left free for concurrent kernels (the
+// window engine's other view lanes: binning and chain co-run with the blend).
+static int persistent_grid(const void* fn, int ntiles, int reserve = 0) {
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * WPB, 0);
     const int need = (ntiles + WPB - 1) / WPB;
-    const int g = sms * (per_sm > 0 ? per_sm : 1);
+    const int g = sms * (per_sm > reserve ? per_sm - reserve : 1);
     return g < need ? g : need;
 }
 
@@ -823,10 +825,11 @@ cudaError_t launch_blend_fused(const Ws& w, const lsb_settings& s, int W, int H,
     if (e != cudaSuccess) return e;
     const LossArgs L{observed, nullptr, w.loss_part, loss_out, nullptr, kind, grad_scale};
     if (s.alpha_cut > 0.0)
-        k_blend_fused<true><<<persistent_grid((const void*)k_blend_fused<true>, w.ntiles), 32 * WPB, 0, st>>>(w, a, L);
+        k_blend_fused<true><<<persistent_grid((const void*)k_blend_fused<true>, w.ntiles, 1), 32 * WPB, 0, st>>>(w, a,
+                                                                                                                L);
     else
-        k_blend_fused<false><<<persistent_grid((const void*)k_blend_fused<false>, w.ntiles), 32 * WPB, 0, st>>>(w, a,
-                                                                                                             L);
+        k_blend_fused<false><<<persistent_grid((const void*)k_blend_fused<false>, w.ntiles, 1), 32 * WPB, 0, st>>>(
+            w, a, L);
     k_loss_total<<<1, LT_THREADS, 0, st>>>(w.ntiles, w.loss_part, loss_out);
     return cudaGetLastError();
 }
