@@ -11,7 +11,7 @@ constexpr int TILE = 16;
 constexpr int NUM_PART = 9;          // d_color(3), d_opac, d_mean2d(2), d_cov2d(3)
 constexpr int POSE_VALS = 9;         // rho_cam(3), tau_cam(3), d_cam_center(3)
 #ifndef LSB_PRE_THREADS
-#define LSB_PRE_THREADS 256
+#define LSB_PRE_THREADS 128
 #endif
 constexpr int PRE_THREADS = LSB_PRE_THREADS;     // preprocess block size
 constexpr int PRE_ITEMS = 1;         // Gaussians per preprocess thread

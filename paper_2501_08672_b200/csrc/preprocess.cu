@@ -301,21 +301,17 @@ __device__ __forceinline__ void emit_splat(const PreArgs& a, const Ws& w, Rec& r
         }
 }
 
-// Exclusive scan of the tile histogram (single CTA, one pass: each thread
-// owns a run of SCAN_PER consecutive tiles).
-constexpr int SCAN_PER = 16;      // tiles per thread: 16 K tiles (4K x 4K px) per CTA
-__global__ void __launch_bounds__(1024) k_scan_tiles(Ws w) {
-    __shared__ int s_w[32];
+// Exclusive scan of the tile histogram (single CTA; each thread owns a run of
+// consecutive tiles, re-read from L2 instead of held in registers).
+constexpr int ST_THREADS = 1024;
+__global__ void __launch_bounds__(ST_THREADS) k_scan_tiles(Ws w) {
+    __shared__ int s_w[ST_THREADS / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int per = (w.ntiles + 1023) / 1024;     // <= SCAN_PER (checked at launch)
+    const int per = (w.ntiles + ST_THREADS - 1) / ST_THREADS;
     const int b0 = tid * per;
-    int v[SCAN_PER];
     int sum = 0;
-#pragma unroll
-    for (int i = 0; i < SCAN_PER; ++i) {
-        v[i] = (i < per && b0 + i < w.ntiles) ? w.tile_count[b0 + i] : 0;
-        sum += v[i];
-    }
+    for (int i = 0; i < per; ++i)
+        if (b0 + i < w.ntiles) sum += w.tile_count[b0 + i];
     int x = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -324,64 +320,52 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(Ws w) {
     }
     if (lane == 31) s_w[warp] = x;
     __syncthreads();
-    if (warp == 0) {
-        int y = s_w[lane];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int z = __shfl_up_sync(0xffffffffu, y, o);
-            if (lane >= o) y += z;
+    int before = 0;
+    for (int k = 0; k < warp; ++k) before += s_w[k];
+    int run = x - sum + before;
+    for (int i = 0; i < per; ++i)
+        if (b0 + i < w.ntiles) {
+            w.tile_start[b0 + i] = run;
+            run += w.tile_count[b0 + i];
         }
-        s_w[lane] = y;
-    }
-    __syncthreads();
-    int run = x - sum + (warp > 0 ? s_w[warp - 1] : 0);
-#pragma unroll
-    for (int i = 0; i < SCAN_PER; ++i) {
-        if (i < per && b0 + i < w.ntiles) w.tile_start[b0 + i] = run;
-        run += v[i];
-    }
-    if (tid == 1023) w.tile_start[w.ntiles] = run;
+    if (tid == ST_THREADS - 1) w.tile_start[w.ntiles] = run;
     // Processing order of the persistent blend kernels: a counting sort of
     // the tiles by descending list length (4-entry buckets), so the longest
     // tiles start first and the tail of the tile queue is short work.
+    // (warp-aggregated: most tiles share a few buckets, and same-address
+    // shared atomics serialise)
     __shared__ int s_hist[256];
     if (tid < 256) s_hist[tid] = 0;
     __syncthreads();
     auto key = [](int c) { return 255 - min(c >> 2, 255); };
-    // (warp-aggregated: most tiles share a few buckets, and same-address
-    // shared atomics serialise)
-#pragma unroll
-    for (int i = 0; i < SCAN_PER; ++i) {
-        if (i >= per) break;
+    for (int i = 0; i < per; ++i) {
         const bool ok = b0 + i < w.ntiles;
-        const int k = ok ? key(v[i]) : -1;
+        const int k = ok ? key(w.tile_count[b0 + i]) : -1;
         const unsigned grp = __match_any_sync(0xffffffffu, k);
         if (ok && lane == __ffs(grp) - 1) atomicAdd(&s_hist[k], __popc(grp));
     }
     __syncthreads();
     if (warp == 0) {
-        int loc[8], sum = 0;
+        int loc[8], tot = 0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            loc[i] = sum;
-            sum += s_hist[8 * lane + i];
+            loc[i] = tot;
+            tot += s_hist[8 * lane + i];
         }
-        int x = sum;
+        int y = tot;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
+            const int z = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += z;
         }
-        const int excl = x - sum;
+        const int excl = y - tot;
 #pragma unroll
         for (int i = 0; i < 8; ++i) s_hist[8 * lane + i] = excl + loc[i];
     }
     __syncthreads();
-#pragma unroll
-    for (int i = 0; i < SCAN_PER; ++i) {
-        if (i >= per) break;
+    for (int i = 0; i < per; ++i) {
         const bool ok = b0 + i < w.ntiles;
-        const int k = ok ? key(v[i]) : -1;
+        const int k = ok ? key(w.tile_count[b0 + i]) : -1;
         const unsigned grp = __match_any_sync(0xffffffffu, k);
         const int leader = __ffs(grp) - 1;
         int base = 0;
@@ -659,10 +643,11 @@ __global__ void __launch_bounds__(PRE_THREADS) k_pre_count(PreArgs a, Ws w) {
     }
 }
 
-__global__ void __launch_bounds__(1024) k_pre_scan(Ws w, int64_t nw) {
-    __shared__ long long s_v[32], s_t[32];
+constexpr int PS_THREADS = 1024;
+__global__ void __launch_bounds__(PS_THREADS) k_pre_scan(Ws w, int64_t nw) {
+    __shared__ long long s_v[PS_THREADS / 32], s_t[PS_THREADS / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t per = (nw + 1023) / 1024, b0 = tid * per;
+    const int64_t per = (nw + PS_THREADS - 1) / PS_THREADS, b0 = tid * per;
     long long sv = 0, st = 0;
     for (int64_t k = 0; k < per; ++k)
         if (b0 + k < nw) {
@@ -683,21 +668,12 @@ __global__ void __launch_bounds__(1024) k_pre_scan(Ws w, int64_t nw) {
         s_t[warp] = xt;
     }
     __syncthreads();
-    if (warp == 0) {
-        long long yv = s_v[lane], yt = s_t[lane];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const long long zv = __shfl_up_sync(0xffffffffu, yv, o), zt = __shfl_up_sync(0xffffffffu, yt, o);
-            if (lane >= o) {
-                yv += zv;
-                yt += zt;
-            }
-        }
-        s_v[lane] = yv;
-        s_t[lane] = yt;
+    long long bv = 0, bt = 0;
+    for (int k = 0; k < warp; ++k) {
+        bv += s_v[k];
+        bt += s_t[k];
     }
-    __syncthreads();
-    long long rv = xv - sv + (warp > 0 ? s_v[warp - 1] : 0), rt = xt - st + (warp > 0 ? s_t[warp - 1] : 0);
+    long long rv = xv - sv + bv, rt = xt - st + bt;
     for (int64_t k = 0; k < per; ++k)
         if (b0 + k < nw) {
             w.warp_off[2 * (b0 + k)] = (int32_t)rv;
@@ -705,7 +681,7 @@ __global__ void __launch_bounds__(1024) k_pre_scan(Ws w, int64_t nw) {
             rv += w.warp_cnt[2 * (b0 + k)];
             rt += w.warp_cnt[2 * (b0 + k) + 1];
         }
-    if (tid == 1023) {
+    if (tid == PS_THREADS - 1) {
         w.ctr[0] = (unsigned long long)rv;
         w.ctr[1] = (unsigned long long)rt;
         w.vis_ebase[rv] = (int32_t)min(rt, 0x7fffffffll);
@@ -752,11 +728,10 @@ cudaError_t launch_preprocess(const lsb_params& p, const lsb_camera& cam, const 
         const int64_t nw = (p.n + 31) / 32;
         const unsigned nb = (unsigned)((p.n + PRE_THREADS - 1) / PRE_THREADS);
         if (p.n > 0) k_pre_count<<<nb, PRE_THREADS, 0, st>>>(a, w);
-        k_pre_scan<<<1, 1024, 0, st>>>(w, nw);
+        k_pre_scan<<<1, PS_THREADS, 0, st>>>(w, nw);
         if (p.n > 0) k_pre_emit<<<nb, PRE_THREADS, 0, st>>>(a, w);
     }
-    if (w.ntiles > 1024 * SCAN_PER) return cudaErrorInvalidValue;     // > 16 K tiles: image too large
-    k_scan_tiles<<<1, 1024, 0, st>>>(w);
+    k_scan_tiles<<<1, ST_THREADS, 0, st>>>(w);
     k_scatter_emitted<<<8 * 148, 256, 0, st>>>(w);
     k_tile_sort<<<(w.ntiles + 3) / 4, 128, 0, st>>>(w);
     cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_sort_smem());
