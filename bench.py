@@ -388,7 +388,7 @@ def run_ours(args, wl, rank, world, local_rank):
                          "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                          "algorithmic_bytes_per_launch": ab[dom], "avg_launch_ms": dom_ms,
                          "note": "blend is FP32-issue bound (SURVEY.md §8(d)); see profiles/"},
-            "issue_roofline": None if not issue else {
+            "issue_roofline": None if not issue or args.config != "cfg2" else {
                 "kernel": dom, "unit": "warp-inst/s", "warp_inst_per_launch": issue["warp_inst_per_launch"],
                 "achieved": issue["warp_inst_per_launch"] / (dom_ms * 1e-3),
                 "peak": 148 * 4 * (clk_sum["sm_mhz"] or 1965.0) * 1e6,
