@@ -272,6 +272,17 @@ int lsb_hb_reduce(const double* rows, const double* z, int64_t m, double inv_sig
 int lsb_semidense_mask(const float* observed, const float* t_final, int32_t width, int32_t height,
                        double grad_thr, double t_max, uint8_t* mask_out, void* stream);
 
+/* Visual measurement selection, on the device with no host round trip
+ * (estimator.py:241-277 after the render): from the semi-dense mask, the
+ * candidate ids ascending, subsampled to `budget` at round(linspace(0, L-1,
+ * budget)); the grey residual obs - image (channel means in f64) kept where
+ * |res| <= gate, in order -> ids_out / res_out (budget entries max);
+ * counts (device, 3 int64) = [candidates L, selected, kept].  scratch:
+ * lsb_visual_select_scratch_bytes(npx, budget) bytes. */
+int64_t lsb_visual_select_scratch_bytes(int64_t npx, int32_t budget);
+int lsb_visual_select(const uint8_t* mask, const float* observed, const float* image, int64_t npx, int32_t budget,
+                      double gate, void* scratch, int32_t* ids_out, double* res_out, int64_t* counts, void* stream);
+
 /* ---- voxel map: replaces HashOctree's batch operations (voxmap.py:99-251)
  * Open-addressing table of octree LEAVES (the octree is implied by its leaf
  * set; parents/roots by floor division).  All arrays are caller-allocated

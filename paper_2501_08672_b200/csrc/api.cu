@@ -33,6 +33,9 @@ cudaError_t launch_pose_rows(const Ws&, const lsb_settings&, int, int, int, cons
                              cudaStream_t);
 cudaError_t launch_hb(const double*, const double*, int64_t, double, double*, double*, cudaStream_t);
 int hb_scratch_doubles();
+cudaError_t launch_visual_select(const uint8_t*, const float*, const float*, int64_t, int, double, void*, int32_t*,
+                                 double*, int64_t*, cudaStream_t);
+int64_t visual_select_scratch_bytes(int64_t, int);
 cudaError_t launch_semidense(const float*, const float*, int, int, double, double, uint8_t*, cudaStream_t);
 cudaError_t launch_vox_keys(const double*, int64_t, double, int64_t*, cudaStream_t);
 cudaError_t launch_vox_insert(const lsb_voxmap&, const double*, int64_t, int, int64_t*, cudaStream_t);
@@ -574,6 +577,19 @@ int lsb_adam_peer_step(const lsb_params* replicas, int32_t n_ranks, int32_t rank
     return check_cuda(launch_adam_peer(replicas, n_ranks, rank, grads, lo, hi, m, v, touched, *cfg, ibc_table,
                                        table_len, step_dev, (cudaStream_t)stream),
                       "adam_peer");
+}
+
+int64_t lsb_visual_select_scratch_bytes(int64_t npx, int32_t budget) {
+    return visual_select_scratch_bytes(npx, budget);
+}
+
+int lsb_visual_select(const uint8_t* mask, const float* observed, const float* image, int64_t npx, int32_t budget,
+                      double gate, void* scratch, int32_t* ids_out, double* res_out, int64_t* counts, void* stream) {
+    if (!mask || !observed || !image || !scratch || !ids_out || !res_out || !counts || npx < 0 || budget < 1)
+        return fail(LSB_EINVAL, "bad argument");
+    return check_cuda(launch_visual_select(mask, observed, image, npx, budget, gate, scratch, ids_out,
+                                           res_out, counts, (cudaStream_t)stream),
+                      "visual_select");
 }
 
 }  // extern "C"

@@ -416,6 +416,145 @@ cudaError_t launch_hb(const double* rows, const double* z, int64_t m, double inv
 
 int hb_scratch_doubles() { return HB_BLOCKS * HB_VALS; }
 
+// Semi-dense selection + photometric residual + gate of the visual
+// measurement on the device, no host round trip (estimator.py:241-277):
+// ids = nonzero(mask) ascending; if more than `budget`, the ones at
+// round(linspace(0, L-1, budget)) (numpy's k * step, half-to-even; the step
+// exceeds 1 so the rounded indices are already unique); gray = channel mean
+// ((r + g) + b) / 3 in f64; res = gray_obs - gray_hat, kept where |res| <=
+// gate, in order.  counts = [L, selected, kept].
+//   k_vs_count : per VS_CHUNK-pixel chunk, the number of mask hits
+//   k_vs_emit  : the chunk's ascending ids at (sum of earlier chunks) + rank
+//   k_vs_select: one CTA — subsample, residuals, gate, ordered compaction
+constexpr int VS_THREADS = 256, VS_PER = 16, VS_CHUNK = VS_THREADS * VS_PER;
+
+__device__ __forceinline__ int vs_block_scan(int v, int& total, int* s_w) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int k = 0; k < nw; ++k) {
+        if (k < warp) before += s_w[k];
+        tot += s_w[k];
+    }
+    total = tot;
+    __syncthreads();
+    return x - v + before;
+}
+
+__device__ __forceinline__ unsigned vs_bits(const uint8_t* mask, int64_t p0, int64_t npx) {
+    unsigned bits = 0;
+    if (p0 + VS_PER <= npx && ((uintptr_t)(mask + p0) & 15) == 0) {
+        const uint4 q = *(const uint4*)(mask + p0);
+        const unsigned w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int i = 0; i < 16; ++i) bits |= (((w[i >> 2] >> (8 * (i & 3))) & 0xffu) != 0u) << i;
+    } else {
+        for (int i = 0; i < VS_PER; ++i)
+            if (p0 + i < npx && mask[p0 + i]) bits |= 1u << i;
+    }
+    return bits;
+}
+
+__global__ void __launch_bounds__(VS_THREADS) k_vs_count(const uint8_t* __restrict__ mask, int64_t npx,
+                                                          int* __restrict__ cnt) {
+    __shared__ int s_w[VS_THREADS / 32];
+    const int64_t p0 = (int64_t)blockIdx.x * VS_CHUNK + (int64_t)threadIdx.x * VS_PER;
+    int tot;
+    vs_block_scan(__popc(vs_bits(mask, p0, npx)), tot, s_w);
+    if (threadIdx.x == 0) cnt[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(VS_THREADS) k_vs_emit(const uint8_t* __restrict__ mask, int64_t npx,
+                                                         const int* __restrict__ cnt, int nchunk,
+                                                         int32_t* __restrict__ ids_all, int* __restrict__ total) {
+    __shared__ int s_w[VS_THREADS / 32];
+    int before = 0, all;
+    for (int k = threadIdx.x; k < nchunk; k += VS_THREADS) before += k < (int)blockIdx.x ? cnt[k] : 0;
+    int dummy;
+    const int ex = vs_block_scan(before, dummy, s_w);   // block sum of the earlier chunks
+    (void)ex;
+    const int64_t p0 = (int64_t)blockIdx.x * VS_CHUNK + (int64_t)threadIdx.x * VS_PER;
+    unsigned bits = vs_bits(mask, p0, npx);
+    int off = vs_block_scan(__popc(bits), all, s_w) + dummy;
+    while (bits) {
+        const int i = __ffs(bits) - 1;
+        bits &= bits - 1;
+        ids_all[off++] = (int32_t)(p0 + i);
+    }
+    if (blockIdx.x == nchunk - 1 && threadIdx.x == 0) *total = dummy + all;
+}
+
+__global__ void __launch_bounds__(1024) k_vs_select(const float* __restrict__ obs, const float* __restrict__ img,
+                                                    int budget, double gate, const int32_t* __restrict__ ids_all,
+                                                    const int* __restrict__ total, int32_t* sel, double* sel_res,
+                                                    int32_t* ids_out, double* res_out, int64_t* counts) {
+    __shared__ int s_w[32];
+    const int tid = threadIdx.x;
+    const int L = *total;
+    const int nsel = L > budget ? budget : L;
+    const double step = budget > 1 ? (double)(L - 1) / (double)(budget - 1) : 0.0;
+    for (int k = tid; k < nsel; k += 1024) {
+        int src = k;
+        if (L > budget) src = (budget > 1 && k == budget - 1) ? L - 1 : (int)rint((double)k * step);
+        const int32_t p = ids_all[src];
+        const float* o = obs + 3 * (int64_t)p;
+        const float* h = img + 3 * (int64_t)p;
+        const double go = (((double)o[0] + (double)o[1]) + (double)o[2]) / 3.0;
+        const double gh = (((double)h[0] + (double)h[1]) + (double)h[2]) / 3.0;
+        sel[k] = p;
+        sel_res[k] = go - gh;
+    }
+    __syncthreads();
+    const int per = (nsel + 1023) / 1024, c0 = tid * per;
+    int c = 0;
+    for (int j = 0; j < per; ++j)
+        if (c0 + j < nsel && fabs(sel_res[c0 + j]) <= gate) ++c;
+    int nok;
+    int off = vs_block_scan(c, nok, s_w);
+    for (int j = 0; j < per; ++j)
+        if (c0 + j < nsel && fabs(sel_res[c0 + j]) <= gate) {
+            ids_out[off] = sel[c0 + j];
+            res_out[off] = sel_res[c0 + j];
+            ++off;
+        }
+    if (tid == 0) {
+        counts[0] = L;
+        counts[1] = nsel;
+        counts[2] = nok;
+    }
+}
+
+int64_t visual_select_scratch_bytes(int64_t npx, int budget) {
+    const int64_t nchunk = (npx + VS_CHUNK - 1) / VS_CHUNK;
+    return 8 * ((nchunk + 1 + 1) / 2 + 1) + 4 * npx + 4 * (int64_t)budget + 8 + 8 * (int64_t)budget;
+}
+
+cudaError_t launch_visual_select(const uint8_t* mask, const float* obs, const float* img, int64_t npx, int budget,
+                                 double gate, void* scratch, int32_t* ids_out, double* res_out, int64_t* counts,
+                                 cudaStream_t st) {
+    const int nchunk = (int)((npx + VS_CHUNK - 1) / VS_CHUNK);
+    int* cnt = (int*)scratch;                                          // nchunk + 1 (total)
+    int* total = cnt + nchunk;
+    int32_t* ids_all = (int32_t*)((char*)scratch + 8 * ((nchunk + 1 + 1) / 2 + 1));
+    int32_t* sel = ids_all + npx;
+    double* sel_res = (double*)(((uintptr_t)(sel + budget) + 7) & ~(uintptr_t)7);
+    cudaError_t e = cudaMemsetAsync(total, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    if (nchunk > 0) {
+        k_vs_count<<<nchunk, VS_THREADS, 0, st>>>(mask, npx, cnt);
+        k_vs_emit<<<nchunk, VS_THREADS, 0, st>>>(mask, npx, cnt, nchunk, ids_all, total);
+    }
+    k_vs_select<<<1, 1024, 0, st>>>(obs, img, budget, gate, ids_all, total, sel, sel_res, ids_out, res_out, counts);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_semidense(const float* obs, const float* tfin, int W, int H, double thr, double tmax,
                              uint8_t* out, cudaStream_t st) {
     k_semidense<<<4 * 148, 256, 0, st>>>(obs, tfin, W, H, thr, tmax, out);

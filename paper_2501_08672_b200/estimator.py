@@ -142,23 +142,38 @@ def visual_measurement(state, observed, window, cam, T_ic, cfg: FilterConfig,
     """Photometric residuals I(u) - I_hat(u) on semi-dense pixels
     (estimator.py:260-280)."""
     T_wc = state.T_WI @ T_ic
-    out = render(window, T_wc, cam, settings)
+    # contributing-list binning when alpha_cut > 0: the same image, T and pose
+    # rows (the dropped entries never composite), fewer tile entries
+    out = render(window, T_wc, cam, settings, bin_mode=1 if settings.alpha_cut > 0 else 0)
     dev = out.image.device
     h, w = int(cam.height), int(cam.width)
     obs = _f32(observed, (h, w, 3), dev)
-    ids = select_semi_dense_pixels(obs, out.final_transmittance, cfg)
-    if len(ids) < cfg.min_pixels:
-        raise TooFewPixels(f"{len(ids)} < {cfg.min_pixels}")
-    idt = torch.as_tensor(ids, device=dev)
-    gray_obs = obs.view(-1, 3).to(torch.float64)[idt].sum(dim=1) / 3.0
-    gray_hat = out.image.view(-1, 3).to(torch.float64)[idt].sum(dim=1) / 3.0
-    res = gray_obs - gray_hat
-    ok = res.abs() <= cfg.photo_gate
-    n_ok = int(ok.sum().item())
+    # semi-dense mask, then selection + residual + gate in one device pass;
+    # one small read-back for the counts the reference's exceptions need
+    lib = _lib.load()
+    npx = h * w
+    mask = torch.empty(npx, dtype=torch.uint8, device=dev)
+    _lib.check(lib.lsb_semidense_mask(ctypes.c_void_p(obs.data_ptr()),
+                                      ctypes.c_void_p(out.final_transmittance.data_ptr()), w, h,
+                                      float(cfg.grad_threshold), float(cfg.coverage_max_transmittance),
+                                      ctypes.c_void_p(mask.data_ptr()), _lib.stream_ptr()), "semidense")
+    budget = int(cfg.pixel_budget)
+    scratch = torch.empty(int(lib.lsb_visual_select_scratch_bytes(npx, budget)), dtype=torch.uint8, device=dev)
+    ids = torch.empty(budget, dtype=torch.int32, device=dev)
+    res = torch.empty(budget, dtype=torch.float64, device=dev)
+    counts = torch.empty(3, dtype=torch.int64, device=dev)
+    _lib.check(lib.lsb_visual_select(ctypes.c_void_p(mask.data_ptr()), ctypes.c_void_p(obs.data_ptr()),
+                                     ctypes.c_void_p(out.image.data_ptr()), npx, budget, float(cfg.photo_gate),
+                                     ctypes.c_void_p(scratch.data_ptr()), ctypes.c_void_p(ids.data_ptr()),
+                                     ctypes.c_void_p(res.data_ptr()), ctypes.c_void_p(counts.data_ptr()),
+                                     _lib.stream_ptr()), "visual_select")
+    _, n_sel, n_ok = (int(v) for v in counts.cpu())
+    if n_sel < cfg.min_pixels:
+        raise TooFewPixels(f"{n_sel} < {cfg.min_pixels}")
     if n_ok < cfg.min_pixels:
         raise TooFewPixels(f"{n_ok} < {cfg.min_pixels} after gating")
-    idt = idt[ok]
-    res = res[ok].contiguous()
+    idt = ids[:n_ok]
+    res = res[:n_ok].contiguous()
     rows = pose_rows(out, idt, T_ic=T_ic, as_numpy=False)
     return Measurement(rows_dev=rows, z_dev=res, sigma2=cfg.photo_sigma ** 2)
 

@@ -68,3 +68,32 @@ def test_ieskf_visual_update_matches_reference():
     assert np.abs(post.T_WI.t - d["post_t"]).max() <= 1e-4
     assert np.abs(post.T_WI.R - d["post_R"]).max() <= 1e-4
     assert np.abs(cov - d["post_cov"]).max() <= 1e-3 * np.abs(d["post_cov"]).max()
+
+
+@pytest.mark.parametrize("budget,gate", [(1, 0.15), (2, 0.15), (7, 0.15), (300, 0.02), (1024, 0.15), (10 ** 6, 0.15)])
+def test_device_selection_budget_and_gate(budget, gate):
+    """The on-device selection (lsb_visual_select) against the reference's
+    steps restated in numpy on the same mask and render: linspace subsample
+    at every budget regime (1, tiny, below and above the candidate count),
+    grey residual, ordered gate (estimator.py:241-277)."""
+    import torch
+
+    from paper_2501_08672_b200.estimator import FilterConfig, NavState, select_semi_dense_pixels, visual_measurement
+    from paper_2501_08672_b200.raster import RasterSettings, render
+    d, arrays, cam, T_wi, T_ic = _setup()
+    st = RasterSettings(alpha_cut=1 / 255)
+    cfg = FilterConfig(pixel_budget=budget, photo_gate=gate, min_pixels=1)
+    out = render(arrays, T_wi @ T_ic, cam, st, bin_mode=1)
+    ids = select_semi_dense_pixels(d["observed"], out.final_transmittance, cfg)
+    obs = np.asarray(d["observed"], np.float32).astype(np.float64).reshape(-1, 3)
+    img = out.image.cpu().numpy().astype(np.float64).reshape(-1, 3)
+    res = obs[ids].mean(axis=1) - img[ids].mean(axis=1)
+    res = res[np.abs(res) <= gate]
+    if len(res) < cfg.min_pixels:
+        from paper_2501_08672_b200.errors import TooFewPixels
+        with pytest.raises(TooFewPixels):
+            visual_measurement(NavState(T_wi), d["observed"], arrays, cam, T_ic, cfg, st)
+        return
+    meas = visual_measurement(NavState(T_wi), d["observed"], arrays, cam, T_ic, cfg, st)
+    torch.cuda.synchronize()
+    assert np.array_equal(meas.z, res)
