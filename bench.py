@@ -113,7 +113,7 @@ def build_workload(cfg_name, alpha_cut):
 
 
 # ---------------------------------------------------------------- CPU legs ---
-def cpu_sample(wl, n_views_sample):
+def cpu_sample(wl, n_views_sample, frames="u8"):
     """Reference algorithm on this host (oracle port, C + numpy, all cores):
     n_views_sample views of render + L1 loss + backward, then one Adam step
     on all window Gaussians.  Returns (seconds per sampled view, seconds per
@@ -133,6 +133,8 @@ def cpu_sample(wl, n_views_sample):
     for T in wl["views"][:n_views_sample]:
         T_cw = T.inverse()
         obs = orc.render(gt, T_cw.R, T_cw.t, cam, st)["image"]
+        if frames == "u8":      # the same 8-bit frames the GPU arm reads, as read_ppm returns them
+            obs = np.clip(np.round(obs * 255.0), 0, 255).astype(np.uint8).astype(np.float64) / 255.0
         t0 = time.perf_counter()
         c = orc.render(P, T_cw.R, T_cw.t, cam, st)
         _, _, g_img = photometric_loss(c["image"], obs)
@@ -156,7 +158,7 @@ def run_reference(args, wl, rank):
     V, P_px = wl["V"], wl["W"] * wl["H"]
     times = []
     for i in range(args.warmup + args.steps):
-        tv, ta, cores = cpu_sample(wl, 1)
+        tv, ta, cores = cpu_sample(wl, 1, args.frames)
         if i >= args.warmup:
             times.append(V * tv + ta)      # one full step, extrapolated from one sampled view
     t = float(np.mean(times))
@@ -169,26 +171,29 @@ def run_reference(args, wl, rank):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "gaussians_per_s": V * wl["N"] / t,
         "config": {"workload": args.config, "gaussians": wl["N"], "views": V, "width": wl["W"],
-                   "height": wl["H"], "alpha_cut": wl["alpha_cut"], "parallelism": "cpu threads"},
+                   "height": wl["H"], "alpha_cut": wl["alpha_cut"], "parallelism": "cpu threads",
+                   "frames": "8-bit, read_ppm's u/255.0 (f64)" if args.frames == "u8" else "float"},
         "cpu_baseline": {"value": value, "unit": "Mpix/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
 # ---------------------------------------------------------------- GPU leg ----
-def algorithmic_bytes(N, K, M, I, P, pbytes=8):
+def algorithmic_bytes(N, K, M, I, P, pbytes=8, obytes=4):
     """Per-launch algorithmic HBM bytes.  pbytes: bytes per
-    parameter of the working copy (8: the f64 copy optimize_window steps)."""
+    parameter of the working copy (8: the f64 copy optimize_window steps);
+    obytes: bytes per observed channel (1 for 8-bit frames, 4 for f32)."""
+    ob = 3 * obytes
     prm = pbytes * (16 + 3 * K)     # one Gaussian's parameters
     grd = 4 * (10 + 3 * K)          # one Gaussian's gradient row (f32)
     mom = pbytes * (10 + 3 * K)     # one Gaussian's Adam moment row
     return {
         "bin": N * prm + M * (64 + 8 + 4) + I * (4 + 4 + 4 + 8 + 4 + 4),
-        "blend_fwd": I * (64 + 4) + P * (12 + 4 + 4 + 12 + 12),   # + fused loss: read observed, write dL/dI
+        "blend_fwd": I * (64 + 4) + P * (12 + 4 + 4 + ob + 12),   # + fused loss: read observed, write dL/dI
         "blend_bwd": I * (64 + 4 + 4 + 36) + P * (12 + 12 + 4),
         # fused forward + loss + backward: records and slots read by both walks,
         # intersection ids, partials written; observed read (no image round trip)
-        "blend": I * (64 + 4 + 64 + 4 + 4 + 36) + P * 12,
+        "blend": I * (64 + 4 + 64 + 4 + 4 + 36) + P * ob,
         "chain": M * (64 + 4 + prm + 2 * grd) + I * 36,
         "adam": N * (2 * prm + grd + 4 * mom + 1),
     }
@@ -209,7 +214,26 @@ def run_ours(args, wl, rank, world, local_rank):
     my_views = [v for v in range(V) if v % world == rank]
     observed = [render(gt, wl["views"][v], wl["cam"], settings, retain_cache=False).image.clone()
                 for v in my_views]
+    if args.frames == "u8":
+        # the camera's 8-bit frames, quantised the way write_ppm stores them
+        # (raster.py:511-517); the kernels read u / 255.0 like read_ppm
+        observed = [torch.clamp(torch.round(o.double() * 255.0), 0, 255).to(torch.uint8) for o in observed]
     del gt
+    # L2 flush between timed steps: a write larger than the 126 MB L2, issued
+    # outside each step's event pair
+    flush_buf = torch.empty(64 * 2 ** 20, dtype=torch.int32, device=dev)
+
+    def timed(run_one):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        with torch.cuda.stream(stream):
+            for a, b in evs:
+                flush_buf.zero_()
+                a.record(stream)
+                run_one()
+                b.record(stream)
+        torch.cuda.synchronize()
+        return float(np.mean([a.elapsed_time(b) for a, b in evs]))
     stream = torch.cuda.Stream(dev)
     eng = WindowEngine(win, wl["cam"], [wl["views"][v] for v in my_views], settings, OptimConfig(),
                        n_views_total=V, stream=stream, lanes=args.lanes)
@@ -254,15 +278,9 @@ def run_ours(args, wl, rank, world, local_rank):
     timers: dict = {}
     keng = WindowEngine(win, wl["cam"], [wl["views"][v] for v in my_views], settings, OptimConfig(),
                         n_views_total=V, stream=stream, lanes=1, isect_cap=eng.lanes[0].state.dims.isect_cap)
-    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         keng.step(observed, allreduce=allreduce)
-        k0.record(stream)
-        for _ in range(args.steps):
-            keng.step(observed, allreduce=allreduce, timers=timers)
-        k1.record(stream)
-    torch.cuda.synchronize()
-    eager_ms = k0.elapsed_time(k1) / args.steps
+    eager_ms = timed(lambda: keng.step(observed, allreduce=allreduce, timers=timers))
     del keng
 
     # pass 2 (the headline): the same step captured once as a CUDA graph (the
@@ -289,23 +307,16 @@ def run_ours(args, wl, rank, world, local_rank):
 
     use_graph = bool(args.graph) and try_capture(observed)
     graph_headline = use_graph
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
+    torch.cuda.synchronize()
     with ClockSampler(smi_index) as clk:
-        with torch.cuda.stream(stream):
-            start.record(stream)
-            for _ in range(args.steps):
-                if use_graph:
-                    eng.replay()
-                else:
-                    eng.step(observed, allreduce=allreduce)
-            eng.finish()
-            end.record(stream)
-        torch.cuda.synchronize()
+        ms = timed(lambda: eng.replay() if use_graph else eng.step(observed, allreduce=allreduce))
+    with torch.cuda.stream(stream):
+        eng.finish()
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms = start.elapsed_time(end) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -318,7 +329,8 @@ def run_ours(args, wl, rank, world, local_rank):
     M_avg = float(np.mean([c[0] for c in counts])) if counts else 0.0
     I_avg = float(np.mean([c[1] for c in counts])) if counts else 0.0
     K = int(win.shs.shape[1])
-    ab = algorithmic_bytes(N, K, M_avg, I_avg, W * H, pbytes=eng.arrays.means.element_size())
+    ab = algorithmic_bytes(N, K, M_avg, I_avg, W * H, pbytes=eng.arrays.means.element_size(),
+                           obytes=observed[0].element_size())
     per_step_ms = {k: float(np.sum(v)) / args.steps for k, v in ktime.items()}
     dom = max(("bin", "blend", "blend_fwd", "blend_bwd", "chain"), key=lambda k: per_step_ms.get(k, 0.0))
     dom_ms = float(np.mean(ktime[dom]))
@@ -348,23 +360,19 @@ def run_ours(args, wl, rank, world, local_rank):
     torch.cuda.synchronize()
     if use_graph:
         use_graph = try_capture(host_obs)
-    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(stream):
-        e_start.record(stream)
-        for _ in range(args.steps):
-            if use_graph:
-                eng.replay()
-            else:
-                eng.step(host_obs, allreduce=allreduce)
-            _ = eng.loss.sums().to("cpu", non_blocking=False)
-        e_end.record(stream)
-    torch.cuda.synchronize()
-    e_ms = e_start.elapsed_time(e_end) / args.steps
+    def e2e_step():
+        if use_graph:
+            eng.replay()
+        else:
+            eng.step(host_obs, allreduce=allreduce)
+        _ = eng.loss.sums().to("cpu", non_blocking=False)
+
+    e_ms = timed(e2e_step)
     if world > 1:
         t = torch.tensor([e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e_ms = float(t.item())
-    h2d = sum(o.numel() * 4 for o in observed)
+    h2d = sum(o.numel() * o.element_size() for o in observed)
     d2h = int(eng.loss.sums().numel() * 8)
 
     clk_sum = clk.summary()
@@ -382,7 +390,10 @@ def run_ours(args, wl, rank, world, local_rank):
                        "cuda_graph": graph_headline, "cuda_graph_e2e": use_graph,
                        "serial_ms_per_step": eager_ms,
                        "kernel_timing": "separate one-lane eager pass of the same steps, events around each kernel",
-                       "l2": "working set > L2: observed views alone are V x 15.7 MB",
+                       "frames": ("8-bit (H,W,3), u/255.0 on the device like read_ppm" if args.frames == "u8"
+                                  else "float32 (H,W,3)"),
+                       "l2": "flushed before every timed step (256 MB write outside the step's event pair)",
+                       "timing": "CUDA events around each step on the launching stream, mean over steps",
                        "loss_last_step": float(np.mean(losses))},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "peak_source": hbm_src,
                          "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
@@ -401,12 +412,12 @@ def run_ours(args, wl, rank, world, local_rank):
             "clocks": clk_sum,
             "e2e": {"value": V * W * H / (e_ms * 1e-3) / 1e6, "unit": "Mpix/s",
                     "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world, "ms_per_step": e_ms},
-            "gpu_launches": args.steps * (len(my_views) * 10 + 2) + 1,   # per view: preprocess count / scan /
+            "gpu_launches": args.steps * (len(my_views) * 10 + 2),   # per view: preprocess count / scan /
             # emit, tile scan, scatter, tile sort, big-tile sort, fused blend (fwd + loss + bwd), loss total,
-            # chain; + adam and step counter per step; + final orthonormalize
+            # chain; + adam and step counter per step
         }
         if world == 1 and not args.no_cpu_baseline:
-            tv, ta, cores = cpu_sample(wl, 2)
+            tv, ta, cores = cpu_sample(wl, 2, args.frames)
             t_cpu = V * tv + ta
             out["cpu_baseline"] = {
                 "value": V * W * H / t_cpu / 1e6, "unit": "Mpix/s", "cores": cores, "kind": "port",
@@ -713,6 +724,8 @@ def main():
     ap.add_argument("--lanes", type=int, default=5, help="concurrent view pipelines per GPU")
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="eager launches instead of a CUDA graph")
     ap.add_argument("--copy-streams", type=int, default=1, help="H2D staging streams for the e2e pass")
+    ap.add_argument("--frames", default="u8", choices=["u8", "f32"],
+                    help="observed frames: 8-bit (the dataset's PPM frames, u/255 like read_ppm) or float32")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
                     help="N>1 gradient exchange: NCCL all-reduce + Adam, or the fused peer-memory step")
     args = ap.parse_args()

@@ -173,13 +173,21 @@ int lsb_render_bin(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T
  * T bit-identically); it may be NULL. */
 int lsb_render_blend(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
                      float* image, float* t_final, int32_t* n_contrib, float* depth, void* stream);
+/* Observed frames.  Every call taking `observed` with a loss `kind` (0 = L1,
+ * 1 = L2) reads a float32 (H,W,3) image; with kind | LSB_OBS_U8 it reads the
+ * camera's 8-bit (H,W,3) frame instead and uses u / 255.0 (f64), exactly the
+ * reference's read_ppm (raster.py:520-541; dataset.py:231) — a quarter of
+ * the host->device bytes, and the loss is formed from the same f64 values
+ * the reference subtracts. */
+#define LSB_OBS_U8 0x100
+
 /* Blend forward fused with the photometric loss (optimize.py:48-74, no mask):
  * also writes grad_out (H,W,3) = dL/dI * grad_scale from observed (H,W,3) and
  * loss_out[0..1] = [sum |diff| (L1) or diff^2 (L2), sum diff^2] over all
  * pixels (deterministic: per-tile partials summed in tile order). */
 int lsb_render_blend_loss(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
                           float* image, float* t_final, int32_t* n_contrib, float* depth,
-                          const float* observed, int kind, float grad_scale, float* grad_out,
+                          const void* observed, int kind, float grad_scale, float* grad_out,
                           double* loss_out, void* stream);
 int lsb_render_blend_bwd(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
                          const float* image, const int32_t* n_contrib, const float* grad_image,
@@ -196,9 +204,9 @@ int lsb_render_blend_bwd(const lsb_settings* s, void* ws, size_t ws_bytes, const
  * count) followed by lsb_render_blend_bwd_loss, without writing the image,
  * T or dL/dI; loss_out as there. */
 int lsb_render_blend_fused_loss(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
-                                const float* observed, int kind, float grad_scale, double* loss_out, void* stream);
+                                const void* observed, int kind, float grad_scale, double* loss_out, void* stream);
 int lsb_render_blend_bwd_loss(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
-                              const float* image, const float* observed, int kind, float grad_scale,
+                              const float* image, const void* observed, int kind, float grad_scale,
                               double* loss_out, void* stream);
 int lsb_render_chain(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T_cw,
                      const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* dims,
@@ -406,7 +414,7 @@ int lsb_window_append(const lsb_params* arena, int64_t* wkeys, const int64_t* ok
  * at allocation; on completion sums_out[0] = sum |diff| (L1) or sum diff^2
  * (L2) and sums_out[1] = sum diff^2 over the mask.  Deterministic. */
 int lsb_loss_scratch_doubles(void);
-int lsb_photometric_loss(const float* rendered, const float* observed, const uint8_t* mask,
+int lsb_photometric_loss(const float* rendered, const void* observed, const uint8_t* mask,
                          int64_t npx, int64_t mask_count, int kind, float grad_scale,
                          float* grad_out, double* sums_out, void* stream);
 

@@ -9,15 +9,15 @@ namespace lsb {
 cudaError_t launch_preprocess(const lsb_params&, const lsb_camera&, const lsb_pose&, const lsb_settings&,
                               const Ws&, cudaStream_t);
 cudaError_t launch_blend_fwd(const Ws&, const lsb_settings&, int, int, float*, float*, int32_t*, float*,
-                             const float*, int, float, float*, double*, cudaStream_t);
-cudaError_t launch_blend_fused(const Ws&, const lsb_settings&, int, int, const float*, int, float, double*, cudaStream_t);
-cudaError_t launch_blend_bwd_loss(const Ws&, const lsb_settings&, int, int, const float*, const float*, int, float,
+                             const void*, int, float, float*, double*, cudaStream_t);
+cudaError_t launch_blend_fused(const Ws&, const lsb_settings&, int, int, const void*, int, float, double*, cudaStream_t);
+cudaError_t launch_blend_bwd_loss(const Ws&, const lsb_settings&, int, int, const float*, const void*, int, float,
                                   double*, cudaStream_t);
 cudaError_t launch_blend_bwd(const Ws&, const lsb_settings&, int, int, const float*, const int32_t*,
                              const float*, float, cudaStream_t);
 cudaError_t launch_chain(const Ws&, const lsb_params&, const lsb_grads&, const lsb_camera&, const lsb_pose&,
                          const lsb_settings&, double*, cudaStream_t);
-cudaError_t launch_loss(const float*, const float*, const uint8_t*, int64_t, int, float, float*, double*,
+cudaError_t launch_loss(const float*, const void*, const uint8_t*, int64_t, int, float, float*, double*,
                         cudaStream_t);
 int loss_scratch_doubles();
 cudaError_t launch_adam(const lsb_params&, const float*, void*, void*, uint8_t*, const lsb_adam_cfg&, const double*,
@@ -245,12 +245,13 @@ int lsb_render_blend(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb
 }
 
 int lsb_render_blend_loss(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* d, float* image,
-                          float* t_final, int32_t* n_contrib, float* depth, const float* observed, int kind,
+                          float* t_final, int32_t* n_contrib, float* depth, const void* observed, int kind,
                           float grad_scale, float* grad_out, double* loss_out, void* stream) {
     if (!s || !image || !t_final || !observed || !grad_out || !loss_out)
         return fail(LSB_EINVAL, "NULL argument");
     if (!n_contrib && depth) return fail(LSB_EINVAL, "depth needs n_contrib");
-    if (kind != 0 && kind != 1) return fail(LSB_EINVAL, "kind must be 0 (l1) or 1 (l2)");
+    if ((kind & ~LSB_OBS_U8) != 0 && (kind & ~LSB_OBS_U8) != 1)
+        return fail(LSB_EINVAL, "kind must be 0 (l1) or 1 (l2), optionally | LSB_OBS_U8");
     Ws w;
     int rc = get_ws(ws, ws_bytes, d, &w);
     if (rc) return rc;
@@ -272,9 +273,10 @@ int lsb_render_blend_bwd(const lsb_settings* s, void* ws, size_t ws_bytes, const
 }
 
 int lsb_render_blend_fused_loss(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* d,
-                                const float* observed, int kind, float grad_scale, double* loss_out, void* stream) {
+                                const void* observed, int kind, float grad_scale, double* loss_out, void* stream) {
     if (!s || !observed || !loss_out) return fail(LSB_EINVAL, "NULL argument");
-    if (kind != 0 && kind != 1) return fail(LSB_EINVAL, "kind must be 0 (l1) or 1 (l2)");
+    if ((kind & ~LSB_OBS_U8) != 0 && (kind & ~LSB_OBS_U8) != 1)
+        return fail(LSB_EINVAL, "kind must be 0 (l1) or 1 (l2), optionally | LSB_OBS_U8");
     Ws w;
     int rc = get_ws(ws, ws_bytes, d, &w);
     if (rc) return rc;
@@ -284,11 +286,12 @@ int lsb_render_blend_fused_loss(const lsb_settings* s, void* ws, size_t ws_bytes
 }
 
 int lsb_render_blend_bwd_loss(const lsb_settings* s, void* ws, size_t ws_bytes, const lsb_dims* d,
-                              const float* image, const float* observed, int kind, float grad_scale,
+                              const float* image, const void* observed, int kind, float grad_scale,
                               double* loss_out, void* stream) {
     if (!s || !observed || !loss_out) return fail(LSB_EINVAL, "NULL argument");
     if (!image) return fail(LSB_EMISSING_CACHE, "render outputs missing");
-    if (kind != 0 && kind != 1) return fail(LSB_EINVAL, "kind must be 0 (l1) or 1 (l2)");
+    if ((kind & ~LSB_OBS_U8) != 0 && (kind & ~LSB_OBS_U8) != 1)
+        return fail(LSB_EINVAL, "kind must be 0 (l1) or 1 (l2), optionally | LSB_OBS_U8");
     Ws w;
     int rc = get_ws(ws, ws_bytes, d, &w);
     if (rc) return rc;
@@ -449,12 +452,13 @@ int lsb_voxmap_rehash(const lsb_voxmap* src, const lsb_voxmap* dst, void* stream
     return check_cuda(launch_vox_rehash(*src, *dst, (cudaStream_t)stream), "voxmap_rehash");
 }
 
-int lsb_photometric_loss(const float* rendered, const float* observed, const uint8_t* mask, int64_t npx,
+int lsb_photometric_loss(const float* rendered, const void* observed, const uint8_t* mask, int64_t npx,
                          int64_t mask_count, int kind, float grad_scale, float* grad_out,
                          double* sums_out, void* stream) {
     (void)mask_count;
     if (!rendered || !observed || !sums_out) return fail(LSB_EINVAL, "NULL argument");
-    if (kind != 0 && kind != 1) return fail(LSB_EINVAL, "kind must be 0 (l1) or 1 (l2)");
+    if ((kind & ~LSB_OBS_U8) != 0 && (kind & ~LSB_OBS_U8) != 1)
+        return fail(LSB_EINVAL, "kind must be 0 (l1) or 1 (l2), optionally | LSB_OBS_U8");
     return check_cuda(launch_loss(rendered, observed, mask, npx, kind, grad_scale, grad_out, sums_out,
                                   (cudaStream_t)stream),
                       "loss");

@@ -207,13 +207,14 @@ __device__ __forceinline__ void bwd_pixel(float al, float u, float thr, float cu
 #undef LSB_BWD_BODY
 
 struct LossArgs {
-    const float* observed;   // (H,W,3) or NULL: no fused loss
+    const void* observed;    // (H,W,3) f32 or u8 (obs_u8), or NULL: no fused loss
     float* grad;             // (H,W,3) dL/dI out
     double* sums;            // [ntiles*2] tile partials
     double* sums_out;        // [2] totals
     unsigned long long* ticket;    // (unused: the totals come from k_loss_total)
     int kind;                // 0 L1, 1 L2
     float gscale;
+    bool obs_u8;             // observed is an 8-bit frame (LSB_OBS_U8)
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -411,7 +412,7 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
                     const float i3[3] = {ir, ig, ib};
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
-                        const double d = (double)i3[c] - (double)L.observed[3 * p + c];
+                        const double d = (double)i3[c] - obs_value(L.observed, L.obs_u8, 3 * p + c);
                         l1 += d * d;
                         float gv;
                         if (L.kind == 0) {
@@ -627,7 +628,7 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __r
                         const float i3[3] = {i0, i1, i2};
 #pragma unroll
                         for (int c = 0; c < 3; ++c) {
-                            const double d = (double)i3[c] - (double)L.observed[3 * p + c];
+                            const double d = (double)i3[c] - obs_value(L.observed, L.obs_u8, 3 * p + c);
                             l1 += d * d;
                             if (L.kind == 0) {
                                 l0 += fabs(d);
@@ -787,7 +788,7 @@ k_blend_fused(Ws w, BlendArgs a, LossArgs L) {
                     float g3[3];
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
-                        const double d = (double)i3[c] - (double)L.observed[3 * p + c];
+                        const double d = (double)i3[c] - obs_value(L.observed, L.obs_u8, 3 * p + c);
                         l1 += d * d;
                         if (L.kind == 0) {
                             l0 += fabs(d);
@@ -818,12 +819,12 @@ k_blend_fused(Ws w, BlendArgs a, LossArgs L) {
     }
 }
 
-cudaError_t launch_blend_fused(const Ws& w, const lsb_settings& s, int W, int H, const float* observed, int kind,
+cudaError_t launch_blend_fused(const Ws& w, const lsb_settings& s, int W, int H, const void* observed, int kind,
                                float grad_scale, double* loss_out, cudaStream_t st) {
     const BlendArgs a = blend_args(s, W, H);
     cudaError_t e = cudaMemsetAsync(w.ctr + 8, 0, sizeof(unsigned long long), st);   // tile queue
     if (e != cudaSuccess) return e;
-    const LossArgs L{observed, nullptr, w.loss_part, loss_out, nullptr, kind, grad_scale};
+    const LossArgs L{observed, nullptr, w.loss_part, loss_out, nullptr, kind & 0xff, grad_scale, (kind & LSB_OBS_U8) != 0};
     if (s.alpha_cut > 0.0)
         k_blend_fused<true><<<persistent_grid((const void*)k_blend_fused<true>, w.ntiles, 1), 32 * WPB, 0, st>>>(w, a,
                                                                                                                 L);
@@ -835,10 +836,10 @@ cudaError_t launch_blend_fused(const Ws& w, const lsb_settings& s, int W, int H,
 }
 
 static cudaError_t blend_fwd_kernel(const Ws& w, const lsb_settings& s, int W, int H, float* image, float* t_final,
-                                    int32_t* n_contrib, float* depth, const float* observed, int kind, float gscale,
+                                    int32_t* n_contrib, float* depth, const void* observed, int kind, float gscale,
                                     float* grad, double* loss_out, cudaStream_t st) {
     const BlendArgs a = blend_args(s, W, H);
-    LossArgs L{observed, grad, w.loss_part, loss_out, nullptr, kind, gscale};
+    LossArgs L{observed, grad, w.loss_part, loss_out, nullptr, kind & 0xff, gscale, (kind & LSB_OBS_U8) != 0};
     // reset the forward tile queue ([7])
     cudaError_t e = cudaMemsetAsync(w.ctr + 7, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
@@ -868,7 +869,7 @@ static cudaError_t blend_fwd_kernel(const Ws& w, const lsb_settings& s, int W, i
 }
 
 cudaError_t launch_blend_fwd(const Ws& w, const lsb_settings& s, int W, int H, float* image, float* t_final,
-                             int32_t* n_contrib, float* depth, const float* observed, int kind, float gscale,
+                             int32_t* n_contrib, float* depth, const void* observed, int kind, float gscale,
                              float* grad, double* loss_out, cudaStream_t st) {
     cudaError_t e = blend_fwd_kernel(w, s, W, H, image, t_final, n_contrib, depth, observed, kind, gscale, grad,
                                      loss_out, st);
@@ -883,19 +884,19 @@ cudaError_t launch_blend_bwd(const Ws& w, const lsb_settings& s, int W, int H, c
     const BlendArgs a = blend_args(s, W, H);
     cudaError_t e = cudaMemsetAsync(w.ctr + 8, 0, sizeof(unsigned long long), st);   // backward tile queue
     if (e != cudaSuccess) return e;
-    const LossArgs L{nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0.f};
+    const LossArgs L{nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0.f, false};
     k_blend_bwd<false><<<persistent_grid((const void*)k_blend_bwd<false>, w.ntiles), 32 * WPB, 0, st>>>(
         w, a, image, gimg, gscale, L);
     return cudaGetLastError();
 }
 
 cudaError_t launch_blend_bwd_loss(const Ws& w, const lsb_settings& s, int W, int H, const float* image,
-                                  const float* observed, int kind, float grad_scale, double* loss_out,
+                                  const void* observed, int kind, float grad_scale, double* loss_out,
                                   cudaStream_t st) {
     const BlendArgs a = blend_args(s, W, H);
     cudaError_t e = cudaMemsetAsync(w.ctr + 8, 0, sizeof(unsigned long long), st);   // backward tile queue
     if (e != cudaSuccess) return e;
-    const LossArgs L{observed, nullptr, w.loss_part, loss_out, nullptr, kind, grad_scale};
+    const LossArgs L{observed, nullptr, w.loss_part, loss_out, nullptr, kind & 0xff, grad_scale, (kind & LSB_OBS_U8) != 0};
     k_blend_bwd<true><<<persistent_grid((const void*)k_blend_bwd<true>, w.ntiles), 32 * WPB, 0, st>>>(
         w, a, image, nullptr, 1.0f, L);
     k_loss_total<<<1, LT_THREADS, 0, st>>>(w.ntiles, w.loss_part, loss_out);

@@ -145,4 +145,20 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
+// Observed camera frames: float32 (H,W,3), or 8-bit (H,W,3) when the loss
+// kind carries LSB_OBS_U8 — then the value is u / 255.0 in f64, exactly the
+// reference's read_ppm (raster.py:520-541, maxval 255).
+// The quotient without a division: q = u * RN(1/255), then one fma residual
+// correction, which is the correctly rounded u / 255 for every u in 0..255
+// (checked exhaustively on the host: tests/test_frames.py).
+__device__ __forceinline__ double u8_unit(unsigned u) {
+    const double x = (double)u, r = 1.0 / 255.0;
+    const double q = __dmul_rn(x, r);
+    return fma(fma(-q, 255.0, x), r, q);
+}
+
+__device__ __forceinline__ double obs_value(const void* obs, bool u8, int64_t i) {
+    return u8 ? u8_unit(((const uint8_t*)obs)[i]) : (double)((const float*)obs)[i];
+}
+
 }  // namespace lsb

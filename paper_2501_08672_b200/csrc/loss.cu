@@ -12,7 +12,7 @@ constexpr int LOSS_BLOCKS = 296;
 constexpr int LOSS_THREADS = 256;
 
 __global__ void __launch_bounds__(LOSS_THREADS)
-k_loss(const float* __restrict__ rend, const float* __restrict__ obs, const uint8_t* __restrict__ mask,
+k_loss(const float* __restrict__ rend, const void* __restrict__ obs, bool obs_u8, const uint8_t* __restrict__ mask,
        int64_t npx, int kind, float gscale, float* __restrict__ grad, double* scratch) {
     __shared__ double s_r[LOSS_THREADS / 32][2];
     __shared__ bool s_last;
@@ -21,7 +21,7 @@ k_loss(const float* __restrict__ rend, const float* __restrict__ obs, const uint
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const bool m = mask ? (mask[i / 3] != 0) : true;
-        const double dd = (double)rend[i] - (double)obs[i];
+        const double dd = (double)rend[i] - obs_value(obs, obs_u8, i);
         float gv = 0.f;
         if (m) {
             acc1 += dd * dd;
@@ -68,9 +68,10 @@ k_loss(const float* __restrict__ rend, const float* __restrict__ obs, const uint
     }
 }
 
-cudaError_t launch_loss(const float* rend, const float* obs, const uint8_t* mask, int64_t npx,
+cudaError_t launch_loss(const float* rend, const void* obs, const uint8_t* mask, int64_t npx,
                         int kind, float gscale, float* grad, double* scratch, cudaStream_t st) {
-    k_loss<<<LOSS_BLOCKS, LOSS_THREADS, 0, st>>>(rend, obs, mask, npx, kind, gscale, grad, scratch);
+    k_loss<<<LOSS_BLOCKS, LOSS_THREADS, 0, st>>>(rend, obs, (kind & LSB_OBS_U8) != 0, mask, npx, kind & 0xff, gscale,
+                                                 grad, scratch);
     return cudaGetLastError();
 }
 

@@ -24,8 +24,8 @@ import torch
 from . import _lib
 from .errors import EmptyMask
 from .geometry import as_se3
-from .raster import (GaussianArrays, ParamGradients, RasterSettings, RenderState, _as_arrays, _f32,
-                     render_bin, render_blend, render_blend_bwd, render_blend_bwd_loss, render_blend_fused_loss,
+from .raster import (GaussianArrays, ParamGradients, RasterSettings, RenderState, _as_arrays, _f32, _obs_kind,
+                     _observed, render_bin, render_blend, render_blend_bwd, render_blend_bwd_loss, render_blend_fused_loss,
                      render_blend_loss, render_chain)
 
 
@@ -80,7 +80,7 @@ def launch_loss(rendered: torch.Tensor, observed: torch.Tensor, mask: Optional[t
     npx = rendered.numel() // 3
     _lib.check(_lib.load().lsb_photometric_loss(
         ctypes.c_void_p(rendered.data_ptr()), ctypes.c_void_p(observed.data_ptr()),
-        ctypes.c_void_p(mask.data_ptr()) if mask is not None else None, npx, count, _KIND[kind],
+        ctypes.c_void_p(mask.data_ptr()) if mask is not None else None, npx, count, _obs_kind(observed, _KIND[kind]),
         float(grad_scale), ctypes.c_void_p(grad_out.data_ptr()) if grad_out is not None else None,
         scratch_ptr, _lib.stream_ptr(stream)), "photometric_loss")
 
@@ -100,7 +100,7 @@ def photometric_loss(rendered, observed, mask=None, kind: str = "l1"):
         raise ValueError(f"unknown loss kind {kind!r}")
     dev = rendered.device if torch.is_tensor(rendered) and rendered.is_cuda else torch.device("cuda")
     r = _f32(rendered, tuple(np.shape(rendered)), dev)
-    o = _f32(observed, tuple(np.shape(observed)), dev)
+    o = _observed(observed, tuple(np.shape(observed)), dev)
     if r.shape != o.shape:
         raise ValueError("image shapes differ")
     h, w = r.shape[:2]
@@ -283,21 +283,23 @@ class WindowEngine:
         if self.copy_stream is None:
             self.copy_stream = torch.cuda.Stream(dev)
             self._copy_streams = [self.copy_stream] + [torch.cuda.Stream(dev) for _ in range(self.copy_streams - 1)]
-            self.obs_dev = [torch.empty((self.h, self.w, 3), dtype=torch.float32, device=dev) for _ in self.views]
+            self.obs_dev = [torch.empty((self.h, self.w, 3), dtype=observed[0].dtype, device=dev)
+                            for _ in self.views]
         for cs in self._copy_streams:
             cs.wait_event(ready)
         lib = _lib.load()
         events = []
         for v, obs in enumerate(observed):
             cs = self._copy_streams[v % len(self._copy_streams)]
-            if obs.dtype != torch.float32 or tuple(obs.shape) != (self.h, self.w, 3) or not obs.is_contiguous():
-                raise ValueError("observed images must be contiguous float32 (H, W, 3)")
+            if (obs.dtype != self.obs_dev[v].dtype or obs.dtype not in (torch.float32, torch.uint8)
+                    or tuple(obs.shape) != (self.h, self.w, 3) or not obs.is_contiguous()):
+                raise ValueError("observed images must be contiguous float32 or uint8 (H, W, 3), one dtype")
             if capturing and not obs.is_pinned():
                 raise ValueError("graph capture needs pinned host images")
             if self._consumed[v] is not None and not capturing:
                 cs.wait_event(self._consumed[v])      # previous step's blend of this view is done
             _lib.check(lib.lsb_copy_h2d(ctypes.c_void_p(self.obs_dev[v].data_ptr()), ctypes.c_void_p(obs.data_ptr()),
-                                        obs.numel() * 4, _lib.stream_ptr(cs)), "copy_h2d")
+                                        obs.numel() * obs.element_size(), _lib.stream_ptr(cs)), "copy_h2d")
             ev = torch.cuda.Event()
             ev.record(cs)
             events.append(ev)
@@ -453,7 +455,7 @@ def optimize_window(window, observed, T_wc, cam, cfg: OptimConfig = OptimConfig(
         return history
     dev = arrays.device
     h, w = int(cam.height), int(cam.width)
-    obs = _f32(observed, (h, w, 3), dev)
+    obs = _observed(observed, (h, w, 3), dev)
     m, count = _mask_u8(mask, h, w, dev)
     if count == 0:
         raise EmptyMask("mask selects no pixels")

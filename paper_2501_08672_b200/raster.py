@@ -60,6 +60,27 @@ def _f32(x, shape, device):
     return _as(x, shape, device, torch.float32)
 
 
+OBS_U8 = 0x100      # include/lsb.h LSB_OBS_U8
+
+
+def _observed(x, shape, device):
+    """An observed frame on the device: 8-bit frames (the camera's / the
+    dataset's PPM bytes, raster.py:520-541) stay 8-bit — the kernels use
+    u / 255.0 like read_ppm — anything else becomes float32."""
+    t = torch.as_tensor(x)
+    if t.dtype == torch.uint8:
+        return _as(t, shape, device, torch.uint8)
+    return _f32(t, shape, device)
+
+
+def _obs_kind(observed, kind: int) -> int:
+    if observed.dtype == torch.uint8:
+        return int(kind) | OBS_U8
+    if observed.dtype != torch.float32:
+        raise ValueError("observed frames are float32 or uint8 (H, W, 3)")
+    return int(kind)
+
+
 class GaussianArrays:
     """Structure-of-arrays Gaussian parameters in HBM.  f32 by default (the
     window arena's storage type, window.py:51-55; the reference upcasts the
@@ -311,7 +332,7 @@ def render_blend_loss(state: RenderState, image, t_final, n_contrib, observed, k
     _lib.check(_lib.load().lsb_render_blend_loss(
         ctypes.byref(state.c_set), state._ws(), state.ws_bytes, ctypes.byref(state.dims),
         ctypes.c_void_p(image.data_ptr()), ctypes.c_void_p(t_final.data_ptr()),
-        _ptr(n_contrib), _ptr(depth), ctypes.c_void_p(observed.data_ptr()), int(kind), float(grad_scale), ctypes.c_void_p(grad_out.data_ptr()),
+        _ptr(n_contrib), _ptr(depth), ctypes.c_void_p(observed.data_ptr()), _obs_kind(observed, kind), float(grad_scale), ctypes.c_void_p(grad_out.data_ptr()),
         loss_ptr, _lib.stream_ptr(stream)), "blend_loss")
 
 
@@ -329,8 +350,8 @@ def render_blend_fused_loss(state: RenderState, observed, kind: int, grad_scale:
     """K3 + loss + K4 in one kernel (the window engine's step; async)."""
     _lib.check(_lib.load().lsb_render_blend_fused_loss(
         ctypes.byref(state.c_set), state._ws(), state.ws_bytes, ctypes.byref(state.dims),
-        ctypes.c_void_p(observed.data_ptr()), int(kind), float(grad_scale), loss_ptr, _lib.stream_ptr(stream)),
-        "blend_fused_loss")
+        ctypes.c_void_p(observed.data_ptr()), _obs_kind(observed, kind), float(grad_scale), loss_ptr,
+        _lib.stream_ptr(stream)), "blend_fused_loss")
 
 
 def render_blend_bwd_loss(state: RenderState, image, observed, kind: int, grad_scale: float, loss_ptr,
@@ -339,8 +360,8 @@ def render_blend_bwd_loss(state: RenderState, image, observed, kind: int, grad_s
     pixel from (image, observed), loss sums to loss_ptr (async)."""
     _lib.check(_lib.load().lsb_render_blend_bwd_loss(
         ctypes.byref(state.c_set), state._ws(), state.ws_bytes, ctypes.byref(state.dims),
-        ctypes.c_void_p(image.data_ptr()), ctypes.c_void_p(observed.data_ptr()), int(kind), float(grad_scale),
-        loss_ptr, _lib.stream_ptr(stream)), "blend_bwd_loss")
+        ctypes.c_void_p(image.data_ptr()), ctypes.c_void_p(observed.data_ptr()), _obs_kind(observed, kind),
+        float(grad_scale), loss_ptr, _lib.stream_ptr(stream)), "blend_bwd_loss")
 
 
 def render_chain(state: RenderState, grads: "ParamGradients", pose_dev=None, stream=None) -> None:

@@ -83,7 +83,13 @@ def test_optimize_zero_iters_is_identity():
     assert bool((arrays.shs == before).all())
 
 
-def _room_engine(lanes, steps=2, mode="eager", loss_in_backward=True, fused=True):
+def _quantize(img):
+    """An 8-bit frame the way write_ppm stores one (raster.py:511-517)."""
+    import torch
+    return torch.clamp(torch.round(img.double() * 255.0), 0, 255).to(torch.uint8)
+
+
+def _room_engine(lanes, steps=2, mode="eager", loss_in_backward=True, fused=True, frames="f32"):
     import torch
     from paper_2501_08672_b200.optimize import OptimConfig, WindowEngine
     from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
@@ -94,6 +100,8 @@ def _room_engine(lanes, steps=2, mode="eager", loss_in_backward=True, fused=True
     st = RasterSettings(alpha_cut=1 / 255)
     gt = GaussianArrays(s["means"], s["rots"], s["scales"], s["opacities"], s["shs"])
     obs = [render(gt, T, cam, st, retain_cache=False).image.clone() for T in views]
+    if frames == "u8":
+        obs = [_quantize(o) for o in obs]
     shs = s["shs"].copy()
     shs[:, 0, :] += np.random.default_rng(0).uniform(-0.1, 0.1, shs[:, 0, :].shape)
     win = GaussianArrays(s["means"], s["rots"], s["scales"], s["opacities"], shs)
@@ -151,12 +159,14 @@ def test_engine_fused_blend_bit_identical():
         assert bool((getattr(w1, k) == getattr(w2, k)).all()), k
 
 
-def test_engine_multiview_matches_oracle():
-    """One multi-view step: the mean of the per-view gradients (oracle)."""
+@pytest.mark.parametrize("frames", ["f32", "u8"])
+def test_engine_multiview_matches_oracle(frames):
+    """One multi-view step: the mean of the per-view gradients (oracle).  With
+    8-bit frames the oracle gets read_ppm's u / 255.0."""
     from types import SimpleNamespace
     from oracle.optim import optimize_views
     from paper_2501_08672_b200.scene import camera_for, orbit_views
-    win, losses, _ = _room_engine(2, steps=1)
+    win, losses, _ = _room_engine(2, steps=1, frames=frames)
     s = load("scene_room_0323")
     cam = camera_for(160, 128)
     views = orbit_views(5)
@@ -165,6 +175,13 @@ def test_engine_multiview_matches_oracle():
     from oracle import raster as orc
     P = {k: s[k].astype(np.float64) for k in ("means", "rots", "scales", "opacities", "shs")}
     obs = [orc.render(P, T.inverse().R, T.inverse().t, cam, st)["image"] for T in views]
+    if frames == "u8":
+        # the engine's frames: the GPU render quantised like write_ppm
+        import torch
+        from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
+        gt = GaussianArrays(s["means"], s["rots"], s["scales"], s["opacities"], s["shs"])
+        obs = [_quantize(render(gt, T, cam, RasterSettings(alpha_cut=1 / 255), retain_cache=False).image)
+               .cpu().numpy().astype(np.float64) / 255.0 for T in views]
     shs = s["shs"].astype(np.float64).copy()
     shs[:, 0, :] += np.random.default_rng(0).uniform(-0.1, 0.1, shs[:, 0, :].shape)
     shs = shs.astype(np.float32).astype(np.float64)
@@ -187,6 +204,40 @@ def test_engine_graph_and_host_staging_bit_identical(mode):
     device-input steps."""
     w1, l1, g1 = _room_engine(3, steps=3)
     w2, l2, g2 = _room_engine(3, steps=3, mode=mode)
+    assert bool((g1 == g2).all())
+    assert np.array_equal(l1, l2)
+    for k in ("means", "rots", "scales", "opacities", "shs"):
+        assert bool((getattr(w1, k) == getattr(w2, k)).all()), k
+
+
+def test_photometric_loss_u8_frames_match_oracle():
+    """8-bit observed frames (LSB_OBS_U8): the loss uses u / 255.0 exactly as
+    read_ppm does (raster.py:520-541) — same sums and gradient as the oracle
+    fed the f64 frame."""
+    from oracle.optim import photometric_loss as ref_loss
+    from paper_2501_08672_b200.optimize import photometric_loss
+    rng = np.random.default_rng(3)
+    b8 = rng.integers(0, 256, (9, 7, 3), dtype=np.uint8)
+    a = (b8.astype(np.float64) / 255.0 + rng.choice([0.0, 0.01, -0.02], (9, 7, 3))).astype(np.float32)
+    mask = rng.uniform(0, 1, (9, 7)) > 0.3
+    for kind in ("l1", "l2"):
+        for m in (None, mask):
+            rep, grad = photometric_loss(a, b8, mask=m, kind=kind)
+            v, mse, g = ref_loss(a.astype(float), b8.astype(float) / 255.0, m, kind)
+            assert abs(rep.value - v) <= 1e-12
+            assert abs(rep.mse - mse) <= 1e-12
+            assert np.abs(grad.cpu().numpy() - g).max() <= 1e-7 * np.abs(g).max()
+
+
+@pytest.mark.parametrize("variant", ["separate", "loss_in_forward", "graph_host", "lanes1"])
+def test_engine_u8_frames_bit_identical(variant):
+    """8-bit frames through every engine variant (fused / separate kernels,
+    loss in the forward, CUDA graph with host staging, one lane) give
+    bit-identical results."""
+    w1, l1, g1 = _room_engine(3, steps=2, frames="u8")
+    kw = {"separate": dict(fused=False), "loss_in_forward": dict(fused=False, loss_in_backward=False),
+          "graph_host": dict(mode="graph_host"), "lanes1": {}}[variant]
+    w2, l2, g2 = _room_engine(1 if variant == "lanes1" else 3, steps=2, frames="u8", **kw)
     assert bool((g1 == g2).all())
     assert np.array_equal(l1, l2)
     for k in ("means", "rots", "scales", "opacities", "shs"):
