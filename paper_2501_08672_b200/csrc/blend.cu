@@ -48,13 +48,19 @@
 
 namespace lsb {
 
-constexpr int WPB = 4;       // tile-warps per CTA
+#ifndef LSB_WPB
+#define LSB_WPB 4
+#endif
+#ifndef FUSED_RESERVE
+#define FUSED_RESERVE 1      // CTA slots per SM the fused blend leaves to the other lanes
+#endif
+constexpr int WPB = LSB_WPB;  // tile-warps per CTA
 constexpr int RUN = 4;       // pixels per lane and row (horizontal run)
 #ifndef FWD_MIN_BLOCKS
 #define FWD_MIN_BLOCKS 6
 #endif
 #ifndef BWD_MIN_BLOCKS
-#define BWD_MIN_BLOCKS 4
+#define BWD_MIN_BLOCKS 5
 #endif
 
 struct BlendArgs {
@@ -824,13 +830,14 @@ cudaError_t launch_blend_fused(const Ws& w, const lsb_settings& s, int W, int H,
     const BlendArgs a = blend_args(s, W, H);
     cudaError_t e = cudaMemsetAsync(w.ctr + 8, 0, sizeof(unsigned long long), st);   // tile queue
     if (e != cudaSuccess) return e;
-    const LossArgs L{observed, nullptr, w.loss_part, loss_out, nullptr, kind & 0xff, grad_scale, (kind & LSB_OBS_U8) != 0};
+    const LossArgs L{observed, nullptr,     w.loss_part, loss_out,
+                     nullptr,  kind & 0xff, grad_scale,  (kind & LSB_OBS_U8) != 0};
+    const void* fn = s.alpha_cut > 0.0 ? (const void*)k_blend_fused<true> : (const void*)k_blend_fused<false>;
+    const int grid = persistent_grid(fn, w.ntiles, FUSED_RESERVE);
     if (s.alpha_cut > 0.0)
-        k_blend_fused<true><<<persistent_grid((const void*)k_blend_fused<true>, w.ntiles, 1), 32 * WPB, 0, st>>>(w, a,
-                                                                                                                L);
+        k_blend_fused<true><<<grid, 32 * WPB, 0, st>>>(w, a, L);
     else
-        k_blend_fused<false><<<persistent_grid((const void*)k_blend_fused<false>, w.ntiles, 1), 32 * WPB, 0, st>>>(
-            w, a, L);
+        k_blend_fused<false><<<grid, 32 * WPB, 0, st>>>(w, a, L);
     k_loss_total<<<1, LT_THREADS, 0, st>>>(w.ntiles, w.loss_part, loss_out);
     return cudaGetLastError();
 }
@@ -896,7 +903,8 @@ cudaError_t launch_blend_bwd_loss(const Ws& w, const lsb_settings& s, int W, int
     const BlendArgs a = blend_args(s, W, H);
     cudaError_t e = cudaMemsetAsync(w.ctr + 8, 0, sizeof(unsigned long long), st);   // backward tile queue
     if (e != cudaSuccess) return e;
-    const LossArgs L{observed, nullptr, w.loss_part, loss_out, nullptr, kind & 0xff, grad_scale, (kind & LSB_OBS_U8) != 0};
+    const LossArgs L{observed, nullptr,     w.loss_part, loss_out,
+                     nullptr,  kind & 0xff, grad_scale,  (kind & LSB_OBS_U8) != 0};
     k_blend_bwd<true><<<persistent_grid((const void*)k_blend_bwd<true>, w.ntiles), 32 * WPB, 0, st>>>(
         w, a, image, nullptr, 1.0f, L);
     k_loss_total<<<1, LT_THREADS, 0, st>>>(w.ntiles, w.loss_part, loss_out);
