@@ -387,6 +387,9 @@ def run_ours(args, wl, rank, world, local_rank):
             "config": {"workload": args.config, "gaussians": N, "views": V, "width": W, "height": H,
                        "alpha_cut": wl["alpha_cut"], "parallelism": f"view-sharded dp{world}",
                        "view_lanes": args.lanes, "exchange": exchange if world > 1 else None,
+                       # views v -> rank v mod N: config 2's 10 views split unevenly at 4 and 8 GPUs
+                       "views_per_rank": [len(range(r, V, world)) for r in range(world)],
+                       "view_imbalance": max(len(range(r, V, world)) for r in range(world)) / (V / world),
                        "cuda_graph": graph_headline, "cuda_graph_e2e": use_graph,
                        "serial_ms_per_step": eager_ms,
                        "kernel_timing": "separate one-lane eager pass of the same steps, events around each kernel",
