@@ -644,48 +644,96 @@ __global__ void __launch_bounds__(PRE_THREADS) k_pre_count(PreArgs a, Ws w) {
 }
 
 constexpr int PS_THREADS = 1024;
+constexpr int PS_ITEMS = 8;          // warp counts per thread and pass (4 x 16-B loads)
+// One CTA scans the per-warp (visible, tile) counts in passes of
+// PS_THREADS x PS_ITEMS: every thread loads its 8 consecutive pairs with
+// vector loads (all in flight at once), scans them locally, and one block
+// scan + a running carry place them — coalesced, a handful of memory
+// latencies per pass instead of one per count.
 __global__ void __launch_bounds__(PS_THREADS) k_pre_scan(Ws w, int64_t nw) {
     __shared__ long long s_v[PS_THREADS / 32], s_t[PS_THREADS / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t per = (nw + PS_THREADS - 1) / PS_THREADS, b0 = tid * per;
-    long long sv = 0, st = 0;
-    for (int64_t k = 0; k < per; ++k)
-        if (b0 + k < nw) {
-            sv += w.warp_cnt[2 * (b0 + k)];
-            st += w.warp_cnt[2 * (b0 + k) + 1];
-        }
-    long long xv = sv, xt = st;
+    const bool vec = ((uintptr_t)w.warp_cnt & 15) == 0 && ((uintptr_t)w.warp_off & 15) == 0;
+    long long carry_v = 0, carry_t = 0;
+    for (int64_t base = 0; base < nw; base += (int64_t)PS_THREADS * PS_ITEMS) {
+        const int64_t b0 = base + (int64_t)tid * PS_ITEMS;
+        int c[2 * PS_ITEMS];
+        if (vec && b0 + PS_ITEMS <= nw) {
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const long long yv = __shfl_up_sync(0xffffffffu, xv, o), yt = __shfl_up_sync(0xffffffffu, xt, o);
-        if (lane >= o) {
-            xv += yv;
-            xt += yt;
+            for (int q = 0; q < PS_ITEMS / 2; ++q) {
+                const int4 x = *(const int4*)(w.warp_cnt + 2 * b0 + 4 * q);
+                c[4 * q] = x.x;
+                c[4 * q + 1] = x.y;
+                c[4 * q + 2] = x.z;
+                c[4 * q + 3] = x.w;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < PS_ITEMS; ++k) {
+                const bool in = b0 + k < nw;
+                c[2 * k] = in ? w.warp_cnt[2 * (b0 + k)] : 0;
+                c[2 * k + 1] = in ? w.warp_cnt[2 * (b0 + k) + 1] : 0;
+            }
         }
-    }
-    if (lane == 31) {
-        s_v[warp] = xv;
-        s_t[warp] = xt;
-    }
-    __syncthreads();
-    long long bv = 0, bt = 0;
-    for (int k = 0; k < warp; ++k) {
-        bv += s_v[k];
-        bt += s_t[k];
-    }
-    long long rv = xv - sv + bv, rt = xt - st + bt;
-    for (int64_t k = 0; k < per; ++k)
-        if (b0 + k < nw) {
-            w.warp_off[2 * (b0 + k)] = (int32_t)rv;
-            w.warp_off[2 * (b0 + k) + 1] = (int32_t)min(rt, 0x7fffffffll);
-            rv += w.warp_cnt[2 * (b0 + k)];
-            rt += w.warp_cnt[2 * (b0 + k) + 1];
+        long long sv = 0, st = 0;
+#pragma unroll
+        for (int k = 0; k < PS_ITEMS; ++k) {
+            sv += c[2 * k];
+            st += c[2 * k + 1];
         }
-    if (tid == PS_THREADS - 1) {
-        w.ctr[0] = (unsigned long long)rv;
-        w.ctr[1] = (unsigned long long)rt;
-        w.vis_ebase[rv] = (int32_t)min(rt, 0x7fffffffll);
-        if (rt > w.cap) w.ctr[2] = 1;
+        long long xv = sv, xt = st;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long yv = __shfl_up_sync(0xffffffffu, xv, o), yt = __shfl_up_sync(0xffffffffu, xt, o);
+            if (lane >= o) {
+                xv += yv;
+                xt += yt;
+            }
+        }
+        if (lane == 31) {
+            s_v[warp] = xv;
+            s_t[warp] = xt;
+        }
+        __syncthreads();
+        long long bv = 0, bt = 0, tv = 0, tt = 0;
+        for (int k = 0; k < PS_THREADS / 32; ++k) {
+            if (k < warp) {
+                bv += s_v[k];
+                bt += s_t[k];
+            }
+            tv += s_v[k];
+            tt += s_t[k];
+        }
+        __syncthreads();                 // s_v / s_t reused by the next pass
+        long long rv = carry_v + xv - sv + bv, rt = carry_t + xt - st + bt;
+        int o[2 * PS_ITEMS];
+#pragma unroll
+        for (int k = 0; k < PS_ITEMS; ++k) {
+            o[2 * k] = (int32_t)rv;
+            o[2 * k + 1] = (int32_t)min(rt, 0x7fffffffll);
+            rv += c[2 * k];
+            rt += c[2 * k + 1];
+        }
+        if (vec && b0 + PS_ITEMS <= nw) {
+#pragma unroll
+            for (int q = 0; q < PS_ITEMS / 2; ++q)
+                *(int4*)(w.warp_off + 2 * b0 + 4 * q) = make_int4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < PS_ITEMS; ++k)
+                if (b0 + k < nw) {
+                    w.warp_off[2 * (b0 + k)] = o[2 * k];
+                    w.warp_off[2 * (b0 + k) + 1] = o[2 * k + 1];
+                }
+        }
+        carry_v += tv;
+        carry_t += tt;
+    }
+    if (tid == 0) {
+        w.ctr[0] = (unsigned long long)carry_v;
+        w.ctr[1] = (unsigned long long)carry_t;
+        w.vis_ebase[carry_v] = (int32_t)min(carry_t, 0x7fffffffll);
+        if (carry_t > w.cap) w.ctr[2] = 1;
     }
 }
 
