@@ -67,6 +67,7 @@ struct Ws {
     uint32_t* warp_mask;        // [ceil(n/32)] visible lanes per preprocess warp
     int32_t* warp_cnt;          // [2 ceil(n/32)] visible count, tile count per warp
     int32_t* warp_off;          // [2 ceil(n/32)] their exclusive scans
+    int32_t* chunk_cnt;         // [2 ceil(n/32/1024)] (visible, tile) totals per 1024 preprocess warps
     int64_t n, cap;
     int32_t ntx, nty, ntiles, nblocks_pre;
 };
@@ -96,6 +97,7 @@ inline size_t carve(const lsb_dims& d, char* base, Ws* w) {
     t.ctr = (unsigned long long*)take(16 * sizeof(unsigned long long));
     t.tile_count = (int32_t*)take(sizeof(int32_t) * t.ntiles);
     t.tile_cursor = (int32_t*)take(sizeof(int32_t) * t.ntiles);
+    t.chunk_cnt = (int32_t*)take(sizeof(int32_t) * 2 * (((n + 31) / 32 + 1023) / 1024));
     // not zeroed
     t.tile_start = (int32_t*)take(sizeof(int32_t) * (t.ntiles + 1));
     t.tile_last = (int32_t*)take(sizeof(int32_t) * t.ntiles);

@@ -306,12 +306,17 @@ __device__ __forceinline__ void emit_splat(const PreArgs& a, const Ws& w, Rec& r
 constexpr int ST_THREADS = 1024;
 __global__ void __launch_bounds__(ST_THREADS) k_scan_tiles(Ws w) {
     __shared__ int s_w[ST_THREADS / 32];
+    // the tile counts, staged once (coalesced); skewed by one word per 32 so
+    // the per-thread runs below read distinct banks
+    extern __shared__ int s_cnt[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < w.ntiles; i += ST_THREADS) s_cnt[i + (i >> 5)] = w.tile_count[i];
+    __syncthreads();
     const int per = (w.ntiles + ST_THREADS - 1) / ST_THREADS;
     const int b0 = tid * per;
     int sum = 0;
     for (int i = 0; i < per; ++i)
-        if (b0 + i < w.ntiles) sum += w.tile_count[b0 + i];
+        if (b0 + i < w.ntiles) sum += s_cnt[b0 + i + ((b0 + i) >> 5)];
     int x = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -320,13 +325,22 @@ __global__ void __launch_bounds__(ST_THREADS) k_scan_tiles(Ws w) {
     }
     if (lane == 31) s_w[warp] = x;
     __syncthreads();
-    int before = 0;
-    for (int k = 0; k < warp; ++k) before += s_w[k];
-    int run = x - sum + before;
+    if (warp == 0) {                     // exclusive scan of the warp totals
+        const int tv = s_w[lane];
+        int z = tv;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, z, o);
+            if (lane >= o) z += y;
+        }
+        s_w[lane] = z - tv;
+    }
+    __syncthreads();
+    int run = x - sum + s_w[warp];
     for (int i = 0; i < per; ++i)
         if (b0 + i < w.ntiles) {
             w.tile_start[b0 + i] = run;
-            run += w.tile_count[b0 + i];
+            run += s_cnt[b0 + i + ((b0 + i) >> 5)];
         }
     if (tid == ST_THREADS - 1) w.tile_start[w.ntiles] = run;
     // Processing order of the persistent blend kernels: a counting sort of
@@ -340,7 +354,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_scan_tiles(Ws w) {
     auto key = [](int c) { return 255 - min(c >> 2, 255); };
     for (int i = 0; i < per; ++i) {
         const bool ok = b0 + i < w.ntiles;
-        const int k = ok ? key(w.tile_count[b0 + i]) : -1;
+        const int k = ok ? key(s_cnt[b0 + i + ((b0 + i) >> 5)]) : -1;
         const unsigned grp = __match_any_sync(0xffffffffu, k);
         if (ok && lane == __ffs(grp) - 1) atomicAdd(&s_hist[k], __popc(grp));
     }
@@ -365,7 +379,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_scan_tiles(Ws w) {
     __syncthreads();
     for (int i = 0; i < per; ++i) {
         const bool ok = b0 + i < w.ntiles;
-        const int k = ok ? key(w.tile_count[b0 + i]) : -1;
+        const int k = ok ? key(s_cnt[b0 + i + ((b0 + i) >> 5)]) : -1;
         const unsigned grp = __match_any_sync(0xffffffffu, k);
         const int leader = __ffs(grp) - 1;
         int base = 0;
@@ -640,100 +654,85 @@ __global__ void __launch_bounds__(PRE_THREADS) k_pre_count(PreArgs a, Ws w) {
         w.warp_mask[wid] = mask;
         w.warp_cnt[2 * wid] = __popc(mask);
         w.warp_cnt[2 * wid + 1] = t;
+        if (mask) {                      // chunk totals for the scan (integer: order-free)
+            atomicAdd(&w.chunk_cnt[2 * (wid >> 10)], __popc(mask));
+            atomicAdd(&w.chunk_cnt[2 * (wid >> 10) + 1], t);
+        }
     }
 }
 
-constexpr int PS_THREADS = 1024;
-constexpr int PS_ITEMS = 8;          // warp counts per thread and pass (4 x 16-B loads)
-// One CTA scans the per-warp (visible, tile) counts in passes of
-// PS_THREADS x PS_ITEMS: every thread loads its 8 consecutive pairs with
-// vector loads (all in flight at once), scans them locally, and one block
-// scan + a running carry place them — coalesced, a handful of memory
-// latencies per pass instead of one per count.
+constexpr int PS_THREADS = 1024;     // preprocess warps per scan chunk (one CTA each)
+// Exclusive scan of the per-warp (visible, tile) counts, one CTA per chunk
+// of 1024 warps: the chunk's base is the sum of the earlier chunks' totals
+// (k_pre_count adds them with integer atomics), then one block scan.  Wide
+// and single-pass: every SM pulls its own slice (a one-CTA scan is bound by
+// one SM's memory parallelism, ~40 us for config 5's 64K warps).
 __global__ void __launch_bounds__(PS_THREADS) k_pre_scan(Ws w, int64_t nw) {
-    __shared__ long long s_v[PS_THREADS / 32], s_t[PS_THREADS / 32];
+    __shared__ int s_v[PS_THREADS / 32], s_t[PS_THREADS / 32], s_pass[2];
+    __shared__ long long s_base[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const bool vec = ((uintptr_t)w.warp_cnt & 15) == 0 && ((uintptr_t)w.warp_off & 15) == 0;
-    long long carry_v = 0, carry_t = 0;
-    for (int64_t base = 0; base < nw; base += (int64_t)PS_THREADS * PS_ITEMS) {
-        const int64_t b0 = base + (int64_t)tid * PS_ITEMS;
-        int c[2 * PS_ITEMS];
-        if (vec && b0 + PS_ITEMS <= nw) {
-#pragma unroll
-            for (int q = 0; q < PS_ITEMS / 2; ++q) {
-                const int4 x = *(const int4*)(w.warp_cnt + 2 * b0 + 4 * q);
-                c[4 * q] = x.x;
-                c[4 * q + 1] = x.y;
-                c[4 * q + 2] = x.z;
-                c[4 * q + 3] = x.w;
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < PS_ITEMS; ++k) {
-                const bool in = b0 + k < nw;
-                c[2 * k] = in ? w.warp_cnt[2 * (b0 + k)] : 0;
-                c[2 * k + 1] = in ? w.warp_cnt[2 * (b0 + k) + 1] : 0;
-            }
+    const int c = blockIdx.x, nchunk = gridDim.x;
+    if (warp == 0) {                     // base = totals of the chunks before this one
+        long long bv = 0, bt = 0;
+        for (int k = lane; k < c; k += 32) {
+            bv += w.chunk_cnt[2 * k];
+            bt += w.chunk_cnt[2 * k + 1];
         }
-        long long sv = 0, st = 0;
 #pragma unroll
-        for (int k = 0; k < PS_ITEMS; ++k) {
-            sv += c[2 * k];
-            st += c[2 * k + 1];
+        for (int o = 16; o > 0; o >>= 1) {
+            bv += __shfl_xor_sync(0xffffffffu, bv, o);
+            bt += __shfl_xor_sync(0xffffffffu, bt, o);
         }
-        long long xv = sv, xt = st;
+        if (lane == 0) {
+            s_base[0] = bv;
+            s_base[1] = bt;
+        }
+    }
+    const int64_t wid = (int64_t)c * PS_THREADS + tid;
+    int2 cv = make_int2(0, 0);
+    if (wid < nw) cv = *(const int2*)(w.warp_cnt + 2 * wid);
+    int xv = cv.x, xt = cv.y;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int yv = __shfl_up_sync(0xffffffffu, xv, o), yt = __shfl_up_sync(0xffffffffu, xt, o);
+        if (lane >= o) {
+            xv += yv;
+            xt += yt;
+        }
+    }
+    if (lane == 31) {
+        s_v[warp] = xv;
+        s_t[warp] = xt;
+    }
+    __syncthreads();
+    if (warp == 0) {                     // exclusive scan of the warp totals
+        const int tv = s_v[lane], tt = s_t[lane];
+        int zv = tv, zt = tt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const long long yv = __shfl_up_sync(0xffffffffu, xv, o), yt = __shfl_up_sync(0xffffffffu, xt, o);
+            const int yv = __shfl_up_sync(0xffffffffu, zv, o), yt = __shfl_up_sync(0xffffffffu, zt, o);
             if (lane >= o) {
-                xv += yv;
-                xt += yt;
+                zv += yv;
+                zt += yt;
             }
         }
+        s_v[lane] = zv - tv;
+        s_t[lane] = zt - tt;
         if (lane == 31) {
-            s_v[warp] = xv;
-            s_t[warp] = xt;
+            s_pass[0] = zv;
+            s_pass[1] = zt;
         }
-        __syncthreads();
-        long long bv = 0, bt = 0, tv = 0, tt = 0;
-        for (int k = 0; k < PS_THREADS / 32; ++k) {
-            if (k < warp) {
-                bv += s_v[k];
-                bt += s_t[k];
-            }
-            tv += s_v[k];
-            tt += s_t[k];
-        }
-        __syncthreads();                 // s_v / s_t reused by the next pass
-        long long rv = carry_v + xv - sv + bv, rt = carry_t + xt - st + bt;
-        int o[2 * PS_ITEMS];
-#pragma unroll
-        for (int k = 0; k < PS_ITEMS; ++k) {
-            o[2 * k] = (int32_t)rv;
-            o[2 * k + 1] = (int32_t)min(rt, 0x7fffffffll);
-            rv += c[2 * k];
-            rt += c[2 * k + 1];
-        }
-        if (vec && b0 + PS_ITEMS <= nw) {
-#pragma unroll
-            for (int q = 0; q < PS_ITEMS / 2; ++q)
-                *(int4*)(w.warp_off + 2 * b0 + 4 * q) = make_int4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
-        } else {
-#pragma unroll
-            for (int k = 0; k < PS_ITEMS; ++k)
-                if (b0 + k < nw) {
-                    w.warp_off[2 * (b0 + k)] = o[2 * k];
-                    w.warp_off[2 * (b0 + k) + 1] = o[2 * k + 1];
-                }
-        }
-        carry_v += tv;
-        carry_t += tt;
     }
-    if (tid == 0) {
-        w.ctr[0] = (unsigned long long)carry_v;
-        w.ctr[1] = (unsigned long long)carry_t;
-        w.vis_ebase[carry_v] = (int32_t)min(carry_t, 0x7fffffffll);
-        if (carry_t > w.cap) w.ctr[2] = 1;
+    __syncthreads();
+    const long long rv = s_base[0] + (xv - cv.x + s_v[warp]);
+    const long long rt = s_base[1] + (xt - cv.y + s_t[warp]);
+    if (wid < nw) *(int2*)(w.warp_off + 2 * wid) = make_int2((int32_t)rv, (int32_t)min(rt, 0x7fffffffll));
+    if (c == nchunk - 1 && tid == 0) {
+        const long long tv = s_base[0] + s_pass[0], tt = s_base[1] + s_pass[1];
+        w.ctr[0] = (unsigned long long)tv;
+        w.ctr[1] = (unsigned long long)tt;
+        w.vis_ebase[tv] = (int32_t)min(tt, 0x7fffffffll);
+        if (tt > w.cap) w.ctr[2] = 1;
     }
 }
 
@@ -776,10 +775,13 @@ cudaError_t launch_preprocess(const lsb_params& p, const lsb_camera& cam, const 
         const int64_t nw = (p.n + 31) / 32;
         const unsigned nb = (unsigned)((p.n + PRE_THREADS - 1) / PRE_THREADS);
         if (p.n > 0) k_pre_count<<<nb, PRE_THREADS, 0, st>>>(a, w);
-        k_pre_scan<<<1, PS_THREADS, 0, st>>>(w, nw);
+        k_pre_scan<<<(unsigned)((nw + PS_THREADS - 1) / PS_THREADS > 0 ? (nw + PS_THREADS - 1) / PS_THREADS : 1),
+                     PS_THREADS, 0, st>>>(w, nw);
         if (p.n > 0) k_pre_emit<<<nb, PRE_THREADS, 0, st>>>(a, w);
     }
-    k_scan_tiles<<<1, ST_THREADS, 0, st>>>(w);
+    const int st_smem = (int)sizeof(int) * (w.ntiles + w.ntiles / 32 + 1);
+    if (st_smem > 48 * 1024) cudaFuncSetAttribute(k_scan_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, st_smem);
+    k_scan_tiles<<<1, ST_THREADS, st_smem, st>>>(w);
     k_scatter_emitted<<<8 * 148, 256, 0, st>>>(w);
     k_tile_sort<<<(w.ntiles + 3) / 4, 128, 0, st>>>(w);
     cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_sort_smem());
