@@ -222,6 +222,7 @@ def run_ours(args, wl, rank, world, local_rank):
     # L2 flush between timed steps: a write larger than the 126 MB L2, issued
     # outside each step's event pair
     flush_buf = torch.empty(64 * 2 ** 20, dtype=torch.int32, device=dev)
+    spreads = []
 
     def timed(run_one):
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -233,7 +234,10 @@ def run_ours(args, wl, rank, world, local_rank):
                 run_one()
                 b.record(stream)
         torch.cuda.synchronize()
-        return float(np.mean([a.elapsed_time(b) for a, b in evs]))
+        # the median step; the spread is kept for the JSON line
+        ts = [a.elapsed_time(b) for a, b in evs]
+        spreads.append((float(np.min(ts)), float(np.max(ts))))
+        return float(np.median(ts))
     stream = torch.cuda.Stream(dev)
     eng = WindowEngine(win, wl["cam"], [wl["views"][v] for v in my_views], settings, OptimConfig(),
                        n_views_total=V, stream=stream, lanes=args.lanes)
@@ -396,7 +400,9 @@ def run_ours(args, wl, rank, world, local_rank):
                        "frames": ("8-bit (H,W,3), u/255.0 on the device like read_ppm" if args.frames == "u8"
                                   else "float32 (H,W,3)"),
                        "l2": "flushed before every timed step (256 MB write outside the step's event pair)",
-                       "timing": "CUDA events around each step on the launching stream, mean over steps",
+                       "timing": "CUDA events around each step on the launching stream, median over steps",
+                       "step_ms_min_max": {"serial": spreads[0], "headline": spreads[1],
+                                           "e2e": spreads[2] if len(spreads) > 2 else None},
                        "loss_last_step": float(np.mean(losses))},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "peak_source": hbm_src,
                          "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
