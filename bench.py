@@ -741,6 +741,10 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: run every rank on GPU 0 (exercises the N > 1 path on a
+    # one-GPU box; with LSB_BENCH_BACKEND=gloo, since NCCL needs one GPU per rank)
+    if os.environ.get("LSB_BENCH_SHARE_GPU") == "1":
+        local_rank = 0
     if args.config == "cfg3":
         run_voxel(args, rank, world, local_rank)
         return
@@ -761,7 +765,11 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("LSB_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     run_ours(args, wl, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
