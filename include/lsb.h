@@ -267,14 +267,17 @@ int lsb_pose_prepare(const lsb_params* p, const lsb_camera* cam, const lsb_pose*
                      float* chain, void* stream);
 int lsb_pose_rows(const lsb_settings* s, int sh_degree_used, void* ws, size_t ws_bytes,
                   const lsb_dims* dims, const float* image, const int32_t* n_contrib,
-                  const float* chain, const int32_t* pixel_ids, int64_t m, const double* A,
-                  const double* R_cw, double* rows_out, void* stream);
-/* out (42 doubles): [0..35] sum h h^T / sigma^2 (6x6), [36..41] sum h z / sigma^2,
+                  const float* chain, const int32_t* pixel_ids, int64_t m, const int64_t* m_dev,
+                  const double* A, const double* R_cw, double* rows_out, void* stream);
+/* m_dev (lsb_pose_rows, lsb_hb_reduce; may be NULL): a device count — only
+ * the first min(*m_dev, m) ids / rows are used, so a count produced on the
+ * device (lsb_visual_select's kept count, counts + 2) needs no host read.
+ * out (42 doubles): [0..35] sum h h^T / sigma^2 (6x6), [36..41] sum h z / sigma^2,
  * h = -row (the pose block of H).  Deterministic: fixed-grid CTA partials in
  * `scratch` (lsb_hb_scratch_doubles() doubles), then a fixed-order sum. */
 int lsb_hb_scratch_doubles(void);
-int lsb_hb_reduce(const double* rows, const double* z, int64_t m, double inv_sigma2, double* out, double* scratch,
-                  void* stream);
+int lsb_hb_reduce(const double* rows, const double* z, int64_t m, const int64_t* m_dev, double inv_sigma2,
+                  double* out, double* scratch, void* stream);
 /* Semi-dense candidate mask (estimator.py:241-252): Sobel/8 magnitude of the
  * grey observed image (nearest border) > grad_thr and t_final < t_max. */
 int lsb_semidense_mask(const float* observed, const float* t_final, int32_t width, int32_t height,

@@ -102,9 +102,9 @@ SIGNATURES = [
     ("lsb_pose_prepare", _c.c_int, [_c.POINTER(Params), _c.POINTER(Camera), _c.POINTER(Pose),
                                     _c.POINTER(Settings), _P, _c.c_size_t, _c.POINTER(Dims), _P, _P]),
     ("lsb_pose_rows", _c.c_int, [_c.POINTER(Settings), _c.c_int, _P, _c.c_size_t, _c.POINTER(Dims), _P, _P, _P,
-                                 _P, _c.c_int64, _c.POINTER(_c.c_double), _c.POINTER(_c.c_double), _P, _P]),
+                                 _P, _c.c_int64, _P, _c.POINTER(_c.c_double), _c.POINTER(_c.c_double), _P, _P]),
     ("lsb_hb_scratch_doubles", _c.c_int, []),
-    ("lsb_hb_reduce", _c.c_int, [_P, _P, _c.c_int64, _c.c_double, _P, _P, _P]),
+    ("lsb_hb_reduce", _c.c_int, [_P, _P, _c.c_int64, _P, _c.c_double, _P, _P, _P]),
     ("lsb_visual_select_scratch_bytes", _c.c_int64, [_c.c_int64, _c.c_int32]),
     ("lsb_visual_select", _c.c_int, [_P, _P, _P, _c.c_int64, _c.c_int32, _c.c_double, _P, _P, _P, _P, _P]),
     ("lsb_semidense_mask", _c.c_int, [_P, _P, _c.c_int32, _c.c_int32, _c.c_double, _c.c_double, _P, _P]),

@@ -29,9 +29,9 @@ int adam_max_peers();
 cudaError_t launch_pose_prepare(const Ws&, const lsb_params&, const lsb_camera&, const lsb_pose&,
                                 const lsb_settings&, float*, cudaStream_t);
 cudaError_t launch_pose_rows(const Ws&, const lsb_settings&, int, int, int, const float*, const int32_t*,
-                             const float*, const int32_t*, int64_t, const double*, const double*, double*,
-                             cudaStream_t);
-cudaError_t launch_hb(const double*, const double*, int64_t, double, double*, double*, cudaStream_t);
+                             const float*, const int32_t*, int64_t, const int64_t*, const double*, const double*,
+                             double*, cudaStream_t);
+cudaError_t launch_hb(const double*, const double*, int64_t, const int64_t*, double, double*, double*, cudaStream_t);
 int hb_scratch_doubles();
 cudaError_t launch_visual_select(const uint8_t*, const float*, const float*, int64_t, int, double, void*, int32_t*,
                                  double*, int64_t*, cudaStream_t);
@@ -362,22 +362,22 @@ int lsb_pose_prepare(const lsb_params* p, const lsb_camera* cam, const lsb_pose*
 
 int lsb_pose_rows(const lsb_settings* s, int sh_degree_used, void* ws, size_t ws_bytes, const lsb_dims* d,
                   const float* image, const int32_t* n_contrib, const float* chain, const int32_t* ids, int64_t m,
-                  const double* A, const double* R_cw, double* rows, void* stream) {
+                  const int64_t* m_dev, const double* A, const double* R_cw, double* rows, void* stream) {
     if (!s || !A || !R_cw) return fail(LSB_EINVAL, "NULL argument");
     if (m > 0 && (!image || !n_contrib || !chain || !ids || !rows)) return fail(LSB_EINVAL, "NULL array");
     Ws w;
     int rc = get_ws(ws, ws_bytes, d, &w);
     if (rc) return rc;
     return check_cuda(launch_pose_rows(w, *s, sh_degree_used, d->width, d->height, image, n_contrib, chain, ids, m,
-                                       A, R_cw, rows, (cudaStream_t)stream), "pose_rows");
+                                       m_dev, A, R_cw, rows, (cudaStream_t)stream), "pose_rows");
 }
 
 int lsb_hb_scratch_doubles(void) { return hb_scratch_doubles(); }
 
-int lsb_hb_reduce(const double* rows, const double* z, int64_t m, double inv_sigma2, double* out, double* scratch,
-                  void* stream) {
+int lsb_hb_reduce(const double* rows, const double* z, int64_t m, const int64_t* m_dev, double inv_sigma2,
+                  double* out, double* scratch, void* stream) {
     if (!out || !scratch || (m > 0 && (!rows || !z))) return fail(LSB_EINVAL, "NULL argument");
-    return check_cuda(launch_hb(rows, z, m, inv_sigma2, out, scratch, (cudaStream_t)stream), "hb_reduce");
+    return check_cuda(launch_hb(rows, z, m, m_dev, inv_sigma2, out, scratch, (cudaStream_t)stream), "hb_reduce");
 }
 
 int lsb_semidense_mask(const float* obs, const float* tfin, int32_t W, int32_t H, double thr, double tmax,

@@ -205,9 +205,11 @@ __device__ __forceinline__ float warp_scan_add_incl(float v, int lane, float& to
 __global__ void __launch_bounds__(128) k_pose_rows(Ws w, RowArgs a, const float* __restrict__ image,
                                                    const int32_t* __restrict__ n_contrib,
                                                    const float* __restrict__ chain, const int32_t* __restrict__ ids,
-                                                   int64_t m, double* __restrict__ rows) {
+                                                   int64_t m, const int64_t* __restrict__ m_dev,
+                                                   double* __restrict__ rows) {
     const int lane = threadIdx.x & 31;
     const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (m_dev && *m_dev < m) m = *m_dev;
     if (r >= m) return;
     const int p = ids[r];
     const int px = p % a.W, py = p / a.W;
@@ -310,7 +312,9 @@ __global__ void __launch_bounds__(128) k_pose_rows(Ws w, RowArgs a, const float*
 // in CTA order.  Deterministic; every row is read once.
 constexpr int HB_BLOCKS = 296, HB_VALS = 27;
 __global__ void __launch_bounds__(256) k_hb_partial(const double* __restrict__ rows, const double* __restrict__ z,
-                                                    int64_t m, double* __restrict__ part) {
+                                                    int64_t m, const int64_t* __restrict__ m_dev,
+                                                    double* __restrict__ part) {
+    if (m_dev && *m_dev < m) m = *m_dev;
     __shared__ double s[HB_VALS][256 / 32];
     double v[HB_VALS];
 #pragma unroll
@@ -395,7 +399,7 @@ cudaError_t launch_pose_prepare(const Ws& w, const lsb_params& p, const lsb_came
 
 cudaError_t launch_pose_rows(const Ws& w, const lsb_settings& s, int degree, int W, int H, const float* image,
                              const int32_t* n_contrib, const float* chain, const int32_t* ids, int64_t m,
-                             const double* A, const double* Rcw, double* rows, cudaStream_t st) {
+                             const int64_t* m_dev, const double* A, const double* Rcw, double* rows, cudaStream_t st) {
     RowArgs a;
     a.W = W; a.H = H; a.clamp = (float)s.alpha_clamp; a.cut = (float)s.alpha_cut; a.degree = degree;
     a.iclamp = (float)(1.0 / s.alpha_clamp);
@@ -403,13 +407,14 @@ cudaError_t launch_pose_rows(const Ws& w, const lsb_settings& s, int degree, int
     for (int k = 0; k < 9; ++k) a.Rcw[k] = Rcw[k];
     if (m == 0) return cudaSuccess;
     const int64_t threads = m * 32;
-    k_pose_rows<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(w, a, image, n_contrib, chain, ids, m, rows);
+    k_pose_rows<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(w, a, image, n_contrib, chain, ids, m, m_dev,
+                                                                      rows);
     return cudaGetLastError();
 }
 
-cudaError_t launch_hb(const double* rows, const double* z, int64_t m, double inv_s2, double* out, double* part,
-                      cudaStream_t st) {
-    k_hb_partial<<<HB_BLOCKS, 256, 0, st>>>(rows, z, m, part);
+cudaError_t launch_hb(const double* rows, const double* z, int64_t m, const int64_t* m_dev, double inv_s2, double* out,
+                      double* part, cudaStream_t st) {
+    k_hb_partial<<<HB_BLOCKS, 256, 0, st>>>(rows, z, m, m_dev, part);
     k_hb_final<<<1, 32, 0, st>>>(part, HB_BLOCKS, inv_s2, out);
     return cudaGetLastError();
 }

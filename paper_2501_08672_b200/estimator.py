@@ -21,7 +21,8 @@ import torch
 from . import _lib
 from .errors import NoAssociations, SingularGain, TooFewPixels
 from .geometry import SE3, so3_exp, so3_left_jacobian, so3_log, so3_right_jacobian_inv
-from .raster import RasterSettings, _f32, pose_rows, render
+from .raster import (_CAP_HINT, RasterSettings, RenderState, _as_arrays, _degree_used, _f32, pose_rows, render,
+                     render_fwd)
 
 DIM = 15
 
@@ -112,7 +113,7 @@ class Measurement:
         out = torch.empty(42, dtype=torch.float64, device=self.z_dev.device)
         scratch = torch.empty(lib.lsb_hb_scratch_doubles(), dtype=torch.float64, device=self.z_dev.device)
         _lib.check(lib.lsb_hb_reduce(ctypes.c_void_p(self.rows_dev.data_ptr()), ctypes.c_void_p(self.z_dev.data_ptr()),
-                                     m, float(inv), ctypes.c_void_p(out.data_ptr()),
+                                     m, None, float(inv), ctypes.c_void_p(out.data_ptr()),
                                      ctypes.c_void_p(scratch.data_ptr()), _lib.stream_ptr()), "hb_reduce")
         o = out.cpu().numpy()
         return o[:36].reshape(6, 6), o[36:]
@@ -209,6 +210,100 @@ def lidar_measurement(state: NavState, points_l, vmap, T_il, cfg: FilterConfig,
     return Measurement(rows_dev=rows[:n][k].contiguous(), z_dev=z[:n][k].contiguous(), sigma2=cfg.lidar_sigma ** 2)
 
 
+class _VisualPass:
+    """The device side of one visual IESKF iteration with ONE host sync:
+    render (contributing lists) -> semi-dense mask -> selection / residual /
+    gate (lsb_visual_select) -> pose chain -> pose rows -> H/b, the kept
+    count staying on the device (the m_dev arguments); the counts, the
+    intersection overflow flag and the 42 H/b numbers come back in one
+    read.  Buffers persist across the iterations of an update.  Same kernels
+    and the same bits as visual_measurement(...).hb() (tested)."""
+
+    def __init__(self, window, observed, cam, cfg: FilterConfig, settings: RasterSettings):
+        self.arrays = _as_arrays(window)
+        self.cam, self.cfg, self.settings = cam, cfg, settings
+        dev = self.arrays.device
+        self.h, self.w = h, w = int(cam.height), int(cam.width)
+        self.bin_mode = 1 if settings.alpha_cut > 0 else 0
+        self.key = (len(self.arrays), w, h, float(settings.alpha_cut), self.bin_mode)
+        self.cap = max(_CAP_HINT.get(self.key, 0), 1 << 16, 8 * len(self.arrays))
+        self.obs = _f32(observed, (h, w, 3), dev)
+        self.image = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
+        self.t_final = torch.empty((h, w), dtype=torch.float32, device=dev)
+        self.n_contrib = torch.empty((h, w), dtype=torch.int32, device=dev)
+        lib = _lib.load()
+        npx, B = h * w, int(cfg.pixel_budget)
+        self.mask = torch.empty(npx, dtype=torch.uint8, device=dev)
+        self.scratch = torch.empty(int(lib.lsb_visual_select_scratch_bytes(npx, B)), dtype=torch.uint8, device=dev)
+        self.ids = torch.empty(B, dtype=torch.int32, device=dev)
+        self.res = torch.empty(B, dtype=torch.float64, device=dev)
+        self.rows = torch.zeros((B, 6), dtype=torch.float64, device=dev)
+        self.chain = torch.empty((max(len(self.arrays), 1), 48), dtype=torch.float32, device=dev)
+        self.hb_scratch = torch.empty(lib.lsb_hb_scratch_doubles(), dtype=torch.float64, device=dev)
+        # one device buffer read back per iteration: [L, selected, kept] + the
+        # render counters [M, I, overflow] as int64, then the 42 H/b doubles
+        self.dev_out = torch.empty(6 + 42, dtype=torch.float64, device=dev)
+        self.host_out = torch.empty(6 + 42, dtype=torch.float64).pin_memory()
+        self.state = None
+
+    def run(self, nav: NavState, T_ic):
+        from .geometry import imu_camera_adjoint
+        lib = _lib.load()
+        T_cw = (nav.T_WI @ T_ic).inverse()
+        cfg, B = self.cfg, int(self.cfg.pixel_budget)
+        while True:
+            if self.state is None or self.state.dims.isect_cap != self.cap:
+                self.state = RenderState(self.arrays, self.cam, T_cw.R, T_cw.t, self.settings, self.cap,
+                                         self.bin_mode)
+            else:
+                self.state.set_pose(T_cw.R, T_cw.t)
+            st = self.state
+            sp = _lib.stream_ptr()
+            render_fwd(st, self.image, self.t_final, self.n_contrib)
+            cnt = self.dev_out[:6].view(torch.int64)
+            _lib.check(lib.lsb_semidense_mask(ctypes.c_void_p(self.obs.data_ptr()),
+                                              ctypes.c_void_p(self.t_final.data_ptr()), self.w, self.h,
+                                              float(cfg.grad_threshold), float(cfg.coverage_max_transmittance),
+                                              ctypes.c_void_p(self.mask.data_ptr()), sp), "semidense")
+            _lib.check(lib.lsb_visual_select(ctypes.c_void_p(self.mask.data_ptr()), ctypes.c_void_p(self.obs.data_ptr()),
+                                             ctypes.c_void_p(self.image.data_ptr()), self.h * self.w, B,
+                                             float(cfg.photo_gate), ctypes.c_void_p(self.scratch.data_ptr()),
+                                             ctypes.c_void_p(self.ids.data_ptr()), ctypes.c_void_p(self.res.data_ptr()),
+                                             ctypes.c_void_p(cnt.data_ptr()), sp), "visual_select")
+            kept = ctypes.c_void_p(cnt.data_ptr() + 16)          # counts[2], on the device
+            p = st.arrays.params()
+            _lib.check(lib.lsb_pose_prepare(ctypes.byref(p), ctypes.byref(st.c_cam), ctypes.byref(st.c_pose),
+                                            ctypes.byref(st.c_set), st._ws(), st.ws_bytes, ctypes.byref(st.dims),
+                                            ctypes.c_void_p(self.chain.data_ptr()), sp), "pose_prepare")
+            A = imu_camera_adjoint(st.R_cw, T_ic)
+            Ac = (ctypes.c_double * 36)(*A.ravel().tolist())
+            Rc = (ctypes.c_double * 9)(*st.R_cw.ravel().tolist())
+            _lib.check(lib.lsb_pose_rows(ctypes.byref(st.c_set), _degree_used(st), st._ws(), st.ws_bytes,
+                                         ctypes.byref(st.dims), ctypes.c_void_p(self.image.data_ptr()),
+                                         ctypes.c_void_p(self.n_contrib.data_ptr()),
+                                         ctypes.c_void_p(self.chain.data_ptr()), ctypes.c_void_p(self.ids.data_ptr()),
+                                         B, kept, Ac, Rc, ctypes.c_void_p(self.rows.data_ptr()), sp), "pose_rows")
+            _lib.check(lib.lsb_hb_reduce(ctypes.c_void_p(self.rows.data_ptr()), ctypes.c_void_p(self.res.data_ptr()),
+                                         B, kept, 1.0 / float(cfg.photo_sigma) ** 2,
+                                         ctypes.c_void_p(self.dev_out.data_ptr() + 48),
+                                         ctypes.c_void_p(self.hb_scratch.data_ptr()), sp), "hb_reduce")
+            cnt[3:6].copy_(st.ws[:24].view(torch.int64))       # the render's [M, I, overflow] counters
+            self.host_out.copy_(self.dev_out, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            c = self.host_out[:6].view(torch.int64).tolist()
+            _, n_sel, n_ok, _, I, overflow = c
+            if not overflow:
+                break
+            self.cap = int(I * 1.25) + 1024                  # grow and redo (rare)
+        _CAP_HINT[self.key] = int(I * 1.25) + 1024
+        if n_sel < cfg.min_pixels:
+            raise TooFewPixels(f"{n_sel} < {cfg.min_pixels}")
+        if n_ok < cfg.min_pixels:
+            raise TooFewPixels(f"{n_ok} < {cfg.min_pixels} after gating")
+        o = self.host_out[6:].numpy()
+        return o[:36].reshape(6, 6).copy(), o[36:].copy()
+
+
 def ieskf_visual_update(state: NavState, cov: np.ndarray, observed, window, cam, T_ic, cfg: FilterConfig,
                         settings: RasterSettings, max_iter: int = 5, step_tol: float = 1e-6,
                         bias_limit: float = 0.5):
@@ -219,9 +314,9 @@ def ieskf_visual_update(state: NavState, cov: np.ndarray, observed, window, cam,
     K z = S^-1 b and K H = S^-1 A (H is zero outside its 6 pose columns)."""
     x_bar, x_hat = state, state.clone()
     K_H = P = None
+    vis = _VisualPass(window, observed, cam, cfg, settings)
     for _ in range(max_iter):
-        meas = visual_measurement(x_hat, observed, window, cam, T_ic, cfg, settings)
-        A6, b6 = meas.hb()
+        A6, b6 = vis.run(x_hat, T_ic)
         delta = x_hat.boxminus(x_bar)
         Hj_inv = np.eye(DIM)
         Hj_inv[0:3, 0:3] = so3_left_jacobian(-delta[0:3])

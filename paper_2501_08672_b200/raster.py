@@ -474,6 +474,6 @@ def pose_rows(out: RenderOutput, pixel_ids, T_ic=None, as_numpy: bool = True):
         _lib.check(lib.lsb_pose_rows(ctypes.byref(state.c_set), _degree_used(state), state._ws(), state.ws_bytes,
                                      ctypes.byref(state.dims), ctypes.c_void_p(out.image.data_ptr()),
                                      ctypes.c_void_p(out.contrib_count.data_ptr()), ctypes.c_void_p(chain.data_ptr()),
-                                     ctypes.c_void_p(ids.data_ptr()), m, Ac, Rc, ctypes.c_void_p(rows.data_ptr()),
-                                     _lib.stream_ptr()), "pose_rows")
+                                     ctypes.c_void_p(ids.data_ptr()), m, None, Ac, Rc,
+                                     ctypes.c_void_p(rows.data_ptr()), _lib.stream_ptr()), "pose_rows")
     return rows.cpu().numpy() if as_numpy else rows

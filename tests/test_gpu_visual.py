@@ -97,3 +97,24 @@ def test_device_selection_budget_and_gate(budget, gate):
     meas = visual_measurement(NavState(T_wi), d["observed"], arrays, cam, T_ic, cfg, st)
     torch.cuda.synchronize()
     assert np.array_equal(meas.z, res)
+
+
+def test_single_sync_pass_bit_identical_to_measurement():
+    """The IESKF iteration's one-sync device pass (_VisualPass: the kept count
+    stays on the device for the pose rows and H/b) gives the same bits as
+    visual_measurement(...).hb(), and raises TooFewPixels the same way."""
+    from paper_2501_08672_b200.errors import TooFewPixels
+    from paper_2501_08672_b200.estimator import FilterConfig, NavState, _VisualPass, visual_measurement
+    from paper_2501_08672_b200.raster import RasterSettings
+    d, arrays, cam, T_wi, T_ic = _setup()
+    st = RasterSettings(alpha_cut=1 / 255)
+    for budget in (1024, 64):
+        cfg = FilterConfig(pixel_budget=budget, min_pixels=10)
+        A, b = visual_measurement(NavState(T_wi), d["observed"], arrays, cam, T_ic, cfg, st).hb()
+        vis = _VisualPass(arrays, d["observed"], cam, cfg, st)
+        for _ in range(2):                       # buffers reused across iterations
+            A2, b2 = vis.run(NavState(T_wi), T_ic)
+            assert np.array_equal(A, A2) and np.array_equal(b, b2)
+    with pytest.raises(TooFewPixels):
+        _VisualPass(arrays, np.zeros_like(d["observed"]), cam, FilterConfig(min_pixels=10 ** 6), st).run(
+            NavState(T_wi), T_ic)
