@@ -62,6 +62,13 @@ constexpr int RUN = 4;       // pixels per lane and row (horizontal run)
 #ifndef BWD_MIN_BLOCKS
 #define BWD_MIN_BLOCKS 5
 #endif
+#ifndef BWD_UNROLL
+#define BWD_UNROLL 1          // record-loop unroll of the backward walk
+#endif
+#ifndef FUSED_FWD_UNROLL
+#define FUSED_FWD_UNROLL 1    // record-loop unroll of the fused kernel's forward walk
+#endif
+constexpr int kBwdUnroll = BWD_UNROLL, kFusedFwdUnroll = FUSED_FWD_UNROLL;
 
 struct BlendArgs {
     int W, H;
@@ -524,6 +531,7 @@ __device__ __forceinline__ void bwd_walk(const Ws& w, const BlendArgs& a, RecPip
         const int ecur = base + lane < end ? w.tile_e[base + lane] : 0;
         const Rec* sr = pipe.next(w, b, lane);
         const int nb = min(32, end - base);
+#pragma unroll kBwdUnroll
         for (int k = 0; k < nb; ++k) {
             const float4 q0 = *(const float4*)&sr[k].mxh;        // mxh myh mxl myl
             const float4 q1 = *(const float4*)&sr[k].A;          // A s E lop
@@ -743,6 +751,7 @@ k_blend_fused(Ws w, BlendArgs a, LossArgs L) {
             if (!__any_sync(0xffffffffu, alive)) break;
             const Rec* sr = pipe.next(w, b, lane);
             const int nb = min(32, end - base);
+#pragma unroll kFusedFwdUnroll
             for (int k = 0; k < nb; ++k) {
                 const int4 qi = *(const int4*)&sr[k].bbx;
                 const int cx0 = (qi.x & 0xffff) - gx0, cx1 = (qi.x >> 16) - gx0;
