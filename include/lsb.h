@@ -279,9 +279,11 @@ int lsb_hb_scratch_doubles(void);
 int lsb_hb_reduce(const double* rows, const double* z, int64_t m, const int64_t* m_dev, double inv_sigma2,
                   double* out, double* scratch, void* stream);
 /* Semi-dense candidate mask (estimator.py:241-252): Sobel/8 magnitude of the
- * grey observed image (nearest border) > grad_thr and t_final < t_max. */
-int lsb_semidense_mask(const float* observed, const float* t_final, int32_t width, int32_t height,
-                       double grad_thr, double t_max, uint8_t* mask_out, void* stream);
+ * grey observed image (nearest border) > grad_thr and t_final < t_max.
+ * observed_u8 (here and in lsb_visual_select): the frame is 8-bit, read as
+ * u / 255.0 like LSB_OBS_U8; else float32. */
+int lsb_semidense_mask(const void* observed, int32_t observed_u8, const float* t_final, int32_t width,
+                       int32_t height, double grad_thr, double t_max, uint8_t* mask_out, void* stream);
 
 /* Visual measurement selection, on the device with no host round trip
  * (estimator.py:241-277 after the render): from the semi-dense mask, the
@@ -291,7 +293,8 @@ int lsb_semidense_mask(const float* observed, const float* t_final, int32_t widt
  * counts (device, 3 int64) = [candidates L, selected, kept].  scratch:
  * lsb_visual_select_scratch_bytes(npx, budget) bytes. */
 int64_t lsb_visual_select_scratch_bytes(int64_t npx, int32_t budget);
-int lsb_visual_select(const uint8_t* mask, const float* observed, const float* image, int64_t npx, int32_t budget,
+int lsb_visual_select(const uint8_t* mask, const void* observed, int32_t observed_u8, const float* image, int64_t npx,
+                      int32_t budget,
                       double gate, void* scratch, int32_t* ids_out, double* res_out, int64_t* counts, void* stream);
 
 /* ---- voxel map: replaces HashOctree's batch operations (voxmap.py:99-251)

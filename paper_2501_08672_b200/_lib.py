@@ -106,8 +106,9 @@ SIGNATURES = [
     ("lsb_hb_scratch_doubles", _c.c_int, []),
     ("lsb_hb_reduce", _c.c_int, [_P, _P, _c.c_int64, _P, _c.c_double, _P, _P, _P]),
     ("lsb_visual_select_scratch_bytes", _c.c_int64, [_c.c_int64, _c.c_int32]),
-    ("lsb_visual_select", _c.c_int, [_P, _P, _P, _c.c_int64, _c.c_int32, _c.c_double, _P, _P, _P, _P, _P]),
-    ("lsb_semidense_mask", _c.c_int, [_P, _P, _c.c_int32, _c.c_int32, _c.c_double, _c.c_double, _P, _P]),
+    ("lsb_visual_select", _c.c_int, [_P, _P, _c.c_int32, _P, _c.c_int64, _c.c_int32, _c.c_double, _P, _P, _P, _P,
+                                     _P]),
+    ("lsb_semidense_mask", _c.c_int, [_P, _c.c_int32, _P, _c.c_int32, _c.c_int32, _c.c_double, _c.c_double, _P, _P]),
     ("lsb_voxmap_keys", _c.c_int, [_P, _c.c_int64, _c.c_double, _P, _P]),
     ("lsb_voxmap_insert_points", _c.c_int, [_c.POINTER(VoxMap), _P, _c.c_int64, _c.c_int32, _P, _P]),
     ("lsb_voxmap_try_insert", _c.c_int, [_c.POINTER(VoxMap), _P, _c.c_int64, _c.c_int32, _P, _P, _P]),

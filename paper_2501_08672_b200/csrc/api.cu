@@ -33,10 +33,10 @@ cudaError_t launch_pose_rows(const Ws&, const lsb_settings&, int, int, int, cons
                              double*, cudaStream_t);
 cudaError_t launch_hb(const double*, const double*, int64_t, const int64_t*, double, double*, double*, cudaStream_t);
 int hb_scratch_doubles();
-cudaError_t launch_visual_select(const uint8_t*, const float*, const float*, int64_t, int, double, void*, int32_t*,
+cudaError_t launch_visual_select(const uint8_t*, const void*, bool, const float*, int64_t, int, double, void*, int32_t*,
                                  double*, int64_t*, cudaStream_t);
 int64_t visual_select_scratch_bytes(int64_t, int);
-cudaError_t launch_semidense(const float*, const float*, int, int, double, double, uint8_t*, cudaStream_t);
+cudaError_t launch_semidense(const void*, bool, const float*, int, int, double, double, uint8_t*, cudaStream_t);
 cudaError_t launch_vox_keys(const double*, int64_t, double, int64_t*, cudaStream_t);
 cudaError_t launch_vox_insert(const lsb_voxmap&, const double*, int64_t, int, int64_t*, cudaStream_t);
 cudaError_t launch_vox_try_insert(const lsb_voxmap&, const double*, int64_t, int32_t, int64_t*, int32_t*,
@@ -380,10 +380,11 @@ int lsb_hb_reduce(const double* rows, const double* z, int64_t m, const int64_t*
     return check_cuda(launch_hb(rows, z, m, m_dev, inv_sigma2, out, scratch, (cudaStream_t)stream), "hb_reduce");
 }
 
-int lsb_semidense_mask(const float* obs, const float* tfin, int32_t W, int32_t H, double thr, double tmax,
-                       uint8_t* out, void* stream) {
+int lsb_semidense_mask(const void* obs, int32_t observed_u8, const float* tfin, int32_t W, int32_t H, double thr,
+                       double tmax, uint8_t* out, void* stream) {
     if (!obs || !tfin || !out || W <= 0 || H <= 0) return fail(LSB_EINVAL, "bad argument");
-    return check_cuda(launch_semidense(obs, tfin, W, H, thr, tmax, out, (cudaStream_t)stream), "semidense");
+    return check_cuda(launch_semidense(obs, observed_u8 != 0, tfin, W, H, thr, tmax, out, (cudaStream_t)stream),
+                      "semidense");
 }
 
 static int vox_ok(const lsb_voxmap* m) {
@@ -587,11 +588,12 @@ int64_t lsb_visual_select_scratch_bytes(int64_t npx, int32_t budget) {
     return visual_select_scratch_bytes(npx, budget);
 }
 
-int lsb_visual_select(const uint8_t* mask, const float* observed, const float* image, int64_t npx, int32_t budget,
+int lsb_visual_select(const uint8_t* mask, const void* observed, int32_t observed_u8, const float* image, int64_t npx,
+                      int32_t budget,
                       double gate, void* scratch, int32_t* ids_out, double* res_out, int64_t* counts, void* stream) {
     if (!mask || !observed || !image || !scratch || !ids_out || !res_out || !counts || npx < 0 || budget < 1)
         return fail(LSB_EINVAL, "bad argument");
-    return check_cuda(launch_visual_select(mask, observed, image, npx, budget, gate, scratch, ids_out,
+    return check_cuda(launch_visual_select(mask, observed, observed_u8 != 0, image, npx, budget, gate, scratch, ids_out,
                                            res_out, counts, (cudaStream_t)stream),
                       "visual_select");
 }

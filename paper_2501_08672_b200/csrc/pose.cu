@@ -368,7 +368,7 @@ __global__ void k_hb_final(const double* __restrict__ part, int nblocks, double 
     out[6 * j + i] = t;
 }
 
-__global__ void __launch_bounds__(256) k_semidense(const float* __restrict__ obs, const float* __restrict__ tfin,
+__global__ void __launch_bounds__(256) k_semidense(const void* __restrict__ obs, bool u8, const float* __restrict__ tfin,
                                                    int W, int H, double thr, double tmax, uint8_t* __restrict__ out) {
     const int64_t n = (int64_t)W * H;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
@@ -377,8 +377,8 @@ __global__ void __launch_bounds__(256) k_semidense(const float* __restrict__ obs
         for (int dy = -1; dy <= 1; ++dy)
             for (int dx = -1; dx <= 1; ++dx) {
                 const int xx = min(max(x + dx, 0), W - 1), yy = min(max(y + dy, 0), H - 1);
-                const float* q = obs + 3 * ((int64_t)yy * W + xx);
-                g[dy + 1][dx + 1] = ((double)q[0] + (double)q[1] + (double)q[2]) / 3.0;
+                const int64_t q = 3 * ((int64_t)yy * W + xx);
+                g[dy + 1][dx + 1] = (obs_value(obs, u8, q) + obs_value(obs, u8, q + 1) + obs_value(obs, u8, q + 2)) / 3.0;
             }
         // ndimage.sobel(axis=1): d/dx [-1,0,1], smoothed [1,2,1] along y; axis=0 the transpose
         const double gx = ((g[0][2] - g[0][0]) + 2.0 * (g[1][2] - g[1][0]) + (g[2][2] - g[2][0])) / 8.0;
@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(VS_THREADS) k_vs_emit(const uint8_t* __restric
     if (blockIdx.x == nchunk - 1 && threadIdx.x == 0) *total = dummy + all;
 }
 
-__global__ void __launch_bounds__(1024) k_vs_select(const float* __restrict__ obs, const float* __restrict__ img,
+__global__ void __launch_bounds__(1024) k_vs_select(const void* __restrict__ obs, bool u8, const float* __restrict__ img,
                                                     int budget, double gate, const int32_t* __restrict__ ids_all,
                                                     const int* __restrict__ total, int32_t* sel, double* sel_res,
                                                     int32_t* ids_out, double* res_out, int64_t* counts) {
@@ -509,9 +509,9 @@ __global__ void __launch_bounds__(1024) k_vs_select(const float* __restrict__ ob
         int src = k;
         if (L > budget) src = (budget > 1 && k == budget - 1) ? L - 1 : (int)rint((double)k * step);
         const int32_t p = ids_all[src];
-        const float* o = obs + 3 * (int64_t)p;
         const float* h = img + 3 * (int64_t)p;
-        const double go = (((double)o[0] + (double)o[1]) + (double)o[2]) / 3.0;
+        const int64_t q = 3 * (int64_t)p;
+        const double go = ((obs_value(obs, u8, q) + obs_value(obs, u8, q + 1)) + obs_value(obs, u8, q + 2)) / 3.0;
         const double gh = (((double)h[0] + (double)h[1]) + (double)h[2]) / 3.0;
         sel[k] = p;
         sel_res[k] = go - gh;
@@ -541,7 +541,7 @@ int64_t visual_select_scratch_bytes(int64_t npx, int budget) {
     return 8 * ((nchunk + 1 + 1) / 2 + 1) + 4 * npx + 4 * (int64_t)budget + 8 + 8 * (int64_t)budget;
 }
 
-cudaError_t launch_visual_select(const uint8_t* mask, const float* obs, const float* img, int64_t npx, int budget,
+cudaError_t launch_visual_select(const uint8_t* mask, const void* obs, bool u8, const float* img, int64_t npx, int budget,
                                  double gate, void* scratch, int32_t* ids_out, double* res_out, int64_t* counts,
                                  cudaStream_t st) {
     const int nchunk = (int)((npx + VS_CHUNK - 1) / VS_CHUNK);
@@ -556,13 +556,13 @@ cudaError_t launch_visual_select(const uint8_t* mask, const float* obs, const fl
         k_vs_count<<<nchunk, VS_THREADS, 0, st>>>(mask, npx, cnt);
         k_vs_emit<<<nchunk, VS_THREADS, 0, st>>>(mask, npx, cnt, nchunk, ids_all, total);
     }
-    k_vs_select<<<1, 1024, 0, st>>>(obs, img, budget, gate, ids_all, total, sel, sel_res, ids_out, res_out, counts);
+    k_vs_select<<<1, 1024, 0, st>>>(obs, u8, img, budget, gate, ids_all, total, sel, sel_res, ids_out, res_out, counts);
     return cudaGetLastError();
 }
 
-cudaError_t launch_semidense(const float* obs, const float* tfin, int W, int H, double thr, double tmax,
+cudaError_t launch_semidense(const void* obs, bool u8, const float* tfin, int W, int H, double thr, double tmax,
                              uint8_t* out, cudaStream_t st) {
-    k_semidense<<<4 * 148, 256, 0, st>>>(obs, tfin, W, H, thr, tmax, out);
+    k_semidense<<<4 * 148, 256, 0, st>>>(obs, u8, tfin, W, H, thr, tmax, out);
     return cudaGetLastError();
 }
 

@@ -21,8 +21,8 @@ import torch
 from . import _lib
 from .errors import NoAssociations, SingularGain, TooFewPixels
 from .geometry import SE3, so3_exp, so3_left_jacobian, so3_log, so3_right_jacobian_inv
-from .raster import (_CAP_HINT, RasterSettings, RenderState, _as_arrays, _degree_used, _f32, pose_rows, render,
-                     render_fwd)
+from .raster import (_CAP_HINT, RasterSettings, RenderState, _as_arrays, _degree_used, _f32, _observed, pose_rows,
+                     render, render_fwd)
 
 DIM = 15
 
@@ -125,10 +125,11 @@ def select_semi_dense_pixels(observed, coverage_t, cfg: FilterConfig) -> np.ndar
     _lib.require()
     dev = coverage_t.device if torch.is_tensor(coverage_t) and coverage_t.is_cuda else torch.device("cuda")
     h, w = int(np.shape(coverage_t)[0]), int(np.shape(coverage_t)[1])
-    obs = _f32(observed, (h, w, 3), dev)
+    obs = _observed(observed, (h, w, 3), dev)
     tf = _f32(coverage_t, (h, w), dev)
     mask = torch.empty((h, w), dtype=torch.uint8, device=dev)
-    _lib.check(_lib.load().lsb_semidense_mask(ctypes.c_void_p(obs.data_ptr()), ctypes.c_void_p(tf.data_ptr()), w, h,
+    _lib.check(_lib.load().lsb_semidense_mask(ctypes.c_void_p(obs.data_ptr()), int(obs.dtype == torch.uint8),
+                                              ctypes.c_void_p(tf.data_ptr()), w, h,
                                               float(cfg.grad_threshold), float(cfg.coverage_max_transmittance),
                                               ctypes.c_void_p(mask.data_ptr()), _lib.stream_ptr()), "semidense")
     ids = torch.nonzero(mask.view(-1)).view(-1).cpu().numpy()
@@ -148,13 +149,14 @@ def visual_measurement(state, observed, window, cam, T_ic, cfg: FilterConfig,
     out = render(window, T_wc, cam, settings, bin_mode=1 if settings.alpha_cut > 0 else 0)
     dev = out.image.device
     h, w = int(cam.height), int(cam.width)
-    obs = _f32(observed, (h, w, 3), dev)
+    obs = _observed(observed, (h, w, 3), dev)
+    u8 = int(obs.dtype == torch.uint8)
     # semi-dense mask, then selection + residual + gate in one device pass;
     # one small read-back for the counts the reference's exceptions need
     lib = _lib.load()
     npx = h * w
     mask = torch.empty(npx, dtype=torch.uint8, device=dev)
-    _lib.check(lib.lsb_semidense_mask(ctypes.c_void_p(obs.data_ptr()),
+    _lib.check(lib.lsb_semidense_mask(ctypes.c_void_p(obs.data_ptr()), u8,
                                       ctypes.c_void_p(out.final_transmittance.data_ptr()), w, h,
                                       float(cfg.grad_threshold), float(cfg.coverage_max_transmittance),
                                       ctypes.c_void_p(mask.data_ptr()), _lib.stream_ptr()), "semidense")
@@ -163,7 +165,7 @@ def visual_measurement(state, observed, window, cam, T_ic, cfg: FilterConfig,
     ids = torch.empty(budget, dtype=torch.int32, device=dev)
     res = torch.empty(budget, dtype=torch.float64, device=dev)
     counts = torch.empty(3, dtype=torch.int64, device=dev)
-    _lib.check(lib.lsb_visual_select(ctypes.c_void_p(mask.data_ptr()), ctypes.c_void_p(obs.data_ptr()),
+    _lib.check(lib.lsb_visual_select(ctypes.c_void_p(mask.data_ptr()), ctypes.c_void_p(obs.data_ptr()), u8,
                                      ctypes.c_void_p(out.image.data_ptr()), npx, budget, float(cfg.photo_gate),
                                      ctypes.c_void_p(scratch.data_ptr()), ctypes.c_void_p(ids.data_ptr()),
                                      ctypes.c_void_p(res.data_ptr()), ctypes.c_void_p(counts.data_ptr()),
@@ -227,7 +229,8 @@ class _VisualPass:
         self.bin_mode = 1 if settings.alpha_cut > 0 else 0
         self.key = (len(self.arrays), w, h, float(settings.alpha_cut), self.bin_mode)
         self.cap = max(_CAP_HINT.get(self.key, 0), 1 << 16, 8 * len(self.arrays))
-        self.obs = _f32(observed, (h, w, 3), dev)
+        self.obs = _observed(observed, (h, w, 3), dev)
+        self.u8 = int(self.obs.dtype == torch.uint8)
         self.image = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
         self.t_final = torch.empty((h, w), dtype=torch.float32, device=dev)
         self.n_contrib = torch.empty((h, w), dtype=torch.int32, device=dev)
@@ -261,12 +264,12 @@ class _VisualPass:
             sp = _lib.stream_ptr()
             render_fwd(st, self.image, self.t_final, self.n_contrib)
             cnt = self.dev_out[:6].view(torch.int64)
-            _lib.check(lib.lsb_semidense_mask(ctypes.c_void_p(self.obs.data_ptr()),
+            _lib.check(lib.lsb_semidense_mask(ctypes.c_void_p(self.obs.data_ptr()), self.u8,
                                               ctypes.c_void_p(self.t_final.data_ptr()), self.w, self.h,
                                               float(cfg.grad_threshold), float(cfg.coverage_max_transmittance),
                                               ctypes.c_void_p(self.mask.data_ptr()), sp), "semidense")
             _lib.check(lib.lsb_visual_select(ctypes.c_void_p(self.mask.data_ptr()), ctypes.c_void_p(self.obs.data_ptr()),
-                                             ctypes.c_void_p(self.image.data_ptr()), self.h * self.w, B,
+                                             self.u8, ctypes.c_void_p(self.image.data_ptr()), self.h * self.w, B,
                                              float(cfg.photo_gate), ctypes.c_void_p(self.scratch.data_ptr()),
                                              ctypes.c_void_p(self.ids.data_ptr()), ctypes.c_void_p(self.res.data_ptr()),
                                              ctypes.c_void_p(cnt.data_ptr()), sp), "visual_select")

@@ -118,3 +118,32 @@ def test_single_sync_pass_bit_identical_to_measurement():
     with pytest.raises(TooFewPixels):
         _VisualPass(arrays, np.zeros_like(d["observed"]), cam, FilterConfig(min_pixels=10 ** 6), st).run(
             NavState(T_wi), T_ic)
+
+
+def test_u8_frames_selection_and_residuals():
+    """8-bit observed frames through the visual measurement: the selection
+    and the residuals equal the reference's steps (estimator.py:241-277,
+    scipy's Sobel as the reference calls it) on read_ppm's u / 255.0."""
+    import torch
+    from scipy import ndimage
+
+    from paper_2501_08672_b200.estimator import FilterConfig, NavState, visual_measurement
+    from paper_2501_08672_b200.raster import RasterSettings, render
+    d, arrays, cam, T_wi, T_ic = _setup()
+    st = RasterSettings(alpha_cut=1 / 255)
+    cfg = FilterConfig(min_pixels=10)
+    obs8 = np.clip(np.round(np.asarray(d["observed"], np.float64) * 255.0), 0, 255).astype(np.uint8)
+    obs = obs8.astype(np.float64) / 255.0
+    out = render(arrays, T_wi @ T_ic, cam, st, bin_mode=1)
+    gray = obs.mean(axis=2)
+    mag = np.hypot(ndimage.sobel(gray, axis=1, mode="nearest") / 8.0, ndimage.sobel(gray, axis=0, mode="nearest") / 8.0)
+    T = out.final_transmittance.cpu().numpy()
+    ids = np.flatnonzero((mag > cfg.grad_threshold) & (T < cfg.coverage_max_transmittance))
+    if len(ids) > cfg.pixel_budget:
+        ids = ids[np.unique(np.round(np.linspace(0, len(ids) - 1, cfg.pixel_budget)).astype(int))]
+    img = out.image.cpu().numpy().astype(np.float64).reshape(-1, 3)
+    res = gray.reshape(-1)[ids] - img[ids].mean(axis=1)
+    res = res[np.abs(res) <= cfg.photo_gate]
+    meas = visual_measurement(NavState(T_wi), obs8, arrays, cam, T_ic, cfg, st)
+    torch.cuda.synchronize()
+    assert np.array_equal(meas.z, res)
