@@ -745,6 +745,12 @@ def main():
     # one-GPU box; with LSB_BENCH_BACKEND=gloo, since NCCL needs one GPU per rank)
     if os.environ.get("LSB_BENCH_SHARE_GPU") == "1":
         local_rank = 0
+    if args.impl == "reference" and args.config in ("cfg3", "cfg4", "window", "lidar"):
+        if rank == 0:
+            print(json.dumps({"impl": "reference", "config": {"workload": args.config},
+                              "unavailable": "the reference arm times the splat step (cfg1/cfg2/cfg5); this "
+                                             "config's own line carries the oracle's cpu_baseline"}), flush=True)
+        return
     if args.config == "cfg3":
         run_voxel(args, rank, world, local_rank)
         return
