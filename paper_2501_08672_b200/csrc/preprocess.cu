@@ -310,6 +310,14 @@ __global__ void __launch_bounds__(ST_THREADS) k_scan_tiles(Ws w) {
     // the per-thread runs below read distinct banks
     extern __shared__ int s_cnt[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (w.ctr[1] > (unsigned long long)w.cap) {
+        // capacity overflow: splats past the capacity emitted nothing, so the
+        // intersection arrays are incomplete — publish empty tiles (nothing
+        // downstream reads them) and let the caller regrow and retry
+        for (int i = tid; i <= w.ntiles; i += ST_THREADS) w.tile_start[i] = 0;
+        for (int i = tid; i < w.ntiles; i += ST_THREADS) w.tile_order[i] = i;
+        return;
+    }
     for (int i = tid; i < w.ntiles; i += ST_THREADS) s_cnt[i + (i >> 5)] = w.tile_count[i];
     __syncthreads();
     const int per = (w.ntiles + ST_THREADS - 1) / ST_THREADS;
@@ -392,7 +400,8 @@ __global__ void __launch_bounds__(ST_THREADS) k_scan_tiles(Ws w) {
 // Scatter with the (slot, tile) pairs the preprocess emitted: one thread per
 // intersection claims a position in its tile's bucket.
 __global__ void __launch_bounds__(256) k_scatter_emitted(Ws w) {
-    const int64_t I = min((int64_t)w.ctr[1], w.cap);
+    if (w.ctr[1] > (unsigned long long)w.cap) return;     // overflow: tiles published empty
+    const int64_t I = (int64_t)w.ctr[1];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < I; e += stride) {
         const int t = w.emit_tile[e];
