@@ -102,3 +102,26 @@ def test_4k_frame_tile_ranges_and_image():
     Tg, Tr = o["final_transmittance"][bad], ref["t_final"].reshape(2160, 3840)[bad]
     ratio = np.maximum(Tg, Tr) / np.minimum(Tg, Tr)
     assert np.all(np.abs(ratio - 1 / (1 - 1 / 255)) < 1e-4), ratio
+
+
+def test_engine_capacity_overflow_is_reported_not_fatal():
+    """A window engine whose intersection capacity is far too small: every
+    kernel of the step stays in bounds (the tiles are published empty), the
+    overflow is reported by check_capacity(), and the device stays usable."""
+    import torch
+    from golden_io import load
+    from paper_2501_08672_b200.optimize import OptimConfig, WindowEngine
+    from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
+    from paper_2501_08672_b200.scene import camera_for, orbit_views
+    s = load("scene_room_0323")
+    cam = camera_for(160, 128)
+    views = orbit_views(3)
+    st = RasterSettings(alpha_cut=1 / 255)
+    win = GaussianArrays(s["means"], s["rots"], s["scales"], s["opacities"], s["shs"])
+    obs = [render(win, T, cam, st, retain_cache=False).image.clone() for T in views]
+    eng = WindowEngine(win, cam, views, st, OptimConfig(), isect_cap=64, lanes=2)
+    eng.step(obs)
+    torch.cuda.synchronize()
+    assert not eng.check_capacity()
+    out = render(win, views[0], cam, st)        # the context is healthy
+    assert torch.isfinite(out.image).all()
