@@ -93,6 +93,24 @@ __device__ __forceinline__ void adam_gaussian(const AdamArgs<PT>& a, const GS& g
                                               PT ibc2) {
     const int64_t n = a.n;
     const int64_t o_rot = 3 * n, o_scale = 6 * n, o_op = 9 * n, o_sh = 10 * n;
+    {
+        // a row with zero gradient and zero moments (never seen by any view)
+        // is an exact no-op — the reference's "a zero gradient is an exact
+        // no-op" (optimize.py:164-166): skip its sqrt / division chain and
+        // its stores
+        const int64_t nk = 3 * (int64_t)a.K;
+        bool idle = true;
+        auto chk = [&](int64_t idx) { idle = idle && gs(idx) == 0.f && a.m[idx] == (PT)0 && a.v[idx] == (PT)0; };
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            chk(3 * i + k);
+            chk(o_rot + 3 * i + k);
+            chk(o_scale + 3 * i + k);
+        }
+        chk(o_op + i);
+        for (int64_t k = 0; k < nk; ++k) chk(o_sh + nk * i + k);
+        if (idle) return;
+    }
     const PT lr_mean = (PT)(a.c.lr_mean * a.c.scene_scale), lr_rot = (PT)a.c.lr_rot;
     const PT lr_scale = (PT)a.c.lr_scale, lr_op = (PT)a.c.lr_opacity, lr_sh = (PT)a.c.lr_sh;
     const PT floor_s = (PT)a.c.scale_floor, oclip = (PT)a.c.opacity_clip;
