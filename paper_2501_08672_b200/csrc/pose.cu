@@ -368,23 +368,32 @@ __global__ void k_hb_final(const double* __restrict__ part, int nblocks, double 
     out[6 * j + i] = t;
 }
 
-__global__ void __launch_bounds__(256) k_semidense(const void* __restrict__ obs, bool u8, const float* __restrict__ tfin,
-                                                   int W, int H, double thr, double tmax, uint8_t* __restrict__ out) {
-    const int64_t n = (int64_t)W * H;
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-        const int x = (int)(p % W), y = (int)(p / W);
-        double g[3][3];
-        for (int dy = -1; dy <= 1; ++dy)
-            for (int dx = -1; dx <= 1; ++dx) {
-                const int xx = min(max(x + dx, 0), W - 1), yy = min(max(y + dy, 0), H - 1);
-                const int64_t q = 3 * ((int64_t)yy * W + xx);
-                g[dy + 1][dx + 1] = (obs_value(obs, u8, q) + obs_value(obs, u8, q + 1) + obs_value(obs, u8, q + 2)) / 3.0;
-            }
-        // ndimage.sobel(axis=1): d/dx [-1,0,1], smoothed [1,2,1] along y; axis=0 the transpose
-        const double gx = ((g[0][2] - g[0][0]) + 2.0 * (g[1][2] - g[1][0]) + (g[2][2] - g[2][0])) / 8.0;
-        const double gy = ((g[2][0] - g[0][0]) + 2.0 * (g[2][1] - g[0][1]) + (g[2][2] - g[0][2])) / 8.0;
-        out[p] = (hypot(gx, gy) > thr && (double)tfin[p] < tmax) ? 1 : 0;
+// One 32x8 block of pixels per CTA: the grey values of the block and its
+// one-pixel (clamped) border are computed once into shared memory, then
+// every pixel reads its 3x3 neighbourhood from there — the same f64 values
+// and operation order as per-pixel recomputation.
+constexpr int SD_BX = 32, SD_BY = 8;
+__global__ void __launch_bounds__(SD_BX * SD_BY) k_semidense(const void* __restrict__ obs, bool u8,
+                                                            const float* __restrict__ tfin, int W, int H, double thr,
+                                                            double tmax, uint8_t* __restrict__ out) {
+    __shared__ double g[SD_BY + 2][SD_BX + 2];
+    const int x0 = blockIdx.x * SD_BX, y0 = blockIdx.y * SD_BY;
+    for (int k = threadIdx.x; k < (SD_BX + 2) * (SD_BY + 2); k += SD_BX * SD_BY) {
+        const int ly = k / (SD_BX + 2), lx = k % (SD_BX + 2);
+        const int xx = min(max(x0 + lx - 1, 0), W - 1), yy = min(max(y0 + ly - 1, 0), H - 1);
+        const int64_t q = 3 * ((int64_t)yy * W + xx);
+        g[ly][lx] = (obs_value(obs, u8, q) + obs_value(obs, u8, q + 1) + obs_value(obs, u8, q + 2)) / 3.0;
     }
+    __syncthreads();
+    const int tx = threadIdx.x % SD_BX, ty = threadIdx.x / SD_BX;
+    const int x = x0 + tx, y = y0 + ty;
+    if (x >= W || y >= H) return;
+    // ndimage.sobel(axis=1): d/dx [-1,0,1], smoothed [1,2,1] along y; axis=0 the transpose
+    const double(*c)[SD_BX + 2] = (const double(*)[SD_BX + 2]) & g[ty][tx];
+    const double gx = ((c[0][2] - c[0][0]) + 2.0 * (c[1][2] - c[1][0]) + (c[2][2] - c[2][0])) / 8.0;
+    const double gy = ((c[2][0] - c[0][0]) + 2.0 * (c[2][1] - c[0][1]) + (c[2][2] - c[0][2])) / 8.0;
+    const int64_t p = (int64_t)y * W + x;
+    out[p] = (hypot(gx, gy) > thr && (double)tfin[p] < tmax) ? 1 : 0;
 }
 
 cudaError_t launch_pose_prepare(const Ws& w, const lsb_params& p, const lsb_camera& cam, const lsb_pose& T,
@@ -562,7 +571,8 @@ cudaError_t launch_visual_select(const uint8_t* mask, const void* obs, bool u8, 
 
 cudaError_t launch_semidense(const void* obs, bool u8, const float* tfin, int W, int H, double thr, double tmax,
                              uint8_t* out, cudaStream_t st) {
-    k_semidense<<<4 * 148, 256, 0, st>>>(obs, u8, tfin, W, H, thr, tmax, out);
+    const dim3 grid((W + SD_BX - 1) / SD_BX, (H + SD_BY - 1) / SD_BY);
+    k_semidense<<<grid, SD_BX * SD_BY, 0, st>>>(obs, u8, tfin, W, H, thr, tmax, out);
     return cudaGetLastError();
 }
 
