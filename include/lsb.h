@@ -278,6 +278,46 @@ int lsb_pose_rows(const lsb_settings* s, int sh_degree_used, void* ws, size_t ws
 int lsb_hb_scratch_doubles(void);
 int lsb_hb_reduce(const double* rows, const double* z, int64_t m, const int64_t* m_dev, double inv_sigma2,
                   double* out, double* scratch, void* stream);
+/* One visual IESKF iteration in a single call (estimator.py:241-318 for the
+ * pose block): lsb_render_fwd -> lsb_semidense_mask -> lsb_visual_select ->
+ * lsb_pose_prepare -> lsb_pose_rows -> lsb_hb_reduce with the kept count on
+ * the device, then the render's [M, I, overflow] counters copied next to
+ * the selection counts.  Asynchronous; the caller reads b->out (48 x 8
+ * bytes: int64 [L, selected, kept, M, I, overflow], then the 42 H/b
+ * doubles) after one stream sync — the same bits as the separate calls. */
+typedef struct lsb_visual_cfg {
+    int32_t budget;             /* pixel_budget */
+    int32_t observed_u8;        /* observed is the 8-bit frame */
+    int32_t sh_degree_used;
+    int32_t _pad;
+    double grad_thr, t_max, gate, inv_sigma2;
+    double A[36];               /* imu_camera_adjoint(R_cw, T_ic), row-major */
+} lsb_visual_cfg;
+typedef struct lsb_visual_bufs {
+    uint8_t* mask;              /* H*W */
+    void* select_scratch;       /* lsb_visual_select_scratch_bytes(H*W, budget) */
+    int32_t* ids;               /* budget */
+    double* res;                /* budget */
+    float* chain;               /* n * LSB_POSE_CHAIN_FLOATS */
+    double* rows;               /* budget * 6 */
+    double* hb_scratch;         /* lsb_hb_scratch_doubles() */
+    int64_t* out;               /* 48 x 8 bytes, see above */
+} lsb_visual_bufs;
+int lsb_visual_pass(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T_cw, const lsb_settings* s,
+                    void* ws, size_t ws_bytes, const lsb_dims* dims, float* image, float* t_final,
+                    int32_t* n_contrib, const void* observed, const lsb_visual_cfg* cfg, const lsb_visual_bufs* b,
+                    void* stream);
+
+/* Host-side gain algebra of one IESKF iteration for a pose-block measurement
+ * (estimator.py:292-331): P = Hj^-1 cov Hj^-T (Hj^-1 = I with jinv3 =
+ * J_l(-delta_rho) in the rotation block), S = A + P^-1 (A = the 6x6 block
+ * A6), K H = S^-1 A -> KH (15x15), xi = -S^-1 b - (I - K H) Hj^-1 delta
+ * (b = b6 padded) -> xi (15), P -> P (15x15).  All host pointers, row-major.
+ * LSB_EINVAL with "singular matrix" / "non-finite gain" where the reference
+ * raises SingularGain. */
+int lsb_ieskf_gain(const double* cov, const double* jinv3, const double* A6, const double* b6, const double* delta,
+                   double* xi, double* KH, double* P);
+
 /* Semi-dense candidate mask (estimator.py:241-252): Sobel/8 magnitude of the
  * grey observed image (nearest border) > grad_thr and t_final < t_max.
  * observed_u8 (here and in lsb_visual_select): the frame is 8-bit, read as

@@ -64,6 +64,16 @@ class AdamCfg(_c.Structure):
         ("step", _c.c_int64)]
 
 
+class VisualCfg(_c.Structure):
+    _fields_ = [("budget", _c.c_int32), ("observed_u8", _c.c_int32), ("sh_degree_used", _c.c_int32),
+                ("_pad", _c.c_int32), ("grad_thr", _c.c_double), ("t_max", _c.c_double), ("gate", _c.c_double),
+                ("inv_sigma2", _c.c_double), ("A", _c.c_double * 36)]
+
+
+class VisualBufs(_c.Structure):
+    _fields_ = [(k, _P) for k in ("mask", "select_scratch", "ids", "res", "chain", "rows", "hb_scratch", "out")]
+
+
 # (name, restype, argtypes) for every symbol include/lsb.h declares
 SIGNATURES = [
     ("lsb_abi_version", _c.c_int, []),
@@ -73,6 +83,10 @@ SIGNATURES = [
                                   _c.POINTER(Settings), _P, _c.c_size_t, _c.POINTER(Dims),
                                   _P, _P, _P, _P, _P]),
     ("lsb_render_counts", _c.c_int, [_P, _c.POINTER(Dims), _c.POINTER(_c.c_int64), _P]),
+    ("lsb_ieskf_gain", _c.c_int, [_P] * 8),
+    ("lsb_visual_pass", _c.c_int, [_c.POINTER(Params), _c.POINTER(Camera), _c.POINTER(Pose), _c.POINTER(Settings),
+                                   _P, _c.c_size_t, _c.POINTER(Dims), _P, _P, _P, _P, _c.POINTER(VisualCfg),
+                                   _c.POINTER(VisualBufs), _P]),
     ("lsb_render_export", _c.c_int, [_P, _c.POINTER(Dims), _c.c_int, _P, _P]),
     ("lsb_render_bwd", _c.c_int, [_c.POINTER(Params), _c.POINTER(Camera), _c.POINTER(Pose),
                                   _c.POINTER(Settings), _P, _c.c_size_t, _c.POINTER(Dims),

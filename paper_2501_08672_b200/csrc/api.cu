@@ -33,6 +33,7 @@ cudaError_t launch_pose_rows(const Ws&, const lsb_settings&, int, int, int, cons
                              double*, cudaStream_t);
 cudaError_t launch_hb(const double*, const double*, int64_t, const int64_t*, double, double*, double*, cudaStream_t);
 int hb_scratch_doubles();
+int ieskf_gain(const double*, const double*, const double*, const double*, const double*, double*, double*, double*);
 cudaError_t launch_visual_select(const uint8_t*, const void*, bool, const float*, int64_t, int, double, void*, int32_t*,
                                  double*, int64_t*, cudaStream_t);
 int64_t visual_select_scratch_bytes(int64_t, int);
@@ -596,6 +597,51 @@ int lsb_visual_select(const uint8_t* mask, const void* observed, int32_t observe
     return check_cuda(launch_visual_select(mask, observed, observed_u8 != 0, image, npx, budget, gate, scratch, ids_out,
                                            res_out, counts, (cudaStream_t)stream),
                       "visual_select");
+}
+
+int lsb_visual_pass(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T, const lsb_settings* s,
+                    void* ws, size_t ws_bytes, const lsb_dims* d, float* image, float* t_final, int32_t* n_contrib,
+                    const void* observed, const lsb_visual_cfg* c, const lsb_visual_bufs* b, void* stream) {
+    if (!p || !cam || !T || !s || !c || !b || !observed) return fail(LSB_EINVAL, "NULL argument");
+    if (!image || !t_final || !n_contrib || !b->mask || !b->select_scratch || !b->ids || !b->res || !b->chain ||
+        !b->rows || !b->hb_scratch || !b->out || c->budget < 1)
+        return fail(LSB_EINVAL, "bad buffers");
+    int rc = lsb_render_fwd(p, cam, T, s, ws, ws_bytes, d, image, t_final, n_contrib, nullptr, stream);
+    if (rc) return rc;
+    Ws w;
+    rc = get_ws(ws, ws_bytes, d, &w);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t npx = (int64_t)d->width * d->height;
+    const bool u8 = c->observed_u8 != 0;
+    int64_t* cnt = b->out;
+    const int64_t* kept = cnt + 2;
+    rc = check_cuda(launch_semidense(observed, u8, t_final, d->width, d->height, c->grad_thr, c->t_max, b->mask, st),
+                    "semidense");
+    if (rc) return rc;
+    rc = check_cuda(launch_visual_select(b->mask, observed, u8, image, npx, c->budget, c->gate, b->select_scratch,
+                                         b->ids, b->res, cnt, st),
+                    "visual_select");
+    if (rc) return rc;
+    rc = check_cuda(launch_pose_prepare(w, *p, *cam, *T, *s, b->chain, st), "pose_prepare");
+    if (rc) return rc;
+    rc = check_cuda(launch_pose_rows(w, *s, c->sh_degree_used, d->width, d->height, image, n_contrib, b->chain, b->ids,
+                                     c->budget, kept, c->A, T->R, b->rows, st),
+                    "pose_rows");
+    if (rc) return rc;
+    rc = check_cuda(launch_hb(b->rows, b->res, c->budget, kept, c->inv_sigma2, (double*)(b->out + 6), b->hb_scratch, st),
+                    "hb_reduce");
+    if (rc) return rc;
+    return check_cuda(cudaMemcpyAsync(cnt + 3, w.ctr, 3 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st), "counters");
+}
+
+int lsb_ieskf_gain(const double* cov, const double* jinv3, const double* A6, const double* b6, const double* delta,
+                   double* xi, double* KH, double* P) {
+    if (!cov || !jinv3 || !A6 || !b6 || !delta || !xi || !KH || !P) return fail(LSB_EINVAL, "NULL argument");
+    const int r = ieskf_gain(cov, jinv3, A6, b6, delta, xi, KH, P);
+    if (r == 1) return fail(LSB_EINVAL, "singular matrix");
+    if (r == 2) return fail(LSB_EINVAL, "non-finite gain");
+    return LSB_OK;
 }
 
 }  // extern "C"

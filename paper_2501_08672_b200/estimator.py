@@ -213,10 +213,10 @@ def lidar_measurement(state: NavState, points_l, vmap, T_il, cfg: FilterConfig,
 
 
 class _VisualPass:
-    """The device side of one visual IESKF iteration with ONE host sync:
-    render (contributing lists) -> semi-dense mask -> selection / residual /
-    gate (lsb_visual_select) -> pose chain -> pose rows -> H/b, the kept
-    count staying on the device (the m_dev arguments); the counts, the
+    """The device side of one visual IESKF iteration in ONE library call
+    (lsb_visual_pass) and ONE host sync: render (contributing lists) ->
+    semi-dense mask -> selection / residual / gate -> pose chain -> pose
+    rows -> H/b, the kept count staying on the device; the counts, the
     intersection overflow flag and the 42 H/b numbers come back in one
     read.  Buffers persist across the iterations of an update.  Same kernels
     and the same bits as visual_measurement(...).hb() (tested)."""
@@ -229,8 +229,7 @@ class _VisualPass:
         self.bin_mode = 1 if settings.alpha_cut > 0 else 0
         self.key = (len(self.arrays), w, h, float(settings.alpha_cut), self.bin_mode)
         self.cap = max(_CAP_HINT.get(self.key, 0), 1 << 16, 8 * len(self.arrays))
-        self.obs = _observed(observed, (h, w, 3), dev)
-        self.u8 = int(self.obs.dtype == torch.uint8)
+        self.set_observed(observed)
         self.image = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
         self.t_final = torch.empty((h, w), dtype=torch.float32, device=dev)
         self.n_contrib = torch.empty((h, w), dtype=torch.int32, device=dev)
@@ -249,52 +248,41 @@ class _VisualPass:
         self.host_out = torch.empty(6 + 42, dtype=torch.float64).pin_memory()
         self.state = None
 
+    def set_observed(self, observed) -> None:
+        self.obs = _observed(observed, (self.h, self.w, 3), self.arrays.device)
+        self.u8 = int(self.obs.dtype == torch.uint8)
+
     def run(self, nav: NavState, T_ic):
         from .geometry import imu_camera_adjoint
         lib = _lib.load()
         T_cw = (nav.T_WI @ T_ic).inverse()
-        cfg, B = self.cfg, int(self.cfg.pixel_budget)
+        cfg = self.cfg
+        c = _lib.VisualCfg()
+        c.budget, c.observed_u8 = int(cfg.pixel_budget), self.u8
+        c.grad_thr, c.t_max = float(cfg.grad_threshold), float(cfg.coverage_max_transmittance)
+        c.gate, c.inv_sigma2 = float(cfg.photo_gate), 1.0 / float(cfg.photo_sigma) ** 2
+        c.A[:] = imu_camera_adjoint(T_cw.R, T_ic).ravel().tolist()
         while True:
             if self.state is None or self.state.dims.isect_cap != self.cap:
                 self.state = RenderState(self.arrays, self.cam, T_cw.R, T_cw.t, self.settings, self.cap,
                                          self.bin_mode)
+                self.bufs = _lib.VisualBufs(*(t.data_ptr() for t in (
+                    self.mask, self.scratch, self.ids, self.res, self.chain, self.rows, self.hb_scratch,
+                    self.dev_out)))
             else:
                 self.state.set_pose(T_cw.R, T_cw.t)
             st = self.state
-            sp = _lib.stream_ptr()
-            render_fwd(st, self.image, self.t_final, self.n_contrib)
-            cnt = self.dev_out[:6].view(torch.int64)
-            _lib.check(lib.lsb_semidense_mask(ctypes.c_void_p(self.obs.data_ptr()), self.u8,
-                                              ctypes.c_void_p(self.t_final.data_ptr()), self.w, self.h,
-                                              float(cfg.grad_threshold), float(cfg.coverage_max_transmittance),
-                                              ctypes.c_void_p(self.mask.data_ptr()), sp), "semidense")
-            _lib.check(lib.lsb_visual_select(ctypes.c_void_p(self.mask.data_ptr()), ctypes.c_void_p(self.obs.data_ptr()),
-                                             self.u8, ctypes.c_void_p(self.image.data_ptr()), self.h * self.w, B,
-                                             float(cfg.photo_gate), ctypes.c_void_p(self.scratch.data_ptr()),
-                                             ctypes.c_void_p(self.ids.data_ptr()), ctypes.c_void_p(self.res.data_ptr()),
-                                             ctypes.c_void_p(cnt.data_ptr()), sp), "visual_select")
-            kept = ctypes.c_void_p(cnt.data_ptr() + 16)          # counts[2], on the device
+            c.sh_degree_used = _degree_used(st)
             p = st.arrays.params()
-            _lib.check(lib.lsb_pose_prepare(ctypes.byref(p), ctypes.byref(st.c_cam), ctypes.byref(st.c_pose),
-                                            ctypes.byref(st.c_set), st._ws(), st.ws_bytes, ctypes.byref(st.dims),
-                                            ctypes.c_void_p(self.chain.data_ptr()), sp), "pose_prepare")
-            A = imu_camera_adjoint(st.R_cw, T_ic)
-            Ac = (ctypes.c_double * 36)(*A.ravel().tolist())
-            Rc = (ctypes.c_double * 9)(*st.R_cw.ravel().tolist())
-            _lib.check(lib.lsb_pose_rows(ctypes.byref(st.c_set), _degree_used(st), st._ws(), st.ws_bytes,
-                                         ctypes.byref(st.dims), ctypes.c_void_p(self.image.data_ptr()),
-                                         ctypes.c_void_p(self.n_contrib.data_ptr()),
-                                         ctypes.c_void_p(self.chain.data_ptr()), ctypes.c_void_p(self.ids.data_ptr()),
-                                         B, kept, Ac, Rc, ctypes.c_void_p(self.rows.data_ptr()), sp), "pose_rows")
-            _lib.check(lib.lsb_hb_reduce(ctypes.c_void_p(self.rows.data_ptr()), ctypes.c_void_p(self.res.data_ptr()),
-                                         B, kept, 1.0 / float(cfg.photo_sigma) ** 2,
-                                         ctypes.c_void_p(self.dev_out.data_ptr() + 48),
-                                         ctypes.c_void_p(self.hb_scratch.data_ptr()), sp), "hb_reduce")
-            cnt[3:6].copy_(st.ws[:24].view(torch.int64))       # the render's [M, I, overflow] counters
+            _lib.check(lib.lsb_visual_pass(
+                ctypes.byref(p), ctypes.byref(st.c_cam), ctypes.byref(st.c_pose), ctypes.byref(st.c_set), st._ws(),
+                st.ws_bytes, ctypes.byref(st.dims), ctypes.c_void_p(self.image.data_ptr()),
+                ctypes.c_void_p(self.t_final.data_ptr()), ctypes.c_void_p(self.n_contrib.data_ptr()),
+                ctypes.c_void_p(self.obs.data_ptr()), ctypes.byref(c), ctypes.byref(self.bufs), _lib.stream_ptr()),
+                "visual_pass")
             self.host_out.copy_(self.dev_out, non_blocking=True)
             torch.cuda.current_stream().synchronize()
-            c = self.host_out[:6].view(torch.int64).tolist()
-            _, n_sel, n_ok, _, I, overflow = c
+            _, n_sel, n_ok, _, I, overflow = self.host_out[:6].view(torch.int64).tolist()
             if not overflow:
                 break
             self.cap = int(I * 1.25) + 1024                  # grow and redo (rare)
@@ -307,6 +295,26 @@ class _VisualPass:
         return o[:36].reshape(6, 6).copy(), o[36:].copy()
 
 
+_VIS_CACHE: dict = {}
+
+
+def _visual_pass(window, observed, cam, cfg: FilterConfig, settings: RasterSettings) -> _VisualPass:
+    """The update's _VisualPass, reused across updates on the same window /
+    camera / configuration (its device buffers and pinned read-back buffer
+    are allocated once); the observed frame is refreshed every update."""
+    arrays = _as_arrays(window)
+    key = (id(arrays), len(arrays), int(arrays.shs.shape[1]), int(cam.width), int(cam.height), float(cam.fx),
+           float(cam.fy), float(cam.cx), float(cam.cy), repr(cfg), repr(settings))
+    vis = _VIS_CACHE.get(key)
+    if vis is None or vis.arrays is not arrays:
+        if len(_VIS_CACHE) > 4:
+            _VIS_CACHE.clear()
+        vis = _VIS_CACHE[key] = _VisualPass(arrays, observed, cam, cfg, settings)
+    else:
+        vis.set_observed(observed)
+    return vis
+
+
 def ieskf_visual_update(state: NavState, cov: np.ndarray, observed, window, cam, T_ic, cfg: FilterConfig,
                         settings: RasterSettings, max_iter: int = 5, step_tol: float = 1e-6,
                         bias_limit: float = 0.5):
@@ -317,27 +325,20 @@ def ieskf_visual_update(state: NavState, cov: np.ndarray, observed, window, cam,
     K z = S^-1 b and K H = S^-1 A (H is zero outside its 6 pose columns)."""
     x_bar, x_hat = state, state.clone()
     K_H = P = None
-    vis = _VisualPass(window, observed, cam, cfg, settings)
+    vis = _visual_pass(window, observed, cam, cfg, settings)
+    lib = _lib.load()
+    cov_c = np.ascontiguousarray(cov, dtype=np.float64)
+    ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)
     for _ in range(max_iter):
         A6, b6 = vis.run(x_hat, T_ic)
         delta = x_hat.boxminus(x_bar)
-        Hj_inv = np.eye(DIM)
-        Hj_inv[0:3, 0:3] = so3_left_jacobian(-delta[0:3])
-        P = Hj_inv @ cov @ Hj_inv.T
-        A = np.zeros((DIM, DIM))
-        A[:6, :6] = A6
-        b = np.zeros(DIM)
-        b[:6] = b6
-        try:
-            S = A + np.linalg.inv(P)
-            S_inv = np.linalg.inv(S)
-        except np.linalg.LinAlgError as exc:
-            raise SingularGain(str(exc)) from exc
-        K_H = S_inv @ A
-        Kz = S_inv @ b
-        if not np.all(np.isfinite(K_H)):
-            raise SingularGain("non-finite gain")
-        xi = -Kz - (np.eye(DIM) - K_H) @ (Hj_inv @ delta)
+        jinv = np.ascontiguousarray(so3_left_jacobian(-delta[0:3]), dtype=np.float64)
+        xi, K_H, P = np.empty(DIM), np.empty((DIM, DIM)), np.empty((DIM, DIM))
+        # the 15x15 gain algebra (lsb_ieskf_gain, host C++): S = A + P^-1,
+        # K H = S^-1 A, K z = S^-1 b, xi = -K z - (I - K H) Hj^-1 delta
+        if lib.lsb_ieskf_gain(ptr(cov_c), ptr(jinv), ptr(np.ascontiguousarray(A6)), ptr(np.ascontiguousarray(b6)),
+                              ptr(np.ascontiguousarray(delta)), ptr(xi), ptr(K_H), ptr(P)):
+            raise SingularGain(lib.lsb_last_error().decode())
         x_hat = x_hat.boxplus(xi, bias_limit=bias_limit)
         if np.linalg.norm(xi) < step_tol:
             break
