@@ -211,14 +211,21 @@ def run_ours(args, wl, rank, world, local_rank):
     V, W, H, N = wl["V"], wl["W"], wl["H"], wl["N"]
     gt = GaussianArrays(*wl["gt"], device=dev)
     win = GaussianArrays(*wl["win"], device=dev)
-    my_views = [v for v in range(V) if v % world == rank]
-    observed = [render(gt, wl["views"][v], wl["cam"], settings, retain_cache=False).image.clone()
-                for v in my_views]
+    # this rank's render units: whole views (v -> rank v mod N), or row bands
+    # of the views when N does not divide them (dist.shard_units: config 2's
+    # 10 views become 20 half views at N = 4, 40 quarter views at N = 8)
+    from paper_2501_08672_b200.dist import shard_units, view_bands
+    units = shard_units(V, world, rank, H)
+    my_views = [u[0] for u in units]
+    bands = [(u[1], u[2]) for u in units]
+    frames = {v: render(gt, wl["views"][v], wl["cam"], settings, retain_cache=False).image.clone()
+              for v in sorted(set(my_views))}
     if args.frames == "u8":
         # the camera's 8-bit frames, quantised the way write_ppm stores them
         # (raster.py:511-517); the kernels read u / 255.0 like read_ppm
-        observed = [torch.clamp(torch.round(o.double() * 255.0), 0, 255).to(torch.uint8) for o in observed]
-    del gt
+        frames = {v: torch.clamp(torch.round(o.double() * 255.0), 0, 255).to(torch.uint8) for v, o in frames.items()}
+    observed = [frames[v][y0:y1].contiguous() for v, y0, y1 in units]
+    del gt, frames
     # L2 flush between timed steps: a write larger than the 126 MB L2, issued
     # outside each step's event pair
     flush_buf = torch.empty(64 * 2 ** 20, dtype=torch.int32, device=dev)
@@ -240,11 +247,12 @@ def run_ours(args, wl, rank, world, local_rank):
         return float(np.median(ts))
     stream = torch.cuda.Stream(dev)
     eng = WindowEngine(win, wl["cam"], [wl["views"][v] for v in my_views], settings, OptimConfig(),
-                       n_views_total=V, stream=stream, lanes=args.lanes)
+                       n_views_total=V, stream=stream, lanes=args.lanes, bands=bands)
     counts = []
-    for v in range(len(my_views)):      # per-view M, I for the byte model
+    for v in range(len(my_views)):      # per-unit M, I for the byte model
         T = eng.views[v]
         eng.state.set_pose(T.R, T.t)
+        eng.state.set_camera(eng.view_cams[v])
         from paper_2501_08672_b200.raster import render_bin
         render_bin(eng.state, stream)
         counts.append(eng.state.read_counts(stream)[:2])
@@ -281,7 +289,8 @@ def run_ours(args, wl, rank, world, local_rank):
     # so each kernel's duration is its own (not shared with a concurrent lane)
     timers: dict = {}
     keng = WindowEngine(win, wl["cam"], [wl["views"][v] for v in my_views], settings, OptimConfig(),
-                        n_views_total=V, stream=stream, lanes=1, isect_cap=eng.lanes[0].state.dims.isect_cap)
+                        n_views_total=V, stream=stream, lanes=1, isect_cap=eng.lanes[0].state.dims.isect_cap,
+                        bands=bands)
     with torch.cuda.stream(stream):
         keng.step(observed, allreduce=allreduce)
     eager_ms = timed(lambda: keng.step(observed, allreduce=allreduce, timers=timers))
@@ -333,7 +342,8 @@ def run_ours(args, wl, rank, world, local_rank):
     M_avg = float(np.mean([c[0] for c in counts])) if counts else 0.0
     I_avg = float(np.mean([c[1] for c in counts])) if counts else 0.0
     K = int(win.shs.shape[1])
-    ab = algorithmic_bytes(N, K, M_avg, I_avg, W * H, pbytes=eng.arrays.means.element_size(),
+    P_avg = float(np.mean([W * (y1 - y0) for y0, y1 in bands]))
+    ab = algorithmic_bytes(N, K, M_avg, I_avg, P_avg, pbytes=eng.arrays.means.element_size(),
                            obytes=observed[0].element_size())
     per_step_ms = {k: float(np.sum(v)) / args.steps for k, v in ktime.items()}
     dom = max(("bin", "blend", "blend_fwd", "blend_bwd", "chain"), key=lambda k: per_step_ms.get(k, 0.0))
@@ -391,9 +401,11 @@ def run_ours(args, wl, rank, world, local_rank):
             "config": {"workload": args.config, "gaussians": N, "views": V, "width": W, "height": H,
                        "alpha_cut": wl["alpha_cut"], "parallelism": f"view-sharded dp{world}",
                        "view_lanes": args.lanes, "exchange": exchange if world > 1 else None,
-                       # views v -> rank v mod N: config 2's 10 views split unevenly at 4 and 8 GPUs
-                       "views_per_rank": [len(range(r, V, world)) for r in range(world)],
-                       "view_imbalance": max(len(range(r, V, world)) for r in range(world)) / (V / world),
+                       # render units per rank: whole views, or row bands when N does not divide the views
+                       "units_per_rank": [len(shard_units(V, world, r, H)) for r in range(world)],
+                       "bands_per_view": view_bands(V, world, H),
+                       "unit_imbalance": max(len(shard_units(V, world, r, H)) for r in range(world))
+                       / (V * view_bands(V, world, H) / world),
                        "cuda_graph": graph_headline, "cuda_graph_e2e": use_graph,
                        "serial_ms_per_step": eager_ms,
                        "kernel_timing": "separate one-lane eager pass of the same steps, events around each kernel",
@@ -417,7 +429,7 @@ def run_ours(args, wl, rank, world, local_rank):
             "step_roofline": {"algorithmic_bytes_per_step_rank0": step_bytes,
                               "frac": step_bytes / (ms * 1e-3) / 1e9 / hbm},
             "kernel_ms_per_step": per_step_ms,
-            "counts_per_view": {"visible_M": M_avg, "intersections_I": I_avg},
+            "counts_per_unit": {"visible_M": M_avg, "intersections_I": I_avg, "pixels": P_avg},
             "clocks": clk_sum,
             "e2e": {"value": V * W * H / (e_ms * 1e-3) / 1e6, "unit": "Mpix/s",
                     "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world, "ms_per_step": e_ms},

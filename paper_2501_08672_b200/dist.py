@@ -26,6 +26,39 @@ def shard_views(n_views: int, world: int, rank: int) -> list:
     return [v for v in range(n_views) if v % world == rank]
 
 
+def view_bands(n_views: int, world: int, height: int, tile: int = 16, max_split: int = 8) -> int:
+    """Row bands per view for a view-sharded step: 1 when the ranks divide
+    the views, else the smallest b in (2, 4, 8) with (n_views * b) % world
+    == 0 and at least one tile row per band — so every rank renders the same
+    number of (view, band) units (config 2's 10 views at 4 GPUs: 20 half
+    views, 5 per rank; at 8 GPUs: 40 quarter views, 5 per rank)."""
+    if world <= 1 or n_views % world == 0:
+        return 1
+    rows = (height + tile - 1) // tile
+    for b in (2, 4, 8):
+        if b <= max_split and b <= rows and (n_views * b) % world == 0:
+            return b
+    return 1
+
+
+def shard_units(n_views: int, world: int, rank: int, height: int, tile: int = 16) -> list:
+    """This rank's (view, y0, y1) render units.  Unbanded: views v -> rank
+    v mod world (shard_views).  Banded: the (view, band) units in view-major
+    order, cut into `world` equal contiguous runs (each rank gets a mix of
+    bands, so systematic cost differences between image regions average
+    out)."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad world/rank")
+    b = view_bands(n_views, world, height, tile)
+    if b == 1:
+        return [(v, 0, height) for v in shard_views(n_views, world, rank)]
+    rows = (height + tile - 1) // tile
+    edges = [min(height, tile * (k * rows // b)) for k in range(b)] + [height]
+    units = [(v, edges[k], edges[k + 1]) for v in range(n_views) for k in range(b)]
+    per = len(units) // world
+    return units[rank * per:(rank + 1) * per]
+
+
 def make_allreduce(group=None) -> Optional[Callable[[torch.Tensor], None]]:
     """The gradient exchange: in-place sum over the process group (None if
     not distributed or world size 1)."""
@@ -55,20 +88,29 @@ def replicas_identical(t: torch.Tensor, group=None) -> bool:
 
 
 class ViewShardedWindow:
-    """Multi-GPU WindowEngine: this rank's share of the keyframe views."""
+    """Multi-GPU WindowEngine: this rank's share of the keyframe views —
+    whole views, or row bands of them when the ranks do not divide the
+    views (shard_units)."""
 
     def __init__(self, arrays, cam, views_all: Sequence, settings, cfg=None, group=None, stream=None,
-                 master: str = "f64"):
+                 master: str = "f64", lanes: int = 1):
         from .optimize import OptimConfig, WindowEngine
 
         world = dist.get_world_size(group) if dist.is_initialized() else 1
         rank = dist.get_rank(group) if dist.is_initialized() else 0
-        self.mine = shard_views(len(views_all), world, rank)
+        self.units = shard_units(len(views_all), world, rank, int(cam.height))
+        self.mine = [u[0] for u in self.units]
         self.engine = WindowEngine(arrays, cam, [views_all[v] for v in self.mine], settings, cfg or OptimConfig(),
-                                   n_views_total=len(views_all), stream=stream, master=master)
+                                   n_views_total=len(views_all), stream=stream, master=master, lanes=lanes,
+                                   bands=[(u[1], u[2]) for u in self.units])
         self.allreduce = make_allreduce(group)
 
+    def observed_for(self, frames: Sequence[torch.Tensor]) -> list:
+        """This rank's unit images from the full frames (indexed by view)."""
+        return [frames[v][y0:y1].contiguous() for v, y0, y1 in self.units]
+
     def step(self, observed_mine: Sequence[torch.Tensor], timers: Optional[dict] = None) -> None:
+        """observed_mine: one image per unit (observed_for)."""
         self.engine.step(observed_mine, allreduce=self.allreduce, timers=timers)
 
     def finish(self) -> None:

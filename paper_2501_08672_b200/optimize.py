@@ -25,7 +25,7 @@ from . import _lib
 from .errors import EmptyMask
 from .geometry import as_se3
 from .raster import (GaussianArrays, ParamGradients, RasterSettings, RenderState, _as_arrays, _f32, _obs_kind,
-                     _observed, render_bin, render_blend, render_blend_bwd, render_blend_bwd_loss, render_blend_fused_loss,
+                     _observed, crop_rows, render_bin, render_blend, render_blend_bwd, render_blend_bwd_loss, render_blend_fused_loss,
                      render_blend_loss, render_chain)
 
 
@@ -202,7 +202,7 @@ class WindowEngine:
     def __init__(self, arrays: GaussianArrays, cam, views: Sequence, settings: RasterSettings,
                  cfg: OptimConfig = OptimConfig(), n_views_total: Optional[int] = None,
                  isect_cap: Optional[int] = None, stream=None, master: str = "f64", lanes: int = 1,
-                 bin_mode: Optional[int] = None):
+                 bin_mode: Optional[int] = None, bands: Optional[Sequence] = None):
         _lib.require()
         self.bin_mode = (1 if settings.alpha_cut > 0.0 else 0) if bin_mode is None else int(bin_mode)
         self.fused_blend = True             # forward + loss + backward in one kernel per view
@@ -224,6 +224,13 @@ class WindowEngine:
         dev = arrays.device
         h, w = int(cam.height), int(cam.width)
         self.h, self.w = h, w
+        # optional row bands: unit v renders rows bands[v] of view v's frame
+        # (a multi-GPU step splits views into bands when the ranks do not
+        # divide the views); the loss stays normalised by the full frame
+        self.bands = [tuple(int(y) for y in b) for b in bands] if bands is not None else [(0, h)] * len(self.views)
+        if len(self.bands) != len(self.views):
+            raise ValueError("one band per view")
+        self.view_cams = [cam if b == (0, h) else crop_rows(cam, *b) for b in self.bands]
         self.loss = LossBuffers(dev, max(1, len(self.views)))
         self.grads = ParamGradients.zeros(len(arrays), int(arrays.shs.shape[1]), dev)
         self.adam = AdamState(arrays, cfg)
@@ -261,9 +268,9 @@ class WindowEngine:
         """Measure the largest per-view intersection count (one sync per view)."""
         cap = max(1 << 16, 8 * len(self.arrays))
         worst = 0
-        for T in self.views:
+        for T, vc in zip(self.views, self.view_cams):
             while True:
-                st = RenderState(self.arrays, self.cam, T.R, T.t, self.settings, cap, self.bin_mode)
+                st = RenderState(self.arrays, vc, T.R, T.t, self.settings, cap, self.bin_mode)
                 render_bin(st, stream=self.stream)
                 M, I, over, _ = st.read_counts(self.stream)
                 if not over:
@@ -283,8 +290,8 @@ class WindowEngine:
         if self.copy_stream is None:
             self.copy_stream = torch.cuda.Stream(dev)
             self._copy_streams = [self.copy_stream] + [torch.cuda.Stream(dev) for _ in range(self.copy_streams - 1)]
-            self.obs_dev = [torch.empty((self.h, self.w, 3), dtype=observed[0].dtype, device=dev)
-                            for _ in self.views]
+            self.obs_dev = [torch.empty((y1 - y0, self.w, 3), dtype=observed[0].dtype, device=dev)
+                            for (y0, y1) in self.bands]
         for cs in self._copy_streams:
             cs.wait_event(ready)
         lib = _lib.load()
@@ -292,7 +299,7 @@ class WindowEngine:
         for v, obs in enumerate(observed):
             cs = self._copy_streams[v % len(self._copy_streams)]
             if (obs.dtype != self.obs_dev[v].dtype or obs.dtype not in (torch.float32, torch.uint8)
-                    or tuple(obs.shape) != (self.h, self.w, 3) or not obs.is_contiguous()):
+                    or tuple(obs.shape) != tuple(self.obs_dev[v].shape) or not obs.is_contiguous()):
                 raise ValueError("observed images must be contiguous float32 or uint8 (H, W, 3), one dtype")
             if capturing and not obs.is_pinned():
                 raise ValueError("graph capture needs pinned host images")
@@ -336,6 +343,7 @@ class WindowEngine:
             if sm is not main:
                 sm.wait_event(ready)
             st.set_pose(T.R, T.t)
+            st.set_camera(self.view_cams[v])
             mark("bin", sm); render_bin(st, sm); mark("bin", sm)
             obs = observed[v]
             if host:
@@ -423,7 +431,8 @@ class WindowEngine:
                 self.arena.copy_from(self.arrays)
 
     def losses(self) -> np.ndarray:
-        """Per-view loss values of the last step (syncs; one small D2H)."""
+        """Per-view loss values of the last step (syncs; one small D2H); for
+        banded units, each band's share of its view's loss."""
         s = self.loss.sums()[: len(self.views)].cpu().numpy()
         return s[:, 0] / (3.0 * self.h * self.w)
 

@@ -249,6 +249,7 @@ class RenderState:
         _lib.check(_lib.load().lsb_workspace_bytes(ctypes.byref(self.dims), ctypes.byref(nb)), "workspace")
         self.ws = torch.empty(nb.value, dtype=torch.uint8, device=arrays.device)
         self.counts = None
+        self._max_px = int(cam.width) * int(cam.height)
 
     @property
     def ws_bytes(self) -> int:
@@ -258,6 +259,15 @@ class RenderState:
         self.R_cw = np.asarray(R_cw, dtype=np.float64)
         self.t_cw = np.asarray(t_cw, dtype=np.float64)
         self.c_pose = _lib.make_pose(self.R_cw, self.t_cw)
+
+    def set_camera(self, cam) -> None:
+        """Render through another camera of at most the workspace's size (a
+        row band of the full frame: crop_rows)."""
+        if int(cam.width) * int(cam.height) > self._max_px:
+            raise ValueError("camera larger than the workspace was sized for")
+        self.cam = cam
+        self.c_cam = _lib.make_camera(cam)
+        self.dims.width, self.dims.height = int(cam.width), int(cam.height)
 
     def _ws(self):
         return ctypes.c_void_p(self.ws.data_ptr())
@@ -281,6 +291,17 @@ class RenderState:
                                                      what, ctypes.c_void_p(dst.data_ptr()),
                                                      _lib.stream_ptr(stream)), "export")
         return dst.cpu().numpy()
+
+
+def crop_rows(cam, y0: int, y1: int):
+    """The camera of rows [y0, y1) of `cam`'s frame (y0 a multiple of the
+    16-pixel tile, so the band's tiles are the frame's tiles): same
+    intrinsics with the principal point shifted up by y0."""
+    from types import SimpleNamespace
+    if y0 % TILE or not (0 <= y0 < y1 <= int(cam.height)):
+        raise ValueError("band rows must start on a tile row and lie inside the frame")
+    return SimpleNamespace(fx=float(cam.fx), fy=float(cam.fy), cx=float(cam.cx), cy=float(cam.cy) - y0,
+                           width=int(cam.width), height=int(y1 - y0))
 
 
 def _as_arrays(source) -> GaussianArrays:

@@ -32,6 +32,24 @@ def test_shard_views_partition():
             assert max(map(len, parts)) - min(map(len, parts)) <= 1
 
 
+@pytest.mark.parametrize("n,height", [(10, 1024), (64, 1080), (10, 80), (3, 48), (7, 1024)])
+def test_shard_units_cover_every_row_once_and_balance(n, height):
+    """Row-band units: every (view, row) rendered by exactly one rank; equal
+    unit counts whenever a band split exists; bands start on tile rows."""
+    from paper_2501_08672_b200.dist import shard_units, view_bands
+    for world in (1, 2, 4, 8):
+        parts = [shard_units(n, world, r, height) for r in range(world)]
+        cover = np.zeros((n, height), np.int32)
+        for p in parts:
+            for v, y0, y1 in p:
+                assert y0 % 16 == 0 and y0 < y1
+                cover[v, y0:y1] += 1
+        assert (cover == 1).all()
+        b = view_bands(n, world, height)
+        if b > 1 or n % world == 0:
+            assert len({len(p) for p in parts}) == 1
+
+
 def _views_and_scene():
     from types import SimpleNamespace
     from paper_2501_08672_b200.scene import camera_for, orbit_views

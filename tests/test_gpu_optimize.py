@@ -242,3 +242,43 @@ def test_engine_u8_frames_bit_identical(variant):
     assert np.array_equal(l1, l2)
     for k in ("means", "rots", "scales", "opacities", "shs"):
         assert bool((getattr(w1, k) == getattr(w2, k)).all()), k
+
+
+def test_engine_row_bands_equal_whole_views():
+    """Units that are row bands of the views (the multi-GPU split when the
+    ranks do not divide the views, dist.shard_units) reproduce the whole-view
+    step: per-view losses are the sums of their bands' shares, the summed
+    gradient agrees to round-off (only the order of the per-splat sums over
+    bands differs)."""
+    import torch
+    from paper_2501_08672_b200.dist import shard_units
+    from paper_2501_08672_b200.optimize import OptimConfig, WindowEngine
+    from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
+    from paper_2501_08672_b200.scene import camera_for, orbit_views
+    s = load("scene_room_0323")
+    cam = camera_for(160, 128)
+    views = orbit_views(5)
+    st = RasterSettings(alpha_cut=1 / 255)
+    gt = GaussianArrays(s["means"], s["rots"], s["scales"], s["opacities"], s["shs"])
+    frames = [_quantize(render(gt, T, cam, st, retain_cache=False).image) for T in views]
+    shs = s["shs"].copy()
+    shs[:, 0, :] += np.random.default_rng(0).uniform(-0.1, 0.1, shs[:, 0, :].shape)
+
+    def run(units):
+        win = GaussianArrays(s["means"], s["rots"], s["scales"], s["opacities"], shs)
+        eng = WindowEngine(win, cam, [views[v] for v, _, _ in units], st, OptimConfig(), lanes=2,
+                           n_views_total=len(views), bands=[(y0, y1) for _, y0, y1 in units])
+        eng.step([frames[v][y0:y1].contiguous() for v, y0, y1 in units])
+        torch.cuda.synchronize()
+        return eng.losses(), eng.grads.flat.clone()
+
+    whole = [(v, 0, 128) for v in range(5)]
+    banded = [(v, y0, y1) for v in range(5) for (y0, y1) in ((0, 48), (48, 96), (96, 128))]
+    assert sorted(u for r in range(4) for u in shard_units(5, 4, r, 128)) == \
+        [(v, y0, y0 + 32) for v in range(5) for y0 in (0, 32, 64, 96)]
+    l1, g1 = run(whole)
+    l2, g2 = run(banded)
+    per_view = l2.reshape(5, 3).sum(axis=1)
+    assert np.abs(per_view - l1).max() <= 1e-6 * np.abs(l1).max()     # f32 pixels: the shifted principal point rounds differently
+    g1, g2 = g1.cpu().numpy(), g2.cpu().numpy()
+    assert np.abs(g1 - g2).max() <= 1e-4 * np.abs(g1).max()
