@@ -301,8 +301,9 @@ __device__ __forceinline__ void emit_splat(const PreArgs& a, const Ws& w, Rec& r
         }
 }
 
-// Exclusive scan of the tile histogram (single CTA; each thread owns a run of
-// consecutive tiles, re-read from L2 instead of held in registers).
+// Exclusive scan of the tile histogram (single CTA: the counts are staged in
+// shared memory once; each thread owns a run of consecutive tiles), then the
+// heaviest-first processing order of the tiles.
 constexpr int ST_THREADS = 1024;
 __global__ void __launch_bounds__(ST_THREADS) k_scan_tiles(Ws w) {
     __shared__ int s_w[ST_THREADS / 32];
@@ -638,9 +639,11 @@ size_t tile_sort_smem() { return SORT_CAP * (sizeof(uint64_t) + 2 * sizeof(int))
 // ---- barrier-free preprocess: count, scan, emit ------------------------------
 // A single-pass preprocess with a chained scan (decoupled look-back) spent
 // ~60% of its stall samples in block barriers and look-back spins, and its
-// spinning CTAs co-ran badly with other views' blends.  Instead: (1) every warp independently computes its 32 Gaussians'
+// spinning CTAs co-ran badly with other views' blends.  Instead: (1) every
+// warp independently computes its 32 Gaussians'
 // visibility and tile counts (no barrier, no record) and writes a ballot
-// mask and two counts; (2) one CTA scans the per-warp counts; (3) warps that
+// mask and two counts (plus its 1024-warp chunk's totals); (2) one CTA per
+// chunk scans the per-warp counts from the chunk's base; (3) warps that
 // hold a visible Gaussian recompute it fully (the same code, so the same
 // bits) and write the records, keys and intersections at their offsets.
 // Slot order is still id order.
