@@ -318,6 +318,14 @@ int lsb_visual_pass(const lsb_params* p, const lsb_camera* cam, const lsb_pose* 
 int lsb_ieskf_gain(const double* cov, const double* jinv3, const double* A6, const double* b6, const double* delta,
                    double* xi, double* KH, double* P);
 
+/* A whole IESKF iteration on the host state vectors x = [R (9, row-major) |
+ * t | v | b_g | b_a] (21 doubles): delta = x_hat [-] x_bar (NavState.boxminus,
+ * estimator.py:70-75), lsb_ieskf_gain, then x_hat <- x_hat [+] xi in place
+ * (NavState.boxplus with the bias clip, estimator.py:63-68); xi, KH, P out as
+ * in lsb_ieskf_gain. */
+int lsb_ieskf_iterate(const double* cov, const double* x_bar, double* x_hat, const double* A6, const double* b6,
+                      double bias_limit, double* xi, double* KH, double* P);
+
 /* Semi-dense candidate mask (estimator.py:241-252): Sobel/8 magnitude of the
  * grey observed image (nearest border) > grad_thr and t_final < t_max.
  * observed_u8 (here and in lsb_visual_select): the frame is 8-bit, read as

@@ -84,6 +84,7 @@ SIGNATURES = [
                                   _P, _P, _P, _P, _P]),
     ("lsb_render_counts", _c.c_int, [_P, _c.POINTER(Dims), _c.POINTER(_c.c_int64), _P]),
     ("lsb_ieskf_gain", _c.c_int, [_P] * 8),
+    ("lsb_ieskf_iterate", _c.c_int, [_P, _P, _P, _P, _P, _c.c_double, _P, _P, _P]),
     ("lsb_visual_pass", _c.c_int, [_c.POINTER(Params), _c.POINTER(Camera), _c.POINTER(Pose), _c.POINTER(Settings),
                                    _P, _c.c_size_t, _c.POINTER(Dims), _P, _P, _P, _P, _c.POINTER(VisualCfg),
                                    _c.POINTER(VisualBufs), _P]),

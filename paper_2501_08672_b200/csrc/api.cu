@@ -34,6 +34,8 @@ cudaError_t launch_pose_rows(const Ws&, const lsb_settings&, int, int, int, cons
 cudaError_t launch_hb(const double*, const double*, int64_t, const int64_t*, double, double*, double*, cudaStream_t);
 int hb_scratch_doubles();
 int ieskf_gain(const double*, const double*, const double*, const double*, const double*, double*, double*, double*);
+int ieskf_iterate(const double*, const double*, double*, const double*, const double*, double, double*, double*,
+                  double*);
 cudaError_t launch_visual_select(const uint8_t*, const void*, bool, const float*, int64_t, int, double, void*, int32_t*,
                                  double*, int64_t*, cudaStream_t);
 int64_t visual_select_scratch_bytes(int64_t, int);
@@ -639,6 +641,15 @@ int lsb_ieskf_gain(const double* cov, const double* jinv3, const double* A6, con
                    double* xi, double* KH, double* P) {
     if (!cov || !jinv3 || !A6 || !b6 || !delta || !xi || !KH || !P) return fail(LSB_EINVAL, "NULL argument");
     const int r = ieskf_gain(cov, jinv3, A6, b6, delta, xi, KH, P);
+    if (r == 1) return fail(LSB_EINVAL, "singular matrix");
+    if (r == 2) return fail(LSB_EINVAL, "non-finite gain");
+    return LSB_OK;
+}
+
+int lsb_ieskf_iterate(const double* cov, const double* x_bar, double* x_hat, const double* A6, const double* b6,
+                      double bias_limit, double* xi, double* KH, double* P) {
+    if (!cov || !x_bar || !x_hat || !A6 || !b6 || !xi || !KH || !P) return fail(LSB_EINVAL, "NULL argument");
+    const int r = ieskf_iterate(cov, x_bar, x_hat, A6, b6, bias_limit, xi, KH, P);
     if (r == 1) return fail(LSB_EINVAL, "singular matrix");
     if (r == 2) return fail(LSB_EINVAL, "non-finite gain");
     return LSB_OK;

@@ -295,6 +295,17 @@ class _VisualPass:
         return o[:36].reshape(6, 6).copy(), o[36:].copy()
 
 
+def _pack(x: NavState) -> np.ndarray:
+    return np.concatenate([np.asarray(x.T_WI.R, float).reshape(9), np.asarray(x.T_WI.t, float).reshape(3),
+                           np.asarray(x.velocity, float).reshape(3), np.asarray(x.bias_gyro, float).reshape(3),
+                           np.asarray(x.bias_accel, float).reshape(3)])
+
+
+def _unpack(v: np.ndarray) -> NavState:
+    return NavState(SE3(v[:9].reshape(3, 3).copy(), v[9:12].copy()), v[12:15].copy(), v[15:18].copy(),
+                    v[18:21].copy())
+
+
 _VIS_CACHE: dict = {}
 
 
@@ -323,25 +334,27 @@ def ieskf_visual_update(state: NavState, cov: np.ndarray, observed, window, cam,
     and reduces the pose block of H^T R^-1 H and H^T R^-1 z on the GPU
     (Measurement.hb); only the 15x15 filter algebra runs on the host, using
     K z = S^-1 b and K H = S^-1 A (H is zero outside its 6 pose columns)."""
-    x_bar, x_hat = state, state.clone()
     K_H = P = None
     vis = _visual_pass(window, observed, cam, cfg, settings)
     lib = _lib.load()
     cov_c = np.ascontiguousarray(cov, dtype=np.float64)
     ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    # the states as [R | t | v | b_g | b_a] vectors; one host C++ call per
+    # iteration does boxminus, the 15x15 gain algebra and boxplus
+    # (lsb_ieskf_iterate: estimator.py:292-331)
+    x_bar = _pack(state)
+    x_hat = x_bar.copy()
+    xi, KH_buf, P_buf = np.empty(DIM), np.empty((DIM, DIM)), np.empty((DIM, DIM))
     for _ in range(max_iter):
-        A6, b6 = vis.run(x_hat, T_ic)
-        delta = x_hat.boxminus(x_bar)
-        jinv = np.ascontiguousarray(so3_left_jacobian(-delta[0:3]), dtype=np.float64)
-        xi, K_H, P = np.empty(DIM), np.empty((DIM, DIM)), np.empty((DIM, DIM))
-        # the 15x15 gain algebra (lsb_ieskf_gain, host C++): S = A + P^-1,
-        # K H = S^-1 A, K z = S^-1 b, xi = -K z - (I - K H) Hj^-1 delta
-        if lib.lsb_ieskf_gain(ptr(cov_c), ptr(jinv), ptr(np.ascontiguousarray(A6)), ptr(np.ascontiguousarray(b6)),
-                              ptr(np.ascontiguousarray(delta)), ptr(xi), ptr(K_H), ptr(P)):
+        A6, b6 = vis.run(_unpack(x_hat), T_ic)
+        if lib.lsb_ieskf_iterate(ptr(cov_c), ptr(x_bar), ptr(x_hat), ptr(np.ascontiguousarray(A6)),
+                                 ptr(np.ascontiguousarray(b6)), float(bias_limit), ptr(xi), ptr(KH_buf),
+                                 ptr(P_buf)):
             raise SingularGain(lib.lsb_last_error().decode())
-        x_hat = x_hat.boxplus(xi, bias_limit=bias_limit)
-        if np.linalg.norm(xi) < step_tol:
+        K_H, P = KH_buf, P_buf
+        if float(np.sqrt(xi @ xi)) < step_tol:
             break
+    x_hat = _unpack(x_hat)
     if K_H is None:
         return state.clone(), cov.copy()
     cov_post = (np.eye(DIM) - K_H) @ P

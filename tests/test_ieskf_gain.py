@@ -59,3 +59,35 @@ def test_singular_covariance_reports_error():
     rc, *_ = _call(np.zeros((15, 15)), np.eye(3), np.eye(6), np.zeros(6), np.zeros(15))
     assert rc != 0
     assert b"singular" in _lib().lsb_last_error()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_iterate_matches_python_state_algebra(seed):
+    """lsb_ieskf_iterate (boxminus, gain, boxplus on the state vectors) against
+    the NavState / numpy restatement of one ieskf_update iteration."""
+    from paper_2501_08672_b200.estimator import NavState, _pack, _unpack
+    from paper_2501_08672_b200.geometry import SE3, so3_exp, so3_left_jacobian
+    rng = np.random.default_rng(10 + seed)
+    xb = NavState(SE3(so3_exp(rng.normal(size=3)), rng.normal(size=3)), rng.normal(size=3),
+                  rng.uniform(-0.1, 0.1, 3), rng.uniform(-0.1, 0.1, 3))
+    xh = xb.boxplus(rng.normal(size=15) * 1e-2)
+    L = rng.normal(size=(15, 15))
+    cov = 1e-4 * (L @ L.T + 15 * np.eye(15))
+    Hr = rng.normal(size=(100, 6))
+    A6, b6 = Hr.T @ Hr * 50.0, Hr.T @ rng.normal(size=100) * 5.0
+    delta = xh.boxminus(xb)
+    xr, KHr, Pr = _ref(cov, so3_left_jacobian(-delta[:3]), A6, b6, delta)
+    ref = xh.boxplus(xr, bias_limit=0.5)
+    lib = _lib()
+    x_bar, x_hat = _pack(xb), _pack(xh)
+    xi, KH, P = np.empty(15), np.empty((15, 15)), np.empty((15, 15))
+    p = lambda a: np.ascontiguousarray(a, dtype=np.float64).ctypes.data_as(ctypes.c_void_p)
+    assert lib.lsb_ieskf_iterate(p(cov), x_bar.ctypes.data_as(ctypes.c_void_p), x_hat.ctypes.data_as(ctypes.c_void_p),
+                                 p(A6), p(b6), 0.5, xi.ctypes.data_as(ctypes.c_void_p),
+                                 KH.ctypes.data_as(ctypes.c_void_p), P.ctypes.data_as(ctypes.c_void_p)) == 0
+    assert np.abs(xi - xr).max() <= 1e-9 * max(np.abs(xr).max(), 1e-12)
+    got = _unpack(x_hat)
+    assert np.abs(got.T_WI.R - ref.T_WI.R).max() <= 1e-12
+    assert np.abs(got.T_WI.t - ref.T_WI.t).max() <= 1e-12
+    for a, b in ((got.velocity, ref.velocity), (got.bias_gyro, ref.bias_gyro), (got.bias_accel, ref.bias_accel)):
+        assert np.abs(a - b).max() <= 1e-12
