@@ -147,10 +147,12 @@ __global__ void k_fov_leaves(lsb_voxmap m, const unsigned long long* __restrict_
     const int L = m.max_level;
     const unsigned lane = threadIdx.x & 31;
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < m.cap; s += (int64_t)gridDim.x * blockDim.x) {
-        const unsigned long long key = (unsigned long long)m.keys[s];
+        // gslot first: 4 bytes per slot streamed, the key only for the leaves
+        // that hold a Gaussian (gslot >= 0 implies an occupied slot)
         bool hit = false;
         long long ix = 0, iy = 0, iz = 0;
-        if (key != EMPTY && m.gslot[s] >= 0) {
+        const unsigned long long key = m.gslot[s] >= 0 ? (unsigned long long)m.keys[s] : EMPTY;
+        if (key != EMPTY) {
             unpack_key(key, ix, iy, iz);
             const long long rx = ix >> L, ry = iy >> L, rz = iz >> L;   // floor division by 2^L
             const unsigned long long rkey = pack_key(rx, ry, rz);
