@@ -33,6 +33,9 @@ sys.path.insert(0, ROOT)
 METRIC = "splat fwd+bwd Mpix/s & Gaussians/s at 1/2/4/8 B200; % HBM roofline"
 CONFIGS = {
     # name: (v_s, n_views, width, height)
+    # "target": the north star's 500k-Gaussian / 1280x1024 / 10-keyframe window
+    # (bake_room(0.0457) = 512,808 Gaussians, the CLI orbit)
+    "target": (0.0457, 10, 1280, 1024),
     "cfg1": (0.323, 1, 640, 512),
     "cfg2": (0.0723, 10, 1280, 1024),
     "cfg5": (0.0229, 64, 1920, 1080),
@@ -101,7 +104,7 @@ class ClockSampler:
 
 
 def build_workload(cfg_name, alpha_cut):
-    from paper_2501_08672_b200.scene import bake_room, camera_for, orbit_views
+    from tools.scene import bake_room, camera_for, orbit_views
     v_s, V, W, H = CONFIGS[cfg_name]
     means, rots, scales, opac, shs = bake_room(v_s)
     rng = np.random.default_rng(0)
@@ -113,67 +116,109 @@ def build_workload(cfg_name, alpha_cut):
 
 
 # ---------------------------------------------------------------- CPU legs ---
-def cpu_sample(wl, n_views_sample, frames="u8"):
-    """Reference algorithm on this host (oracle port, C + numpy, all cores):
-    n_views_sample views of render + L1 loss + backward, then one Adam step
-    on all window Gaussians.  Returns (seconds per sampled view, seconds per
-    Adam step, host threads)."""
-    from types import SimpleNamespace
-    from oracle import raster as orc
-    from oracle.optim import Adam, DEFAULT_CFG, adam_param_step, photometric_loss
+class CpuStep:
+    """The reference algorithm on this host (oracle port: C + OpenMP blend,
+    numpy elsewhere, all host threads), on the same window, views and frames
+    as the GPU arm.  `view(v)` is one keyframe's render + L1 loss + backward,
+    accumulating the mean gradient; `adam()` is the storage-coordinate Adam
+    step on all window Gaussians with the accumulated gradient.  Observed
+    frames are rendered from the clean scene once per view, untimed."""
 
-    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)
-    keys = ("means", "rots", "scales", "opacities", "shs")
-    gt = {k: f32(v) for k, v in zip(keys, wl["gt"])}
-    P = {k: f32(v) for k, v in zip(keys, wl["win"])}
-    cam = wl["cam"]
-    st = SimpleNamespace(near=0.01, dilation=0.3, alpha_clamp=0.99, transmittance_min=1e-4, footprint_sigma=6.0,
-                         alpha_cut=wl["alpha_cut"], max_footprint_px=512.0, background=np.zeros(3), sh_degree=0)
-    t_view = []
-    for T in wl["views"][:n_views_sample]:
-        T_cw = T.inverse()
-        obs = orc.render(gt, T_cw.R, T_cw.t, cam, st)["image"]
-        if frames == "u8":      # the same 8-bit frames the GPU arm reads, as read_ppm returns them
-            obs = np.clip(np.round(obs * 255.0), 0, 255).astype(np.uint8).astype(np.float64) / 255.0
+    def __init__(self, wl, frames="u8"):
+        from types import SimpleNamespace
+        from oracle import raster as orc
+        from oracle.optim import Adam, DEFAULT_CFG, adam_param_step, photometric_loss
+        self.orc, self.loss, self.adam_step, self.cfg = orc, photometric_loss, adam_param_step, DEFAULT_CFG
+        f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)
+        keys = ("means", "rots", "scales", "opacities", "shs")
+        self.gt = {k: f32(v) for k, v in zip(keys, wl["gt"])}
+        self.P = {k: f32(v) for k, v in zip(keys, wl["win"])}
+        self.wl, self.frames, self.cam = wl, frames, wl["cam"]
+        self.st = SimpleNamespace(near=0.01, dilation=0.3, alpha_clamp=0.99, transmittance_min=1e-4,
+                                  footprint_sigma=6.0, alpha_cut=wl["alpha_cut"], max_footprint_px=512.0,
+                                  background=np.zeros(3), sh_degree=0)
+        n = len(self.P["means"])
+        self.opt = Adam({"mean": (n, 3), "rot": (n, 3), "scale": (n, 3), "opacity": (n,), "sh": self.P["shs"].shape})
+        self.obs = {}
+        self.zero()
+
+    def zero(self):
+        n = len(self.P["means"])
+        self.g = {"mean": np.zeros((n, 3)), "rot": np.zeros((n, 3)), "scale": np.zeros((n, 3)),
+                  "opacity": np.zeros(n), "sh": np.zeros(self.P["shs"].shape)}
+
+    def observed(self, v):
+        if v not in self.obs:
+            T_cw = self.wl["views"][v].inverse()
+            o = self.orc.render(self.gt, T_cw.R, T_cw.t, self.cam, self.st)["image"]
+            if self.frames == "u8":     # the same 8-bit frames the GPU arm reads, as read_ppm returns them
+                o = np.clip(np.round(o * 255.0), 0, 255).astype(np.uint8).astype(np.float64) / 255.0
+            self.obs[v] = o
+        return self.obs[v]
+
+    def view(self, v):
+        """Seconds for view v's render + loss + backward (+ gradient accumulation)."""
+        obs = self.observed(v)
+        T_cw = self.wl["views"][v].inverse()
         t0 = time.perf_counter()
-        c = orc.render(P, T_cw.R, T_cw.t, cam, st)
-        _, _, g_img = photometric_loss(c["image"], obs)
-        orc.backward(c, g_img)
-        t_view.append(time.perf_counter() - t0)
-        del c
-    n = len(P["means"])
-    adam = Adam({"mean": (n, 3), "rot": (n, 3), "scale": (n, 3), "opacity": (n,), "sh": P["shs"].shape})
-    rng = np.random.default_rng(1)
-    grads = {"mean": rng.normal(size=(n, 3)), "rot": rng.normal(size=(n, 3)), "scale": rng.normal(size=(n, 3)),
-             "opacity": rng.normal(size=n), "sh": rng.normal(size=P["shs"].shape)}
-    t0 = time.perf_counter()
-    adam_param_step(P, grads, adam, DEFAULT_CFG, np.zeros(n, bool))
-    t_adam = time.perf_counter() - t0
-    return float(np.mean(t_view)), t_adam, os.cpu_count()
+        c = self.orc.render(self.P, T_cw.R, T_cw.t, self.cam, self.st)
+        _, _, g_img = self.loss(c["image"], obs)
+        rb = self.orc.backward(c, g_img)
+        for k in self.g:
+            self.g[k] += rb["grads"][k] / self.wl["V"]
+        return time.perf_counter() - t0
+
+    def adam(self):
+        t0 = time.perf_counter()
+        self.adam_step(self.P, self.g, self.opt, self.cfg, np.zeros(len(self.P["means"]), bool))
+        self.zero()
+        return time.perf_counter() - t0
+
+
+def workload_config(args, wl):
+    """The `config` object both arms print (identical keys and values)."""
+    return {"workload": args.config, "gaussians": wl["N"], "views": wl["V"], "width": wl["W"],
+            "height": wl["H"], "alpha_cut": wl["alpha_cut"],
+            "frames": ("8-bit (H,W,3), u/255.0 in f64 like read_ppm" if args.frames == "u8" else "float32 (H,W,3)"),
+            "l2": "GPU arm: flushed before every timed step (256 MB write outside the step's event pair)"}
 
 
 def run_reference(args, wl, rank):
+    """`--impl reference`: the reference's CPU algorithm (the oracle port; the
+    Python reference cannot travel to the GPU box) on this host's cores.  A
+    timed step is ONE keyframe view (view i mod V: render + L1 loss +
+    backward), and every V-th step also runs the Adam step over all window
+    Gaussians with the accumulated mean gradient - so V consecutive steps are
+    one full window step and `value` = pixels processed / time spent."""
     if rank != 0:
         return
     V, P_px = wl["V"], wl["W"] * wl["H"]
+    cs = CpuStep(wl, args.frames)
+    for v in range(V):
+        cs.observed(v)                  # observed frames: untimed set-up
     times = []
     for i in range(args.warmup + args.steps):
-        tv, ta, cores = cpu_sample(wl, 1, args.frames)
+        v = i % V
+        t = cs.view(v)
+        if v == V - 1:
+            t += cs.adam()
         if i >= args.warmup:
-            times.append(V * tv + ta)      # one full step, extrapolated from one sampled view
+            times.append(t)
     t = float(np.mean(times))
-    value = V * P_px / t / 1e6
-    sample = (f"1 of {V} views per step (render + L1 loss + backward, {wl['W']}x{wl['H']}, {wl['N']} Gaussians, "
-              f"alpha_cut={wl['alpha_cut']:.6g}) + one Adam step; step time = {V} x view + Adam")
+    value = P_px / t / 1e6
+    sample = (f"each step = one keyframe view (render + L1 loss + backward, {wl['W']}x{wl['H']}, {wl['N']} "
+              f"Gaussians, alpha_cut={wl['alpha_cut']:.6g}), views in turn, + the Adam step over all window "
+              f"Gaussians on every {V}-th step ({sum(1 for i in range(args.warmup, args.warmup + args.steps) if i % V == V - 1)}"
+              f" Adam steps timed); oracle port, {os.cpu_count()} host threads")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Mpix/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "gaussians_per_s": V * wl["N"] / t,
-        "config": {"workload": args.config, "gaussians": wl["N"], "views": V, "width": wl["W"],
-                   "height": wl["H"], "alpha_cut": wl["alpha_cut"], "parallelism": "cpu threads",
-                   "frames": "8-bit, read_ppm's u/255.0 (f64)" if args.frames == "u8" else "float"},
-        "cpu_baseline": {"value": value, "unit": "Mpix/s", "cores": cores, "kind": "port", "sample": sample},
+        "step_unit": f"one keyframe view (+ Adam every {V}-th step); {V} steps = one window step",
+        "gaussians_per_s": wl["N"] / t,
+        "parallelism": f"cpu threads ({os.cpu_count()})",
+        "config": workload_config(args, wl),
+        "cpu_baseline": {"value": value, "unit": "Mpix/s", "cores": os.cpu_count(), "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -197,6 +242,21 @@ def algorithmic_bytes(N, K, M, I, P, pbytes=8, obytes=4):
         "chain": M * (64 + 4 + prm + 2 * grd) + I * 36,
         "adam": N * (2 * prm + grd + 4 * mom + 1),
     }
+
+
+def profile_figure(name, workload, kernel):
+    """profiles/<name> is {workload: {kernel: figure}} (one ncu capture per workload)."""
+    p = os.path.join(ROOT, "profiles", name)
+    if not os.path.exists(p):
+        return None
+    return json.load(open(p)).get(workload, {}).get(kernel)
+
+
+def survey_step_bytes(N, K, counts, bands, W):
+    """SURVEY.md §8(d) as written: B_step = 504 N + sum_v (420 M_v + 12 I_v + 52 P_v)
+    (its K = 1 figures: 64 B of parameters, 52 B of gradient / moment rows)."""
+    assert K == 1, "the survey's step model is stated for SH degree 0"
+    return 504 * N + sum(420 * c[0] + 12 * c[1] + 52 * W * (y1 - y0) for c, (y0, y1) in zip(counts, bands))
 
 
 def run_ours(args, wl, rank, world, local_rank):
@@ -350,19 +410,15 @@ def run_ours(args, wl, rank, world, local_rank):
     dom_ms = float(np.mean(ktime[dom]))
     hbm, hbm_src = peaks()
     achieved = ab[dom] / (dom_ms * 1e-3) / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(dom)
-    step_bytes = sum(ab[k] * (len(my_views) if k != "adam" else 1) for k in ab)
-    # issue-slot roofline of the same kernel: the blend is bound by instruction
-    # issue, not HBM.  Warp instructions per launch come from
-    # the committed ncu capture (profiles/issue.json); peak = 148 SMs x 4
-    # schedulers x 1 warp-instruction/clock at the SM clock sampled under load.
-    issue = None
-    ip = os.path.join(ROOT, "profiles", "issue.json")
-    if os.path.exists(ip):
-        issue = json.load(open(ip)).get(dom)
+    # ncu figures of the same kernel on the same workload (profiles/*.json are
+    # keyed by workload; another workload's capture is never attached)
+    traffic = profile_figure("traffic.json", args.config, dom)
+    issue = profile_figure("issue.json", args.config, dom)
+    # bytes of the kernels that ran in the timed step, each at its launch count
+    nlaunch = {k: len(v) // args.steps for k, v in ktime.items()}
+    ran_bytes = sum(ab[k] * nlaunch[k] for k in nlaunch)
+    # SURVEY.md §8(d)'s step model: B_step = 504 N + sum_v (420 M_v + 12 I_v + 52 P)
+    survey_bytes = survey_step_bytes(N, K, counts, bands, W)
 
     # end-to-end through the public API with host buffers: every step copies
     # this rank's observed images from pinned host memory (copy stream, in
@@ -398,9 +454,9 @@ def run_ours(args, wl, rank, world, local_rank):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "gaussians_per_s": V * N / (ms * 1e-3),
             "visible_splats_per_s": float(sum(c[0] for c in counts)) * world / (ms * 1e-3),
-            "config": {"workload": args.config, "gaussians": N, "views": V, "width": W, "height": H,
-                       "alpha_cut": wl["alpha_cut"], "parallelism": f"view-sharded dp{world}",
-                       "view_lanes": args.lanes, "exchange": exchange if world > 1 else None,
+            "parallelism": f"view-sharded dp{world}",
+            "config": workload_config(args, wl),
+            "details": {"view_lanes": args.lanes, "exchange": exchange if world > 1 else None,
                        # render units per rank: whole views, or row bands when N does not divide the views
                        "units_per_rank": [len(shard_units(V, world, r, H)) for r in range(world)],
                        "bands_per_view": view_bands(V, world, H),
@@ -409,9 +465,6 @@ def run_ours(args, wl, rank, world, local_rank):
                        "cuda_graph": graph_headline, "cuda_graph_e2e": use_graph,
                        "serial_ms_per_step": eager_ms,
                        "kernel_timing": "separate one-lane eager pass of the same steps, events around each kernel",
-                       "frames": ("8-bit (H,W,3), u/255.0 on the device like read_ppm" if args.frames == "u8"
-                                  else "float32 (H,W,3)"),
-                       "l2": "flushed before every timed step (256 MB write outside the step's event pair)",
                        "timing": "CUDA events around each step on the launching stream, median over steps",
                        "step_ms_min_max": {"serial": spreads[0], "headline": spreads[1],
                                            "e2e": spreads[2] if len(spreads) > 2 else None},
@@ -420,14 +473,20 @@ def run_ours(args, wl, rank, world, local_rank):
                          "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                          "algorithmic_bytes_per_launch": ab[dom], "avg_launch_ms": dom_ms,
                          "note": "blend is FP32-issue bound (SURVEY.md §8(d)); see profiles/"},
-            "issue_roofline": None if not issue or args.config != "cfg2" else {
+            "issue_roofline": None if not issue else {
                 "kernel": dom, "unit": "warp-inst/s", "warp_inst_per_launch": issue["warp_inst_per_launch"],
                 "achieved": issue["warp_inst_per_launch"] / (dom_ms * 1e-3),
                 "peak": 148 * 4 * (clk_sum["sm_mhz"] or 1965.0) * 1e6,
                 "frac": issue["warp_inst_per_launch"] / (dom_ms * 1e-3) / (148 * 4 * (clk_sum["sm_mhz"] or 1965.0) * 1e6),
-                "source": f"ncu capture {issue.get('capture')} (one config-2 view), live launch time"},
-            "step_roofline": {"algorithmic_bytes_per_step_rank0": step_bytes,
-                              "frac": step_bytes / (ms * 1e-3) / 1e9 / hbm},
+                "source": f"ncu capture {issue.get('capture')} (one {args.config} view), live launch time"},
+            "step_roofline": {
+                "survey_bytes_per_step_rank0": survey_bytes,
+                "survey_frac": survey_bytes / (ms * 1e-3) / 1e9 / hbm,
+                "survey_model": "SURVEY.md §8(d): 504 N + sum_v (420 M_v + 12 I_v + 52 P) (f32, K=1 form)",
+                "kernel_bytes_per_step_rank0": ran_bytes,
+                "kernel_frac": ran_bytes / (ms * 1e-3) / 1e9 / hbm,
+                "kernel_model": "algorithmic_bytes() of the kernels that ran, x their launches per step",
+                "launches_per_step": nlaunch},
             "kernel_ms_per_step": per_step_ms,
             "counts_per_unit": {"visible_M": M_avg, "intersections_I": I_avg, "pixels": P_avg},
             "clocks": clk_sum,
@@ -438,12 +497,14 @@ def run_ours(args, wl, rank, world, local_rank):
             # chain; + adam and step counter per step
         }
         if world == 1 and not args.no_cpu_baseline:
-            tv, ta, cores = cpu_sample(wl, 2, args.frames)
-            t_cpu = V * tv + ta
+            cs = CpuStep(wl, args.frames)
+            tv = [cs.view(v) for v in range(2)]
+            ta = cs.adam()
+            t_cpu = sum(tv) + ta
             out["cpu_baseline"] = {
-                "value": V * W * H / t_cpu / 1e6, "unit": "Mpix/s", "cores": cores, "kind": "port",
-                "sample": f"2 of {V} views (render + L1 + backward) + 1 Adam step on the oracle port; "
-                          f"step = {V} x mean view time + Adam ({t_cpu:.2f} s)"}
+                "value": 2 * W * H / t_cpu / 1e6, "unit": "Mpix/s", "cores": os.cpu_count(), "kind": "port",
+                "sample": f"views 0 and 1 of {V} (render + L1 + backward) + one Adam step over all {N} window "
+                          f"Gaussians on the oracle port ({t_cpu:.2f} s); value = 2 views' pixels / that time"}
         print(json.dumps(out), flush=True)
 
 
@@ -457,7 +518,7 @@ def run_voxel(args, rank, world, local_rank):
     import ctypes
     import torch
     from paper_2501_08672_b200 import _lib
-    from paper_2501_08672_b200.scene import T_LI, lidar_scan, orbit_imu_pose, room_triangles, scan_directions
+    from tools.scene import T_LI, lidar_scan, orbit_imu_pose, room_triangles, scan_directions
     from paper_2501_08672_b200.voxmap import HashOctree
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
@@ -548,7 +609,7 @@ def run_window(args, rank, world, local_rank):
     region; the timed region is the maintain calls (host wall clock around
     each, synchronised: maintain reads its counts back).  Replicas only."""
     import torch
-    from paper_2501_08672_b200.scene import T_LI, lidar_scan, orbit_imu_pose, room_triangles, scan_directions
+    from tools.scene import T_LI, lidar_scan, orbit_imu_pose, room_triangles, scan_directions
     from paper_2501_08672_b200.voxmap import HashOctree
     from paper_2501_08672_b200.window import GaussianWindow
     dev = torch.device("cuda", local_rank)
@@ -630,7 +691,7 @@ def run_lidar(args, rank, world, local_rank):
     import torch
     from paper_2501_08672_b200.estimator import FilterConfig, NavState, lidar_measurement
     from paper_2501_08672_b200.geometry import SE3
-    from paper_2501_08672_b200.scene import T_LI, lidar_scan, orbit_imu_pose, room_triangles, scan_directions
+    from tools.scene import T_LI, lidar_scan, orbit_imu_pose, room_triangles, scan_directions
     from paper_2501_08672_b200.voxmap import HashOctree
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
@@ -692,7 +753,7 @@ def run_ieskf(args, rank, world, local_rank):
     from paper_2501_08672_b200.estimator import FilterConfig, NavState, ieskf_visual_update
     from paper_2501_08672_b200.geometry import SE3, so3_exp
     from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
-    from paper_2501_08672_b200.scene import T_IC, bake_room, camera_for, orbit_imu_pose
+    from tools.scene import T_IC, bake_room, camera_for, orbit_imu_pose
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     means, rots, scales, opac, shs = bake_room(0.0457)
@@ -739,7 +800,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS) + ["cfg3", "cfg4", "window", "lidar"])
+    ap.add_argument("--config", default="target", choices=sorted(CONFIGS) + ["cfg3", "cfg4", "window", "lidar"])
     ap.add_argument("--alpha-cut", type=float, default=1.0 / 255.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--lanes", type=int, default=5, help="concurrent view pipelines per GPU")

@@ -136,9 +136,46 @@ int lsb_render_fwd(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T
                    float* image, float* t_final, int32_t* n_contrib, float* depth,
                    void* stream);
 
+/* ---- splat: replaces raster.splat (raster.py:188-205), batched --------
+ * Per Gaussian i of p (async, device outputs): geo[7 i ..] = visible (1/0),
+ * mu_i (x, y), cov_i (00, 01, 11), camera depth; color[3 i ..] = the
+ * clipped SH colour (raster.py:232-238), valid where visible.  Same f64
+ * projection / EWA covariance / footprint cull as the render's preprocess. */
+int lsb_splat(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T_cw, const lsb_settings* s,
+              double* geo, double* color, void* stream);
+
+/* ---- device sort / grouping (voxmap.py:213-230 group_by_leaf, window.py
+ * and initialize.py key grouping) -------------------------------------------
+ * Stable LSD radix sort of n (u64 key, i32 value) pairs on the low key_bits
+ * bits (8-bit digits); vals_in NULL sorts the indices 0..n-1 along.  Outputs
+ * must not alias the inputs.  lsb_segments: the start index of every run of
+ * equal keys of a sorted array (starts: up to n entries; *nseg device int64).
+ * Both use a caller workspace of lsb_sort_temp_bytes(n) bytes; async. */
+int lsb_sort_temp_bytes(int64_t n, size_t* bytes);
+int lsb_sort_pairs(const uint64_t* keys_in, const int32_t* vals_in, uint64_t* keys_out, int32_t* vals_out,
+                   int64_t n, int key_bits, void* temp, size_t temp_bytes, void* stream);
+int lsb_segments(const uint64_t* keys_sorted, int64_t n, int64_t* starts, int64_t* nseg, void* temp,
+                 size_t temp_bytes, void* stream);
+
 /* Synchronises `stream`; counts[0]=visible splats M, [1]=intersections I,
  * [2]=overflow flag (1 if I > isect_cap), [3]=isect_cap. */
 int lsb_render_counts(const void* ws, const lsb_dims* dims, int64_t counts[4], void* stream);
+
+/* Sticky capacity overflow of a workspace: set by every render whose
+ * intersections exceed isect_cap (the per-render flag, counts[2], is reset
+ * by the next render; this one is not).  `out` (host, may be NULL) receives
+ * it after synchronising `stream`; clear != 0 then resets it (stream-ordered,
+ * graph-capturable when out == NULL).  Call with clear = 1 once after
+ * allocating a workspace. */
+int lsb_render_sticky(void* ws, const lsb_dims* dims, int64_t* out, int clear, void* stream);
+
+/* Synchronises `stream`; the alpha_cut band statistics of the last forward
+ * (_kernels.py:104 decided in f64 where the blend's f32 alpha is within
+ * CUT_BAND of the cut): out[0]=tiles re-blended, [1]=band pairs decided in
+ * f64, [2]=of those, pairs composited, [3]=the largest relative error of the
+ * f32 alpha against the f64 one over those pairs, as float bits.  All zero
+ * when alpha_cut == 0. */
+int lsb_render_band_stats(const void* ws, const lsb_dims* dims, int64_t out[4], void* stream);
 
 /* Export the render state for parity checks (async):
  *   what=0: visible Gaussian ids, ascending (= slot order)  -> int32[M]

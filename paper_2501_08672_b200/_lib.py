@@ -79,10 +79,17 @@ SIGNATURES = [
     ("lsb_abi_version", _c.c_int, []),
     ("lsb_last_error", _c.c_char_p, []),
     ("lsb_workspace_bytes", _c.c_int, [_c.POINTER(Dims), _c.POINTER(_c.c_size_t)]),
+    ("lsb_sort_temp_bytes", _c.c_int, [_c.c_int64, _c.POINTER(_c.c_size_t)]),
+    ("lsb_sort_pairs", _c.c_int, [_P, _P, _P, _P, _c.c_int64, _c.c_int, _P, _c.c_size_t, _P]),
+    ("lsb_segments", _c.c_int, [_P, _c.c_int64, _P, _P, _P, _c.c_size_t, _P]),
+    ("lsb_splat", _c.c_int, [_c.POINTER(Params), _c.POINTER(Camera), _c.POINTER(Pose), _c.POINTER(Settings),
+                             _P, _P, _P]),
     ("lsb_render_fwd", _c.c_int, [_c.POINTER(Params), _c.POINTER(Camera), _c.POINTER(Pose),
                                   _c.POINTER(Settings), _P, _c.c_size_t, _c.POINTER(Dims),
                                   _P, _P, _P, _P, _P]),
     ("lsb_render_counts", _c.c_int, [_P, _c.POINTER(Dims), _c.POINTER(_c.c_int64), _P]),
+    ("lsb_render_sticky", _c.c_int, [_P, _c.POINTER(Dims), _c.POINTER(_c.c_int64), _c.c_int, _P]),
+    ("lsb_render_band_stats", _c.c_int, [_P, _c.POINTER(Dims), _c.POINTER(_c.c_int64), _P]),
     ("lsb_ieskf_gain", _c.c_int, [_P] * 8),
     ("lsb_ieskf_iterate", _c.c_int, [_P, _P, _P, _P, _P, _c.c_double, _P, _P, _P]),
     ("lsb_visual_pass", _c.c_int, [_c.POINTER(Params), _c.POINTER(Camera), _c.POINTER(Pose), _c.POINTER(Settings),

@@ -17,7 +17,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path
 # per-file extra flags: the preprocess keeps f64 rounding where numpy rounds
 EXTRA = {"preprocess.cu": ["--fmad=false"], "adam.cu": ["--fmad=false"]}
 SOURCES = ["preprocess.cu", "blend.cu", "chain.cu", "loss.cu", "adam.cu", "pose.cu", "voxmap.cu", "window.cu",
-           "ieskf.cu", "api.cu"]
+           "ieskf.cu", "sort.cu", "api.cu"]
 
 
 def build(verbose: bool = False, defines=(), out: str = OUT, tag: str = "") -> str:

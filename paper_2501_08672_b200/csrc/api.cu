@@ -6,6 +6,11 @@
 #include "common.cuh"
 
 namespace lsb {
+cudaError_t launch_splat(const lsb_params&, const lsb_camera&, const lsb_pose&, const lsb_settings&, double*, double*,
+                         cudaStream_t);
+size_t sort_temp_bytes(int64_t n);
+cudaError_t launch_sort_pairs(const uint64_t*, const int32_t*, uint64_t*, int32_t*, int64_t, int, void*, cudaStream_t);
+cudaError_t launch_segments(const uint64_t*, int64_t, int64_t*, int64_t*, void*, cudaStream_t);
 cudaError_t launch_preprocess(const lsb_params&, const lsb_camera&, const lsb_pose&, const lsb_settings&,
                               const Ws&, cudaStream_t);
 cudaError_t launch_blend_fwd(const Ws&, const lsb_settings&, int, int, float*, float*, int32_t*, float*,
@@ -142,6 +147,41 @@ int lsb_render_fwd(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T
                       "blend_fwd");
 }
 
+int lsb_sort_temp_bytes(int64_t n, size_t* bytes) {
+    if (!bytes || n < 0) return fail(LSB_EINVAL, "bad argument");
+    *bytes = sort_temp_bytes(n);
+    return LSB_OK;
+}
+
+int lsb_sort_pairs(const uint64_t* keys_in, const int32_t* vals_in, uint64_t* keys_out, int32_t* vals_out, int64_t n,
+                   int key_bits, void* temp, size_t temp_bytes, void* stream) {
+    if (n < 0 || n > 0x7fffffffll || key_bits < 1 || key_bits > 64) return fail(LSB_EINVAL, "bad n or key_bits");
+    if (n > 0 && (!keys_in || !keys_out || !vals_out || !temp)) return fail(LSB_EINVAL, "NULL argument");
+    if ((const void*)keys_in == (const void*)keys_out || (vals_in && (const void*)vals_in == (const void*)vals_out))
+        return fail(LSB_EINVAL, "sort outputs must not alias the inputs");
+    if (temp_bytes < sort_temp_bytes(n)) return fail(LSB_EINVAL, "sort workspace too small");
+    return check_cuda(launch_sort_pairs(keys_in, vals_in, keys_out, vals_out, n, key_bits, temp, (cudaStream_t)stream),
+                      "sort_pairs");
+}
+
+int lsb_segments(const uint64_t* keys_sorted, int64_t n, int64_t* starts, int64_t* nseg, void* temp,
+                 size_t temp_bytes, void* stream) {
+    if (n < 0 || n > 0x7fffffffll) return fail(LSB_EINVAL, "bad n");
+    if (!nseg || (n > 0 && (!keys_sorted || !starts || !temp))) return fail(LSB_EINVAL, "NULL argument");
+    if (temp_bytes < sort_temp_bytes(n)) return fail(LSB_EINVAL, "sort workspace too small");
+    return check_cuda(launch_segments(keys_sorted, n, starts, nseg, temp, (cudaStream_t)stream), "segments");
+}
+
+int lsb_splat(const lsb_params* p, const lsb_camera* cam, const lsb_pose* T, const lsb_settings* s, double* geo,
+              double* color, void* stream) {
+    if (!p || !cam || !T || !s || !geo || !color) return fail(LSB_EINVAL, "NULL argument");
+    if (p->n > 0 && (!p->means || !p->rots || !p->scales || !p->opacities || !p->shs))
+        return fail(LSB_EINVAL, "NULL parameter array");
+    if (p->sh_coeffs < 1 || p->sh_coeffs > 16) return fail(LSB_EINVAL, "sh_coeffs must be 1..16");
+    if (p->dtype != 0 && p->dtype != 1) return fail(LSB_EINVAL, "params dtype must be 0 (f32) or 1 (f64)");
+    return check_cuda(launch_splat(*p, *cam, *T, *s, geo, color, (cudaStream_t)stream), "splat");
+}
+
 int lsb_render_counts(const void* ws, const lsb_dims* d, int64_t counts[4], void* stream) {
     Ws w;
     int rc = get_ws((void*)ws, (size_t)-1, d, &w);
@@ -156,6 +196,40 @@ int lsb_render_counts(const void* ws, const lsb_dims* d, int64_t counts[4], void
     counts[1] = (int64_t)h[1];
     counts[2] = (int64_t)h[2];
     counts[3] = d->isect_cap;
+    return LSB_OK;
+}
+
+int lsb_render_sticky(void* ws, const lsb_dims* d, int64_t* out, int clear, void* stream) {
+    Ws w;
+    int rc = get_ws(ws, (size_t)-1, d, &w);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (out) {
+        unsigned long long h = 0;
+        rc = check_cuda(cudaMemcpyAsync(&h, w.sticky, sizeof(h), cudaMemcpyDeviceToHost, st), "sticky");
+        if (rc) return rc;
+        rc = check_cuda(cudaStreamSynchronize(st), "sticky sync");
+        if (rc) return rc;
+        *out = (int64_t)h;
+    }
+    if (clear) return check_cuda(cudaMemsetAsync(w.sticky, 0, sizeof(unsigned long long), st), "sticky clear");
+    return LSB_OK;
+}
+
+int lsb_render_band_stats(const void* ws, const lsb_dims* d, int64_t out[4], void* stream) {
+    Ws w;
+    int rc = get_ws((void*)ws, (size_t)-1, d, &w);
+    if (rc) return rc;
+    unsigned long long h[16];
+    cudaStream_t st = (cudaStream_t)stream;
+    rc = check_cuda(cudaMemcpyAsync(h, w.ctr, sizeof(h), cudaMemcpyDeviceToHost, st), "band stats");
+    if (rc) return rc;
+    rc = check_cuda(cudaStreamSynchronize(st), "band stats sync");
+    if (rc) return rc;
+    out[0] = (int64_t)h[9];
+    out[1] = (int64_t)h[12];
+    out[2] = (int64_t)h[13];
+    out[3] = (int64_t)(h[14] & 0xffffffffull);
     return LSB_OK;
 }
 
@@ -179,7 +253,7 @@ __global__ void k_export(Ws w, int what, void* dst) {
             ((int32_t*)dst)[2 * t + 1] = w.tile_start[t + 1];
         }
     } else if (what == 3) {
-        for (int64_t j = i0; j < I && j < w.cap; j += stride) ((int32_t*)dst)[j] = w.rec[w.tile_slot[j]].id;
+        for (int64_t j = i0; j < I && j < w.cap; j += stride) ((int32_t*)dst)[j] = w.rec[w.tile_slot[j] & SLOT_MASK].id;
     } else if (what == 4) {
         for (int64_t i = i0; i < M; i += stride) ((double*)dst)[i] = __longlong_as_double((long long)w.vkey[i]);
     }

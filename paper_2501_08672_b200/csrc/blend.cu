@@ -55,7 +55,7 @@ namespace lsb {
 #define FUSED_RESERVE 1      // CTA slots per SM the fused blend leaves to the other lanes
 #endif
 constexpr int WPB = LSB_WPB;  // tile-warps per CTA
-constexpr int RUN = 4;       // pixels per lane and row (horizontal run)
+constexpr int RUN = RUN_PX;  // pixels per lane and row (horizontal run)
 #ifndef FWD_MIN_BLOCKS
 #define FWD_MIN_BLOCKS 6
 #endif
@@ -76,48 +76,46 @@ struct BlendArgs {
     float bg0, bg1, bg2;
     float cutp;       // cut / clamp: the test on the saturated alpha
     float ik;         // 1 / clamp
+    float cutlo, cuthi;    // cut' (1 -+ CUT_BAND): the band where a flagged entry's pairs are decided in f64
+    double clamp_d, cut_d;
 };
-
-// Per-record frame of one lane: the splat mean relative to the lane's first
-// pixel (gx0, gy0) and the opacity folded into the exponent.
-struct Frame {
-    float mxr, myr, lop;
-};
-
-__device__ __forceinline__ Frame frame_of(float4 q0, float lop, float gx0f, float gy0f) {
-    Frame f;
-    f.mxr = __fadd_rn(__fsub_rn(q0.x, gx0f), q0.z);
-    f.myr = __fadd_rn(__fsub_rn(q0.y, gy0f), q0.w);
-    f.lop = lop;
-    return f;
-}
-
-// Records with lop below this cannot saturate (a' < 1 for every pixel).
-constexpr float SAT_LOP = -1e-6f;
-
-// Row terms: u0 = x_local + s dy - mx at the run's first pixel, and the
-// row part of the exponent E dy^2 + log2(op / clamp).
-__device__ __forceinline__ void row_terms(const Frame& f, float s, float E, float rowoff, float& dy, float& u0,
-                                          float& edy) {
-    dy = __fsub_rn(rowoff, f.myr);
-    u0 = __fmaf_rn(s, dy, -f.mxr);
-    edy = __fmaf_rn(__fmul_rn(E, dy), dy, f.lop);
-}
-
-// Saturated alpha of pixel j of the run: a = min(1, op g / clamp).  With
-// SAT false the record cannot saturate and the min is dropped.
-template <bool SAT = true>
-__device__ __forceinline__ float alpha_sat(float A, float u0, float edy, int j, float& u) {
-    u = j == 0 ? u0 : __fadd_rn(u0, (float)j);
-    const float e = ex2_approx(__fmaf_rn(A, __fmul_rn(u, u), edy));
-    return SAT ? __saturatef(e) : e;
-}
 
 // Per-column liveness threshold of a record: T must reach t_min for pixels
 // inside the bbox columns [cx0, cx1) of the run, +inf outside, so one
 // compare gives "alive and in bbox".
 __device__ __forceinline__ float col_thr(int j, int cx0, int cx1, float tmin) {
     return (j >= cx0 && j < cx1) ? tmin : __int_as_float(0x7f800000);
+}
+
+// ---- the alpha_cut band -----------------------------------------------------
+// The walks decide `alpha < alpha_cut` (_kernels.py:104) in f32.  Where the
+// f32 alpha lies too close to the cut for that to be the reference's f64
+// decision, the decision was taken in f64 during binning (preprocess.cu,
+// band_search in the scatter): a tile entry with such pixels carries OVR_BIT
+// in tile_slot and a row of 256-bit masks (the tile's band pixels, and their
+// f64 decisions), which the walks' threshold for those pixels follows: 0
+// (composite) or +inf (skip) instead of cut'.  All other pairs are decided in
+// f32 at least 5x farther from the cut than the f32 alpha's error (CUT_BAND,
+// common.cuh); the hot path pays one bit test per record.
+
+// Thresholds of the lane's pixels for a flagged entry.  Nibble h holds the
+// lane's 4 pixels of row r0 + 8h.
+struct OvrNib {
+    unsigned band[2], take[2];
+};
+__device__ __forceinline__ OvrNib ovr_nibbles(const Ws& w, int j, int lane) {
+    const uint32_t* m = w.ovr + (size_t)w.ovr_of[w.tile_e[j]] * 16;
+    OvrNib o;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int bit = ((lane >> 2) + 8 * h) * TILE + (lane & 3) * RUN;
+        o.band[h] = (m[bit >> 5] >> (bit & 31)) & 0xfu;
+        o.take[h] = (m[8 + (bit >> 5)] >> (bit & 31)) & 0xfu;
+    }
+    return o;
+}
+__device__ __forceinline__ float ovr_cut(const OvrNib& o, int h, int j, float cutp) {
+    return ((o.band[h] >> j) & 1u) ? (((o.take[h] >> j) & 1u) ? 0.f : __int_as_float(0x7f800000)) : cutp;
 }
 
 // Forward pixel update, predicated (no branches, no selects):
@@ -238,13 +236,16 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-// Per-warp record pipeline over one tile list [start, end).
+// Per-warp record pipeline over one tile list [start, end).  `ovr` holds
+// one bit per record of the batch being blended: the entry has band pixels
+// whose alpha_cut decisions come from the f64 override masks.
 struct RecPipe {
     Rec* buf;           // [2][32] in shared memory
     int start, end, slot_next;
+    unsigned ovr, ovr_next;
     __device__ __forceinline__ void fetch(const Ws& w, int batch, int slot, int lane) {
         if (slot >= 0) {
-            const float4* src = (const float4*)(w.rec + slot);
+            const float4* src = (const float4*)(w.rec + (slot & SLOT_MASK));
             float4* dst = (float4*)(buf + (batch & 1) * 32 + lane);
 #pragma unroll
             for (int q = 0; q < 4; ++q) cp_async16(dst + q, src + q);
@@ -254,11 +255,15 @@ struct RecPipe {
     __device__ __forceinline__ int slot_at(const Ws& w, int j) const { return j < end ? w.tile_slot[j] : -1; }
     // prologue: batch 0 in flight, slots of batch 1 loaded
     __device__ __forceinline__ void begin(const Ws& w, int lane) {
-        fetch(w, 0, slot_at(w, start + lane), lane);
+        const int s0 = slot_at(w, start + lane);
+        ovr_next = __ballot_sync(0xffffffffu, s0 > 0 && (s0 & OVR_BIT));
+        fetch(w, 0, s0, lane);
         slot_next = slot_at(w, start + 32 + lane);
     }
     // start fetching batch b+1, then wait for batch b; returns its records
     __device__ __forceinline__ const Rec* next(const Ws& w, int b, int lane) {
+        ovr = ovr_next;
+        ovr_next = __ballot_sync(0xffffffffu, slot_next > 0 && (slot_next & OVR_BIT));
         fetch(w, b + 1, slot_next, lane);
         slot_next = slot_at(w, start + 32 * (b + 2) + lane);
         cp_wait<1>();
@@ -305,6 +310,35 @@ __global__ void __launch_bounds__(LT_THREADS) k_loss_total(int ntiles, const dou
         }
         out[0] = a0;
         out[1] = a1;
+    }
+}
+
+// One record's update of the lane's 8 pixels (rows r0, r0 + 8 of the run)
+// in the forward walk.  OVR: the entry has band pixels (per-pixel thresholds
+// from the f64 override masks), else the one threshold `cut`.
+template <bool COUNT, bool DEPTH, bool OVR>
+__device__ __forceinline__ void fwd_pixels(const Frame& f, float4 qb, float4 qc, bool row0, bool row1,
+                                           const float* thr, float cut, float nkap, const OvrNib& o,
+                                           float (&T)[2][RUN], float (&cnt)[2][RUN], float (&cr)[2][RUN],
+                                           float (&cg)[2][RUN], float (&cb)[2][RUN], float (&dz)[2][RUN]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        if (!(h ? row1 : row0)) continue;
+        float dy, u0, edy;
+        row_terms(f, qb.y, qb.z, 8.f * h, dy, u0, edy);
+#pragma unroll
+        for (int j = 0; j < RUN; ++j) {
+            float u;
+            const float al = alpha_sat(qb.x, u0, edy, j, u);
+            const float cj = OVR ? ovr_cut(o, h, j, cut) : cut;
+            if (!COUNT && !DEPTH)
+                fwd_pixel_nc(al, thr[j], cj, nkap, qc.x, qc.y, qc.z, T[h][j], cr[h][j], cg[h][j], cb[h][j]);
+            else if (DEPTH)
+                fwd_pixel_depth(al, thr[j], cj, nkap, qc.x, qc.y, qc.z, qc.w, T[h][j], cnt[h][j], cr[h][j], cg[h][j],
+                                cb[h][j], dz[h][j]);
+            else
+                fwd_pixel(al, thr[j], cj, nkap, qc.x, qc.y, qc.z, T[h][j], cnt[h][j], cr[h][j], cg[h][j], cb[h][j]);
+        }
     }
 }
 
@@ -378,26 +412,12 @@ k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __r
                 const float4 qb = *(const float4*)&sr[k].A;          // A s E lop
                 const float4 qc = *(const float4*)&sr[k].kc0;        // clamp * (c0 c1 c2 z)
                 const Frame f = frame_of(q0, qb.w, gx0f, gy0f);
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    if (!(h ? row1 : row0)) continue;
-                    float dy, u0, edy;
-                    row_terms(f, qb.y, qb.z, 8.f * h, dy, u0, edy);
-#pragma unroll
-                    for (int j = 0; j < RUN; ++j) {
-                        float u;
-                        const float al = alpha_sat(qb.x, u0, edy, j, u);
-                        if (!COUNT && !DEPTH)
-                            fwd_pixel_nc(al, thr[j], CUT ? a.cutp : 0.f, -kap, qc.x, qc.y, qc.z, T[h][j], cr[h][j],
-                                         cg[h][j], cb[h][j]);
-                        else if (DEPTH)
-                            fwd_pixel_depth(al, thr[j], CUT ? a.cutp : 0.f, -kap, qc.x, qc.y, qc.z, qc.w, T[h][j],
-                                            cnt[h][j], cr[h][j], cg[h][j], cb[h][j], dz[h][j]);
-                        else
-                            fwd_pixel(al, thr[j], CUT ? a.cutp : 0.f, -kap, qc.x, qc.y, qc.z, T[h][j], cnt[h][j],
-                                      cr[h][j], cg[h][j], cb[h][j]);
-                    }
-                }
+                if (CUT && ((pipe.ovr >> k) & 1u))      // band pixels: the f64 decisions
+                    fwd_pixels<COUNT, DEPTH, true>(f, qb, qc, row0, row1, thr, a.cutp, -kap,
+                                                   ovr_nibbles(w, base + k, lane), T, cnt, cr, cg, cb, dz);
+                else
+                    fwd_pixels<COUNT, DEPTH, false>(f, qb, qc, row0, row1, thr, CUT ? a.cutp : 0.f, -kap, OvrNib{},
+                                                    T, cnt, cr, cg, cb, dz);
             }
             __syncwarp();
         }
@@ -482,23 +502,26 @@ __device__ __forceinline__ float reduce8(const float* v, int lane) {
 // alphas, skip the half when no pixel of it reaches alpha_cut (a superset of
 // the exact per-pixel test in bwd_pixel), else update the pixels and fold the
 // row sums into the record's moments M.
-template <bool SAT>
+template <bool SAT, bool OVR = false>
 __device__ __forceinline__ void bwd_half(const Frame& f, float4 q1, bool rin, float dyoff, const float* thr,
                                          const BlendArgs& a, float kap, float4 q2, const float* Gr, const float* Gg,
-                                         const float* Gb, float* T, float* gD, float* c, float* M) {
+                                         const float* Gb, float* T, float* gD, float* c, float* M,
+                                         const OvrNib& o = OvrNib{}, int h = 0) {
     float dy, u0, edy;
     row_terms(f, q1.y, q1.z, dyoff, dy, u0, edy);
     float al[RUN], uu[RUN];
 #pragma unroll
     for (int j = 0; j < RUN; ++j) al[j] = alpha_sat<SAT>(q1.x, u0, edy, j, uu[j]);
-    const float amax = fmaxf(fmaxf(al[0], al[1]), fmaxf(al[2], al[3]));
-    if (!__any_sync(0xffffffffu, rin && amax >= a.cutp)) return;
+    if (!OVR) {        // (with band pixels an overridden pair may composite below cut')
+        const float amax = fmaxf(fmaxf(al[0], al[1]), fmaxf(al[2], al[3]));
+        if (!__any_sync(0xffffffffu, rin && amax >= a.cutp)) return;
+    }
     if (!rin) return;
     float S0 = 0.f, S1 = 0.f, S2 = 0.f;
 #pragma unroll
     for (int j = 0; j < RUN; ++j)
-        bwd_pixel<SAT>(al[j], uu[j], thr[j], a.cutp, -kap, a.ik, q2.x, q2.y, q2.z, Gr[j], Gg[j], Gb[j], T[j], gD[j],
-                       c[0], c[1], c[2], S0, S1, S2);
+        bwd_pixel<SAT>(al[j], uu[j], thr[j], OVR ? ovr_cut(o, h, j, a.cutp) : a.cutp, -kap, a.ik, q2.x, q2.y, q2.z,
+                       Gr[j], Gg[j], Gb[j], T[j], gD[j], c[0], c[1], c[2], S0, S1, S2);
     M[0] += S0;
     M[1] += S1;
     M[2] = fmaf(S0, dy, M[2]);
@@ -551,7 +574,13 @@ __device__ __forceinline__ void bwd_walk(const Ws& w, const BlendArgs& a, RecPip
 #pragma unroll
                 for (int j = 0; j < RUN; ++j) thr[j] = over ? col_thr(j, cx0, cx1, a.tmin) : __int_as_float(0x7f800000);
                 const Frame f = frame_of(q0, q1.w, gx0f, gy0f);
-                if (q1.w >= SAT_LOP) {
+                if ((pipe.ovr >> k) & 1u) {            // band pixels: the f64 decisions (saturating form)
+                    const OvrNib o = ovr_nibbles(w, base + k, lane);
+                    bwd_half<true, true>(f, q1, over && row0, 0.f, thr, a, kap, q2, Gr[0], Gg[0], Gb[0], T[0], gD[0], c,
+                                         M, o, 0);
+                    bwd_half<true, true>(f, q1, over && row1, 8.f, thr, a, kap, q2, Gr[1], Gg[1], Gb[1], T[1], gD[1], c,
+                                         M, o, 1);
+                } else if (q1.w >= SAT_LOP) {
                     bwd_half<true>(f, q1, over && row0, 0.f, thr, a, kap, q2, Gr[0], Gg[0], Gb[0], T[0], gD[0], c, M);
                     bwd_half<true>(f, q1, over && row1, 8.f, thr, a, kap, q2, Gr[1], Gg[1], Gb[1], T[1], gD[1], c, M);
                 } else {
@@ -682,6 +711,10 @@ static BlendArgs blend_args(const lsb_settings& s, int W, int H) {
                 (float)s.background[0], (float)s.background[1], (float)s.background[2], 0.f, 0.f};
     a.cutp = (float)(s.alpha_cut / s.alpha_clamp);
     a.ik = (float)(1.0 / s.alpha_clamp);
+    a.cutlo = (float)(s.alpha_cut / s.alpha_clamp * (1.0 - CUT_BAND));
+    a.cuthi = (float)(s.alpha_cut / s.alpha_clamp * (1.0 + CUT_BAND));
+    a.clamp_d = s.alpha_clamp;
+    a.cut_d = s.alpha_cut;
     return a;
 }
 
@@ -766,19 +799,12 @@ k_blend_fused(Ws w, BlendArgs a, LossArgs L) {
                 const float4 qb = *(const float4*)&sr[k].A;
                 const float4 qc = *(const float4*)&sr[k].kc0;
                 const Frame f = frame_of(q0v, qb.w, gx0f, gy0f);
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    if (!(h ? row1 : row0)) continue;
-                    float dy, u0, edy;
-                    row_terms(f, qb.y, qb.z, 8.f * h, dy, u0, edy);
-#pragma unroll
-                    for (int j = 0; j < RUN; ++j) {
-                        float u;
-                        const float al = alpha_sat(qb.x, u0, edy, j, u);
-                        fwd_pixel_nc(al, thr[j], CUT ? a.cutp : 0.f, -kap, qc.x, qc.y, qc.z, T[h][j], cr[h][j],
-                                     cg[h][j], cb[h][j]);
-                    }
-                }
+                if (CUT && ((pipe.ovr >> k) & 1u))      // band pixels: the f64 decisions
+                    fwd_pixels<false, false, true>(f, qb, qc, row0, row1, thr, a.cutp, -kap,
+                                                   ovr_nibbles(w, base + k, lane), T, T, cr, cg, cb, T);
+                else
+                    fwd_pixels<false, false, false>(f, qb, qc, row0, row1, thr, CUT ? a.cutp : 0.f, -kap, OvrNib{},
+                                                    T, T, cr, cg, cb, T);
             }
             __syncwarp();
         }

@@ -34,17 +34,77 @@ struct __align__(16) Rec {
 };
 static_assert(sizeof(Rec) == 64, "Rec must be 64 bytes");
 
-// Footprint of a splat's alpha >= alpha_cut region for the contributing-list
-// binning mode (lsb_settings.bin_mode = 1): the ellipse
-// d^T cov_i^-1 d <= thr around mu_i, f64 (written by the preprocess, re-read
-// by the scatter so both enumerate the same tiles).
+// f64 screen geometry of a visible splat, written by the preprocess whenever
+// alpha_cut > 0: mu_i, cov_i (ca, cb, cc), the opacity, and the threshold of
+// its alpha >= alpha_cut ellipse d^T cov_i^-1 d <= thr for the
+// contributing-list binning mode (lsb_settings.bin_mode = 1; re-read by the
+// scatter so both enumerate the same tiles).  The blend re-reads it for the
+// rare pairs whose f32 alpha lies within rounding of alpha_cut
+// (exact_alpha below).
 struct CullGeo {
-    double mux, muy, ca, cb, cc, thr;
+    double mux, muy, ca, cb, cc, thr, op;
+    double c0, c1, c2;            // conic = (cc, -cb, ca) / det, as raster.py:175 forms it
+    float kf, sf, ic0f, qcf;      // f32 row form of q for the band search: q = c0 (dx + s dy)^2 + k dy^2,
+                                  // 1 / c0, and q at alpha = cut: 2 ln(op / cut)
 };
+static_assert(sizeof(CullGeo) == 96, "CullGeo is 96 bytes");
 
+// The f64 screen geometry of a visible splat (preprocess, alpha_cut > 0).
+__device__ __forceinline__ CullGeo make_cull_geo(double mux, double muy, double ca, double cb, double cc, double thr,
+                                                 double op, double cut) {
+    CullGeo g;
+    g.mux = mux;
+    g.muy = muy;
+    g.ca = ca;
+    g.cb = cb;
+    g.cc = cc;
+    g.thr = thr;
+    g.op = op;
+    const double det = __dsub_rn(__dmul_rn(ca, cc), __dmul_rn(cb, cb));
+    g.c0 = __ddiv_rn(cc, det);
+    g.c1 = __ddiv_rn(-cb, det);
+    g.c2 = __ddiv_rn(ca, det);
+    const double sr = g.c1 / g.c0;
+    g.sf = (float)sr;
+    g.kf = (float)(g.c2 - g.c1 * sr);
+    g.ic0f = (float)(1.0 / g.c0);
+    g.qcf = (float)(2.0 * log(fmax(op / cut, 1e-300)));
+    return g;
+}
+
+// Relative half-width of the band around alpha_cut inside which the blend's
+// f32 alpha (shear-form exponent + ex2.approx) is not trusted to decide
+// `alpha < alpha_cut` the way the reference's f64 does: every (pixel, splat)
+// pair inside it gets its decision from exact_alpha instead (the tile
+// entries that can hold such pairs are flagged before the blend,
+// k_band_overrides).  The largest f32 error measured over the band pixels of the
+// benchmark views is 1.4e-6 (lsb_render_band_stats), 5.4x inside the band.
+#ifndef LSB_CUT_BAND_LOG2
+#define LSB_CUT_BAND_LOG2 17
+#endif
+constexpr double CUT_BAND = 1.0 / (double)(1 << LSB_CUT_BAND_LOG2);
+// A sorted tile entry (tile_slot[j]) with band pixels carries this bit; the
+// slot is tile_slot[j] & SLOT_MASK.
+constexpr int32_t OVR_BIT = 1 << 30;
+constexpr int32_t SLOT_MASK = OVR_BIT - 1;
+
+// The reference's alpha in f64 (_kernels.py:64-71): conic = (cc, -cb, ca) /
+// det (raster.py:175), q = c0 dx^2 + 2 c1 dx dy + c2 dy^2 left to right
+// without contraction, a = min(op exp(-q/2), clamp).  The pair composites
+// iff !(a < alpha_cut) (_kernels.py:104).
+__device__ __forceinline__ double exact_alpha(const CullGeo& g, double clamp, double px, double py) {
+    const double dx = __dsub_rn(px, g.mux), dy = __dsub_rn(py, g.muy);
+    double q = __dmul_rn(__dmul_rn(g.c0, dx), dx);
+    q = __dadd_rn(q, __dmul_rn(__dmul_rn(__dmul_rn(2.0, g.c1), dx), dy));
+    q = __dadd_rn(q, __dmul_rn(__dmul_rn(g.c2, dy), dy));
+    const double a = __dmul_rn(g.op, exp(__dmul_rn(-0.5, q)));
+    return a > clamp ? clamp : a;
+}
 struct Ws {
     unsigned long long* ctr;    // [0] M, [1] I, [2] overflow, [3] preprocess ticket, [4] chain ticket,
-                                // [5] fused-loss tiles done, [6] big-tile count, [7] fwd / [8] bwd tile queues
+                                // [5] fused-loss tiles done, [6] big-tile count, [7] fwd / [8] bwd tile queues,
+                                // [9] entries flagged OVR_BIT (rows of ovr used), [12] band pixels decided
+                                // in f64, [13] of them composited, [14] max relative f32 alpha error there
     Rec* rec;                   // [n] (only the first M are live)
     uint64_t* vkey;             // [n] depth bits of live splats
     uint32_t* colmask;          // [n] interior bits (3) of live splats
@@ -58,6 +118,12 @@ struct Ws {
     int32_t* tile_slot;         // [cap] visible slot, per-tile depth order
     int32_t* sort_scratch;      // [cap * 8] fallback sort buffers (tiles > SORT_CAP)
     float* part;                // [cap * NUM_PART] per-intersection gradient partials (AoS)
+    int32_t* ovr_of;            // [cap] per intersection e whose entry is flagged OVR_BIT: its row of `ovr`
+    uint32_t* ovr;              // [ovr_cap][16]: per flagged (tile, splat) entry, 256-bit masks of the
+                                // tile's band pixels [0..7] and of their f64 decisions (1 = composite) [8..15]
+    int32_t ovr_cap;
+    unsigned long long* sticky; // [1] overflow seen by any render since the caller last cleared it (not
+                                // part of the per-render zeroed prefix: lsb_render_sticky reads / clears it)
     double* pose_part;          // [CHAIN_BLOCKS * POSE_VALS]
     double* loss_part;          // [ntiles * 2] fused-loss tile partials
     int32_t* vis_ebase;         // [n + 1] first intersection of each visible slot (exclusive scan)
@@ -93,6 +159,9 @@ inline size_t carve(const lsb_dims& d, char* base, Ws* w) {
     };
     const size_t n = (size_t)(d.n > 0 ? d.n : 1);
     const size_t cap = (size_t)(d.isect_cap > 0 ? d.isect_cap : 1);
+    // first, at a fixed offset whatever the dims (a row band renders through
+    // the same workspace with fewer tiles): the sticky overflow flag
+    t.sticky = (unsigned long long*)take(sizeof(unsigned long long));
     // zeroed prefix: counters, tile histogram, tile cursors
     t.ctr = (unsigned long long*)take(16 * sizeof(unsigned long long));
     t.tile_count = (int32_t*)take(sizeof(int32_t) * t.ntiles);
@@ -110,6 +179,9 @@ inline size_t carve(const lsb_dims& d, char* base, Ws* w) {
     t.tile_slot = (int32_t*)take(sizeof(int32_t) * cap);
     t.sort_scratch = (int32_t*)take(sizeof(int32_t) * cap * 8);
     t.part = (float*)take(sizeof(float) * NUM_PART * cap);
+    t.ovr_cap = (int32_t)(cap / 16 + 1024);
+    t.ovr_of = (int32_t*)take(sizeof(int32_t) * cap);
+    t.ovr = (uint32_t*)take(sizeof(uint32_t) * 16 * (size_t)t.ovr_cap);
     t.pose_part = (double*)take(sizeof(double) * CHAIN_BLOCKS * POSE_VALS);
     t.loss_part = (double*)take(sizeof(double) * 2 * t.ntiles);
     t.vis_ebase = (int32_t*)take(sizeof(int32_t) * (n + 1));
@@ -139,6 +211,43 @@ __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+
+// ---- the blend's f32 alpha (shared with the binning's band search) ---------
+constexpr int RUN_PX = 4;    // pixels per lane and row in the blend walks (blend.cu RUN)
+// Per-record frame of one lane: the splat mean relative to the lane's first
+// pixel (gx0, gy0) and the opacity folded into the exponent.
+struct Frame {
+    float mxr, myr, lop;
+};
+
+__device__ __forceinline__ Frame frame_of(float4 q0, float lop, float gx0f, float gy0f) {
+    Frame f;
+    f.mxr = __fadd_rn(__fsub_rn(q0.x, gx0f), q0.z);
+    f.myr = __fadd_rn(__fsub_rn(q0.y, gy0f), q0.w);
+    f.lop = lop;
+    return f;
+}
+
+// Records with lop below this cannot saturate (a' < 1 for every pixel).
+constexpr float SAT_LOP = -1e-6f;
+
+// Row terms: u0 = x_local + s dy - mx at the run's first pixel, and the
+// row part of the exponent E dy^2 + log2(op / clamp).
+__device__ __forceinline__ void row_terms(const Frame& f, float s, float E, float rowoff, float& dy, float& u0,
+                                          float& edy) {
+    dy = __fsub_rn(rowoff, f.myr);
+    u0 = __fmaf_rn(s, dy, -f.mxr);
+    edy = __fmaf_rn(__fmul_rn(E, dy), dy, f.lop);
+}
+
+// Saturated alpha of pixel j of the run: a = min(1, op g / clamp).  With
+// SAT false the record cannot saturate and the min is dropped.
+template <bool SAT = true>
+__device__ __forceinline__ float alpha_sat(float A, float u0, float edy, int j, float& u) {
+    u = j == 0 ? u0 : __fadd_rn(u0, (float)j);
+    const float e = ex2_approx(__fmaf_rn(A, __fmul_rn(u, u), edy));
+    return SAT ? __saturatef(e) : e;
 }
 
 __device__ __forceinline__ float rcp_approx(float x) {

@@ -174,6 +174,8 @@ __global__ void __launch_bounds__(256) k_pose_prepare(Ws w, PosePrepArgs a) {
 struct RowArgs {
     int W, H;
     float clamp, cut, iclamp;
+    float cutlo, cuthi;      // cut (1 -+ CUT_BAND): inside, the f64 decision (exact_alpha)
+    double clamp_d, cut_d;
     int degree;
     double A[36];
     double Rcw[9];
@@ -228,7 +230,7 @@ __global__ void __launch_bounds__(128) k_pose_rows(Ws w, RowArgs a, const float*
         int slot = 0;
         Rec rc;
         if (j < end) {
-            slot = w.tile_slot[j];
+            slot = w.tile_slot[j] & SLOT_MASK;
             rc = w.rec[slot];
             const int x0 = rc.bbx & 0xffff, x1 = rc.bbx >> 16, y0 = rc.bby & 0xffff, y1 = rc.bby >> 16;
             inside = px >= x0 && px < x1 && py >= y0 && py < y1;
@@ -249,6 +251,8 @@ __global__ void __launch_bounds__(128) k_pose_rows(Ws w, RowArgs a, const float*
             rc.kc1 *= a.iclamp;
             rc.kc2 *= a.iclamp;
             contrib = (al >= a.cut) && al != 0.f;
+            if (a.cut_d > 0.0 && al >= a.cutlo && al < a.cuthi)       // the forward's f64 decision
+                contrib = !(exact_alpha(w.cgeo[slot], a.clamp_d, (double)px, (double)py) < a.cut_d);
         }
         float tot;
         const float Tk = Tc * warp_scan_mul_excl(contrib ? 1.f - al : 1.f, lane, tot);
@@ -410,7 +414,9 @@ cudaError_t launch_pose_rows(const Ws& w, const lsb_settings& s, int degree, int
                              const int32_t* n_contrib, const float* chain, const int32_t* ids, int64_t m,
                              const int64_t* m_dev, const double* A, const double* Rcw, double* rows, cudaStream_t st) {
     RowArgs a;
-    a.W = W; a.H = H; a.clamp = (float)s.alpha_clamp; a.cut = (float)s.alpha_cut; a.degree = degree;
+    a.W = W; a.H = H; a.clamp = (float)s.alpha_clamp; a.cut = (float)s.alpha_cut;
+    a.cutlo = (float)(s.alpha_cut * (1.0 - CUT_BAND)); a.cuthi = (float)(s.alpha_cut * (1.0 + CUT_BAND));
+    a.clamp_d = s.alpha_clamp; a.cut_d = s.alpha_cut; a.degree = degree;
     a.iclamp = (float)(1.0 / s.alpha_clamp);
     for (int k = 0; k < 36; ++k) a.A[k] = A[k];
     for (int k = 0; k < 9; ++k) a.Rcw[k] = Rcw[k];

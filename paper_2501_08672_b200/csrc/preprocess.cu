@@ -19,6 +19,8 @@ struct PreArgs {
     lsb_settings s;
     int degree;
     int cull;          // bin_mode 1 with alpha_cut > 0: contributing tile lists
+    int want_geo;      // fill the f64 screen geometry even when alpha_cut == 0 (lsb_splat)
+    double* col_out;   // optional: the f64 clipped colour per Gaussian (lsb_splat)
 };
 
 // ---- contributing-list binning (bin_mode 1) ---------------------------------
@@ -204,8 +206,8 @@ __device__ bool splat_one(const PreArgs& a, int64_t i, Rec& r, int& ntiles, uint
     const double y1 = fmin(floor(muy + radius) + 1.0, H_);
     if (!(x0 < x1 && y0 < y1 && radius <= a.s.max_footprint_px)) return false;
     const int ix0 = (int)x0, ix1 = (int)x1, iy0 = (int)y0, iy1 = (int)y1;
+    if (a.s.alpha_cut > 0.0 || a.want_geo) geo = make_cull_geo(mux, muy, ca, cb, cc, cull_thr(op, a.s.alpha_cut), op, a.s.alpha_cut);
     if (a.cull) {
-        geo = CullGeo{mux, muy, ca, cb, cc, cull_thr(op, a.s.alpha_cut)};
         ntiles = cull_tile_count(geo, ix0, ix1, iy0, iy1);
     } else {
         ntiles = (((ix1 - 1) >> 4) - (ix0 >> 4) + 1) * (((iy1 - 1) >> 4) - (iy0 >> 4) + 1);
@@ -248,6 +250,7 @@ __device__ bool splat_one(const PreArgs& a, int64_t i, Rec& r, int& ntiles, uint
             if (k < kk) acc += b[k] * pld(a.p.shs, sho + 3 * k + c, f64);
         const double raw = 0.5 + acc;
         col[c] = (float)fmin(fmax(raw, 0.0), 1.0);
+        if (a.col_out) a.col_out[3 * i + c] = fmin(fmax(raw, 0.0), 1.0);
         if (raw > 0.0 && raw < 1.0) cmask |= 1u << c;
     }
     const float kap = (float)a.s.alpha_clamp;
@@ -275,13 +278,13 @@ __device__ __forceinline__ void emit_splat(const PreArgs& a, const Ws& w, Rec& r
     w.vis_ebase[slot] = (int32_t)min(e0, (int64_t)0x7fffffff);
     w.vkey[slot] = key;
     w.colmask[slot] = cm;
+    if (a.s.alpha_cut > 0.0) w.cgeo[slot] = geo;     // the blend's f64 alpha_cut decisions (exact_alpha)
     if (!fits) return;
     const int x0 = r.bbx & 0xffff, x1 = r.bbx >> 16, y0 = r.bby & 0xffff, y1 = r.bby >> 16;
     // tile histogram, and each intersection's (slot, tile) for the scatter,
     // e running row-major over the splat's tiles from e0
     int e = (int)e0;
     if (a.cull) {
-        w.cgeo[slot] = geo;
         for (int ty = y0 >> 4; ty <= (y1 - 1) >> 4; ++ty) {
             int tx0, tx1;
             if (!cull_tile_row(geo, ty, x0, x1, y0, y1, tx0, tx1)) continue;
@@ -398,23 +401,141 @@ __global__ void __launch_bounds__(ST_THREADS) k_scan_tiles(Ws w) {
     }
 }
 
+// sqrt(x) for x >= 0 from the MUFU reciprocal square root (the band search
+// widens its annulus far beyond this rounding).
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return x > 0.f ? x * r : 0.f;
+}
+
+// The alpha_cut band of one (splat, tile) entry.  The blend decides `alpha <
+// alpha_cut` (_kernels.py:104) in f32; where its f32 alpha may lie too close
+// to the cut for that to be the reference's f64 decision, the entry carries
+// OVR_BIT and a row of 256-bit masks (the band pixels of the tile and their
+// decisions taken here in f64 with exact_alpha), which the blend follows.
+// The search: the pixel centres of the tile (inside the splat's bbox) in the
+// annulus |q - qc| <= W around q = qc = 2 ln(op / cut), row by row from the
+// roots of the row's quadratic q = c0 (dx + s dy)^2 + k dy^2 (f32, tile-
+// relative centre from f64).  W covers 2 CUT_BAND plus this search's own f32
+// error, so every pixel whose alpha / cut lies within 1 +- CUT_BAND is found;
+// the blend's f32 alpha is at least 5x more accurate than CUT_BAND.  For each
+// band pixel the f32 alpha the blend computes (same instruction sequence and
+// lane frame) is also formed and the largest relative error against the f64
+// one is kept in ctr[14] (the evidence for the band width).  Nearly every
+// entry has no band pixel and costs a few instructions per tile row.
+// One band pixel (tile-relative x, ry) of an entry: allocate the entry's
+// mask row at its first band pixel (idx < 0), take the f64 decision, record
+// it, and keep the f32-error evidence.  Returns the row, or -1 when the mask
+// table is full (reported as a capacity overflow: regrow and redo).
+__device__ __forceinline__ int band_pixel(const Ws& w, const CullGeo& g, const Rec& r, double clamp, double cut, int idx,
+                                       int ox, int oy, int x, int ry) {
+    if (idx < 0) {
+        idx = (int)atomicAdd(&w.ctr[9], 1ull);
+        if (idx >= w.ovr_cap) {
+            w.ctr[2] = 1;
+            *w.sticky = 1ull;
+            return -1;
+        }
+        for (int q = 0; q < 16; ++q) w.ovr[(size_t)idx * 16 + q] = 0u;
+    }
+    const double ad = exact_alpha(g, clamp, (double)(ox + x), (double)(oy + ry));
+    const bool take = !(ad < cut);
+    const int bit = ry * TILE + x;
+    uint32_t* m = w.ovr + (size_t)idx * 16;
+    m[bit >> 5] |= 1u << (bit & 31);
+    if (take) m[8 + (bit >> 5)] |= 1u << (bit & 31);
+    atomicAdd(&w.ctr[12], 1ull);
+    if (take) atomicAdd(&w.ctr[13], 1ull);
+    // the blend's own f32 alpha for this pixel (its lane's frame)
+    const Frame f = frame_of(*(const float4*)&r.mxh, r.lop, (float)(ox + (x & ~(RUN_PX - 1))), (float)(oy + (ry & 7)));
+    float dyf, u0, edy, u;
+    row_terms(f, r.s, r.E, 8.f * (float)(ry >> 3), dyf, u0, edy);
+    const float al = alpha_sat(r.A, u0, edy, x & (RUN_PX - 1), u);
+    atomicMax((unsigned int*)&w.ctr[14], __float_as_uint((float)fabs((double)al * clamp / ad - 1.0)));
+    return idx;
+}
+
+__device__ __forceinline__ bool band_search(const Ws& w, double clamp, double cut, int64_t e, int slot, int tile) {
+    const CullGeo& g = w.cgeo[slot];
+    const float qc = g.qcf;
+    const float W = (float)(4.0 * CUT_BAND) + 4e-6f * fabsf(qc) + 1e-6f;
+    const float qo = qc + W, qi = qc - W;
+    if (qo < 0.f) return false;              // op below the band: no pair comes near the cut
+    const int ox = (tile % w.ntx) * TILE, oy = (tile / w.ntx) * TILE;
+    const Rec& r = w.rec[slot];
+    const int x0 = r.bbx & 0xffff, x1 = r.bbx >> 16, y0 = r.bby & 0xffff, y1 = r.bby >> 16;
+    const float mxr = (float)(g.mux - (double)ox), myr = (float)(g.muy - (double)oy);
+    const float k = g.kf, sr = g.sf, ic0 = g.ic0f;
+    const int cx0 = max(ox, x0) - ox, cx1 = min(ox + TILE, x1) - 1 - ox;     // tile-relative columns
+    const float dyx = sqrt_approx(qo / k) + 1e-3f;
+    const int ry0 = max(max(0, y0 - oy), __float2int_ru(myr - dyx));
+    const int ry1 = min(min(TILE, y1 - oy), __float2int_rd(myr + dyx) + 1);
+    if (ry0 >= ry1 || cx0 > cx1) return false;
+    // an entry whose pixel rectangle lies inside the inner ellipse has no band
+    // pixel: q is convex, so its maximum over the rectangle is at a corner
+    {
+        const float c0 = (float)g.c0;
+        const float da = (float)ry0 - myr, db = (float)(ry1 - 1) - myr;
+        const float ua = __fmaf_rn(sr, da, (float)cx0 - mxr), ub = __fmaf_rn(sr, db, (float)cx0 - mxr);
+        const float w = (float)(cx1 - cx0);
+        const float va = k * da * da, vb = k * db * db;
+        const float qmax = fmaxf(fmaxf(__fmaf_rn(c0 * ua, ua, va), __fmaf_rn(c0 * (ua + w), ua + w, va)),
+                                 fmaxf(__fmaf_rn(c0 * ub, ub, vb), __fmaf_rn(c0 * (ub + w), ub + w, vb)));
+        if (qmax < qi * 0.999f) return false;
+    }
+    int idx = -1;
+    for (int ry = ry0; ry < ry1; ++ry) {
+        const float dy = (float)ry - myr;
+        const float v = k * dy * dy;
+        const float to = qo - v;
+        if (to < 0.f) continue;
+        const float xm = __fmaf_rn(-sr, dy, mxr);        // the row's centre
+        const float ho = sqrt_approx(to * ic0);
+        const int xa = max(cx0, __float2int_ru(xm - ho));
+        const int xb = min(cx1, __float2int_rd(xm + ho));
+        if (xa > xb) continue;
+        const float ti = qi - v;
+        const float hi = ti > 0.f ? sqrt_approx(ti * ic0) : -1.f;
+        // candidates |x - xm| >= hi: the left run up to xm - hi, the right run from xm + hi
+        const int xl = hi < 0.f ? xb : __float2int_rd(xm - hi);
+        const int xr = hi < 0.f ? xb + 1 : __float2int_ru(xm + hi);
+        if (xl < xa && xr > xb) continue;                 // the segment lies inside the inner ellipse
+        for (int x = xa; x <= xb; ++x) {
+            if (x > xl && x < xr) x = xr;                 // jump over the inner run
+            if (x > xb) break;
+            idx = band_pixel(w, g, r, clamp, cut, idx, ox, oy, x, ry);
+            if (idx < 0) return false;                    // (no room: a capacity overflow was reported)
+        }
+    }
+    if (idx < 0) return false;
+    w.ovr_of[e] = idx;
+    return true;
+}
+
 // Scatter with the (slot, tile) pairs the preprocess emitted: one thread per
-// intersection claims a position in its tile's bucket.
-__global__ void __launch_bounds__(256) k_scatter_emitted(Ws w) {
+// intersection claims a position in its tile's bucket (and, with alpha_cut
+// > 0, searches its entry for alpha_cut band pixels: band_search).
+__global__ void __launch_bounds__(256) k_scatter_emitted(Ws w, double clamp, double cut) {
     if (w.ctr[1] > (unsigned long long)w.cap) return;     // overflow: tiles published empty
     const int64_t I = (int64_t)w.ctr[1];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < I; e += stride) {
         const int t = w.emit_tile[e];
+        const int slot = w.emit_slot[e];
         const int j = w.tile_start[t] + atomicAdd(&w.tile_cursor[t], 1);
+        const bool band = cut > 0.0 && band_search(w, clamp, cut, e, slot, t);
         w.tile_e[j] = (int32_t)e;
-        w.tile_slot[j] = w.emit_slot[e];
+        w.tile_slot[j] = slot | (band ? OVR_BIT : 0);      // the flag rides on the slot (sorts mask it)
     }
 }
 
 constexpr int SORT_CAP = 4096;   // entries sorted entirely in shared memory
 
+// (slots may carry OVR_BIT: compared and indexed without it)
 __device__ __forceinline__ bool key_less(uint64_t ka, int sa, uint64_t kb, int sb) {
+    sa &= SLOT_MASK;
+    sb &= SLOT_MASK;
     return ka < kb || (ka == kb && sa < sb);
 }
 
@@ -501,7 +622,7 @@ __device__ void warp_sort_tile(const Ws& w, int start, int n, int lane) {
         if (i < n) {
             e[r] = w.tile_e[start + i];
             s[r] = w.tile_slot[start + i];
-            k[r] = w.vkey[s[r]];
+            k[r] = w.vkey[s[r] & SLOT_MASK];
         } else {
             k[r] = ~0ull;
             s[r] = 0x7fffffff;
@@ -565,7 +686,7 @@ __global__ void __launch_bounds__(256) k_tile_sort_big(Ws w) {
             for (int i = threadIdx.x; i < n; i += blockDim.x) {
                 const int e = w.tile_e[start + i];
                 const int slot = w.tile_slot[start + i];
-                sk[i] = w.vkey[slot];
+                sk[i] = w.vkey[slot & SLOT_MASK];
                 ss[i] = slot;
                 se[i] = e;
             }
@@ -585,7 +706,7 @@ __global__ void __launch_bounds__(256) k_tile_sort_big(Ws w) {
             for (int i = threadIdx.x; i < cn; i += blockDim.x) {
                 const int e = w.tile_e[start + c0 + i];
                 const int slot = w.tile_slot[start + c0 + i];
-                sk[i] = w.vkey[slot];
+                sk[i] = w.vkey[slot & SLOT_MASK];
                 ss[i] = slot;
                 se[i] = e;
             }
@@ -744,7 +865,10 @@ __global__ void __launch_bounds__(PS_THREADS) k_pre_scan(Ws w, int64_t nw) {
         w.ctr[0] = (unsigned long long)tv;
         w.ctr[1] = (unsigned long long)tt;
         w.vis_ebase[tv] = (int32_t)min(tt, 0x7fffffffll);
-        if (tt > w.cap) w.ctr[2] = 1;
+        if (tt > w.cap) {
+            w.ctr[2] = 1;
+            *w.sticky = 1ull;          // sticky across renders until the caller clears it
+        }
     }
 }
 
@@ -777,7 +901,7 @@ __global__ void __launch_bounds__(PRE_THREADS, PRE_MIN_BLOCKS) k_pre_emit(PreArg
 
 cudaError_t launch_preprocess(const lsb_params& p, const lsb_camera& cam, const lsb_pose& T,
                               const lsb_settings& s, const Ws& w, cudaStream_t st) {
-    PreArgs a{p, cam, T, s, 0, (s.bin_mode == 1 && s.alpha_cut > 0.0) ? 1 : 0};
+    PreArgs a{p, cam, T, s, 0, (s.bin_mode == 1 && s.alpha_cut > 0.0) ? 1 : 0, 0, nullptr};
     int deg_store = 0;
     while ((deg_store + 2) * (deg_store + 2) <= p.sh_coeffs) ++deg_store;
     a.degree = s.sh_degree < deg_store ? s.sh_degree : deg_store;
@@ -794,10 +918,46 @@ cudaError_t launch_preprocess(const lsb_params& p, const lsb_camera& cam, const 
     const int st_smem = (int)sizeof(int) * (w.ntiles + w.ntiles / 32 + 1);
     if (st_smem > 48 * 1024) cudaFuncSetAttribute(k_scan_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, st_smem);
     k_scan_tiles<<<1, ST_THREADS, st_smem, st>>>(w);
-    k_scatter_emitted<<<8 * 148, 256, 0, st>>>(w);
+    k_scatter_emitted<<<8 * 148, 256, 0, st>>>(w, s.alpha_clamp, s.alpha_cut);
     k_tile_sort<<<(w.ntiles + 3) / 4, 128, 0, st>>>(w);
     cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_sort_smem());
     k_tile_sort_big<<<148, 256, tile_sort_smem(), st>>>(w);
+    return cudaGetLastError();
+}
+
+// raster.splat (raster.py:188-205) for a batch: the same projection,
+// covariance, footprint cull and SH colour as the preprocess, per Gaussian
+// i: geo[7 i ..] = visible, mu_i (2), cov_i (00, 01, 11), camera depth and
+// color[3 i ..] = the clipped SH colour (visible Gaussians), all f64.
+__global__ void k_splat_out(PreArgs a, double* __restrict__ out) {
+    const int64_t n = a.p.n;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        Rec r;
+        int nt = 0;
+        uint64_t key = 0;
+        uint32_t cm = 0;
+        CullGeo g{};
+        const bool vis = splat_one<true>(a, i, r, nt, key, cm, g);
+        double* o = out + 7 * i;
+        o[0] = vis ? 1.0 : 0.0;
+        o[1] = g.mux;
+        o[2] = g.muy;
+        o[3] = g.ca;
+        o[4] = g.cb;
+        o[5] = g.cc;
+        o[6] = vis ? __longlong_as_double((long long)key) : 0.0;
+    }
+}
+
+cudaError_t launch_splat(const lsb_params& p, const lsb_camera& cam, const lsb_pose& T, const lsb_settings& s,
+                         double* geo, double* color, cudaStream_t st) {
+    PreArgs a{p, cam, T, s, 0, 0, 1, color};
+    int deg_store = 0;
+    while ((deg_store + 2) * (deg_store + 2) <= p.sh_coeffs) ++deg_store;
+    a.degree = s.sh_degree < deg_store ? s.sh_degree : deg_store;
+    if (p.n <= 0) return cudaSuccess;
+    const unsigned nb = (unsigned)((p.n + 127) / 128);
+    k_splat_out<<<nb < 1184 ? nb : 1184, 128, 0, st>>>(a, geo);
     return cudaGetLastError();
 }
 

@@ -146,12 +146,15 @@ __global__ void k_fov_leaves(lsb_voxmap m, const unsigned long long* __restrict_
                              int64_t* __restrict__ out, unsigned long long* __restrict__ n_out, int64_t out_cap) {
     const int L = m.max_level;
     const unsigned lane = threadIdx.x & 31;
-    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < m.cap; s += (int64_t)gridDim.x * blockDim.x) {
+    // warp-uniform trip count (every block's threads share `base`), so the
+    // ballots below see the whole warp converged
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < m.cap; base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = base + threadIdx.x;
         // gslot first: 4 bytes per slot streamed, the key only for the leaves
         // that hold a Gaussian (gslot >= 0 implies an occupied slot)
         bool hit = false;
         long long ix = 0, iy = 0, iz = 0;
-        const unsigned long long key = m.gslot[s] >= 0 ? (unsigned long long)m.keys[s] : EMPTY;
+        const unsigned long long key = (s < m.cap && m.gslot[s] >= 0) ? (unsigned long long)m.keys[s] : EMPTY;
         if (key != EMPTY) {
             unpack_key(key, ix, iy, iz);
             const long long rx = ix >> L, ry = iy >> L, rz = iz >> L;   // floor division by 2^L
@@ -166,15 +169,15 @@ __global__ void k_fov_leaves(lsb_voxmap m, const unsigned long long* __restrict_
             }
         }
         // warp-aggregated output slot: one atomic per warp instead of per leaf
-        const unsigned act = __activemask();
-        const unsigned hits = __ballot_sync(act, hit);
+        __syncwarp();
+        const unsigned hits = __ballot_sync(0xffffffffu, hit);
         if (!hits) continue;
         const int leader = __ffs(hits) - 1;
-        unsigned long long base = 0;
-        if ((int)lane == leader) base = atomicAdd(n_out, (unsigned long long)__popc(hits));
-        base = __shfl_sync(act, base, leader);
+        unsigned long long ob = 0;
+        if ((int)lane == leader) ob = atomicAdd(n_out, (unsigned long long)__popc(hits));
+        ob = __shfl_sync(0xffffffffu, ob, leader);
         if (!hit) continue;
-        const unsigned long long o = base + __popc(hits & ((1u << lane) - 1u));
+        const unsigned long long o = ob + __popc(hits & ((1u << lane) - 1u));
         if ((int64_t)o < out_cap) {
             out[3 * o] = ix;
             out[3 * o + 1] = iy;

@@ -109,11 +109,30 @@ class ViewShardedWindow:
         """This rank's unit images from the full frames (indexed by view)."""
         return [frames[v][y0:y1].contiguous() for v, y0, y1 in self.units]
 
-    def step(self, observed_mine: Sequence[torch.Tensor], timers: Optional[dict] = None) -> None:
-        """observed_mine: one image per unit (observed_for)."""
+    def step(self, observed_mine: Sequence[torch.Tensor], timers: Optional[dict] = None, check: bool = False) -> None:
+        """observed_mine: one image per unit (observed_for).  check=True
+        syncs after the step and raises CapacityExceeded on every rank if
+        any rank's render overflowed (else see check_capacity / finish)."""
         self.engine.step(observed_mine, allreduce=self.allreduce, timers=timers)
+        if check:
+            self.require_capacity()
+
+    def check_capacity(self) -> bool:
+        """True if no render on ANY rank overflowed since the last check
+        (syncs; one MAX all-reduce of the ranks' sticky flags)."""
+        over = torch.tensor([0 if self.engine.check_capacity(clear=False) else 1],
+                            dtype=torch.int32, device=self.engine.grads.flat.device)
+        if self.allreduce is not None:
+            dist.all_reduce(over, op=dist.ReduceOp.MAX)
+        return not bool(over.item())
+
+    def require_capacity(self) -> None:
+        from .errors import CapacityExceeded
+        if not self.check_capacity():
+            raise CapacityExceeded("a rank's render overflowed its intersection capacity: regrow and redo the step")
 
     def finish(self) -> None:
+        self.require_capacity()
         self.engine.finish()
 
 

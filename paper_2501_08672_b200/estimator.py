@@ -314,16 +314,76 @@ def _visual_pass(window, observed, cam, cfg: FilterConfig, settings: RasterSetti
     camera / configuration (its device buffers and pinned read-back buffer
     are allocated once); the observed frame is refreshed every update."""
     arrays = _as_arrays(window)
-    key = (id(arrays), len(arrays), int(arrays.shs.shape[1]), int(cam.width), int(cam.height), float(cam.fx),
-           float(cam.fy), float(cam.cx), float(cam.cy), repr(cfg), repr(settings))
+    # keyed on the parameter storage, not the wrapper object: a window's
+    # as_gaussian_arrays() returns a new wrapper of the same tensors per call
+    key = (arrays.means.data_ptr(), arrays.shs.data_ptr(), len(arrays), int(arrays.shs.shape[1]), int(cam.width),
+           int(cam.height), float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy), repr(cfg), repr(settings))
     vis = _VIS_CACHE.get(key)
-    if vis is None or vis.arrays is not arrays:
+    if vis is None:
         if len(_VIS_CACHE) > 4:
             _VIS_CACHE.clear()
         vis = _VIS_CACHE[key] = _VisualPass(arrays, observed, cam, cfg, settings)
     else:
+        vis.arrays = arrays
         vis.set_observed(observed)
     return vis
+
+
+def _meas_len(meas) -> int:
+    try:
+        return len(meas)
+    except TypeError:                     # a reference Measurement (numpy z)
+        return int(np.asarray(meas.z).size)
+
+
+def _pose_hb(meas):
+    """(A6, b6) = the pose block of H^T R^-1 H and H^T R^-1 z of a
+    measurement: reduced on the device when the measurement is this
+    package's (Measurement.hb), else from its numpy H / z / R_diag."""
+    if hasattr(meas, "hb"):
+        return meas.hb()
+    H = np.asarray(meas.H, dtype=float)
+    if H.shape[1] > 6 and np.any(H[:, 6:] != 0.0):
+        raise ValueError("ieskf_update: measurement rows beyond the pose block are not supported")
+    HtRi = H[:, :6].T / np.asarray(meas.R_diag, dtype=float)[None, :]
+    return HtRi @ H[:, :6], HtRi @ np.asarray(meas.z, dtype=float)
+
+
+def ieskf_update(state: NavState, cov: np.ndarray, meas_fn, max_iter: int = 5, step_tol: float = 1e-6,
+                 bias_limit: float = 0.5):
+    """Iterated EKF update re-linearising meas_fn(state) -> Measurement about
+    the running estimate (estimator.py:292-331), the reference's generic
+    signature.  meas_fn may raise NoAssociations / TooFewPixels (callers
+    skip the update) and SingularGain comes from a singular gain; an empty
+    measurement keeps the prior.  The pose block of H^T R^-1 H / H^T R^-1 z
+    comes from the measurement (reduced on the device for this package's
+    measurements) and the 15x15 gain algebra runs in one host call per
+    iteration (lsb_ieskf_iterate; K z = S^-1 b, K H = S^-1 A)."""
+    lib = _lib.load()
+    cov_c = np.ascontiguousarray(cov, dtype=np.float64)
+    ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    x_bar = _pack(state)
+    x_hat = x_bar.copy()
+    K_H = P = None
+    xi, KH_buf, P_buf = np.empty(DIM), np.empty((DIM, DIM)), np.empty((DIM, DIM))
+    for _ in range(max_iter):
+        meas = meas_fn(_unpack(x_hat))
+        if meas is None or _meas_len(meas) == 0:
+            if K_H is None:
+                return state.clone(), cov.copy()
+            break
+        A6, b6 = _pose_hb(meas)
+        if lib.lsb_ieskf_iterate(ptr(cov_c), ptr(x_bar), ptr(x_hat), ptr(np.ascontiguousarray(A6, dtype=np.float64)),
+                                 ptr(np.ascontiguousarray(b6, dtype=np.float64)), float(bias_limit), ptr(xi),
+                                 ptr(KH_buf), ptr(P_buf)):
+            raise SingularGain(lib.lsb_last_error().decode())
+        K_H, P = KH_buf.copy(), P_buf.copy()
+        if float(np.sqrt(xi @ xi)) < step_tol:
+            break
+    if K_H is None:
+        return state.clone(), cov.copy()
+    cov_post = (np.eye(DIM) - K_H) @ P
+    return _unpack(x_hat), 0.5 * (cov_post + cov_post.T)
 
 
 def ieskf_visual_update(state: NavState, cov: np.ndarray, observed, window, cam, T_ic, cfg: FilterConfig,

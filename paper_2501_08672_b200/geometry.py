@@ -141,3 +141,43 @@ def so3_right_jacobian_inv(phi) -> np.ndarray:
         return np.eye(3) - 0.5 * S + (S @ S) / 12.0
     b = (1.0 / theta**2) - 0.5 / (theta * np.tan(0.5 * theta))
     return np.eye(3) - 0.5 * S + b * (S @ S)
+
+
+@dataclass
+class Gaussian3D:
+    """Planar-slice Gaussian primitive (geometry.py:271-309): the same fields
+    and defaults as the reference's, so reference-built Gaussians and these
+    are interchangeable at the boundary."""
+
+    mean_w: np.ndarray
+    rot: np.ndarray
+    scale: np.ndarray
+    opacity: float
+    sh: np.ndarray
+    level: int = 0
+
+    def __post_init__(self):
+        self.mean_w = np.asarray(self.mean_w, dtype=float).reshape(3)
+        self.rot = np.asarray(self.rot, dtype=float).reshape(3, 3)
+        self.scale = np.asarray(self.scale, dtype=float).reshape(3)
+        self.sh = np.asarray(self.sh, dtype=float).reshape(-1, 3)
+
+    def covariance(self) -> np.ndarray:
+        B = self.rot * self.scale[None, :]
+        return B @ B.T
+
+
+@dataclass
+class Gaussian2D:
+    """Screen-space footprint of a splatted Gaussian (geometry.py:311-323)."""
+
+    mean_i: np.ndarray
+    cov_i: np.ndarray
+    depth: float
+    color: np.ndarray
+    opacity: float
+
+    def __post_init__(self):
+        self.mean_i = np.asarray(self.mean_i, dtype=float).reshape(2)
+        self.cov_i = np.asarray(self.cov_i, dtype=float).reshape(2, 2)
+        self.color = np.asarray(self.color, dtype=float).reshape(3)

@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import EmptyMask
+from .errors import CapacityExceeded, EmptyMask
 from .geometry import as_se3
 from .raster import (GaussianArrays, ParamGradients, RasterSettings, RenderState, _as_arrays, _f32, _obs_kind,
                      _observed, crop_rows, render_bin, render_blend, render_blend_bwd, render_blend_bwd_loss, render_blend_fused_loss,
@@ -123,13 +123,29 @@ def adam_cfg(cfg: OptimConfig, step: int) -> _lib.AdamCfg:
                         cfg.eps, cfg.scene_scale, cfg.opacity_clip, cfg.scale_floor, int(step))
 
 
-IBC_ROWS = 1 << 16     # beyond 2^16 steps both bias corrections are exactly 1.0 in f64
+IBC_ROWS = 1 << 16     # table rows at least (enough for beta2 <= 0.9994)
 
 
-def bias_correction_table(beta1: float, beta2: float, rows: int = IBC_ROWS) -> np.ndarray:
-    """(rows, 2) of 1/(1-beta1^t), 1/(1-beta2^t) for t = 1..rows, with the
-    C library pow the reference's `beta ** t` uses (optimize.py:116-117)."""
+def bias_correction_rows(beta1: float, beta2: float) -> int:
+    """Rows after which both corrections are exactly 1.0 in f64: beta^t <
+    2^-54 makes 1 - beta^t round to 1.0 (the device clamps to the last row)."""
     import math
+    need = 1
+    for b in (beta1, beta2):
+        if 0.0 < b < 1.0:
+            need = max(need, int(math.ceil(-54.0 * math.log(2.0) / math.log(b))) + 2)
+    if need > (1 << 24):
+        raise ValueError(f"Adam betas {beta1}, {beta2} too close to 1 for the bias-correction table")
+    return max(IBC_ROWS, need)
+
+
+def bias_correction_table(beta1: float, beta2: float, rows: int = None) -> np.ndarray:
+    """(rows, 2) of 1/(1-beta1^t), 1/(1-beta2^t) for t = 1..rows, with the
+    C library pow the reference's `beta ** t` uses (optimize.py:116-117).
+    Sized (bias_correction_rows) so that the device's clamp to the last row
+    is exact for every later step."""
+    import math
+    rows = bias_correction_rows(beta1, beta2) if rows is None else rows
     return np.array([(1.0 / (1.0 - math.pow(beta1, t)), 1.0 / (1.0 - math.pow(beta2, t)))
                      for t in range(1, rows + 1)], dtype=np.float64)
 
@@ -280,9 +296,36 @@ class WindowEngine:
         self.max_isect = worst
         return int(worst * headroom) + 1024
 
-    def check_capacity(self) -> bool:
-        """True if the last render in every lane's workspace fit (syncs)."""
-        return all(not ln.state.read_counts(ln.stream)[2] for ln in self.lanes)
+    def check_capacity(self, clear: bool = True) -> bool:
+        """True if EVERY render since the last check fit its intersection
+        capacity (syncs).  A render that overflows publishes empty tiles, so
+        its view would contribute a zero gradient: each lane's workspace keeps
+        a sticky overflow flag (set by the preprocess of any view on that
+        lane, cleared only here), so an overflow in an earlier view or an
+        earlier step is never masked by a later render that fit."""
+        over = [ln.state.sticky(read=True, stream=ln.stream) for ln in self.lanes]
+        if clear and any(over):
+            for ln in self.lanes:
+                ln.state.sticky(clear=True, stream=ln.stream)
+        return not any(over)
+
+    def require_capacity(self) -> None:
+        """Raise CapacityExceeded if any render since the last check
+        overflowed (the flag stays set, so later checks raise too)."""
+        if not self.check_capacity(clear=False):
+            raise CapacityExceeded("intersection capacity exceeded in a window step: regrow() and redo the step")
+
+    def regrow(self, factor: float = 1.5) -> int:
+        """Re-measure the views' intersection counts and reallocate every
+        lane's workspace with `factor` headroom (drops a captured graph:
+        capture() again).  Returns the new capacity."""
+        cap = max(self.calibrate(headroom=factor), int(self.lanes[0].state.dims.isect_cap * factor))
+        T0 = self.views[0] if self.views else _identity()
+        for ln in self.lanes:
+            ln.state = RenderState(self.arrays, self.cam, T0.R, T0.t, self.settings, cap, self.bin_mode)
+        self.state = self.lanes[0].state
+        self.graph = None
+        return cap
 
     def _stage(self, observed, ready, capturing):
         """Queue the H2D copies of host `observed` images; returns one event per view."""
@@ -424,7 +467,9 @@ class WindowEngine:
 
     def finish(self) -> None:
         """End of the window optimisation: re-orthonormalise stepped rotations
-        and write the working copy back into the arena."""
+        and write the working copy back into the arena.  Raises
+        CapacityExceeded (and writes nothing back) if any step overflowed."""
+        self.require_capacity()
         self.adam.orthonormalize(self.arrays, self.stream)
         if self.arrays is not self.arena:
             with torch.cuda.stream(self.stream) if self.stream is not None else _nullctx():
@@ -432,7 +477,9 @@ class WindowEngine:
 
     def losses(self) -> np.ndarray:
         """Per-view loss values of the last step (syncs; one small D2H); for
-        banded units, each band's share of its view's loss."""
+        banded units, each band's share of its view's loss.  Raises
+        CapacityExceeded if a render since the last check overflowed."""
+        self.require_capacity()
         s = self.loss.sums()[: len(self.views)].cpu().numpy()
         return s[:, 0] / (3.0 * self.h * self.w)
 
@@ -473,10 +520,12 @@ def optimize_window(window, observed, T_wc, cam, cfg: OptimConfig = OptimConfig(
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
         start.record()
+        # the splats moved since the capacity was sized: bin first and regrow
+        # (before any Adam step) if this iteration's lists would not fit,
+        # as the reference never fails here (optimize.py:159-201)
+        _ensure_capacity(eng)
         if m is None:
             eng.step([obs])
-            if not eng.check_capacity():
-                raise RuntimeError("intersection capacity exceeded mid-optimisation")
         else:
             _masked_step(eng, obs, m, count)
         end.record()
@@ -489,6 +538,21 @@ def optimize_window(window, observed, T_wc, cam, cfg: OptimConfig = OptimConfig(
         window.mark_device_dirty_live()
     torch.cuda.synchronize()
     return history
+
+
+def _ensure_capacity(eng: WindowEngine) -> None:
+    """Bin the (single) view at the current parameters; regrow the engine
+    until its lists fit.  One sync per call."""
+    st = eng.state
+    T = eng.views[0]
+    while True:
+        st.set_pose(T.R, T.t)
+        render_bin(st, eng.stream)
+        if not st.read_counts(eng.stream)[2]:
+            break
+        eng.regrow()
+        st = eng.state
+    st.sticky(clear=True, stream=eng.stream)
 
 
 def _masked_step(eng: WindowEngine, obs, m, count):

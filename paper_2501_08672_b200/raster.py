@@ -248,6 +248,7 @@ class RenderState:
         nb = ctypes.c_size_t()
         _lib.check(_lib.load().lsb_workspace_bytes(ctypes.byref(self.dims), ctypes.byref(nb)), "workspace")
         self.ws = torch.empty(nb.value, dtype=torch.uint8, device=arrays.device)
+        self.sticky(clear=True)
         self.counts = None
         self._max_px = int(cam.width) * int(cam.height)
 
@@ -278,6 +279,26 @@ class RenderState:
                                                  c, _lib.stream_ptr(stream)), "counts")
         self.counts = tuple(int(v) for v in c)
         return self.counts
+
+    def sticky(self, clear: bool = False, read: bool = False, stream=None) -> Optional[bool]:
+        """The workspace's sticky overflow flag: set by any render since the
+        last clear (read: syncs `stream`; clear: stream-ordered reset)."""
+        out = ctypes.c_int64(0) if read else None
+        _lib.check(_lib.load().lsb_render_sticky(ctypes.c_void_p(self.ws.data_ptr()), ctypes.byref(self.dims),
+                                                 ctypes.byref(out) if read else None, 1 if clear else 0,
+                                                 _lib.stream_ptr(stream)), "sticky")
+        return bool(out.value) if read else None
+
+    def band_stats(self, stream=None):
+        """(tiles re-blended, band pairs decided in f64, of them composited,
+        max relative f32 alpha error over those pairs) of the last forward:
+        the alpha_cut decisions the f32 alpha cannot take the reference's way
+        by itself (_kernels.py:104), see csrc/blend.cu."""
+        c = (ctypes.c_int64 * 4)()
+        _lib.check(_lib.load().lsb_render_band_stats(ctypes.c_void_p(self.ws.data_ptr()), ctypes.byref(self.dims),
+                                                     c, _lib.stream_ptr(stream)), "band_stats")
+        err = float(np.frombuffer(np.uint32(c[3]).tobytes(), np.float32)[0])
+        return int(c[0]), int(c[1]), int(c[2]), err
 
     def export(self, what: int, stream=None) -> np.ndarray:
         """Parity hooks: 0 ids, 1 bboxes, 2 tile ranges, 3 tile entry ids, 4 depth."""
@@ -409,6 +430,47 @@ def render_bwd(state: RenderState, out: "RenderOutput", grad_image: torch.Tensor
         float(grad_scale), ctypes.byref(g),
         ctypes.c_void_p(pose_dev.data_ptr()) if pose_dev is not None else None,
         _lib.stream_ptr(stream)), "backward")
+
+
+class Culled:
+    """Normal outcome for a splat that cannot contribute to the image (raster.py:78-82)."""
+
+    def __repr__(self):
+        return "Culled()"
+
+
+def splat_batch(source, T_cw, cam, settings: RasterSettings = RasterSettings()):
+    """Per-Gaussian screen footprints of `source` on the device (lsb_splat):
+    (visible (n,) bool, mu_i (n,2), cov_i (n,2,2), depth (n,), color (n,3)),
+    device f64 tensors; the same projection, EWA covariance, footprint cull
+    and SH colour as render()'s preprocess (raster.py:134-185, 232-238)."""
+    _lib.require()
+    arrays = _as_arrays(source)
+    T_cw = as_se3(T_cw)
+    n = len(arrays)
+    dev = arrays.device
+    geo = torch.zeros((max(n, 1), 7), dtype=torch.float64, device=dev)
+    col = torch.zeros((max(n, 1), 3), dtype=torch.float64, device=dev)
+    if n:
+        p = arrays.params()
+        _lib.check(_lib.load().lsb_splat(ctypes.byref(p), ctypes.byref(_lib.make_camera(cam)),
+                                         ctypes.byref(_lib.make_pose(T_cw.R, T_cw.t)),
+                                         ctypes.byref(_lib.make_settings(settings, 0)),
+                                         ctypes.c_void_p(geo.data_ptr()), ctypes.c_void_p(col.data_ptr()),
+                                         _lib.stream_ptr()), "splat")
+    geo, col = geo[:n], col[:n]
+    cov = torch.stack([geo[:, 3], geo[:, 4], geo[:, 4], geo[:, 5]], dim=1).reshape(n, 2, 2)
+    return geo[:, 0] > 0.5, geo[:, 1:3], cov, geo[:, 6], col
+
+
+def splat(g, T_cw, cam, settings: RasterSettings = RasterSettings()):
+    """Project one Gaussian; returns a Gaussian2D or Culled (raster.py:188-205)."""
+    from .geometry import Gaussian2D
+    vis, mu, cov, depth, col = splat_batch(GaussianArrays.from_gaussians([g]), T_cw, cam, settings)
+    if not bool(vis[0]):
+        return Culled()
+    return Gaussian2D(mean_i=mu[0].cpu().numpy(), cov_i=cov[0].cpu().numpy(), depth=float(depth[0]),
+                      color=col[0].cpu().numpy(), opacity=float(g.opacity))
 
 
 def render(source, T_wc, cam, settings: RasterSettings = RasterSettings(), retain_cache: bool = True,

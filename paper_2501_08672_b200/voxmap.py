@@ -72,6 +72,24 @@ def gaussian_row(g, width: Optional[int] = None) -> np.ndarray:
                            np.asarray(g.scale, float).ravel(), [float(g.opacity)], shk.ravel()]).astype(np.float32)
 
 
+def voxel_center(key, v_s: float) -> np.ndarray:
+    """Centre of a voxel key at its level (voxmap.py:54-56)."""
+    edge = v_s / (1 << key.level)
+    return (np.array([key.ix, key.iy, key.iz], dtype=float) + 0.5) * edge
+
+
+class LeafView:
+    """A leaf of the device map seen through the reference's OctreeNode
+    interface (voxmap.py:68-97): is_leaf, children (none), gaussians."""
+
+    __slots__ = ("key", "gaussians", "count")
+    is_leaf = True
+    children = (None,) * 8
+
+    def __init__(self, key, gaussians, count):
+        self.key, self.gaussians, self.count = key, gaussians, count
+
+
 class Inserted:
     pass
 
@@ -489,6 +507,79 @@ class HashOctree:
         centers = (roots + 0.5) * self.root_len     # floor(center / root_len) == root key
         keys = self.fov_leaf_keys_dev(centers).cpu().numpy()
         return {VoxelKey(int(a), int(b), int(c), self.max_level) for a, b, c in keys}
+
+    def fov_leaf_keys(self, points_w) -> set:
+        """voxmap.py:187-188: the leaf keys of the points themselves."""
+        return set(keys_of_points(points_w, self.leaf_len, self.max_level))
+
+    def group_by_leaf(self, points_w) -> dict:
+        """Leaf key -> stacked points (voxmap.py:213-230): keys ascend in
+        (ix, iy, iz) order and each group keeps scan order.  The keys and
+        the stable grouping sort run on the device; the groups are numpy
+        arrays like the reference's."""
+        pts = np.atleast_2d(np.asarray(points_w, dtype=float))
+        if pts.size == 0:
+            return {}
+        keys = keys_of_points_dev(pts, self.leaf_len, self.device)
+        from .window import order_keys
+        from .sort import sort_pairs
+        ok, order = sort_pairs(order_keys(keys))
+        ok, order = ok.cpu().numpy(), order.cpu().numpy()
+        idx = keys.cpu().numpy()[order]
+        spts = pts[order]
+        cuts = np.flatnonzero(ok[1:] != ok[:-1]) + 1
+        groups = {}
+        for ci, cp in zip(np.split(idx, cuts), np.split(spts, cuts)):
+            groups[VoxelKey(int(ci[0, 0]), int(ci[0, 1]), int(ci[0, 2]), self.max_level)] = cp
+        return groups
+
+    def add_leaf_stats(self, key, pts) -> None:
+        """voxmap.py:204-211: count += n; sum += pts.sum(axis=0); outer +=
+        pts^T pts, the group's sums formed like the reference's and added to
+        the leaf's device statistics (created if needed)."""
+        pts = np.atleast_2d(np.asarray(pts, dtype=float))
+        if pts.size == 0:
+            return
+        leaf = self.ensure_leaf(key)
+        s = leaf["slot"]
+        psum = pts.sum(axis=0)
+        po = pts.T @ pts
+        self.count[s] += len(pts)
+        self.sum[s] += torch.as_tensor(psum, device=self.device)
+        self.outer[s] += torch.as_tensor([po[0, 0], po[0, 1], po[0, 2], po[1, 1], po[1, 2], po[2, 2]],
+                                         device=self.device)
+
+    def iter_leaves(self):
+        """(key, leaf) in the reference's order (voxmap.py:339-353): sorted
+        root tuple, then octant DFS.  leaf.gaussians holds the leaf's
+        Gaussian (the host payload given to try_insert, else one built from
+        its device store row)."""
+        from .geometry import Gaussian3D
+        keys, slots = self.dump_dev()
+        k = keys.cpu().numpy()
+        if len(k) == 0:
+            return
+        order = _iter_order(k, self.max_level)
+        sl = slots[torch.as_tensor(order, device=self.device)]
+        gids = self.gslot[sl].cpu().numpy()
+        counts = self.count[sl].cpu().numpy()
+        rows = None
+        if getattr(self, "store", None) is not None and (gids >= 0).any():
+            g = torch.as_tensor(np.where(gids >= 0, gids, 0), device=self.device).long()
+            rows = self.store[g].cpu().numpy()
+        for i, (a, b, c) in enumerate(k[order]):
+            key = VoxelKey(int(a), int(b), int(c), self.max_level)
+            gs = []
+            gid = int(gids[i])
+            if gid >= 0:
+                if gid in self.gaussians:
+                    gs = [self.gaussians[gid]]
+                elif rows is not None:
+                    r = rows[i].astype(np.float64)
+                    K = (r.shape[0] - 16) // 3
+                    gs = [Gaussian3D(r[0:3], r[3:12].reshape(3, 3), r[12:15], float(r[15]), r[16:].reshape(K, 3),
+                                     level=self.max_level)]
+            yield key, LeafView(key, gs, int(counts[i]))
 
     def iter_leaf_keys(self) -> list:
         """Leaf keys in the reference's iteration order (voxmap.py:339-353):

@@ -125,6 +125,21 @@ class GaussianWindow:
         return torch.cat([self.means[:n], self.rots[:n].reshape(n, 9), self.scales[:n], self.opacities[:n, None],
                           self.shs[:n].reshape(n, -1)], dim=1)
 
+    def gaussian_at(self, key, device: bool = False):
+        """The live Gaussian of a leaf key (window.py:106-109; the window is
+        the device arena, so `device` changes nothing).  KeyError if the key
+        is not live."""
+        from .geometry import Gaussian3D
+        ok = order_keys(torch.as_tensor([[key[0], key[1], key[2]]], dtype=torch.int64, device=self.device))
+        hit = (self.wkeys[: self.n] == ok[0]).nonzero().flatten()
+        if hit.numel() == 0:
+            raise KeyError(key)
+        s = int(hit[0])
+        r = self.rows_dev()[s].double().cpu().numpy()
+        K = self.sh_coeffs
+        return Gaussian3D(r[0:3], r[3:12].reshape(3, 3), r[12:15], float(r[15]), r[16:16 + 3 * K].reshape(K, 3),
+                          level=int(key[3]) if len(key) > 3 else 0)
+
     def as_gaussian_arrays(self) -> GaussianArrays:
         """The live prefix as the renderer's arrays (views, no copy;
         window.py:109-120 upcasts a copy instead)."""
@@ -194,6 +209,31 @@ class GaussianWindow:
                 raise MissingVoxel("a window key has no leaf in the map")
         self.n = n - k
         return k, h
+
+    def writeback_deleted(self, vmap: HashOctree, diff: FrameDiff) -> None:
+        """Write the rows of diff.delete back to the map (window.py:145-150);
+        compact() then closes the holes.  Marks the live keys of the diff's
+        overlap as kept (the same marks diff() leaves)."""
+        keep = list(diff.overlap)
+        fov_ok = torch.sort(self._fov_order_keys(keep)).values if keep else torch.empty(0, dtype=torch.int64,
+                                                                                     device=self.device)
+        self._mark(fov_ok)
+        if diff.delete:
+            rows = self.rows_dev()
+            gone = ~self._keep[: self.n].bool()
+            vmap.set_gaussians_dev(self.live_keys_dev()[gone], rows[gone])
+        self._pending_vmap = vmap
+
+    def compact(self) -> int:
+        """Close the holes of the deleted slots (window.py:152-181: each
+        deleted slot, ascending, takes the rearmost live slot).  Returns the
+        number of moves."""
+        vmap = getattr(self, "_pending_vmap", None)
+        if vmap is None:
+            return 0
+        self._pending_vmap = None
+        _, moved = self.writeback_and_compact(vmap)
+        return moved
 
     def _leaf_gids(self, vmap: HashOctree, ok: torch.Tensor) -> torch.Tensor:
         gids = torch.empty(max(ok.numel(), 1), dtype=torch.int32, device=self.device)

@@ -52,7 +52,7 @@ def test_shard_units_cover_every_row_once_and_balance(n, height):
 
 def _views_and_scene():
     from types import SimpleNamespace
-    from paper_2501_08672_b200.scene import camera_for, orbit_views
+    from tools.scene import camera_for, orbit_views
     s = load("scene_room_0323")
     P = {k: s[k].astype(np.float64) for k in ("means", "rots", "scales", "opacities", "shs")}
     cam = camera_for(96, 80)

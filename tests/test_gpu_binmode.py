@@ -60,7 +60,7 @@ def test_binmode1_lists_and_outputs(name):
 
 def test_binmode1_fullsize_cfg2_view():
     from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings
-    from paper_2501_08672_b200.scene import bake_room, camera_for, orbit_views
+    from tools.scene import bake_room, camera_for, orbit_views
     arrays = GaussianArrays(*bake_room(0.0723))
     cam = camera_for(1280, 1024)
     T = orbit_views(10)[3]

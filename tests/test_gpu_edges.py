@@ -93,15 +93,11 @@ def test_4k_frame_tile_ranges_and_image():
     assert np.array_equal(s.export(3), gid)
     o = out.numpy()
     assert np.array_equal(o["contrib_count"], ref["n_proc"].reshape(2160, 3840))
-    # f32 alpha vs the reference's f64 at the alpha_cut test (_kernels.py:104) may
-    # flip a pair whose alpha is within rounding of 1/255: a
-    # flipped pixel's T differs by one factor (1 - 1/255); allow a handful
-    d = np.abs(o["image"] - ref["image"]).max(axis=2)
-    bad = d > 1e-4
-    assert bad.sum() <= 4, int(bad.sum())
-    Tg, Tr = o["final_transmittance"][bad], ref["t_final"].reshape(2160, 3840)[bad]
-    ratio = np.maximum(Tg, Tr) / np.minimum(Tg, Tr)
-    assert np.all(np.abs(ratio - 1 / (1 - 1 / 255)) < 1e-4), ratio
+    # the alpha_cut test (_kernels.py:104) is the reference's f64 decision for
+    # every pair, including those whose f32 alpha is within rounding of 1/255
+    # (decided in f64 by the re-blend of their tiles): no flipped pixel
+    assert np.abs(o["image"] - ref["image"]).max() <= 1e-4
+    assert np.abs(o["final_transmittance"] - ref["t_final"].reshape(2160, 3840)).max() <= 1e-4
 
 
 def test_engine_capacity_overflow_is_reported_not_fatal():
@@ -112,7 +108,7 @@ def test_engine_capacity_overflow_is_reported_not_fatal():
     from golden_io import load
     from paper_2501_08672_b200.optimize import OptimConfig, WindowEngine
     from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
-    from paper_2501_08672_b200.scene import camera_for, orbit_views
+    from tools.scene import camera_for, orbit_views
     s = load("scene_room_0323")
     cam = camera_for(160, 128)
     views = orbit_views(3)
@@ -125,3 +121,71 @@ def test_engine_capacity_overflow_is_reported_not_fatal():
     assert not eng.check_capacity()
     out = render(win, views[0], cam, st)        # the context is healthy
     assert torch.isfinite(out.image).all()
+
+
+def test_engine_overflow_of_an_earlier_view_is_sticky():
+    """Only the FIRST view of a 3-view step overflows its capacity (it sees
+    the whole room; the others look away): the sticky per-lane flag still
+    reports it after the later views fit, losses() / finish() raise
+    CapacityExceeded, and regrow() makes the next step fit."""
+    import torch
+    from golden_io import load
+    from paper_2501_08672_b200.errors import CapacityExceeded
+    from paper_2501_08672_b200.geometry import SE3
+    from paper_2501_08672_b200.optimize import OptimConfig, WindowEngine
+    from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
+    from tools.scene import camera_for, orbit_views
+    s = load("scene_room_0323")
+    cam = camera_for(160, 128)
+    T0 = orbit_views(3)[0]
+    away = SE3(T0.R, T0.t + 1000.0 * T0.R[:, 2])                  # 1 km ahead, looking on: sees nothing
+    views = [T0, away, away]
+    st = RasterSettings(alpha_cut=1 / 255)
+    win = GaussianArrays(s["means"], s["rots"], s["scales"], s["opacities"], s["shs"])
+    obs = [render(win, T, cam, st, retain_cache=False).image.clone() for T in views]
+    full = render(win, T0, cam, st, bin_mode=1).cache.read_counts()[1]
+    eng = WindowEngine(win, cam, views, st, OptimConfig(), isect_cap=max(64, full // 2), lanes=1)
+    eng.step(obs)
+    torch.cuda.synchronize()
+    assert not eng.lanes[0].state.read_counts()[2]                # the LAST render on the lane fit
+    with pytest.raises(CapacityExceeded):
+        eng.losses()
+    with pytest.raises(CapacityExceeded):
+        eng.finish()
+    assert not eng.check_capacity()                               # (clears the flag)
+    eng.regrow()
+    eng.step(obs)
+    assert eng.check_capacity()
+    assert np.isfinite(eng.losses()).all()
+
+
+def test_optimize_window_regrows_before_adam(monkeypatch):
+    """optimize_window with a far too small initial capacity regrows before
+    each Adam step (the reference never fails here, optimize.py:159-201):
+    the result equals the run whose capacity was right from the start."""
+    import torch
+    from golden_io import load
+    from paper_2501_08672_b200.optimize import OptimConfig, WindowEngine, optimize_window
+    from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
+    from tools.scene import camera_for, orbit_views
+    s = load("scene_room_0323")
+    cam = camera_for(160, 128)
+    T = orbit_views(3)[1]
+    st = RasterSettings(alpha_cut=1 / 255)
+    gt = GaussianArrays(s["means"], s["rots"], s["scales"], s["opacities"], s["shs"])
+    obs = render(gt, T, cam, st, retain_cache=False).image.clone()
+    shs = s["shs"].copy()
+    shs[:, 0, :] += 0.05
+
+    def run():
+        w = GaussianArrays(s["means"], s["rots"], s["scales"], s["opacities"], shs)
+        hist = optimize_window(w, obs, T, cam, OptimConfig(iters=3), st)
+        torch.cuda.synchronize()
+        return w, [h.value for h in hist]
+
+    w1, h1 = run()
+    monkeypatch.setattr(WindowEngine, "calibrate", lambda self, headroom=1.3: 64)
+    w2, h2 = run()
+    assert h1 == h2
+    for k in ("means", "rots", "scales", "opacities", "shs"):
+        assert bool((getattr(w1, k) == getattr(w2, k)).all()), k

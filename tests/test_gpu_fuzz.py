@@ -3,9 +3,9 @@ oracle: odd image sizes (not multiples of the 16-pixel tile), 1..400
 Gaussians, SH degrees 0-3, both alpha_cut settings, random backgrounds,
 footprints from sub-pixel to near the 512-px cap, opacities near the clamp.
 Same bars as test_gpu_render.py: tile ranges / entries bit-exact, RGB / T
-within 1e-4 (a pair whose f32 alpha sits within rounding of alpha_cut may
-flip: at most a few pixels, each off by exactly one (1 - cut) factor of T),
-gradients and pose within 1e-3 relative."""
+within 1e-4 on every pixel (the alpha_cut decision is the reference's f64
+one, also for pairs whose f32 alpha is within rounding of the cut),
+gradients and pose within 1e-3 relative on every seed."""
 from types import SimpleNamespace
 
 import numpy as np
@@ -61,13 +61,8 @@ def test_random_scene_parity(seed):
     assert np.array_equal(s.export(3), gid)
     o = out.numpy()
     h, w = cam.height, cam.width
-    d = np.abs(o["image"] - ref["image"]).max(axis=2)
-    bad = d > 1e-4
-    assert bad.sum() <= 3, int(bad.sum())
-    if bad.any():
-        Tg, Tr = o["final_transmittance"][bad], ref["t_final"].reshape(h, w)[bad]
-        assert np.all(np.abs(np.maximum(Tg, Tr) / np.minimum(Tg, Tr) - 1 / (1 - st.alpha_cut)) < 1e-3)
-        return                      # a flipped pair also changes that pixel's gradients
+    assert np.abs(o["image"] - ref["image"]).max() <= 1e-4
+    assert np.array_equal(o["contrib_count"], ref["n_proc"].reshape(h, w))
     assert np.abs(o["final_transmittance"] - ref["t_final"].reshape(h, w)).max() <= 1e-4
     grads, pose = backward(out, g_img)
     rb = orc.backward(ref, g_img)

@@ -93,7 +93,7 @@ def _room_engine(lanes, steps=2, mode="eager", loss_in_backward=True, fused=True
     import torch
     from paper_2501_08672_b200.optimize import OptimConfig, WindowEngine
     from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
-    from paper_2501_08672_b200.scene import camera_for, orbit_views
+    from tools.scene import camera_for, orbit_views
     s = load("scene_room_0323")
     cam = camera_for(160, 128)
     views = orbit_views(5)
@@ -165,7 +165,7 @@ def test_engine_multiview_matches_oracle(frames):
     8-bit frames the oracle gets read_ppm's u / 255.0."""
     from types import SimpleNamespace
     from oracle.optim import optimize_views
-    from paper_2501_08672_b200.scene import camera_for, orbit_views
+    from tools.scene import camera_for, orbit_views
     win, losses, _ = _room_engine(2, steps=1, frames=frames)
     s = load("scene_room_0323")
     cam = camera_for(160, 128)
@@ -254,7 +254,7 @@ def test_engine_row_bands_equal_whole_views():
     from paper_2501_08672_b200.dist import shard_units
     from paper_2501_08672_b200.optimize import OptimConfig, WindowEngine
     from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
-    from paper_2501_08672_b200.scene import camera_for, orbit_views
+    from tools.scene import camera_for, orbit_views
     s = load("scene_room_0323")
     cam = camera_for(160, 128)
     views = orbit_views(5)

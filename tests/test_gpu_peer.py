@@ -68,7 +68,7 @@ def test_peer_exchange_single_rank(tmp_path):
     from paper_2501_08672_b200.dist import PeerExchange
     from paper_2501_08672_b200.optimize import OptimConfig, WindowEngine
     from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
-    from paper_2501_08672_b200.scene import camera_for, orbit_views
+    from tools.scene import camera_for, orbit_views
     s = load("scene_room_0323")
     cam = camera_for(160, 128)
     views = orbit_views(3)
@@ -106,7 +106,7 @@ def test_peer_exchange_in_cuda_graph(tmp_path):
     from paper_2501_08672_b200.dist import PeerExchange
     from paper_2501_08672_b200.optimize import OptimConfig, WindowEngine
     from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
-    from paper_2501_08672_b200.scene import camera_for, orbit_views
+    from tools.scene import camera_for, orbit_views
     s = load("scene_room_0323")
     cam = camera_for(160, 128)
     views = orbit_views(3)

@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 def _setup():
     from paper_2501_08672_b200.geometry import PinholeCamera, SE3
     from paper_2501_08672_b200.raster import GaussianArrays
-    from paper_2501_08672_b200.scene import T_IC
+    from tools.scene import T_IC
     d = load("visual_room")
     s = load("scene_room_0323")
     arrays = GaussianArrays(s["means"], s["rots"], s["scales"], s["opacities"], s["shs"])

@@ -5,7 +5,7 @@ from golden_io import load
 
 
 def test_bake_room_matches_reference_fixture():
-    from paper_2501_08672_b200.scene import bake_room
+    from tools.scene import bake_room
     d = load("scene_room_0323")
     m, r, s, o, sh = bake_room(0.323)
     f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)
@@ -18,5 +18,5 @@ def test_bake_room_matches_reference_fixture():
 
 
 def test_room_sizes_match_survey():
-    from paper_2501_08672_b200.scene import bake_room
+    from tools.scene import bake_room
     assert len(bake_room(0.0723)[0]) == 203877

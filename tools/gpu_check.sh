@@ -1,12 +1,15 @@
 #!/bin/bash
-# One GPU session: tests, smoke, bench, launch list, one full ncu capture.
-# usage (under gpurun): bash tools/gpu_check.sh [tag]
-TAG=${1:-r01}
+# One GPU session: tests, smoke, bench (+ reference arm).
+# usage (under gpurun): bash tools/gpu_check.sh [tag] [pytest selection]
+TAG=${1:-r02}
+SEL=${2:-tests}
 mkdir -p gpurun_out
 export PYTHONDONTWRITEBYTECODE=1
-timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_$TAG.log 2>&1
+timeout 1500 python -m pytest $SEL -m gpu -x -q -s -p no:cacheprovider > gpurun_out/pytest_gpu_$TAG.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pytest_gpu_$TAG.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1
 timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
 echo "bench rc=$?" >> gpurun_out/bench_$TAG.err
-tail -3 gpurun_out/pytest_gpu_$TAG.log; tail -2 gpurun_out/smoke_$TAG.log; cat gpurun_out/bench_$TAG.json; tail -5 gpurun_out/bench_$TAG.err
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err
+tail -5 gpurun_out/pytest_gpu_$TAG.log; tail -2 gpurun_out/smoke_$TAG.log; cat gpurun_out/bench_$TAG.json; tail -5 gpurun_out/bench_$TAG.err
+cat gpurun_out/bench_ref_$TAG.json; tail -3 gpurun_out/bench_ref_$TAG.err

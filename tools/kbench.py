@@ -33,7 +33,7 @@ def main():
                                               render_blend, render_blend_bwd, render_blend_bwd_loss,
                                               render_blend_fused_loss,
                                               render_blend_loss, render_chain)
-    from paper_2501_08672_b200.scene import bake_room, camera_for, orbit_views
+    from tools.scene import bake_room, camera_for, orbit_views
     torch.cuda.set_device(0)
     P = bake_room(args.vs)
     W, H = (int(v) for v in args.size.split("x"))

@@ -1,4 +1,5 @@
-"""Synthetic benchmark inputs: the reference's own scene generator, restated.
+"""Synthetic benchmark inputs (bench and test support, not part of the product
+package): the reference's own scene generator, restated.
 
 The reference bakes its benchmark scenes with sim.bake_scene(default_room())
 (sim.py:131-169, 436-445): one Gaussian per surface leaf voxel of a textured
@@ -15,7 +16,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .geometry import SE3
+from paper_2501_08672_b200.geometry import SE3
 
 SH_C0 = 0.28209479177387814
 T_IC = SE3(np.array([[0.0, 0.0, 1.0], [-1.0, 0.0, 0.0], [0.0, -1.0, 0.0]]), [0.05, 0.0, 0.0])
@@ -165,7 +166,7 @@ def orbit_views(n_views: int):
 
 
 def camera_for(width: int, height: int):
-    from .geometry import PinholeCamera
+    from paper_2501_08672_b200.geometry import PinholeCamera
     return PinholeCamera(0.9375 * width, 0.9375 * width, width / 2, height / 2, width, height)
 
 
