@@ -539,13 +539,19 @@ def run_voxel(args, rank, world, local_rank):
     status = torch.empty_like(cslots, dtype=torch.int32)
     out = torch.empty((1 << 23, 3), dtype=torch.int64, device=dev)
 
+    nb = ctypes.c_size_t()
+    lib.lsb_voxmap_accumulate_temp_bytes(max(n_pts), ctypes.byref(nb))
+    acc_tmp = torch.empty(nb.value, dtype=torch.uint8, device=dev)
+
     def run(m, frames):
         st = m.struct()
         gid = 0
         for f in frames:
             p, c = scans[f], cands[f]
-            lib.lsb_voxmap_insert_points(ctypes.byref(st), ctypes.c_void_p(p.data_ptr()), p.shape[0], 1,
-                                         ctypes.c_void_p(slots.data_ptr()), _lib.stream_ptr())
+            # deterministic leaf statistics: stable device radix sort by leaf, one add per leaf
+            lib.lsb_voxmap_accumulate(ctypes.byref(st), ctypes.c_void_p(p.data_ptr()), p.shape[0],
+                                      ctypes.c_void_p(slots.data_ptr()), ctypes.c_void_p(acc_tmp.data_ptr()),
+                                      acc_tmp.numel(), _lib.stream_ptr())
             lib.lsb_voxmap_try_insert(ctypes.byref(st), ctypes.c_void_p(c.data_ptr()), c.shape[0], gid,
                                       ctypes.c_void_p(cslots.data_ptr()), ctypes.c_void_p(status.data_ptr()),
                                       _lib.stream_ptr())

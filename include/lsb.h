@@ -410,6 +410,14 @@ int lsb_voxmap_keys(const double* pts, int64_t n, double edge, int64_t* keys_out
  * point's leaf slot (may be NULL). */
 int lsb_voxmap_insert_points(const lsb_voxmap* m, const double* pts, int64_t n, int32_t accumulate,
                              int64_t* slots_out, void* stream);
+/* Deterministic accumulate_points (voxmap.py:184-211): the points are
+ * grouped by leaf with a stable device radix sort and each leaf adds its
+ * group's count / sum / outer, summed in scan order, once - identical
+ * statistics run to run (lsb_voxmap_insert_points with accumulate uses
+ * f64 atomics instead).  temp: lsb_voxmap_accumulate_temp_bytes(n) bytes. */
+int lsb_voxmap_accumulate_temp_bytes(int64_t n, size_t* bytes);
+int lsb_voxmap_accumulate(const lsb_voxmap* m, const double* pts, int64_t n, int64_t* slots_out, void* temp,
+                          size_t temp_bytes, void* stream);
 /* try_insert for a batch of Gaussian means with leaf_capacity 1: the lowest
  * batch index landing in an empty leaf is stored (gslot = first_gid + i) and
  * gets status 1 (Inserted), the others 0 (Full).  slots (n) int64 scratch. */

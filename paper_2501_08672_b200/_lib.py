@@ -79,6 +79,8 @@ SIGNATURES = [
     ("lsb_abi_version", _c.c_int, []),
     ("lsb_last_error", _c.c_char_p, []),
     ("lsb_workspace_bytes", _c.c_int, [_c.POINTER(Dims), _c.POINTER(_c.c_size_t)]),
+    ("lsb_voxmap_accumulate_temp_bytes", _c.c_int, [_c.c_int64, _c.POINTER(_c.c_size_t)]),
+    ("lsb_voxmap_accumulate", _c.c_int, [_c.POINTER(VoxMap), _P, _c.c_int64, _P, _P, _c.c_size_t, _P]),
     ("lsb_sort_temp_bytes", _c.c_int, [_c.c_int64, _c.POINTER(_c.c_size_t)]),
     ("lsb_sort_pairs", _c.c_int, [_P, _P, _P, _P, _c.c_int64, _c.c_int, _P, _c.c_size_t, _P]),
     ("lsb_segments", _c.c_int, [_P, _c.c_int64, _P, _P, _P, _c.c_size_t, _P]),

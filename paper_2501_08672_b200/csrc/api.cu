@@ -11,6 +11,8 @@ cudaError_t launch_splat(const lsb_params&, const lsb_camera&, const lsb_pose&, 
 size_t sort_temp_bytes(int64_t n);
 cudaError_t launch_sort_pairs(const uint64_t*, const int32_t*, uint64_t*, int32_t*, int64_t, int, void*, cudaStream_t);
 cudaError_t launch_segments(const uint64_t*, int64_t, int64_t*, int64_t*, void*, cudaStream_t);
+size_t vox_accumulate_temp_bytes(int64_t n);
+cudaError_t launch_vox_accumulate(const lsb_voxmap&, const double*, int64_t, int64_t*, void*, cudaStream_t);
 cudaError_t launch_preprocess(const lsb_params&, const lsb_camera&, const lsb_pose&, const lsb_settings&,
                               const Ws&, cudaStream_t);
 cudaError_t launch_blend_fwd(const Ws&, const lsb_settings&, int, int, float*, float*, int32_t*, float*,
@@ -485,6 +487,22 @@ int lsb_voxmap_insert_points(const lsb_voxmap* m, const double* pts, int64_t n, 
     if (rc) return rc;
     if (n > 0 && !pts) return fail(LSB_EINVAL, "NULL points");
     return check_cuda(launch_vox_insert(*m, pts, n, accumulate, slots, (cudaStream_t)stream), "voxmap_insert");
+}
+
+int lsb_voxmap_accumulate_temp_bytes(int64_t n, size_t* bytes) {
+    if (!bytes || n < 0) return fail(LSB_EINVAL, "bad argument");
+    *bytes = vox_accumulate_temp_bytes(n);
+    return LSB_OK;
+}
+
+int lsb_voxmap_accumulate(const lsb_voxmap* m, const double* pts, int64_t n, int64_t* slots, void* temp,
+                          size_t temp_bytes, void* stream) {
+    int rc = vox_ok(m);
+    if (rc) return rc;
+    if (n < 0 || n > 0x7fffffffll) return fail(LSB_EINVAL, "bad n");
+    if (n > 0 && (!pts || !temp)) return fail(LSB_EINVAL, "NULL argument");
+    if (temp_bytes < vox_accumulate_temp_bytes(n)) return fail(LSB_EINVAL, "accumulate workspace too small");
+    return check_cuda(launch_vox_accumulate(*m, pts, n, slots, temp, (cudaStream_t)stream), "voxmap_accumulate");
 }
 
 int lsb_voxmap_try_insert(const lsb_voxmap* m, const double* means, int64_t n, int32_t first_gid, int64_t* slots,

@@ -231,6 +231,105 @@ cudaError_t launch_vox_keys(const double* pts, int64_t n, double edge, int64_t* 
     return cudaGetLastError();
 }
 
+// ---- deterministic accumulate (voxmap.py:184-211) ---------------------------
+// The reference groups a scan by leaf and adds each group's sums to the
+// leaf's statistics in one fixed order (count += n, sum += pts.sum(axis=0),
+// outer += pts^T pts).  Here: every point finds (or creates) its leaf's
+// table slot, the points are radix-sorted stably by slot (scan order kept
+// inside a leaf; log2(cap) + 1 key bits, 3 passes at the default capacity),
+// the runs of equal slots are found, and one thread per run sums its points
+// in scan order and adds the sums to the leaf once - no floating-point
+// atomics, so the statistics are identical run to run.
+size_t sort_temp_bytes(int64_t n);
+cudaError_t launch_sort_pairs(const uint64_t*, const int32_t*, uint64_t*, int32_t*, int64_t, int, void*, cudaStream_t);
+cudaError_t launch_segments(const uint64_t*, int64_t, int64_t*, int64_t*, void*, cudaStream_t);
+
+__global__ void k_slot_keys(const int64_t* __restrict__ slots, int64_t n, int64_t bad,
+                            unsigned long long* __restrict__ keys) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = slots[i];
+        keys[i] = (unsigned long long)(s >= 0 ? s : bad);
+    }
+}
+
+__global__ void k_accumulate_runs(lsb_voxmap m, const double* __restrict__ pts, int64_t n,
+                                  const unsigned long long* __restrict__ skeys, const int32_t* __restrict__ perm,
+                                  const int64_t* __restrict__ starts, const int64_t* __restrict__ nseg_p) {
+    const int64_t nseg = *nseg_p;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nseg; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i0 = starts[r], i1 = r + 1 < nseg ? starts[r + 1] : n;
+        const int64_t s = (int64_t)skeys[i0];
+        if (s >= m.cap) continue;                         // points without a leaf (flagged by the insert)
+        double sx = 0.0, sy = 0.0, sz = 0.0, oxx = 0.0, oxy = 0.0, oxz = 0.0, oyy = 0.0, oyz = 0.0, ozz = 0.0;
+        for (int64_t i = i0; i < i1; ++i) {
+            const int64_t q = perm[i];
+            const double x = pts[3 * q], y = pts[3 * q + 1], z = pts[3 * q + 2];
+            sx += x;
+            sy += y;
+            sz += z;
+            oxx += x * x;
+            oxy += x * y;
+            oxz += x * z;
+            oyy += y * y;
+            oyz += y * z;
+            ozz += z * z;
+        }
+        // one run per leaf per call: the only writer of this leaf's statistics
+        m.count[s] += i1 - i0;
+        m.sum[3 * s] += sx;
+        m.sum[3 * s + 1] += sy;
+        m.sum[3 * s + 2] += sz;
+        double* o = m.outer + 6 * s;
+        o[0] += oxx;
+        o[1] += oxy;
+        o[2] += oxz;
+        o[3] += oyy;
+        o[4] += oyz;
+        o[5] += ozz;
+    }
+}
+
+static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t vox_accumulate_temp_bytes(int64_t n) {
+    const size_t nn = (size_t)(n > 0 ? n : 1);
+    return al256(8 * nn) * 3 + al256(4 * nn) + al256(8 * nn) + al256(8) + sort_temp_bytes(n);
+}
+
+cudaError_t launch_vox_insert(const lsb_voxmap& m, const double* pts, int64_t n, int accumulate, int64_t* slots,
+                              cudaStream_t st);
+
+cudaError_t launch_vox_accumulate(const lsb_voxmap& m, const double* pts, int64_t n, int64_t* slots, void* temp,
+                                  cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    const size_t nn = (size_t)n;
+    char* t = (char*)temp;
+    int64_t* sl = (int64_t*)t;
+    t += al256(8 * nn);
+    unsigned long long* keys = (unsigned long long*)t;
+    t += al256(8 * nn);
+    unsigned long long* skeys = (unsigned long long*)t;
+    t += al256(8 * nn);
+    int32_t* perm = (int32_t*)t;
+    t += al256(4 * nn);
+    int64_t* starts = (int64_t*)t;
+    t += al256(8 * nn);
+    int64_t* nseg = (int64_t*)t;
+    t += al256(8);
+    if (!slots) slots = sl;
+    cudaError_t e = launch_vox_insert(m, pts, n, 0, slots, st);      // find / create every point's leaf
+    if (e != cudaSuccess) return e;
+    int bits = 1;
+    while ((1ll << bits) <= m.cap) ++bits;                          // slots < cap, and `cap` marks a miss
+    k_slot_keys<<<grid_for(n), 256, 0, st>>>(slots, n, m.cap, keys);
+    e = launch_sort_pairs((const uint64_t*)keys, nullptr, (uint64_t*)skeys, perm, n, bits, t, st);
+    if (e != cudaSuccess) return e;
+    e = launch_segments((const uint64_t*)skeys, n, starts, nseg, t, st);
+    if (e != cudaSuccess) return e;
+    k_accumulate_runs<<<grid_for(n), 256, 0, st>>>(m, pts, n, skeys, perm, starts, nseg);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_vox_insert(const lsb_voxmap& m, const double* pts, int64_t n, int accumulate, int64_t* slots,
                               cudaStream_t st) {
     if (n > 0) k_insert_points<<<grid_for(n), 256, 0, st>>>(m, pts, n, accumulate, slots);

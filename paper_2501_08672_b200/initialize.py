@@ -8,8 +8,8 @@ and one device thread per group (sorted key order, like the reference's
 loop) skips leaves that already hold a Gaussian, applies the observability
 pre-check, fits the plane normal (view-direction fallback), samples the
 image bilinearly, and emits the slab-frame Gaussian row; the rows go into
-the map's device store (`HashOctree.set_gaussians_dev`).  Sorting the group
-keys uses torch.sort (library radix sort; per scan, not the splat hot path).
+the map's device store (`HashOctree.set_gaussians_dev`).  The grouping is
+the library's own stable radix sort and run segmentation (csrc/sort.cu).
 """
 
 from __future__ import annotations
@@ -21,6 +21,7 @@ import torch
 
 from . import _lib
 from .geometry import as_se3
+from .sort import segments, sort_pairs
 from .voxmap import HashOctree, keys_of_points_dev
 from .window import order_keys, unpack_order_keys
 
@@ -47,11 +48,12 @@ def insert_new_gaussians(vmap: HashOctree, points_w, image, T_wc, cam, sensor_or
         return (torch.empty((0, 3), dtype=torch.int64, device=dev), torch.empty((0, R), device=dev),
                 torch.empty(0, dtype=torch.bool, device=dev))
     keys = keys_of_points_dev(pts, vmap.leaf_len, dev)
-    srt = torch.sort(order_keys(keys), stable=True)
-    uniq, counts = torch.unique_consecutive(srt.values, return_counts=True)
-    starts = torch.cumsum(counts, 0) - counts
-    k = int(uniq.numel())
-    perm = srt.indices.contiguous()
+    skeys, perm32 = sort_pairs(order_keys(keys), key_bits=63, signed=False)
+    starts = segments(skeys)
+    k = int(starts.numel())
+    uniq = skeys[starts]
+    counts = torch.diff(starts, append=torch.full((1,), skeys.numel(), dtype=torch.int64, device=dev))
+    perm = perm32.to(torch.int64)
     cent = torch.empty((k, 3), dtype=torch.float64, device=dev)
     lib = _lib.load()
     _lib.check(lib.lsb_segment_mean(ctypes.c_void_p(pts.data_ptr()), ctypes.c_void_p(perm.data_ptr()),

@@ -122,17 +122,17 @@ class GaussianArrays:
         return self.means.device
 
     @staticmethod
-    def from_gaussians(gaussians, device=None) -> "GaussianArrays":
+    def from_gaussians(gaussians, device=None, dtype=torch.float32) -> "GaussianArrays":
         if not gaussians:
             return GaussianArrays(np.zeros((0, 3)), np.zeros((0, 3, 3)), np.zeros((0, 3)), np.zeros(0),
-                                  np.zeros((0, 1, 3)), device)
+                                  np.zeros((0, 1, 3)), device, dtype)
         k = max(g.sh.shape[0] for g in gaussians)
         shs = np.zeros((len(gaussians), k, 3))
         for i, g in enumerate(gaussians):
             shs[i, : g.sh.shape[0]] = g.sh
         return GaussianArrays(np.stack([g.mean_w for g in gaussians]), np.stack([g.rot for g in gaussians]),
                               np.stack([g.scale for g in gaussians]),
-                              np.array([g.opacity for g in gaussians], dtype=float), shs, device)
+                              np.array([g.opacity for g in gaussians], dtype=float), shs, device, dtype)
 
     def params(self) -> _lib.Params:
         return _lib.Params(self.means.data_ptr(), self.rots.data_ptr(), self.scales.data_ptr(),
@@ -466,7 +466,8 @@ def splat_batch(source, T_cw, cam, settings: RasterSettings = RasterSettings()):
 def splat(g, T_cw, cam, settings: RasterSettings = RasterSettings()):
     """Project one Gaussian; returns a Gaussian2D or Culled (raster.py:188-205)."""
     from .geometry import Gaussian2D
-    vis, mu, cov, depth, col = splat_batch(GaussianArrays.from_gaussians([g]), T_cw, cam, settings)
+    vis, mu, cov, depth, col = splat_batch(GaussianArrays.from_gaussians([g], dtype=torch.float64), T_cw, cam,
+                                           settings)
     if not bool(vis[0]):
         return Culled()
     return Gaussian2D(mean_i=mu[0].cpu().numpy(), cov_i=cov[0].cpu().numpy(), depth=float(depth[0]),

@@ -205,9 +205,20 @@ class HashOctree:
         self._reserve(n)
         slots = torch.empty(n, dtype=torch.int64, device=self.device)
         m = self.struct()
-        _lib.check(_lib.load().lsb_voxmap_insert_points(ctypes.byref(m), ctypes.c_void_p(pts.data_ptr()), n,
-                                                        int(accumulate), ctypes.c_void_p(slots.data_ptr()),
-                                                        _lib.stream_ptr()),
+        lib = _lib.load()
+        if accumulate:
+            # deterministic: grouped by a stable device sort, one add per leaf
+            nb = ctypes.c_size_t()
+            _lib.check(lib.lsb_voxmap_accumulate_temp_bytes(n, ctypes.byref(nb)), "accumulate_temp")
+            if getattr(self, "_acc_tmp", None) is None or self._acc_tmp.numel() < nb.value:
+                self._acc_tmp = torch.empty(max(nb.value, 1), dtype=torch.uint8, device=self.device)
+            _lib.check(lib.lsb_voxmap_accumulate(ctypes.byref(m), ctypes.c_void_p(pts.data_ptr()), n,
+                                                 ctypes.c_void_p(slots.data_ptr()),
+                                                 ctypes.c_void_p(self._acc_tmp.data_ptr()), self._acc_tmp.numel(),
+                                                 _lib.stream_ptr()), "voxmap_accumulate")
+            return slots
+        _lib.check(lib.lsb_voxmap_insert_points(ctypes.byref(m), ctypes.c_void_p(pts.data_ptr()), n, 0,
+                                                ctypes.c_void_p(slots.data_ptr()), _lib.stream_ptr()),
                    "voxmap_insert")
         return slots
 
@@ -215,7 +226,8 @@ class HashOctree:
         """Reference-shaped: returns the set of touched leaf keys."""
         slots = self.accumulate_points_dev(points_w)
         self._check_flags()
-        u = torch.unique(slots)
+        from .sort import sort_pairs, unique_sorted
+        u = unique_sorted(sort_pairs(slots)[0])
         return {self._key_of_slot(k) for k in self._keys_of_slots(u)}
 
     def try_insert_batch(self, means, first_gid: Optional[int] = None) -> torch.Tensor:
@@ -498,6 +510,19 @@ class HashOctree:
         o = self.outer[s].cpu().numpy()
         outer = np.array([[o[0], o[1], o[2]], [o[1], o[3], o[4]], [o[2], o[4], o[5]]])
         return [leaf["count"], self.sum[s].cpu().numpy(), outer]
+
+    def leaf_stats_dev(self, keys):
+        """Batched leaf_stats for (k,3) leaf keys: (count (k,) int64, sum
+        (k,3) f64, outer (k,3,3) f64); zeros where the key has no leaf."""
+        t = self.lookup_dev(keys)
+        ok = t >= 0
+        tc = t.clamp(min=0)
+        cnt = torch.where(ok, self.count[tc], torch.zeros_like(self.count[tc]))
+        sm = torch.where(ok[:, None], self.sum[tc], torch.zeros_like(self.sum[tc]))
+        o = torch.where(ok[:, None], self.outer[tc], torch.zeros_like(self.outer[tc]))
+        outer = torch.stack([o[:, 0], o[:, 1], o[:, 2], o[:, 1], o[:, 3], o[:, 4], o[:, 2], o[:, 4], o[:, 5]],
+                            dim=1).reshape(-1, 3, 3)
+        return cnt, sm, outer
 
     def fov_root_keys(self, points_w) -> set:
         return set(keys_of_points(points_w, self.root_len, 0))

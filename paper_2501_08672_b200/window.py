@@ -20,9 +20,9 @@ map's device store (`HashOctree.store`, indexed by the leaf's gid), and
 Slot layout, rows and report counts are identical to the reference's
 (tests/test_gpu_window.py against tests/golden/window_walk.npz, produced by
 the reference itself).  There is no host mirror, so `sync_to_device` /
-`sync_to_host` move nothing and the report's byte counters stay 0.  Sorting
-the add list uses torch.sort (library radix sort; maintenance, not the splat
-hot path).  `init_fn` (Gaussian synthesis for FoV leaves without one) is a
+`sync_to_host` move nothing and the report's byte counters stay 0.  Key
+sorting and de-duplication use the library's own stable radix sort
+(csrc/sort.cu).  `init_fn` (Gaussian synthesis for FoV leaves without one) is a
 host callback, as in the reference.
 """
 
@@ -39,6 +39,7 @@ import torch
 from . import _lib
 from .errors import WindowFull
 from .raster import GaussianArrays
+from .sort import sort_pairs, unique_sorted
 from .voxmap import HashOctree, VoxelKey, gaussian_row
 
 _KOFF = 1 << 20
@@ -50,6 +51,15 @@ def order_keys(keys) -> torch.Tensor:
     k = keys if torch.is_tensor(keys) else torch.as_tensor(np.asarray(keys, dtype=np.int64).reshape(-1, 3))
     k = k.to(torch.int64)
     return ((k[:, 0] + _KOFF) << 42) | ((k[:, 1] + _KOFF) << 21) | (k[:, 2] + _KOFF)
+
+
+def _sorted(ok: torch.Tensor) -> torch.Tensor:
+    """Order keys ascending (the library's radix sort; keys are < 2^63)."""
+    return sort_pairs(ok, key_bits=63, signed=False)[0]
+
+
+def _sorted_unique(ok: torch.Tensor) -> torch.Tensor:
+    return unique_sorted(_sorted(ok))
 
 
 def unpack_order_keys(ok: torch.Tensor) -> torch.Tensor:
@@ -151,7 +161,8 @@ class GaussianWindow:
         """Prefix liveness and key uniqueness (window.py:122-133)."""
         k = self.wkeys[: self.n]
         assert bool((k >= 0).all()), "free slot inside the live prefix"
-        assert int(torch.unique(k).numel()) == self.n, "key mapped twice"
+        assert int(unique_sorted(sort_pairs(k, key_bits=63, signed=False)[0]).numel()) == self.n, \
+            "key mapped twice"
         assert bool((self.wkeys[self.n:] < 0).all()), "live key outside the prefix"
 
     # ---- protocol --------------------------------------------------------------
@@ -174,13 +185,13 @@ class GaussianWindow:
 
     def diff(self, fov_keys) -> FrameDiff:
         """Sorted overlap / delete / add key lists (window.py:136-143)."""
-        fov_ok = torch.unique(self._fov_order_keys(fov_keys))
+        fov_ok = _sorted_unique(self._fov_order_keys(fov_keys))
         is_add = self._mark(fov_ok).bool()
         live = self.wkeys[: self.n]
         keep = self._keep[: self.n].bool()
         lv = -1
         to_keys = lambda ok: [VoxelKey(int(a), int(b), int(c), lv)
-                              for a, b, c in unpack_order_keys(torch.sort(ok).values).cpu().numpy()]
+                              for a, b, c in unpack_order_keys(_sorted(ok)).cpu().numpy()]
         return FrameDiff(overlap=to_keys(live[keep]), delete=to_keys(live[~keep]), add=to_keys(fov_ok[is_add]))
 
     def writeback_and_compact(self, vmap: HashOctree) -> tuple:
@@ -215,8 +226,8 @@ class GaussianWindow:
         compact() then closes the holes.  Marks the live keys of the diff's
         overlap as kept (the same marks diff() leaves)."""
         keep = list(diff.overlap)
-        fov_ok = torch.sort(self._fov_order_keys(keep)).values if keep else torch.empty(0, dtype=torch.int64,
-                                                                                     device=self.device)
+        fov_ok = _sorted(self._fov_order_keys(keep)) if keep else torch.empty(0, dtype=torch.int64,
+                                                                               device=self.device)
         self._mark(fov_ok)
         if diff.delete:
             rows = self.rows_dev()
@@ -280,8 +291,8 @@ class GaussianWindow:
 
     def append(self, vmap: HashOctree, add: list, init_fn: Optional[Callable] = None) -> int:
         """Reference-shaped append of a key list (window.py:183)."""
-        ok = torch.sort(self._fov_order_keys(add)).values if len(add) else torch.empty(0, dtype=torch.int64,
-                                                                                     device=self.device)
+        ok = _sorted(self._fov_order_keys(add)) if len(add) else torch.empty(0, dtype=torch.int64,
+                                                                            device=self.device)
         return self.append_keys(vmap, ok, init_fn)
 
     def sync_to_device(self) -> int:
@@ -300,7 +311,7 @@ class GaussianWindow:
         an iterable of VoxelKey."""
         t0 = time.perf_counter()
         rep = MaintenanceReport()
-        fov_ok = torch.unique(self._fov_order_keys(fov_keys))   # sorted, unique
+        fov_ok = _sorted_unique(self._fov_order_keys(fov_keys))   # sorted, unique
         is_add = self._mark(fov_ok).bool()
         rep.removed, rep.moved = self.writeback_and_compact(vmap)
         add_ok = fov_ok[is_add]                                 # sorted (unique returns sorted)
@@ -315,9 +326,11 @@ class GaussianWindow:
                                                    vmap.root_len / (1 << vmap.max_level), origin,
                                                    ctypes.c_void_p(dist.data_ptr()), _lib.stream_ptr()),
                        "window_dist")
-            order = torch.sort(dist[:n_add], stable=True).indices      # keys already ascending: ties by key
+            # stable ascending distance (non-negative f64: its bits order as int64); the
+            # keys are already ascending, so ties keep key order
+            order = sort_pairs(dist[:n_add].view(torch.int64), key_bits=63, signed=False)[1].long()
             rep.dropped = n_add - room
-            add_ok = torch.sort(add_ok[order[:room]]).values
+            add_ok = _sorted(add_ok[order[:room]])
         rep.added = self.append_keys(vmap, add_ok, init_fn)
         rep.n_live = self.n
         rep.t_maintain_ms = (time.perf_counter() - t0) * 1e3

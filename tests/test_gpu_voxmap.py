@@ -35,13 +35,33 @@ def test_accumulate_points_matches_reference():
     touched = m.accumulate_points(d["pts"])      # also exercises the rehash growth path
     ref_keys = {tuple(k[:3]) for k in d["stat_keys"]}
     assert {k[:3] for k in touched} == ref_keys
-    for i in range(0, len(d["stat_keys"]), 37):
-        from paper_2501_08672_b200.voxmap import VoxelKey
-        k = d["stat_keys"][i]
-        st = m.leaf_stats(VoxelKey(int(k[0]), int(k[1]), int(k[2]), int(d["max_level"])))
-        assert st[0] == d["stat_count"][i]
-        assert np.allclose(st[1], d["stat_sum"][i], rtol=1e-12, atol=1e-12)
-        assert np.allclose(st[2], d["stat_outer"][i], rtol=1e-12, atol=1e-12)
+    # every leaf: counts exact, sums / outer products to f64 round-off (the
+    # reference's numpy pairwise / BLAS order vs scan order)
+    cnt, sm, outer = (t.cpu().numpy() for t in m.leaf_stats_dev(d["stat_keys"][:, :3]))
+    assert np.array_equal(cnt, d["stat_count"])
+    assert np.allclose(sm, d["stat_sum"], rtol=1e-12, atol=1e-12)
+    assert np.allclose(outer, d["stat_outer"], rtol=1e-12, atol=1e-12)
+    from paper_2501_08672_b200.voxmap import VoxelKey
+    k = d["stat_keys"][5]
+    st = m.leaf_stats(VoxelKey(int(k[0]), int(k[1]), int(k[2]), int(d["max_level"])))
+    assert st[0] == cnt[5] and np.array_equal(st[1], sm[5]) and np.array_equal(st[2], outer[5])
+
+
+def test_accumulate_is_deterministic():
+    """The leaf statistics are bit-identical across runs (sorted grouping,
+    fixed-order sums; no floating-point atomics)."""
+    import torch
+    d = load("voxmap")
+    out = []
+    for _ in range(2):
+        from paper_2501_08672_b200.voxmap import HashOctree
+        m = HashOctree(float(d["root_len"]), max_level=int(d["max_level"]))
+        for chunk in np.array_split(d["pts"], 3):
+            m.accumulate_points_dev(chunk)
+        out.append(tuple(t.cpu().numpy() for t in m.leaf_stats_dev(d["stat_keys"][:, :3])))
+        torch.cuda.synchronize()
+    for a, b in zip(*out):
+        assert np.array_equal(a, b)
 
 
 def test_try_insert_iter_order_and_fov_match_reference():
