@@ -1,7 +1,8 @@
 // K5 backward chain: one thread per visible splat (fixed grid, grid-stride).
 //
-// Sums the splat's per-intersection partials in intersection order (fixed,
-// so the result is deterministic), then applies the reference's chain rule
+// Takes the splat's summed per-intersection partials (k_chain_sums: a
+// balanced, fixed-shape segmented reduction, so the result is
+// deterministic), then applies the reference's chain rule
 // in f64 (raster.py:267-399): 2-D covariance -> world covariance ->
 // (rotation right tangent, scale); 2-D mean -> camera mean -> world mean;
 // SH colour with the clamp gate and view-direction term; camera-tangent pose
@@ -77,6 +78,187 @@ __device__ void sh_basis_grad_d(int degree, T x, T y, T z, T (*g)[3]) {
     }
 }
 
+// ---- partial sums: a balanced segmented reduction over the intersections ----
+// Intersections are splat-major (a splat's run is [vis_ebase[s],
+// vis_ebase[s + 1]); emit_slot[e] names its splat).  One warp per chunk of
+// CHAIN_CH = 256 intersections, lane l taking 8 consecutive ones (18 float4
+// loads): each lane sums its runs locally in f64, then one segmented warp
+// scan (fixed shape) stitches the runs that cross lanes.  A run closed inside
+// the chunk is written back in f64 over its own first two partials (72 B of
+// its own storage; a one-intersection run keeps its f32 partial); the
+// chunk's first run when it started in an earlier chunk, and its last run
+// when it continues in a later one, go to chain_carry[chunk] (first / last),
+// which k_chain adds chunk by chunk in order.  Every sum has a fixed shape:
+// deterministic, balanced however long a splat's run is, no atomics.
+constexpr int CHAIN_CH = 256;
+constexpr int CHAIN_PER_LANE = CHAIN_CH / 32;
+
+__device__ __forceinline__ void store_f64x9(float* dst, const double* v) {
+    uint32_t* d = (uint32_t*)dst;
+#pragma unroll
+    for (int c = 0; c < NUM_PART; ++c) {
+        const unsigned long long b = (unsigned long long)__double_as_longlong(v[c]);
+        d[2 * c] = (uint32_t)b;
+        d[2 * c + 1] = (uint32_t)(b >> 32);
+    }
+}
+
+__device__ __forceinline__ double load_f64(const float* src, int c) {
+    const uint32_t* s = (const uint32_t*)src;
+    return __longlong_as_double((long long)(((unsigned long long)s[2 * c + 1] << 32) | s[2 * c]));
+}
+
+__global__ void __launch_bounds__(128) k_chain_sums(Ws w) {
+    const int64_t I = (int64_t)w.ctr[1];
+    if (I > (int64_t)w.cap) return;                  // overflow: no partials were written
+    const int lane = threadIdx.x & 31;
+    const int64_t nch = (I + CHAIN_CH - 1) / CHAIN_CH;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nch; c += nw) {
+        const int64_t cb = c * CHAIN_CH, ce = cb + CHAIN_CH < I ? cb + CHAIN_CH : I;
+        const int first_own = w.emit_slot[cb];
+        const bool open_start = cb > 0 && w.emit_slot[cb - 1] == first_own;
+        const int after_own = ce < I ? w.emit_slot[ce] : -3;
+        double* carry = w.chain_carry + (size_t)c * 2 * NUM_PART;
+        // ---- load the lane's 8 intersections ----
+        const int64_t lb = cb + (int64_t)lane * CHAIN_PER_LANE;
+        const int n = lb < ce ? (int)((ce - lb) < CHAIN_PER_LANE ? ce - lb : CHAIN_PER_LANE) : 0;
+        float v[CHAIN_PER_LANE][NUM_PART];
+        int own[CHAIN_PER_LANE];
+        if (n == CHAIN_PER_LANE) {
+            const float4* src = (const float4*)(w.part + lb * NUM_PART);
+            float* dst = &v[0][0];
+#pragma unroll
+            for (int q = 0; q < CHAIN_PER_LANE * NUM_PART / 4; ++q) {
+                const float4 x = __ldcs(src + q);
+                dst[4 * q] = x.x;
+                dst[4 * q + 1] = x.y;
+                dst[4 * q + 2] = x.z;
+                dst[4 * q + 3] = x.w;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < CHAIN_PER_LANE; ++k)
+#pragma unroll
+                for (int q = 0; q < NUM_PART; ++q) v[k][q] = k < n ? w.part[(lb + k) * NUM_PART + q] : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < CHAIN_PER_LANE; ++k) own[k] = k < n ? w.emit_slot[lb + k] : -2;
+        __syncwarp();                                  // every partial is read before any run is written back
+        // ---- lane-local runs: head (first), closed interior ones, tail (last) ----
+        double hs[NUM_PART], ts[NUM_PART];
+#pragma unroll
+        for (int q = 0; q < NUM_PART; ++q) hs[q] = ts[q] = 0.0;
+        int nseg = 0, h_cnt = 0, t_cnt = 0;
+        const int h_own = own[0];
+        int t_own = -2;
+        int64_t t_start = lb;
+#pragma unroll
+        for (int k = 0; k < CHAIN_PER_LANE; ++k) {
+            if (k >= n) break;
+            if (own[k] != t_own) {
+                if (nseg == 1) {                       // the head closed inside the lane
+#pragma unroll
+                    for (int q = 0; q < NUM_PART; ++q) hs[q] = ts[q];
+                    h_cnt = t_cnt;
+                } else if (nseg >= 2 && t_cnt >= 2) {  // an interior run: closed, local
+                    store_f64x9(w.part + t_start * NUM_PART, ts);
+                }
+                ++nseg;
+                t_own = own[k];
+                t_start = lb + k;
+                t_cnt = 0;
+#pragma unroll
+                for (int q = 0; q < NUM_PART; ++q) ts[q] = 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < NUM_PART; ++q) ts[q] += (double)v[k][q];
+            ++t_cnt;
+        }
+        // ---- stitch the runs that cross lanes: segmented scan of the tails ----
+        const int key = n ? t_own : -2 - lane;        // empty lanes: unique keys
+        const int kup = __shfl_up_sync(0xffffffffu, key, 1);
+        const int left_key = lane ? kup : (open_start ? first_own : -1);
+        double S[NUM_PART];
+#pragma unroll
+        for (int q = 0; q < NUM_PART; ++q) S[q] = ts[q];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int ko = __shfl_up_sync(0xffffffffu, key, o);
+            const bool add = lane >= o && ko == key;
+#pragma unroll
+            for (int q = 0; q < NUM_PART; ++q) {
+                const double y = __shfl_up_sync(0xffffffffu, S[q], o);
+                if (add) S[q] += y;
+            }
+        }
+        double Sl[NUM_PART];                          // the scan at the lane to the left
+#pragma unroll
+        for (int q = 0; q < NUM_PART; ++q) Sl[q] = __shfl_up_sync(0xffffffffu, S[q], 1);
+        const int right_head = __shfl_down_sync(0xffffffffu, n ? h_own : -7, 1);
+        const bool last_lane = n > 0 && (lane == 31 || lb + n >= ce);
+        // the head of a lane with >= 2 runs closes inside the lane
+        if (n > 0 && nseg >= 2) {
+            const bool cont = h_own == left_key;      // started in an earlier lane or chunk
+            if (!cont) {
+                if (h_cnt >= 2) store_f64x9(w.part + lb * NUM_PART, hs);
+            } else {
+                double tot[NUM_PART];
+#pragma unroll
+                for (int q = 0; q < NUM_PART; ++q) tot[q] = (lane ? Sl[q] : 0.0) + hs[q];
+                if (h_own == first_own && open_start) {
+#pragma unroll
+                    for (int q = 0; q < NUM_PART; ++q) carry[q] = tot[q];       // chunk's first run: first
+                } else {
+                    store_f64x9(w.part + (int64_t)w.vis_ebase[h_own] * NUM_PART, tot);
+                }
+            }
+        }
+        // a lane's tail closes at the lane's end when the next lane starts another run
+        if (n > 0 && (last_lane || right_head != t_own)) {
+            const bool from_before = t_own == first_own && open_start;
+            const bool open_end = last_lane && lb + n == ce && after_own == t_own;
+            if (from_before)
+#pragma unroll
+                for (int q = 0; q < NUM_PART; ++q) carry[q] = S[q];
+            if (open_end)
+#pragma unroll
+                for (int q = 0; q < NUM_PART; ++q) carry[NUM_PART + q] = S[q];
+            if (!from_before && !open_end) {
+                const bool cont = nseg == 1 && t_own == left_key;
+                if (cont) store_f64x9(w.part + (int64_t)w.vis_ebase[t_own] * NUM_PART, S);
+                else if (t_cnt >= 2) store_f64x9(w.part + t_start * NUM_PART, S);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// The partial sums of splat `slot` (after k_chain_sums).
+__device__ __forceinline__ bool chain_q(const Ws& w, int64_t slot, double* q) {
+    const int64_t e0 = w.vis_ebase[slot], e1 = w.vis_ebase[slot + 1];
+    if (e1 <= e0) return false;
+    const int64_t c0 = e0 / CHAIN_CH, c1 = (e1 - 1) / CHAIN_CH;
+    if (c0 == c1) {
+        const float* p = w.part + e0 * NUM_PART;
+        if (e1 - e0 == 1) {
+#pragma unroll
+            for (int k = 0; k < NUM_PART; ++k) q[k] = (double)p[k];
+        } else {
+#pragma unroll
+            for (int k = 0; k < NUM_PART; ++k) q[k] = load_f64(p, k);
+        }
+        return true;
+    }
+    const double* cr = w.chain_carry;
+#pragma unroll
+    for (int k = 0; k < NUM_PART; ++k) q[k] = cr[(size_t)c0 * 2 * NUM_PART + NUM_PART + k];
+    for (int64_t c = c0 + 1; c <= c1; ++c)
+#pragma unroll
+        for (int k = 0; k < NUM_PART; ++k) q[k] += cr[(size_t)c * 2 * NUM_PART + k];
+    return true;
+}
+
 using CT = double;  // chain-rule arithmetic: f64 keeps Adam's sign-sensitive first steps on the reference trajectory
 
 __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
@@ -93,21 +275,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
         const Rec& r = w.rec[slot];
         if (r.ebase < 0) continue;
         double q[NUM_PART];
-        // the splat's intersection partials (contiguous, e in [ebase, ebase + nt)),
-        // summed in e order
-#pragma unroll
-        for (int c = 0; c < NUM_PART; ++c) q[c] = 0.0;
-        {
-            const float* src = w.part + (int64_t)r.ebase * NUM_PART;
-            const int nt = w.vis_ebase[slot + 1] - r.ebase;
-            for (int k = 0; k < nt; ++k, src += NUM_PART) {
-                float v[NUM_PART];
-#pragma unroll
-                for (int c = 0; c < NUM_PART; ++c) v[c] = __ldcs(src + c);
-#pragma unroll
-                for (int c = 0; c < NUM_PART; ++c) q[c] += (double)v[c];
-            }
-        }
+        if (!chain_q(w, slot, q)) continue;
         bool nz = false;
 #pragma unroll
         for (int c = 0; c < NUM_PART; ++c) nz |= (q[c] != 0.0);
@@ -270,12 +438,29 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
     }
     __syncthreads();
     if (s_last) {
+        // all CHAIN_THREADS threads: thread t sums the blocks b = t, t + T, ...
+        // (independent loads, pipelined), then a fixed tree over the threads
         __threadfence();
+        double v[POSE_VALS];
+#pragma unroll
+        for (int c = 0; c < POSE_VALS; ++c) v[c] = 0.0;
+        for (int b2 = threadIdx.x; b2 < (int)gridDim.x; b2 += CHAIN_THREADS)
+#pragma unroll
+            for (int c = 0; c < POSE_VALS; ++c) v[c] += __ldcg(w.pose_part + b2 * POSE_VALS + c);
+#pragma unroll
+        for (int c = 0; c < POSE_VALS; ++c) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v[c] += __shfl_xor_sync(0xffffffffu, v[c], o);
+        }
+        __syncthreads();
+        if (lane == 0)
+#pragma unroll
+            for (int c = 0; c < POSE_VALS; ++c) s_red[warp][c] = v[c];
+        __syncthreads();
         if (threadIdx.x < POSE_VALS) {
-            double v = 0.0;
-            for (int b2 = 0; b2 < (int)gridDim.x; ++b2)
-                v += ((volatile double*)w.pose_part)[b2 * POSE_VALS + threadIdx.x];
-            if (a.pose_out) a.pose_out[threadIdx.x] = v;
+            double t = 0.0;
+            for (int k = 0; k < CHAIN_THREADS / 32; ++k) t += s_red[k][threadIdx.x];
+            if (a.pose_out) a.pose_out[threadIdx.x] = t;
         }
         if (threadIdx.x == 0) w.ctr[4] = 0;
     }
@@ -288,6 +473,7 @@ cudaError_t launch_chain(const Ws& w, const lsb_params& p, const lsb_grads& g, c
     int deg_store = 0;
     while ((deg_store + 2) * (deg_store + 2) <= p.sh_coeffs) ++deg_store;
     a.degree = s.sh_degree < deg_store ? s.sh_degree : deg_store;
+    k_chain_sums<<<8 * 148, 128, 0, st>>>(w);
     k_chain<<<CHAIN_BLOCKS, CHAIN_THREADS, 0, st>>>(w, a);
     return cudaGetLastError();
 }
