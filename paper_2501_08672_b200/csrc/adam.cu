@@ -184,16 +184,148 @@ __device__ __forceinline__ void bias_corr(const AdamArgs<PT>& a, PT& ibc1, PT& i
     }
 }
 
-// One thread per Gaussian.  PT = double steps the f64 working copy exactly
-// like the reference (optimize.py:142-188); PT = float steps the f32 arena.
+// ---- the single-GPU step as a streaming kernel ------------------------------
+// The same arithmetic as adam_gaussian, element by element over the flat
+// groups (mean | scale | opacity | sh: independent elements; rotation: per
+// Gaussian, R <- R Exp(phi)), so the loads of four elements per thread are
+// issued together and every warp access is contiguous.  An element with a
+// zero gradient and zero moments is an exact no-op (its step is -0: adding
+// it, or testing it against 0, changes nothing), so it is skipped without
+// stores - the same bits as the per-Gaussian form.  Blocks [0, eb) take the
+// elements, blocks [eb, grid) the rotations.
+constexpr int ADAM_U = 4;
+
 template <typename PT>
-__global__ void __launch_bounds__(256) k_adam(AdamArgs<PT> a) {
+__device__ __forceinline__ PT adam_step_el(const lsb_adam_cfg& c, PT ibc1, PT ibc2, PT& m, PT& v, PT G, PT lr) {
+    m = (PT)c.beta1 * m + (PT)(1.0 - c.beta1) * G;
+    v = (PT)c.beta2 * v + (PT)(1.0 - c.beta2) * G * G;
+    return -lr * (m * ibc1) / (sqrt(v * ibc2) + (PT)c.eps);
+}
+
+template <typename PT>
+__global__ void __launch_bounds__(256) k_adam_flat(AdamArgs<PT> a, int eb) {
     PT ibc1, ibc2;
     bias_corr(a, ibc1, ibc2);
-    const GradLocal gs{a.g};
-    const ParamLocal<PT> ps{a.means, a.rots, a.scales, a.opac, a.shs, a.touched};
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x)
-        adam_gaussian(a, gs, ps, i, ibc1, ibc2);
+    const int64_t n = a.n, nk = 3 * (int64_t)a.K;
+    const int64_t o_rot = 3 * n, o_scale = 6 * n, o_op = 9 * n, o_sh = 10 * n;
+    const PT* __restrict__ mm_ = a.m;
+    const float* __restrict__ g_ = a.g;
+    if ((int)blockIdx.x < eb) {
+        // element u: [0,3n) mean, [3n,6n) scale, [6n,7n) opacity, [7n, 7n + nk n) sh
+        const int64_t total = 7 * n + nk * n;
+        const int64_t stride = (int64_t)eb * blockDim.x * ADAM_U;
+        for (int64_t u0 = (int64_t)blockIdx.x * blockDim.x * ADAM_U + threadIdx.x; u0 < total; u0 += stride) {
+            int64_t gi[ADAM_U];
+            float gr[ADAM_U];
+            PT m0[ADAM_U], v0[ADAM_U], p0[ADAM_U];
+            PT* pp[ADAM_U];
+#pragma unroll
+            for (int q = 0; q < ADAM_U; ++q) {
+                const int64_t u = u0 + (int64_t)q * blockDim.x;
+                int64_t j = u;
+                PT* base = a.means;
+                gi[q] = -1;
+                if (u < 3 * n) {
+                    gi[q] = u;
+                } else if (u < 6 * n) {
+                    j = u - 3 * n;
+                    base = a.scales;
+                    gi[q] = o_scale + j;
+                } else if (u < 7 * n) {
+                    j = u - 6 * n;
+                    base = a.opac;
+                    gi[q] = o_op + j;
+                } else if (u < total) {
+                    j = u - 7 * n;
+                    base = a.shs;
+                    gi[q] = o_sh + j;
+                }
+                pp[q] = base + j;
+                if (gi[q] >= 0) {
+                    gr[q] = g_[gi[q]];
+                    m0[q] = mm_[gi[q]];
+                    v0[q] = a.v[gi[q]];
+                    p0[q] = *pp[q];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < ADAM_U; ++q) {
+                if (gi[q] < 0) continue;
+                if (gr[q] == 0.f && m0[q] == (PT)0 && v0[q] == (PT)0) continue;      // exact no-op
+                const int64_t u = u0 + (int64_t)q * blockDim.x;
+                PT mq = m0[q], vq = v0[q];
+                if (u < 3 * n) {
+                    const PT st = adam_step_el(a.c, ibc1, ibc2, mq, vq, (PT)gr[q], (PT)(a.c.lr_mean * a.c.scene_scale));
+                    *pp[q] = p0[q] + st;
+                } else if (u < 6 * n) {
+                    const PT s = p0[q];
+                    const PT st = adam_step_el(a.c, ibc1, ibc2, mq, vq, (PT)gr[q] * s, (PT)a.c.lr_scale);
+                    const PT fl = (PT)a.c.scale_floor;
+                    if (st != (PT)0) *pp[q] = fmax(exp(log(fmax(s, fl)) + st), fl);
+                } else if (u < 7 * n) {
+                    const PT oclip = (PT)a.c.opacity_clip;
+                    const PT oc = fmin(fmax(p0[q], oclip), (PT)1 - oclip);
+                    const PT st = adam_step_el(a.c, ibc1, ibc2, mq, vq, (PT)gr[q] * oc * ((PT)1 - oc),
+                                               (PT)a.c.lr_opacity);
+                    if (st != (PT)0) *pp[q] = (PT)1 / ((PT)1 + exp(-(log(oc / ((PT)1 - oc)) + st)));
+                } else {
+                    const PT st = adam_step_el(a.c, ibc1, ibc2, mq, vq, (PT)gr[q], (PT)a.c.lr_sh);
+                    *pp[q] = p0[q] + st;
+                }
+                a.m[gi[q]] = mq;
+                a.v[gi[q]] = vq;
+            }
+        }
+        return;
+    }
+    // rotations: R <- R Exp(phi) on rows with phi != 0 (optimize.py:172-176)
+    const int64_t rstride = (int64_t)(gridDim.x - eb) * blockDim.x;
+    for (int64_t i = (int64_t)(blockIdx.x - eb) * blockDim.x + threadIdx.x; i < n; i += rstride) {
+        float gr[3];
+        PT m0[3], v0[3];
+        bool idle = true;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            gr[k] = g_[o_rot + 3 * i + k];
+            m0[k] = mm_[o_rot + 3 * i + k];
+            v0[k] = a.v[o_rot + 3 * i + k];
+            idle = idle && gr[k] == 0.f && m0[k] == (PT)0 && v0[k] == (PT)0;
+        }
+        if (idle) continue;
+        PT phi[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            phi[k] = adam_step_el(a.c, ibc1, ibc2, m0[k], v0[k], (PT)gr[k], (PT)a.c.lr_rot);
+            a.m[o_rot + 3 * i + k] = m0[k];
+            a.v[o_rot + 3 * i + k] = v0[k];
+        }
+        if (phi[0] != (PT)0 || phi[1] != (PT)0 || phi[2] != (PT)0) {
+            const double p0 = phi[0], p1 = phi[1], p2 = phi[2];
+            const double th = sqrt(p0 * p0 + p1 * p1 + p2 * p2);
+            const bool small = th < 1e-8;
+            const double ca = small ? 1.0 : sin(th) / th;
+            const double cb = small ? 0.5 : (1.0 - cos(th)) / (th * th);
+            const double S[9] = {0.0, -p2, p1, p2, 0.0, -p0, -p1, p0, 0.0};
+            double E[9];
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const double s2 = S[3 * r] * S[c] + S[3 * r + 1] * S[3 + c] + S[3 * r + 2] * S[6 + c];
+                    E[3 * r + c] = (r == c ? 1.0 : 0.0) + ca * S[3 * r + c] + cb * s2;
+                }
+            PT* R = a.rots + 9 * i;
+            double Rd[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) Rd[k] = R[k];
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    R[3 * r + c] = (PT)(Rd[3 * r] * E[c] + Rd[3 * r + 1] * E[3 + c] + Rd[3 * r + 2] * E[6 + c]);
+            a.touched[i] = 1;
+        }
+    }
 }
 
 // Fused multi-GPU step over NVLink peer memory (one kernel per rank): for the
@@ -253,7 +385,15 @@ static cudaError_t adam_t(const lsb_params& p, const float* g, void* m, void* v,
         a.ibc1 = (PT)(1.0 / (1.0 - pow(c.beta1, (double)c.step)));
         a.ibc2 = (PT)(1.0 / (1.0 - pow(c.beta2, (double)c.step)));
     }
-    if (p.n > 0) k_adam<PT><<<grid_of(p.n), 256, 0, st>>>(a);
+    if (p.n > 0) {
+        // element blocks (~ADAM_U elements per thread, one wave of 148 x 8 CTAs at most) + rotation blocks
+        const int64_t total = (7 + 3 * (int64_t)p.sh_coeffs) * p.n;
+        int64_t eb = (total + 256 * ADAM_U - 1) / (256 * ADAM_U);
+        eb = eb < 148 * 6 ? eb : 148 * 6;
+        int64_t rb = (p.n + 255) / 256;
+        rb = rb < 148 * 2 ? rb : 148 * 2;
+        k_adam_flat<PT><<<(unsigned)(eb + rb), 256, 0, st>>>(a, (int)eb);
+    }
     if (step_dev) k_step_bump<<<1, 1, 0, st>>>(step_dev);
     return cudaGetLastError();
 }
