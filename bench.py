@@ -575,6 +575,21 @@ def run_voxel(args, rank, world, local_rank):
     assert int(m.flags.item()) == 0, "voxel table overflow"
     leaves, fov = int(m.n_used.item()), int(n_out.item())
     total_pts = sum(n_pts)
+    # byte model: 12 n_pts + 168 g + 8 n_fov per frame, g the
+    # leaves a frame's scan touches (key 8 + statistics read-modify-write 2 x 80)
+    # and n_fov the FoV leaves it lists - counted in an untimed replay
+    from paper_2501_08672_b200.sort import segments, sort_pairs
+    from paper_2501_08672_b200.voxmap import keys_of_points_dev
+    from paper_2501_08672_b200.window import order_keys
+    rep = HashOctree(VOXEL_CFG["root_len"], VOXEL_CFG["max_level"], capacity=1 << 23, device=dev)
+    g_tot, fov_tot = 0, 0
+    for f in range(F):
+        g_tot += int(segments(sort_pairs(order_keys(keys_of_points_dev(scans[f], rep.leaf_len, dev)), key_bits=63,
+                                         signed=False)[0]).numel())
+        fov_tot += int(run(rep, [f]).item())
+    vox_bytes = 12 * total_pts + 168 * g_tot + 8 * fov_tot
+    hbm, hbm_src = peaks()
+    vox_gbs = vox_bytes / (ms * 1e-3) / 1e9
     # CPU baseline: the oracle's dict map on the first frames of the same scans
     from oracle.voxmap import Map
     om = Map(VOXEL_CFG["root_len"], VOXEL_CFG["max_level"])
@@ -595,7 +610,16 @@ def run_voxel(args, rank, world, local_rank):
             "data": "synthetic", "config": {"workload": "cfg3", "frames": F, "points_per_frame": int(np.mean(n_pts)),
                                             "root_len": VOXEL_CFG["root_len"], "max_level": VOXEL_CFG["max_level"],
                                             "leaves_after": leaves, "fov_leaves_last": fov},
-            "clocks": clk.summary(), "gpu_launches": F * 6,
+            "clocks": clk.summary(),
+            # per frame: insert, slot keys, 3 radix passes x 3, segments x 3, run sums; claim / commit x 2;
+            # FoV roots + leaves
+            "gpu_launches": F * 20,
+            "roofline": {"bound": "hbm", "kernel": "whole frame (accumulate + try_insert + FoV)",
+                         "achieved": vox_gbs, "peak": hbm, "peak_source": hbm_src, "unit": "GB/s",
+                         "frac": vox_gbs / hbm, "traffic": None,
+                         "algorithmic_bytes_per_frame": vox_bytes / F,
+                         "model": "SURVEY.md §8(d): 12 n_pts + 168 g + 8 n_fov per frame",
+                         "g_per_frame": g_tot / F, "n_fov_per_frame": fov_tot / F},
             "cpu_baseline": {"value": int(np.mean(n_pts[:nb])) / t_cpu / 1e6, "unit": "Mpts/s", "cores": 1,
                              "kind": "port", "sample": f"{nb} frames on the oracle's dict map"},
         }), flush=True)
@@ -655,6 +679,7 @@ def run_window(args, rank, world, local_rank):
         times, reps = walk(GaussianWindow(WINDOW_CFG["capacity"], K, device=dev), range(F))
     ms = float(np.median(times)) * 1e3
     fov_avg = float(np.mean([f.shape[0] for f in fovs]))
+    win_bytes = 16 * fov_avg + 152 * float(np.mean([r.removed + r.moved + r.added for r in reps[1:]]))
     # CPU baseline: the oracle restatement (dict map) on the first frames
     from oracle.window import Window
     store = {tuple(int(v) for v in k): r for k, r in zip(keys.cpu().numpy(), rows.cpu().numpy())}
@@ -680,6 +705,13 @@ def run_window(args, rank, world, local_rank):
                        "dropped_avg": float(np.mean([r.dropped for r in reps[1:]])),
                        "timing": "host wall clock per maintain (synchronised), median over frames"},
             "clocks": clk.summary(),
+            "roofline": {"bound": "hbm", "kernel": "maintain (diff, write-back, compaction, append)", "unit": "GB/s",
+                         "achieved": win_bytes / (ms * 1e-3) / 1e9, "peak": peaks()[0], "peak_source": peaks()[1],
+                         "frac": win_bytes / (ms * 1e-3) / 1e9 / peaks()[0], "traffic": None,
+                         "algorithmic_bytes_per_frame": win_bytes,
+                         "model": "16 n_fov (FoV keys in, diff marks) + 152 (removed + moved + added) (f32 row "
+                                  "read + write)",
+                         "note": "a few host syncs per frame (counts): latency bound"},
             "cpu_baseline": {"value": float(np.median(t_cpu)) * 1e3, "unit": "ms/frame", "cores": 1, "kind": "port",
                              "sample": f"first {nb} frames on the oracle restatement (dict map)"},
         }), flush=True)
@@ -739,6 +771,11 @@ def run_lidar(args, rank, world, local_rank):
             "metric": "LiDAR point-to-plane rows + H/b, Mpts/s (SURVEY.md §8(f) rank 2)", "value": n / (ms * 1e-3) / 1e6,
             "unit": "Mpts/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "replicas", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "roofline": {"bound": "hbm", "kernel": "measurement + H/b", "unit": "GB/s",
+                         "achieved": 640 * n / (ms * 1e-3) / 1e9, "peak": peaks()[0], "peak_source": peaks()[1],
+                         "frac": 640 * n / (ms * 1e-3) / 1e9 / peaks()[0], "traffic": None,
+                         "model": "640 B per scan point: point 24 + 7 leaf statistics x 80 + z / row 56",
+                         "note": "host-synchronised measurement (one read-back): latency bound"},
             "config": {"workload": "lidar", "scan_points": n, "rows_kept": int(len(meas.z)), "root_len": 0.1,
                        "max_level": 3, "map_scans": 20,
                        "timing": "host wall clock per measurement + device H/b (synchronised), median"},
@@ -786,12 +823,59 @@ def run_ieskf(args, rank, world, local_rank):
             times.append(time.perf_counter() - t0)
     ms = float(np.median(times)) * 1e3
     err_t = float(np.abs(post.T_WI.t - T_wi.t).max())
+    # per-iteration bytes: the render at the estimate (preprocess + binning + the
+    # counted forward, f32 parameters and f32 observed frame), the semi-dense
+    # selection (observed + T) and the pose rows / H-b (selected pixels' tile
+    # lists are a small fraction); counts from one render at the prior
+    from paper_2501_08672_b200.raster import render as _render
+    T_wc0 = prior.T_WI @ T_IC
+    out0 = _render(arrays, T_wc0, cam, st, bin_mode=1)
+    M0, I0 = out0.cache.counts[0], out0.cache.counts[1]
+    ab = algorithmic_bytes(len(means), int(shs.shape[1]), M0, I0, 1280 * 1024, pbytes=4, obytes=4)
+    it_bytes = ab["bin"] + ab["blend_fwd"] + 1280 * 1024 * (12 + 4)
+    hbm, hbm_src = peaks()
+    it_gbs = it_bytes / (ms * 1e-3 / iters) / 1e9
+    # CPU baseline: one iteration of the reference's steps on the oracle port
+    # (render at the prior, Sobel selection, residual gate, pose rows, H^T R^-1 H)
+    cpu = None
+    if not args.no_cpu_baseline:
+        from types import SimpleNamespace
+        from scipy import ndimage
+        from oracle import raster as orc
+        f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)
+        P = {"means": f32(means), "rots": f32(rots), "scales": f32(scales), "opacities": f32(opac), "shs": f32(shs)}
+        ost = SimpleNamespace(near=0.01, dilation=0.3, alpha_clamp=0.99, transmittance_min=1e-4, footprint_sigma=6.0,
+                              alpha_cut=args.alpha_cut, max_footprint_px=512.0, background=np.zeros(3), sh_degree=0)
+        obs = observed.cpu().numpy().astype(np.float64)
+        t0 = time.perf_counter()
+        T_cw = T_wc0.inverse()
+        ref = orc.render(P, T_cw.R, T_cw.t, cam, ost)
+        gray = obs.mean(axis=2)
+        mag = np.hypot(ndimage.sobel(gray, axis=1, mode="nearest") / 8.0,
+                       ndimage.sobel(gray, axis=0, mode="nearest") / 8.0)
+        ids = np.flatnonzero((mag > fcfg.grad_threshold) & (ref["t_final"].reshape(1024, 1280) <
+                                                            fcfg.coverage_max_transmittance))
+        if len(ids) > fcfg.pixel_budget:
+            ids = ids[np.unique(np.round(np.linspace(0, len(ids) - 1, fcfg.pixel_budget)).astype(int))]
+        res = gray.reshape(-1)[ids] - ref["image"].reshape(-1, 3)[ids].mean(axis=1)
+        keep = np.abs(res) <= fcfg.photo_gate
+        H = -orc.pose_rows(ref, ids[keep], T_IC.R, T_IC.t)
+        _ = H.T @ H, H.T @ res[keep]
+        t_it = time.perf_counter() - t0
+        cpu = {"value": 1.0 / t_it, "unit": "iterations/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"one IESKF iteration's measurement (render at the prior, selection, {int(keep.sum())} pose "
+                         f"rows, H/b) on the oracle port ({t_it:.2f} s); the 15x15 algebra excluded"}
     if rank == 0:
         print(json.dumps({
             "metric": "IESKF photometric update iterations/s (config 4)", "value": iters / (ms * 1e-3),
             "unit": "iterations/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "replicas", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
+            "roofline": {"bound": "hbm", "kernel": "one iteration (render + selection + pose rows + H/b)",
+                         "achieved": it_gbs, "peak": hbm, "peak_source": hbm_src, "unit": "GB/s",
+                         "frac": it_gbs / hbm, "traffic": None, "algorithmic_bytes_per_iteration": it_bytes,
+                         "note": "host-synchronised filter iterations: latency bound, not bandwidth bound"},
+            "cpu_baseline": cpu,
             "config": {"workload": "cfg4", "gaussians": len(means), "width": 1280, "height": 1024,
                        "iterations": iters, "alpha_cut": args.alpha_cut,
                        "timing": "host wall clock per full update (includes the per-iteration host syncs "
