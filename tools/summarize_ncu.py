@@ -1,6 +1,6 @@
 """Summarise ncu reports and launch lists into profiles/ (text, committed).
 
-    python tools/summarize_ncu.py TAG            # reads gpurun_out/prof_TAG_*.ncu-rep,
+    python tools/summarize_ncu.py TAG [WORKLOAD] # reads gpurun_out/prof_TAG_*.ncu-rep,
                                                  # gpurun_out/launches_TAG.csv
 Writes profiles/TAG_kernels.md, profiles/TAG_launches.csv (copy) and updates
 profiles/traffic.json (dram bytes per launch of each profiled kernel, read by
@@ -36,9 +36,11 @@ METRICS = [
     ("gpc__cycles_elapsed.max", "elapsed_cyc"),
 ]
 
-KEY = {"k_blend_fused": "blend", "k_blend_bwd": "blend_bwd", "k_blend_fwd": "blend_fwd", "k_preprocess": "bin", "k_pre_count": "bin",
-       "k_chain": "chain",
-       "k_adam": "adam", "k_tile_sort": "bin"}
+# ncu kernel -> bench.py kernel group; figures are summed over a group's kernels
+KEY = {"k_blend_fused": "blend", "k_blend_bwd": "blend_bwd", "k_blend_fwd": "blend_fwd",
+       "k_pre_count": "bin", "k_pre_scan": "bin", "k_pre_emit": "bin", "k_scan_tiles": "bin",
+       "k_scatter_emitted": "bin", "k_tile_sort": "bin", "k_tile_sort_big": "bin",
+       "k_chain_sums": "chain", "k_chain": "chain", "k_adam": "adam", "k_adam_flat": "adam"}
 
 
 def raw(rep):
@@ -74,17 +76,18 @@ def raw(rep):
     return res
 
 
-def main(tag):
+def main(tag, workload):
     os.makedirs(PROF, exist_ok=True)
     lines = [f"# ncu summary, {tag}", "",
              "One `ncu --set full --clock-control none` capture per kernel of `python bench.py --steps 2 --warmup 1`",
-             "(config 2 view; cold-cache, serialised replay: compare shares, not absolute times).", "",
+             f"(workload `{workload}`; cold-cache, serialised replay: compare shares, not absolute times).", "",
              "| kernel | dur (us) | DRAM rd+wr (MB) | DRAM % | warp inst (M) | issue-active % (elapsed) | FMA pipe % | occupancy % | regs | SM active / elapsed |",
              "|---|---|---|---|---|---|---|---|---|---|"]
     traffic_path = os.path.join(PROF, "traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
     issue_path = os.path.join(PROF, "issue.json")
     issue = json.load(open(issue_path)) if os.path.exists(issue_path) else {}
+    sums = {}
     for rep in sorted(glob.glob(os.path.join(OUT, f"prof_{tag}_*.ncu-rep"))):
         for d in raw(rep):
             name = d["kernel"].replace("void ", "").split("(")[0].split("::")[-1].split("<")[0]
@@ -93,9 +96,16 @@ def main(tag):
                          f"{d.get('warp_inst', 0) / 1e6:.1f} | {d.get('issue_active_%', 0):.1f} | "
                          f"{d.get('fma_pipe_%', 0):.1f} | {d.get('occupancy_%', 0):.1f} | {d.get('regs', 0):.0f} | "
                          f"{d.get('sm_active_cyc', 0) / max(d.get('elapsed_cyc', 1), 1):.2f} |")
-            if name in KEY and name != "k_tile_sort":
-                traffic[KEY[name]] = tb
-                issue[KEY[name]] = {"warp_inst_per_launch": d.get("warp_inst", 0), "capture": tag}
+            if name in KEY:
+                grp = KEY[name]
+                sums.setdefault(grp, {"traffic": 0.0, "inst": 0.0, "kernels": []})
+                sums[grp]["traffic"] += tb
+                sums[grp]["inst"] += d.get("warp_inst", 0)
+                sums[grp]["kernels"].append(name)
+    tw, iw = traffic.setdefault(workload, {}), issue.setdefault(workload, {})
+    for grp, v in sums.items():
+        tw[grp] = v["traffic"]
+        iw[grp] = {"warp_inst_per_launch": v["inst"], "capture": tag, "kernels": sorted(v["kernels"])}
     open(os.path.join(PROF, f"{tag}_kernels.md"), "w").write("\n".join(lines) + "\n")
     json.dump(traffic, open(traffic_path, "w"), indent=1)
     json.dump(issue, open(issue_path, "w"), indent=1)
@@ -122,4 +132,4 @@ def main(tag):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "cfg2")
