@@ -51,6 +51,9 @@ namespace lsb {
 #ifndef LSB_WPB
 #define LSB_WPB 4
 #endif
+#ifndef LSB_BLEND_PRIO
+#define LSB_BLEND_PRIO 0      // launch the fused blend at the greatest priority (cudaLaunchAttributePriority)
+#endif
 #ifndef FUSED_RESERVE
 #define FUSED_RESERVE 1      // CTA slots per SM the fused blend leaves to the other lanes
 #endif
@@ -530,13 +533,79 @@ __device__ __forceinline__ void bwd_half(const Frame& f, float4 q1, bool rin, fl
     M[5] = fmaf(S0 * dy, dy, M[5]);
 }
 
+#ifndef LSB_SMEM_RED
+#define LSB_SMEM_RED 1
+#endif
+// Deferred screen-partial reduction (LSB_SMEM_RED): per record every lane
+// parks its 9 raw sums (colour x3, moments x6) in shared memory (3 x 16 B,
+// conflict-free), and every RED_RB records the warp reduces them at once:
+// lanes 8r..8r+7 own record r of the group, lane sub adds the source lanes
+// sub, sub+8, sub+16, sub+24 (LDS.128, one bank group per lane of a
+// quarter-warp) and a 3-level butterfly finishes the sum — a fixed tree, so
+// deterministic.  The moments -> conic-space map is linear with per-record
+// coefficients, so it is applied once to the sums.  Per record this costs
+// ~25 warp instructions instead of ~90 for a per-record 9-value
+// transpose-reduce.
+constexpr int RED_RB = 4;                      // records per deferred reduction
+constexpr int RED_F4 = 3;                      // float4 per lane and record
+
+__device__ __forceinline__ void red_park(float4* buf, int slot, int lane, const float* c, const float* M) {
+    float4* d = buf + (slot * 32 + lane) * RED_F4;
+    d[0] = make_float4(c[0], c[1], c[2], M[0]);
+    d[1] = make_float4(M[1], M[2], M[3], M[4]);
+    d[2] = make_float4(M[5], 0.f, 0.f, 0.f);
+}
+
+// Reduce the `n` parked records (group starting at batch record kb) and
+// write their 9 partials per intersection.
+__device__ __forceinline__ void red_flush(const Ws& w, const BlendArgs& a, const float4* buf, const Rec* sr, int kb,
+                                          int n, int ecur, int lane) {
+    __syncwarp();
+    const int r = lane >> 3, sub = lane & 7;
+    float t[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) t[q] = 0.f;
+    if (r < n) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float4* sp = buf + (r * 32 + sub + 8 * j) * RED_F4;
+            const float4 x0 = sp[0], x1 = sp[1], x2 = sp[2];
+            t[0] += x0.x; t[1] += x0.y; t[2] += x0.z; t[3] += x0.w;
+            t[4] += x1.x; t[5] += x1.y; t[6] += x1.z; t[7] += x1.w;
+            t[8] += x2.x;
+        }
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < 9; ++q) t[q] += __shfl_xor_sync(0xffffffffu, t[q], o);
+    const int e = __shfl_sync(0xffffffffu, ecur, kb + (r < n ? r : 0));
+    __syncwarp();                                  // the buffer may be refilled from here
+    if (r >= n) return;
+    const float4 q1 = *(const float4*)&sr[kb + r].A;     // A s E lop
+    const float k2 = -2.0f / (float)LOG2E;
+    const float ak = q1.x * k2, ek = q1.z * k2, sa = q1.y * ak;
+    // moments -> conic-space sums, v0 = a_k u, v1 = s v0 + e dy (all
+    // candidates, then a select tree: no divergent branches)
+    const float c01 = (sub & 1) ? t[1] : t[0];
+    const float c23 = (sub & 1) ? t[3] * (a.ik * ex2_approx(-q1.w)) : t[2];     // 1/op
+    const float v45 = (sub & 1) ? fmaf(sa, t[4], ek * t[5]) : ak * t[4];
+    const float v67 = 0.5f * ((sub & 1) ? ak * fmaf(sa, t[6], ek * t[7]) : ak * ak * t[6]);
+    const float lo = (sub & 2) ? c23 : c01, hi = (sub & 2) ? v67 : v45;
+    const float v = (sub & 4) ? hi : (sub < 3 ? lo * a.clamp : lo);
+    float* dst = w.part + (int64_t)e * NUM_PART;
+    dst[sub] = v;
+    if (sub == 0) dst[8] = 0.5f * fmaf(sa * sa, t[6], fmaf(2.f * sa * ek, t[7], ek * ek * t[8]));
+}
+
 // The backward's record walk over one tile's list [start, end): the forward
 // recomputed per pixel (same instruction sequence as the forward, so T is
 // bit-identical), per-record screen partials reduced across the warp and
 // written per intersection; entries the walk never reaches get zeros.
-__device__ __forceinline__ void bwd_walk(const Ws& w, const BlendArgs& a, RecPipe& pipe, int tile, int start,
-                                         int end, int gx0, int gy0, float (&T)[2][RUN], float (&gD)[2][RUN],
-                                         float (&Gr)[2][RUN], float (&Gg)[2][RUN], float (&Gb)[2][RUN], int lane) {
+__device__ __forceinline__ void bwd_walk(const Ws& w, const BlendArgs& a, RecPipe& pipe, float4* red, int tile,
+                                         int start, int end, int gx0, int gy0, float (&T)[2][RUN],
+                                         float (&gD)[2][RUN], float (&Gr)[2][RUN], float (&Gg)[2][RUN],
+                                         float (&Gb)[2][RUN], int lane) {
     const float k2 = -2.0f / (float)LOG2E;     // undo the exp2 scaling: a_k = A k2, e = E k2
     const float kap = a.clamp;
     const float gx0f = (float)gx0, gy0f = (float)gy0;
@@ -590,6 +659,12 @@ __device__ __forceinline__ void bwd_walk(const Ws& w, const BlendArgs& a, RecPip
                                     M);
                 }
             }
+#if LSB_SMEM_RED
+            (void)wover;
+            red_park(red, k & (RED_RB - 1), lane, c, M);
+            if ((k & (RED_RB - 1)) == RED_RB - 1 || k == nb - 1)
+                red_flush(w, a, red, sr, k & ~(RED_RB - 1), (k & (RED_RB - 1)) + 1, ecur, lane);
+#else
             float val = 0.f;
             if (wover) {
                 // moments -> conic-space sums with v0 = a_k u, v1 = s v0 + e dy
@@ -615,6 +690,7 @@ __device__ __forceinline__ void bwd_walk(const Ws& w, const BlendArgs& a, RecPip
             }
             const int e = __shfl_sync(0xffffffffu, ecur, k);
             if (lane < NUM_PART) w.part[(int64_t)e * NUM_PART + lane] = val;
+#endif
         }
         __syncwarp();
     }
@@ -630,6 +706,7 @@ __global__ void __launch_bounds__(32 * WPB, BWD_MIN_BLOCKS)
 k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __restrict__ gimg, float gscale,
             LossArgs L) {
     __shared__ Rec s_rec[WPB][2 * 32];
+    __shared__ float4 s_red[WPB][LSB_SMEM_RED ? RED_RB * 32 * RED_F4 : 1];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int qx = (lane & 3) * RUN, r0 = lane >> 2;
     RecPipe pipe;
@@ -702,7 +779,8 @@ k_blend_bwd(Ws w, BlendArgs a, const float* __restrict__ image, const float* __r
                 L.sums[2 * tile + 1] = l1;
             }
         }
-        bwd_walk(w, a, pipe, tile, w.tile_start[tile], w.tile_last[tile], gx0, gy0, T, gD, Gr, Gg, Gb, lane);
+        bwd_walk(w, a, pipe, s_red[wib], tile, w.tile_start[tile], w.tile_last[tile], gx0, gy0, T, gD, Gr, Gg, Gb,
+                 lane);
     }
 }
 
@@ -742,6 +820,7 @@ template <bool CUT>
 __global__ void __launch_bounds__(32 * WPB, BWD_MIN_BLOCKS)
 k_blend_fused(Ws w, BlendArgs a, LossArgs L) {
     __shared__ Rec s_rec[WPB][2 * 32];
+    __shared__ float4 s_red[WPB][LSB_SMEM_RED ? RED_RB * 32 * RED_F4 : 1];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int qx = (lane & 3) * RUN, r0 = lane >> 2;
     RecPipe pipe;
@@ -856,7 +935,7 @@ k_blend_fused(Ws w, BlendArgs a, LossArgs L) {
             L.sums[2 * tile + 1] = l1;
         }
         // ---- backward ----
-        bwd_walk(w, a, pipe, tile, start, last, gx0, gy0, T, gD, Gr, Gg, Gb, lane);
+        bwd_walk(w, a, pipe, s_red[wib], tile, start, last, gx0, gy0, T, gD, Gr, Gg, Gb, lane);
     }
 }
 
@@ -869,10 +948,34 @@ cudaError_t launch_blend_fused(const Ws& w, const lsb_settings& s, int W, int H,
                      nullptr,  kind & 0xff, grad_scale,  (kind & LSB_OBS_U8) != 0};
     const void* fn = s.alpha_cut > 0.0 ? (const void*)k_blend_fused<true> : (const void*)k_blend_fused<false>;
     const int grid = persistent_grid(fn, w.ntiles, FUSED_RESERVE);
+#if LSB_BLEND_PRIO
+    // the blend (the step's throughput-limiting kernel) at the device's
+    // greatest priority: its CTAs are dispatched ahead of the other lanes'
+    // binning / chain CTAs as SM slots free up
+    {
+        int least = 0, greatest = 0;
+        cudaDeviceGetStreamPriorityRange(&least, &greatest);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(32 * WPB);
+        cfg.stream = st;
+        cudaLaunchAttribute at{};
+        at.id = cudaLaunchAttributePriority;
+        at.val.priority = greatest;
+        cfg.attrs = &at;
+        cfg.numAttrs = 1;
+        if (s.alpha_cut > 0.0)
+            e = cudaLaunchKernelEx(&cfg, k_blend_fused<true>, w, a, L);
+        else
+            e = cudaLaunchKernelEx(&cfg, k_blend_fused<false>, w, a, L);
+        if (e != cudaSuccess) return e;
+    }
+#else
     if (s.alpha_cut > 0.0)
         k_blend_fused<true><<<grid, 32 * WPB, 0, st>>>(w, a, L);
     else
         k_blend_fused<false><<<grid, 32 * WPB, 0, st>>>(w, a, L);
+#endif
     k_loss_total<<<1, LT_THREADS, 0, st>>>(w.ntiles, w.loss_part, loss_out);
     return cudaGetLastError();
 }

@@ -81,7 +81,7 @@ __device__ void sh_basis_grad_d(int degree, T x, T y, T z, T (*g)[3]) {
 // ---- partial sums: a balanced segmented reduction over the intersections ----
 // Intersections are splat-major (a splat's run is [vis_ebase[s],
 // vis_ebase[s + 1]); emit_slot[e] names its splat).  One warp per chunk of
-// CHAIN_CH = 256 intersections, lane l taking 8 consecutive ones (18 float4
+// CHAIN_CH = 128 intersections, lane l taking 4 consecutive ones (9 float4
 // loads): each lane sums its runs locally in f64, then one segmented warp
 // scan (fixed shape) stitches the runs that cross lanes.  A run closed inside
 // the chunk is written back in f64 over its own first two partials (72 B of
@@ -90,7 +90,6 @@ __device__ void sh_basis_grad_d(int degree, T x, T y, T z, T (*g)[3]) {
 // when it continues in a later one, go to chain_carry[chunk] (first / last),
 // which k_chain adds chunk by chunk in order.  Every sum has a fixed shape:
 // deterministic, balanced however long a splat's run is, no atomics.
-constexpr int CHAIN_CH = 256;
 constexpr int CHAIN_PER_LANE = CHAIN_CH / 32;
 
 __device__ __forceinline__ void store_f64x9(float* dst, const double* v) {
@@ -234,34 +233,23 @@ __global__ void __launch_bounds__(128) k_chain_sums(Ws w) {
     }
 }
 
-// The partial sums of splat `slot` (after k_chain_sums).
-__device__ __forceinline__ bool chain_q(const Ws& w, int64_t slot, double* q) {
-    const int64_t e0 = w.vis_ebase[slot], e1 = w.vis_ebase[slot + 1];
-    if (e1 <= e0) return false;
-    const int64_t c0 = e0 / CHAIN_CH, c1 = (e1 - 1) / CHAIN_CH;
-    if (c0 == c1) {
-        const float* p = w.part + e0 * NUM_PART;
-        if (e1 - e0 == 1) {
-#pragma unroll
-            for (int k = 0; k < NUM_PART; ++k) q[k] = (double)p[k];
-        } else {
-#pragma unroll
-            for (int k = 0; k < NUM_PART; ++k) q[k] = load_f64(p, k);
-        }
-        return true;
-    }
-    const double* cr = w.chain_carry;
-#pragma unroll
-    for (int k = 0; k < NUM_PART; ++k) q[k] = cr[(size_t)c0 * 2 * NUM_PART + NUM_PART + k];
-    for (int64_t c = c0 + 1; c <= c1; ++c)
-#pragma unroll
-        for (int k = 0; k < NUM_PART; ++k) q[k] += cr[(size_t)c * 2 * NUM_PART + k];
-    return true;
-}
-
 using CT = double;  // chain-rule arithmetic: f64 keeps Adam's sign-sensitive first steps on the reference trajectory
 
+// Parameter load from an f32 / f64 arena, widened to f64 (F64 fixed at compile time).
+template <int F64>
+__device__ __forceinline__ double tld(const void* p, int64_t i) {
+    return F64 ? __ldg((const double*)p + i) : (double)__ldg((const float*)p + i);
+}
+
+// One thread per visible splat.  The thread's loads are issued in two waves
+// (record header / intersection range / colour mask, then the splat's
+// parameters, its current gradient rows and its partial sums together), so
+// a splat costs two dependent memory round trips before its arithmetic
+// instead of one per load; SH degree and arena dtype are template
+// parameters, so the SH basis and its gradient stay in registers.
+template <int DEG, int F64, bool POSE>
 __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
+    constexpr int KK = (DEG + 1) * (DEG + 1);
     __shared__ double s_red[CHAIN_THREADS / 32][POSE_VALS];
     __shared__ bool s_last;
     const int64_t M = (int64_t)w.ctr[0];
@@ -270,30 +258,72 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
     double pose[POSE_VALS];
 #pragma unroll
     for (int c = 0; c < POSE_VALS; ++c) pose[c] = 0.0;
+    const int K = a.p.sh_coeffs;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; slot < M; slot += stride) {
-        const Rec& r = w.rec[slot];
-        if (r.ebase < 0) continue;
+        // ---- wave 1: the record header, the intersection range, the colour mask ----
+        const int2 ie = *(const int2*)&w.rec[slot].id;           // id, ebase
+        const int64_t e0 = w.vis_ebase[slot], e1 = w.vis_ebase[slot + 1];
+        const uint32_t cm = w.colmask[slot];
+        if (ie.y < 0 || e1 <= e0) continue;
+        const int64_t i = ie.x;
+        // ---- wave 2: parameters, gradient rows, partial sums ----
+        const double px = tld<F64>(a.p.means, 3 * i), py = tld<F64>(a.p.means, 3 * i + 1),
+                     pz = tld<F64>(a.p.means, 3 * i + 2);
+        CT Rg[9], S[3];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) Rg[k] = tld<F64>(a.p.rots, 9 * i + k);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) S[k] = tld<F64>(a.p.scales, 3 * i + k);
+        const int64_t sho = i * K * 3;
+        CT shv[DEG >= 1 ? KK * 3 : 1];
+        if (DEG >= 1) {
+#pragma unroll
+            for (int k = 0; k < KK * 3; ++k) shv[k] = tld<F64>(a.p.shs, sho + k);
+        }
+        float gm[3], gr[3], gs[3], gsh[KK * 3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            gm[k] = a.g.mean[3 * i + k];
+            gr[k] = a.g.rot[3 * i + k];
+            gs[k] = a.g.scale[3 * i + k];
+        }
+        const float go = a.g.opacity[i];
+#pragma unroll
+        for (int k = 0; k < KK * 3; ++k) gsh[k] = a.g.sh[sho + k];
         double q[NUM_PART];
-        if (!chain_q(w, slot, q)) continue;
+        {
+            const int64_t c0 = e0 / CHAIN_CH, c1 = (e1 - 1) / CHAIN_CH;
+            if (c0 == c1) {
+                const float* p = w.part + e0 * NUM_PART;
+                if (e1 - e0 == 1) {
+#pragma unroll
+                    for (int k = 0; k < NUM_PART; ++k) q[k] = (double)p[k];
+                } else {
+#pragma unroll
+                    for (int k = 0; k < NUM_PART; ++k) q[k] = load_f64(p, k);
+                }
+            } else {
+                const double* cr = w.chain_carry;
+#pragma unroll
+                for (int k = 0; k < NUM_PART; ++k) q[k] = cr[(size_t)c0 * 2 * NUM_PART + NUM_PART + k];
+                for (int64_t c = c0 + 1; c <= c1; ++c)
+#pragma unroll
+                    for (int k = 0; k < NUM_PART; ++k) q[k] += cr[(size_t)c * 2 * NUM_PART + k];
+            }
+        }
         bool nz = false;
 #pragma unroll
         for (int c = 0; c < NUM_PART; ++c) nz |= (q[c] != 0.0);
         if (!nz) continue;
-        const int64_t i = r.id;
         // ---- recompute the forward geometry in f64 ----
-        const int f64 = a.p.dtype;
-        const double px = pld(a.p.means, 3 * i, f64), py = pld(a.p.means, 3 * i + 1, f64),
-                     pz = pld(a.p.means, 3 * i + 2, f64);
         const CT x = (CT)(R[0] * px + R[1] * py + R[2] * pz + a.T.t[0]);
         const CT y = (CT)(R[3] * px + R[4] * py + R[5] * pz + a.T.t[1]);
         const CT z = (CT)(R[6] * px + R[7] * py + R[8] * pz + a.T.t[2]);
         const CT fx = a.cam.fx, fy = a.cam.fy;
         const CT J00 = fx / z, J02 = -fx * x / (z * z);
         const CT J11 = fy / z, J12 = -fy * y / (z * z);
-        CT Rg[9], S[3], B[9], Wc[9];
-        for (int k = 0; k < 9; ++k) Rg[k] = pld(a.p.rots, 9 * i + k, f64);
-        for (int k = 0; k < 3; ++k) S[k] = pld(a.p.scales, 3 * i + k, f64);
+        CT B[9], Wc[9];
         for (int r3 = 0; r3 < 3; ++r3)
             for (int c3 = 0; c3 < 3; ++c3) B[3 * r3 + c3] = Rg[3 * r3 + c3] * S[c3];
         for (int r3 = 0; r3 < 3; ++r3)
@@ -357,7 +387,6 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
         for (int c3 = 0; c3 < 3; ++c3)
             dscale[c3] = Rg[c3] * dB[c3] + Rg[3 + c3] * dB[3 + c3] + Rg[6 + c3] * dB[6 + c3];
         // ---- appearance ----
-        const uint32_t cm = w.colmask[slot];
         const CT dcol[3] = {(cm & 1u) ? (CT)q[0] : 0.0f, (cm & 2u) ? (CT)q[1] : 0.0f, (cm & 4u) ? (CT)q[2] : 0.0f};
         const double* cc3 = a.T.cam_center;
         const CT dvx = px - cc3[0], dvy = py - cc3[1], dvz = pz - cc3[2];
@@ -368,21 +397,20 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
             dx_ = dvx / inv; dy_ = dvy / inv; dz_ = dvz / inv;
         }
         CT b[16];
-        sh_basis_d(a.degree, dx_, dy_, dz_, b);
-        const int K = a.p.sh_coeffs;
-        const int kk = (a.degree + 1) * (a.degree + 1);
-        float* gsh = a.g.sh + i * K * 3;
-        for (int k = 0; k < kk; ++k)
-            for (int c = 0; c < 3; ++c) gsh[3 * k + c] += (float)(b[k] * dcol[c]);
+        sh_basis_d(DEG, dx_, dy_, dz_, b);
+        float* gsho = a.g.sh + sho;
+#pragma unroll
+        for (int k = 0; k < KK; ++k)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) gsho[3 * k + c] = gsh[3 * k + c] + (float)(b[k] * dcol[c]);
         CT dpt[3] = {0.0f, 0.0f, 0.0f};
-        if (a.degree >= 1) {
+        if (DEG >= 1) {
             CT gb[16][3];
-            sh_basis_grad_d(a.degree, dx_, dy_, dz_, gb);
-            const int64_t sho = i * K * 3;
+            sh_basis_grad_d(DEG, dx_, dy_, dz_, gb);
             CT dd[3] = {0.0f, 0.0f, 0.0f};
-            for (int k = 0; k < kk; ++k) {
-                const CT t = dcol[0] * pld(a.p.shs, sho + 3 * k, f64) + dcol[1] * pld(a.p.shs, sho + 3 * k + 1, f64) +
-                                 dcol[2] * pld(a.p.shs, sho + 3 * k + 2, f64);
+#pragma unroll
+            for (int k = 0; k < KK; ++k) {
+                const CT t = dcol[0] * shv[3 * k] + dcol[1] * shv[3 * k + 1] + dcol[2] * shv[3 * k + 2];
                 dd[0] += t * gb[k][0]; dd[1] += t * gb[k][1]; dd[2] += t * gb[k][2];
             }
             const CT dot = dx_ * dd[0] + dy_ * dd[1] + dz_ * dd[2];
@@ -393,12 +421,14 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
             dmean[0] += dpt[0]; dmean[1] += dpt[1]; dmean[2] += dpt[2];
         }
         // ---- write (accumulate) ----
+#pragma unroll
         for (int k = 0; k < 3; ++k) {
-            a.g.mean[3 * i + k] += (float)dmean[k];
-            a.g.rot[3 * i + k] += (float)drot[k];
-            a.g.scale[3 * i + k] += (float)dscale[k];
+            a.g.mean[3 * i + k] = gm[k] + (float)dmean[k];
+            a.g.rot[3 * i + k] = gr[k] + (float)drot[k];
+            a.g.scale[3 * i + k] = gs[k] + (float)dscale[k];
         }
-        a.g.opacity[i] += (float)q[3];
+        a.g.opacity[i] = go + (float)q[3];
+        if (!POSE) continue;       // the caller wants no pose gradient (window engine)
         // ---- pose pieces (camera tangent) ----
         CT Z[9];   // dW R^T
         for (int r3 = 0; r3 < 3; ++r3)
@@ -415,6 +445,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
         pose[7] -= dpt[1];
         pose[8] -= dpt[2];
     }
+    if (!POSE) return;
     // ---- deterministic pose reduction ----
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -466,6 +497,21 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain(Ws w, ChainArgs a) {
     }
 }
 
+template <int DEG, bool POSE>
+static void chain_kernel_p(const Ws& w, const ChainArgs& a, cudaStream_t st) {
+    if (a.p.dtype)
+        k_chain<DEG, 1, POSE><<<CHAIN_BLOCKS, CHAIN_THREADS, 0, st>>>(w, a);
+    else
+        k_chain<DEG, 0, POSE><<<CHAIN_BLOCKS, CHAIN_THREADS, 0, st>>>(w, a);
+}
+template <int DEG>
+static void chain_kernel(const Ws& w, const ChainArgs& a, cudaStream_t st) {
+    if (a.pose_out)
+        chain_kernel_p<DEG, true>(w, a, st);
+    else
+        chain_kernel_p<DEG, false>(w, a, st);
+}
+
 cudaError_t launch_chain(const Ws& w, const lsb_params& p, const lsb_grads& g, const lsb_camera& cam,
                          const lsb_pose& T, const lsb_settings& s, double* pose_out,
                          cudaStream_t st) {
@@ -473,8 +519,14 @@ cudaError_t launch_chain(const Ws& w, const lsb_params& p, const lsb_grads& g, c
     int deg_store = 0;
     while ((deg_store + 2) * (deg_store + 2) <= p.sh_coeffs) ++deg_store;
     a.degree = s.sh_degree < deg_store ? s.sh_degree : deg_store;
+    if (a.degree < 0) a.degree = 0;
     k_chain_sums<<<8 * 148, 128, 0, st>>>(w);
-    k_chain<<<CHAIN_BLOCKS, CHAIN_THREADS, 0, st>>>(w, a);
+    switch (a.degree) {
+        case 0: chain_kernel<0>(w, a, st); break;
+        case 1: chain_kernel<1>(w, a, st); break;
+        case 2: chain_kernel<2>(w, a, st); break;
+        default: chain_kernel<3>(w, a, st); break;
+    }
     return cudaGetLastError();
 }
 

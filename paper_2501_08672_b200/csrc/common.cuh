@@ -17,6 +17,10 @@ constexpr int PRE_THREADS = LSB_PRE_THREADS;     // preprocess block size
 constexpr int PRE_ITEMS = 1;         // Gaussians per preprocess thread
 constexpr int CHAIN_BLOCKS = 592;    // fixed grid of the chain kernel (4 x 148 SMs)
 constexpr int CHAIN_THREADS = 64;
+#ifndef LSB_CHAIN_CH
+#define LSB_CHAIN_CH 128
+#endif
+constexpr int CHAIN_CH = LSB_CHAIN_CH;   // intersections per warp in the chain's partial sums (32 lanes x 4)
 constexpr double LOG2E = 1.4426950408889634;
 
 // One visible splat, 64 B, written once by preprocess and read by every tile
@@ -125,7 +129,7 @@ struct Ws {
     unsigned long long* sticky; // [1] overflow seen by any render since the caller last cleared it (not
                                 // part of the per-render zeroed prefix: lsb_render_sticky reads / clears it)
     double* pose_part;          // [CHAIN_BLOCKS * POSE_VALS]
-    double* chain_carry;        // [cap / 256 + 1][2][NUM_PART] partial-sum pieces of runs crossing chunks
+    double* chain_carry;        // [cap / CHAIN_CH + 1][2][NUM_PART] partial-sum pieces of runs crossing chunks
     double* loss_part;          // [ntiles * 2] fused-loss tile partials
     int32_t* vis_ebase;         // [n + 1] first intersection of each visible slot (exclusive scan)
     int32_t* big_tiles;         // [ntiles] tiles queued for the shared-memory sort
@@ -184,7 +188,7 @@ inline size_t carve(const lsb_dims& d, char* base, Ws* w) {
     t.ovr_of = (int32_t*)take(sizeof(int32_t) * cap);
     t.ovr = (uint32_t*)take(sizeof(uint32_t) * 16 * (size_t)t.ovr_cap);
     t.pose_part = (double*)take(sizeof(double) * CHAIN_BLOCKS * POSE_VALS);
-    t.chain_carry = (double*)take(sizeof(double) * 2 * NUM_PART * (cap / 256 + 1));
+    t.chain_carry = (double*)take(sizeof(double) * 2 * NUM_PART * (cap / CHAIN_CH + 1));
     t.loss_part = (double*)take(sizeof(double) * 2 * t.ntiles);
     t.vis_ebase = (int32_t*)take(sizeof(int32_t) * (n + 1));
     t.big_tiles = (int32_t*)take(sizeof(int32_t) * t.ntiles);
