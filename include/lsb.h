@@ -271,6 +271,24 @@ int lsb_adam_step(const lsb_params* p, const float* grads, void* m, void* v, uin
 int lsb_adam_step_dev(const lsb_params* p, const float* grads, void* m, void* v, uint8_t* touched,
                       const lsb_adam_cfg* cfg, const double* ibc_table, int64_t table_len, int64_t* step_dev,
                       void* stream);
+/* Parameter groups of lsb_adam_step_dev_groups (gradient buffer ranges
+ * [0,3n) mean, [3n,6n) rot, [6n,9n) scale, [9n,10n) opacity, [10n,..) sh). */
+#define LSB_ADAM_MEAN 1
+#define LSB_ADAM_ROT 2
+#define LSB_ADAM_SCALE 4
+#define LSB_ADAM_OPACITY 8
+#define LSB_ADAM_SH 16
+#define LSB_ADAM_ALL 31
+/* lsb_adam_step_dev restricted to the parameter groups in `groups` (the
+ * non-rotation groups must be contiguous in the order mean, scale, opacity,
+ * sh), so a multi-GPU step can apply Adam to one all-reduce bucket while the
+ * next bucket is still being reduced.  Every part of one step reads the same
+ * step count t = *step_dev + 1; only the part with `advance` != 0 (the last
+ * one) increments *step_dev.  The parts of a step together give the same
+ * bits as one lsb_adam_step_dev call (each element's update is independent). */
+int lsb_adam_step_dev_groups(const lsb_params* p, const float* grads, void* m, void* v, uint8_t* touched,
+                             const lsb_adam_cfg* cfg, const double* ibc_table, int64_t table_len,
+                             int64_t* step_dev, int32_t groups, int32_t advance, void* stream);
 /* Fused multi-GPU optimiser step over NVLink peer memory (replaces the
  * NCCL all-reduce + Adam pair of the view-sharded step).  replicas[q] /
  * grads[q] / touched[q] are rank q's parameter arena, flat f32 gradient

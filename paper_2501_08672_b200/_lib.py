@@ -119,6 +119,8 @@ SIGNATURES = [
     ("lsb_adam_step", _c.c_int, [_c.POINTER(Params), _P, _P, _P, _P, _c.POINTER(AdamCfg), _P]),
     ("lsb_adam_step_dev", _c.c_int, [_c.POINTER(Params), _P, _P, _P, _P, _c.POINTER(AdamCfg), _P, _c.c_int64, _P,
                                      _P]),
+    ("lsb_adam_step_dev_groups", _c.c_int, [_c.POINTER(Params), _P, _P, _P, _P, _c.POINTER(AdamCfg), _P,
+                                            _c.c_int64, _P, _c.c_int32, _c.c_int32, _P]),
     ("lsb_adam_peer_step", _c.c_int, [_P, _c.c_int32, _c.c_int32, _P, _c.c_int64, _c.c_int64, _P, _P, _P,
                                       _c.POINTER(AdamCfg), _P, _c.c_int64, _P, _P]),
     ("lsb_copy_h2d", _c.c_int, [_P, _P, _c.c_size_t, _P]),

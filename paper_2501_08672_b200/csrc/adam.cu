@@ -202,19 +202,54 @@ __device__ __forceinline__ PT adam_step_el(const lsb_adam_cfg& c, PT ibc1, PT ib
     return -lr * (m * ibc1) / (sqrt(v * ibc2) + (PT)c.eps);
 }
 
+// The element range [ulo, uhi) of a set of non-rotation groups (contiguous
+// in element order mean, scale, opacity, sh; checked by the caller).
+inline void adam_group_range(int groups, int64_t n, int K, int64_t& ulo, int64_t& uhi) {
+    const int64_t lo_of[4] = {0, 3 * n, 6 * n, 7 * n};
+    const int64_t hi_of[4] = {3 * n, 6 * n, 7 * n, (7 + 3 * (int64_t)K) * n};
+    const int bit[4] = {LSB_ADAM_MEAN, LSB_ADAM_SCALE, LSB_ADAM_OPACITY, LSB_ADAM_SH};
+    ulo = uhi = 0;
+    bool any = false;
+    for (int q = 0; q < 4; ++q)
+        if (groups & bit[q]) {
+            if (!any) ulo = lo_of[q];
+            uhi = hi_of[q];
+            any = true;
+        }
+}
+
+// True if the non-rotation groups in `groups` are contiguous in element order.
+bool adam_groups_contiguous(int groups) {
+    const int bit[4] = {LSB_ADAM_MEAN, LSB_ADAM_SCALE, LSB_ADAM_OPACITY, LSB_ADAM_SH};
+    int first = -1, last = -1;
+    for (int q = 0; q < 4; ++q)
+        if (groups & bit[q]) {
+            if (first < 0) first = q;
+            last = q;
+        }
+    for (int q = first; q >= 0 && q <= last; ++q)
+        if (!(groups & bit[q])) return false;
+    return true;
+}
+
+// Element blocks step the elements u in [ulo, uhi) of the non-rotation
+// groups — u: [0,3n) mean, [3n,6n) scale, [6n,7n) opacity, [7n, 7n + nk n)
+// sh — and the blocks from `eb` on step the rotation rows (none when the
+// launch has no rotation blocks).  The whole step is ulo = 0, uhi = total
+// plus rotation blocks; a multi-GPU step launches one group range per
+// all-reduce bucket (lsb_adam_step_dev_groups).
 template <typename PT>
-__global__ void __launch_bounds__(256) k_adam_flat(AdamArgs<PT> a, int eb) {
+__global__ void __launch_bounds__(256) k_adam_flat(AdamArgs<PT> a, int eb, int64_t ulo, int64_t uhi) {
     PT ibc1, ibc2;
     bias_corr(a, ibc1, ibc2);
-    const int64_t n = a.n, nk = 3 * (int64_t)a.K;
+    const int64_t n = a.n;
     const int64_t o_rot = 3 * n, o_scale = 6 * n, o_op = 9 * n, o_sh = 10 * n;
     const PT* __restrict__ mm_ = a.m;
     const float* __restrict__ g_ = a.g;
     if ((int)blockIdx.x < eb) {
-        // element u: [0,3n) mean, [3n,6n) scale, [6n,7n) opacity, [7n, 7n + nk n) sh
-        const int64_t total = 7 * n + nk * n;
+        const int64_t total = uhi;
         const int64_t stride = (int64_t)eb * blockDim.x * ADAM_U;
-        for (int64_t u0 = (int64_t)blockIdx.x * blockDim.x * ADAM_U + threadIdx.x; u0 < total; u0 += stride) {
+        for (int64_t u0 = ulo + (int64_t)blockIdx.x * blockDim.x * ADAM_U + threadIdx.x; u0 < total; u0 += stride) {
             int64_t gi[ADAM_U];
             float gr[ADAM_U];
             PT m0[ADAM_U], v0[ADAM_U], p0[ADAM_U];
@@ -225,7 +260,9 @@ __global__ void __launch_bounds__(256) k_adam_flat(AdamArgs<PT> a, int eb) {
                 int64_t j = u;
                 PT* base = a.means;
                 gi[q] = -1;
-                if (u < 3 * n) {
+                if (u >= total) {
+                    // past this launch's group range (another part's elements)
+                } else if (u < 3 * n) {
                     gi[q] = u;
                 } else if (u < 6 * n) {
                     j = u - 3 * n;
@@ -378,7 +415,7 @@ __global__ void k_step_bump(int64_t* step_dev) { *step_dev += 1; }
 template <typename PT>
 static cudaError_t adam_t(const lsb_params& p, const float* g, void* m, void* v, uint8_t* touched,
                           const lsb_adam_cfg& c, const double* tab, int64_t tab_len, int64_t* step_dev,
-                          cudaStream_t st) {
+                          cudaStream_t st, int groups = LSB_ADAM_ALL, bool advance = true) {
     AdamArgs<PT> a{(PT*)p.means, (PT*)p.rots, (PT*)p.scales, (PT*)p.opacities, (PT*)p.shs, p.n, p.sh_coeffs,
                    g, (PT*)m, (PT*)v, touched, c, (PT)0, (PT)0, tab, tab_len, step_dev};
     if (!tab) {
@@ -387,23 +424,24 @@ static cudaError_t adam_t(const lsb_params& p, const float* g, void* m, void* v,
     }
     if (p.n > 0) {
         // element blocks (~ADAM_U elements per thread, one wave of 148 x 8 CTAs at most) + rotation blocks
-        const int64_t total = (7 + 3 * (int64_t)p.sh_coeffs) * p.n;
-        int64_t eb = (total + 256 * ADAM_U - 1) / (256 * ADAM_U);
+        int64_t ulo = 0, uhi = 0;
+        adam_group_range(groups, p.n, p.sh_coeffs, ulo, uhi);
+        int64_t eb = (uhi - ulo + 256 * ADAM_U - 1) / (256 * ADAM_U);
         eb = eb < 148 * 6 ? eb : 148 * 6;
-        int64_t rb = (p.n + 255) / 256;
+        int64_t rb = (groups & LSB_ADAM_ROT) ? (p.n + 255) / 256 : 0;
         rb = rb < 148 * 2 ? rb : 148 * 2;
-        k_adam_flat<PT><<<(unsigned)(eb + rb), 256, 0, st>>>(a, (int)eb);
+        if (eb + rb > 0) k_adam_flat<PT><<<(unsigned)(eb + rb), 256, 0, st>>>(a, (int)eb, ulo, uhi);
     }
-    if (step_dev) k_step_bump<<<1, 1, 0, st>>>(step_dev);
+    if (step_dev && advance) k_step_bump<<<1, 1, 0, st>>>(step_dev);
     return cudaGetLastError();
 }
 
 cudaError_t launch_adam(const lsb_params& p, const float* g, void* m, void* v, uint8_t* touched,
                         const lsb_adam_cfg& c, const double* tab, int64_t tab_len, int64_t* step_dev,
-                        cudaStream_t st) {
-    if (p.n == 0 && !step_dev) return cudaSuccess;
-    return p.dtype ? adam_t<double>(p, g, m, v, touched, c, tab, tab_len, step_dev, st)
-                   : adam_t<float>(p, g, m, v, touched, c, tab, tab_len, step_dev, st);
+                        cudaStream_t st, int groups, bool advance) {
+    if (p.n == 0 && !(step_dev && advance)) return cudaSuccess;
+    return p.dtype ? adam_t<double>(p, g, m, v, touched, c, tab, tab_len, step_dev, st, groups, advance)
+                   : adam_t<float>(p, g, m, v, touched, c, tab, tab_len, step_dev, st, groups, advance);
 }
 
 template <typename PT>

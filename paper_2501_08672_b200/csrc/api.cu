@@ -28,7 +28,8 @@ cudaError_t launch_loss(const float*, const void*, const uint8_t*, int64_t, int,
                         cudaStream_t);
 int loss_scratch_doubles();
 cudaError_t launch_adam(const lsb_params&, const float*, void*, void*, uint8_t*, const lsb_adam_cfg&, const double*,
-                        int64_t, int64_t*, cudaStream_t);
+                        int64_t, int64_t*, cudaStream_t, int groups = LSB_ADAM_ALL, bool advance = true);
+bool adam_groups_contiguous(int groups);
 cudaError_t launch_orthonormalize(void*, int, const uint8_t*, int64_t, cudaStream_t);
 cudaError_t launch_adam_peer(const lsb_params*, int, int, const float* const*, int64_t, int64_t, void*, void*,
                              uint8_t* const*, const lsb_adam_cfg&, const double*, int64_t, int64_t*, cudaStream_t);
@@ -414,6 +415,20 @@ int lsb_adam_step_dev(const lsb_params* p, const float* grads, void* m, void* v,
         return fail(LSB_EINVAL, "NULL array");
     return check_cuda(launch_adam(*p, grads, m, v, touched, *cfg, ibc_table, table_len, step_dev,
                                   (cudaStream_t)stream), "adam_dev");
+}
+
+int lsb_adam_step_dev_groups(const lsb_params* p, const float* grads, void* m, void* v, uint8_t* touched,
+                             const lsb_adam_cfg* cfg, const double* ibc_table, int64_t table_len,
+                             int64_t* step_dev, int32_t groups, int32_t advance, void* stream) {
+    if (!p || !cfg || !ibc_table || !step_dev) return fail(LSB_EINVAL, "NULL argument");
+    if (table_len < 1) return fail(LSB_EINVAL, "empty bias-correction table");
+    if (groups & ~LSB_ADAM_ALL) return fail(LSB_EINVAL, "unknown parameter group bits");
+    if (!adam_groups_contiguous(groups)) return fail(LSB_EINVAL, "non-rotation groups must be contiguous");
+    if (p->n > 0 && (!grads || !m || !v || !touched || !p->means || !p->rots || !p->scales || !p->opacities ||
+                     !p->shs))
+        return fail(LSB_EINVAL, "NULL array");
+    return check_cuda(launch_adam(*p, grads, m, v, touched, *cfg, ibc_table, table_len, step_dev,
+                                  (cudaStream_t)stream, groups, advance != 0), "adam_dev_groups");
 }
 
 int lsb_copy_h2d(void* dst, const void* src, size_t bytes, void* stream) {

@@ -59,18 +59,37 @@ def shard_units(n_views: int, world: int, rank: int, height: int, tile: int = 16
     return units[rank * per:(rank + 1) * per]
 
 
+class AllReduce:
+    """The gradient exchange: in-place sum over the process group.  Called
+    on the whole flat buffer it blocks the current stream on one all-reduce;
+    `start` / `wait` split it into buckets (WindowEngine steps the Adam
+    groups of bucket b while bucket b + 1 is still being reduced).  Each
+    element is reduced once and the result broadcast, so every rank receives
+    the same bits and the replicas stay identical; with two ranks the sum is
+    a + b whichever way the buffer is cut, with more ranks the summation
+    order (hence the last bit) may differ from a one-shot all-reduce's."""
+
+    def __init__(self, group=None):
+        self.group = group
+
+    def __call__(self, flat: torch.Tensor) -> None:
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.group)
+
+    def start(self, part: torch.Tensor):
+        return dist.all_reduce(part, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+
+    @staticmethod
+    def wait(work) -> None:
+        work.wait()          # NCCL: the current stream waits on the collective (no host sync)
+
+
 def make_allreduce(group=None) -> Optional[Callable[[torch.Tensor], None]]:
-    """The gradient exchange: in-place sum over the process group (None if
-    not distributed or world size 1)."""
+    """The gradient exchange (None if not distributed or world size 1)."""
     if not dist.is_available() or not dist.is_initialized():
         return None
     if dist.get_world_size(group) == 1:
         return None
-
-    def allreduce(flat: torch.Tensor) -> None:
-        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
-
-    return allreduce
+    return AllReduce(group)
 
 
 def replicas_identical(t: torch.Tensor, group=None) -> bool:

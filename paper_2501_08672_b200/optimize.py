@@ -123,6 +123,19 @@ def adam_cfg(cfg: OptimConfig, step: int) -> _lib.AdamCfg:
                         cfg.eps, cfg.scene_scale, cfg.opacity_clip, cfg.scale_floor, int(step))
 
 
+# parameter groups (include/lsb.h LSB_ADAM_*)
+ADAM_MEAN, ADAM_ROT, ADAM_SCALE, ADAM_OPACITY, ADAM_SH = 1, 2, 4, 8, 16
+ADAM_ALL = 31
+
+
+def exchange_buckets(n: int, k: int) -> list:
+    """All-reduce buckets of the flat gradient buffer [mean 3n | rot 3n |
+    scale 3n | opacity n | sh 3kn] for a step that applies Adam to one bucket
+    while the next is still being reduced: (lo, hi, Adam groups)."""
+    return [(0, 3 * n, ADAM_MEAN), (3 * n, 6 * n, ADAM_ROT), (6 * n, 10 * n, ADAM_SCALE | ADAM_OPACITY),
+            (10 * n, (10 + 3 * k) * n, ADAM_SH)]
+
+
 IBC_ROWS = 1 << 16     # table rows at least (enough for beta2 <= 0.9994)
 
 
@@ -165,19 +178,30 @@ class AdamState:
         self.step_dev = None
         self.ibc = None
 
-    def apply_dev(self, arrays: GaussianArrays, grads: ParamGradients, stream=None) -> None:
-        """Like apply(), with the step count read and advanced on the device."""
+    def apply_dev(self, arrays: GaussianArrays, grads: ParamGradients, stream=None, groups: int = None,
+                  advance: bool = True) -> None:
+        """Like apply(), with the step count read and advanced on the device.
+        `groups` (ADAM_* bits) restricts the step to some parameter groups:
+        the parts of one step all read the same step count, and only the
+        part with `advance` (the last one) moves it on."""
         if self.step_dev is None:
             self.ibc = torch.from_numpy(bias_correction_table(self.cfg.beta1, self.cfg.beta2)).to(self.m.device)
             self.step_dev = torch.full((1,), self.step, dtype=torch.int64, device=self.m.device)
-        self.step += 1
-        c = adam_cfg(self.cfg, self.step)
+        c = adam_cfg(self.cfg, self.step + 1)
         p = arrays.params()
-        _lib.check(_lib.load().lsb_adam_step_dev(
-            ctypes.byref(p), ctypes.c_void_p(grads.flat.data_ptr()), ctypes.c_void_p(self.m.data_ptr()),
-            ctypes.c_void_p(self.v.data_ptr()), ctypes.c_void_p(self.touched.data_ptr()), ctypes.byref(c),
-            ctypes.c_void_p(self.ibc.data_ptr()), int(self.ibc.shape[0]), ctypes.c_void_p(self.step_dev.data_ptr()),
-            _lib.stream_ptr(stream)), "adam_dev")
+        lib = _lib.load()
+        args = (ctypes.byref(p), ctypes.c_void_p(grads.flat.data_ptr()), ctypes.c_void_p(self.m.data_ptr()),
+                ctypes.c_void_p(self.v.data_ptr()), ctypes.c_void_p(self.touched.data_ptr()), ctypes.byref(c),
+                ctypes.c_void_p(self.ibc.data_ptr()), int(self.ibc.shape[0]), ctypes.c_void_p(self.step_dev.data_ptr()))
+        if groups is None or groups == ADAM_ALL:
+            if not advance:
+                raise ValueError("a whole-step Adam call always advances the step count")
+            _lib.check(lib.lsb_adam_step_dev(*args, _lib.stream_ptr(stream)), "adam_dev")
+        else:
+            _lib.check(lib.lsb_adam_step_dev_groups(*args, int(groups), 1 if advance else 0, _lib.stream_ptr(stream)),
+                       "adam_dev_groups")
+        if advance:
+            self.step += 1
 
     def apply(self, arrays: GaussianArrays, grads: ParamGradients, stream=None) -> None:
         """One Adam step in storage coordinates, in place on the arena."""
@@ -224,6 +248,7 @@ class WindowEngine:
         self.fused_blend = True             # forward + loss + backward in one kernel per view
         self.loss_in_backward = True        # (unfused) photometric loss fused into the backward (else the forward)
         self.exchange = None                # dist.PeerExchange: multi-GPU step over NVLink peer memory
+        self.overlap_exchange = True        # bucketed all-reduce, Adam per bucket (multi-GPU NCCL step)
         self.copy_streams = 1               # H2D staging streams (views round-robin)
         self.arena = arrays
         if master == "f64" and arrays.dtype != torch.float64:
@@ -365,10 +390,15 @@ class WindowEngine:
         capturing = torch.cuda.is_current_stream_capturing()
         if capturing:
             timers = None
-        with torch.cuda.stream(main):
-            self.grads.flat.zero_()
+        # the lanes start binning as soon as the previous step's parameters
+        # are final; only the first chain (the first writer of the gradient
+        # buffer) waits for the buffer to be zeroed
         ready = torch.cuda.Event()
         ready.record(main)
+        with torch.cuda.stream(main):
+            self.grads.flat.zero_()
+        zeroed = torch.cuda.Event()
+        zeroed.record(main)
         host = len(observed) > 0 and not observed[0].is_cuda
         copied = self._stage(observed, ready, capturing) if host else None
 
@@ -421,6 +451,8 @@ class WindowEngine:
                 self._consumed[v] = ev
             if prev_chain is not None and sm is not main:
                 sm.wait_event(prev_chain)
+            elif prev_chain is None and sm is not main:
+                sm.wait_event(zeroed)
             mark("chain", sm); render_chain(st, self.grads, None, sm); mark("chain", sm)
             prev_chain = torch.cuda.Event()
             prev_chain.record(sm)
@@ -438,6 +470,16 @@ class WindowEngine:
             mark("adam", main)
             if self.exchange is not None:       # fused peer-memory exchange + Adam (dist.PeerExchange)
                 self.exchange.step(main)
+            elif allreduce is not None and self.overlap_exchange and hasattr(allreduce, "start"):
+                # bucketed exchange: every bucket's all-reduce is queued at
+                # once on the communicator's stream, and Adam steps bucket b
+                # (its parameter groups) as soon as that bucket is reduced,
+                # while the later buckets are still on the wire
+                buckets = exchange_buckets(len(self.arrays), int(self.arrays.shs.shape[1]))
+                works = [allreduce.start(self.grads.flat[lo:hi]) for lo, hi, _ in buckets]
+                for q, ((lo, hi, groups), wk) in enumerate(zip(buckets, works)):
+                    allreduce.wait(wk)
+                    self.adam.apply_dev(self.arrays, self.grads, main, groups=groups, advance=q == len(buckets) - 1)
             else:
                 if allreduce is not None:
                     allreduce(self.grads.flat)

@@ -124,3 +124,60 @@ def test_view_sharded_allreduce_equals_single_process_mean():
     P, cam, st, views = _views_and_scene()
     ref = sum(_view_grad_flat(P, cam, st, T, len(views)) for T in views).numpy()
     assert np.abs(out[0][1] - ref).max() <= 1e-6 * max(np.abs(ref).max(), 1e-12)
+
+
+def test_exchange_buckets_tile_the_flat_buffer_and_adam_groups():
+    """The bucketed exchange's buckets cover the ParamGradients flat layout
+    exactly once, in order, and their Adam groups partition every group."""
+    from paper_2501_08672_b200.optimize import ADAM_ALL, exchange_buckets
+    from paper_2501_08672_b200.raster import ParamGradients
+    for n, k in ((1, 1), (37, 1), (1000, 4), (5, 16)):
+        b = exchange_buckets(n, k)
+        assert b[0][0] == 0 and b[-1][1] == ParamGradients.zeros(n, k, "cpu").flat.numel()
+        assert all(b[q][1] == b[q + 1][0] for q in range(len(b) - 1))
+        groups = [g for _, _, g in b]
+        assert sum(groups) == ADAM_ALL and all(g & h == 0 for i, g in enumerate(groups) for h in groups[i + 1:])
+        pg = ParamGradients.zeros(n, k, "cpu")
+        # each bucket is exactly the flat range of its groups' tensors
+        names = {1: ["mean"], 2: ["rot"], 12: ["scale", "opacity"], 16: ["sh"]}
+        for lo, hi, g in b:
+            size = sum(getattr(pg, f).numel() for f in names[g])
+            assert hi - lo == size
+
+
+def _bucket_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2501_08672_b200.dist import make_allreduce
+        from paper_2501_08672_b200.optimize import exchange_buckets
+        n, k = 301, 1
+        g = torch.from_numpy(np.random.default_rng(rank).standard_normal((10 + 3 * k) * n).astype(np.float32))
+        one = g.clone()
+        ar = make_allreduce()
+        ar(one)
+        part = g.clone()
+        works = [ar.start(part[lo:hi]) for lo, hi, _ in exchange_buckets(n, k)]
+        for w in works:
+            ar.wait(w)
+        q.put((rank, bool(torch.equal(one, part)), one.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bucketed_allreduce_equals_one_shot_two_ranks():
+    """Two ranks: the bucketed (async, in-place on views) all-reduce gives the
+    one-shot all-reduce's bits on every rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_bucket_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _ in res)
+    assert np.array_equal(res[0][2], res[1][2])

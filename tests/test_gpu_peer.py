@@ -140,3 +140,83 @@ def test_peer_exchange_in_cuda_graph(tmp_path):
         dist.destroy_process_group()
     for f in ("means", "rots", "scales", "opacities", "shs"):
         assert torch.equal(getattr(out[0], f), getattr(out[1], f)), f
+
+
+@pytest.mark.parametrize("steps", [1, 3])
+def test_adam_group_parts_equal_whole_step(steps):
+    """lsb_adam_step_dev_groups: the bucketed multi-GPU step applies Adam to
+    one all-reduce bucket at a time (exchange_buckets).  The parts of every
+    step together give the bits of one whole-step call — parameters, moments,
+    touched flags and the device step count — and a bad group set is refused."""
+    from paper_2501_08672_b200 import _lib
+    from paper_2501_08672_b200.optimize import AdamState, OptimConfig, exchange_buckets
+    from paper_2501_08672_b200.raster import GaussianArrays, ParamGradients
+    s = load("scene_room_0323")
+    base = GaussianArrays(s["means"], s["rots"], s["scales"], s["opacities"], s["shs"]).clone(torch.float64)
+    n, k = len(base), int(base.shs.shape[1])
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    gs = [torch.randn(n * (10 + 3 * k), generator=gen, device="cuda") * 1e-3 for _ in range(steps)]
+    for g in gs:
+        g[: 5 * n // 7] *= (torch.rand(5 * n // 7, generator=gen, device="cuda") > 0.5)   # idle rows too
+    cfg = OptimConfig()
+    whole, parts = base.clone(), base.clone()
+    sw, sp = AdamState(whole, cfg), AdamState(parts, cfg)
+    buckets = exchange_buckets(n, k)
+    for g in gs:
+        sw.apply_dev(whole, ParamGradients.from_flat(g, n, k))
+        for q, (_, _, groups) in enumerate(buckets):
+            sp.apply_dev(parts, ParamGradients.from_flat(g, n, k), groups=groups, advance=q == len(buckets) - 1)
+    torch.cuda.synchronize()
+    for f in ("means", "rots", "scales", "opacities", "shs"):
+        assert torch.equal(getattr(whole, f), getattr(parts, f)), f
+    assert torch.equal(sw.m, sp.m) and torch.equal(sw.v, sp.v) and torch.equal(sw.touched, sp.touched)
+    assert int(sw.step_dev.item()) == int(sp.step_dev.item()) == steps and sw.step == sp.step == steps
+    with pytest.raises(Exception):
+        sp.apply_dev(parts, ParamGradients.from_flat(gs[0], n, k), groups=1 | 16)   # mean + sh: not contiguous
+    assert _lib.load().lsb_last_error() is not None
+
+
+def test_bucketed_nccl_exchange_in_cuda_graph(tmp_path):
+    """The bucketed NCCL exchange (async all-reduce per bucket, Adam per
+    bucket as each completes) on a one-rank NCCL group: eager and captured in
+    the step's CUDA graph, the same bits as the engine step without an
+    exchange (a one-rank all-reduce is the identity)."""
+    import torch.distributed as dist
+    from paper_2501_08672_b200.dist import AllReduce
+    from paper_2501_08672_b200.optimize import OptimConfig, WindowEngine
+    from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
+    from tools.scene import camera_for, orbit_views
+    s = load("scene_room_0323")
+    cam = camera_for(160, 128)
+    views = orbit_views(3)
+    st = RasterSettings(alpha_cut=1 / 255)
+    gt = GaussianArrays(s["means"], s["rots"], s["scales"], s["opacities"], s["shs"])
+    obs = [render(gt, T, cam, st, retain_cache=False).image.clone() for T in views]
+    shs = s["shs"].copy()
+    shs[:, 0, :] += 0.05
+    out = []
+    dist.init_process_group("nccl", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        for mode in ("none", "eager", "graph"):
+            win = GaussianArrays(s["means"], s["rots"], s["scales"], s["opacities"], shs)
+            stream = torch.cuda.Stream()
+            eng = WindowEngine(win, cam, views, st, OptimConfig(), lanes=2, stream=stream)
+            ar = None if mode == "none" else AllReduce()
+            with torch.cuda.stream(stream):
+                eng.step(obs, allreduce=ar)
+                if mode == "graph":
+                    eng.capture(obs, allreduce=ar)
+                    for _ in range(2):
+                        eng.replay()
+                else:
+                    for _ in range(2):
+                        eng.step(obs, allreduce=ar)
+                eng.finish()
+            torch.cuda.synchronize()
+            out.append(win)
+    finally:
+        dist.destroy_process_group()
+    for w in out[1:]:
+        for f in ("means", "rots", "scales", "opacities", "shs"):
+            assert torch.equal(getattr(out[0], f), getattr(w, f)), f
