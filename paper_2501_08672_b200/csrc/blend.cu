@@ -345,6 +345,65 @@ __device__ __forceinline__ void fwd_pixels(const Frame& f, float4 qb, float4 qc,
     }
 }
 
+#ifndef LSB_PACKED_FWD
+#define LSB_PACKED_FWD 1
+#endif
+// The count-free forward update of one record with packed FP32 (FFMA2 /
+// FMUL2 / FADD2 on pixel pairs of the run: half the issue slots of the
+// alpha and compositing arithmetic).  Per component the operations are the
+// scalar fwd_pixel_nc's (same rounding: mul -> fma multiplicand only, never
+// mul -> add, which ptxas would contract for packed operands), and a pair
+// that does not composite gets w = 0, so C + 0 c and T + 0 (-clamp) leave
+// the accumulators bit-identical to the predicated scalar update.
+// w if (T >= thr && a >= cut) else 0: one select on a combined predicate
+__device__ __forceinline__ float take_w(float w, float T, float thr, float a, float cut) {
+    float r;
+    asm("{\n\t.reg .pred p, q;\n\t"
+        "setp.ge.f32 p, %2, %3;\n\t"
+        "setp.ge.and.f32 q, %4, %5, p;\n\t"
+        "selp.f32 %0, %1, 0f00000000, q;\n\t}"
+        : "=f"(r)
+        : "f"(w), "f"(T), "f"(thr), "f"(a), "f"(cut));
+    return r;
+}
+
+template <bool OVR, bool SAT>
+__device__ __forceinline__ void fwd_pixels2(const Frame& f, float4 qb, float4 qc, bool row0, bool row1,
+                                            const float* thr, float cut, float nkap, const OvrNib& o,
+                                            float (&T)[2][RUN], float (&cr)[2][RUN], float (&cg)[2][RUN],
+                                            float (&cb)[2][RUN]) {
+    const float2 A2 = make_float2(qb.x, qb.x), NK = make_float2(nkap, nkap);
+    const float2 C0 = make_float2(qc.x, qc.x), C1 = make_float2(qc.y, qc.y), C2 = make_float2(qc.z, qc.z);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        if (!(h ? row1 : row0)) continue;
+        float dy, u0, edy;
+        row_terms(f, qb.y, qb.z, 8.f * h, dy, u0, edy);
+        const float2 E2 = make_float2(edy, edy), U0 = make_float2(u0, u0);
+#pragma unroll
+        for (int p = 0; p < RUN / 2; ++p) {
+            const int j = 2 * p;
+            const float2 u = __fadd2_rn(U0, make_float2((float)j, (float)(j + 1)));
+            const float2 q = __ffma2_rn(A2, __fmul2_rn(u, u), E2);
+            const float e0 = ex2_approx(q.x), e1 = ex2_approx(q.y);
+            const float a0 = SAT ? __saturatef(e0) : e0, a1 = SAT ? __saturatef(e1) : e1;
+            float2 t2 = make_float2(T[h][j], T[h][j + 1]);
+            float2 w = __fmul2_rn(t2, make_float2(a0, a1));
+            const float k0 = OVR ? ovr_cut(o, h, j, cut) : cut, k1 = OVR ? ovr_cut(o, h, j + 1, cut) : cut;
+            w.x = take_w(w.x, t2.x, thr[j], a0, k0);
+            w.y = take_w(w.y, t2.y, thr[j + 1], a1, k1);
+            float2 r2 = __ffma2_rn(w, C0, make_float2(cr[h][j], cr[h][j + 1]));
+            float2 g2 = __ffma2_rn(w, C1, make_float2(cg[h][j], cg[h][j + 1]));
+            float2 b2 = __ffma2_rn(w, C2, make_float2(cb[h][j], cb[h][j + 1]));
+            t2 = __ffma2_rn(w, NK, t2);
+            cr[h][j] = r2.x; cr[h][j + 1] = r2.y;
+            cg[h][j] = g2.x; cg[h][j + 1] = g2.y;
+            cb[h][j] = b2.x; cb[h][j + 1] = b2.y;
+            T[h][j] = t2.x; T[h][j + 1] = t2.y;
+        }
+    }
+}
+
 template <bool DEPTH, bool CUT, bool COUNT>
 __global__ void __launch_bounds__(32 * WPB, FWD_MIN_BLOCKS)
 k_blend_fwd(Ws w, BlendArgs a, LossArgs L, float* __restrict__ image, float* __restrict__ t_final,
@@ -598,6 +657,104 @@ __device__ __forceinline__ void red_flush(const Ws& w, const BlendArgs& a, const
     if (sub == 0) dst[8] = 0.5f * fmaf(sa * sa, t[6], fmaf(2.f * sa * ek, t[7], ek * ek * t[8]));
 }
 
+#ifndef LSB_PACKED_BWD
+#define LSB_PACKED_BWD 1
+#endif
+// The selects of one backward pixel from one predicate pair:
+//   take = T >= thr && a >= cut'  -> ws = take ? w : 0
+//   gate = take (&& a < 1 with SAT)  -> as = gate ? a : 0
+template <bool SAT>
+__device__ __forceinline__ void take_wa(float w, float T, float thr, float a, float cut, float& ws, float& as) {
+    if (SAT)
+        asm("{\n\t.reg .pred p, q, g;\n\t"
+            "setp.ge.f32 p, %3, %4;\n\t"
+            "setp.ge.and.f32 q, %5, %6, p;\n\t"
+            "setp.lt.and.f32 g, %5, 0f3F800000, q;\n\t"
+            "selp.f32 %0, %2, 0f00000000, q;\n\t"
+            "selp.f32 %1, %5, 0f00000000, g;\n\t}"
+            : "=f"(ws), "=f"(as)
+            : "f"(w), "f"(T), "f"(thr), "f"(a), "f"(cut));
+    else
+        asm("{\n\t.reg .pred p, q;\n\t"
+            "setp.ge.f32 p, %3, %4;\n\t"
+            "setp.ge.and.f32 q, %5, %6, p;\n\t"
+            "selp.f32 %0, %2, 0f00000000, q;\n\t"
+            "selp.f32 %1, %5, 0f00000000, q;\n\t}"
+            : "=f"(ws), "=f"(as)
+            : "f"(w), "f"(T), "f"(thr), "f"(a), "f"(cut));
+}
+
+// bwd_half with packed FP32 on pixel pairs.  Per component the arithmetic is
+// bwd_pixel's (T recurrence bit-identical to the forward's: w = T a, T + ws
+// (-clamp) with ws = 0 for a pair that does not composite); the per-record
+// sums (colour, moments) are accumulated per pair lane and folded once, and
+// the moment sums use fma (S0 + a da, S1 + gd u, S2 + gu u): never a packed
+// mul feeding an add, which ptxas would contract.
+template <bool SAT, bool OVR = false>
+__device__ __forceinline__ void bwd_half2(const Frame& f, float4 q1, bool rin, float dyoff, const float* thr,
+                                          const BlendArgs& a, float kap, float4 q2, const float* Gr, const float* Gg,
+                                          const float* Gb, float* T, float* gD, float* c, float* M,
+                                          const OvrNib& o = OvrNib{}, int h = 0) {
+    float dy, u0, edy;
+    row_terms(f, q1.y, q1.z, dyoff, dy, u0, edy);
+    const float2 A2 = make_float2(q1.x, q1.x), E2 = make_float2(edy, edy), U0 = make_float2(u0, u0);
+    float2 al[RUN / 2], uu[RUN / 2];
+#pragma unroll
+    for (int p = 0; p < RUN / 2; ++p) {
+        uu[p] = __fadd2_rn(U0, make_float2((float)(2 * p), (float)(2 * p + 1)));
+        const float2 q = __ffma2_rn(A2, __fmul2_rn(uu[p], uu[p]), E2);
+        const float e0 = ex2_approx(q.x), e1 = ex2_approx(q.y);
+        al[p] = SAT ? make_float2(__saturatef(e0), __saturatef(e1)) : make_float2(e0, e1);
+    }
+    if (!OVR) {        // (with band pixels an overridden pair may composite below cut')
+        const float amax = fmaxf(fmaxf(al[0].x, al[0].y), fmaxf(al[1].x, al[1].y));
+        if (!__any_sync(0xffffffffu, rin && amax >= a.cutp)) return;
+    }
+    if (!rin) return;
+    const float2 C0 = make_float2(q2.x, q2.x), C1 = make_float2(q2.y, q2.y), C2 = make_float2(q2.z, q2.z);
+    const float2 NK = make_float2(-kap, -kap), IK = make_float2(a.ik, a.ik);
+    float2 s0 = make_float2(-0.f, -0.f), s1 = s0, s2 = s0, S0 = s0, S1 = s0, S2 = s0;
+#pragma unroll
+    for (int p = 0; p < RUN / 2; ++p) {
+        const int j = 2 * p;
+        float2 t2 = make_float2(T[j], T[j + 1]);
+        const float2 w = __fmul2_rn(t2, al[p]);
+        float2 ws, as;
+        take_wa<SAT>(w.x, t2.x, thr[j], al[p].x, OVR ? ovr_cut(o, h, j, a.cutp) : a.cutp, ws.x, as.x);
+        take_wa<SAT>(w.y, t2.y, thr[j + 1], al[p].y, OVR ? ovr_cut(o, h, j + 1, a.cutp) : a.cutp, ws.y, as.y);
+        const float2 g0 = make_float2(Gr[j], Gr[j + 1]), g1 = make_float2(Gg[j], Gg[j + 1]),
+                     g2 = make_float2(Gb[j], Gb[j + 1]);
+        const float2 gc = __ffma2_rn(g0, C0, __ffma2_rn(g1, C1, __fmul2_rn(g2, C2)));     // g . c'
+        float2 d2 = make_float2(gD[j], gD[j + 1]);
+        d2 = __ffma2_rn(make_float2(-ws.x, -ws.y), gc, d2);                             // gD -= w g.c'
+        const float2 ia = __fadd2_rn(IK, make_float2(-al[p].x, -al[p].y));
+        const float2 r = make_float2(rcp_approx(ia.x), rcp_approx(ia.y));
+        const float2 da = __ffma2_rn(make_float2(-d2.x, -d2.y), r, __fmul2_rn(t2, gc));  // T g.c' - gD / (1/clamp - a)
+        s0 = __ffma2_rn(ws, g0, s0);
+        s1 = __ffma2_rn(ws, g1, s1);
+        s2 = __ffma2_rn(ws, g2, s2);
+        S0 = __ffma2_rn(as, da, S0);                                                    // sum gd
+        const float2 gd = __fmul2_rn(as, da);
+        S1 = __ffma2_rn(gd, uu[p], S1);                                                 // sum gd u
+        S2 = __ffma2_rn(__fmul2_rn(gd, uu[p]), uu[p], S2);                              // sum gd u^2
+        t2 = __ffma2_rn(ws, NK, t2);
+        T[j] = t2.x;
+        T[j + 1] = t2.y;
+        gD[j] = d2.x;
+        gD[j + 1] = d2.y;
+    }
+    c[0] += s0.x + s0.y;
+    c[1] += s1.x + s1.y;
+    c[2] += s2.x + s2.y;
+    const float m0 = S0.x + S0.y, m1 = S1.x + S1.y, m2 = S2.x + S2.y;
+    M[0] += m0;
+    M[1] += m1;
+    M[2] = fmaf(m0, dy, M[2]);
+    M[3] += m2;
+    M[4] = fmaf(m1, dy, M[4]);
+    M[5] = fmaf(m0 * dy, dy, M[5]);
+}
+
 // The backward's record walk over one tile's list [start, end): the forward
 // recomputed per pixel (same instruction sequence as the forward, so T is
 // bit-identical), per-record screen partials reduced across the warp and
@@ -635,7 +792,8 @@ __device__ __forceinline__ void bwd_walk(const Ws& w, const BlendArgs& a, RecPip
             const bool over = alive && cx0 < RUN && cx1 > 0 && (row0 || row1);
             // accumulators: colour (3, x clamp) and the moments sum gd, gd u,
             // gd dy, gd u^2, gd u dy, gd dy^2 with gd = alpha dL/dalpha
-            float c[3] = {0.f, 0.f, 0.f}, M[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            // (-0 is the additive identity the compiler may fold: -0 + x == x for every x)
+            float c[3] = {-0.f, -0.f, -0.f}, M[6] = {-0.f, -0.f, -0.f, -0.f, -0.f, -0.f};
             const bool wover = __any_sync(0xffffffffu, over);
             if (wover) {
                 // warp-uniform from here: lanes without work get +inf thresholds
@@ -643,6 +801,9 @@ __device__ __forceinline__ void bwd_walk(const Ws& w, const BlendArgs& a, RecPip
 #pragma unroll
                 for (int j = 0; j < RUN; ++j) thr[j] = over ? col_thr(j, cx0, cx1, a.tmin) : __int_as_float(0x7f800000);
                 const Frame f = frame_of(q0, q1.w, gx0f, gy0f);
+#if LSB_PACKED_BWD
+#define bwd_half bwd_half2
+#endif
                 if ((pipe.ovr >> k) & 1u) {            // band pixels: the f64 decisions (saturating form)
                     const OvrNib o = ovr_nibbles(w, base + k, lane);
                     bwd_half<true, true>(f, q1, over && row0, 0.f, thr, a, kap, q2, Gr[0], Gg[0], Gb[0], T[0], gD[0], c,
@@ -658,6 +819,7 @@ __device__ __forceinline__ void bwd_walk(const Ws& w, const BlendArgs& a, RecPip
                     bwd_half<false>(f, q1, over && row1, 8.f, thr, a, kap, q2, Gr[1], Gg[1], Gb[1], T[1], gD[1], c,
                                     M);
                 }
+#undef bwd_half
             }
 #if LSB_SMEM_RED
             (void)wover;
@@ -878,12 +1040,25 @@ k_blend_fused(Ws w, BlendArgs a, LossArgs L) {
                 const float4 qb = *(const float4*)&sr[k].A;
                 const float4 qc = *(const float4*)&sr[k].kc0;
                 const Frame f = frame_of(q0v, qb.w, gx0f, gy0f);
+#if LSB_PACKED_FWD
+                // (a record with lop < SAT_LOP cannot saturate: its alphas skip the clamp, same bits)
+                if (CUT && ((pipe.ovr >> k) & 1u))      // band pixels: the f64 decisions
+                    fwd_pixels2<true, true>(f, qb, qc, row0, row1, thr, a.cutp, -kap, ovr_nibbles(w, base + k, lane),
+                                            T, cr, cg, cb);
+                else if (qb.w >= SAT_LOP)
+                    fwd_pixels2<false, true>(f, qb, qc, row0, row1, thr, CUT ? a.cutp : 0.f, -kap, OvrNib{}, T, cr,
+                                             cg, cb);
+                else
+                    fwd_pixels2<false, false>(f, qb, qc, row0, row1, thr, CUT ? a.cutp : 0.f, -kap, OvrNib{}, T, cr,
+                                              cg, cb);
+#else
                 if (CUT && ((pipe.ovr >> k) & 1u))      // band pixels: the f64 decisions
                     fwd_pixels<false, false, true>(f, qb, qc, row0, row1, thr, a.cutp, -kap,
                                                    ovr_nibbles(w, base + k, lane), T, T, cr, cg, cb, T);
                 else
                     fwd_pixels<false, false, false>(f, qb, qc, row0, row1, thr, CUT ? a.cutp : 0.f, -kap, OvrNib{},
                                                     T, T, cr, cg, cb, T);
+#endif
             }
             __syncwarp();
         }
