@@ -78,6 +78,10 @@ class ClockSampler:
                 time.sleep(0.02)
         except OSError:
             self.proc = None
+        # the timed region as an NVTX range: `ncu --nvtx --nvtx-include lsb_timed/`
+        # profiles exactly the kernels the line's numbers come from
+        import torch
+        torch.cuda.nvtx.range_push("lsb_timed")
         return self
 
     def _read(self):
@@ -85,6 +89,8 @@ class ClockSampler:
             self.rows.append([x.strip() for x in line.split(",")])
 
     def __exit__(self, *a):
+        import torch
+        torch.cuda.nvtx.range_pop()
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -250,6 +256,10 @@ def profile_figure(name, workload, kernel):
     if not os.path.exists(p):
         return None
     return json.load(open(p)).get(workload, {}).get(kernel)
+
+
+AUX_TRAFFIC_NOTE = ("ncu dram__bytes_read + write summed over every kernel of the timed region (NVTX lsb_timed; "
+                    "cold caches between launches; profiles/r02c_aux_kernels.md)")
 
 
 def survey_step_bytes(N, K, counts, bands, W):
@@ -616,7 +626,8 @@ def run_voxel(args, rank, world, local_rank):
             "gpu_launches": F * 20,
             "roofline": {"bound": "hbm", "kernel": "whole frame (accumulate + try_insert + FoV)",
                          "achieved": vox_gbs, "peak": hbm, "peak_source": hbm_src, "unit": "GB/s",
-                         "frac": vox_gbs / hbm, "traffic": None,
+                         "frac": vox_gbs / hbm, "traffic": profile_figure("traffic.json", "cfg3", "unit"),
+                         "traffic_note": AUX_TRAFFIC_NOTE + " per frame",
                          "algorithmic_bytes_per_frame": vox_bytes / F,
                          "model": "SURVEY.md §8(d): 12 n_pts + 168 g + 8 n_fov per frame",
                          "g_per_frame": g_tot / F, "n_fov_per_frame": fov_tot / F},
@@ -707,7 +718,9 @@ def run_window(args, rank, world, local_rank):
             "clocks": clk.summary(),
             "roofline": {"bound": "hbm", "kernel": "maintain (diff, write-back, compaction, append)", "unit": "GB/s",
                          "achieved": win_bytes / (ms * 1e-3) / 1e9, "peak": peaks()[0], "peak_source": peaks()[1],
-                         "frac": win_bytes / (ms * 1e-3) / 1e9 / peaks()[0], "traffic": None,
+                         "frac": win_bytes / (ms * 1e-3) / 1e9 / peaks()[0],
+                         "traffic": profile_figure("traffic.json", "window", "unit"),
+                         "traffic_note": AUX_TRAFFIC_NOTE + " per maintain",
                          "algorithmic_bytes_per_frame": win_bytes,
                          "model": "16 n_fov (FoV keys in, diff marks) + 152 (removed + moved + added) (f32 row "
                                   "read + write)",
@@ -773,7 +786,9 @@ def run_lidar(args, rank, world, local_rank):
             "higher_is_better": True, "scaling": "replicas", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "roofline": {"bound": "hbm", "kernel": "measurement + H/b", "unit": "GB/s",
                          "achieved": 640 * n / (ms * 1e-3) / 1e9, "peak": peaks()[0], "peak_source": peaks()[1],
-                         "frac": 640 * n / (ms * 1e-3) / 1e9 / peaks()[0], "traffic": None,
+                         "frac": 640 * n / (ms * 1e-3) / 1e9 / peaks()[0],
+                         "traffic": profile_figure("traffic.json", "lidar", "unit"),
+                         "traffic_note": AUX_TRAFFIC_NOTE + " per measurement",
                          "model": "640 B per scan point: point 24 + 7 leaf statistics x 80 + z / row 56",
                          "note": "host-synchronised measurement (one read-back): latency bound"},
             "config": {"workload": "lidar", "scan_points": n, "rows_kept": int(len(meas.z)), "root_len": 0.1,
@@ -873,7 +888,10 @@ def run_ieskf(args, rank, world, local_rank):
             "dtype": "f32", "data": "synthetic",
             "roofline": {"bound": "hbm", "kernel": "one iteration (render + selection + pose rows + H/b)",
                          "achieved": it_gbs, "peak": hbm, "peak_source": hbm_src, "unit": "GB/s",
-                         "frac": it_gbs / hbm, "traffic": None, "algorithmic_bytes_per_iteration": it_bytes,
+                         "frac": it_gbs / hbm, "algorithmic_bytes_per_iteration": it_bytes,
+                         "traffic": (lambda t: None if t is None else t / iters)(
+                             profile_figure("traffic.json", "cfg4", "unit")),
+                         "traffic_note": AUX_TRAFFIC_NOTE + " per update / iterations",
                          "note": "host-synchronised filter iterations: latency bound, not bandwidth bound"},
             "cpu_baseline": cpu,
             "config": {"workload": "cfg4", "gaussians": len(means), "width": 1280, "height": 1024,
