@@ -428,11 +428,13 @@ int lsb_voxmap_keys(const double* pts, int64_t n, double edge, int64_t* keys_out
  * point's leaf slot (may be NULL). */
 int lsb_voxmap_insert_points(const lsb_voxmap* m, const double* pts, int64_t n, int32_t accumulate,
                              int64_t* slots_out, void* stream);
-/* Deterministic accumulate_points (voxmap.py:184-211): the points are
- * grouped by leaf with a stable device radix sort and each leaf adds its
- * group's count / sum / outer, summed in scan order, once - identical
- * statistics run to run (lsb_voxmap_insert_points with accumulate uses
- * f64 atomics instead).  temp: lsb_voxmap_accumulate_temp_bytes(n) bytes. */
+/* Deterministic accumulate_points (voxmap.py:184-211): each leaf adds its
+ * group's count / sum / outer once; the group sums are exact (per-point
+ * terms in 128-bit fixed point, 2^-60, added with integer atomics, which
+ * are order-free) and rounded to f64 once - identical statistics run to run
+ * (lsb_voxmap_insert_points with accumulate uses f64 atomics instead).
+ * Uses the map's claim scratch (restored).  temp:
+ * lsb_voxmap_accumulate_temp_bytes(n) bytes. */
 int lsb_voxmap_accumulate_temp_bytes(int64_t n, size_t* bytes);
 int lsb_voxmap_accumulate(const lsb_voxmap* m, const double* pts, int64_t n, int64_t* slots_out, void* temp,
                           size_t temp_bytes, void* stream);

@@ -5,11 +5,11 @@
 // keys), on the device with no library sort.
 //
 // Radix sort, 8-bit digits, one pass per digit of the key bits in use:
-//   k_rs_hist    per 4096-element tile: the digit histogram (shared-memory
+//   k_rs_hist    per RS_TILE-element tile: the digit histogram (shared-memory
 //                atomics) -> hist[digit][tile]
 //   k_rs_scan    one CTA: exclusive scan of hist in digit-major order, so
 //                tile t's digit-d elements go to offset[d][t] onwards
-//   k_rs_scatter per tile, 8 warps x 512 consecutive elements: each warp
+//   k_rs_scatter per tile, 8 warps x 32 RS_ITEMS consecutive elements: each warp
 //                walks its chunk 32 elements at a time in order; an element's
 //                rank among equal digits is the popcount of its
 //                __match_any_sync peers below it plus the warp's running
@@ -27,8 +27,13 @@ namespace lsb {
 
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
-constexpr int RS_ITEMS = 16;                       // elements per thread
-constexpr int RS_TILE = RS_THREADS * RS_ITEMS;     // 4096
+#ifndef LSB_RS_ITEMS
+#define LSB_RS_ITEMS 4
+#endif
+// elements per thread: 1024-element tiles, so a scan's 100k keys spread over
+// ~100 CTAs (the passes are latency-bound at these sizes, not bandwidth-bound)
+constexpr int RS_ITEMS = LSB_RS_ITEMS;
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;     // 1024
 constexpr int RS_RADIX = 256;
 
 __device__ __forceinline__ unsigned digit_of(uint64_t k, int shift) { return (unsigned)(k >> shift) & 0xffu; }
@@ -173,7 +178,7 @@ cudaError_t launch_sort_pairs(const uint64_t* keys_in, const int32_t* vals_in, u
 }
 
 // ---- segments of a sorted key array ------------------------------------------
-constexpr int SG_TILE = 4096;
+constexpr int SG_TILE = 1024;
 __global__ void __launch_bounds__(RS_THREADS) k_seg_count(const uint64_t* __restrict__ k, int64_t n,
                                                          uint32_t* __restrict__ tile_cnt) {
     __shared__ uint32_t c;

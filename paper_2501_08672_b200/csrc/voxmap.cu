@@ -231,69 +231,117 @@ cudaError_t launch_vox_keys(const double* pts, int64_t n, double edge, int64_t* 
     return cudaGetLastError();
 }
 
-// ---- deterministic accumulate (voxmap.py:184-211) ---------------------------
-// The reference groups a scan by leaf and adds each group's sums to the
-// leaf's statistics in one fixed order (count += n, sum += pts.sum(axis=0),
-// outer += pts^T pts).  Here: every point finds (or creates) its leaf's
-// table slot, the points are radix-sorted stably by slot (scan order kept
-// inside a leaf; log2(cap) + 1 key bits, 3 passes at the default capacity),
-// the runs of equal slots are found, and one thread per run sums its points
-// in scan order and adds the sums to the leaf once - no floating-point
-// atomics, so the statistics are identical run to run.
-size_t sort_temp_bytes(int64_t n);
-cudaError_t launch_sort_pairs(const uint64_t*, const int32_t*, uint64_t*, int32_t*, int64_t, int, void*, cudaStream_t);
-cudaError_t launch_segments(const uint64_t*, int64_t, int64_t*, int64_t*, void*, cudaStream_t);
+static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-__global__ void k_slot_keys(const int64_t* __restrict__ slots, int64_t n, int64_t bad,
-                            unsigned long long* __restrict__ keys) {
+// ---- deterministic leaf statistics: exact fixed-point group sums -------------
+// add_leaf_stats (voxmap.py:204-211) adds each leaf group's (count, sum p,
+// sum p p^T) once per call.  Floating-point atomics would make the sums
+// depend on the arrival order; here every per-point term is converted
+// exactly (to 2^-60, far below f64 resolution at these magnitudes) into a
+// signed 128-bit fixed-point value split over three 64-bit limbs
+// (a 2^64 + b 2^32 + c, b and c < 2^32), and the limbs are added with
+// integer atomics, which are associative: the group sum is the same exact
+// integer whatever the order, converted to f64 once and added to the leaf's
+// statistics once.  Three kernels (local leaf index per touched slot, the
+// atomic adds, the fold) instead of a sort of the points by leaf.
+constexpr int ACC_FRAC = 60;                 // fixed-point fraction bits
+constexpr int ACC_W = 1 + 9 * 3;             // count + 9 values x 3 limbs
+
+__device__ __forceinline__ void fixed_limbs(double v, long long& a, unsigned long long& b, unsigned long long& c) {
+    a = 0;
+    b = c = 0;
+    if (v == 0.0) return;
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    const int e = (int)((bits >> 52) & 0x7ff);
+    unsigned long long m = bits & ((1ull << 52) - 1);
+    if (e) m |= 1ull << 52;
+    const int k = (e ? e : 1) - 1075 + ACC_FRAC;          // y = m 2^k
+    unsigned long long lo, hi;                             // |y| as a 128-bit (hi, lo)
+    if (k >= 0) {
+        lo = k >= 64 ? 0ull : m << k;
+        hi = k == 0 ? 0ull : (k >= 64 ? m << (k - 64) : m >> (64 - k));
+    } else {
+        const int r = -k;
+        lo = r >= 64 ? 0ull : (m + (1ull << (r - 1))) >> r;   // round half up on the magnitude
+        hi = 0;
+    }
+    if (bits >> 63) {                                      // negate the 128-bit value
+        lo = ~lo + 1ull;
+        hi = ~hi + (lo == 0ull ? 1ull : 0ull);
+    }
+    c = lo & 0xffffffffull;
+    b = lo >> 32;
+    a = (long long)hi;
+}
+
+__device__ __forceinline__ double fixed_value(long long a, unsigned long long b, unsigned long long c) {
+    b += c >> 32;
+    c &= 0xffffffffull;
+    a += (long long)(b >> 32);
+    b &= 0xffffffffull;
+    const double hi = (double)a * 18446744073709551616.0;                 // a 2^64 (exact: |a| < 2^53)
+    const double lo = (double)((b << 32) | c);
+    return (hi + lo) * 0x1p-60;
+}
+
+__global__ void k_acc_local(lsb_voxmap m, const int64_t* __restrict__ slots, int64_t n, int64_t* __restrict__ loc_slot,
+                            unsigned long long* __restrict__ nloc, unsigned long long* __restrict__ acc) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t s = slots[i];
-        keys[i] = (unsigned long long)(s >= 0 ? s : bad);
+        if (s < 0 || s >= m.cap) continue;
+        if (atomicCAS(&m.claim[s], 0x7fffffff, -2) != 0x7fffffff) continue;
+        const unsigned long long j = atomicAdd(nloc, 1ull);
+        loc_slot[j] = s;
+        for (int q = 0; q < ACC_W; ++q) acc[j * ACC_W + q] = 0ull;
+        m.claim[s] = (int)j;
     }
 }
 
-__global__ void k_accumulate_runs(lsb_voxmap m, const double* __restrict__ pts, int64_t n,
-                                  const unsigned long long* __restrict__ skeys, const int32_t* __restrict__ perm,
-                                  const int64_t* __restrict__ starts, const int64_t* __restrict__ nseg_p) {
-    const int64_t nseg = *nseg_p;
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nseg; r += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i0 = starts[r], i1 = r + 1 < nseg ? starts[r + 1] : n;
-        const int64_t s = (int64_t)skeys[i0];
-        if (s >= m.cap) continue;                         // points without a leaf (flagged by the insert)
-        double sx = 0.0, sy = 0.0, sz = 0.0, oxx = 0.0, oxy = 0.0, oxz = 0.0, oyy = 0.0, oyz = 0.0, ozz = 0.0;
-        for (int64_t i = i0; i < i1; ++i) {
-            const int64_t q = perm[i];
-            const double x = pts[3 * q], y = pts[3 * q + 1], z = pts[3 * q + 2];
-            sx += x;
-            sy += y;
-            sz += z;
-            oxx += x * x;
-            oxy += x * y;
-            oxz += x * z;
-            oyy += y * y;
-            oyz += y * z;
-            ozz += z * z;
+__global__ void k_acc_add(lsb_voxmap m, const double* __restrict__ pts, const int64_t* __restrict__ slots, int64_t n,
+                          unsigned long long* __restrict__ acc) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = slots[i];
+        if (s < 0 || s >= m.cap) continue;
+        unsigned long long* r = acc + (int64_t)m.claim[s] * ACC_W;
+        const double x = pts[3 * i], y = pts[3 * i + 1], z = pts[3 * i + 2];
+        const double v[9] = {x, y, z, x * x, x * y, x * z, y * y, y * z, z * z};
+        atomicAdd(r, 1ull);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+            long long a;
+            unsigned long long b, c;
+            fixed_limbs(v[q], a, b, c);
+            if (a) atomicAdd(r + 1 + 3 * q, (unsigned long long)a);
+            if (b) atomicAdd(r + 2 + 3 * q, b);
+            if (c) atomicAdd(r + 3 + 3 * q, c);
         }
-        // one run per leaf per call: the only writer of this leaf's statistics
-        m.count[s] += i1 - i0;
-        m.sum[3 * s] += sx;
-        m.sum[3 * s + 1] += sy;
-        m.sum[3 * s + 2] += sz;
-        double* o = m.outer + 6 * s;
-        o[0] += oxx;
-        o[1] += oxy;
-        o[2] += oxz;
-        o[3] += oyy;
-        o[4] += oyz;
-        o[5] += ozz;
     }
 }
 
-static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+__global__ void k_acc_fold(lsb_voxmap m, const int64_t* __restrict__ loc_slot, const unsigned long long* __restrict__ nloc,
+                           const unsigned long long* __restrict__ acc) {
+    const int64_t nl = (int64_t)*nloc;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nl; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = loc_slot[j];
+        const unsigned long long* r = acc + j * ACC_W;
+        double g[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) g[q] = fixed_value((long long)r[1 + 3 * q], r[2 + 3 * q], r[3 + 3 * q]);
+        // one group per leaf per call: the only writer of this leaf's statistics
+        m.count[s] += r[0];
+        m.sum[3 * s] += g[0];
+        m.sum[3 * s + 1] += g[1];
+        m.sum[3 * s + 2] += g[2];
+        double* o = m.outer + 6 * s;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) o[q] += g[3 + q];
+        m.claim[s] = 0x7fffffff;
+    }
+}
 
 size_t vox_accumulate_temp_bytes(int64_t n) {
     const size_t nn = (size_t)(n > 0 ? n : 1);
-    return al256(8 * nn) * 3 + al256(4 * nn) + al256(8 * nn) + al256(8) + sort_temp_bytes(n);
+    return al256(8 * nn) * 2 + al256(8) + al256(8 * ACC_W * nn);
 }
 
 cudaError_t launch_vox_insert(const lsb_voxmap& m, const double* pts, int64_t n, int accumulate, int64_t* slots,
@@ -306,27 +354,19 @@ cudaError_t launch_vox_accumulate(const lsb_voxmap& m, const double* pts, int64_
     char* t = (char*)temp;
     int64_t* sl = (int64_t*)t;
     t += al256(8 * nn);
-    unsigned long long* keys = (unsigned long long*)t;
+    int64_t* loc_slot = (int64_t*)t;
     t += al256(8 * nn);
-    unsigned long long* skeys = (unsigned long long*)t;
-    t += al256(8 * nn);
-    int32_t* perm = (int32_t*)t;
-    t += al256(4 * nn);
-    int64_t* starts = (int64_t*)t;
-    t += al256(8 * nn);
-    int64_t* nseg = (int64_t*)t;
+    unsigned long long* nloc = (unsigned long long*)t;
     t += al256(8);
+    unsigned long long* acc = (unsigned long long*)t;
     if (!slots) slots = sl;
     cudaError_t e = launch_vox_insert(m, pts, n, 0, slots, st);      // find / create every point's leaf
     if (e != cudaSuccess) return e;
-    int bits = 1;
-    while ((1ll << bits) <= m.cap) ++bits;                          // slots < cap, and `cap` marks a miss
-    k_slot_keys<<<grid_for(n), 256, 0, st>>>(slots, n, m.cap, keys);
-    e = launch_sort_pairs((const uint64_t*)keys, nullptr, (uint64_t*)skeys, perm, n, bits, t, st);
+    e = cudaMemsetAsync(nloc, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
-    e = launch_segments((const uint64_t*)skeys, n, starts, nseg, t, st);
-    if (e != cudaSuccess) return e;
-    k_accumulate_runs<<<grid_for(n), 256, 0, st>>>(m, pts, n, skeys, perm, starts, nseg);
+    k_acc_local<<<grid_for(n), 256, 0, st>>>(m, slots, n, loc_slot, nloc, acc);
+    k_acc_add<<<grid_for(n), 256, 0, st>>>(m, pts, slots, n, acc);
+    k_acc_fold<<<grid_for(n), 256, 0, st>>>(m, loc_slot, nloc, acc);
     return cudaGetLastError();
 }
 

@@ -207,7 +207,7 @@ class HashOctree:
         m = self.struct()
         lib = _lib.load()
         if accumulate:
-            # deterministic: grouped by a stable device sort, one add per leaf
+            # deterministic: exact fixed-point group sums (integer atomics), one add per leaf
             nb = ctypes.c_size_t()
             _lib.check(lib.lsb_voxmap_accumulate_temp_bytes(n, ctypes.byref(nb)), "accumulate_temp")
             if getattr(self, "_acc_tmp", None) is None or self._acc_tmp.numel() < nb.value:

@@ -48,8 +48,8 @@ def test_accumulate_points_matches_reference():
 
 
 def test_accumulate_is_deterministic():
-    """The leaf statistics are bit-identical across runs (sorted grouping,
-    fixed-order sums; no floating-point atomics)."""
+    """The leaf statistics are bit-identical across runs (exact fixed-point
+    group sums with integer atomics; no floating-point atomics)."""
     import torch
     d = load("voxmap")
     out = []
