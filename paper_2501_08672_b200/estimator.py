@@ -29,15 +29,26 @@ DIM = 15
 
 @dataclass
 class FilterConfig:
-    """The measurement fields of estimator.FilterConfig (estimator.py:95-115)."""
+    """estimator.FilterConfig (estimator.py:100-115): same fields, order and
+    defaults, so a config loaded for the reference drives this package.  The
+    IMU noise fields belong to imu_propagate (out of scope) and are carried
+    for schema compatibility only."""
 
+    gyro_noise: float = 1e-3
+    accel_noise: float = 1e-2
+    gyro_bias_rw: float = 1e-5
+    accel_bias_rw: float = 1e-4
     lidar_sigma: float = 0.02
-    lidar_gate: float = 1.0
     photo_sigma: float = 0.1
+    lidar_gate: float = 1.0
     pixel_budget: int = 1024
     grad_threshold: float = 0.05
     photo_gate: float = 0.15
     min_pixels: int = 50
+    max_iter: int = 5
+    visual_max_iter: int = 2
+    step_tol: float = 1e-6
+    bias_limit: float = 0.5
     coverage_max_transmittance: float = 0.9
 
 

@@ -70,6 +70,14 @@ def _observed(x, shape, device):
     t = torch.as_tensor(x)
     if t.dtype == torch.uint8:
         return _as(t, shape, device, torch.uint8)
+    if t.dtype == torch.float64:
+        # a frame read by read_ppm is u / 255.0 in f64: keep it as those
+        # bytes (decoded exactly in the kernels) instead of rounding to f32,
+        # which moves the Sobel magnitudes of quantised edges across the
+        # gradient threshold (estimator.py:248-252)
+        u = torch.round(t * 255.0)
+        if bool(((u >= 0) & (u <= 255) & (u / 255.0 == t)).all()):
+            return _as(u.to(torch.uint8), shape, device, torch.uint8)
     return _f32(t, shape, device)
 
 
