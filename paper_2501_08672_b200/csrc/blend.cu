@@ -81,6 +81,7 @@ struct BlendArgs {
     float ik;         // 1 / clamp
     float cutlo, cuthi;    // cut' (1 -+ CUT_BAND): the band where a flagged entry's pairs are decided in f64
     double clamp_d, cut_d;
+    float bflim;           // records with lop <= bflim are bbox-free (common.cuh bbox_free_lim)
 };
 
 // Per-column liveness threshold of a record: T must reach t_min for pixels
@@ -345,6 +346,9 @@ __device__ __forceinline__ void fwd_pixels(const Frame& f, float4 qb, float4 qc,
     }
 }
 
+#ifndef LSB_BBOX_FREE
+#define LSB_BBOX_FREE 1       // bbox-free records skip the per-pixel bbox test (common.cuh bbox_free_lim)
+#endif
 #ifndef LSB_PACKED_FWD
 #define LSB_PACKED_FWD 1
 #endif
@@ -766,6 +770,7 @@ __device__ __forceinline__ void bwd_walk(const Ws& w, const BlendArgs& a, RecPip
     const float k2 = -2.0f / (float)LOG2E;     // undo the exp2 scaling: a_k = A k2, e = E k2
     const float kap = a.clamp;
     const float gx0f = (float)gx0, gy0f = (float)gy0;
+    const int oy = gy0 - (lane >> 2);          // the tile's first row
     pipe.start = start;
     pipe.end = end;
     pipe.begin(w, lane);
@@ -786,10 +791,24 @@ __device__ __forceinline__ void bwd_walk(const Ws& w, const BlendArgs& a, RecPip
             const float4 q1 = *(const float4*)&sr[k].A;          // A s E lop
             const float4 q2 = *(const float4*)&sr[k].kc0;        // clamp * (c0 c1 c2 z)
             const int4 q3 = *(const int4*)&sr[k].bbx;            // bbx bby id ebase
-            const int cx0 = (q3.x & 0xffff) - gx0, cx1 = (q3.x >> 16) - gx0;
-            const int ry0 = (q3.y & 0xffff) - gy0, ry1 = (q3.y >> 16) - gy0;
-            const bool row0 = ry0 <= 0 && ry1 > 0, row1 = ry0 <= 8 && ry1 > 8;
-            const bool over = alive && cx0 < RUN && cx1 > 0 && (row0 || row1);
+            // a bbox-free record (warp-uniform, alpha_cut > 0 only): every live
+            // lane walks the half-tiles the bbox rows reach, deciding on alpha
+            const bool bfree = LSB_BBOX_FREE && a.cut > 0.f && q1.w <= a.bflim;
+            bool row0, row1, over;
+            int cx0 = 0, cx1 = RUN;
+            if (bfree) {
+                const int y0 = (q3.y & 0xffff) - oy, y1 = (q3.y >> 16) - oy;
+                row0 = y0 < 8 && y1 > 0;
+                row1 = y0 < 16 && y1 > 8;
+                over = alive;
+            } else {
+                cx0 = (q3.x & 0xffff) - gx0;
+                cx1 = (q3.x >> 16) - gx0;
+                const int ry0 = (q3.y & 0xffff) - gy0, ry1 = (q3.y >> 16) - gy0;
+                row0 = ry0 <= 0 && ry1 > 0;
+                row1 = ry0 <= 8 && ry1 > 8;
+                over = alive && cx0 < RUN && cx1 > 0 && (row0 || row1);
+            }
             // accumulators: colour (3, x clamp) and the moments sum gd, gd u,
             // gd dy, gd u^2, gd u dy, gd dy^2 with gd = alpha dL/dalpha
             // (-0 is the additive identity the compiler may fold: -0 + x == x for every x)
@@ -799,7 +818,8 @@ __device__ __forceinline__ void bwd_walk(const Ws& w, const BlendArgs& a, RecPip
                 // warp-uniform from here: lanes without work get +inf thresholds
                 float thr[RUN];
 #pragma unroll
-                for (int j = 0; j < RUN; ++j) thr[j] = over ? col_thr(j, cx0, cx1, a.tmin) : __int_as_float(0x7f800000);
+                for (int j = 0; j < RUN; ++j)
+                    thr[j] = !over ? __int_as_float(0x7f800000) : (bfree ? a.tmin : col_thr(j, cx0, cx1, a.tmin));
                 const Frame f = frame_of(q0, q1.w, gx0f, gy0f);
 #if LSB_PACKED_BWD
 #define bwd_half bwd_half2
@@ -955,6 +975,7 @@ static BlendArgs blend_args(const lsb_settings& s, int W, int H) {
     a.cuthi = (float)(s.alpha_cut / s.alpha_clamp * (1.0 + CUT_BAND));
     a.clamp_d = s.alpha_clamp;
     a.cut_d = s.alpha_cut;
+    a.bflim = bbox_free_lim(s.alpha_cut, s.alpha_clamp, s.footprint_sigma);
     return a;
 }
 
@@ -1028,16 +1049,28 @@ k_blend_fused(Ws w, BlendArgs a, LossArgs L) {
 #pragma unroll kFusedFwdUnroll
             for (int k = 0; k < nb; ++k) {
                 const int4 qi = *(const int4*)&sr[k].bbx;
-                const int cx0 = (qi.x & 0xffff) - gx0, cx1 = (qi.x >> 16) - gx0;
-                const int ry0 = (qi.y & 0xffff) - gy0, ry1 = (qi.y >> 16) - gy0;
-                const bool row0 = ry0 <= 0 && ry1 > 0, row1 = ry0 <= 8 && ry1 > 8;
-                if (cx0 >= RUN || cx1 <= 0 || !(row0 || row1)) continue;
-                if (alive) last = base + k + 1;
-                float thr[RUN];
-#pragma unroll
-                for (int j = 0; j < RUN; ++j) thr[j] = col_thr(j, cx0, cx1, a.tmin);
-                const float4 q0v = *(const float4*)&sr[k].mxh;
                 const float4 qb = *(const float4*)&sr[k].A;
+                bool row0, row1;
+                float thr[RUN];
+                if (CUT && LSB_BBOX_FREE && qb.w <= a.bflim) {
+                    // bbox-free record (warp-uniform): every pixel decides on alpha alone;
+                    // a half-tile is walked iff the bbox rows reach it
+                    const int y0 = (qi.y & 0xffff) - oy, y1 = (qi.y >> 16) - oy;
+                    row0 = y0 < 8 && y1 > 0;
+                    row1 = y0 < 16 && y1 > 8;
+#pragma unroll
+                    for (int j = 0; j < RUN; ++j) thr[j] = a.tmin;
+                } else {
+                    const int cx0 = (qi.x & 0xffff) - gx0, cx1 = (qi.x >> 16) - gx0;
+                    const int ry0 = (qi.y & 0xffff) - gy0, ry1 = (qi.y >> 16) - gy0;
+                    row0 = ry0 <= 0 && ry1 > 0;
+                    row1 = ry0 <= 8 && ry1 > 8;
+                    if (cx0 >= RUN || cx1 <= 0 || !(row0 || row1)) continue;
+#pragma unroll
+                    for (int j = 0; j < RUN; ++j) thr[j] = col_thr(j, cx0, cx1, a.tmin);
+                }
+                if (alive) last = base + k + 1;
+                const float4 q0v = *(const float4*)&sr[k].mxh;
                 const float4 qc = *(const float4*)&sr[k].kc0;
                 const Frame f = frame_of(q0v, qb.w, gx0f, gy0f);
 #if LSB_PACKED_FWD

@@ -1,6 +1,7 @@
 // Shared device-side definitions for the B200 splat path.
 #pragma once
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
 
 #include "lsb.h"
@@ -87,6 +88,25 @@ __device__ __forceinline__ CullGeo make_cull_geo(double mux, double muy, double 
 #define LSB_CUT_BAND_LOG2 17
 #endif
 constexpr double CUT_BAND = 1.0 / (double)(1 << LSB_CUT_BAND_LOG2);
+// Bbox-free records.  With alpha_cut > 0 the footprint is nsig =
+// min(footprint_sigma, sqrt(2 ln(op / cut))) sigmas (raster.py:160-166).
+// When the cut sets it, the bbox square holds the whole ellipse q <= 2 ln(op
+// / cut) (its extent along any axis is at most nsig sqrt(lambda_max), the
+// bbox radius), i.e. every pixel whose f64 alpha reaches the cut: a pixel
+// outside the bbox never composites, so the walks may drop the per-pixel bbox
+// test for such a record and decide on alpha alone.  The one exception, f32
+// alphas of out-of-bbox pixels inside the alpha_cut band (the sliver just
+// beyond the ellipse's extreme points), gets f64 "skip" decisions from the
+// band search, which for these records scans the tile, not the bbox.  A
+// record is bbox-free iff lop = log2(op / clamp) <= this limit (f32, the same
+// value and comparison in the binning and the blend; 0.01 below the exact
+// boundary log2(cut / clamp) + fs^2 / (2 ln 2), so lop's rounding cannot
+// cross it).
+inline float bbox_free_lim(double cut, double clamp, double footprint_sigma) {
+    if (!(cut > 0.0)) return -INFINITY;
+    return (float)(log2(cut / clamp) + footprint_sigma * footprint_sigma / (2.0 * 0.69314718055994530942) - 0.01);
+}
+
 // A sorted tile entry (tile_slot[j]) with band pixels carries this bit; the
 // slot is tile_slot[j] & SLOT_MASK.
 constexpr int32_t OVR_BIT = 1 << 30;

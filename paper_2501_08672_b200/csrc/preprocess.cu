@@ -429,7 +429,7 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 // it, and keep the f32-error evidence.  Returns the row, or -1 when the mask
 // table is full (reported as a capacity overflow: regrow and redo).
 __device__ __forceinline__ int band_pixel(const Ws& w, const CullGeo& g, const Rec& r, double clamp, double cut, int idx,
-                                       int ox, int oy, int x, int ry) {
+                                       int ox, int oy, int x, int ry, bool inbox) {
     if (idx < 0) {
         idx = (int)atomicAdd(&w.ctr[9], 1ull);
         if (idx >= w.ovr_cap) {
@@ -440,7 +440,7 @@ __device__ __forceinline__ int band_pixel(const Ws& w, const CullGeo& g, const R
         for (int q = 0; q < 16; ++q) w.ovr[(size_t)idx * 16 + q] = 0u;
     }
     const double ad = exact_alpha(g, clamp, (double)(ox + x), (double)(oy + ry));
-    const bool take = !(ad < cut);
+    const bool take = inbox && !(ad < cut);       // outside the bbox: not in the pixel's list
     const int bit = ry * TILE + x;
     uint32_t* m = w.ovr + (size_t)idx * 16;
     m[bit >> 5] |= 1u << (bit & 31);
@@ -456,7 +456,8 @@ __device__ __forceinline__ int band_pixel(const Ws& w, const CullGeo& g, const R
     return idx;
 }
 
-__device__ __forceinline__ bool band_search(const Ws& w, double clamp, double cut, int64_t e, int slot, int tile) {
+__device__ __forceinline__ bool band_search(const Ws& w, double clamp, double cut, float bflim, int64_t e, int slot,
+                                            int tile) {
     const CullGeo& g = w.cgeo[slot];
     const float qc = g.qcf;
     const float W = (float)(4.0 * CUT_BAND) + 4e-6f * fabsf(qc) + 1e-6f;
@@ -467,10 +468,14 @@ __device__ __forceinline__ bool band_search(const Ws& w, double clamp, double cu
     const int x0 = r.bbx & 0xffff, x1 = r.bbx >> 16, y0 = r.bby & 0xffff, y1 = r.bby >> 16;
     const float mxr = (float)(g.mux - (double)ox), myr = (float)(g.muy - (double)oy);
     const float k = g.kf, sr = g.sf, ic0 = g.ic0f;
-    const int cx0 = max(ox, x0) - ox, cx1 = min(ox + TILE, x1) - 1 - ox;     // tile-relative columns
+    // a bbox-free record (bbox_free_lim) is searched over the whole tile, not
+    // only its bbox: out-of-bbox band pixels get "skip"
+    const bool bf = r.lop <= bflim;
+    const int bx0 = bf ? ox : x0, bx1 = bf ? ox + TILE : x1, by0 = bf ? oy : y0, by1 = bf ? oy + TILE : y1;
+    const int cx0 = max(ox, bx0) - ox, cx1 = min(ox + TILE, bx1) - 1 - ox;     // tile-relative columns
     const float dyx = sqrt_approx(qo / k) + 1e-3f;
-    const int ry0 = max(max(0, y0 - oy), __float2int_ru(myr - dyx));
-    const int ry1 = min(min(TILE, y1 - oy), __float2int_rd(myr + dyx) + 1);
+    const int ry0 = max(max(0, by0 - oy), __float2int_ru(myr - dyx));
+    const int ry1 = min(min(TILE, by1 - oy), __float2int_rd(myr + dyx) + 1);
     if (ry0 >= ry1 || cx0 > cx1) return false;
     // an entry whose pixel rectangle lies inside the inner ellipse has no band
     // pixel: q is convex, so its maximum over the rectangle is at a corner
@@ -504,7 +509,8 @@ __device__ __forceinline__ bool band_search(const Ws& w, double clamp, double cu
         for (int x = xa; x <= xb; ++x) {
             if (x > xl && x < xr) x = xr;                 // jump over the inner run
             if (x > xb) break;
-            idx = band_pixel(w, g, r, clamp, cut, idx, ox, oy, x, ry);
+            const bool inbox = ox + x >= x0 && ox + x < x1 && oy + ry >= y0 && oy + ry < y1;
+            idx = band_pixel(w, g, r, clamp, cut, idx, ox, oy, x, ry, inbox);
             if (idx < 0) return false;                    // (no room: a capacity overflow was reported)
         }
     }
@@ -516,7 +522,7 @@ __device__ __forceinline__ bool band_search(const Ws& w, double clamp, double cu
 // Scatter with the (slot, tile) pairs the preprocess emitted: one thread per
 // intersection claims a position in its tile's bucket (and, with alpha_cut
 // > 0, searches its entry for alpha_cut band pixels: band_search).
-__global__ void __launch_bounds__(256) k_scatter_emitted(Ws w, double clamp, double cut) {
+__global__ void __launch_bounds__(256) k_scatter_emitted(Ws w, double clamp, double cut, float bflim) {
     if (w.ctr[1] > (unsigned long long)w.cap) return;     // overflow: tiles published empty
     const int64_t I = (int64_t)w.ctr[1];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -524,7 +530,7 @@ __global__ void __launch_bounds__(256) k_scatter_emitted(Ws w, double clamp, dou
         const int t = w.emit_tile[e];
         const int slot = w.emit_slot[e];
         const int j = w.tile_start[t] + atomicAdd(&w.tile_cursor[t], 1);
-        const bool band = cut > 0.0 && band_search(w, clamp, cut, e, slot, t);
+        const bool band = cut > 0.0 && band_search(w, clamp, cut, bflim, e, slot, t);
         w.tile_e[j] = (int32_t)e;
         w.tile_slot[j] = slot | (band ? OVR_BIT : 0);      // the flag rides on the slot (sorts mask it)
     }
@@ -918,7 +924,8 @@ cudaError_t launch_preprocess(const lsb_params& p, const lsb_camera& cam, const 
     const int st_smem = (int)sizeof(int) * (w.ntiles + w.ntiles / 32 + 1);
     if (st_smem > 48 * 1024) cudaFuncSetAttribute(k_scan_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, st_smem);
     k_scan_tiles<<<1, ST_THREADS, st_smem, st>>>(w);
-    k_scatter_emitted<<<8 * 148, 256, 0, st>>>(w, s.alpha_clamp, s.alpha_cut);
+    k_scatter_emitted<<<8 * 148, 256, 0, st>>>(w, s.alpha_clamp, s.alpha_cut,
+                                               bbox_free_lim(s.alpha_cut, s.alpha_clamp, s.footprint_sigma));
     k_tile_sort<<<(w.ntiles + 3) / 4, 128, 0, st>>>(w);
     cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_sort_smem());
     k_tile_sort_big<<<148, 256, tile_sort_smem(), st>>>(w);

@@ -11,7 +11,8 @@ libsplat_b200.so (include/lsb.h) working on HBM-resident torch tensors:
     K5 chain       (per-splat chain rule, pose reduction)               f64
 
 Outputs are device tensors (image (H,W,3) f32, final_transmittance (H,W),
-contrib_count (H,W) int32); `RenderOutput.numpy()` gives host copies.
+contrib_count (H,W) int32) that numpy reads through np.asarray (a host copy,
+HostReadable); `RenderOutput.numpy()` gives all of them as f64 / int64.
 """
 
 from __future__ import annotations
@@ -212,6 +213,23 @@ class PoseGradient:
 
     def as_vector(self) -> np.ndarray:
         return np.concatenate([self.rho, self.tau])
+
+
+class HostReadable(torch.Tensor):
+    """A device tensor that numpy can read: np.asarray(x) (what the
+    reference's consumers of a render call -- write_ppm, metrics.psnr,
+    raster.py:511-517, metrics.py:12-22) copies it to the host.  Torch
+    operations on it return plain tensors (no subclass dispatch)."""
+
+    __torch_function__ = torch._C._disabled_torch_function_impl
+
+    def __array__(self, dtype=None, copy=None):
+        a = self.detach().cpu().as_subclass(torch.Tensor).numpy()
+        return a if dtype is None else a.astype(dtype, copy=False)
+
+
+def host_readable(t: Optional[torch.Tensor]) -> Optional[torch.Tensor]:
+    return None if t is None else t.as_subclass(HostReadable)
 
 
 @dataclass
@@ -510,8 +528,9 @@ def render(source, T_wc, cam, settings: RasterSettings = RasterSettings(), retai
             break
         cap = int(I * 1.25) + 1024
     _CAP_HINT[key] = int(I * 1.25) + 1024
-    return RenderOutput(image=image, final_transmittance=t_final, contrib_count=n_contrib,
-                        cache=state if retain_cache else None, depth=depth)
+    return RenderOutput(image=host_readable(image), final_transmittance=host_readable(t_final),
+                        contrib_count=host_readable(n_contrib), cache=state if retain_cache else None,
+                        depth=host_readable(depth))
 
 
 def backward(out: RenderOutput, grad_image, T_ic=None):

@@ -174,3 +174,22 @@ def test_generic_ieskf_update_equals_the_visual_update():
     assert np.array_equal(p1.T_WI.R, p2.T_WI.R) and np.array_equal(p1.T_WI.t, p2.T_WI.t)
     assert np.array_equal(c1, c2)
     assert np.abs(p1.T_WI.t - d["post_t"]).max() <= 1e-4
+
+
+def test_render_outputs_are_numpy_readable():
+    """The reference's consumers of a render (write_ppm raster.py:511-517,
+    metrics.psnr metrics.py:12-22) call np.asarray on the image."""
+    from golden_io import case_inputs, load
+    from paper_2501_08672_b200.geometry import SE3
+    from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
+    d = load("room_v0_cut1")
+    P, _, _, cam, st = case_inputs(d)
+    out = render(GaussianArrays(P["means"], P["rots"], P["scales"], P["opacities"], P["shs"]),
+                 SE3(d["R_wc"], d["t_wc"]), cam, RasterSettings(alpha_cut=float(st.alpha_cut)))
+    img = np.asarray(out.image, dtype=float)
+    assert img.shape == (cam.height, cam.width, 3)
+    assert np.array_equal(img, out.image.cpu().numpy().astype(np.float64))
+    assert np.array_equal(np.asarray(out.final_transmittance), out.final_transmittance.cpu().numpy())
+    img8 = np.clip(np.round(np.asarray(out.image) * 255.0), 0, 255).astype(np.uint8)
+    assert img8.shape == img.shape
+    assert np.abs(img - np.asarray(d["image"])).max() <= 1e-4
