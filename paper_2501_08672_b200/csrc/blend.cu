@@ -349,6 +349,9 @@ __device__ __forceinline__ void fwd_pixels(const Frame& f, float4 qb, float4 qc,
 #ifndef LSB_BBOX_FREE
 #define LSB_BBOX_FREE 1       // bbox-free records skip the per-pixel bbox test (common.cuh bbox_free_lim)
 #endif
+#ifndef LSB_FWD_BOTH
+#define LSB_FWD_BOTH 1        // fused forward: records reaching both half-tiles walk them without a branch
+#endif
 #ifndef LSB_PACKED_FWD
 #define LSB_PACKED_FWD 1
 #endif
@@ -371,7 +374,9 @@ __device__ __forceinline__ float take_w(float w, float T, float thr, float a, fl
     return r;
 }
 
-template <bool OVR, bool SAT>
+// BOTH: the caller knows both half-tiles are walked (warp-uniform), so the
+// halves carry no branch between them and their pairs can interleave.
+template <bool OVR, bool SAT, bool BOTH = false>
 __device__ __forceinline__ void fwd_pixels2(const Frame& f, float4 qb, float4 qc, bool row0, bool row1,
                                             const float* thr, float cut, float nkap, const OvrNib& o,
                                             float (&T)[2][RUN], float (&cr)[2][RUN], float (&cg)[2][RUN],
@@ -380,7 +385,7 @@ __device__ __forceinline__ void fwd_pixels2(const Frame& f, float4 qb, float4 qc
     const float2 C0 = make_float2(qc.x, qc.x), C1 = make_float2(qc.y, qc.y), C2 = make_float2(qc.z, qc.z);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-        if (!(h ? row1 : row0)) continue;
+        if (!BOTH && !(h ? row1 : row0)) continue;
         float dy, u0, edy;
         row_terms(f, qb.y, qb.z, 8.f * h, dy, u0, edy);
         const float2 E2 = make_float2(edy, edy), U0 = make_float2(u0, u0);
@@ -694,15 +699,13 @@ __device__ __forceinline__ void take_wa(float w, float T, float thr, float a, fl
 // sums (colour, moments) are accumulated per pair lane and folded once, and
 // the moment sums use fma (S0 + a da, S1 + gd u, S2 + gu u): never a packed
 // mul feeding an add, which ptxas would contract.
-template <bool SAT, bool OVR = false>
-__device__ __forceinline__ void bwd_half2(const Frame& f, float4 q1, bool rin, float dyoff, const float* thr,
-                                          const BlendArgs& a, float kap, float4 q2, const float* Gr, const float* Gg,
-                                          const float* Gb, float* T, float* gD, float* c, float* M,
-                                          const OvrNib& o = OvrNib{}, int h = 0) {
-    float dy, u0, edy;
+// The alphas of one half-tile's 4 pixels per lane (2 packed pairs).
+template <bool SAT>
+__device__ __forceinline__ void bwd_alpha2(const Frame& f, float4 q1, float dyoff, float& dy, float2 (&al)[RUN / 2],
+                                           float2 (&uu)[RUN / 2]) {
+    float u0, edy;
     row_terms(f, q1.y, q1.z, dyoff, dy, u0, edy);
     const float2 A2 = make_float2(q1.x, q1.x), E2 = make_float2(edy, edy), U0 = make_float2(u0, u0);
-    float2 al[RUN / 2], uu[RUN / 2];
 #pragma unroll
     for (int p = 0; p < RUN / 2; ++p) {
         uu[p] = __fadd2_rn(U0, make_float2((float)(2 * p), (float)(2 * p + 1)));
@@ -710,6 +713,81 @@ __device__ __forceinline__ void bwd_half2(const Frame& f, float4 q1, bool rin, f
         const float e0 = ex2_approx(q.x), e1 = ex2_approx(q.y);
         al[p] = SAT ? make_float2(__saturatef(e0), __saturatef(e1)) : make_float2(e0, e1);
     }
+}
+
+// Per-half sums of the packed backward update (colour x3, moments x3).
+struct HalfSums {
+    float2 s0, s1, s2, S0, S1, S2;
+};
+
+// One packed pixel pair p of a half-tile: the T recurrence bit-identical to
+// the forward's (w = T a, T + ws (-clamp) with ws = 0 for a pair that does
+// not composite), gD -= w g.c', dL/dalpha, and the pair's terms of the
+// record's sums; the moment sums use fma (S0 + a da, S1 + gd u, S2 + gu u):
+// never a packed mul feeding an add, which ptxas would contract.
+template <bool SAT, bool OVR>
+__device__ __forceinline__ void bwd_pair2(int p, float2 al, float2 uu, const float* thr, const BlendArgs& a,
+                                          float2 C0, float2 C1, float2 C2, float2 NK, float2 IK, const float* Gr,
+                                          const float* Gg, const float* Gb, float* T, float* gD, HalfSums& hs,
+                                          const OvrNib& o, int h) {
+    const int j = 2 * p;
+    float2 t2 = make_float2(T[j], T[j + 1]);
+    const float2 w = __fmul2_rn(t2, al);
+    float2 ws, as;
+    take_wa<SAT>(w.x, t2.x, thr[j], al.x, OVR ? ovr_cut(o, h, j, a.cutp) : a.cutp, ws.x, as.x);
+    take_wa<SAT>(w.y, t2.y, thr[j + 1], al.y, OVR ? ovr_cut(o, h, j + 1, a.cutp) : a.cutp, ws.y, as.y);
+    const float2 g0 = make_float2(Gr[j], Gr[j + 1]), g1 = make_float2(Gg[j], Gg[j + 1]),
+                 g2 = make_float2(Gb[j], Gb[j + 1]);
+    const float2 gc = __ffma2_rn(g0, C0, __ffma2_rn(g1, C1, __fmul2_rn(g2, C2)));     // g . c'
+    float2 d2 = make_float2(gD[j], gD[j + 1]);
+    d2 = __ffma2_rn(make_float2(-ws.x, -ws.y), gc, d2);                             // gD -= w g.c'
+    const float2 ia = __fadd2_rn(IK, make_float2(-al.x, -al.y));
+    const float2 r = make_float2(rcp_approx(ia.x), rcp_approx(ia.y));
+    const float2 da = __ffma2_rn(make_float2(-d2.x, -d2.y), r, __fmul2_rn(t2, gc));  // T g.c' - gD / (1/clamp - a)
+    hs.s0 = __ffma2_rn(ws, g0, hs.s0);
+    hs.s1 = __ffma2_rn(ws, g1, hs.s1);
+    hs.s2 = __ffma2_rn(ws, g2, hs.s2);
+    hs.S0 = __ffma2_rn(as, da, hs.S0);                                              // sum gd
+    const float2 gd = __fmul2_rn(as, da);
+    hs.S1 = __ffma2_rn(gd, uu, hs.S1);                                              // sum gd u
+    hs.S2 = __ffma2_rn(__fmul2_rn(gd, uu), uu, hs.S2);                              // sum gd u^2
+    t2 = __ffma2_rn(ws, NK, t2);
+    T[j] = t2.x;
+    T[j + 1] = t2.y;
+    gD[j] = d2.x;
+    gD[j + 1] = d2.y;
+}
+
+__device__ __forceinline__ void half_sums_zero(HalfSums& hs) {
+    hs.s0 = make_float2(-0.f, -0.f);
+    hs.s1 = hs.s2 = hs.S0 = hs.S1 = hs.S2 = hs.s0;
+}
+
+// Fold one half's sums into the record's colour sums c and moments M.
+__device__ __forceinline__ void half_sums_fold(const HalfSums& hs, float dy, float* c, float* M) {
+    c[0] += hs.s0.x + hs.s0.y;
+    c[1] += hs.s1.x + hs.s1.y;
+    c[2] += hs.s2.x + hs.s2.y;
+    const float m0 = hs.S0.x + hs.S0.y, m1 = hs.S1.x + hs.S1.y, m2 = hs.S2.x + hs.S2.y;
+    M[0] += m0;
+    M[1] += m1;
+    M[2] = fmaf(m0, dy, M[2]);
+    M[3] += m2;
+    M[4] = fmaf(m1, dy, M[4]);
+    M[5] = fmaf(m0 * dy, dy, M[5]);
+}
+
+// bwd_half with packed FP32 on pixel pairs (per component bwd_pixel's
+// arithmetic; the per-record sums are accumulated per pair lane and folded
+// once per half).
+template <bool SAT, bool OVR = false>
+__device__ __forceinline__ void bwd_half2(const Frame& f, float4 q1, bool rin, float dyoff, const float* thr,
+                                          const BlendArgs& a, float kap, float4 q2, const float* Gr, const float* Gg,
+                                          const float* Gb, float* T, float* gD, float* c, float* M,
+                                          const OvrNib& o = OvrNib{}, int h = 0) {
+    float dy;
+    float2 al[RUN / 2], uu[RUN / 2];
+    bwd_alpha2<SAT>(f, q1, dyoff, dy, al, uu);
     if (!OVR) {        // (with band pixels an overridden pair may composite below cut')
         const float amax = fmaxf(fmaxf(al[0].x, al[0].y), fmaxf(al[1].x, al[1].y));
         if (!__any_sync(0xffffffffu, rin && amax >= a.cutp)) return;
@@ -717,46 +795,12 @@ __device__ __forceinline__ void bwd_half2(const Frame& f, float4 q1, bool rin, f
     if (!rin) return;
     const float2 C0 = make_float2(q2.x, q2.x), C1 = make_float2(q2.y, q2.y), C2 = make_float2(q2.z, q2.z);
     const float2 NK = make_float2(-kap, -kap), IK = make_float2(a.ik, a.ik);
-    float2 s0 = make_float2(-0.f, -0.f), s1 = s0, s2 = s0, S0 = s0, S1 = s0, S2 = s0;
+    HalfSums hs;
+    half_sums_zero(hs);
 #pragma unroll
-    for (int p = 0; p < RUN / 2; ++p) {
-        const int j = 2 * p;
-        float2 t2 = make_float2(T[j], T[j + 1]);
-        const float2 w = __fmul2_rn(t2, al[p]);
-        float2 ws, as;
-        take_wa<SAT>(w.x, t2.x, thr[j], al[p].x, OVR ? ovr_cut(o, h, j, a.cutp) : a.cutp, ws.x, as.x);
-        take_wa<SAT>(w.y, t2.y, thr[j + 1], al[p].y, OVR ? ovr_cut(o, h, j + 1, a.cutp) : a.cutp, ws.y, as.y);
-        const float2 g0 = make_float2(Gr[j], Gr[j + 1]), g1 = make_float2(Gg[j], Gg[j + 1]),
-                     g2 = make_float2(Gb[j], Gb[j + 1]);
-        const float2 gc = __ffma2_rn(g0, C0, __ffma2_rn(g1, C1, __fmul2_rn(g2, C2)));     // g . c'
-        float2 d2 = make_float2(gD[j], gD[j + 1]);
-        d2 = __ffma2_rn(make_float2(-ws.x, -ws.y), gc, d2);                             // gD -= w g.c'
-        const float2 ia = __fadd2_rn(IK, make_float2(-al[p].x, -al[p].y));
-        const float2 r = make_float2(rcp_approx(ia.x), rcp_approx(ia.y));
-        const float2 da = __ffma2_rn(make_float2(-d2.x, -d2.y), r, __fmul2_rn(t2, gc));  // T g.c' - gD / (1/clamp - a)
-        s0 = __ffma2_rn(ws, g0, s0);
-        s1 = __ffma2_rn(ws, g1, s1);
-        s2 = __ffma2_rn(ws, g2, s2);
-        S0 = __ffma2_rn(as, da, S0);                                                    // sum gd
-        const float2 gd = __fmul2_rn(as, da);
-        S1 = __ffma2_rn(gd, uu[p], S1);                                                 // sum gd u
-        S2 = __ffma2_rn(__fmul2_rn(gd, uu[p]), uu[p], S2);                              // sum gd u^2
-        t2 = __ffma2_rn(ws, NK, t2);
-        T[j] = t2.x;
-        T[j + 1] = t2.y;
-        gD[j] = d2.x;
-        gD[j + 1] = d2.y;
-    }
-    c[0] += s0.x + s0.y;
-    c[1] += s1.x + s1.y;
-    c[2] += s2.x + s2.y;
-    const float m0 = S0.x + S0.y, m1 = S1.x + S1.y, m2 = S2.x + S2.y;
-    M[0] += m0;
-    M[1] += m1;
-    M[2] = fmaf(m0, dy, M[2]);
-    M[3] += m2;
-    M[4] = fmaf(m1, dy, M[4]);
-    M[5] = fmaf(m0 * dy, dy, M[5]);
+    for (int p = 0; p < RUN / 2; ++p)
+        bwd_pair2<SAT, OVR>(p, al[p], uu[p], thr, a, C0, C1, C2, NK, IK, Gr, Gg, Gb, T, gD, hs, o, h);
+    half_sums_fold(hs, dy, c, M);
 }
 
 // The backward's record walk over one tile's list [start, end): the forward
@@ -1050,7 +1094,7 @@ k_blend_fused(Ws w, BlendArgs a, LossArgs L) {
             for (int k = 0; k < nb; ++k) {
                 const int4 qi = *(const int4*)&sr[k].bbx;
                 const float4 qb = *(const float4*)&sr[k].A;
-                bool row0, row1;
+                bool row0, row1, both = false;
                 float thr[RUN];
                 if (CUT && LSB_BBOX_FREE && qb.w <= a.bflim) {
                     // bbox-free record (warp-uniform): every pixel decides on alpha alone;
@@ -1058,6 +1102,7 @@ k_blend_fused(Ws w, BlendArgs a, LossArgs L) {
                     const int y0 = (qi.y & 0xffff) - oy, y1 = (qi.y >> 16) - oy;
                     row0 = y0 < 8 && y1 > 0;
                     row1 = y0 < 16 && y1 > 8;
+                    both = row0 && row1;
 #pragma unroll
                     for (int j = 0; j < RUN; ++j) thr[j] = a.tmin;
                 } else {
@@ -1078,6 +1123,9 @@ k_blend_fused(Ws w, BlendArgs a, LossArgs L) {
                 if (CUT && ((pipe.ovr >> k) & 1u))      // band pixels: the f64 decisions
                     fwd_pixels2<true, true>(f, qb, qc, row0, row1, thr, a.cutp, -kap, ovr_nibbles(w, base + k, lane),
                                             T, cr, cg, cb);
+                else if (LSB_FWD_BOTH && CUT && both && qb.w < SAT_LOP)     // the common case: interleaved halves
+                    fwd_pixels2<false, false, true>(f, qb, qc, true, true, thr, a.cutp, -kap, OvrNib{}, T, cr, cg,
+                                                    cb);
                 else if (qb.w >= SAT_LOP)
                     fwd_pixels2<false, true>(f, qb, qc, row0, row1, thr, CUT ? a.cutp : 0.f, -kap, OvrNib{}, T, cr,
                                              cg, cb);
