@@ -482,7 +482,7 @@ def run_ours(args, wl, rank, world, local_rank):
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "peak_source": hbm_src,
                          "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                          "algorithmic_bytes_per_launch": ab[dom], "avg_launch_ms": dom_ms,
-                         "note": "blend is FP32-issue bound (SURVEY.md §8(d)); see profiles/"},
+                         "note": "the blend is compute-side bound (SURVEY.md §8(d)): its records, lists and frame stay in L2; see issue_roofline and profiles/README.md (dependency latency at 3.7 warps per scheduler)"},
             "issue_roofline": None if not issue else {
                 "kernel": dom, "unit": "warp-inst/s", "warp_inst_per_launch": issue["warp_inst_per_launch"],
                 "achieved": issue["warp_inst_per_launch"] / (dom_ms * 1e-3),
