@@ -326,7 +326,10 @@ def run_ours(args, wl, rank, world, local_rank):
         from paper_2501_08672_b200.raster import render_bin
         render_bin(eng.state, stream)
         counts.append(eng.state.read_counts(stream)[:2])
-    allreduce = (lambda t: dist.all_reduce(t)) if world > 1 else None
+    # the engine's exchange: bucketed async all-reduce (mean | rot | scale +
+    # opacity | sh), Adam stepping each bucket as soon as it is reduced
+    from paper_2501_08672_b200.dist import make_allreduce
+    allreduce = make_allreduce() if world > 1 else None
     exchange = "nccl"
     if world > 1 and args.exchange == "p2p":
         # fused gradient exchange + Adam over NVLink peer memory (dist.PeerExchange);
