@@ -419,6 +419,9 @@ typedef struct lsb_voxmap {
     double root_len;
     int32_t max_level;
     int32_t _pad;
+    uint64_t* gkeys;         /* (cap) packed keys of the leaves holding a Gaussian, append-only (may be
+                                NULL: the FoV then scans the whole table)      */
+    uint64_t* n_gkeys;       /* entries of gkeys (device counter)            */
 } lsb_voxmap;
 /* keys_of_points: (n,3) f64 points -> (n,3) int64 floor(p / edge). */
 int lsb_voxmap_keys(const double* pts, int64_t n, double edge, int64_t* keys_out, void* stream);

@@ -55,7 +55,7 @@ class Dims(_c.Structure):
 class VoxMap(_c.Structure):
     _fields_ = [("keys", _P), ("count", _P), ("sum", _P), ("outer", _P), ("gslot", _P), ("claim", _P),
                 ("n_used", _P), ("flags", _P), ("cap", _c.c_int64), ("root_len", _c.c_double),
-                ("max_level", _c.c_int32), ("_pad", _c.c_int32)]
+                ("max_level", _c.c_int32), ("_pad", _c.c_int32), ("gkeys", _P), ("n_gkeys", _P)]
 
 
 class AdamCfg(_c.Structure):

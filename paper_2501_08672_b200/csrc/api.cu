@@ -484,6 +484,8 @@ int lsb_semidense_mask(const void* obs, int32_t observed_u8, const float* tfin, 
 static int vox_ok(const lsb_voxmap* m) {
     if (!m || !m->keys || !m->count || !m->sum || !m->outer || !m->gslot || !m->claim || !m->n_used || !m->flags)
         return fail(LSB_EINVAL, "voxmap: NULL array");
+    if ((m->gkeys == nullptr) != (m->n_gkeys == nullptr))
+        return fail(LSB_EINVAL, "voxmap: gkeys and n_gkeys go together");
     if (m->cap < 2 || (m->cap & (m->cap - 1))) return fail(LSB_EINVAL, "voxmap: cap must be a power of two");
     if (!(m->root_len > 0.0)) return fail(LSB_EINVAL, "root_len must be positive");
     if (m->max_level < 0 || m->max_level > 16) return fail(LSB_EINVAL, "max_level out of range");

@@ -12,8 +12,9 @@
 //
 // Keys are floor(p / edge) with TRUE division in f64 (voxmap.py:50,64), so
 // the integer keys are bit-exact with the reference.  Leaf statistics
-// (count, sum p, sum p p^T) accumulate with f64 atomics (order-dependent at
-// round-off level only).
+// (count, sum p, sum p p^T) are exact fixed-point group sums (deterministic,
+// lsb_voxmap_accumulate below).  The map also keeps the packed keys of its
+// Gaussian leaves in an append-only list, which the FoV enumeration walks.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -103,7 +104,10 @@ __global__ void k_commit2(lsb_voxmap m, const int64_t* __restrict__ slots, int64
                           const int32_t* __restrict__ status) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const long long s = slots[i];
-        if (status[i]) m.gslot[s] = first_gid + (int32_t)i;
+        if (status[i]) {
+            m.gslot[s] = first_gid + (int32_t)i;
+            if (m.gkeys) m.gkeys[atomicAdd((unsigned long long*)m.n_gkeys, 1ull)] = m.keys[s];   // a new Gaussian leaf
+        }
         if (s >= 0) m.claim[s] = 0x7fffffff;
     }
 }
@@ -169,6 +173,47 @@ __global__ void k_fov_leaves(lsb_voxmap m, const unsigned long long* __restrict_
             }
         }
         // warp-aggregated output slot: one atomic per warp instead of per leaf
+        __syncwarp();
+        const unsigned hits = __ballot_sync(0xffffffffu, hit);
+        if (!hits) continue;
+        const int leader = __ffs(hits) - 1;
+        unsigned long long ob = 0;
+        if ((int)lane == leader) ob = atomicAdd(n_out, (unsigned long long)__popc(hits));
+        ob = __shfl_sync(0xffffffffu, ob, leader);
+        if (!hit) continue;
+        const unsigned long long o = ob + __popc(hits & ((1u << lane) - 1u));
+        if ((int64_t)o < out_cap) {
+            out[3 * o] = ix;
+            out[3 * o + 1] = iy;
+            out[3 * o + 2] = iz;
+        }
+    }
+}
+
+// The same over the list of Gaussian leaves (gkeys): n_gkeys entries instead
+// of the whole table's cap slots.
+__global__ void k_fov_gleaves(lsb_voxmap m, const unsigned long long* __restrict__ rset, int64_t rcap,
+                              int64_t* __restrict__ out, unsigned long long* __restrict__ n_out, int64_t out_cap) {
+    const int L = m.max_level;
+    const unsigned lane = threadIdx.x & 31;
+    const int64_t ng = (int64_t)*m.n_gkeys;           // the same for every thread: warp-uniform trip count
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < ng; base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = base + threadIdx.x;
+        bool hit = false;
+        long long ix = 0, iy = 0, iz = 0;
+        if (j < ng) {
+            unpack_key(m.gkeys[j], ix, iy, iz);
+            const long long rx = ix >> L, ry = iy >> L, rz = iz >> L;   // floor division by 2^L
+            const unsigned long long rkey = pack_key(rx, ry, rz);
+            const unsigned long long mask = (unsigned long long)rcap - 1;
+            unsigned long long q = slot_of(rx, ry, rz, 0, mask);
+            for (long long probe = 0; probe < rcap; ++probe) {
+                const unsigned long long cur = rset[q];
+                if (cur == rkey) { hit = true; break; }
+                if (cur == EMPTY) break;
+                q = (q + 1) & mask;
+            }
+        }
         __syncwarp();
         const unsigned hits = __ballot_sync(0xffffffffu, hit);
         if (!hits) continue;
@@ -397,7 +442,10 @@ cudaError_t launch_vox_fov(const lsb_voxmap& m, const double* pts, int64_t n, un
     e = cudaMemsetAsync(n_out, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
     if (n > 0) k_fov_roots<<<grid_for(n), 256, 0, st>>>(pts, n, m.root_len, rset, rcap);
-    k_fov_leaves<<<grid_for(m.cap), 256, 0, st>>>(m, rset, rcap, out, n_out, out_cap);
+    if (m.gkeys && m.n_gkeys)
+        k_fov_gleaves<<<148 * 8, 256, 0, st>>>(m, rset, rcap, out, n_out, out_cap);
+    else
+        k_fov_leaves<<<grid_for(m.cap), 256, 0, st>>>(m, rset, rcap, out, n_out, out_cap);
     return cudaGetLastError();
 }
 

@@ -170,11 +170,16 @@ class HashOctree:
         self.claim = torch.full((cap,), 0x7FFFFFFF, dtype=torch.int32, device=d)
         self.n_used = torch.zeros(1, dtype=torch.int64, device=d)
         self.flags = torch.zeros(1, dtype=torch.int64, device=d)
+        # packed keys of the leaves that hold a Gaussian (append-only): the FoV
+        # enumeration walks this list instead of the whole table
+        self.gkeys = torch.empty(cap, dtype=torch.int64, device=d)
+        self.n_gkeys = torch.zeros(1, dtype=torch.int64, device=d)
 
     def struct(self) -> _lib.VoxMap:
         return _lib.VoxMap(self.keys.data_ptr(), self.count.data_ptr(), self.sum.data_ptr(), self.outer.data_ptr(),
                            self.gslot.data_ptr(), self.claim.data_ptr(), self.n_used.data_ptr(),
-                           self.flags.data_ptr(), self.cap, self.root_len, self.max_level, 0)
+                           self.flags.data_ptr(), self.cap, self.root_len, self.max_level, 0,
+                           self.gkeys.data_ptr(), self.n_gkeys.data_ptr())
 
     def _reserve(self, extra: int):
         """Keep the load factor <= 1/2 (grow + rehash on the device; one sync)."""
@@ -182,13 +187,16 @@ class HashOctree:
         if used + extra <= self.cap // 2:
             return
         old = self.struct()
-        keep = (self.keys, self.count, self.sum, self.outer, self.gslot, self.claim, self.n_used, self.flags)
+        keep = (self.keys, self.count, self.sum, self.outer, self.gslot, self.claim, self.n_used, self.flags,
+                self.gkeys, self.n_gkeys)
         new_cap = self.cap
         while used + extra > new_cap // 2:
             new_cap *= 2
         self._alloc(new_cap)
         new = self.struct()
         _lib.check(_lib.load().lsb_voxmap_rehash(ctypes.byref(old), ctypes.byref(new), _lib.stream_ptr()), "rehash")
+        self.gkeys[: keep[8].shape[0]].copy_(keep[8])         # packed keys do not move with the slots
+        self.n_gkeys.copy_(keep[9])
         del keep
 
     def _check_flags(self):
@@ -359,6 +367,11 @@ class HashOctree:
             g[new] = torch.arange(self._next_gid, self._next_gid + n_new, dtype=torch.int32, device=self.device)
             self._next_gid += n_new
             self.gslot[tslots] = g
+            # new Gaussian leaves join the FoV list (tslots may repeat a key: once each)
+            nk = torch.unique(self.keys[tslots[new]])
+            pos = self.n_gkeys + torch.arange(nk.numel(), dtype=torch.int64, device=self.device)
+            self.gkeys[pos] = nk
+            self.n_gkeys += nk.numel()
         self._store_reserve(self._next_gid, rows.shape[1])
         self.store[g.long()] = rows
         return g

@@ -92,3 +92,32 @@ def test_try_insert_capacity_one():
     assert isinstance(m.try_insert(G([0.1, 0.1, 0.1])), Inserted)
     assert isinstance(m.try_insert(G([0.2, 0.2, 0.2])), Full)
     assert isinstance(m.try_insert(G([0.9, 0.1, 0.1])), Inserted)
+
+
+def test_fov_list_survives_growth_and_store_writes():
+    """The FoV walks the map's list of Gaussian leaves (gkeys): Gaussians made
+    by try_insert, by set_gaussians_dev (new leaves and replacements, with a
+    repeated key) and a table growth (rehash) in between must leave it equal
+    to the brute-force set of Gaussian leaves under the roots
+    (leaf_keys_under_roots, voxmap.py:232-251)."""
+    import torch
+    from paper_2501_08672_b200.voxmap import HashOctree, VoxelKey
+    rng = np.random.default_rng(5)
+    m = HashOctree(0.5, max_level=2, capacity=1 << 10)
+    m.try_insert_batch(rng.uniform(-2, 2, size=(300, 3)))
+    m.accumulate_points(rng.uniform(-4, 4, size=(20000, 3)))        # grows the table (rehash)
+    assert m.cap > 1 << 10
+    L = m.max_level
+    new_keys = np.floor(rng.uniform(-4, 4, size=(200, 3)) / m.leaf_len).astype(np.int64)
+    new_keys = np.concatenate([new_keys, new_keys[:7]])             # repeated keys in one call
+    m.set_gaussians_dev(new_keys, np.zeros((len(new_keys), 19), np.float32))
+    m.try_insert_batch(rng.uniform(-3, 3, size=(300, 3)))
+    keys, slots = m.dump_dev()
+    g = m.gslot[slots].cpu().numpy()
+    gk = keys.cpu().numpy()[g >= 0]
+    assert int(m.n_gkeys.item()) == len(gk)
+    roots = {tuple(int(v) for v in r) for r in np.floor(rng.uniform(-4, 4, size=(60, 3)) / m.root_len).astype(np.int64)}
+    want = {tuple(int(v) for v in k) for k in gk if (int(k[0]) >> L, int(k[1]) >> L, int(k[2]) >> L) in roots}
+    got = m.leaf_keys_under_roots([VoxelKey(a, b, c, 0) for a, b, c in roots])
+    assert {k[:3] for k in got} == want and len(want) > 0
+    torch.cuda.synchronize()

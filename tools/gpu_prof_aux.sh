@@ -11,8 +11,8 @@ export PYTHONDONTWRITEBYTECODE=1
 NCU=/usr/local/cuda/bin/ncu
 MET=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum
 declare -A STEPS=([cfg3]=10 [lidar]=3 [cfg4]=2 [window]=10)
-declare -A TOP=([cfg3]=k_insert_points [lidar]=k_lidar_rows [cfg4]=k_pose_rows [window]=k_win_mark)
-for W in cfg3 lidar cfg4 window; do
+declare -A TOP=([cfg3]=k_acc_fold [lidar]=k_lidar_rows [cfg4]=k_pose_rows [window]=k_win_mark)
+for W in ${WL:-cfg3 lidar cfg4 window}; do
   timeout 900 $NCU --metrics $MET --clock-control none --nvtx --nvtx-include "lsb_timed/" --csv \
     --log-file gpurun_out/aux_${TAG}_$W.csv python bench.py --config $W --steps ${STEPS[$W]} --warmup 1 \
     --no-cpu-baseline > gpurun_out/aux_${TAG}_$W.log 2>&1
