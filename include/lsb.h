@@ -519,14 +519,19 @@ int lsb_segment_mean(const double* pts, const int64_t* perm, const int64_t* star
  *            first_slot + 1, ... (*n_added on the device; window.py:183-209). */
 int lsb_window_mark(const int64_t* wkeys, int64_t n, uint64_t* hkeys, int32_t* hslots, int64_t hcap,
                     const int64_t* fov, int64_t m, uint8_t* keep, uint8_t* is_add, void* stream);
-int lsb_window_plan(const uint8_t* keep, int64_t n, int32_t* dels, int32_t* movers, int64_t* counts, void* stream);
+/* plan / append take an int32 scratch of lsb_window_plan_tiles(n) /
+ * lsb_window_append_tiles(cnt) entries (per-tile counts and offsets). */
+int64_t lsb_window_plan_tiles(int64_t n);
+int64_t lsb_window_append_tiles(int64_t cnt);
+int lsb_window_plan(const uint8_t* keep, int64_t n, int32_t* dels, int32_t* movers, int64_t* counts, int32_t* tiles,
+                    void* stream);
 int lsb_window_compact(const lsb_voxmap* m, const lsb_params* arena, int64_t* wkeys, const int32_t* dels, int64_t k,
                        const int32_t* movers, int64_t h, int64_t n, float* store, void* stream);
 int lsb_window_leaf_gids(const lsb_voxmap* m, const int64_t* okeys, int64_t cnt, int32_t* gids, void* stream);
 int lsb_window_dist(const int64_t* okeys, int64_t cnt, double edge, const double* origin, double* out,
                     void* stream);
 int lsb_window_append(const lsb_params* arena, int64_t* wkeys, const int64_t* okeys, const int32_t* gids, int64_t cnt,
-                      const float* store, int64_t first_slot, int64_t* n_added, void* stream);
+                      const float* store, int64_t first_slot, int64_t* n_added, int32_t* tiles, void* stream);
 
 /* ---- photometric loss: replaces optimize.photometric_loss (optimize.py:48-74)
  * kind 0 = L1, 1 = L2 over (npx, 3) f32 images; mask (npx) u8 may be NULL.

@@ -153,12 +153,14 @@ SIGNATURES = [
                                       _c.c_int32, _P, _P, _P]),
     ("lsb_segment_mean", _c.c_int, [_P, _P, _P, _P, _c.c_int64, _P, _P]),
     ("lsb_window_mark", _c.c_int, [_P, _c.c_int64, _P, _P, _c.c_int64, _P, _c.c_int64, _P, _P, _P]),
-    ("lsb_window_plan", _c.c_int, [_P, _c.c_int64, _P, _P, _P, _P]),
+    ("lsb_window_plan_tiles", _c.c_int64, [_c.c_int64]),
+    ("lsb_window_append_tiles", _c.c_int64, [_c.c_int64]),
+    ("lsb_window_plan", _c.c_int, [_P, _c.c_int64, _P, _P, _P, _P, _P]),
     ("lsb_window_compact", _c.c_int, [_c.POINTER(VoxMap), _c.POINTER(Params), _P, _P, _c.c_int64, _P, _c.c_int64,
                                       _c.c_int64, _P, _P]),
     ("lsb_window_leaf_gids", _c.c_int, [_c.POINTER(VoxMap), _P, _c.c_int64, _P, _P]),
     ("lsb_window_dist", _c.c_int, [_P, _c.c_int64, _c.c_double, _c.POINTER(_c.c_double), _P, _P]),
-    ("lsb_window_append", _c.c_int, [_c.POINTER(Params), _P, _P, _P, _c.c_int64, _P, _c.c_int64, _P, _P]),
+    ("lsb_window_append", _c.c_int, [_c.POINTER(Params), _P, _P, _P, _c.c_int64, _P, _c.c_int64, _P, _P, _P]),
     ("lsb_loss_scratch_doubles", _c.c_int, []),
     ("lsb_photometric_loss", _c.c_int, [_P, _P, _P, _c.c_int64, _c.c_int64, _c.c_int, _c.c_float,
                                         _P, _P, _P]),

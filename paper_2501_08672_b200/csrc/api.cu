@@ -68,13 +68,15 @@ cudaError_t launch_segment_mean(const double*, const int64_t*, const int64_t*, c
                                 cudaStream_t);
 cudaError_t launch_win_mark(const int64_t*, int64_t, uint64_t*, int32_t*, int64_t, const int64_t*, int64_t, uint8_t*,
                             uint8_t*, cudaStream_t);
-cudaError_t launch_win_plan(const uint8_t*, int64_t, int32_t*, int32_t*, int64_t*, cudaStream_t);
+cudaError_t launch_win_plan(const uint8_t*, int64_t, int32_t*, int32_t*, int64_t*, int32_t*, cudaStream_t);
+int64_t win_plan_tiles(int64_t);
+int64_t win_append_tiles(int64_t);
 cudaError_t launch_win_compact(const lsb_voxmap&, const lsb_params&, int64_t*, const int32_t*, int64_t,
                                const int32_t*, int64_t, int64_t, float*, cudaStream_t);
 cudaError_t launch_win_leaf_gids(const lsb_voxmap&, const int64_t*, int64_t, int32_t*, cudaStream_t);
 cudaError_t launch_win_dist(const int64_t*, int64_t, double, const double*, double*, cudaStream_t);
 cudaError_t launch_win_append(const lsb_params&, int64_t*, const int64_t*, const int32_t*, int64_t, const float*,
-                              int64_t, int64_t*, cudaStream_t);
+                              int64_t, int64_t*, int32_t*, cudaStream_t);
 }  // namespace lsb
 
 using namespace lsb;
@@ -594,9 +596,13 @@ int lsb_window_mark(const int64_t* wkeys, int64_t n, uint64_t* hkeys, int32_t* h
                       "window_mark");
 }
 
-int lsb_window_plan(const uint8_t* keep, int64_t n, int32_t* dels, int32_t* movers, int64_t* counts, void* stream) {
-    if (n < 0 || !counts || (n && (!keep || !dels || !movers))) return fail(LSB_EINVAL, "NULL array");
-    return check_cuda(launch_win_plan(keep, n, dels, movers, counts, (cudaStream_t)stream), "window_plan");
+int64_t lsb_window_plan_tiles(int64_t n) { return n > 0 ? win_plan_tiles(n) : 0; }
+int64_t lsb_window_append_tiles(int64_t cnt) { return cnt > 0 ? win_append_tiles(cnt) : 0; }
+
+int lsb_window_plan(const uint8_t* keep, int64_t n, int32_t* dels, int32_t* movers, int64_t* counts, int32_t* tiles,
+                    void* stream) {
+    if (n < 0 || !counts || (n && (!keep || !dels || !movers || !tiles))) return fail(LSB_EINVAL, "NULL array");
+    return check_cuda(launch_win_plan(keep, n, dels, movers, counts, tiles, (cudaStream_t)stream), "window_plan");
 }
 
 int lsb_window_compact(const lsb_voxmap* m, const lsb_params* arena, int64_t* wkeys, const int32_t* dels, int64_t k,
@@ -626,11 +632,12 @@ int lsb_window_dist(const int64_t* okeys, int64_t cnt, double edge, const double
 }
 
 int lsb_window_append(const lsb_params* arena, int64_t* wkeys, const int64_t* okeys, const int32_t* gids, int64_t cnt,
-                      const float* store, int64_t first_slot, int64_t* n_added, void* stream) {
+                      const float* store, int64_t first_slot, int64_t* n_added, int32_t* tiles, void* stream) {
     int rc = arena_ok(arena);
     if (rc) return rc;
-    if (!n_added || cnt < 0 || (cnt && (!okeys || !gids || !store || !wkeys))) return fail(LSB_EINVAL, "NULL array");
-    return check_cuda(launch_win_append(*arena, wkeys, okeys, gids, cnt, store, first_slot, n_added,
+    if (!n_added || cnt < 0 || (cnt && (!okeys || !gids || !store || !wkeys || !tiles)))
+        return fail(LSB_EINVAL, "NULL array");
+    return check_cuda(launch_win_append(*arena, wkeys, okeys, gids, cnt, store, first_slot, n_added, tiles,
                                         (cudaStream_t)stream),
                       "window_append");
 }

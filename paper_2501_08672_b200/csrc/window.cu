@@ -81,8 +81,21 @@ __global__ void k_win_mark(const unsigned long long* __restrict__ hk, const int3
 }
 
 // Block-wide exclusive scan of one int per thread (1024 threads).
-__device__ __forceinline__ int block_excl_scan(int v, int* s_w, int& total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+// The compaction plan as three multi-CTA passes over tiles of PLAN_TILE
+// slots (a one-CTA pass over the whole window was bound by one SM: ~160 us
+// per maintain): per tile the count of deleted slots, one CTA's exclusive
+// scan of the tile counts (k = their total), and per tile the emission:
+// dels = deleted slots ascending (k of them; the first h lie below the new
+// live count nk = n - k and are the holes), movers[r] = the r-th live slot
+// >= nk counted from the rear, counts = [k, h] with h = deleted slots below
+// nk (added per tile: integer atomics, order-free).
+constexpr int PLAN_TILE = 1024;
+constexpr int APPEND_TILE = 256;
+
+// Exclusive block scan for any block size that is a multiple of 32 (<= 1024).
+__device__ __forceinline__ int block_scan_n(int v, int* s_w, int& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     int x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -92,7 +105,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s_w, int& total) {
     if (lane == 31) s_w[warp] = x;
     __syncthreads();
     if (warp == 0) {
-        int y = s_w[lane];
+        int y = lane < nw ? s_w[lane] : 0;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int z = __shfl_up_sync(0xffffffffu, y, o);
@@ -102,55 +115,68 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s_w, int& total) {
     }
     __syncthreads();
     const int excl = x - v + (warp > 0 ? s_w[warp - 1] : 0);
-    total = s_w[31];
+    total = s_w[nw - 1];
     __syncthreads();
     return excl;
 }
 
-// One CTA: dels = deleted slots ascending (k of them); the first h of them
-// lie below the new live count nk = n - k and are the holes; movers[r] = the
-// r-th live slot >= nk counted from the rear.  counts = [k, h].
-__global__ void __launch_bounds__(1024) k_win_plan(const uint8_t* __restrict__ keep, int64_t n, int32_t* dels,
-                                                   int32_t* movers, int64_t* counts) {
+// per tile: how many of its slots are deleted (keep == 0)
+__global__ void __launch_bounds__(PLAN_TILE) k_plan_count(const uint8_t* __restrict__ keep, int64_t n,
+                                                          int32_t* __restrict__ tile_cnt) {
     __shared__ int s_w[32];
-    int tot = 0;
-    // pass 1: k
-    int kk = 0;
-    for (int64_t b = 0; b < n; b += 1024) {
-        const int64_t s = b + threadIdx.x;
-        int t;
-        (void)block_excl_scan(s < n && !keep[s] ? 1 : 0, s_w, t);
-        kk += t;
-    }
-    const int64_t nk = n - kk;
-    // pass 2: the lists
-    int D = 0;
-    for (int64_t b = 0; b < n; b += 1024) {
-        const int64_t s = b + threadIdx.x;
-        const int d = s < n && !keep[s] ? 1 : 0;
-        const int ex = block_excl_scan(d, s_w, tot);
-        const int Ds = D + ex;                    // deleted slots in [0, s)
-        if (s < n) {
-            if (d) {
-                dels[Ds] = (int32_t)s;
-            } else if (s >= nk) {
-                movers[(n - 1 - s) - (kk - Ds)] = (int32_t)s;    // rank = live slots in (s, n)
-            }
-        }
-        D += tot;
-    }
-    // h = live slots at or above nk (== deleted slots below nk)
-    int live_hi = 0;
-    for (int64_t b = nk; b < n; b += 1024) {
-        const int64_t s = b + threadIdx.x;
-        int t;
-        (void)block_excl_scan(s < n && keep[s] ? 1 : 0, s_w, t);
-        live_hi += t;
+    const int64_t s = (int64_t)blockIdx.x * PLAN_TILE + threadIdx.x;
+    int tot;
+    (void)block_scan_n(s < n && !keep[s] ? 1 : 0, s_w, tot);
+    if (threadIdx.x == 0) tile_cnt[blockIdx.x] = tot;
+}
+
+// per tile: valid adds (gid >= 0)
+__global__ void __launch_bounds__(APPEND_TILE) k_append_count(const int32_t* __restrict__ gids, int64_t cnt,
+                                                              int32_t* __restrict__ tile_cnt) {
+    __shared__ int s_w[32];
+    const int64_t i = (int64_t)blockIdx.x * APPEND_TILE + threadIdx.x;
+    int tot;
+    (void)block_scan_n(i < cnt && gids[i] >= 0 ? 1 : 0, s_w, tot);
+    if (threadIdx.x == 0) tile_cnt[blockIdx.x] = tot;
+}
+
+// one CTA: tile_off = exclusive scan of tile_cnt; *total = the sum (and
+// *zero, when given, = 0: the h counter the emission adds to)
+__global__ void __launch_bounds__(1024) k_tiles_scan(const int32_t* __restrict__ tile_cnt, int64_t ntiles,
+                                                     int32_t* __restrict__ tile_off, int64_t* total, int64_t* zero) {
+    __shared__ int s_w[32];
+    int base = 0;
+    for (int64_t b = 0; b < ntiles; b += 1024) {
+        const int64_t t = b + threadIdx.x;
+        int tot;
+        const int ex = block_scan_n(t < ntiles ? tile_cnt[t] : 0, s_w, tot);
+        if (t < ntiles) tile_off[t] = base + ex;
+        base += tot;
     }
     if (threadIdx.x == 0) {
-        counts[0] = kk;
-        counts[1] = live_hi;
+        *total = base;
+        if (zero) *zero = 0;
     }
+}
+
+__global__ void __launch_bounds__(PLAN_TILE) k_plan_emit(const uint8_t* __restrict__ keep, int64_t n,
+                                                         const int32_t* __restrict__ tile_off, int64_t* counts,
+                                                         int32_t* dels, int32_t* movers) {
+    __shared__ int s_w[32];
+    const int64_t s = (int64_t)blockIdx.x * PLAN_TILE + threadIdx.x;
+    const int64_t kk = counts[0], nk = n - kk;
+    const int d = s < n && !keep[s] ? 1 : 0;
+    int tot;
+    const int64_t Ds = tile_off[blockIdx.x] + block_scan_n(d, s_w, tot);   // deleted slots in [0, s)
+    if (s < n) {
+        if (d)
+            dels[Ds] = (int32_t)s;
+        else if (s >= nk)
+            movers[(n - 1 - s) - (kk - Ds)] = (int32_t)s;    // rank = live slots in (s, n)
+    }
+    int below;
+    (void)block_scan_n(d && s < nk ? 1 : 0, s_w, below);
+    if (threadIdx.x == 0 && below) atomicAdd((unsigned long long*)&counts[1], (unsigned long long)below);
 }
 
 struct Arena {
@@ -237,26 +263,23 @@ __global__ void k_win_dist(const int64_t* __restrict__ okeys, int64_t cnt, doubl
 }
 
 // Ordered append: the adds (sorted keys) that hold a Gaussian go to slots
-// first_slot, first_slot + 1, ... in key order (one CTA, chunked scan).
-__global__ void __launch_bounds__(1024) k_win_from_map(Arena a, int64_t* wkeys, const int64_t* __restrict__ okeys,
-                                                       const int32_t* __restrict__ gids, int64_t cnt,
-                                                       const float* __restrict__ store, int64_t first_slot,
-                                                       int64_t* n_added) {
+// first_slot, first_slot + 1, ... in key order (tile counts, one-CTA scan,
+// then every tile copies its rows in parallel).
+__global__ void __launch_bounds__(APPEND_TILE) k_win_from_map(Arena a, int64_t* wkeys, const int64_t* __restrict__ okeys,
+                                                              const int32_t* __restrict__ gids, int64_t cnt,
+                                                              const float* __restrict__ store, int64_t first_slot,
+                                                              const int32_t* __restrict__ tile_off) {
     __shared__ int s_w[32];
     const int R = 16 + 3 * a.K;
-    int base = 0, tot = 0;
-    for (int64_t b = 0; b < cnt; b += 1024) {
-        const int64_t i = b + threadIdx.x;
-        const int g = i < cnt ? gids[i] : -1;
-        const int ex = block_excl_scan(g >= 0 ? 1 : 0, s_w, tot);
-        if (g >= 0) {
-            const int64_t s = first_slot + base + ex;
-            row_copy_in(a, s, store + (int64_t)g * R);
-            wkeys[s] = okeys[i];
-        }
-        base += tot;
+    const int64_t i = (int64_t)blockIdx.x * APPEND_TILE + threadIdx.x;
+    const int g = i < cnt ? gids[i] : -1;
+    int tot;
+    const int ex = block_scan_n(g >= 0 ? 1 : 0, s_w, tot);
+    if (g >= 0) {
+        const int64_t s = first_slot + tile_off[blockIdx.x] + ex;
+        row_copy_in(a, s, store + (int64_t)g * R);
+        wkeys[s] = okeys[i];
     }
-    if (threadIdx.x == 0) *n_added = base;
 }
 
 static Arena arena_of(const lsb_params& p) {
@@ -279,9 +302,19 @@ cudaError_t launch_win_mark(const int64_t* wkeys, int64_t n, uint64_t* hkeys, in
     return cudaGetLastError();
 }
 
+int64_t win_plan_tiles(int64_t n) { return 2 * ((n + PLAN_TILE - 1) / PLAN_TILE) + 2; }
+int64_t win_append_tiles(int64_t cnt) { return 2 * ((cnt + APPEND_TILE - 1) / APPEND_TILE) + 2; }
+
 cudaError_t launch_win_plan(const uint8_t* keep, int64_t n, int32_t* dels, int32_t* movers, int64_t* counts,
-                            cudaStream_t st) {
-    k_win_plan<<<1, 1024, 0, st>>>(keep, n, dels, movers, counts);
+                            int32_t* tiles, cudaStream_t st) {
+    const int64_t nt = (n + PLAN_TILE - 1) / PLAN_TILE;
+    if (nt == 0) {
+        cudaError_t e = cudaMemsetAsync(counts, 0, 2 * sizeof(int64_t), st);
+        return e;
+    }
+    k_plan_count<<<(unsigned)nt, PLAN_TILE, 0, st>>>(keep, n, tiles);
+    k_tiles_scan<<<1, 1024, 0, st>>>(tiles, nt, tiles + nt, counts, counts + 1);
+    k_plan_emit<<<(unsigned)nt, PLAN_TILE, 0, st>>>(keep, n, tiles + nt, counts, dels, movers);
     return cudaGetLastError();
 }
 
@@ -307,8 +340,14 @@ cudaError_t launch_win_dist(const int64_t* okeys, int64_t cnt, double edge, cons
 }
 
 cudaError_t launch_win_append(const lsb_params& arena, int64_t* wkeys, const int64_t* okeys, const int32_t* gids,
-                              int64_t cnt, const float* store, int64_t first_slot, int64_t* n_added, cudaStream_t st) {
-    k_win_from_map<<<1, 1024, 0, st>>>(arena_of(arena), wkeys, okeys, gids, cnt, store, first_slot, n_added);
+                              int64_t cnt, const float* store, int64_t first_slot, int64_t* n_added, int32_t* tiles,
+                              cudaStream_t st) {
+    const int64_t nt = (cnt + APPEND_TILE - 1) / APPEND_TILE;
+    if (nt == 0) return cudaMemsetAsync(n_added, 0, sizeof(int64_t), st);
+    k_append_count<<<(unsigned)nt, APPEND_TILE, 0, st>>>(gids, cnt, tiles);
+    k_tiles_scan<<<1, 1024, 0, st>>>(tiles, nt, tiles + nt, n_added, nullptr);
+    k_win_from_map<<<(unsigned)nt, APPEND_TILE, 0, st>>>(arena_of(arena), wkeys, okeys, gids, cnt, store, first_slot,
+                                                         tiles + nt);
     return cudaGetLastError();
 }
 

@@ -112,6 +112,13 @@ class GaussianWindow:
         self._n_added = torch.zeros(1, dtype=torch.int64, device=d)
         self._pending: Optional[dict] = None
 
+    def _tile_scratch(self, ints: int) -> torch.Tensor:
+        """int32 scratch of the multi-CTA plan / append scans (kept, grown)."""
+        t = getattr(self, "_tiles", None)
+        if t is None or t.numel() < max(int(ints), 1):
+            t = self._tiles = torch.empty(max(int(ints), 64), dtype=torch.int32, device=self.device)
+        return t
+
     @property
     def row_floats(self) -> int:
         return 16 + 3 * self.sh_coeffs
@@ -202,7 +209,9 @@ class GaussianWindow:
         _lib.check(lib.lsb_window_plan(ctypes.c_void_p(self._keep.data_ptr()), n,
                                        ctypes.c_void_p(self._dels.data_ptr()),
                                        ctypes.c_void_p(self._movers.data_ptr()),
-                                       ctypes.c_void_p(self._counts.data_ptr()), _lib.stream_ptr()), "window_plan")
+                                       ctypes.c_void_p(self._counts.data_ptr()),
+                                       ctypes.c_void_p(self._tile_scratch(lib.lsb_window_plan_tiles(n)).data_ptr()),
+                                       _lib.stream_ptr()), "window_plan")
         k, h = (int(v) for v in self._counts.cpu())
         if k:
             if getattr(vmap, "store", None) is None:
@@ -284,7 +293,10 @@ class GaussianWindow:
         _lib.check(_lib.load().lsb_window_append(ctypes.byref(a), ctypes.c_void_p(self.wkeys.data_ptr()),
                                                  ctypes.c_void_p(add_ok.data_ptr()), ctypes.c_void_p(gids.data_ptr()),
                                                  add_ok.numel(), ctypes.c_void_p(vmap.store.data_ptr()), self.n,
-                                                 ctypes.c_void_p(self._n_added.data_ptr()), _lib.stream_ptr()),
+                                                 ctypes.c_void_p(self._n_added.data_ptr()),
+                                                 ctypes.c_void_p(self._tile_scratch(
+                                                     _lib.load().lsb_window_append_tiles(add_ok.numel())).data_ptr()),
+                                                 _lib.stream_ptr()),
                    "window_append")
         self.n += n_rows
         return n_rows
@@ -311,10 +323,13 @@ class GaussianWindow:
         an iterable of VoxelKey."""
         t0 = time.perf_counter()
         rep = MaintenanceReport()
-        fov_ok = _sorted_unique(self._fov_order_keys(fov_keys))   # sorted, unique
+        # the FoV keys need no order: the hash marks give keep / add per key,
+        # and only the adds (a few percent of the FoV) are sorted and
+        # de-duplicated for the ordered append (window.py:254-276)
+        fov_ok = self._fov_order_keys(fov_keys)
         is_add = self._mark(fov_ok).bool()
         rep.removed, rep.moved = self.writeback_and_compact(vmap)
-        add_ok = fov_ok[is_add]                                 # sorted (unique returns sorted)
+        add_ok = _sorted_unique(fov_ok[is_add])                 # sorted, unique
         n_add = int(add_ok.numel())
         if self.n + n_add > self.capacity:
             if sensor_pos is None:
