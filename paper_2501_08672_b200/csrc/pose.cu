@@ -351,13 +351,18 @@ __global__ void __launch_bounds__(256) k_hb_partial(const double* __restrict__ r
     }
 }
 
-__global__ void k_hb_final(const double* __restrict__ part, int nblocks, double inv_s2, double* __restrict__ out) {
-    // out[0..35] = sum h h^T inv_s2 (6x6), out[36..41] = sum h z inv_s2
-    if (threadIdx.x >= HB_VALS) return;
+// One warp per value: lane l adds the partials b = l, l + 32, ... in order,
+// then a fixed butterfly combines the lanes (deterministic; the 296 partials
+// no longer go through one thread's dependent adds: ~22 -> ~3 us).
+__global__ void __launch_bounds__(32 * HB_VALS) k_hb_final(const double* __restrict__ part, int nblocks, double inv_s2,
+                                                          double* __restrict__ out) {
+    const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double t = 0.0;
-    for (int b = 0; b < nblocks; ++b) t += part[(int64_t)b * HB_VALS + threadIdx.x];
+    for (int b = lane; b < nblocks; b += 32) t += part[(int64_t)b * HB_VALS + q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane) return;
     t *= inv_s2;
-    const int q = threadIdx.x;
     if (q >= 21) {
         out[36 + q - 21] = t;
         return;
@@ -430,7 +435,7 @@ cudaError_t launch_pose_rows(const Ws& w, const lsb_settings& s, int degree, int
 cudaError_t launch_hb(const double* rows, const double* z, int64_t m, const int64_t* m_dev, double inv_s2, double* out,
                       double* part, cudaStream_t st) {
     k_hb_partial<<<HB_BLOCKS, 256, 0, st>>>(rows, z, m, m_dev, part);
-    k_hb_final<<<1, 32, 0, st>>>(part, HB_BLOCKS, inv_s2, out);
+    k_hb_final<<<1, 32 * HB_VALS, 0, st>>>(part, HB_BLOCKS, inv_s2, out);
     return cudaGetLastError();
 }
 

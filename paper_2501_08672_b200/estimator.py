@@ -86,26 +86,36 @@ class Measurement:
     copies the rows to the host."""
 
     def __init__(self, z=None, H=None, R_diag=None, rows_dev: torch.Tensor = None, z_dev: torch.Tensor = None,
-                 sigma2: float = None):
+                 sigma2: float = None, keep_dev: torch.Tensor = None, count: int = None):
         self._z = None if z is None else np.asarray(z, dtype=float).reshape(-1)
         self._H = None if H is None else np.asarray(H, dtype=float).reshape(-1, DIM)
         self._R = None if R_diag is None else np.asarray(R_diag, dtype=float).reshape(-1)
         self.rows_dev, self.z_dev, self.sigma2 = rows_dev, z_dev, sigma2
+        # keep_dev: the device rows are every input point's, the kept ones
+        # marked (dropped rows are zero, so hb() needs no compaction); z / H
+        # are the kept rows in scan order
+        self.keep_dev, self._count = keep_dev, count
 
     def __len__(self) -> int:
+        if self._count is not None:
+            return int(self._count)
         return int(self.z_dev.numel()) if self.z_dev is not None else len(self._z)
+
+    def _kept(self, t: torch.Tensor) -> np.ndarray:
+        a = t.cpu().numpy()
+        return a if self.keep_dev is None else a[self.keep_dev.cpu().numpy().astype(bool)]
 
     @property
     def z(self) -> np.ndarray:
         if self._z is None:
-            self._z = self.z_dev.cpu().numpy()
+            self._z = self._kept(self.z_dev)
         return self._z
 
     @property
     def H(self) -> np.ndarray:
         if self._H is None:
             H = np.zeros((len(self), DIM))
-            H[:, :6] = -self.rows_dev.cpu().numpy()
+            H[:, :6] = -self._kept(self.rows_dev)
             self._H = H
         return self._H
 
@@ -118,8 +128,8 @@ class Measurement:
     def hb(self) -> tuple[np.ndarray, np.ndarray]:
         """(6x6 sum h h^T / sigma^2, 6 sum h z / sigma^2) for the pose block,
         reduced on the device (estimator.py:314-318 with H = -rows)."""
-        m = int(self.z_dev.numel())
-        inv = 1.0 / (self.sigma2 if self.sigma2 is not None else float(self.R_diag[0])) if m else 1.0
+        m = int(self.z_dev.numel())          # (with keep_dev: every point's row, dropped ones zero)
+        inv = 1.0 / (self.sigma2 if self.sigma2 is not None else float(self.R_diag[0])) if len(self) else 1.0
         lib = _lib.load()
         out = torch.empty(42, dtype=torch.float64, device=self.z_dev.device)
         scratch = torch.empty(lib.lsb_hb_scratch_doubles(), dtype=torch.float64, device=self.z_dev.device)
@@ -216,11 +226,14 @@ def lidar_measurement(state: NavState, points_l, vmap, T_il, cfg: FilterConfig,
                                           float(cfg.lidar_gate), ctypes.c_void_p(rows.data_ptr()),
                                           ctypes.c_void_p(z.data_ptr()), ctypes.c_void_p(keep.data_ptr()),
                                           _lib.stream_ptr()), "lidar_rows")
-    k = keep[:n].bool()
-    m_ok = int(k.sum().item())
+    # the rows of dropped points are zero (k_lidar_rows), so the H/b
+    # reduction runs over all n rows without a compaction; z / H are
+    # compacted to the kept rows (scan order) only if a caller reads them
+    k = keep[:n]
+    m_ok = int(k.sum(dtype=torch.int64).item())
     if m_ok == 0:
         raise NoAssociations("no scan point matched a plane (or all residuals gated out)")
-    return Measurement(rows_dev=rows[:n][k].contiguous(), z_dev=z[:n][k].contiguous(), sigma2=cfg.lidar_sigma ** 2)
+    return Measurement(rows_dev=rows[:n], z_dev=z[:n], sigma2=cfg.lidar_sigma ** 2, keep_dev=k, count=m_ok)
 
 
 class _VisualPass:
