@@ -284,7 +284,7 @@ def run_ours(args, wl, rank, world, local_rank):
     # this rank's render units: whole views (v -> rank v mod N), or row bands
     # of the views when N does not divide them (dist.shard_units: config 2's
     # 10 views become 20 half views at N = 4, 40 quarter views at N = 8)
-    from paper_2501_08672_b200.dist import shard_units, view_bands
+    from paper_2501_08672_b200.dist import shard_units_mixed as shard_units
     units = shard_units(V, world, rank, H)
     my_views = [u[0] for u in units]
     bands = [(u[1], u[2]) for u in units]
@@ -470,11 +470,11 @@ def run_ours(args, wl, rank, world, local_rank):
             "parallelism": f"view-sharded dp{world}",
             "config": workload_config(args, wl),
             "details": {"view_lanes": args.lanes, "exchange": exchange if world > 1 else None,
-                       # render units per rank: whole views, or row bands when N does not divide the views
-                       "units_per_rank": [len(shard_units(V, world, r, H)) for r in range(world)],
-                       "bands_per_view": view_bands(V, world, H),
-                       "unit_imbalance": max(len(shard_units(V, world, r, H)) for r in range(world))
-                       / (V * view_bands(V, world, H) / world),
+                       # render units per rank (dist.shard_units_mixed): whole views first,
+                       # row bands of the leftover views when N does not divide the views
+                       "units_per_rank": [shard_units(V, world, r, H) for r in range(world)],
+                       "pixel_row_imbalance": max(sum(y1 - y0 for _, y0, y1 in shard_units(V, world, r, H))
+                                                  for r in range(world)) / (V * H / world),
                        "cuda_graph": graph_headline, "cuda_graph_e2e": use_graph,
                        "serial_ms_per_step": eager_ms,
                        "kernel_timing": "separate one-lane eager pass of the same steps, events around each kernel",

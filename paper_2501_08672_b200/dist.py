@@ -59,6 +59,28 @@ def shard_units(n_views: int, world: int, rank: int, height: int, tile: int = 16
     return units[rank * per:(rank + 1) * per]
 
 
+def shard_units_mixed(n_views: int, world: int, rank: int, height: int, tile: int = 16) -> list:
+    """Whole views first, bands for the remainder: with n_views = q world + r,
+    rank r' renders the q whole views r', r' + world, ... and the r leftover
+    views are cut into b row bands (b in 2, 4, 8 with r b divisible by
+    world) shared out evenly — fewer, larger units than banding every view
+    (the target window at 8 ranks: 1 whole + 1 quarter view per rank instead
+    of 5 quarter views).  Falls back to shard_units when no split exists."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad world/rank")
+    q, r = divmod(n_views, world)
+    if r == 0:
+        return [(v, 0, height) for v in shard_views(n_views, world, rank)]
+    rows = (height + tile - 1) // tile
+    for b in (2, 4, 8):
+        if b <= rows and (r * b) % world == 0:
+            edges = [min(height, tile * (k * rows // b)) for k in range(b)] + [height]
+            rest = [(v, edges[k], edges[k + 1]) for v in range(q * world, n_views) for k in range(b)]
+            per = len(rest) // world
+            return [(v, 0, height) for v in range(rank, q * world, world)] + rest[rank * per:(rank + 1) * per]
+    return shard_units(n_views, world, rank, height, tile)
+
+
 class AllReduce:
     """The gradient exchange: in-place sum over the process group.  Called
     on the whole flat buffer it blocks the current stream on one all-reduce;
@@ -108,8 +130,8 @@ def replicas_identical(t: torch.Tensor, group=None) -> bool:
 
 class ViewShardedWindow:
     """Multi-GPU WindowEngine: this rank's share of the keyframe views —
-    whole views, or row bands of them when the ranks do not divide the
-    views (shard_units)."""
+    whole views, and row bands of the leftover views when the ranks do not
+    divide the views (shard_units_mixed)."""
 
     def __init__(self, arrays, cam, views_all: Sequence, settings, cfg=None, group=None, stream=None,
                  master: str = "f64", lanes: int = 1):
@@ -117,7 +139,7 @@ class ViewShardedWindow:
 
         world = dist.get_world_size(group) if dist.is_initialized() else 1
         rank = dist.get_rank(group) if dist.is_initialized() else 0
-        self.units = shard_units(len(views_all), world, rank, int(cam.height))
+        self.units = shard_units_mixed(len(views_all), world, rank, int(cam.height))
         self.mine = [u[0] for u in self.units]
         self.engine = WindowEngine(arrays, cam, [views_all[v] for v in self.mine], settings, cfg or OptimConfig(),
                                    n_views_total=len(views_all), stream=stream, master=master, lanes=lanes,

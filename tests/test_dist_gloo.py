@@ -33,6 +33,26 @@ def test_shard_views_partition():
 
 
 @pytest.mark.parametrize("n,height", [(10, 1024), (64, 1080), (10, 80), (3, 48), (7, 1024)])
+def test_mixed_units_cover_every_row_once_and_balance_pixels(n, height):
+    """shard_units_mixed (the default split): every (view, row) rendered by
+    exactly one rank, whole views first, every rank the same number of pixel
+    rows whenever a band split exists."""
+    from paper_2501_08672_b200.dist import shard_units_mixed
+    for world in (1, 2, 4, 8):
+        parts = [shard_units_mixed(n, world, r, height) for r in range(world)]
+        cover = np.zeros((n, height), np.int32)
+        for p in parts:
+            for v, y0, y1 in p:
+                assert y0 % 16 == 0 and y0 < y1
+                cover[v, y0:y1] += 1
+        assert (cover == 1).all()
+        rows = [sum(y1 - y0 for _, y0, y1 in p) for p in parts]
+        r, trows = n % world, (height + 15) // 16
+        if r == 0 or any(b <= trows and (r * b) % world == 0 for b in (2, 4, 8)):
+            assert max(rows) - min(rows) <= 16, rows                 # tile-aligned bands
+
+
+@pytest.mark.parametrize("n,height", [(10, 1024), (64, 1080), (10, 80), (3, 48), (7, 1024)])
 def test_shard_units_cover_every_row_once_and_balance(n, height):
     """Row-band units: every (view, row) rendered by exactly one rank; equal
     unit counts whenever a band split exists; bands start on tile rows."""

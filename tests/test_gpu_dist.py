@@ -125,10 +125,10 @@ def test_four_ranks_row_bands_match_single_process():
     import torch
     from paper_2501_08672_b200.dist import view_bands
     from paper_2501_08672_b200.optimize import OptimConfig, WindowEngine
-    assert view_bands(6, 4, 128) == 2                      # 12 half views, 3 per rank
-    out = _run(4, 6, 1)
+    assert view_bands(6, 4, 128) == 2
+    out = _run(4, 6, 1)                 # shard_units_mixed: 1 whole view + 1 half of views 4, 5 per rank
     assert all(o[3] for o in out), "replicas diverged"
-    assert all(len(o[1]) == 3 for o in out)
+    assert all(len(o[1]) == 2 for o in out)
     assert any(y0 > 0 for o in out for _, y0, _ in o[1])         # (row bands, not whole views)
     for r in range(1, 4):
         for k in ("means", "shs"):

@@ -1,8 +1,8 @@
 """Per-rank compute of the view-sharded step at G = 1, 2, 4, 8 GPUs, measured
 on ONE B200 (this pool has no multi-GPU node): for every rank r of a G-rank
 job, the WindowEngine that rank would build (its render units:
-dist.shard_units — whole views, or row bands when G does not divide the
-views) is captured as a CUDA graph WITHOUT the gradient exchange and timed
+dist.shard_units_mixed — whole views first, row bands of the leftover views
+when G does not divide them; --units banded bands every view) is captured as a CUDA graph WITHOUT the gradient exchange and timed
 alone (L2 flushed before each step, median of --steps).  The job's step is
 then max over ranks of that time plus the exchange, which is modelled, not
 measured: one NCCL all-reduce of the flat f32 gradient buffer (4 (10 + 3K) N
@@ -30,10 +30,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--lanes", type=int, default=5)
     ap.add_argument("--busbw", type=float, default=600.0, help="assumed NCCL all-reduce bus bandwidth, GB/s")
+    ap.add_argument("--units", default="mixed", choices=["banded", "mixed"],
+                    help="dist.shard_units (band every view) or dist.shard_units_mixed (whole views first)")
     args = ap.parse_args()
     import torch
     import bench
-    from paper_2501_08672_b200.dist import shard_units, view_bands
+    from paper_2501_08672_b200.dist import shard_units, shard_units_mixed, view_bands
     from paper_2501_08672_b200.optimize import OptimConfig, WindowEngine
     from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
 
@@ -55,7 +57,7 @@ def main():
     for G in args.gpus:
         per_rank = []
         for r in range(G):
-            units = shard_units(V, G, r, H)
+            units = (shard_units if args.units == "banded" else shard_units_mixed)(V, G, r, H)
             win = GaussianArrays(*wl["win"], device=dev)
             eng = WindowEngine(win, wl["cam"], [wl["views"][u[0]] for u in units], settings, OptimConfig(),
                                n_views_total=V, stream=stream, lanes=args.lanes,
@@ -81,7 +83,8 @@ def main():
         comp = max(per_rank)
         ar_ms = 0.0 if G == 1 else 2.0 * (G - 1) / G * grad_bytes / (args.busbw * 1e9) * 1e3
         out["per_world"][str(G)] = {
-            "units_per_rank": len(shard_units(V, G, 0, H)), "bands_per_view": view_bands(V, G, H),
+            "units_per_rank": len((shard_units if args.units == "banded" else shard_units_mixed)(V, G, 0, H)),
+            "unit_mode": args.units, "bands_per_view": view_bands(V, G, H),
             "rank_compute_ms": per_rank, "max_rank_compute_ms": comp,
             "allreduce_model_ms": ar_ms, "step_model_ms": comp + ar_ms,
             "mpix_per_s_model": V * W * H / ((comp + ar_ms) * 1e-3) / 1e6}
