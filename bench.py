@@ -914,7 +914,7 @@ def main():
     ap.add_argument("--config", default="target", choices=sorted(CONFIGS) + ["cfg3", "cfg4", "window", "lidar"])
     ap.add_argument("--alpha-cut", type=float, default=1.0 / 255.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--lanes", type=int, default=5, help="concurrent view pipelines per GPU")
+    ap.add_argument("--lanes", type=int, default=8, help="concurrent view pipelines per GPU")
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="eager launches instead of a CUDA graph")
     ap.add_argument("--copy-streams", type=int, default=1, help="H2D staging streams for the e2e pass")
     ap.add_argument("--frames", default="u8", choices=["u8", "f32"],
