@@ -159,6 +159,14 @@ struct Ws {
     int32_t* warp_cnt;          // [2 ceil(n/32)] visible count, tile count per warp
     int32_t* warp_off;          // [2 ceil(n/32)] their exclusive scans
     int32_t* chunk_cnt;         // [2 ceil(n/32/1024)] (visible, tile) totals per 1024 preprocess warps
+    // the counting pass's full result per visible Gaussian, by Gaussian id
+    // (the emitting pass copies it to the Gaussian's slot instead of
+    // recomputing the geometry)
+    Rec* st_rec;                // [n]
+    CullGeo* st_geo;            // [n] (alpha_cut > 0)
+    uint64_t* st_key;           // [n]
+    uint32_t* st_cm;            // [n]
+    int32_t* st_nt;             // [n]
     int64_t n, cap;
     int32_t ntx, nty, ntiles, nblocks_pre;
 };
@@ -218,6 +226,11 @@ inline size_t carve(const lsb_dims& d, char* base, Ws* w) {
     t.warp_mask = (uint32_t*)take(sizeof(uint32_t) * nw);
     t.warp_cnt = (int32_t*)take(sizeof(int32_t) * 2 * nw);
     t.warp_off = (int32_t*)take(sizeof(int32_t) * 2 * nw);
+    t.st_rec = (Rec*)take(sizeof(Rec) * n);
+    t.st_geo = (CullGeo*)take(sizeof(CullGeo) * n);
+    t.st_key = (uint64_t*)take(sizeof(uint64_t) * n);
+    t.st_cm = (uint32_t*)take(sizeof(uint32_t) * n);
+    t.st_nt = (int32_t*)take(sizeof(int32_t) * n);
     if (w) *w = t;
     return off;
 }

@@ -775,6 +775,9 @@ size_t tile_sort_smem() { return SORT_CAP * (sizeof(uint64_t) + 2 * sizeof(int))
 // bits) and write the records, keys and intersections at their offsets.
 // Slot order is still id order.
 
+#ifndef LSB_PRE_STASH
+#define LSB_PRE_STASH 1       // the counting pass computes visible Gaussians in full and stashes them
+#endif
 __global__ void __launch_bounds__(PRE_THREADS) k_pre_count(PreArgs a, Ws w) {
     const int64_t i = (int64_t)blockIdx.x * PRE_THREADS + threadIdx.x;
     const int lane = threadIdx.x & 31;
@@ -783,7 +786,16 @@ __global__ void __launch_bounds__(PRE_THREADS) k_pre_count(PreArgs a, Ws w) {
     uint64_t key = 0;
     uint32_t cm = 0;
     CullGeo geo;
-    const bool vis = (i < a.p.n) && splat_one<false>(a, i, r, nt, key, cm, geo);
+    const bool vis = (i < a.p.n) && splat_one<LSB_PRE_STASH>(a, i, r, nt, key, cm, geo);
+#if LSB_PRE_STASH
+    if (vis) {                          // the emitting pass copies this instead of recomputing it
+        w.st_rec[i] = r;
+        w.st_key[i] = key;
+        w.st_cm[i] = cm;
+        w.st_nt[i] = nt;
+        if (a.s.alpha_cut > 0.0) w.st_geo[i] = geo;
+    }
+#endif
     const unsigned mask = __ballot_sync(0xffffffffu, vis);
     int t = vis ? nt : 0;
 #pragma unroll
@@ -891,7 +903,17 @@ __global__ void __launch_bounds__(PRE_THREADS, PRE_MIN_BLOCKS) k_pre_emit(PreArg
     uint64_t key = 0;
     uint32_t cm = 0;
     CullGeo geo;
+#if LSB_PRE_STASH
+    if (mine) {                                              // visible: the counting pass's result
+        r = w.st_rec[i];
+        key = w.st_key[i];
+        cm = w.st_cm[i];
+        nt = w.st_nt[i];
+        if (a.s.alpha_cut > 0.0) geo = w.st_geo[i];
+    }
+#else
     if (mine) splat_one<true>(a, i, r, nt, key, cm, geo);   // visible: the counting pass said so
+#endif
     int ex = mine ? nt : 0;                                  // exclusive scan of nt over the warp
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
