@@ -12,7 +12,7 @@ timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline "$@" \
   > gpurun_out/ncu_bench_$TAG.log 2>&1
 for K in ${KERNELS:-k_blend_fused k_pre_count k_pre_emit k_chain}; do
-  timeout 600 $NCU --set full --clock-control none --import-source on -k regex:$K -s 12 -c 1 \
+  timeout 600 $NCU --set full --clock-control none --import-source on -k regex:"(^|:)$K\$" -s 12 -c 1 \
     -o gpurun_out/prof_${TAG}_$K python bench.py --steps 2 --warmup 3 --no-cpu-baseline "$@" \
     > gpurun_out/ncu_${K}_$TAG.log 2>&1
 done

@@ -88,7 +88,10 @@ def main(tag, workload):
     issue_path = os.path.join(PROF, "issue.json")
     issue = json.load(open(issue_path)) if os.path.exists(issue_path) else {}
     sums = {}
+    aux = tuple(f"prof_{tag}_{wl}_" for wl in ("cfg3", "cfg4", "lidar", "window"))    # summarize_aux.py's
     for rep in sorted(glob.glob(os.path.join(OUT, f"prof_{tag}_*.ncu-rep"))):
+        if os.path.basename(rep).startswith(aux):
+            continue
         for d in raw(rep):
             name = d["kernel"].replace("void ", "").split("(")[0].split("::")[-1].split("<")[0]
             tb = d.get("dram_read", 0) + d.get("dram_write", 0)
