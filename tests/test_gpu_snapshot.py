@@ -43,6 +43,12 @@ def test_snapshot_round_trip(tmp_path):
     assert q.read_bytes() == d["snapshot"].tobytes()
     rows = m.gaussian_rows_dev(d["keys"]).cpu().numpy()
     assert np.array_equal(rows, d["rows"])
+    # the loaded map's FoV (its Gaussian-leaf key list) covers every stored leaf
+    from paper_2501_08672_b200.voxmap import VoxelKey
+    keys = np.asarray(d["keys"], np.int64).reshape(-1, 3)
+    roots = {tuple(int(v) for v in (k >> m.max_level)) for k in keys}
+    got = m.leaf_keys_under_roots([VoxelKey(a, b, c, 0) for a, b, c in roots])
+    assert {k[:3] for k in got} == {tuple(int(v) for v in k) for k in keys}
 
 
 def test_snapshot_rejects_other_files(tmp_path):

@@ -28,14 +28,17 @@ class _G:          # Gaussian3D-like payload for init_fn
         self.opacity, self.sh = float(row[15]), row[16:].reshape(K, 3)
 
 
-@pytest.mark.parametrize("fov_as", ["tensor", "set"])
+@pytest.mark.parametrize("fov_as", ["tensor", "set", "tensor_dup"])
 def test_window_walk_matches_reference(fov_as):
     from paper_2501_08672_b200.voxmap import VoxelKey
     d, frames, K, L, root, vmap, win = _setup()
     for f, fr in enumerate(frames):
         init = (lambda k: [_G(init_row(k, root, L, K), K)]) if f >= 20 else None
-        fov = torch.as_tensor(fr["fov"], device="cuda") if fov_as == "tensor" else \
+        fov = torch.as_tensor(fr["fov"], device="cuda") if fov_as != "set" else \
             {VoxelKey(int(a), int(b), int(c), L) for a, b, c in fr["fov"]}
+        if fov_as == "tensor_dup":      # repeated, unordered FoV keys: the same window
+            g = torch.Generator().manual_seed(f)
+            fov = torch.cat([fov, fov[torch.randperm(fov.shape[0], generator=g).to(fov.device)]])
         rep = win.maintain(vmap, fov, init_fn=init, sensor_pos=fr["sensor"])
         got = [rep.n_live, rep.added, rep.removed, rep.moved, rep.dropped]
         assert got == list(fr["report"]), (f, got, fr["report"])
