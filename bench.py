@@ -522,9 +522,9 @@ def run_ours(args, wl, rank, world, local_rank):
                     "h2d_GBps_measured": h2d_gbps,
                     "note": "frames copied on one copy stream in view order, each view's blend waits for its own "
                             "copy; at h2d_GBps_measured the copies take h2d_bytes / bandwidth per step"},
-            "gpu_launches": args.steps * (len(my_views) * 10 + 2),   # per view: preprocess count / scan /
+            "gpu_launches": args.steps * (len(my_views) * 11 + 2),   # per view: preprocess count / scan /
             # emit, tile scan, scatter, tile sort, big-tile sort, fused blend (fwd + loss + bwd), loss total,
-            # chain; + adam and step counter per step
+            # chain partial sums, chain; + adam and step counter per step (profiles/r02k_launches.csv)
         }
         if world == 1 and not args.no_cpu_baseline:
             cs = CpuStep(wl, args.frames)
