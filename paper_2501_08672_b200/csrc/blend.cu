@@ -863,7 +863,7 @@ __device__ __forceinline__ void bwd_walk(const Ws& w, const BlendArgs& a, RecPip
                 float thr[RUN];
 #pragma unroll
                 for (int j = 0; j < RUN; ++j)
-                    thr[j] = !over ? __int_as_float(0x7f800000) : (bfree ? a.tmin : col_thr(j, cx0, cx1, a.tmin));
+                    thr[j] = over ? col_thr(j, cx0, cx1, a.tmin) : __int_as_float(0x7f800000);   // (bfree: cx0 0, cx1 RUN)
                 const Frame f = frame_of(q0, q1.w, gx0f, gy0f);
 #if LSB_PACKED_BWD
 #define bwd_half bwd_half2
