@@ -20,9 +20,9 @@ import torch
 
 from . import _lib
 from .errors import NoAssociations, SingularGain, TooFewPixels
-from .geometry import SE3, so3_exp, so3_left_jacobian, so3_log, so3_right_jacobian_inv
+from .geometry import SE3, so3_exp, so3_log
 from .raster import (_CAP_HINT, RasterSettings, RenderState, _as_arrays, _degree_used, _f32, _observed, pose_rows,
-                     render, render_fwd)
+                     render)
 
 DIM = 15
 

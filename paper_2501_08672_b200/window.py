@@ -31,7 +31,7 @@ from __future__ import annotations
 import ctypes
 import time
 from dataclasses import dataclass
-from typing import Callable, Iterable, Optional
+from typing import Callable, Optional
 
 import numpy as np
 import torch

@@ -2,7 +2,6 @@
 per view of a workload, and the kernel time of one view's render."""
 import sys
 import numpy as np
-import torch
 sys.path.insert(0, ".")
 from paper_2501_08672_b200.raster import GaussianArrays, RasterSettings, render
 from tools.scene import bake_room, camera_for, orbit_views
