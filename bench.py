@@ -524,7 +524,7 @@ def run_ours(args, wl, rank, world, local_rank):
                             "copy; at h2d_GBps_measured the copies take h2d_bytes / bandwidth per step"},
             "gpu_launches": args.steps * (len(my_views) * 11 + 2),   # per view: preprocess count / scan /
             # emit, tile scan, scatter, tile sort, big-tile sort, fused blend (fwd + loss + bwd), loss total,
-            # chain partial sums, chain; + adam and step counter per step (profiles/r02k_launches.csv)
+            # chain partial sums, chain; + adam and step counter per step (profiles/r02o_launches.csv)
         }
         if world == 1 and not args.no_cpu_baseline:
             cs = CpuStep(wl, args.frames)
