@@ -10,6 +10,10 @@
 
 #include "common.cuh"
 
+#ifndef LSB_BAND_SPLAT
+#define LSB_BAND_SPLAT 1      // band search per splat (each boundary row once), not per tile entry
+#endif
+
 namespace lsb {
 
 struct PreArgs {
@@ -292,6 +296,7 @@ __device__ __forceinline__ void emit_splat(const PreArgs& a, const Ws& w, Rec& r
                 atomicAdd(&w.tile_count[ty * w.ntx + tx], 1);
                 w.emit_tile[e] = ty * w.ntx + tx;
                 w.emit_slot[e] = (int32_t)slot;
+                if (LSB_BAND_SPLAT) w.ovr_of[e] = -1;
             }
         }
         return;
@@ -301,6 +306,7 @@ __device__ __forceinline__ void emit_splat(const PreArgs& a, const Ws& w, Rec& r
             atomicAdd(&w.tile_count[ty * w.ntx + tx], 1);
             w.emit_tile[e] = ty * w.ntx + tx;
             w.emit_slot[e] = (int32_t)slot;
+            if (LSB_BAND_SPLAT) w.ovr_of[e] = -1;
         }
 }
 
@@ -519,6 +525,109 @@ __device__ __forceinline__ bool band_search(const Ws& w, double clamp, double cu
     return true;
 }
 
+constexpr int BAND_GROUP = 8;     // lanes per splat in k_band_splats
+
+// The alpha_cut band of every visible splat at once: the same annulus
+// |q - qc| <= W as band_search, walked once per pixel row of the splat's
+// search region (its bbox; for a bbox-free record the tile hull of the bbox)
+// instead of once per row of every tile entry, BAND_GROUP lanes per splat
+// taking its rows in turn.  A candidate pixel joins the entry of its tile
+// (if the splat emitted that tile): band_pixel, with ovr_of[e] (-1 from the
+// emitting pass) holding the entry's mask row.  Candidates are rare, so the
+// lanes holding some take them one lane at a time (entries are never
+// shared between two lanes' band_pixel calls at once).
+__global__ void __launch_bounds__(256) k_band_splats(Ws w, double clamp, double cut, float bflim) {
+    if (w.ctr[1] > (unsigned long long)w.cap) return;     // overflow: tiles published empty
+    const int64_t M = (int64_t)w.ctr[0];
+    const int lane = threadIdx.x & 31, sub = lane & (BAND_GROUP - 1);
+    const int64_t groups = (int64_t)gridDim.x * (blockDim.x / BAND_GROUP);
+    const int64_t g0 = (int64_t)blockIdx.x * (blockDim.x / BAND_GROUP) + (threadIdx.x / BAND_GROUP);
+    // warp-uniform trip count over the slots
+    const int64_t wbase = g0 - (lane / BAND_GROUP);
+    for (int64_t sb = wbase; sb < M; sb += groups) {
+        const int64_t slot = sb + lane / BAND_GROUP;
+        const bool live = slot < M;
+        float qo = -1.f, qi = 0.f, mxr = 0.f, myr = 0.f, k = 0.f, sr = 0.f, ic0 = 0.f;
+        int ox = 0, oy = 0, cx0 = 0, cx1 = -1, ry0 = 0, ry1 = 0, x0 = 0, x1 = 0, y0 = 0, y1 = 0;
+        bool bf = false;
+        if (live) {
+            const CullGeo& g = w.cgeo[slot];
+            const float qc = g.qcf;
+            const float W = (float)(4.0 * CUT_BAND) + 4e-6f * fabsf(qc) + 1e-6f;
+            qo = qc + W;
+            qi = qc - W;
+            const Rec& r = w.rec[slot];
+            x0 = r.bbx & 0xffff; x1 = r.bbx >> 16; y0 = r.bby & 0xffff; y1 = r.bby >> 16;
+            bf = r.lop <= bflim;
+            ox = x0 & ~(TILE - 1);
+            oy = y0 & ~(TILE - 1);
+            const int bx1 = bf ? (((x1 - 1) | (TILE - 1)) + 1) : x1, by1 = bf ? (((y1 - 1) | (TILE - 1)) + 1) : y1;
+            const int bx0 = bf ? ox : x0, by0 = bf ? oy : y0;
+            mxr = (float)(g.mux - (double)ox);
+            myr = (float)(g.muy - (double)oy);
+            k = g.kf; sr = g.sf; ic0 = g.ic0f;
+            cx0 = bx0 - ox;
+            cx1 = bx1 - 1 - ox;
+            if (qo >= 0.f) {
+                const float dyx = sqrt_approx(qo / k) + 1e-3f;
+                ry0 = max(by0 - oy, __float2int_ru(myr - dyx));
+                ry1 = min(by1 - oy, __float2int_rd(myr + dyx) + 1);
+            }
+        }
+        int rounds = ry1 > ry0 ? (ry1 - ry0 + BAND_GROUP - 1) / BAND_GROUP : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) rounds = max(rounds, __shfl_xor_sync(0xffffffffu, rounds, o));
+        for (int j = 0; j < rounds; ++j) {
+            const int ry = ry0 + j * BAND_GROUP + sub;
+            int xa = 0, xb = -1, xl = 0, xr = 0;
+            bool has = false;
+            if (ry < ry1) {
+                const float dy = (float)ry - myr;
+                const float v = k * dy * dy;
+                const float to = qo - v;
+                if (to >= 0.f) {
+                    const float xm = __fmaf_rn(-sr, dy, mxr);
+                    const float ho = sqrt_approx(to * ic0);
+                    xa = max(cx0, __float2int_ru(xm - ho));
+                    xb = min(cx1, __float2int_rd(xm + ho));
+                    const float ti = qi - v;
+                    const float hi = ti > 0.f ? sqrt_approx(ti * ic0) : -1.f;
+                    xl = hi < 0.f ? xb : __float2int_rd(xm - hi);
+                    xr = hi < 0.f ? xb + 1 : __float2int_ru(xm + hi);
+                    has = xa <= xb && !(xl < xa && xr > xb);
+                }
+            }
+            unsigned pend = __ballot_sync(0xffffffffu, has);
+            while (pend) {
+                const int src = __ffs(pend) - 1;
+                pend &= pend - 1;
+                if (lane == src) {
+                    const CullGeo& g = w.cgeo[slot];
+                    const Rec& r = w.rec[slot];
+                    const int e0 = w.vis_ebase[slot], e1 = w.vis_ebase[slot + 1];
+                    for (int x = xa; x <= xb; ++x) {
+                        if (x > xl && x < xr) x = xr;             // jump over the inner run
+                        if (x > xb) break;
+                        const int X = ox + x, Y = oy + ry;
+                        const bool inbox = X >= x0 && X < x1 && Y >= y0 && Y < y1;
+                        const int t = (Y >> 4) * w.ntx + (X >> 4);
+                        int e = -1;
+                        for (int q = e0; q < e1; ++q)
+                            if (w.emit_tile[q] == t) { e = q; break; }
+                        if (e < 0) continue;                        // a tile the splat did not emit
+                        const int idx = w.ovr_of[e];
+                        const int nidx = band_pixel(w, g, r, clamp, cut, idx, X & ~(TILE - 1), Y & ~(TILE - 1),
+                                                    X & (TILE - 1), Y & (TILE - 1), inbox);
+                        if (nidx < 0) break;                        // (no room: a capacity overflow was reported)
+                        if (idx < 0) w.ovr_of[e] = nidx;
+                    }
+                }
+                __syncwarp();
+            }
+        }
+    }
+}
+
 // Scatter with the (slot, tile) pairs the preprocess emitted: one thread per
 // intersection claims a position in its tile's bucket (and, with alpha_cut
 // > 0, searches its entry for alpha_cut band pixels: band_search).
@@ -530,7 +639,11 @@ __global__ void __launch_bounds__(256) k_scatter_emitted(Ws w, double clamp, dou
         const int t = w.emit_tile[e];
         const int slot = w.emit_slot[e];
         const int j = w.tile_start[t] + atomicAdd(&w.tile_cursor[t], 1);
+#if LSB_BAND_SPLAT
+        const bool band = cut > 0.0 && w.ovr_of[e] >= 0;     // k_band_splats found band pixels in the entry
+#else
         const bool band = cut > 0.0 && band_search(w, clamp, cut, bflim, e, slot, t);
+#endif
         w.tile_e[j] = (int32_t)e;
         w.tile_slot[j] = slot | (band ? OVR_BIT : 0);      // the flag rides on the slot (sorts mask it)
     }
@@ -946,6 +1059,9 @@ cudaError_t launch_preprocess(const lsb_params& p, const lsb_camera& cam, const 
     const int st_smem = (int)sizeof(int) * (w.ntiles + w.ntiles / 32 + 1);
     if (st_smem > 48 * 1024) cudaFuncSetAttribute(k_scan_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, st_smem);
     k_scan_tiles<<<1, ST_THREADS, st_smem, st>>>(w);
+    if (LSB_BAND_SPLAT && s.alpha_cut > 0.0)
+        k_band_splats<<<8 * 148, 256, 0, st>>>(w, s.alpha_clamp, s.alpha_cut,
+                                               bbox_free_lim(s.alpha_cut, s.alpha_clamp, s.footprint_sigma));
     k_scatter_emitted<<<8 * 148, 256, 0, st>>>(w, s.alpha_clamp, s.alpha_cut,
                                                bbox_free_lim(s.alpha_cut, s.alpha_clamp, s.footprint_sigma));
     k_tile_sort<<<(w.ntiles + 3) / 4, 128, 0, st>>>(w);
