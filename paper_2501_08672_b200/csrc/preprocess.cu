@@ -525,7 +525,10 @@ __device__ __forceinline__ bool band_search(const Ws& w, double clamp, double cu
     return true;
 }
 
-constexpr int BAND_GROUP = 8;     // lanes per splat in k_band_splats
+#ifndef LSB_BAND_GROUP
+#define LSB_BAND_GROUP 2     // (measured: 1, 2, 4, 8, 16, 32 lanes; 2 the fastest)
+#endif
+constexpr int BAND_GROUP = LSB_BAND_GROUP;     // lanes per splat in k_band_splats
 
 // The alpha_cut band of every visible splat at once: the same annulus
 // |q - qc| <= W as band_search, walked once per pixel row of the splat's
