@@ -522,8 +522,9 @@ def run_ours(args, wl, rank, world, local_rank):
                     "h2d_GBps_measured": h2d_gbps,
                     "note": "frames copied on one copy stream in view order, each view's blend waits for its own "
                             "copy; at h2d_GBps_measured the copies take h2d_bytes / bandwidth per step"},
-            "gpu_launches": args.steps * (len(my_views) * (12 if wl["alpha_cut"] > 0 else 11) + 2),
-            # per view: preprocess count / scan / emit, tile scan, band search (alpha_cut > 0), scatter, tile
+            "gpu_launches": args.steps * (len(my_views) * (12 if wl["alpha_cut"] > 0 and N >= 65536 else 11) + 2),
+            # per view: preprocess count / scan / emit, tile scan, band search (alpha_cut > 0, N >= 65536: preprocess.cu
+            # LSB_BAND_SPLAT_MIN_N), scatter, tile
             # sort, big-tile sort, fused blend (fwd + loss + bwd), loss total, chain partial sums, chain;
             # + adam and step counter per step (profiles/r02p_launches.csv)
         }

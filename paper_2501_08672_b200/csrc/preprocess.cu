@@ -10,6 +10,9 @@
 
 #include "common.cuh"
 
+#ifndef LSB_BAND_SPLAT_MIN_N
+#define LSB_BAND_SPLAT_MIN_N 65536   // Gaussians from which the per-splat band search runs
+#endif
 #ifndef LSB_BAND_SPLAT
 #define LSB_BAND_SPLAT 1      // band search per splat (each boundary row once), not per tile entry
 #endif
@@ -634,7 +637,7 @@ __global__ void __launch_bounds__(256) k_band_splats(Ws w, double clamp, double 
 // Scatter with the (slot, tile) pairs the preprocess emitted: one thread per
 // intersection claims a position in its tile's bucket (and, with alpha_cut
 // > 0, searches its entry for alpha_cut band pixels: band_search).
-__global__ void __launch_bounds__(256) k_scatter_emitted(Ws w, double clamp, double cut, float bflim) {
+__global__ void __launch_bounds__(256) k_scatter_emitted(Ws w, double clamp, double cut, float bflim, int splat_band) {
     if (w.ctr[1] > (unsigned long long)w.cap) return;     // overflow: tiles published empty
     const int64_t I = (int64_t)w.ctr[1];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -642,11 +645,9 @@ __global__ void __launch_bounds__(256) k_scatter_emitted(Ws w, double clamp, dou
         const int t = w.emit_tile[e];
         const int slot = w.emit_slot[e];
         const int j = w.tile_start[t] + atomicAdd(&w.tile_cursor[t], 1);
-#if LSB_BAND_SPLAT
-        const bool band = cut > 0.0 && w.ovr_of[e] >= 0;     // k_band_splats found band pixels in the entry
-#else
-        const bool band = cut > 0.0 && band_search(w, clamp, cut, bflim, e, slot, t);
-#endif
+        // splat_band: k_band_splats already searched (band pixels found in
+        // the entry: ovr_of[e] >= 0); else the entry is searched here
+        const bool band = cut > 0.0 && (splat_band ? w.ovr_of[e] >= 0 : band_search(w, clamp, cut, bflim, e, slot, t));
         w.tile_e[j] = (int32_t)e;
         w.tile_slot[j] = slot | (band ? OVR_BIT : 0);      // the flag rides on the slot (sorts mask it)
     }
@@ -1062,11 +1063,16 @@ cudaError_t launch_preprocess(const lsb_params& p, const lsb_camera& cam, const 
     const int st_smem = (int)sizeof(int) * (w.ntiles + w.ntiles / 32 + 1);
     if (st_smem > 48 * 1024) cudaFuncSetAttribute(k_scan_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, st_smem);
     k_scan_tiles<<<1, ST_THREADS, st_smem, st>>>(w);
-    if (LSB_BAND_SPLAT && s.alpha_cut > 0.0)
+    // the band search once per splat pays off on large scenes (many entries
+    // per boundary row); on small ones (single-view latency, a few large
+    // splats walked serially) the scatter's per-entry search is faster
+    const int splat_band = (LSB_BAND_SPLAT && s.alpha_cut > 0.0 && p.n >= LSB_BAND_SPLAT_MIN_N) ? 1 : 0;
+    if (splat_band)
         k_band_splats<<<8 * 148, 256, 0, st>>>(w, s.alpha_clamp, s.alpha_cut,
                                                bbox_free_lim(s.alpha_cut, s.alpha_clamp, s.footprint_sigma));
     k_scatter_emitted<<<8 * 148, 256, 0, st>>>(w, s.alpha_clamp, s.alpha_cut,
-                                               bbox_free_lim(s.alpha_cut, s.alpha_clamp, s.footprint_sigma));
+                                               bbox_free_lim(s.alpha_cut, s.alpha_clamp, s.footprint_sigma),
+                                               splat_band);
     k_tile_sort<<<(w.ntiles + 3) / 4, 128, 0, st>>>(w);
     cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_sort_smem());
     k_tile_sort_big<<<148, 256, tile_sort_smem(), st>>>(w);
