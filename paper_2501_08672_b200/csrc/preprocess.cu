@@ -10,6 +10,9 @@
 
 #include "common.cuh"
 
+#ifndef LSB_SORT_KE
+#define LSB_SORT_KE 1       // per-tile warp sort over (depth, e) pairs, slot gathered after
+#endif
 #ifndef LSB_BAND_SPLAT_MIN_N
 #define LSB_BAND_SPLAT_MIN_N 65536   // Gaussians from which the per-splat band search runs
 #endif
@@ -735,6 +738,46 @@ __device__ void warp_bitonic(uint64_t* k, int* s, int* e, int lane) {
     }
 }
 
+// warp_bitonic over (depth, x) pairs, x = e with OVR_BIT (compared without it).
+template <int R>
+__device__ void warp_bitonic_ke(uint64_t* k, int* x, int lane) {
+    constexpr int P = 32 * R;
+#pragma unroll
+    for (int kk = 2; kk <= P; kk <<= 1) {
+#pragma unroll
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+                const int jr = j >> 5;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int rp = r ^ jr;
+                    if (rp > r) {
+                        const int i = r * 32 + lane;
+                        const bool up = (i & kk) == 0;
+                        const bool lt = key_less(k[rp], x[rp], k[r], x[r]);
+                        if (lt == up) {
+                            const uint64_t tk = k[r]; k[r] = k[rp]; k[rp] = tk;
+                            const int tx = x[r]; x[r] = x[rp]; x[rp] = tx;
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int i = r * 32 + lane;
+                    const uint64_t ok = __shfl_xor_sync(0xffffffffu, k[r], j);
+                    const int ox = __shfl_xor_sync(0xffffffffu, x[r], j);
+                    const bool up = (i & kk) == 0;
+                    const bool lower = (lane & j) == 0;
+                    const bool other_less = key_less(ok, ox, k[r], x[r]);
+                    const bool take = (lower == up) ? other_less : !other_less;
+                    if (take) { k[r] = ok; x[r] = ox; }
+                }
+            }
+        }
+    }
+}
+
 template <int R>
 __device__ void warp_sort_tile(const Ws& w, int start, int n, int lane) {
     uint64_t k[R];
@@ -752,6 +795,23 @@ __device__ void warp_sort_tile(const Ws& w, int start, int n, int lane) {
             e[r] = -1;
         }
     }
+#if LSB_SORT_KE
+    // (depth, e) pairs: a tile holds one entry per splat and e runs in slot
+    // order (vis_ebase), so e breaks depth ties exactly as the slot does; the
+    // slot (with the entry's OVR_BIT, carried on e) is gathered after the sort
+#pragma unroll
+    for (int r = 0; r < R; ++r) e[r] = (r * 32 + lane < n) ? (e[r] | (s[r] & OVR_BIT)) : SLOT_MASK;
+    warp_bitonic_ke<R>(k, e, lane);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = r * 32 + lane;
+        if (i < n) {
+            const int ee = e[r] & SLOT_MASK;
+            w.tile_e[start + i] = ee;
+            w.tile_slot[start + i] = w.emit_slot[ee] | (e[r] & OVR_BIT);
+        }
+    }
+#else
     warp_bitonic<R>(k, s, e, lane);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -761,6 +821,7 @@ __device__ void warp_sort_tile(const Ws& w, int start, int n, int lane) {
             w.tile_slot[start + i] = s[r];
         }
     }
+#endif
 }
 
 constexpr int WARP_SORT_CAP = 256;
